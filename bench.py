@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the corner-force hot path on B200 (BASELINE.json metric:
+force-eval quadrature points / s (F.1 + F^T.v) at 1 B200, % of the FP64/HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1] [--impl ours|reference]
+
+A step = one pass of the whole hot path for the workload:
+  c0..c3 : hydro_force_full (gather, forward contractions, pointwise physics + dt,
+           backward contractions, deterministic assembly, dt finalisation);
+  c4     : ROM online step = 3 lifts + hydro_force_sampled (64 instances) + 2
+           projections + the reduced position RHS.
+The headline workload is BASELINE.json configs[1] (c1, Gresho 256^2); the JSON line also
+carries the other configs under "per_config".  Inputs are synthetic (workloads/), resident
+in HBM before timing; L2 (126 MB) is flushed before every timed step by writing a 256 MiB
+buffer (outside the per-step CUDA events).  Multi-GPU: independent replicas (the path is
+sharded by nothing here -- DESIGN "Multi-GPU"), weak scaling, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "force-eval quad-points/sec (F·1 + F^T·v) at 1 B200"
+UNIT = "quad-points/s"
+
+
+# ----------------------------------------------------------------------------- work model
+def contraction_flops(dim, k, q, nfield=2, visc=True):
+    """Algorithmic FP64 flops (2 per multiply-add) of the sum-factorised contractions of
+    one element: forward J, grad v (+ e_q) and backward F.1, F^T.v (DESIGN "Work model")."""
+    n, m = k + 1, k
+    if dim == 3:
+        grad = 2 * q * n ** 3 + 3 * q * q * n * n + 3 * q ** 3 * n      # per scalar field
+        interp = q * m ** 3 + q * q * m * m + q ** 3 * m
+        bwd_f1 = dim * dim * q ** 3 * n + 3 * dim * q * q * n * n + dim * n ** 3 * 2 * q
+    else:
+        grad = 2 * q * n * n + 2 * q * q * n
+        interp = q * m * m + q * q * m
+        bwd_f1 = dim * dim * q * q * n + dim * n * n * 2 * q
+    nq = q ** dim
+    s_form = nq * (dim ** 3 + dim * dim + dim * dim)                   # S_q and A_q
+    macs = nfield * dim * grad + interp + bwd_f1 + interp + s_form
+    return 2 * macs
+
+
+def pointwise_ops(dim, visc, rot_per_lmin3):
+    """(flops, div+sqrt count) of the contract pointwise stage per qp (DESIGN A.3/A.4)."""
+    if dim == 3:
+        flops, ds = 42 + 3 + 3 + 30 + 2 + 4 + 12, 5 + 2     # det/inv, rho, p, cs, J^T J, den, inv_dt, sigma
+        lm = lambda r: (6 + 19 * r + (12 - r) + 2, 4 * r)
+        f, d = lm(rot_per_lmin3)
+        flops += f; ds += d
+        if visc:
+            flops += 45 + 6 + 6
+            f, d = lm(rot_per_lmin3)
+            flops += f; ds += d
+    else:
+        flops, ds = 8 + 3 + 3 + 12 + 2 + 4 + 6, 6 + 3
+        if visc:
+            flops += 12 + 3 + 8 + 6
+            ds += 1
+    return flops, ds
+
+
+# ----------------------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 5 + i and s[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    d = json.load(open(p)) if os.path.exists(p) else {}
+    return d
+
+
+# FP64 pipe peak: DFMA microbenchmark on this pool's B200 (tools/microbench/fp64_peak.cu,
+# profiles/r01_fp64_peak.txt): 34.2 TFLOP/s sustained; IEEE div 1.43e12/s, sqrt 1.29e12/s.
+FP64_PEAK_TFLOPS = 34.2
+DIVSQRT_WEIGHT = 24.0     # flop-equivalents of one IEEE FP64 div/sqrt on the FP64 pipe (12 DFMA slots)
+
+
+# ----------------------------------------------------------------------------- workloads
+def build_problem(name):
+    import workloads as W
+    if name == "c4":
+        return W.c4()
+    return W.config(name)
+
+
+def run_ours(args, rank, world):
+    import torch
+    import workloads as W
+    from paper_2104_11404_b200 import hydro
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    hydro.lib()
+    results = {}
+    names = [args.workload] + ([c for c in ("c0", "c2", "c3", "c4") if c != args.workload]
+                               if args.all else [])
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for name in names:
+        results[name] = bench_one(name, args, dev, flush, rank, world)
+    return results
+
+
+def _t(a, dev, dtype=None):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(a)).to(device=dev, dtype=dtype or torch.float64).contiguous()
+
+
+def bench_one(name, args, dev, flush, rank, world):
+    import torch
+    import workloads as W
+    from paper_2104_11404_b200 import hydro
+
+    prob = build_problem(name)
+    base = prob.base if name == "c4" else prob
+    m = base.mesh
+    ctx = hydro.HydroContext(m.dim, m.k, m.nq, _t(m.elem_nodes, dev, torch.int32), _t(m.x0, dev),
+                             _t(m.rho0, dev))
+    visc = hydro.Visc(base.q1, base.q2, base.visc)
+    cfl = hydro.Cfl(base.alpha, base.alpha_mu)
+    gamma = _t(base.gamma, dev)
+    nq = m.nq ** m.dim
+    if name != "c4":
+        x, v, e = _t(prob.x, dev), _t(prob.v, dev), _t(prob.e, dev)
+        F1 = torch.empty((m.dim, m.n_nodes), dtype=torch.float64, device=dev)
+        FTw = torch.empty((m.n_elem, m.ne), dtype=torch.float64, device=dev)
+        dt = torch.empty(1, dtype=torch.float64, device=dev)
+        n_qp = m.n_elem * nq
+        n_units = m.n_elem
+
+        def step():
+            ctx.force_full(x, v, e, gamma, visc, cfl, F1=F1, FTw=FTw, dt=dt)
+    else:
+        b = prob
+        plan = hydro.SamplePlan(ctx, b.sample_elems, b.B)
+        P_v, P_e, C_xv, c_x = W.offline_projectors(b)
+        Phi_x, Phi_v, Phi_e = _t(b.Phi_x, dev), _t(b.Phi_v, dev), _t(b.Phi_e, dev)
+        x_os, v_os, e_os = _t(b.x_os, dev), _t(b.v_os, dev), _t(b.e_os, dev)
+        Yx, Yv, Ye = _t(b.Yx, dev), _t(b.Yv, dev), _t(b.Ye, dev)
+        Pv, Pe, Cxv, cx = _t(P_v, dev), _t(P_e, dev), _t(C_xv, dev), _t(c_x, dev)
+        xS = torch.empty((Phi_x.shape[0], b.B), dtype=torch.float64, device=dev)
+        vS = torch.empty_like(xS)
+        eS = torch.empty((Phi_e.shape[0], b.B), dtype=torch.float64, device=dev)
+        F1r = torch.empty((plan.s_v, b.B), dtype=torch.float64, device=dev)
+        FTr = torch.empty((plan.s_e, b.B), dtype=torch.float64, device=dev)
+        dt = torch.empty(b.B, dtype=torch.float64, device=dev)
+        rv = torch.empty((b.nv, b.B), dtype=torch.float64, device=dev)
+        re_ = torch.empty((b.ne, b.B), dtype=torch.float64, device=dev)
+        rx = torch.empty((b.nx, b.B), dtype=torch.float64, device=dev)
+        wsv = hydro.rom_project_workspace(b.nv, plan.s_v, b.B, dev)
+        wse = hydro.rom_project_workspace(b.ne, plan.s_e, b.B, dev)
+        n_qp = plan.n_cl * b.B * nq
+        n_units = plan.n_cl * b.B
+
+        def step():
+            hydro.rom_lift(Phi_x, x_os, Yx, out=xS)
+            hydro.rom_lift(Phi_v, v_os, Yv, out=vS)
+            hydro.rom_lift(Phi_e, e_os, Ye, out=eS)
+            plan.force_sampled(xS, vS, eS, gamma, visc, cfl, F1_rows=F1r, FTw_rows=FTr, dt=dt)
+            hydro.rom_project(Pv, F1r, out=rv, workspace=wsv)
+            hydro.rom_project(Pe, FTr, out=re_, workspace=wse)
+            hydro.rom_lift(Cxv, cx, Yv, out=rx)
+
+    # warm-up
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st = ctx.status_sync() if name != "c4" else plan.status_sync()
+    if st[0] != 0:
+        raise RuntimeError(f"{name}: device status {st}")
+    # timed region
+    hydro.profile_enable(True)
+    hydro.profile_read()
+    l0 = hydro.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        for i in range(args.steps):
+            flush.zero_()                      # L2 flush (256 MiB > 126 MB), outside the events
+            evs[i][0].record()
+            step()
+            evs[i][1].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = hydro.launch_count() - l0
+    kern_ms, kern_n = hydro.profile_read()
+    hydro.profile_enable(False)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = sum(step_ms) / len(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    kern_avg = kern_ms / max(kern_n, 1)
+    out = dict(workload=name, ms_per_step=ms, qp_per_s=n_qp / (ms * 1e-3),
+               elements_per_s=n_units / (ms * 1e-3), n_qp=n_qp, force_kernel_ms=kern_avg,
+               force_kernel_share=kern_avg / ms if ms > 0 else None,
+               gpu_launches=launches, clocks=clk.summary())
+    # end to end through the public API with host buffers (pinned), c0..c3
+    if name != "c4":
+        hx = torch.as_tensor(prob.x).pin_memory(); hv = torch.as_tensor(prob.v).pin_memory()
+        he = torch.as_tensor(prob.e).pin_memory(); hg = torch.as_tensor(base.gamma).pin_memory()
+        oF1 = torch.empty(F1.shape, dtype=torch.float64).pin_memory()
+        oFT = torch.empty(FTw.shape, dtype=torch.float64).pin_memory()
+        odt = torch.empty(1, dtype=torch.float64).pin_memory()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for it in range(args.warmup + args.steps):
+            if it == args.warmup:
+                torch.cuda.synchronize(); e0.record()
+            x.copy_(hx, non_blocking=True); v.copy_(hv, non_blocking=True)
+            e.copy_(he, non_blocking=True); gamma.copy_(hg, non_blocking=True)
+            step()
+            oF1.copy_(F1, non_blocking=True); oFT.copy_(FTw, non_blocking=True)
+            odt.copy_(dt, non_blocking=True)
+        e1.record(); torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.steps
+        h2d = sum(t.numel() * 8 for t in (hx, hv, he, hg))
+        d2h = sum(t.numel() * 8 for t in (oF1, oFT, odt))
+        out["e2e"] = {"value": n_qp / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                      "d2h_bytes_per_step": d2h, "ms_per_step": ems}
+    # roofline of the dominant kernel (force kernel)
+    out["roofline"] = roofline(name, base, m, n_units, kern_avg, prob)
+    return out
+
+
+def _rotations_per_lmin3(name, prob):
+    """Data-dependent Jacobi rotation count of the contract, measured by the oracle on a
+    seeded sample of the workload's elements (both sides execute the same sequence)."""
+    import oracle
+    base = prob.base if name == "c4" else prob
+    m = base.mesh
+    if not (m.dim == 3):
+        return 0.0
+    rng = np.random.default_rng(0)
+    el = np.sort(rng.choice(m.n_elem, min(m.n_elem, 2000), replace=False)).astype(np.int32)
+    oracle.lmin3_stats(reset=True)
+    oracle.force(base, elist=el, mode=1)
+    r, c = oracle.lmin3_stats(reset=True)
+    return r / max(c, 1) * (1 if base.visc else 1)
+
+
+def roofline(name, base, m, n_units, kern_ms, prob):
+    rot = _rotations_per_lmin3(name, prob)
+    nq = m.nq ** m.dim
+    cflops = contraction_flops(m.dim, m.k, m.nq)
+    pf, pds = pointwise_ops(m.dim, base.visc, rot)
+    nominal = n_units * (cflops + nq * (pf + pds))
+    weighted = n_units * (cflops + nq * (pf + DIVSQRT_WEIGHT * pds))
+    # algorithmic bytes: x, v [N_V], e [N_E], m_q [Q], elem_nodes, gamma; write F1 [N_V], FTw [N_E]
+    if name == "c4":
+        B = prob.B
+        rows_h1 = prob.Phi_x.shape[0]
+        rows_l2 = prob.Phi_e.shape[0]
+        n_cl = n_units // B
+        byts = 8 * (2 * rows_h1 * B + rows_l2 * B + n_cl * nq + n_cl) + 4 * n_cl * m.nd
+        byts += 8 * (prob.s0_nodes.size * m.dim * B + prob.sample_elems.size * m.ne * B)
+    else:
+        byts = (8 * (2 * m.N_V + m.N_E + m.n_elem * nq + m.n_elem) + 4 * m.n_elem * m.nd
+                + 8 * (m.N_V + m.N_E))
+    t = kern_ms * 1e-3
+    ach = weighted / t / 1e12
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    return {"bound": "alu", "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": None,
+            "kernel": "force_kernel", "flops_weighted_per_launch": weighted,
+            "flops_nominal_per_launch": nominal, "divsqrt_weight": DIVSQRT_WEIGHT,
+            "rotations_per_lmin3": round(rot, 3),
+            "hbm_bytes_alg": byts, "hbm_frac": round(byts / t / 1e9 / hbm, 4),
+            "peak_source": "FP64 DFMA microbenchmark on B200 (profiles/r01_fp64_peak.txt); "
+                           "HBM from MEASURED_PEAKS.json"}
+
+
+# ----------------------------------------------------------------------------- cpu baseline
+def cpu_baseline(name, target_s=12.0):
+    """The oracle as it stands, on a bounded seeded sample of the workload's elements."""
+    import oracle
+    prob = build_problem(name) if name != "c4" else build_problem("c2")
+    m = prob.mesh
+    nq = m.nq ** m.dim
+    cores = os.cpu_count() or 1
+    rng = np.random.default_rng(1)
+    n = min(m.n_elem, 256)
+    el = np.sort(rng.choice(m.n_elem, n, replace=False)).astype(np.int32)
+    t0 = time.perf_counter()
+    oracle.force(prob, elist=el)
+    dt1 = time.perf_counter() - t0
+    n2 = int(min(m.n_elem, max(n, n * target_s / max(dt1, 1e-3))))
+    el = np.sort(rng.choice(m.n_elem, n2, replace=False)).astype(np.int32)
+    t0 = time.perf_counter()
+    oracle.force(prob, elist=el)
+    wall = time.perf_counter() - t0
+    return {"value": n2 * nq / wall, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n2} of {m.n_elem} elements of {name} ({n2 * nq} quad points), F.1+F^T.v+dt, "
+                      f"OpenMP over {cores} host threads, {wall:.1f} s"}
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c1", choices=["c0", "c1", "c2", "c3", "c4"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--all", dest="all", action="store_true", default=True)
+    ap.add_argument("--only", dest="all", action="store_false")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        import oracle
+        cb = []
+        for _ in range(args.warmup):
+            pass
+        vals = []
+        for _ in range(args.steps):
+            r = cpu_baseline(args.workload, target_s=max(2.0, 60.0 / max(args.steps, 1)))
+            vals.append(r["value"])
+        v = float(np.median(vals))
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 1,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": args.workload},
+                "cpu_baseline": {**r, "value": v},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    res = run_ours(args, rank, world)
+    head = res[args.workload]
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": head["qp_per_s"] * world, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (workloads/: seeded SplitMix64, shapes of BASELINE.json configs)",
+            "config": {"workload": f"{args.workload} (BASELINE.json configs[{args.workload[1]}])",
+                       "elements_per_s": head["elements_per_s"] * world, "quad_points": head["n_qp"],
+                       "l2": "flushed before every timed step (256 MiB write)",
+                       "parallelism": f"replicas x{world}"},
+            "e2e": head.get("e2e"), "gpu_launches": head["gpu_launches"],
+            "roofline": head["roofline"], "clocks": head["clocks"],
+            "force_kernel_ms": head["force_kernel_ms"], "force_kernel_share": head["force_kernel_share"],
+            "per_config": {k: {kk: vv for kk, vv in r.items() if kk not in ("clocks",)}
+                           for k, r in res.items() if k != args.workload},
+        }
+        if not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(args.workload)
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

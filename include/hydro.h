@@ -1,0 +1,183 @@
+/*
+ * hydro.h -- C ABI of the B200 corner-force library (libhydro.so).
+ *
+ * The one data-parallel hot path of arXiv 2104.11404 (Copeland, Cheung, Huynh,
+ * Choi, "Reduced order models for Lagrangian hydrodynamics"): the high-order
+ * finite-element force F(v, e, x) of the semi-discrete Euler system
+ *     M_V dv/dt = -F.1,   M_E de/dt = F^T.v,   dx/dt = v
+ * (PAPER.md Eq. fom; F.1 and F^T.v are Eq. forceOneforceTv),
+ * the adaptive time-step estimate (Eq. adaptive-timestep), and the
+ * hyper-reduced ROM online pieces: lifting (Eq. discretesolrepresentation,
+ * P:864-871), sampled force evaluation ("the lifting is computed only for the
+ * sampled degrees of freedom") and the least-squares projection
+ * (Eq. sol-ls-hyper).  The entries of F are not written in the paper
+ * (it defers to Dobrev et al. 2012); R1-R25 give the
+ * reading implemented here, and DESIGN.md "Evaluation contract" fixes the
+ * operation order that makes dt bit-reproducible.
+ *
+ * Conventions (all entry points):
+ *   - FP64 everywhere; indices int32 (element->node table) / int64 (sizes).
+ *   - Pointers are DEVICE pointers owned by the caller unless marked "host".
+ *   - Calls are asynchronous on `stream`; outputs are overwritten, never
+ *     accumulated.  Argument/shape errors return synchronously before any
+ *     launch.  Device-side conditions (detJ <= 0 at a quadrature point, NaN
+ *     time-step) are recorded in a sticky device status word and reported by
+ *     hydro_status_sync(); output contents are unspecified in that case.
+ *   - Layouts: H1 (kinematic) vectors SoA by component [dim][n_nodes]; L2
+ *     (thermodynamic) vectors element-major [n_elem][k^dim] with local
+ *     lexicographic Gauss-Legendre node order (j1 fastest); element->node table
+ *     [n_elem][(k+1)^dim] with local lexicographic Gauss-Lobatto order (a1
+ *     fastest).  Batched ROM arrays are [rows][B] (instance fastest).
+ *   - F.1 is returned exactly as P:437 defines it (the momentum RHS is -F.1);
+ *     no boundary condition is applied (v.n = g, is the solver's).
+ *   - Results are bitwise reproducible run to run (no floating-point atomics).
+ *   - One context/sample plan may be used by one stream at a time.
+ */
+#ifndef HYDRO_H_
+#define HYDRO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *hydro_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef struct hydro_ctx hydro_ctx;       /* opaque mesh context                         */
+typedef struct hydro_sample hydro_sample; /* opaque sample-mesh plan (ROM mode)          */
+
+typedef enum {
+  HYDRO_OK = 0,
+  HYDRO_ERR_ARG = 1,         /* bad pointer / size / unsupported combination             */
+  HYDRO_ERR_UNSUPPORTED = 2, /* (dim, k, q) not compiled in                               */
+  HYDRO_ERR_CUDA = 3,        /* a CUDA runtime call or launch failed                      */
+  HYDRO_ERR_TANGLED = 4,     /* detJ <= 0 at some quadrature point (DESIGN R16)            */
+  HYDRO_ERR_NONFINITE = 5,   /* some dt_q is NaN (DESIGN R15)                              */
+  HYDRO_ERR_WORKSPACE = 6    /* workspace too small or misaligned                          */
+} hydro_status;
+
+/* Mesh description (kinematic H1 Q_k, thermodynamic L2 Q_{k-1}). */
+typedef struct {
+  int dim;                   /* 2 or 3                                                    */
+  int order_h1;              /* k in {2, 3}; L2 order is k-1 (the only supported pair)    */
+  int nq1d;                  /* Gauss-Legendre points per dim: 4 (k=2) or 6 (k=3)          */
+  int64_t n_elem, n_nodes;   /* elements, H1 lattice nodes                                */
+  const int32_t *elem_nodes; /* device [n_elem][(k+1)^dim]                                */
+  const double *x0;          /* device [dim][n_nodes], initial (Lagrangian) positions     */
+  const double *rho0;        /* device [n_elem], initial density, piecewise constant      */
+} hydro_mesh_desc;
+
+/* Artificial viscosity (DESIGN R3, BASELINE.json C0):
+ *   mu = rho h (q1 cs + q2 h |min(lambda_min(eps(v)), 0)|),  sigma_a = mu eps(v).
+ * enabled == 0 => mu = 0 (Gresho).                                     */
+typedef struct { double q1, q2; int enabled; } hydro_visc;
+/* CFL constants alpha, alpha_mu of Eq. adaptive-timestep (defaults 0.5, 2.5).  */
+typedef struct { double alpha, alpha_mu; } hydro_cfl;
+
+/* ------------------------------------------------------------------ context (setup, S0) */
+/* Bytes of caller-provided device workspace hydro_ctx_create needs (0 on bad desc).       */
+size_t hydro_ctx_workspace_bytes(const hydro_mesh_desc *desc /* host */);
+/* Builds the per-quadrature-point mass m_q = rho0_K detJ0(xi_q) (density elimination,
+ * P:389-391), the node->slot assembly map and the dt status block inside `workspace`
+ * (device, >= hydro_ctx_workspace_bytes, 256-byte aligned).  Synchronises `stream`.
+ * Copies desc (the pointers must stay valid for the context's lifetime).                  */
+hydro_status hydro_ctx_create(const hydro_mesh_desc *desc /* host */, void *workspace,
+                              size_t ws_bytes, hydro_stream_t stream, hydro_ctx **out /* host */);
+hydro_status hydro_ctx_destroy(hydro_ctx *ctx);
+
+/* ------------------------------------------------------------------ full-order force */
+/* F1  = F.1  (assembled over shared H1 nodes, [dim][n_nodes]);
+ * FTw = F^T.w (element-local, [n_elem][k^dim]); w == NULL means w = v.  The RK2-average
+ * scheme needs w != v: F(U^n)^T v^{n+1/2}.
+ * dt  = min over all quadrature points of alpha / (cs/h + alpha_mu mu / (rho h^2))
+ *       (device scalar; NULL to skip), bit-identical to the oracle under the contract.
+ * x, v, w: [dim][n_nodes]; e: [n_elem][k^dim]; gamma: [n_elem].                          */
+hydro_status hydro_force_full(hydro_ctx *ctx, const double *x, const double *v, const double *e,
+                              const double *w, const double *gamma, hydro_visc visc,
+                              hydro_cfl cfl, double *F1, double *FTw, double *dt,
+                              hydro_stream_t stream);
+/* dt only (forward contractions + pointwise stage; no backward, no assembly).            */
+hydro_status hydro_dt_estimate(hydro_ctx *ctx, const double *x, const double *v, const double *e,
+                               const double *gamma, hydro_visc visc, hydro_cfl cfl, double *dt,
+                               hydro_stream_t stream);
+/* Synchronises `stream`, returns the sticky device condition (TANGLED before NONFINITE)
+ * and clears it.  *first_bad_elem (host, may be NULL) = lowest tangled element or -1.    */
+hydro_status hydro_status_sync(hydro_ctx *ctx, hydro_stream_t stream, int64_t *first_bad_elem);
+
+/* ------------------------------------------------------------------ ROM mode (C4) */
+/* Sample plan for S0 = sample_elems (host, sorted, unique).  Closure = S0 plus every
+ * element sharing an H1 node with S0 (DESIGN R20).  Row conventions:
+ *   closure H1 rows   : c*n_cl_nodes + i, i over the ascending closure node ids;
+ *   closure L2 rows   : l*k^dim + j, l over the ascending closure element ids;
+ *   sampled F1 rows   : c*n_s0_nodes + i, i over the ascending node ids of S0 elements
+ *                       (= the H1 dofs of S0 in ascending global SoA index);
+ *   sampled FTw rows  : s*k^dim + j, s over S0 (ascending).
+ * B = batch of independent instances evaluated per call (instance fastest).
+ * Allocates its device tables with cudaMalloc (setup; never on the hot path).            */
+hydro_status hydro_sample_create(hydro_ctx *ctx, const int32_t *sample_elems /* host */,
+                                 int64_t n_sample, int B, hydro_sample **out /* host */);
+hydro_status hydro_sample_destroy(hydro_sample *s);
+/* Counts (host outputs, any may be NULL).                                                 */
+hydro_status hydro_sample_info(const hydro_sample *s, int64_t *n_closure_elem,
+                               int64_t *n_closure_nodes, int64_t *n_s0_nodes,
+                               int64_t *s_v /* dim*n_s0_nodes */, int64_t *s_e /* |S0|*k^dim */);
+/* Host copies of the ascending closure element ids / closure node ids / S0 node ids.     */
+hydro_status hydro_sample_lists(const hydro_sample *s, int32_t *closure_elems /* host or NULL */,
+                                int64_t *closure_nodes /* host or NULL */,
+                                int64_t *s0_nodes /* host or NULL */);
+
+/* Lift (restricted to sample-mesh rows):
+ *   out[r][b] = os[r] (os_batched == 0) or os[r][b] (os_batched != 0)
+ *               + sum_k Phi[r][k] Y[k][b],    r < rows, k < n, b < B.
+ * Phi [rows][n] row-major, Y [n][B], out [rows][B].  Also serves the reduced position
+ * RHS r_x = Phi_x^T v_os + (Phi_x^T Phi_v) Yhat_v with Phi = C_xv.            */
+hydro_status hydro_rom_lift(int64_t rows, int n, int B, const double *Phi, const double *os,
+                            int os_batched, const double *Y, double *out, hydro_stream_t stream);
+
+/* Sampled force: S1-S6 over (closure element, instance) pairs; F1_rows [s_v][B] at the
+ * S0 nodes (complete: every element touching them is in the closure), FTw_rows [s_e][B]
+ * of the S0 elements, dt [B] (min over the CLOSURE elements' quadrature points; NULL to
+ * skip).  x_S, v_S, w_S: closure H1 rows [dim*n_cl_nodes][B]; e_S: closure L2 rows
+ * [n_cl_elem*k^dim][B]; gamma: global [n_elem].  w_S == NULL means w = v.               */
+hydro_status hydro_force_sampled(hydro_sample *s, const double *x_S, const double *v_S,
+                                 const double *e_S, const double *w_S, const double *gamma,
+                                 hydro_visc visc, hydro_cfl cfl, double *F1_rows,
+                                 double *FTw_rows, double *dt, hydro_stream_t stream);
+/* Sticky status of the sample plan (same semantics as hydro_status_sync; the element
+ * index is global).                                                                        */
+hydro_status hydro_sample_status_sync(hydro_sample *s, hydro_stream_t stream,
+                                      int64_t *first_bad_elem);
+
+/* Projection (Eq. sol-ls-hyper, P:778-799 with the precomputed (Z^T Phi)^dagger):
+ *   r[i][b] = sum_s P[i][s] f[s][b],  P [n][s_rows] row-major, f [s_rows][B], r [n][B].
+ * Deterministic split-K; `workspace` (device) >= hydro_rom_project_workspace_bytes.     */
+size_t hydro_rom_project_workspace_bytes(int n, int64_t s_rows, int B);
+hydro_status hydro_rom_project(int n, int64_t s_rows, int B, const double *P, const double *f,
+                               double *r, void *workspace, size_t ws_bytes,
+                               hydro_stream_t stream);
+
+/* ------------------------------------------------------------------ profiling (host) */
+/* When enabled, every hydro_force_full / hydro_dt_estimate / hydro_force_sampled call
+ * records a pair of CUDA events around its force kernel on the call's stream (the
+ * dominant kernel; bench.py's live roofline).  hydro_profile_read synchronises the
+ * recorded events and returns the summed kernel time (ms) and launch count since the
+ * last read, then clears them.  Profiling is global to the library (not per context). */
+hydro_status hydro_profile_enable(int on);
+hydro_status hydro_profile_read(double *total_ms /* host */, int64_t *count /* host */);
+
+/* ------------------------------------------------------------------ introspection (host) */
+/* The library's own correctly rounded 1D tables for (k, q) (DESIGN R5, R6): xi[q], w[q],
+ * B[q][k+1], G[q][k+1], Bl[q][k] (host outputs).  Pure host computation, no GPU needed. */
+hydro_status hydro_basis_tables(int k, int q, double *xi, double *w, double *B, double *G,
+                                double *Bl);
+/* Number of kernel launches issued by this library since load (host counter).            */
+int64_t hydro_launch_count(void);
+/* Library version string.                                                                  */
+const char *hydro_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYDRO_H_ */

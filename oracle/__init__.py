@@ -163,5 +163,13 @@ def project(P: np.ndarray, f: np.ndarray) -> np.ndarray:
     return r
 
 
+def lmin3_stats(reset: bool = True):
+    """(Jacobi rotations performed, lmin3 calls) accumulated by oracle.force since the
+    last reset -- bench.py uses it to count the contract's data-dependent work."""
+    r, c = ctypes.c_int64(0), ctypes.c_int64(0)
+    lib().oracle_stats(ctypes.byref(r), ctypes.byref(c), ctypes.c_int(1 if reset else 0))
+    return r.value, c.value
+
+
 def tables(k: int, q: int) -> dict:
     return _tables.tables(k, q)

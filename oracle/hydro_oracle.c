@@ -58,7 +58,19 @@ typedef struct {
  * negligible (<= 2^-53 max|a_ij|, which also covers a_pq == 0) is skipped -- this
  * also removes the 0/0 of a re-introduced subnormal a_pq on an exactly
  * degenerate diagonal. IEEE ops only, no FMA. */
+/* instrumentation for bench.py's algorithmic-work count (not part of the method):
+ * rotations performed / lmin3 calls, summed over threads */
+static int64_t g_rot = 0, g_calls = 0;
+static __thread int64_t t_rot = 0, t_calls = 0;
+
+void oracle_stats(int64_t *rotations, int64_t *calls, int reset) {
+  if (rotations) *rotations = g_rot;
+  if (calls) *calls = g_calls;
+  if (reset) { g_rot = 0; g_calls = 0; }
+}
+
 double oracle_lmin3(const double a_in[6] /* a00 a11 a22 a01 a02 a12 */) {
+  ++t_calls;
   double a[3][3];
   a[0][0] = a_in[0]; a[1][1] = a_in[1]; a[2][2] = a_in[2];
   a[0][1] = a[1][0] = a_in[3];
@@ -74,6 +86,7 @@ double oracle_lmin3(const double a_in[6] /* a00 a11 a22 a01 a02 a12 */) {
       const int p = P[r], q = Qp[r];
       const double apq = a[p][q];
       if (fabs(apq) <= tol) continue;
+      ++t_rot;
       const double dlt = 0.5 * (a[q][q] - a[p][p]);
       const double rr = sqrt(dlt * dlt + apq * apq);
       double t = apq / (fabs(dlt) + rr);
@@ -580,6 +593,7 @@ int oracle_force(const otab *tab, int64_t n_elem, int64_t n_nodes, const int32_t
     }
 #pragma omp critical
     {
+      g_rot += t_rot; g_calls += t_calls; t_rot = 0; t_calls = 0;
       if (my_nan) any_nan = 1;
       if (dt_less(my_dt, dt_min)) dt_min = my_dt;
       if (my_bad < bad) bad = my_bad;

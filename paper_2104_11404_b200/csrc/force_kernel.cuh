@@ -1,0 +1,755 @@
+// force_kernel.cuh -- fused corner-force kernel for sm_100a (FP64).
+//
+// One CTA evaluates EPB "units" (a unit = one element in full-order mode, one
+// (closure element, instance) pair in batched ROM mode); one thread per Gauss
+// point of its unit.  Stages (DESIGN "Kernels"):
+//   S1 gather    element dofs of x, v (w) and e into shared memory;
+//   S2 forward   sum-factorised contractions J = dx/dxi, gradhat v, (gradhat w), e_q,
+//                each output an FMA chain in the canonical order of DESIGN A.2;
+//   S3 pointwise detJ, J^-1, rho = m_q/detJ, p, cs, h, grad v, eps, lambda_min, mu,
+//                sigma, dt_q -- the exact IEEE sequence of DESIGN A.3/A.4 (this file
+//                is compiled with -fmad=false; every FMA is written as __fma_rn);
+//   S4 backward  S_q = w_q detJ sigma J^-T, then sum-factorised transposes:
+//                F1_K[a][c] = sum_q (S_q gradhat phi_a)_c, FTw_K[j] = sum_q psi_j (S_q : gradhat w);
+//   S5 outputs   F1_K to its assembly slots (deterministic gather in assemble_kernel),
+//                FTw_K element-local;
+//   S6 dt        warp/CTA min of order-preserving keys, one atomicMin per CTA (exact).
+// PAPER anchors: Eq. fom, Eq. forceOneforceTv, Eq. EOS P:374-376,
+// stress split P:367-370, density elimination P:389-391, Eq. adaptive-timestep P:533-544.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hydro_internal.h"
+
+namespace hk {
+
+enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2 };
+
+template <int DIM_, int K_, int Q_>
+struct Geo {
+  static constexpr int DIM = DIM_, K = K_, Q = Q_;
+  static constexpr int N = K + 1, M = K;
+  static constexpr int ND = DIM == 2 ? N * N : N * N * N;
+  static constexpr int NE = DIM == 2 ? M * M : M * M * M;
+  static constexpr int NQ = DIM == 2 ? Q * Q : Q * Q * Q;
+  static constexpr int EPB = NQ <= 16 ? 8 : (NQ <= 36 ? 4 : (NQ <= 64 ? 2 : 1));
+  static constexpr int NT = ((EPB * NQ + 31) / 32) * 32;
+  static constexpr int NF = 3;  // fields x, v, w (w only when distinct)
+  // per-unit shared-memory layout (doubles)
+  static constexpr int S1 = DIM == 3 ? Q * N * N : Q * N;       // one stage-1 block
+  static constexpr int S2 = DIM == 3 ? Q * Q * N : 0;           // one stage-2 block
+  static constexpr int E1 = DIM == 3 ? Q * M * M : Q * M;
+  static constexpr int E2 = DIM == 3 ? Q * Q * M : 0;
+  static constexpr int FWD = NF * DIM * 2 * S1 + NF * DIM * 3 * S2 + E1 + E2;
+  static constexpr int TB = DIM == 3 ? DIM * DIM * Q * Q * N : DIM * DIM * Q * N;
+  static constexpr int WB = DIM == 3 ? 2 * DIM * Q * N * N : 0;
+  static constexpr int F1B = DIM == 3 ? Q * Q * M : Q * M;
+  static constexpr int F2B = DIM == 3 ? Q * M * M : 0;
+  static constexpr int BWD = DIM * DIM * NQ + NQ + TB + WB + F1B + F2B;
+  static constexpr int WORK = FWD > BWD ? FWD : BWD;
+  static constexpr int UNIT = NF * DIM * ND + NE + WORK;
+  static constexpr int TABD = Q + Q * N * 2 + Q * M;             // w, B, G, Bl
+  static constexpr size_t SMEM =
+      sizeof(double) * (size_t)(TABD + EPB * UNIT) + sizeof(int) * EPB * ND +
+      sizeof(unsigned long long) * EPB;
+};
+
+struct Params {
+  int64_t n_units;          // full: n_elem; batched: n_cl_elem * B
+  int B;                    // instances (1 in full mode)
+  int64_t ld_nodes;         // H1 component stride in nodes (n_nodes or n_cl_nodes)
+  const int32_t *elem_nodes;  // [n_l][ND] node ids (closure-local in batched mode)
+  const int32_t *elem_gid;    // batched: closure-local -> global element id; NULL = identity
+  const double *x, *v, *w, *e, *gamma, *mq, *rho0;
+  double q1, q2, alpha, alpha_mu;
+  int visc;
+  double *evec;             // F1 slot buffer [slot][DIM][B]
+  const int32_t *slot;      // [n_l][ND] slot or -1
+  double *FTw;              // [row][NE][B]
+  const int32_t *ftw_row;   // [n_l] row or -1; NULL = identity
+  double *mq_out;           // MODE_MQ: [n_elem][NQ]
+  hydro_devstatus *st;      // [B]
+  const double *tab_w, *tab_B, *tab_G, *tab_Bl;  // device tables [Q], [Q][N], [Q][N], [Q][M]
+};
+
+// ----------------------------------------------------------------------------- helpers
+__device__ __forceinline__ unsigned long long dt_key(double d) {
+  // order-preserving map of a double to uint64 (-0 < +0); NaN never reaches here
+  unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ double key_to_dt(unsigned long long k) {
+  unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+// One cyclic-Jacobi rotation of DESIGN A.4 on pair (p,q) with r3 = the third index.
+__device__ __forceinline__ void jacobi_rot(double &app, double &aqq, double &apq, double &arp,
+                                           double &arq, const double tol) {
+  if (fabs(apq) <= tol) return;
+  const double dlt = 0.5 * (aqq - app);
+  const double rr = sqrt(dlt * dlt + apq * apq);
+  double t = apq / (fabs(dlt) + rr);
+  if (dlt < 0.0) t = -t;
+  const double c = 1.0 / sqrt(1.0 + t * t);
+  const double s = t * c;
+  const double rp = arp, rq = arq;
+  app = app - t * apq;
+  aqq = aqq + t * apq;
+  apq = 0.0;
+  arp = c * rp - s * rq;
+  arq = s * rp + c * rq;
+}
+
+// Smallest eigenvalue of the symmetric [[a00 a01 a02][. a11 a12][. . a22]] (DESIGN A.4).
+__device__ __forceinline__ double lmin3(double a00, double a11, double a22, double a01,
+                                        double a02, double a12) {
+  double amax = fabs(a00);
+  amax = fmax(amax, fabs(a11));
+  amax = fmax(amax, fabs(a22));
+  amax = fmax(amax, fabs(a01));
+  amax = fmax(amax, fabs(a02));
+  amax = fmax(amax, fabs(a12));
+  const double tol = amax * 0x1p-53;
+#pragma unroll 1
+  for (int sweep = 0; sweep < 4; ++sweep) {
+    jacobi_rot(a00, a11, a01, a02, a12, tol);  // (0,1), r3 = 2
+    jacobi_rot(a00, a22, a02, a01, a12, tol);  // (0,2), r3 = 1
+    jacobi_rot(a11, a22, a12, a01, a02, tol);  // (1,2), r3 = 0
+  }
+  return fmin(fmin(a00, a11), a22);
+}
+
+// Contract determinant / inverse (DESIGN A.3).
+template <int DIM>
+__device__ __forceinline__ double det_inv(const double (&J)[3][3], double (&Ji)[3][3]) {
+  if (DIM == 2) {
+    const double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    const double inv = 1.0 / det;
+    Ji[0][0] = J[1][1] * inv;
+    Ji[0][1] = -(J[0][1] * inv);
+    Ji[1][0] = -(J[1][0] * inv);
+    Ji[1][1] = J[0][0] * inv;
+    return det;
+  } else {
+    const double C00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    const double C01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    const double C02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    const double C10 = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+    const double C11 = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+    const double C12 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+    const double C20 = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+    const double C21 = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+    const double C22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    const double det = (J[0][0] * C00 + J[0][1] * C01) + J[0][2] * C02;
+    const double inv = 1.0 / det;
+    Ji[0][0] = C00 * inv; Ji[0][1] = C10 * inv; Ji[0][2] = C20 * inv;
+    Ji[1][0] = C01 * inv; Ji[1][1] = C11 * inv; Ji[1][2] = C21 * inv;
+    Ji[2][0] = C02 * inv; Ji[2][1] = C12 * inv; Ji[2][2] = C22 * inv;
+    return det;
+  }
+}
+
+template <int DIM>
+__device__ __forceinline__ double det_only(const double (&J)[3][3]) {
+  double Ji[3][3];
+  return det_inv<DIM>(J, Ji);
+}
+
+// Pointwise stage (DESIGN A.3). Returns dt_q; fills sigma (DIM x DIM), Ji, det.
+template <int DIM, bool VISC>
+__device__ __forceinline__ double pointwise(const double (&J)[3][3], const double (&Gv)[3][3],
+                                            double eq, double mq, double gam, double q1,
+                                            double q2, double alpha, double alpha_mu,
+                                            double (&sig)[3][3], double (&Ji)[3][3],
+                                            double &det_out) {
+  const double det = det_inv<DIM>(J, Ji);
+  det_out = det;
+  const double rho = mq / det;
+  const double p = ((gam - 1.0) * rho) * eq;
+  const double cs = sqrt((gam * (gam - 1.0)) * eq);
+  double h;
+  if (DIM == 2) {
+    const double c00 = J[0][0] * J[0][0] + J[1][0] * J[1][0];
+    const double c11 = J[0][1] * J[0][1] + J[1][1] * J[1][1];
+    const double c01 = J[0][0] * J[0][1] + J[1][0] * J[1][1];
+    const double kk = 0.5 * (c00 - c11);
+    const double smax2 = 0.5 * (c00 + c11) + sqrt(kk * kk + c01 * c01);
+    h = det / sqrt(smax2);
+  } else {
+    const double c00 = (J[0][0] * J[0][0] + J[1][0] * J[1][0]) + J[2][0] * J[2][0];
+    const double c11 = (J[0][1] * J[0][1] + J[1][1] * J[1][1]) + J[2][1] * J[2][1];
+    const double c22 = (J[0][2] * J[0][2] + J[1][2] * J[1][2]) + J[2][2] * J[2][2];
+    const double c01 = (J[0][0] * J[0][1] + J[1][0] * J[1][1]) + J[2][0] * J[2][1];
+    const double c02 = (J[0][0] * J[0][2] + J[1][0] * J[1][2]) + J[2][0] * J[2][2];
+    const double c12 = (J[0][1] * J[0][2] + J[1][1] * J[1][2]) + J[2][1] * J[2][2];
+    h = sqrt(fmax(lmin3(c00, c11, c22, c01, c02, c12), 0.0));
+  }
+  double mu = 0.0;
+  double eps[3][3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) eps[c][d] = 0.0;
+  if (VISC) {
+    double gv[3][3];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        double s = Gv[c][0] * Ji[0][d];
+#pragma unroll
+        for (int i = 1; i < DIM; ++i) s = s + Gv[c][i] * Ji[i][d];
+        gv[c][d] = s;
+      }
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+      eps[c][c] = gv[c][c];
+#pragma unroll
+      for (int d = 0; d < DIM; ++d)
+        if (d != c) eps[c][d] = 0.5 * (gv[c][d] + gv[d][c]);
+    }
+    double lam;
+    if (DIM == 2) {
+      const double k = 0.5 * (eps[0][0] - eps[1][1]);
+      lam = 0.5 * (eps[0][0] + eps[1][1]) - sqrt(k * k + eps[0][1] * eps[0][1]);
+    } else {
+      lam = lmin3(eps[0][0], eps[1][1], eps[2][2], eps[0][1], eps[0][2], eps[1][2]);
+    }
+    const double lneg = fmin(lam, 0.0);
+    mu = (rho * h) * ((q1 * cs) + ((q2 * h) * (-lneg)));
+  }
+  const double den = (rho * h) * h;
+  const double inv_dt = cs / h + (alpha_mu * mu) / den;
+  const double dtq = alpha / inv_dt;
+#pragma unroll
+  for (int c = 0; c < DIM; ++c)
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) sig[c][d] = mu * eps[c][d] - (c == d ? p : 0.0);
+  return dtq;
+}
+
+// ----------------------------------------------------------------------------- kernel
+template <int DIM, int K, int Q, bool VISC, int MODE>
+__global__ void __launch_bounds__(Geo<DIM, K, Q>::NT, (512 / Geo<DIM, K, Q>::NT) > 0 ? (512 / Geo<DIM, K, Q>::NT) : 1)
+force_kernel(const Params P) {
+  using G = Geo<DIM, K, Q>;
+  constexpr int N = G::N, M = G::M, ND = G::ND, NE = G::NE, NQ = G::NQ, EPB = G::EPB,
+                NT = G::NT;
+  extern __shared__ __align__(16) double smem[];
+  double *sW = smem;                    // [Q]
+  double *sB = sW + Q;                  // [Q][N]
+  double *sG = sB + Q * N;              // [Q][N]
+  double *sBl = sG + Q * N;             // [Q][M]
+  double *units = smem + G::TABD;       // EPB * UNIT
+  int *snode = (int *)(units + EPB * G::UNIT);             // [EPB][ND]
+  unsigned long long *skey = (unsigned long long *)(snode + EPB * ND);  // [EPB]
+  static_assert((G::EPB * G::ND) % 2 == 0, "8-byte alignment of the key array");
+
+  const int tid = threadIdx.x;
+  const int u = tid / NQ;               // unit within CTA (may be >= EPB for pad threads)
+  const int lt = tid - u * NQ;          // Gauss point within unit
+  const int64_t unit0 = (int64_t)blockIdx.x * EPB;
+  const int B = P.B;
+  const bool has_w = (MODE == MODE_FORCE) && (P.w != nullptr);
+  const int nf = MODE == MODE_MQ ? 1 : (has_w ? 3 : 2);
+
+  // --- tables to shared memory
+  for (int i = tid; i < Q; i += NT) sW[i] = P.tab_w[i];
+  for (int i = tid; i < Q * N; i += NT) { sB[i] = P.tab_B[i]; sG[i] = P.tab_G[i]; }
+  for (int i = tid; i < Q * M; i += NT) sBl[i] = P.tab_Bl[i];
+  for (int i = tid; i < EPB; i += NT) skey[i] = ~0ull;
+
+  // --- S1 gather: node ids, then fields (unit fastest for coalescing across instances)
+  for (int i = tid; i < EPB * ND; i += NT) {
+    const int uu = i % EPB, a = i / EPB;
+    const int64_t gu = unit0 + uu;
+    int nd = 0;
+    if (gu < P.n_units) nd = P.elem_nodes[(gu / B) * ND + a];
+    snode[uu * ND + a] = nd;
+  }
+  __syncthreads();
+  {
+    const int total = EPB * nf * DIM * ND;
+    for (int i = tid; i < total; i += NT) {
+      const int uu = i % EPB;
+      int r = i / EPB;
+      const int a = r % ND; r /= ND;
+      const int c = r % DIM;
+      const int f = r / DIM;
+      const int64_t gu = unit0 + uu;
+      double val = 0.0;
+      if (gu < P.n_units) {
+        const int64_t b = gu % B;
+        const int64_t idx = ((int64_t)c * P.ld_nodes + snode[uu * ND + a]) * B + b;
+        const double *src = MODE == MODE_MQ ? P.x : (f == 0 ? P.x : (f == 1 ? P.v : P.w));
+        val = __ldg(src + idx);
+      }
+      units[uu * G::UNIT + (f * DIM + c) * ND + a] = val;
+    }
+    if (MODE != MODE_MQ) {
+      for (int i = tid; i < EPB * NE; i += NT) {
+        const int uu = i % EPB, j = i / EPB;
+        const int64_t gu = unit0 + uu;
+        double val = 0.0;
+        if (gu < P.n_units) {
+          const int64_t l = gu / B, b = gu % B;
+          val = __ldg(P.e + (l * NE + j) * B + b);
+        }
+        units[uu * G::UNIT + G::NF * DIM * ND + j] = val;
+      }
+    }
+  }
+  __syncthreads();
+
+  const bool active = (u < EPB) && (unit0 + u < P.n_units);
+  const int uc = u < EPB ? u : EPB - 1;  // clamp pad threads onto a real unit buffer (reads only)
+  double *U = units + uc * G::UNIT;
+  double *Xs = U;                         // [NF][DIM][ND]
+  double *Es = U + G::NF * DIM * ND;      // [NE]
+  double *Wk = Es + NE;                   // work region
+  const int64_t gu = (unit0 + uc < P.n_units) ? unit0 + uc : 0;  // safe unit for reads
+  const int64_t l = gu / B;
+  const int b = (int)(gu % B);
+  const int64_t gid = P.elem_gid ? (int64_t)P.elem_gid[l] : l;
+
+  // --- S2 forward contractions (canonical order, DESIGN A.2)
+  double J[3][3], Gv[3][3], Gw[3][3];
+  double eq = 0.0;
+  int q1i, q2i, q3i = 0;
+  if (DIM == 2) { q1i = lt % Q; q2i = lt / Q; }
+  else { q1i = lt % Q; q2i = (lt / Q) % Q; q3i = lt / (Q * Q); }
+  if (lt >= NQ) { q1i = q2i = q3i = 0; }
+
+  if (DIM == 3) {
+    double *S1b = Wk;                              // [NF*DIM][2][Q][N][N]
+    double *S2b = Wk + G::NF * DIM * 2 * G::S1;    // [NF*DIM][3][Q][Q][N]
+    double *E1b = S2b + G::NF * DIM * 3 * G::S2;   // [Q][M][M]
+    double *E2b = E1b + G::E1;                     // [Q][Q][M]
+    if (u < EPB) {
+      // stage 1: contract a1
+      const int cnt1 = nf * DIM * 2 * Q * N * N;
+      for (int o = lt; o < cnt1; o += NQ) {
+        int r = o;
+        const int a3 = r % N; r /= N;
+        const int a2 = r % N; r /= N;
+        const int q1 = r % Q; r /= Q;
+        const int bg = r % 2;
+        const int fc = r / 2;
+        const double *tab = (bg ? sG : sB) + q1 * N;
+        const double *src = Xs + fc * ND + (a3 * N + a2) * N;
+        double acc = tab[0] * src[0];
+#pragma unroll
+        for (int a1 = 1; a1 < N; ++a1) acc = __fma_rn(tab[a1], src[a1], acc);
+        S1b[((fc * 2 + bg) * Q + q1) * N * N + a2 * N + a3] = acc;
+      }
+      if (MODE != MODE_MQ) {
+        for (int o = lt; o < Q * M * M; o += NQ) {
+          int r = o;
+          const int j3 = r % M; r /= M;
+          const int j2 = r % M;
+          const int q1 = r / M;
+          const double *tab = sBl + q1 * M;
+          const double *src = Es + (j3 * M + j2) * M;
+          double acc = tab[0] * src[0];
+#pragma unroll
+          for (int j1 = 1; j1 < M; ++j1) acc = __fma_rn(tab[j1], src[j1], acc);
+          E1b[(q1 * M + j2) * M + j3] = acc;
+        }
+      }
+    }
+    __syncthreads();
+    if (u < EPB) {
+      // stage 2: contract a2 ; kind 0: B.UG (d/dxi1), 1: G.UB (d/dxi2), 2: B.UB (d/dxi3)
+      const int cnt2 = nf * DIM * 3 * Q * Q * N;
+      for (int o = lt; o < cnt2; o += NQ) {
+        int r = o;
+        const int a3 = r % N; r /= N;
+        const int q2 = r % Q; r /= Q;
+        const int q1 = r % Q; r /= Q;
+        const int kind = r % 3;
+        const int fc = r / 3;
+        const double *tab = (kind == 1 ? sG : sB) + q2 * N;
+        const double *src = S1b + ((fc * 2 + (kind == 0 ? 1 : 0)) * Q + q1) * N * N + a3;
+        double acc = tab[0] * src[0];
+#pragma unroll
+        for (int a2 = 1; a2 < N; ++a2) acc = __fma_rn(tab[a2], src[a2 * N], acc);
+        S2b[((fc * 3 + kind) * Q + q1) * Q * N + q2 * N + a3] = acc;
+      }
+      if (MODE != MODE_MQ) {
+        for (int o = lt; o < Q * Q * M; o += NQ) {
+          int r = o;
+          const int j3 = r % M; r /= M;
+          const int q2 = r % Q;
+          const int q1 = r / Q;
+          const double *tab = sBl + q2 * M;
+          const double *src = E1b + q1 * M * M + j3;
+          double acc = tab[0] * src[0];
+#pragma unroll
+          for (int j2 = 1; j2 < M; ++j2) acc = __fma_rn(tab[j2], src[j2 * M], acc);
+          E2b[(q1 * Q + q2) * M + j3] = acc;
+        }
+      }
+    }
+    __syncthreads();
+    // stage 3 (per Gauss point): contract a3
+    {
+      const double *tB = sB + q3i * N, *tG = sG + q3i * N;
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        if (f >= nf) break;
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+          const int fc = f * DIM + c;
+          const double *p1 = S2b + ((fc * 3 + 0) * Q + q1i) * Q * N + q2i * N;
+          const double *p2 = S2b + ((fc * 3 + 1) * Q + q1i) * Q * N + q2i * N;
+          const double *p3 = S2b + ((fc * 3 + 2) * Q + q1i) * Q * N + q2i * N;
+          double d0 = tB[0] * p1[0], d1 = tB[0] * p2[0], d2 = tG[0] * p3[0];
+#pragma unroll
+          for (int a3 = 1; a3 < N; ++a3) {
+            d0 = __fma_rn(tB[a3], p1[a3], d0);
+            d1 = __fma_rn(tB[a3], p2[a3], d1);
+            d2 = __fma_rn(tG[a3], p3[a3], d2);
+          }
+          double *dst = f == 0 ? J[c] : (f == 1 ? Gv[c] : Gw[c]);
+          dst[0] = d0; dst[1] = d1; dst[2] = d2;
+        }
+      }
+      if (MODE != MODE_MQ) {
+        const double *tb = sBl + q3i * M;
+        const double *src = E2b + (q1i * Q + q2i) * M;
+        double acc = tb[0] * src[0];
+#pragma unroll
+        for (int j3 = 1; j3 < M; ++j3) acc = __fma_rn(tb[j3], src[j3], acc);
+        eq = acc;
+      }
+    }
+  } else {
+    double *S1b = Wk;                              // [NF*DIM][2][Q][N]
+    double *E1b = Wk + G::NF * DIM * 2 * G::S1;    // [Q][M]
+    if (u < EPB) {
+      const int cnt1 = nf * DIM * 2 * Q * N;
+      for (int o = lt; o < cnt1; o += NQ) {
+        int r = o;
+        const int a2 = r % N; r /= N;
+        const int q1 = r % Q; r /= Q;
+        const int bg = r % 2;
+        const int fc = r / 2;
+        const double *tab = (bg ? sG : sB) + q1 * N;
+        const double *src = Xs + fc * ND + a2 * N;
+        double acc = tab[0] * src[0];
+#pragma unroll
+        for (int a1 = 1; a1 < N; ++a1) acc = __fma_rn(tab[a1], src[a1], acc);
+        S1b[((fc * 2 + bg) * Q + q1) * N + a2] = acc;
+      }
+      if (MODE != MODE_MQ) {
+        for (int o = lt; o < Q * M; o += NQ) {
+          const int j2 = o % M, q1 = o / M;
+          const double *tab = sBl + q1 * M;
+          const double *src = Es + j2 * M;
+          double acc = tab[0] * src[0];
+#pragma unroll
+          for (int j1 = 1; j1 < M; ++j1) acc = __fma_rn(tab[j1], src[j1], acc);
+          E1b[q1 * M + j2] = acc;
+        }
+      }
+    }
+    __syncthreads();
+    {
+      const double *tB = sB + q2i * N, *tG = sG + q2i * N;
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        if (f >= nf) break;
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+          const int fc = f * DIM + c;
+          const double *uB = S1b + ((fc * 2 + 0) * Q + q1i) * N;
+          const double *uG = S1b + ((fc * 2 + 1) * Q + q1i) * N;
+          double d0 = tB[0] * uG[0], d1 = tG[0] * uB[0];
+#pragma unroll
+          for (int a2 = 1; a2 < N; ++a2) {
+            d0 = __fma_rn(tB[a2], uG[a2], d0);
+            d1 = __fma_rn(tG[a2], uB[a2], d1);
+          }
+          double *dst = f == 0 ? J[c] : (f == 1 ? Gv[c] : Gw[c]);
+          dst[0] = d0; dst[1] = d1;
+        }
+      }
+      if (MODE != MODE_MQ) {
+        const double *tb = sBl + q2i * M;
+        const double *src = E1b + q1i * M;
+        double acc = tb[0] * src[0];
+#pragma unroll
+        for (int j2 = 1; j2 < M; ++j2) acc = __fma_rn(tb[j2], src[j2], acc);
+        eq = acc;
+      }
+    }
+  }
+
+  // --- MODE_MQ: m_q = rho0_K detJ0 (density elimination)
+  if (MODE == MODE_MQ) {
+    if (active && lt < NQ) {
+      const double det0 = det_only<DIM>(J);
+      P.mq_out[gid * NQ + lt] = P.rho0[gid] * det0;
+    }
+    return;
+  }
+
+  // --- S3 pointwise
+  double sig[3][3], Ji[3][3], det = 1.0, dtq = 0.0;
+  const double gam = __ldg(P.gamma + gid);
+  const double mq = __ldg(P.mq + gid * NQ + lt);
+  dtq = pointwise<DIM, VISC>(J, Gv, eq, mq, gam, P.q1, P.q2, P.alpha, P.alpha_mu, sig, Ji, det);
+
+  // --- S6 dt: status flags, then min of order-preserving keys
+  unsigned long long key = ~0ull;
+  if (active) {
+    if (!(det > 0.0)) atomicMin(&P.st[b].first_bad, (unsigned long long)gid);
+    if (isnan(dtq)) atomicOr(&P.st[b].nan_flag, 1u);
+    else key = dt_key(dtq);
+  }
+  {
+    constexpr bool WARP_IN_UNIT = (NQ % 32 == 0) || (EPB == 1);
+    constexpr bool HALF = (NQ == 16);
+    if (WARP_IN_UNIT || HALF) {
+      const int width = WARP_IN_UNIT ? 32 : 16;
+#pragma unroll
+      for (int off = width / 2; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, key, off);
+        key = o < key ? o : key;
+      }
+      if ((tid & (width - 1)) == 0 && u < EPB) atomicMin(&skey[u], key);
+    } else {
+      if (u < EPB) atomicMin(&skey[u], key);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (B == 1) {
+      unsigned long long k = skey[0];
+      for (int i = 1; i < EPB; ++i) k = skey[i] < k ? skey[i] : k;
+      if (k != ~0ull) atomicMin(&P.st[0].dt_key, k);
+    }
+  }
+  if (B > 1 && tid < EPB) {
+    const int64_t g2 = unit0 + tid;
+    if (g2 < P.n_units && skey[tid] != ~0ull) atomicMin(&P.st[g2 % B].dt_key, skey[tid]);
+  }
+  if (MODE == MODE_DT) return;
+
+  // --- S4 backward
+  double *Ss = Wk;                      // [DIM*DIM][NQ]
+  double *As = Ss + DIM * DIM * NQ;     // [NQ]
+  double *Tb = As + NQ;
+  double *Wb = Tb + G::TB;
+  double *F1b = Wb + G::WB;
+  double *F2b = F1b + G::F1B;
+  __syncthreads();  // forward buffers are dead from here on
+  if (u < EPB && lt < NQ) {
+    double wq = sW[q1i] * sW[q2i];
+    if (DIM == 3) wq = wq * sW[q3i];
+    const double wd = wq * det;
+    double A = 0.0;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        double s = sig[c][0] * Ji[d][0];
+#pragma unroll
+        for (int i = 1; i < DIM; ++i) s = __fma_rn(sig[c][i], Ji[d][i], s);
+        s = wd * s;
+        Ss[(c * DIM + d) * NQ + lt] = s;
+        A = __fma_rn(s, has_w ? Gw[c][d] : Gv[c][d], A);
+      }
+    As[lt] = A;
+  }
+  __syncthreads();
+  const int64_t slot_base = l * ND;
+  if (DIM == 3) {
+    if (u < EPB) {
+      // b1: T[dl][c][q1][q2][a3] = sum_q3 (dl==2 ? G : B)[q3][a3] S[c][dl](q1,q2,q3)
+      for (int o = lt; o < DIM * DIM * Q * Q * N; o += NQ) {
+        int r = o;
+        const int a3 = r % N; r /= N;
+        const int q2 = r % Q; r /= Q;
+        const int q1 = r % Q; r /= Q;
+        const int c = r % DIM;
+        const int dl = r / DIM;
+        const double *tab = dl == 2 ? sG : sB;
+        const double *src = Ss + (c * DIM + dl) * NQ + q1 + Q * q2;
+        double acc = 0.0;
+#pragma unroll
+        for (int q3 = 0; q3 < Q; ++q3) acc = __fma_rn(tab[q3 * N + a3], src[q3 * Q * Q], acc);
+        Tb[o] = acc;
+      }
+      // f1[q1][q2][j3] = sum_q3 Bl[q3][j3] A(q1,q2,q3)
+      for (int o = lt; o < Q * Q * M; o += NQ) {
+        const int j3 = o % M, q2 = (o / M) % Q, q1 = o / (M * Q);
+        double acc = 0.0;
+#pragma unroll
+        for (int q3 = 0; q3 < Q; ++q3) acc = __fma_rn(sBl[q3 * M + j3], As[q1 + Q * q2 + Q * Q * q3], acc);
+        F1b[o] = acc;
+      }
+    }
+    __syncthreads();
+    if (u < EPB) {
+      // b2: W1[c][q1][a2][a3] = sum_q2 B[q2][a2] T0 ; W23 = sum_q2 G[q2][a2] T1 + B[q2][a2] T2
+      for (int o = lt; o < 2 * DIM * Q * N * N; o += NQ) {
+        int r = o;
+        const int a3 = r % N; r /= N;
+        const int a2 = r % N; r /= N;
+        const int q1 = r % Q; r /= Q;
+        const int c = r % DIM;
+        const int which = r / DIM;
+        double acc = 0.0;
+        if (which == 0) {
+          const double *t0 = Tb + ((0 * DIM + c) * Q + q1) * Q * N + a3;
+#pragma unroll
+          for (int q2 = 0; q2 < Q; ++q2) acc = __fma_rn(sB[q2 * N + a2], t0[q2 * N], acc);
+        } else {
+          const double *t1 = Tb + ((1 * DIM + c) * Q + q1) * Q * N + a3;
+          const double *t2 = Tb + ((2 * DIM + c) * Q + q1) * Q * N + a3;
+#pragma unroll
+          for (int q2 = 0; q2 < Q; ++q2) {
+            acc = __fma_rn(sG[q2 * N + a2], t1[q2 * N], acc);
+            acc = __fma_rn(sB[q2 * N + a2], t2[q2 * N], acc);
+          }
+        }
+        Wb[o] = acc;
+      }
+      // f2[q1][j2][j3] = sum_q2 Bl[q2][j2] f1[q1][q2][j3]
+      for (int o = lt; o < Q * M * M; o += NQ) {
+        const int j3 = o % M, j2 = (o / M) % M, q1 = o / (M * M);
+        double acc = 0.0;
+#pragma unroll
+        for (int q2 = 0; q2 < Q; ++q2) acc = __fma_rn(sBl[q2 * M + j2], F1b[(q1 * Q + q2) * M + j3], acc);
+        F2b[o] = acc;
+      }
+    }
+    __syncthreads();
+    if (active) {
+      // b3: F1[c][a] = sum_q1 G[q1][a1] W1[c][q1][a2][a3] + B[q1][a1] W23[c][q1][a2][a3]
+      for (int o = lt; o < DIM * ND; o += NQ) {
+        const int a = o % ND, c = o / ND;
+        const int a1 = a % N, a23 = a / N;  // a23 = a2 + N a3
+        const int a2 = a23 % N, a3 = a23 / N;
+        double acc = 0.0;
+#pragma unroll
+        for (int q1 = 0; q1 < Q; ++q1) {
+          acc = __fma_rn(sG[q1 * N + a1], Wb[((0 * DIM + c) * Q + q1) * N * N + a2 * N + a3], acc);
+          acc = __fma_rn(sB[q1 * N + a1], Wb[((1 * DIM + c) * Q + q1) * N * N + a2 * N + a3], acc);
+        }
+        const int s = P.slot[slot_base + a];
+        if (s >= 0) P.evec[((int64_t)s * DIM + c) * B + b] = acc;
+      }
+      const int64_t row = P.ftw_row ? (int64_t)P.ftw_row[l] : l;
+      if (row >= 0) {
+        for (int o = lt; o < NE; o += NQ) {
+          const int j1 = o % M, j2 = (o / M) % M, j3 = o / (M * M);
+          double acc = 0.0;
+#pragma unroll
+          for (int q1 = 0; q1 < Q; ++q1) acc = __fma_rn(sBl[q1 * M + j1], F2b[(q1 * M + j2) * M + j3], acc);
+          P.FTw[(row * NE + o) * B + b] = acc;
+        }
+      }
+    }
+  } else {
+    if (u < EPB) {
+      // b1: T[dl][c][q1][a2] = sum_q2 (dl==1 ? G : B)[q2][a2] S[c][dl](q1,q2)
+      for (int o = lt; o < DIM * DIM * Q * N; o += NQ) {
+        int r = o;
+        const int a2 = r % N; r /= N;
+        const int q1 = r % Q; r /= Q;
+        const int c = r % DIM;
+        const int dl = r / DIM;
+        const double *tab = dl == 1 ? sG : sB;
+        const double *src = Ss + (c * DIM + dl) * NQ + q1;
+        double acc = 0.0;
+#pragma unroll
+        for (int q2 = 0; q2 < Q; ++q2) acc = __fma_rn(tab[q2 * N + a2], src[q2 * Q], acc);
+        Tb[o] = acc;
+      }
+      for (int o = lt; o < Q * M; o += NQ) {
+        const int j2 = o % M, q1 = o / M;
+        double acc = 0.0;
+#pragma unroll
+        for (int q2 = 0; q2 < Q; ++q2) acc = __fma_rn(sBl[q2 * M + j2], As[q1 + Q * q2], acc);
+        F1b[o] = acc;
+      }
+    }
+    __syncthreads();
+    if (active) {
+      for (int o = lt; o < DIM * ND; o += NQ) {
+        const int a = o % ND, c = o / ND;
+        const int a1 = a % N, a2 = a / N;
+        double acc = 0.0;
+#pragma unroll
+        for (int q1 = 0; q1 < Q; ++q1) {
+          acc = __fma_rn(sG[q1 * N + a1], Tb[((0 * DIM + c) * Q + q1) * N + a2], acc);
+          acc = __fma_rn(sB[q1 * N + a1], Tb[((1 * DIM + c) * Q + q1) * N + a2], acc);
+        }
+        const int s = P.slot[slot_base + a];
+        if (s >= 0) P.evec[((int64_t)s * DIM + c) * B + b] = acc;
+      }
+      const int64_t row = P.ftw_row ? (int64_t)P.ftw_row[l] : l;
+      if (row >= 0) {
+        for (int o = lt; o < NE; o += NQ) {
+          const int j1 = o % M, j2 = o / M;
+          double acc = 0.0;
+#pragma unroll
+          for (int q1 = 0; q1 < Q; ++q1) acc = __fma_rn(sBl[q1 * M + j1], F1b[q1 * M + j2], acc);
+          P.FTw[(row * NE + o) * B + b] = acc;
+        }
+      }
+    }
+  }
+}
+
+// dt of the call = min key (NaN if any dt_q was NaN); per-call state is reset for the
+// next call and the NaN condition is folded into the sticky word read by status_sync.
+__device__ __forceinline__ void finalize_one(hydro_devstatus *st, double *dt_out) {
+  double d = key_to_dt(st->dt_key);
+  if (st->nan_flag) {
+    d = __longlong_as_double(0x7ff8000000000000ll);
+    st->nan_sticky = 1u;
+  }
+  if (dt_out) *dt_out = d;
+  st->dt_key = dt_key(__longlong_as_double(0x7ff0000000000000ll));  // +inf
+  st->nan_flag = 0u;
+}
+
+// ----------------------------------------------------------------------------- assembly
+// F1[c][node] (or F1_rows[(c*n_nodes + node)*B + b]) = sum over the node's slots in
+// ascending order (slots are laid out by ascending element) -- deterministic.
+template <int DIM>
+__global__ void assemble_kernel(int64_t n_nodes, int B, const int32_t *__restrict__ off,
+                                const double *__restrict__ evec, double *__restrict__ F1,
+                                hydro_devstatus *st, double *dt_out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n_nodes * B) {
+    const int64_t node = t / B;
+    const int b = (int)(t % B);
+    const int s0 = off[node], s1 = off[node + 1];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+      double acc = 0.0;
+      for (int s = s0; s < s1; ++s) acc += evec[((int64_t)s * DIM + c) * B + b];
+      F1[((int64_t)c * n_nodes + node) * B + b] = acc;
+    }
+  }
+  // dt finalisation (the force kernel finished before this launch started)
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < B; i += blockDim.x) {
+      finalize_one(st + i, dt_out ? dt_out + i : nullptr);
+    }
+  }
+}
+
+__global__ void finalize_dt_kernel(int B, hydro_devstatus *st, double *dt_out) {
+  for (int i = threadIdx.x; i < B; i += blockDim.x) finalize_one(st + i, dt_out ? dt_out + i : nullptr);
+}
+
+}  // namespace hk

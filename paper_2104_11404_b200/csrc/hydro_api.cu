@@ -1,0 +1,596 @@
+// hydro_api.cu -- the C ABI of include/hydro.h: argument checks, context/sample-plan
+// setup (S0, untimed), and the launch sequences of the hot path (S1-S9).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/hydro.h"
+#include "force_kernel.cuh"
+#include "hydro_internal.h"
+#include "rom_kernels.cuh"
+
+namespace {
+
+std::atomic<int64_t> g_launches{0};
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Layout {
+  size_t tables, status, mq, off, slot, evec, total;
+};
+
+bool supported(int dim, int k, int q) {
+  return (dim == 2 || dim == 3) && ((k == 2 && q == 4) || (k == 3 && q == 6));
+}
+
+int ipow(int b, int e) {
+  int r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+
+bool layout_for(const hydro_mesh_desc *d, Layout *L) {
+  if (!d || !supported(d->dim, d->order_h1, d->nq1d) || d->n_elem <= 0 || d->n_nodes <= 0)
+    return false;
+  const int64_t nd = ipow(d->order_h1 + 1, d->dim), nq = ipow(d->nq1d, d->dim);
+  if (d->n_elem * nd >= (int64_t)1 << 31) return false;  // int32 slots
+  size_t o = 0;
+  L->tables = o; o = align256(o + sizeof(double) * HYDRO_TAB_DOUBLES);
+  L->status = o; o = align256(o + sizeof(hydro_devstatus));
+  L->mq = o;     o = align256(o + sizeof(double) * (size_t)(d->n_elem * nq));
+  L->off = o;    o = align256(o + sizeof(int32_t) * (size_t)(d->n_nodes + 1));
+  L->slot = o;   o = align256(o + sizeof(int32_t) * (size_t)(d->n_elem * nd));
+  L->evec = o;   o = align256(o + sizeof(double) * (size_t)(d->n_elem * nd * d->dim));
+  L->total = o;
+  return true;
+}
+
+#define CUDA_OK(x)                                   \
+  do {                                               \
+    cudaError_t e_ = (x);                            \
+    if (e_ != cudaSuccess) {                         \
+      fprintf(stderr, "hydro: %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return HYDRO_ERR_CUDA;                         \
+    }                                                \
+  } while (0)
+
+// device tables [w(q) | B(q*n) | G(q*n) | Bl(q*m)]
+void pack_tables(const hydro_tables_t &T, std::vector<double> &out) {
+  const int q = T.q, n = T.k + 1, m = T.k;
+  out.assign(HYDRO_TAB_DOUBLES, 0.0);
+  size_t o = 0;
+  for (int i = 0; i < q; ++i) out[o++] = T.w[i];
+  for (int i = 0; i < q; ++i)
+    for (int a = 0; a < n; ++a) out[o++] = T.B[i][a];
+  for (int i = 0; i < q; ++i)
+    for (int a = 0; a < n; ++a) out[o++] = T.G[i][a];
+  for (int i = 0; i < q; ++i)
+    for (int j = 0; j < m; ++j) out[o++] = T.Bl[i][j];
+}
+
+}  // namespace
+
+struct hydro_ctx {
+  hydro_mesh_desc d;
+  int nd, ne, nq;
+  char *ws;
+  Layout L;
+  double *tab;            // device packed tables
+  hydro_devstatus *st;
+  double *mq;
+  int32_t *off, *slot;
+  double *evec;
+  std::vector<int32_t> h_elem_nodes;  // host copy (sample plans)
+};
+
+struct hydro_sample {
+  hydro_ctx *ctx;
+  int B;
+  int64_t n_cl, n_cl_nodes, n_s0_nodes, n_s0;
+  int64_t n_slots;
+  std::vector<int32_t> h_closure;
+  std::vector<int64_t> h_cl_nodes, h_s0_nodes;
+  int32_t *elem_nodes = nullptr, *elem_gid = nullptr, *slot = nullptr, *off = nullptr,
+          *ftw_row = nullptr;
+  double *evec = nullptr;
+  hydro_devstatus *st = nullptr;
+};
+
+namespace {
+
+// --- profiling: event pairs around the force kernel (bench.py's live roofline)
+struct ProfState {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending, pool;
+};
+ProfState g_prof;
+
+std::pair<cudaEvent_t, cudaEvent_t> prof_pair() {
+  if (!g_prof.pool.empty()) {
+    auto p = g_prof.pool.back();
+    g_prof.pool.pop_back();
+    return p;
+  }
+  std::pair<cudaEvent_t, cudaEvent_t> p;
+  cudaEventCreate(&p.first);
+  cudaEventCreate(&p.second);
+  return p;
+}
+
+template <int DIM, int K, int Q>
+hydro_status launch_force_t(int mode, bool visc, const hk::Params &P, cudaStream_t s) {
+  using G = hk::Geo<DIM, K, Q>;
+  const int64_t grid = (P.n_units + G::EPB - 1) / G::EPB;
+  if (grid <= 0) return HYDRO_OK;
+  void (*kern)(const hk::Params);
+  if (mode == hk::MODE_FORCE)
+    kern = visc ? hk::force_kernel<DIM, K, Q, true, hk::MODE_FORCE>
+                : hk::force_kernel<DIM, K, Q, false, hk::MODE_FORCE>;
+  else if (mode == hk::MODE_DT)
+    kern = visc ? hk::force_kernel<DIM, K, Q, true, hk::MODE_DT>
+                : hk::force_kernel<DIM, K, Q, false, hk::MODE_DT>;
+  else
+    kern = hk::force_kernel<DIM, K, Q, false, hk::MODE_MQ>;
+  static bool attr_set[3][2] = {{false, false}, {false, false}, {false, false}};
+  if (!attr_set[mode][visc ? 1 : 0]) {
+    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+    attr_set[mode][visc ? 1 : 0] = true;
+  }
+  std::pair<cudaEvent_t, cudaEvent_t> ev;
+  const bool prof = g_prof.on && mode != hk::MODE_MQ;
+  if (prof) {
+    ev = prof_pair();
+    cudaEventRecord(ev.first, s);
+  }
+  kern<<<(unsigned)grid, G::NT, G::SMEM, s>>>(P);
+  g_launches++;
+  if (prof) {
+    cudaEventRecord(ev.second, s);
+    g_prof.pending.push_back(ev);
+  }
+  CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
+hydro_status launch_force(int dim, int k, int mode, bool visc, const hk::Params &P,
+                          cudaStream_t s) {
+  if (dim == 2 && k == 2) return launch_force_t<2, 2, 4>(mode, visc, P, s);
+  if (dim == 3 && k == 2) return launch_force_t<3, 2, 4>(mode, visc, P, s);
+  if (dim == 2 && k == 3) return launch_force_t<2, 3, 6>(mode, visc, P, s);
+  if (dim == 3 && k == 3) return launch_force_t<3, 3, 6>(mode, visc, P, s);
+  return HYDRO_ERR_UNSUPPORTED;
+}
+
+hydro_status launch_assemble(int dim, int64_t n_nodes, int B, const int32_t *off,
+                             const double *evec, double *F1, hydro_devstatus *st, double *dt,
+                             cudaStream_t s) {
+  const int threads = 256;
+  int64_t blocks = (n_nodes * B + threads - 1) / threads;
+  if (blocks < 1) blocks = 1;
+  if (dim == 2)
+    hk::assemble_kernel<2><<<(unsigned)blocks, threads, 0, s>>>(n_nodes, B, off, evec, F1, st, dt);
+  else
+    hk::assemble_kernel<3><<<(unsigned)blocks, threads, 0, s>>>(n_nodes, B, off, evec, F1, st, dt);
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
+void fill_tables_ptrs(hk::Params &P, const hydro_ctx *c) {
+  const int q = c->d.nq1d, n = c->d.order_h1 + 1;
+  P.tab_w = c->tab;
+  P.tab_B = c->tab + q;
+  P.tab_G = c->tab + q + q * n;
+  P.tab_Bl = c->tab + q + 2 * q * n;
+}
+
+}  // namespace
+
+extern "C" {
+
+hydro_status hydro_profile_enable(int on) {
+  g_prof.on = on != 0;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_profile_read(double *total_ms, int64_t *count) {
+  double tot = 0.0;
+  int64_t n = 0;
+  for (auto &p : g_prof.pending) {
+    CUDA_OK(cudaEventSynchronize(p.second));
+    float ms = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&ms, p.first, p.second));
+    tot += ms;
+    ++n;
+    g_prof.pool.push_back(p);
+  }
+  g_prof.pending.clear();
+  if (total_ms) *total_ms = tot;
+  if (count) *count = n;
+  return HYDRO_OK;
+}
+
+const char *hydro_version(void) { return "hydro-b200 0.1 (sm_100a, FP64)"; }
+
+int64_t hydro_launch_count(void) { return g_launches.load(); }
+
+hydro_status hydro_basis_tables(int k, int q, double *xi, double *w, double *B, double *G,
+                                double *Bl) {
+  hydro_tables_t T;
+  if (hydro_make_tables(k, q, &T)) return HYDRO_ERR_ARG;
+  for (int i = 0; i < q; ++i) {
+    if (xi) xi[i] = T.xi[i];
+    if (w) w[i] = T.w[i];
+    for (int a = 0; a <= k; ++a) {
+      if (B) B[i * (k + 1) + a] = T.B[i][a];
+      if (G) G[i * (k + 1) + a] = T.G[i][a];
+    }
+    for (int j = 0; j < k; ++j)
+      if (Bl) Bl[i * k + j] = T.Bl[i][j];
+  }
+  return HYDRO_OK;
+}
+
+size_t hydro_ctx_workspace_bytes(const hydro_mesh_desc *desc) {
+  Layout L;
+  if (!layout_for(desc, &L)) return 0;
+  return L.total;
+}
+
+hydro_status hydro_ctx_create(const hydro_mesh_desc *desc, void *workspace, size_t ws_bytes,
+                              hydro_stream_t stream, hydro_ctx **out) {
+  if (!desc || !out) return HYDRO_ERR_ARG;
+  *out = nullptr;
+  if (!supported(desc->dim, desc->order_h1, desc->nq1d)) return HYDRO_ERR_UNSUPPORTED;
+  if (!desc->elem_nodes || !desc->x0 || !desc->rho0) return HYDRO_ERR_ARG;
+  Layout L;
+  if (!layout_for(desc, &L)) return HYDRO_ERR_ARG;
+  if (!workspace || ws_bytes < L.total || ((uintptr_t)workspace & 255)) return HYDRO_ERR_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  hydro_ctx *c = new hydro_ctx();
+  c->d = *desc;
+  c->nd = ipow(desc->order_h1 + 1, desc->dim);
+  c->ne = ipow(desc->order_h1, desc->dim);
+  c->nq = ipow(desc->nq1d, desc->dim);
+  c->ws = (char *)workspace;
+  c->L = L;
+  c->tab = (double *)(c->ws + L.tables);
+  c->st = (hydro_devstatus *)(c->ws + L.status);
+  c->mq = (double *)(c->ws + L.mq);
+  c->off = (int32_t *)(c->ws + L.off);
+  c->slot = (int32_t *)(c->ws + L.slot);
+  c->evec = (double *)(c->ws + L.evec);
+  auto fail = [&](hydro_status st) { delete c; return st; };
+  // tables
+  hydro_tables_t T;
+  if (hydro_make_tables(desc->order_h1, desc->nq1d, &T)) return fail(HYDRO_ERR_ARG);
+  std::vector<double> packed;
+  pack_tables(T, packed);
+  if (cudaMemcpyAsync(c->tab, packed.data(), sizeof(double) * HYDRO_TAB_DOUBLES, cudaMemcpyHostToDevice, s) !=
+      cudaSuccess)
+    return fail(HYDRO_ERR_CUDA);
+  // status block
+  hydro_devstatus hst;
+  hst.dt_key = 0xFFF0000000000000ull;  // key(+inf) = bits(+inf) | sign bit
+  hst.first_bad = ~0ull;
+  hst.nan_flag = 0;
+  hst.nan_sticky = 0;
+  // node -> slot CSR on the host (setup, untimed): slots of a node ordered by element
+  const int64_t E = desc->n_elem, NN = desc->n_nodes, nd = c->nd;
+  c->h_elem_nodes.resize((size_t)(E * nd));
+  if (cudaMemcpyAsync(c->h_elem_nodes.data(), desc->elem_nodes, sizeof(int32_t) * E * nd,
+                      cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return fail(HYDRO_ERR_CUDA);
+  std::vector<int32_t> off((size_t)NN + 1, 0), slot((size_t)(E * nd));
+  for (int64_t i = 0; i < E * nd; ++i) {
+    const int32_t nde = c->h_elem_nodes[(size_t)i];
+    if (nde < 0 || nde >= NN) return fail(HYDRO_ERR_ARG);
+    off[(size_t)nde + 1]++;
+  }
+  for (int64_t i = 0; i < NN; ++i) off[(size_t)i + 1] += off[(size_t)i];
+  {
+    std::vector<int32_t> pos(off.begin(), off.end() - 1);
+    for (int64_t i = 0; i < E * nd; ++i) slot[(size_t)i] = pos[(size_t)c->h_elem_nodes[(size_t)i]]++;
+  }
+  if (cudaMemcpyAsync(c->st, &hst, sizeof(hst), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(c->off, off.data(), sizeof(int32_t) * (NN + 1), cudaMemcpyHostToDevice, s) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(c->slot, slot.data(), sizeof(int32_t) * E * nd, cudaMemcpyHostToDevice, s) !=
+          cudaSuccess)
+    return fail(HYDRO_ERR_CUDA);
+  // m_q = rho0_K detJ0 (density elimination) with the contract formulas
+  hk::Params P;
+  std::memset(&P, 0, sizeof(P));
+  P.n_units = E;
+  P.B = 1;
+  P.ld_nodes = NN;
+  P.elem_nodes = desc->elem_nodes;
+  P.x = desc->x0;
+  P.rho0 = desc->rho0;
+  P.mq_out = c->mq;
+  P.st = c->st;
+  fill_tables_ptrs(P, c);
+  hydro_status r = launch_force(desc->dim, desc->order_h1, hk::MODE_MQ, false, P, s);
+  if (r != HYDRO_OK) return fail(r);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return fail(HYDRO_ERR_CUDA);
+  *out = c;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_ctx_destroy(hydro_ctx *ctx) {
+  delete ctx;
+  return HYDRO_OK;
+}
+
+static hydro_status force_common(hydro_ctx *c, int mode, const double *x, const double *v,
+                                 const double *e, const double *w, const double *gamma,
+                                 hydro_visc visc, hydro_cfl cfl, double *F1, double *FTw,
+                                 double *dt, cudaStream_t s) {
+  if (!c || !x || !v || !e || !gamma) return HYDRO_ERR_ARG;
+  if (mode == hk::MODE_FORCE && (!F1 || !FTw)) return HYDRO_ERR_ARG;
+  hk::Params P;
+  std::memset(&P, 0, sizeof(P));
+  P.n_units = c->d.n_elem;
+  P.B = 1;
+  P.ld_nodes = c->d.n_nodes;
+  P.elem_nodes = c->d.elem_nodes;
+  P.x = x; P.v = v; P.w = w; P.e = e; P.gamma = gamma; P.mq = c->mq; P.rho0 = c->d.rho0;
+  P.q1 = visc.q1; P.q2 = visc.q2; P.alpha = cfl.alpha; P.alpha_mu = cfl.alpha_mu;
+  P.visc = visc.enabled;
+  P.evec = c->evec;
+  P.slot = c->slot;
+  P.FTw = FTw;
+  P.st = c->st;
+  fill_tables_ptrs(P, c);
+  hydro_status r = launch_force(c->d.dim, c->d.order_h1, mode, visc.enabled != 0, P, s);
+  if (r != HYDRO_OK) return r;
+  if (mode == hk::MODE_FORCE)
+    return launch_assemble(c->d.dim, c->d.n_nodes, 1, c->off, c->evec, F1, c->st, dt, s);
+  hk::finalize_dt_kernel<<<1, 32, 0, s>>>(1, c->st, dt);
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
+hydro_status hydro_force_full(hydro_ctx *ctx, const double *x, const double *v, const double *e,
+                              const double *w, const double *gamma, hydro_visc visc,
+                              hydro_cfl cfl, double *F1, double *FTw, double *dt,
+                              hydro_stream_t stream) {
+  return force_common(ctx, hk::MODE_FORCE, x, v, e, w, gamma, visc, cfl, F1, FTw, dt,
+                      (cudaStream_t)stream);
+}
+
+hydro_status hydro_dt_estimate(hydro_ctx *ctx, const double *x, const double *v, const double *e,
+                               const double *gamma, hydro_visc visc, hydro_cfl cfl, double *dt,
+                               hydro_stream_t stream) {
+  return force_common(ctx, hk::MODE_DT, x, v, e, nullptr, gamma, visc, cfl, nullptr, nullptr, dt,
+                      (cudaStream_t)stream);
+}
+
+static hydro_status status_sync_impl(hydro_devstatus *st, int B, cudaStream_t s,
+                                     int64_t *first_bad) {
+  CUDA_OK(cudaStreamSynchronize(s));
+  CUDA_OK(cudaGetLastError());
+  std::vector<hydro_devstatus> h((size_t)B);
+  CUDA_OK(cudaMemcpy(h.data(), st, sizeof(hydro_devstatus) * B, cudaMemcpyDeviceToHost));
+  unsigned long long bad = ~0ull;
+  bool nan = false;
+  for (auto &x : h) {
+    bad = std::min(bad, x.first_bad);
+    nan = nan || x.nan_sticky || x.nan_flag;
+    x.first_bad = ~0ull;
+    x.nan_sticky = 0;
+  }
+  CUDA_OK(cudaMemcpy(st, h.data(), sizeof(hydro_devstatus) * B, cudaMemcpyHostToDevice));
+  if (first_bad) *first_bad = bad == ~0ull ? -1 : (int64_t)bad;
+  if (bad != ~0ull) return HYDRO_ERR_TANGLED;
+  if (nan) return HYDRO_ERR_NONFINITE;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_status_sync(hydro_ctx *ctx, hydro_stream_t stream, int64_t *first_bad_elem) {
+  if (!ctx) return HYDRO_ERR_ARG;
+  return status_sync_impl(ctx->st, 1, (cudaStream_t)stream, first_bad_elem);
+}
+
+// ------------------------------------------------------------------------------ ROM
+hydro_status hydro_sample_create(hydro_ctx *c, const int32_t *sample_elems, int64_t n_sample,
+                                 int B, hydro_sample **out) {
+  if (!c || !sample_elems || n_sample <= 0 || B <= 0 || !out) return HYDRO_ERR_ARG;
+  *out = nullptr;
+  const int64_t E = c->d.n_elem, NN = c->d.n_nodes, nd = c->nd, ne = c->ne;
+  for (int64_t i = 0; i < n_sample; ++i) {
+    if (sample_elems[i] < 0 || sample_elems[i] >= E) return HYDRO_ERR_ARG;
+    if (i && sample_elems[i] <= sample_elems[i - 1]) return HYDRO_ERR_ARG;  // sorted unique
+  }
+  const int32_t *en = c->h_elem_nodes.data();
+  std::vector<char> s0node((size_t)NN, 0), clnode((size_t)NN, 0);
+  std::vector<int64_t> s0idx((size_t)E, -1);
+  for (int64_t i = 0; i < n_sample; ++i) {
+    const int64_t K = sample_elems[i];
+    s0idx[(size_t)K] = i;
+    for (int a = 0; a < nd; ++a) s0node[(size_t)en[K * nd + a]] = 1;
+  }
+  hydro_sample *p = new hydro_sample();
+  p->ctx = c;
+  p->B = B;
+  p->n_s0 = n_sample;
+  for (int64_t K = 0; K < E; ++K) {
+    bool hit = false;
+    for (int a = 0; a < nd && !hit; ++a) hit = s0node[(size_t)en[K * nd + a]] != 0;
+    if (hit) {
+      p->h_closure.push_back((int32_t)K);
+      for (int a = 0; a < nd; ++a) clnode[(size_t)en[K * nd + a]] = 1;
+    }
+  }
+  std::vector<int64_t> local((size_t)NN, -1), s0local((size_t)NN, -1);
+  for (int64_t i = 0; i < NN; ++i) {
+    if (clnode[(size_t)i]) { local[(size_t)i] = (int64_t)p->h_cl_nodes.size(); p->h_cl_nodes.push_back(i); }
+    if (s0node[(size_t)i]) { s0local[(size_t)i] = (int64_t)p->h_s0_nodes.size(); p->h_s0_nodes.push_back(i); }
+  }
+  p->n_cl = (int64_t)p->h_closure.size();
+  p->n_cl_nodes = (int64_t)p->h_cl_nodes.size();
+  p->n_s0_nodes = (int64_t)p->h_s0_nodes.size();
+  // local tables; slots (CSR over S0 nodes, ordered by closure element)
+  std::vector<int32_t> len((size_t)(p->n_cl * nd)), gid((size_t)p->n_cl), frow((size_t)p->n_cl),
+      slot((size_t)(p->n_cl * nd), -1), off((size_t)p->n_s0_nodes + 1, 0);
+  for (int64_t l = 0; l < p->n_cl; ++l) {
+    const int64_t K = p->h_closure[(size_t)l];
+    gid[(size_t)l] = (int32_t)K;
+    frow[(size_t)l] = (int32_t)s0idx[(size_t)K];
+    for (int a = 0; a < nd; ++a) {
+      const int32_t g = en[K * nd + a];
+      len[(size_t)(l * nd + a)] = (int32_t)local[(size_t)g];
+      if (s0local[(size_t)g] >= 0) off[(size_t)s0local[(size_t)g] + 1]++;
+    }
+  }
+  for (int64_t i = 0; i < p->n_s0_nodes; ++i) off[(size_t)i + 1] += off[(size_t)i];
+  p->n_slots = off[(size_t)p->n_s0_nodes];
+  {
+    std::vector<int32_t> pos(off.begin(), off.end() - 1);
+    for (int64_t l = 0; l < p->n_cl; ++l)
+      for (int a = 0; a < nd; ++a) {
+        const int64_t sl = s0local[(size_t)en[(int64_t)p->h_closure[(size_t)l] * nd + a]];
+        if (sl >= 0) slot[(size_t)(l * nd + a)] = pos[(size_t)sl]++;
+      }
+  }
+  (void)ne;
+  auto fail = [&](hydro_status st) { hydro_sample_destroy(p); return st; };
+  const size_t evec_bytes = sizeof(double) * (size_t)p->n_slots * c->d.dim * B;
+  if (cudaMalloc(&p->elem_nodes, sizeof(int32_t) * len.size()) != cudaSuccess ||
+      cudaMalloc(&p->elem_gid, sizeof(int32_t) * gid.size()) != cudaSuccess ||
+      cudaMalloc(&p->ftw_row, sizeof(int32_t) * frow.size()) != cudaSuccess ||
+      cudaMalloc(&p->slot, sizeof(int32_t) * slot.size()) != cudaSuccess ||
+      cudaMalloc(&p->off, sizeof(int32_t) * off.size()) != cudaSuccess ||
+      cudaMalloc(&p->evec, evec_bytes > 0 ? evec_bytes : 8) != cudaSuccess ||
+      cudaMalloc(&p->st, sizeof(hydro_devstatus) * B) != cudaSuccess)
+    return fail(HYDRO_ERR_CUDA);
+  std::vector<hydro_devstatus> hst((size_t)B);
+  for (auto &h : hst) { h.dt_key = 0xFFF0000000000000ull; h.first_bad = ~0ull; h.nan_flag = 0; h.nan_sticky = 0; }
+  if (cudaMemcpy(p->elem_nodes, len.data(), sizeof(int32_t) * len.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->elem_gid, gid.data(), sizeof(int32_t) * gid.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->ftw_row, frow.data(), sizeof(int32_t) * frow.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->slot, slot.data(), sizeof(int32_t) * slot.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->off, off.data(), sizeof(int32_t) * off.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->st, hst.data(), sizeof(hydro_devstatus) * B, cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail(HYDRO_ERR_CUDA);
+  *out = p;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_sample_destroy(hydro_sample *p) {
+  if (!p) return HYDRO_OK;
+  cudaFree(p->elem_nodes); cudaFree(p->elem_gid); cudaFree(p->ftw_row); cudaFree(p->slot);
+  cudaFree(p->off); cudaFree(p->evec); cudaFree(p->st);
+  delete p;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_sample_info(const hydro_sample *p, int64_t *n_closure_elem,
+                               int64_t *n_closure_nodes, int64_t *n_s0_nodes, int64_t *s_v,
+                               int64_t *s_e) {
+  if (!p) return HYDRO_ERR_ARG;
+  if (n_closure_elem) *n_closure_elem = p->n_cl;
+  if (n_closure_nodes) *n_closure_nodes = p->n_cl_nodes;
+  if (n_s0_nodes) *n_s0_nodes = p->n_s0_nodes;
+  if (s_v) *s_v = p->n_s0_nodes * p->ctx->d.dim;
+  if (s_e) *s_e = p->n_s0 * p->ctx->ne;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_sample_lists(const hydro_sample *p, int32_t *closure_elems,
+                                int64_t *closure_nodes, int64_t *s0_nodes) {
+  if (!p) return HYDRO_ERR_ARG;
+  if (closure_elems) std::copy(p->h_closure.begin(), p->h_closure.end(), closure_elems);
+  if (closure_nodes) std::copy(p->h_cl_nodes.begin(), p->h_cl_nodes.end(), closure_nodes);
+  if (s0_nodes) std::copy(p->h_s0_nodes.begin(), p->h_s0_nodes.end(), s0_nodes);
+  return HYDRO_OK;
+}
+
+hydro_status hydro_force_sampled(hydro_sample *p, const double *x_S, const double *v_S,
+                                 const double *e_S, const double *w_S, const double *gamma,
+                                 hydro_visc visc, hydro_cfl cfl, double *F1_rows,
+                                 double *FTw_rows, double *dt, hydro_stream_t stream) {
+  if (!p || !x_S || !v_S || !e_S || !gamma || !F1_rows || !FTw_rows) return HYDRO_ERR_ARG;
+  hydro_ctx *c = p->ctx;
+  cudaStream_t s = (cudaStream_t)stream;
+  hk::Params P;
+  std::memset(&P, 0, sizeof(P));
+  P.n_units = p->n_cl * p->B;
+  P.B = p->B;
+  P.ld_nodes = p->n_cl_nodes;
+  P.elem_nodes = p->elem_nodes;
+  P.elem_gid = p->elem_gid;
+  P.x = x_S; P.v = v_S; P.w = w_S; P.e = e_S; P.gamma = gamma; P.mq = c->mq; P.rho0 = c->d.rho0;
+  P.q1 = visc.q1; P.q2 = visc.q2; P.alpha = cfl.alpha; P.alpha_mu = cfl.alpha_mu;
+  P.visc = visc.enabled;
+  P.evec = p->evec;
+  P.slot = p->slot;
+  P.FTw = FTw_rows;
+  P.ftw_row = p->ftw_row;
+  P.st = p->st;
+  fill_tables_ptrs(P, c);
+  hydro_status r = launch_force(c->d.dim, c->d.order_h1, hk::MODE_FORCE, visc.enabled != 0, P, s);
+  if (r != HYDRO_OK) return r;
+  return launch_assemble(c->d.dim, p->n_s0_nodes, p->B, p->off, p->evec, F1_rows, p->st, dt, s);
+}
+
+hydro_status hydro_sample_status_sync(hydro_sample *p, hydro_stream_t stream,
+                                      int64_t *first_bad_elem) {
+  if (!p) return HYDRO_ERR_ARG;
+  return status_sync_impl(p->st, p->B, (cudaStream_t)stream, first_bad_elem);
+}
+
+hydro_status hydro_rom_lift(int64_t rows, int n, int B, const double *Phi, const double *os,
+                            int os_batched, const double *Y, double *out, hydro_stream_t stream) {
+  if (rows < 0 || n <= 0 || n > 256 || B <= 0 || !Phi || !os || !Y || !out) return HYDRO_ERR_ARG;
+  if (rows == 0) return HYDRO_OK;
+  const size_t smem = sizeof(double) * (size_t)(n * hk::LIFT_CB + hk::LIFT_RT * (n + 1));
+  static size_t smem_set = 0;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    CUDA_OK(cudaFuncSetAttribute(hk::lift_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set = smem;
+  }
+  dim3 grid((unsigned)((rows + hk::LIFT_RT - 1) / hk::LIFT_RT), (unsigned)((B + hk::LIFT_CB - 1) / hk::LIFT_CB));
+  hk::lift_kernel<<<grid, hk::LIFT_THREADS, smem, (cudaStream_t)stream>>>(rows, n, B, Phi, os, os_batched, Y, out);
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
+static int project_groups(int64_t s_rows) {
+  int64_t g = (s_rows + 255) / 256;  // >= 256 rows per group
+  if (g > 148 * 8) g = 148 * 8;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+size_t hydro_rom_project_workspace_bytes(int n, int64_t s_rows, int B) {
+  if (n <= 0 || B <= 0 || s_rows < 0) return 0;
+  return sizeof(double) * (size_t)project_groups(s_rows) * n * B;
+}
+
+hydro_status hydro_rom_project(int n, int64_t s_rows, int B, const double *P, const double *f,
+                               double *r, void *workspace, size_t ws_bytes, hydro_stream_t stream) {
+  if (n <= 0 || n > hk::PROJ_MAXN || B <= 0 || B > hk::PROJ_MAXB || s_rows < 0 || !P || !f || !r)
+    return HYDRO_ERR_ARG;
+  const int G = project_groups(s_rows);
+  if (!workspace || ws_bytes < sizeof(double) * (size_t)G * n * B) return HYDRO_ERR_WORKSPACE;
+  const int64_t chunk = (s_rows + G - 1) / G;
+  cudaStream_t s = (cudaStream_t)stream;
+  hk::project_partial_kernel<<<G, hk::PROJ_THREADS, 0, s>>>(n, s_rows, B, chunk > 0 ? chunk : 1, P, f,
+                                                             (double *)workspace);
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  hk::project_reduce_kernel<<<(n * B + 255) / 256, 256, 0, s>>>(n, B, G, (const double *)workspace, r);
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
+}  // extern "C"

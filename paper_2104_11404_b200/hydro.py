@@ -1,0 +1,316 @@
+"""Thin ctypes binding of include/hydro.h (argument marshalling only).
+
+Every step of the hot path runs in libhydro.so's CUDA kernels; this module only
+passes torch tensors' device pointers and the current CUDA stream.  There is no
+CPU fallback: if the library is missing or no CUDA device is present, calls
+raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhydro.so")
+
+HYDRO_OK, HYDRO_ERR_ARG, HYDRO_ERR_UNSUPPORTED, HYDRO_ERR_CUDA = 0, 1, 2, 3
+HYDRO_ERR_TANGLED, HYDRO_ERR_NONFINITE, HYDRO_ERR_WORKSPACE = 4, 5, 6
+STATUS_NAMES = {0: "OK", 1: "ERR_ARG", 2: "ERR_UNSUPPORTED", 3: "ERR_CUDA", 4: "ERR_TANGLED",
+                5: "ERR_NONFINITE", 6: "ERR_WORKSPACE"}
+
+EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy",
+            "hydro_force_full", "hydro_dt_estimate", "hydro_status_sync", "hydro_sample_create",
+            "hydro_sample_destroy", "hydro_sample_info", "hydro_sample_lists", "hydro_rom_lift",
+            "hydro_force_sampled", "hydro_sample_status_sync", "hydro_rom_project_workspace_bytes",
+            "hydro_rom_project", "hydro_basis_tables", "hydro_launch_count", "hydro_version",
+            "hydro_profile_enable", "hydro_profile_read"]
+
+
+class HydroError(RuntimeError):
+    def __init__(self, code: int, what: str, first_bad: int = -1):
+        super().__init__(f"{what}: {STATUS_NAMES.get(code, code)}"
+                         + (f" (first tangled element {first_bad})" if first_bad >= 0 else ""))
+        self.code = code
+        self.first_bad = first_bad
+
+
+class _MeshDesc(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int), ("order_h1", ctypes.c_int), ("nq1d", ctypes.c_int),
+                ("n_elem", ctypes.c_int64), ("n_nodes", ctypes.c_int64),
+                ("elem_nodes", ctypes.c_void_p), ("x0", ctypes.c_void_p), ("rho0", ctypes.c_void_p)]
+
+
+class _Visc(ctypes.Structure):
+    _fields_ = [("q1", ctypes.c_double), ("q2", ctypes.c_double), ("enabled", ctypes.c_int)]
+
+
+class _Cfl(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_double), ("alpha_mu", ctypes.c_double)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libhydro.so (built in-tree by paper_2104_11404_b200.build). Raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2104_11404_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        L.hydro_ctx_workspace_bytes.restype = ctypes.c_size_t
+        L.hydro_ctx_workspace_bytes.argtypes = [ctypes.POINTER(_MeshDesc)]
+        L.hydro_ctx_create.argtypes = [ctypes.POINTER(_MeshDesc), vp, ctypes.c_size_t, vp,
+                                       ctypes.POINTER(vp)]
+        L.hydro_ctx_destroy.argtypes = [vp]
+        L.hydro_force_full.argtypes = [vp, vp, vp, vp, vp, vp, _Visc, _Cfl, vp, vp, vp, vp]
+        L.hydro_dt_estimate.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, vp, vp]
+        L.hydro_status_sync.argtypes = [vp, vp, ctypes.POINTER(i64)]
+        L.hydro_sample_create.argtypes = [vp, vp, i64, i32, ctypes.POINTER(vp)]
+        L.hydro_sample_destroy.argtypes = [vp]
+        L.hydro_sample_info.argtypes = [vp] + [ctypes.POINTER(i64)] * 5
+        L.hydro_sample_lists.argtypes = [vp, vp, vp, vp]
+        L.hydro_rom_lift.argtypes = [i64, i32, i32, vp, vp, i32, vp, vp, vp]
+        L.hydro_force_sampled.argtypes = [vp, vp, vp, vp, vp, vp, _Visc, _Cfl, vp, vp, vp, vp]
+        L.hydro_sample_status_sync.argtypes = [vp, vp, ctypes.POINTER(i64)]
+        L.hydro_rom_project_workspace_bytes.restype = ctypes.c_size_t
+        L.hydro_rom_project_workspace_bytes.argtypes = [i32, i64, i32]
+        L.hydro_rom_project.argtypes = [i32, i64, i32, vp, vp, vp, vp, ctypes.c_size_t, vp]
+        L.hydro_basis_tables.argtypes = [i32, i32, vp, vp, vp, vp, vp]
+        L.hydro_launch_count.restype = i64
+        L.hydro_profile_enable.argtypes = [i32]
+        L.hydro_profile_read.argtypes = [ctypes.POINTER(dbl), ctypes.POINTER(i64)]
+        L.hydro_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("hydro: tensors must live on the CUDA device")
+    if t.dtype not in (torch.float64, torch.int32, torch.uint8):
+        raise ValueError(f"hydro: unexpected dtype {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError("hydro: tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream: Optional[torch.cuda.Stream] = None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check(rc: int, what: str):
+    if rc != HYDRO_OK:
+        raise HydroError(rc, what)
+
+
+@dataclass
+class Visc:
+    q1: float = 0.5
+    q2: float = 2.0
+    enabled: bool = True
+
+    def c(self):
+        return _Visc(self.q1, self.q2, 1 if self.enabled else 0)
+
+
+@dataclass
+class Cfl:
+    alpha: float = 0.5
+    alpha_mu: float = 2.5
+
+    def c(self):
+        return _Cfl(self.alpha, self.alpha_mu)
+
+
+def basis_tables(k: int, q: int) -> dict:
+    """The library's own correctly rounded tables (host computation)."""
+    import numpy as np
+    xi, w = np.zeros(q), np.zeros(q)
+    B, G, Bl = np.zeros((q, k + 1)), np.zeros((q, k + 1)), np.zeros((q, k))
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    _check(lib().hydro_basis_tables(k, q, p(xi), p(w), p(B), p(G), p(Bl)), "hydro_basis_tables")
+    return dict(xi=xi, w=w, B=B, G=G, Bl=Bl)
+
+
+def launch_count() -> int:
+    return int(lib().hydro_launch_count())
+
+
+def profile_enable(on: bool = True) -> None:
+    _check(lib().hydro_profile_enable(1 if on else 0), "hydro_profile_enable")
+
+
+def profile_read():
+    """(summed force-kernel ms, launches) since the last read; synchronises."""
+    ms, n = ctypes.c_double(0.0), ctypes.c_int64(0)
+    _check(lib().hydro_profile_read(ctypes.byref(ms), ctypes.byref(n)), "hydro_profile_read")
+    return ms.value, n.value
+
+
+class HydroContext:
+    """Mesh context (hydro_ctx_create): m_q, assembly slots, dt status in a torch workspace."""
+
+    def __init__(self, dim: int, k: int, nq: int, elem_nodes: torch.Tensor, x0: torch.Tensor,
+                 rho0: torch.Tensor, stream: Optional[torch.cuda.Stream] = None):
+        L = lib()
+        self.dim, self.k, self.nq = dim, k, nq
+        self.elem_nodes = elem_nodes.to(torch.int32).contiguous()
+        self.x0 = x0.to(torch.float64).contiguous()
+        self.rho0 = rho0.to(torch.float64).contiguous()
+        self.n_elem = int(self.elem_nodes.shape[0])
+        self.n_nodes = int(self.x0.shape[1])
+        self._desc = _MeshDesc(dim, k, nq, self.n_elem, self.n_nodes, _ptr(self.elem_nodes),
+                               _ptr(self.x0), _ptr(self.rho0))
+        nbytes = L.hydro_ctx_workspace_bytes(ctypes.byref(self._desc))
+        if nbytes == 0:
+            raise HydroError(HYDRO_ERR_ARG, "hydro_ctx_workspace_bytes")
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.x0.device)
+        base = self.workspace.data_ptr()
+        aligned = (base + 255) & ~255
+        self._ws_ptr = ctypes.c_void_p(aligned)
+        self._ws_bytes = nbytes
+        h = ctypes.c_void_p()
+        _check(L.hydro_ctx_create(ctypes.byref(self._desc), self._ws_ptr, nbytes, _stream(stream),
+                                  ctypes.byref(h)), "hydro_ctx_create")
+        self._h = h
+        self.ne = k ** dim
+        self.nd = (k + 1) ** dim
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) and self._h.value:
+                lib().hydro_ctx_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def mq(self) -> torch.Tensor:
+        """View of the per-quadrature-point mass m_q inside the workspace ([E][nq^dim])."""
+        nq = self.nq ** self.dim
+        off = 256 * ((8 * 128 + 255) // 256) + 256 * ((32 + 255) // 256)
+        start = self._ws_ptr.value - self.workspace.data_ptr() + off
+        return self.workspace[start:start + 8 * self.n_elem * nq].view(torch.float64).view(self.n_elem, nq)
+
+    def force_full(self, x, v, e, gamma, visc: Visc, cfl: Cfl, w=None, F1=None, FTw=None,
+                   dt=None, stream=None):
+        if F1 is None:
+            F1 = torch.empty((self.dim, self.n_nodes), dtype=torch.float64, device=x.device)
+        if FTw is None:
+            FTw = torch.empty((self.n_elem, self.ne), dtype=torch.float64, device=x.device)
+        if dt is None:
+            dt = torch.empty(1, dtype=torch.float64, device=x.device)
+        _check(lib().hydro_force_full(self._h, _ptr(x), _ptr(v), _ptr(e), _ptr(w), _ptr(gamma),
+                                      visc.c(), cfl.c(), _ptr(F1), _ptr(FTw), _ptr(dt),
+                                      _stream(stream)), "hydro_force_full")
+        return F1, FTw, dt
+
+    def dt_estimate(self, x, v, e, gamma, visc: Visc, cfl: Cfl, dt=None, stream=None):
+        if dt is None:
+            dt = torch.empty(1, dtype=torch.float64, device=x.device)
+        _check(lib().hydro_dt_estimate(self._h, _ptr(x), _ptr(v), _ptr(e), _ptr(gamma), visc.c(),
+                                       cfl.c(), _ptr(dt), _stream(stream)), "hydro_dt_estimate")
+        return dt
+
+    def status_sync(self, stream=None):
+        """Returns (status_code, first_bad_element) and clears the sticky status."""
+        fb = ctypes.c_int64(-1)
+        rc = lib().hydro_status_sync(self._h, _stream(stream), ctypes.byref(fb))
+        if rc in (HYDRO_ERR_ARG, HYDRO_ERR_CUDA):
+            raise HydroError(rc, "hydro_status_sync")
+        return rc, fb.value
+
+
+class SamplePlan:
+    """hydro_sample_create: closure of a sample element set, batched over B instances."""
+
+    def __init__(self, ctx: HydroContext, sample_elems, B: int):
+        import numpy as np
+        L = lib()
+        s = np.ascontiguousarray(np.asarray(sample_elems, dtype=np.int32))
+        h = ctypes.c_void_p()
+        _check(L.hydro_sample_create(ctx.handle, s.ctypes.data_as(ctypes.c_void_p), s.size, B,
+                                     ctypes.byref(h)), "hydro_sample_create")
+        self._h, self.ctx, self.B = h, ctx, B
+        v = [ctypes.c_int64() for _ in range(5)]
+        _check(L.hydro_sample_info(h, *[ctypes.byref(t) for t in v]), "hydro_sample_info")
+        self.n_cl, self.n_cl_nodes, self.n_s0_nodes, self.s_v, self.s_e = [t.value for t in v]
+        self.closure_elems = np.zeros(self.n_cl, dtype=np.int32)
+        self.closure_nodes = np.zeros(self.n_cl_nodes, dtype=np.int64)
+        self.s0_nodes = np.zeros(self.n_s0_nodes, dtype=np.int64)
+        _check(L.hydro_sample_lists(h, self.closure_elems.ctypes.data_as(ctypes.c_void_p),
+                                    self.closure_nodes.ctypes.data_as(ctypes.c_void_p),
+                                    self.s0_nodes.ctypes.data_as(ctypes.c_void_p)), "hydro_sample_lists")
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) and self._h.value:
+                lib().hydro_sample_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def force_sampled(self, x_S, v_S, e_S, gamma, visc: Visc, cfl: Cfl, w_S=None, F1_rows=None,
+                      FTw_rows=None, dt=None, stream=None):
+        dev = x_S.device
+        if F1_rows is None:
+            F1_rows = torch.empty((self.s_v, self.B), dtype=torch.float64, device=dev)
+        if FTw_rows is None:
+            FTw_rows = torch.empty((self.s_e, self.B), dtype=torch.float64, device=dev)
+        if dt is None:
+            dt = torch.empty(self.B, dtype=torch.float64, device=dev)
+        _check(lib().hydro_force_sampled(self._h, _ptr(x_S), _ptr(v_S), _ptr(e_S), _ptr(w_S),
+                                         _ptr(gamma), visc.c(), cfl.c(), _ptr(F1_rows),
+                                         _ptr(FTw_rows), _ptr(dt), _stream(stream)),
+               "hydro_force_sampled")
+        return F1_rows, FTw_rows, dt
+
+    def status_sync(self, stream=None):
+        fb = ctypes.c_int64(-1)
+        rc = lib().hydro_sample_status_sync(self._h, _stream(stream), ctypes.byref(fb))
+        if rc in (HYDRO_ERR_ARG, HYDRO_ERR_CUDA):
+            raise HydroError(rc, "hydro_sample_status_sync")
+        return rc, fb.value
+
+
+def rom_lift(Phi: torch.Tensor, os_: torch.Tensor, Y: torch.Tensor, out: Optional[torch.Tensor] = None,
+             stream=None) -> torch.Tensor:
+    """out[r][b] = os[r] (1-D) or os[r][b] (2-D) + sum_k Phi[r][k] Y[k][b]."""
+    rows, n = Phi.shape
+    B = Y.shape[1]
+    if out is None:
+        out = torch.empty((rows, B), dtype=torch.float64, device=Phi.device)
+    _check(lib().hydro_rom_lift(rows, n, B, _ptr(Phi), _ptr(os_), 1 if os_.dim() == 2 else 0,
+                                _ptr(Y), _ptr(out), _stream(stream)), "hydro_rom_lift")
+    return out
+
+
+def rom_project_workspace(n: int, s_rows: int, B: int, device="cuda") -> torch.Tensor:
+    nb = lib().hydro_rom_project_workspace_bytes(n, s_rows, B)
+    return torch.empty(max(nb, 8), dtype=torch.uint8, device=device)
+
+
+def rom_project(P: torch.Tensor, f: torch.Tensor, out: Optional[torch.Tensor] = None,
+                workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """r[i][b] = sum_s P[i][s] f[s][b] (deterministic split-K)."""
+    n, s_rows = P.shape
+    B = f.shape[1]
+    if out is None:
+        out = torch.empty((n, B), dtype=torch.float64, device=P.device)
+    if workspace is None:
+        workspace = rom_project_workspace(n, s_rows, B, P.device)
+    _check(lib().hydro_rom_project(n, s_rows, B, _ptr(P), _ptr(f), _ptr(out), _ptr(workspace),
+                                   workspace.numel(), _stream(stream)), "hydro_rom_project")
+    return out
