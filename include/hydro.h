@@ -177,6 +177,18 @@ int64_t hydro_launch_count(void);
 /* Library version string.                                                                  */
 const char *hydro_version(void);
 
+/* ------------------------------------------------------------------ self-test (device) */
+/* Checks the branch-free FP64 division / reciprocal / square-root fast paths the force
+ * kernel's pointwise stage uses (csrc/ieee_fast.cuh; DESIGN "Kernels") against the IEEE
+ * round-to-nearest operators on n seeded operands generated on the device (SplitMix64
+ * counter stream of `seed`).  op: 0 = a/b, 1 = 1/b, 2 = sqrt.  dist: 0 = exponents in
+ * [-64, 64], 1 = raw 64-bit patterns (NaN, inf, subnormals, extremes).  Atomically ADDS
+ * to counts (device, 3 x uint64, caller zeroes them): [0] fast-path-valid results whose
+ * bits differ from IEEE (the contract requires 0), [1] operands outside the fast range
+ * (re-evaluated exactly by the caller), [2] operands tested.  Asynchronous on `stream`. */
+hydro_status hydro_selftest_ieee_fast(uint64_t seed, int64_t n, int op, int dist,
+                                      unsigned long long *counts, hydro_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,9 +8,14 @@
 //                each output an FMA chain in the canonical order of DESIGN A.2;
 //   S3 pointwise detJ, J^-1, rho = m_q/detJ, p, cs, h, grad v, eps, lambda_min, mu,
 //                sigma, dt_q -- the exact IEEE sequence of DESIGN A.3/A.4 (this file
-//                is compiled with -fmad=false; every FMA is written as __fma_rn);
-//   S4 backward  S_q = w_q detJ sigma J^-T, then sum-factorised transposes:
-//                F1_K[a][c] = sum_q (S_q gradhat phi_a)_c, FTw_K[j] = sum_q psi_j (S_q : gradhat w);
+//                is compiled with -fmad=false; every FMA is written as __fma_rn).  The
+//                stage runs with the branch-free fast div/sqrt of ieee_fast.cuh (the
+//                two Jacobi eigen-solves of a 3D viscous point interleaved for ILP) and
+//                is re-run with the plain IEEE operators on the rare points where a
+//                fast path left its valid range -- bit-identical either way;
+//   S4 backward  S_q = w_q detJ sigma J^-T, A_q = w_q detJ sigma : grad w, then the
+//                sum-factorised transposes F1_K[a][c] = sum_q (S_q gradhat phi_a)_c,
+//                FTw_K[j] = sum_q psi_j A_q;
 //   S5 outputs   F1_K to its assembly slots (deterministic gather in assemble_kernel),
 //                FTw_K element-local;
 //   S6 dt        warp/CTA min of order-preserving keys, one atomicMin per CTA (exact).
@@ -22,21 +27,23 @@
 #include <stdint.h>
 
 #include "hydro_internal.h"
+#include "ieee_fast.cuh"
 
 namespace hk {
 
 enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2 };
 
-template <int DIM_, int K_, int Q_>
+// EPB_: units per CTA (0 = default: 8 for 16-point 2D elements, else 1).
+template <int DIM_, int K_, int Q_, int NF_, int EPB_ = 0>
 struct Geo {
   static constexpr int DIM = DIM_, K = K_, Q = Q_;
   static constexpr int N = K + 1, M = K;
   static constexpr int ND = DIM == 2 ? N * N : N * N * N;
   static constexpr int NE = DIM == 2 ? M * M : M * M * M;
   static constexpr int NQ = DIM == 2 ? Q * Q : Q * Q * Q;
-  static constexpr int EPB = NQ <= 16 ? 8 : (NQ <= 36 ? 4 : (NQ <= 64 ? 2 : 1));
+  static constexpr int EPB = EPB_ > 0 ? EPB_ : (NQ <= 16 ? 8 : 1);
   static constexpr int NT = ((EPB * NQ + 31) / 32) * 32;
-  static constexpr int NF = 3;  // fields x, v, w (w only when distinct)
+  static constexpr int NF = NF_;  // gathered H1 fields: x, v (, w)
   // per-unit shared-memory layout (doubles)
   static constexpr int S1 = DIM == 3 ? Q * N * N : Q * N;       // one stage-1 block
   static constexpr int S2 = DIM == 3 ? Q * Q * N : 0;           // one stage-2 block
@@ -52,12 +59,12 @@ struct Geo {
   static constexpr int UNIT = NF * DIM * ND + NE + WORK;
   static constexpr int TABD = Q + Q * N * 2 + Q * M;             // w, B, G, Bl
   static constexpr size_t SMEM =
-      sizeof(double) * (size_t)(TABD + EPB * UNIT) + sizeof(int) * EPB * ND +
+      sizeof(double) * (size_t)(TABD + EPB * UNIT) + sizeof(int) * ((EPB * ND + 1) / 2 * 2) +
       sizeof(unsigned long long) * EPB;
 };
 
 struct Params {
-  int64_t n_units;          // full: n_elem; batched: n_cl_elem * B
+  int32_t n_units;          // full: n_elem; batched: n_cl_elem * B
   int B;                    // instances (1 in full mode)
   int64_t ld_nodes;         // H1 component stride in nodes (n_nodes or n_cl_nodes)
   const int32_t *elem_nodes;  // [n_l][ND] node ids (closure-local in batched mode)
@@ -86,49 +93,100 @@ __device__ __forceinline__ double key_to_dt(unsigned long long k) {
   return __longlong_as_double((long long)b);
 }
 
-// One cyclic-Jacobi rotation of DESIGN A.4 on pair (p,q) with r3 = the third index.
-__device__ __forceinline__ void jacobi_rot(double &app, double &aqq, double &apq, double &arp,
-                                           double &arq, const double tol) {
-  if (fabs(apq) <= tol) return;
-  const double dlt = 0.5 * (aqq - app);
-  const double rr = sqrt(dlt * dlt + apq * apq);
-  double t = apq / (fabs(dlt) + rr);
-  if (dlt < 0.0) t = -t;
-  const double c = 1.0 / sqrt(1.0 + t * t);
+// One cyclic-Jacobi rotation of DESIGN A.4 on pair (p,q) with r3 = the third index,
+// skipped when |a_pq| <= tol.  Written without branches (the skipped case computes on
+// harmless stand-in values and keeps the old entries) so that two independent matrices'
+// rotations can be interleaved by the scheduler.  The rotated entries are exactly the
+// contract's: dlt = 0.5(a_qq - a_pp), r = sqrt(dlt^2 + a_pq^2), t = a_pq/(|dlt| + r)
+// (negated if dlt < 0), c = 1/sqrt(1 + t^2), s = t c.
+template <class AR>
+__device__ __forceinline__ void jacobi_rot(AR &ar, double &app, double &aqq, double &apq,
+                                           double &arp, double &arq, const double tol) {
+  const bool go = !(fabs(apq) <= tol);
+  const double a_ = go ? apq : 1.0;
+  const double dl = go ? 0.5 * (aqq - app) : 0.0;
+  const double rr = ar.sqrt_(dl * dl + a_ * a_);
+  double t = ar.div(a_, fabs(dl) + rr);
+  t = dl < 0.0 ? -t : t;
+  const double c = ar.rcp(ar.sqrt_(1.0 + t * t));
   const double s = t * c;
   const double rp = arp, rq = arq;
-  app = app - t * apq;
-  aqq = aqq + t * apq;
-  apq = 0.0;
-  arp = c * rp - s * rq;
-  arq = s * rp + c * rq;
+  const double napp = app - t * apq;
+  const double naqq = aqq + t * apq;
+  const double narp = c * rp - s * rq;
+  const double narq = s * rp + c * rq;
+  app = go ? napp : app;
+  aqq = go ? naqq : aqq;
+  apq = go ? 0.0 : apq;
+  arp = go ? narp : arp;
+  arq = go ? narq : arq;
 }
 
-// Smallest eigenvalue of the symmetric [[a00 a01 a02][. a11 a12][. . a22]] (DESIGN A.4).
-__device__ __forceinline__ double lmin3(double a00, double a11, double a22, double a01,
-                                        double a02, double a12) {
+__device__ __forceinline__ double amax6(double a00, double a11, double a22, double a01, double a02,
+                                        double a12) {
   double amax = fabs(a00);
   amax = fmax(amax, fabs(a11));
   amax = fmax(amax, fabs(a22));
   amax = fmax(amax, fabs(a01));
   amax = fmax(amax, fabs(a02));
   amax = fmax(amax, fabs(a12));
-  const double tol = amax * 0x1p-53;
+  return amax;
+}
+
+__device__ __forceinline__ bool offdiag_live(double a01, double a02, double a12, double tol) {
+  return !(fabs(a01) <= tol) || !(fabs(a02) <= tol) || !(fabs(a12) <= tol);
+}
+
+// Smallest eigenvalues of two symmetric 3x3 matrices (DESIGN A.4), their rotations
+// interleaved.  EARLY: the warp leaves the sweep loop once no lane has a live
+// off-diagonal in either matrix (every remaining rotation would be a skip) -- needs all
+// 32 lanes converged, so only the fast (non-divergent) pass uses it.
+template <class AR, bool EARLY>
+__device__ __forceinline__ void lmin3_pair(AR &ar, double a00, double a11, double a22,
+                                           double a01, double a02, double a12, double e00,
+                                           double e11, double e22, double e01, double e02,
+                                           double e12, double &la, double &le) {
+  const double ta = amax6(a00, a11, a22, a01, a02, a12) * 0x1p-53;
+  const double te = amax6(e00, e11, e22, e01, e02, e12) * 0x1p-53;
 #pragma unroll 1
   for (int sweep = 0; sweep < 4; ++sweep) {
-    jacobi_rot(a00, a11, a01, a02, a12, tol);  // (0,1), r3 = 2
-    jacobi_rot(a00, a22, a02, a01, a12, tol);  // (0,2), r3 = 1
-    jacobi_rot(a11, a22, a12, a01, a02, tol);  // (1,2), r3 = 0
+    if (EARLY) {
+      const bool live = offdiag_live(a01, a02, a12, ta) || offdiag_live(e01, e02, e12, te);
+      if (!__any_sync(0xffffffffu, live)) break;
+    }
+    jacobi_rot(ar, a00, a11, a01, a02, a12, ta);  // (0,1), r3 = 2
+    jacobi_rot(ar, e00, e11, e01, e02, e12, te);
+    jacobi_rot(ar, a00, a22, a02, a01, a12, ta);  // (0,2), r3 = 1
+    jacobi_rot(ar, e00, e22, e02, e01, e12, te);
+    jacobi_rot(ar, a11, a22, a12, a01, a02, ta);  // (1,2), r3 = 0
+    jacobi_rot(ar, e11, e22, e12, e01, e02, te);
+  }
+  la = fmin(fmin(a00, a11), a22);
+  le = fmin(fmin(e00, e11), e22);
+}
+
+template <class AR, bool EARLY>
+__device__ __forceinline__ double lmin3(AR &ar, double a00, double a11, double a22, double a01,
+                                        double a02, double a12) {
+  const double ta = amax6(a00, a11, a22, a01, a02, a12) * 0x1p-53;
+#pragma unroll 1
+  for (int sweep = 0; sweep < 4; ++sweep) {
+    if (EARLY) {
+      if (!__any_sync(0xffffffffu, offdiag_live(a01, a02, a12, ta))) break;
+    }
+    jacobi_rot(ar, a00, a11, a01, a02, a12, ta);
+    jacobi_rot(ar, a00, a22, a02, a01, a12, ta);
+    jacobi_rot(ar, a11, a22, a12, a01, a02, ta);
   }
   return fmin(fmin(a00, a11), a22);
 }
 
-// Contract determinant / inverse (DESIGN A.3).
-template <int DIM>
-__device__ __forceinline__ double det_inv(const double (&J)[3][3], double (&Ji)[3][3]) {
+// Determinant / inverse by cofactors (DESIGN A.3).
+template <int DIM, class AR>
+__device__ __forceinline__ double det_inv(AR &ar, const double (&J)[3][3], double (&Ji)[3][3]) {
   if (DIM == 2) {
     const double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
-    const double inv = 1.0 / det;
+    const double inv = ar.rcp(det);
     Ji[0][0] = J[1][1] * inv;
     Ji[0][1] = -(J[0][1] * inv);
     Ji[1][0] = -(J[1][0] * inv);
@@ -145,7 +203,7 @@ __device__ __forceinline__ double det_inv(const double (&J)[3][3], double (&Ji)[
     const double C21 = J[0][2] * J[1][0] - J[0][0] * J[1][2];
     const double C22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
     const double det = (J[0][0] * C00 + J[0][1] * C01) + J[0][2] * C02;
-    const double inv = 1.0 / det;
+    const double inv = ar.rcp(det);
     Ji[0][0] = C00 * inv; Ji[0][1] = C10 * inv; Ji[0][2] = C20 * inv;
     Ji[1][0] = C01 * inv; Ji[1][1] = C11 * inv; Ji[1][2] = C21 * inv;
     Ji[2][0] = C02 * inv; Ji[2][1] = C12 * inv; Ji[2][2] = C22 * inv;
@@ -155,30 +213,66 @@ __device__ __forceinline__ double det_inv(const double (&J)[3][3], double (&Ji)[
 
 template <int DIM>
 __device__ __forceinline__ double det_only(const double (&J)[3][3]) {
-  double Ji[3][3];
-  return det_inv<DIM>(J, Ji);
+  if (DIM == 2) return J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  const double C00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+  const double C01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+  const double C02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  return (J[0][0] * C00 + J[0][1] * C01) + J[0][2] * C02;
 }
 
-// Pointwise stage (DESIGN A.3). Returns dt_q; fills sigma (DIM x DIM), Ji, det.
-template <int DIM, bool VISC>
-__device__ __forceinline__ double pointwise(const double (&J)[3][3], const double (&Gv)[3][3],
-                                            double eq, double mq, double gam, double q1,
-                                            double q2, double alpha, double alpha_mu,
-                                            double (&sig)[3][3], double (&Ji)[3][3],
-                                            double &det_out) {
-  const double det = det_inv<DIM>(J, Ji);
-  det_out = det;
-  const double rho = mq / det;
+struct PhysIn {
+  double q1, q2, alpha, alpha_mu;
+};
+
+struct PointOut {
+  double S[3][3];  // w_q detJ sigma J^-T (DIM x DIM)
+  double A;        // w_q detJ sigma : grad w
+  double det, dtq;
+};
+
+// Pointwise stage (DESIGN A.3/A.4) through arithmetic policy AR; everything dt_q depends
+// on follows the contract exactly.  Gw: gradhat of the field F^T is applied to (== Gv
+// when w is v).  S and A are tolerance-only (A.5).
+template <int DIM, bool VISC, bool HAS_W, bool EARLY, class AR>
+__device__ __forceinline__ void pointwise(AR &ar, const double (&J)[3][3], const double (&Gv)[3][3],
+                                          const double (&Gw)[3][3], double eq, double mq,
+                                          double gam, double wq, const PhysIn &ph, PointOut &o) {
+  double Ji[3][3];
+  const double det = det_inv<DIM>(ar, J, Ji);
+  const double rho = ar.div(mq, det);
   const double p = ((gam - 1.0) * rho) * eq;
-  const double cs = sqrt((gam * (gam - 1.0)) * eq);
-  double h;
+  const double cs = ar.sqrt_((gam * (gam - 1.0)) * eq);
+  // physical velocity gradient (contract order: ascending i, plain mul/add)
+  double gv[3][3];
+#pragma unroll
+  for (int c = 0; c < DIM; ++c)
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      double s = Gv[c][0] * Ji[0][d];
+#pragma unroll
+      for (int i = 1; i < DIM; ++i) s = s + Gv[c][i] * Ji[i][d];
+      gv[c][d] = s;
+    }
+  double eps[3][3];
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) {
+    eps[c][c] = gv[c][c];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d)
+      if (d != c) eps[c][d] = 0.5 * (gv[c][d] + gv[d][c]);
+  }
+  double h, lam = 0.0;
   if (DIM == 2) {
     const double c00 = J[0][0] * J[0][0] + J[1][0] * J[1][0];
     const double c11 = J[0][1] * J[0][1] + J[1][1] * J[1][1];
     const double c01 = J[0][0] * J[0][1] + J[1][0] * J[1][1];
     const double kk = 0.5 * (c00 - c11);
-    const double smax2 = 0.5 * (c00 + c11) + sqrt(kk * kk + c01 * c01);
-    h = det / sqrt(smax2);
+    const double smax2 = 0.5 * (c00 + c11) + ar.sqrt_(kk * kk + c01 * c01);
+    h = ar.div(det, ar.sqrt_(smax2));
+    if (VISC) {
+      const double k = 0.5 * (eps[0][0] - eps[1][1]);
+      lam = 0.5 * (eps[0][0] + eps[1][1]) - ar.sqrt_(k * k + eps[0][1] * eps[0][1]);
+    }
   } else {
     const double c00 = (J[0][0] * J[0][0] + J[1][0] * J[1][0]) + J[2][0] * J[2][0];
     const double c11 = (J[0][1] * J[0][1] + J[1][1] * J[1][1]) + J[2][1] * J[2][1];
@@ -186,57 +280,155 @@ __device__ __forceinline__ double pointwise(const double (&J)[3][3], const doubl
     const double c01 = (J[0][0] * J[0][1] + J[1][0] * J[1][1]) + J[2][0] * J[2][1];
     const double c02 = (J[0][0] * J[0][2] + J[1][0] * J[1][2]) + J[2][0] * J[2][2];
     const double c12 = (J[0][1] * J[0][2] + J[1][1] * J[1][2]) + J[2][1] * J[2][2];
-    h = sqrt(fmax(lmin3(c00, c11, c22, c01, c02, c12), 0.0));
-  }
-  double mu = 0.0;
-  double eps[3][3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int d = 0; d < 3; ++d) eps[c][d] = 0.0;
-  if (VISC) {
-    double gv[3][3];
-#pragma unroll
-    for (int c = 0; c < DIM; ++c)
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        double s = Gv[c][0] * Ji[0][d];
-#pragma unroll
-        for (int i = 1; i < DIM; ++i) s = s + Gv[c][i] * Ji[i][d];
-        gv[c][d] = s;
-      }
-#pragma unroll
-    for (int c = 0; c < DIM; ++c) {
-      eps[c][c] = gv[c][c];
-#pragma unroll
-      for (int d = 0; d < DIM; ++d)
-        if (d != c) eps[c][d] = 0.5 * (gv[c][d] + gv[d][c]);
-    }
-    double lam;
-    if (DIM == 2) {
-      const double k = 0.5 * (eps[0][0] - eps[1][1]);
-      lam = 0.5 * (eps[0][0] + eps[1][1]) - sqrt(k * k + eps[0][1] * eps[0][1]);
+    double lj;
+    if (VISC) {
+      lmin3_pair<AR, EARLY>(ar, c00, c11, c22, c01, c02, c12, eps[0][0], eps[1][1], eps[2][2],
+                            eps[0][1], eps[0][2], eps[1][2], lj, lam);
     } else {
-      lam = lmin3(eps[0][0], eps[1][1], eps[2][2], eps[0][1], eps[0][2], eps[1][2]);
+      lj = lmin3<AR, EARLY>(ar, c00, c11, c22, c01, c02, c12);
     }
-    const double lneg = fmin(lam, 0.0);
-    mu = (rho * h) * ((q1 * cs) + ((q2 * h) * (-lneg)));
+    h = ar.sqrt_(fmax(lj, 0.0));
   }
+  double mu = 0.0, visc_term;
   const double den = (rho * h) * h;
-  const double inv_dt = cs / h + (alpha_mu * mu) / den;
-  const double dtq = alpha / inv_dt;
+  if (VISC) {
+    const double lneg = fmin(lam, 0.0);
+    mu = (rho * h) * ((ph.q1 * cs) + ((ph.q2 * h) * (-lneg)));
+    visc_term = ar.div(ph.alpha_mu * mu, den);
+  } else {
+    // (alpha_mu * 0) / den with IEEE semantics, no division: +-0 (sign xor) unless den is
+    // 0 or NaN (then NaN); a NaN numerator (alpha_mu infinite) stays NaN.
+    const double num = ph.alpha_mu * mu;
+    const bool nanres = (num != num) || (den == 0.0) || (den != den);
+    const double z = (signbit(num) != signbit(den)) ? -0.0 : 0.0;
+    visc_term = nanres ? __longlong_as_double(0x7ff8000000000000ll) : z;
+  }
+  const double inv_dt = ar.div(cs, h) + visc_term;
+  o.dtq = ar.div(ph.alpha, inv_dt);
+  o.det = det;
+  // sigma = -p I + mu eps;  S = w_q detJ sigma J^-T;  A = w_q detJ sigma : grad w
+  double sig[3][3];
 #pragma unroll
   for (int c = 0; c < DIM; ++c)
 #pragma unroll
-    for (int d = 0; d < DIM; ++d) sig[c][d] = mu * eps[c][d] - (c == d ? p : 0.0);
-  return dtq;
+    for (int d = 0; d < DIM; ++d) sig[c][d] = (VISC ? mu * eps[c][d] : 0.0) - (c == d ? p : 0.0);
+  const double wd = wq * det;
+  double A = 0.0;
+#pragma unroll
+  for (int c = 0; c < DIM; ++c)
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      double s = sig[c][0] * Ji[d][0];
+#pragma unroll
+      for (int i = 1; i < DIM; ++i) s = __fma_rn(sig[c][i], Ji[d][i], s);
+      o.S[c][d] = wd * s;
+      double g;
+      if (HAS_W) {
+        g = Gw[c][0] * Ji[0][d];
+#pragma unroll
+        for (int i = 1; i < DIM; ++i) g = __fma_rn(Gw[c][i], Ji[i][d], g);
+      } else {
+        g = eps[c][d];  // sigma symmetric: sigma : grad v = sigma : eps
+      }
+      A = __fma_rn(sig[c][d], g, A);
+    }
+  o.A = wd * A;
+}
+
+// Last forward stage for one Gauss point (DESIGN A.2, canonical order): 3D contracts a3
+// from the stage-2 blocks, 2D contracts a2 from the stage-1 blocks; e_q likewise.  Reads
+// shared memory only, so the exact IEEE re-run of S3 can recompute its inputs instead of
+// keeping them live in registers through the fast pass.
+template <int DIM, int K, int Q, int NF, bool WANT_E>
+__device__ __forceinline__ void forward_point(const double *sB, const double *sG,
+                                              const double *sBl, const double *Wk, int q1i,
+                                              int q2i, int q3i, double (&J)[3][3],
+                                              double (&Gv)[3][3], double (&Gw)[3][3],
+                                              double &eq) {
+  using G = Geo<DIM, K, Q, NF>;
+  constexpr int N = G::N, M = G::M;
+  if (DIM == 3) {
+    const double *S2b = Wk + G::NF * DIM * 2 * G::S1;    // [NF*DIM][3][Q][Q][N]
+    const double *E2b = S2b + G::NF * DIM * 3 * G::S2 + G::E1;  // [Q][Q][M]
+    double tB[N], tG[N];
+#pragma unroll
+    for (int a3 = 0; a3 < N; ++a3) { tB[a3] = sB[q3i * N + a3]; tG[a3] = sG[q3i * N + a3]; }
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) {
+        const int fc = f * DIM + c;
+        const double *p1 = S2b + ((fc * 3 + 0) * Q + q1i) * Q * N + q2i * N;
+        const double *p2 = S2b + ((fc * 3 + 1) * Q + q1i) * Q * N + q2i * N;
+        const double *p3 = S2b + ((fc * 3 + 2) * Q + q1i) * Q * N + q2i * N;
+        double d0 = tB[0] * p1[0], d1 = tB[0] * p2[0], d2 = tG[0] * p3[0];
+#pragma unroll
+        for (int a3 = 1; a3 < N; ++a3) {
+          d0 = __fma_rn(tB[a3], p1[a3], d0);
+          d1 = __fma_rn(tB[a3], p2[a3], d1);
+          d2 = __fma_rn(tG[a3], p3[a3], d2);
+        }
+        double *dst = f == 0 ? J[c] : (f == 1 ? Gv[c] : Gw[c]);
+        dst[0] = d0; dst[1] = d1; dst[2] = d2;
+      }
+    }
+    if (WANT_E) {
+      const double *tb = sBl + q3i * M;
+      const double *src = E2b + (q1i * Q + q2i) * M;
+      double acc = tb[0] * src[0];
+#pragma unroll
+      for (int j3 = 1; j3 < M; ++j3) acc = __fma_rn(tb[j3], src[j3], acc);
+      eq = acc;
+    }
+  } else {
+    const double *S1b = Wk;                              // [NF*DIM][2][Q][N]
+    const double *E1b = Wk + G::NF * DIM * 2 * G::S1;    // [Q][M]
+    double tB[N], tG[N];
+#pragma unroll
+    for (int a2 = 0; a2 < N; ++a2) { tB[a2] = sB[q2i * N + a2]; tG[a2] = sG[q2i * N + a2]; }
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) {
+        const int fc = f * DIM + c;
+        const double *uB = S1b + ((fc * 2 + 0) * Q + q1i) * N;
+        const double *uG = S1b + ((fc * 2 + 1) * Q + q1i) * N;
+        double d0 = tB[0] * uG[0], d1 = tG[0] * uB[0];
+#pragma unroll
+        for (int a2 = 1; a2 < N; ++a2) {
+          d0 = __fma_rn(tB[a2], uG[a2], d0);
+          d1 = __fma_rn(tG[a2], uB[a2], d1);
+        }
+        double *dst = f == 0 ? J[c] : (f == 1 ? Gv[c] : Gw[c]);
+        dst[0] = d0; dst[1] = d1;
+      }
+    }
+    if (WANT_E) {
+      const double *tb = sBl + q2i * M;
+      const double *src = E1b + q1i * M;
+      double acc = tb[0] * src[0];
+#pragma unroll
+      for (int j2 = 1; j2 < M; ++j2) acc = __fma_rn(tb[j2], src[j2], acc);
+      eq = acc;
+    }
+  }
 }
 
 // ----------------------------------------------------------------------------- kernel
-template <int DIM, int K, int Q, bool VISC, int MODE>
-__global__ void __launch_bounds__(Geo<DIM, K, Q>::NT, (512 / Geo<DIM, K, Q>::NT) > 0 ? (512 / Geo<DIM, K, Q>::NT) : 1)
+template <int DIM, int K, int Q, int NF, int EPB_>
+struct KCfg {
+  using G = Geo<DIM, K, Q, NF, EPB_>;
+  // occupancy target: as many CTAs as registers allow at <= 96 registers/thread for the
+  // one-element 3D CTAs (see DESIGN "Kernels"); 2D CTAs are 128 threads.
+  static constexpr int MINB = G::NT >= 224 ? 3 : (G::NT >= 128 ? 5 : 10);
+};
+
+template <int DIM, int K, int Q, bool VISC, int MODE, bool BATCHED, bool HAS_W, int EPB_ = 0>
+__global__ void __launch_bounds__(KCfg<DIM, K, Q, (MODE == MODE_MQ ? 1 : (HAS_W ? 3 : 2)), EPB_>::G::NT,
+                                  KCfg<DIM, K, Q, (MODE == MODE_MQ ? 1 : (HAS_W ? 3 : 2)), EPB_>::MINB)
 force_kernel(const Params P) {
-  using G = Geo<DIM, K, Q>;
+  constexpr int NF = MODE == MODE_MQ ? 1 : (HAS_W ? 3 : 2);
+  using G = Geo<DIM, K, Q, NF, EPB_>;
   constexpr int N = G::N, M = G::M, ND = G::ND, NE = G::NE, NQ = G::NQ, EPB = G::EPB,
                 NT = G::NT;
   extern __shared__ __align__(16) double smem[];
@@ -246,16 +438,13 @@ force_kernel(const Params P) {
   double *sBl = sG + Q * N;             // [Q][M]
   double *units = smem + G::TABD;       // EPB * UNIT
   int *snode = (int *)(units + EPB * G::UNIT);             // [EPB][ND]
-  unsigned long long *skey = (unsigned long long *)(snode + EPB * ND);  // [EPB]
-  static_assert((G::EPB * G::ND) % 2 == 0, "8-byte alignment of the key array");
+  unsigned long long *skey = (unsigned long long *)(snode + (EPB * ND + 1) / 2 * 2);  // [EPB]
 
   const int tid = threadIdx.x;
   const int u = tid / NQ;               // unit within CTA (may be >= EPB for pad threads)
   const int lt = tid - u * NQ;          // Gauss point within unit
-  const int64_t unit0 = (int64_t)blockIdx.x * EPB;
-  const int B = P.B;
-  const bool has_w = (MODE == MODE_FORCE) && (P.w != nullptr);
-  const int nf = MODE == MODE_MQ ? 1 : (has_w ? 3 : 2);
+  const int unit0 = blockIdx.x * EPB;
+  const int B = BATCHED ? P.B : 1;
 
   // --- tables to shared memory
   for (int i = tid; i < Q; i += NT) sW[i] = P.tab_w[i];
@@ -266,24 +455,24 @@ force_kernel(const Params P) {
   // --- S1 gather: node ids, then fields (unit fastest for coalescing across instances)
   for (int i = tid; i < EPB * ND; i += NT) {
     const int uu = i % EPB, a = i / EPB;
-    const int64_t gu = unit0 + uu;
+    const int gu = unit0 + uu;
     int nd = 0;
-    if (gu < P.n_units) nd = P.elem_nodes[(gu / B) * ND + a];
+    if (gu < P.n_units) nd = P.elem_nodes[(BATCHED ? gu / B : gu) * ND + a];
     snode[uu * ND + a] = nd;
   }
   __syncthreads();
   {
-    const int total = EPB * nf * DIM * ND;
+    constexpr int total = EPB * NF * DIM * ND;
     for (int i = tid; i < total; i += NT) {
       const int uu = i % EPB;
       int r = i / EPB;
       const int a = r % ND; r /= ND;
       const int c = r % DIM;
       const int f = r / DIM;
-      const int64_t gu = unit0 + uu;
+      const int gu = unit0 + uu;
       double val = 0.0;
       if (gu < P.n_units) {
-        const int64_t b = gu % B;
+        const int b = BATCHED ? gu % B : 0;
         const int64_t idx = ((int64_t)c * P.ld_nodes + snode[uu * ND + a]) * B + b;
         const double *src = MODE == MODE_MQ ? P.x : (f == 0 ? P.x : (f == 1 ? P.v : P.w));
         val = __ldg(src + idx);
@@ -293,11 +482,11 @@ force_kernel(const Params P) {
     if (MODE != MODE_MQ) {
       for (int i = tid; i < EPB * NE; i += NT) {
         const int uu = i % EPB, j = i / EPB;
-        const int64_t gu = unit0 + uu;
+        const int gu = unit0 + uu;
         double val = 0.0;
         if (gu < P.n_units) {
-          const int64_t l = gu / B, b = gu % B;
-          val = __ldg(P.e + (l * NE + j) * B + b);
+          const int l = BATCHED ? gu / B : gu, b = BATCHED ? gu % B : 0;
+          val = __ldg(P.e + ((int64_t)l * NE + j) * B + b);
         }
         units[uu * G::UNIT + G::NF * DIM * ND + j] = val;
       }
@@ -305,24 +494,24 @@ force_kernel(const Params P) {
   }
   __syncthreads();
 
-  const bool active = (u < EPB) && (unit0 + u < P.n_units);
+  const bool active = (u < EPB) && (unit0 + u < P.n_units) && (lt < NQ);
   const int uc = u < EPB ? u : EPB - 1;  // clamp pad threads onto a real unit buffer (reads only)
   double *U = units + uc * G::UNIT;
   double *Xs = U;                         // [NF][DIM][ND]
   double *Es = U + G::NF * DIM * ND;      // [NE]
   double *Wk = Es + NE;                   // work region
-  const int64_t gu = (unit0 + uc < P.n_units) ? unit0 + uc : 0;  // safe unit for reads
-  const int64_t l = gu / B;
-  const int b = (int)(gu % B);
-  const int64_t gid = P.elem_gid ? (int64_t)P.elem_gid[l] : l;
+  const int gu = (unit0 + uc < P.n_units) ? unit0 + uc : 0;  // safe unit for reads
+  const int l = BATCHED ? gu / B : gu;
+  const int b = BATCHED ? gu % B : 0;
+  const int gid = P.elem_gid ? P.elem_gid[l] : l;
 
   // --- S2 forward contractions (canonical order, DESIGN A.2)
   double J[3][3], Gv[3][3], Gw[3][3];
   double eq = 0.0;
   int q1i, q2i, q3i = 0;
-  if (DIM == 2) { q1i = lt % Q; q2i = lt / Q; }
-  else { q1i = lt % Q; q2i = (lt / Q) % Q; q3i = lt / (Q * Q); }
-  if (lt >= NQ) { q1i = q2i = q3i = 0; }
+  const int lq = lt < NQ ? lt : 0;
+  if (DIM == 2) { q1i = lq % Q; q2i = lq / Q; }
+  else { q1i = lq % Q; q2i = (lq / Q) % Q; q3i = lq / (Q * Q); }
 
   if (DIM == 3) {
     double *S1b = Wk;                              // [NF*DIM][2][Q][N][N]
@@ -331,7 +520,7 @@ force_kernel(const Params P) {
     double *E2b = E1b + G::E1;                     // [Q][Q][M]
     if (u < EPB) {
       // stage 1: contract a1
-      const int cnt1 = nf * DIM * 2 * Q * N * N;
+      constexpr int cnt1 = NF * DIM * 2 * Q * N * N;
       for (int o = lt; o < cnt1; o += NQ) {
         int r = o;
         const int a3 = r % N; r /= N;
@@ -364,20 +553,26 @@ force_kernel(const Params P) {
     __syncthreads();
     if (u < EPB) {
       // stage 2: contract a2 ; kind 0: B.UG (d/dxi1), 1: G.UB (d/dxi2), 2: B.UB (d/dxi3)
-      const int cnt2 = nf * DIM * 3 * Q * Q * N;
+      constexpr int cnt2 = NF * DIM * Q * Q * N;
       for (int o = lt; o < cnt2; o += NQ) {
         int r = o;
         const int a3 = r % N; r /= N;
         const int q2 = r % Q; r /= Q;
-        const int q1 = r % Q; r /= Q;
-        const int kind = r % 3;
-        const int fc = r / 3;
-        const double *tab = (kind == 1 ? sG : sB) + q2 * N;
-        const double *src = S1b + ((fc * 2 + (kind == 0 ? 1 : 0)) * Q + q1) * N * N + a3;
-        double acc = tab[0] * src[0];
+        const int q1 = r % Q;
+        const int fc = r / Q;
+        const double *tB = sB + q2 * N, *tG = sG + q2 * N;
+        const double *uB = S1b + ((fc * 2 + 0) * Q + q1) * N * N + a3;
+        const double *uG = S1b + ((fc * 2 + 1) * Q + q1) * N * N + a3;
+        double d1 = tB[0] * uG[0], d2 = tG[0] * uB[0], d3 = tB[0] * uB[0];
 #pragma unroll
-        for (int a2 = 1; a2 < N; ++a2) acc = __fma_rn(tab[a2], src[a2 * N], acc);
-        S2b[((fc * 3 + kind) * Q + q1) * Q * N + q2 * N + a3] = acc;
+        for (int a2 = 1; a2 < N; ++a2) {
+          d1 = __fma_rn(tB[a2], uG[a2 * N], d1);
+          d2 = __fma_rn(tG[a2], uB[a2 * N], d2);
+          d3 = __fma_rn(tB[a2], uB[a2 * N], d3);
+        }
+        S2b[((fc * 3 + 0) * Q + q1) * Q * N + q2 * N + a3] = d1;
+        S2b[((fc * 3 + 1) * Q + q1) * Q * N + q2 * N + a3] = d2;
+        S2b[((fc * 3 + 2) * Q + q1) * Q * N + q2 * N + a3] = d3;
       }
       if (MODE != MODE_MQ) {
         for (int o = lt; o < Q * Q * M; o += NQ) {
@@ -395,43 +590,12 @@ force_kernel(const Params P) {
       }
     }
     __syncthreads();
-    // stage 3 (per Gauss point): contract a3
-    {
-      const double *tB = sB + q3i * N, *tG = sG + q3i * N;
-#pragma unroll
-      for (int f = 0; f < 3; ++f) {
-        if (f >= nf) break;
-#pragma unroll
-        for (int c = 0; c < DIM; ++c) {
-          const int fc = f * DIM + c;
-          const double *p1 = S2b + ((fc * 3 + 0) * Q + q1i) * Q * N + q2i * N;
-          const double *p2 = S2b + ((fc * 3 + 1) * Q + q1i) * Q * N + q2i * N;
-          const double *p3 = S2b + ((fc * 3 + 2) * Q + q1i) * Q * N + q2i * N;
-          double d0 = tB[0] * p1[0], d1 = tB[0] * p2[0], d2 = tG[0] * p3[0];
-#pragma unroll
-          for (int a3 = 1; a3 < N; ++a3) {
-            d0 = __fma_rn(tB[a3], p1[a3], d0);
-            d1 = __fma_rn(tB[a3], p2[a3], d1);
-            d2 = __fma_rn(tG[a3], p3[a3], d2);
-          }
-          double *dst = f == 0 ? J[c] : (f == 1 ? Gv[c] : Gw[c]);
-          dst[0] = d0; dst[1] = d1; dst[2] = d2;
-        }
-      }
-      if (MODE != MODE_MQ) {
-        const double *tb = sBl + q3i * M;
-        const double *src = E2b + (q1i * Q + q2i) * M;
-        double acc = tb[0] * src[0];
-#pragma unroll
-        for (int j3 = 1; j3 < M; ++j3) acc = __fma_rn(tb[j3], src[j3], acc);
-        eq = acc;
-      }
-    }
+    // stage 3 (per Gauss point): contract a3 -- see forward_point
   } else {
     double *S1b = Wk;                              // [NF*DIM][2][Q][N]
     double *E1b = Wk + G::NF * DIM * 2 * G::S1;    // [Q][M]
     if (u < EPB) {
-      const int cnt1 = nf * DIM * 2 * Q * N;
+      constexpr int cnt1 = NF * DIM * 2 * Q * N;
       for (int o = lt; o < cnt1; o += NQ) {
         int r = o;
         const int a2 = r % N; r /= N;
@@ -458,64 +622,62 @@ force_kernel(const Params P) {
       }
     }
     __syncthreads();
-    {
-      const double *tB = sB + q2i * N, *tG = sG + q2i * N;
-#pragma unroll
-      for (int f = 0; f < 3; ++f) {
-        if (f >= nf) break;
-#pragma unroll
-        for (int c = 0; c < DIM; ++c) {
-          const int fc = f * DIM + c;
-          const double *uB = S1b + ((fc * 2 + 0) * Q + q1i) * N;
-          const double *uG = S1b + ((fc * 2 + 1) * Q + q1i) * N;
-          double d0 = tB[0] * uG[0], d1 = tG[0] * uB[0];
-#pragma unroll
-          for (int a2 = 1; a2 < N; ++a2) {
-            d0 = __fma_rn(tB[a2], uG[a2], d0);
-            d1 = __fma_rn(tG[a2], uB[a2], d1);
-          }
-          double *dst = f == 0 ? J[c] : (f == 1 ? Gv[c] : Gw[c]);
-          dst[0] = d0; dst[1] = d1;
-        }
-      }
-      if (MODE != MODE_MQ) {
-        const double *tb = sBl + q2i * M;
-        const double *src = E1b + q1i * M;
-        double acc = tb[0] * src[0];
-#pragma unroll
-        for (int j2 = 1; j2 < M; ++j2) acc = __fma_rn(tb[j2], src[j2], acc);
-        eq = acc;
-      }
-    }
   }
+  forward_point<DIM, K, Q, NF, MODE != MODE_MQ>(sB, sG, sBl, Wk, q1i, q2i, q3i, J, Gv, Gw, eq);
 
   // --- MODE_MQ: m_q = rho0_K detJ0 (density elimination)
   if (MODE == MODE_MQ) {
-    if (active && lt < NQ) {
+    if (active) {
       const double det0 = det_only<DIM>(J);
-      P.mq_out[gid * NQ + lt] = P.rho0[gid] * det0;
+      P.mq_out[(int64_t)gid * NQ + lt] = P.rho0[gid] * det0;
     }
     return;
   }
+  if (!HAS_W) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) Gw[c][d] = 0.0;
+  }
 
-  // --- S3 pointwise
-  double sig[3][3], Ji[3][3], det = 1.0, dtq = 0.0;
+  // --- S3 pointwise: fast pass, exact IEEE re-run where a fast path was out of range
   const double gam = __ldg(P.gamma + gid);
-  const double mq = __ldg(P.mq + gid * NQ + lt);
-  dtq = pointwise<DIM, VISC>(J, Gv, eq, mq, gam, P.q1, P.q2, P.alpha, P.alpha_mu, sig, Ji, det);
+  const double mq = __ldg(P.mq + (int64_t)gid * NQ + lq);
+  double wq = sW[q1i] * sW[q2i];
+  if (DIM == 3) wq = wq * sW[q3i];
+  const PhysIn ph{P.q1, P.q2, P.alpha, P.alpha_mu};
+  PointOut po;
+  {
+    ArithFast af;
+    pointwise<DIM, VISC, HAS_W, true>(af, J, Gv, Gw, eq, mq, gam, wq, ph, po);
+    if (!af.ok) {
+      // rare: some fast div/sqrt left its exact range; recompute the inputs from shared
+      // memory (not kept live across the fast pass) and re-run with IEEE operators.
+      forward_point<DIM, K, Q, NF, true>(sB, sG, sBl, Wk, q1i, q2i, q3i, J, Gv, Gw, eq);
+      if (!HAS_W) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) Gw[c][d] = 0.0;
+      }
+      ArithIeee ai;
+      pointwise<DIM, VISC, HAS_W, false>(ai, J, Gv, Gw, eq, __ldg(P.mq + (int64_t)gid * NQ + lq),
+                                         __ldg(P.gamma + gid), wq, ph, po);
+    }
+  }
 
   // --- S6 dt: status flags, then min of order-preserving keys
   unsigned long long key = ~0ull;
   if (active) {
-    if (!(det > 0.0)) atomicMin(&P.st[b].first_bad, (unsigned long long)gid);
-    if (isnan(dtq)) atomicOr(&P.st[b].nan_flag, 1u);
-    else key = dt_key(dtq);
+    if (!(po.det > 0.0)) atomicMin(&P.st[b].first_bad, (unsigned long long)gid);
+    if (isnan(po.dtq)) atomicOr(&P.st[b].nan_flag, 1u);
+    else key = dt_key(po.dtq);
   }
   {
     constexpr bool WARP_IN_UNIT = (NQ % 32 == 0) || (EPB == 1);
     constexpr bool HALF = (NQ == 16);
     if (WARP_IN_UNIT || HALF) {
-      const int width = WARP_IN_UNIT ? 32 : 16;
+      constexpr int width = WARP_IN_UNIT ? 32 : 16;
 #pragma unroll
       for (int off = width / 2; off > 0; off >>= 1) {
         const unsigned long long o = __shfl_xor_sync(0xffffffffu, key, off);
@@ -527,15 +689,14 @@ force_kernel(const Params P) {
     }
   }
   __syncthreads();
-  if (tid == 0) {
-    if (B == 1) {
+  if (!BATCHED) {
+    if (tid == 0) {
       unsigned long long k = skey[0];
       for (int i = 1; i < EPB; ++i) k = skey[i] < k ? skey[i] : k;
       if (k != ~0ull) atomicMin(&P.st[0].dt_key, k);
     }
-  }
-  if (B > 1 && tid < EPB) {
-    const int64_t g2 = unit0 + tid;
+  } else if (tid < EPB) {
+    const int g2 = unit0 + tid;
     if (g2 < P.n_units && skey[tid] != ~0ull) atomicMin(&P.st[g2 % B].dt_key, skey[tid]);
   }
   if (MODE == MODE_DT) return;
@@ -547,27 +708,16 @@ force_kernel(const Params P) {
   double *Wb = Tb + G::TB;
   double *F1b = Wb + G::WB;
   double *F2b = F1b + G::F1B;
-  __syncthreads();  // forward buffers are dead from here on
+  // (the __syncthreads above separates the last forward read from these writes)
   if (u < EPB && lt < NQ) {
-    double wq = sW[q1i] * sW[q2i];
-    if (DIM == 3) wq = wq * sW[q3i];
-    const double wd = wq * det;
-    double A = 0.0;
 #pragma unroll
     for (int c = 0; c < DIM; ++c)
 #pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        double s = sig[c][0] * Ji[d][0];
-#pragma unroll
-        for (int i = 1; i < DIM; ++i) s = __fma_rn(sig[c][i], Ji[d][i], s);
-        s = wd * s;
-        Ss[(c * DIM + d) * NQ + lt] = s;
-        A = __fma_rn(s, has_w ? Gw[c][d] : Gv[c][d], A);
-      }
-    As[lt] = A;
+      for (int d = 0; d < DIM; ++d) Ss[(c * DIM + d) * NQ + lt] = po.S[c][d];
+    As[lt] = po.A;
   }
   __syncthreads();
-  const int64_t slot_base = l * ND;
+  const int64_t slot_base = (int64_t)l * ND;
   if (DIM == 3) {
     if (u < EPB) {
       // b1: T[dl][c][q1][q2][a3] = sum_q3 (dl==2 ? G : B)[q3][a3] S[c][dl](q1,q2,q3)
@@ -630,7 +780,7 @@ force_kernel(const Params P) {
       }
     }
     __syncthreads();
-    if (active) {
+    if (u < EPB && unit0 + u < P.n_units) {
       // b3: F1[c][a] = sum_q1 G[q1][a1] W1[c][q1][a2][a3] + B[q1][a1] W23[c][q1][a2][a3]
       for (int o = lt; o < DIM * ND; o += NQ) {
         const int a = o % ND, c = o / ND;
@@ -645,14 +795,14 @@ force_kernel(const Params P) {
         const int s = P.slot[slot_base + a];
         if (s >= 0) P.evec[((int64_t)s * DIM + c) * B + b] = acc;
       }
-      const int64_t row = P.ftw_row ? (int64_t)P.ftw_row[l] : l;
+      const int row = P.ftw_row ? P.ftw_row[l] : l;
       if (row >= 0) {
         for (int o = lt; o < NE; o += NQ) {
           const int j1 = o % M, j2 = (o / M) % M, j3 = o / (M * M);
           double acc = 0.0;
 #pragma unroll
           for (int q1 = 0; q1 < Q; ++q1) acc = __fma_rn(sBl[q1 * M + j1], F2b[(q1 * M + j2) * M + j3], acc);
-          P.FTw[(row * NE + o) * B + b] = acc;
+          P.FTw[((int64_t)row * NE + o) * B + b] = acc;
         }
       }
     }
@@ -681,7 +831,7 @@ force_kernel(const Params P) {
       }
     }
     __syncthreads();
-    if (active) {
+    if (u < EPB && unit0 + u < P.n_units) {
       for (int o = lt; o < DIM * ND; o += NQ) {
         const int a = o % ND, c = o / ND;
         const int a1 = a % N, a2 = a / N;
@@ -694,14 +844,14 @@ force_kernel(const Params P) {
         const int s = P.slot[slot_base + a];
         if (s >= 0) P.evec[((int64_t)s * DIM + c) * B + b] = acc;
       }
-      const int64_t row = P.ftw_row ? (int64_t)P.ftw_row[l] : l;
+      const int row = P.ftw_row ? P.ftw_row[l] : l;
       if (row >= 0) {
         for (int o = lt; o < NE; o += NQ) {
           const int j1 = o % M, j2 = o / M;
           double acc = 0.0;
 #pragma unroll
           for (int q1 = 0; q1 < Q; ++q1) acc = __fma_rn(sBl[q1 * M + j1], F1b[q1 * M + j2], acc);
-          P.FTw[(row * NE + o) * B + b] = acc;
+          P.FTw[((int64_t)row * NE + o) * B + b] = acc;
         }
       }
     }
@@ -730,8 +880,8 @@ __global__ void assemble_kernel(int64_t n_nodes, int B, const int32_t *__restric
                                 hydro_devstatus *st, double *dt_out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n_nodes * B) {
-    const int64_t node = t / B;
-    const int b = (int)(t % B);
+    const int64_t node = B == 1 ? t : t / B;
+    const int b = B == 1 ? 0 : (int)(t % B);
     const int s0 = off[node], s1 = off[node + 1];
 #pragma unroll
     for (int c = 0; c < DIM; ++c) {
@@ -752,4 +902,49 @@ __global__ void finalize_dt_kernel(int B, hydro_devstatus *st, double *dt_out) {
   for (int i = threadIdx.x; i < B; i += blockDim.x) finalize_one(st + i, dt_out ? dt_out + i : nullptr);
 }
 
+}  // namespace hk
+
+namespace hk {
+// ----------------------------------------------------------------------------- self-test
+// Bit-equality of the ieee_fast.cuh fast paths against the IEEE operators on seeded
+// operands (SplitMix64 counter stream).  dist 0: random sign/mantissa, exponent uniform in
+// [-64, 64]; dist 1: raw 64-bit patterns (NaN, inf, subnormals, extremes).  op 0: a/b,
+// 1: 1/b, 2: sqrt(|x|) (dist 1: sqrt(x)).  counts[0] += fast-path-valid results whose bits
+// differ (must stay 0), counts[1] += operands outside the fast range, counts[2] += total.
+__device__ __forceinline__ unsigned long long st_mix(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double st_operand(unsigned long long r, int dist) {
+  if (dist == 1) return __longlong_as_double((long long)r);
+  const unsigned long long mant = r & 0x000FFFFFFFFFFFFFull;
+  const long long ex = (long long)((r >> 52) & 127) - 64 + 1023;
+  const unsigned long long sg = (r >> 63) << 63;
+  return __longlong_as_double((long long)(sg | ((unsigned long long)ex << 52) | mant));
+}
+
+__global__ void selftest_ieee_kernel(unsigned long long seed, long long n, int op, int dist,
+                                     unsigned long long *counts) {
+  unsigned long long bad = 0, slow = 0, tot = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long r1 = st_mix(seed ^ (2ull * (unsigned long long)i));
+    const unsigned long long r2 = st_mix(seed ^ (2ull * (unsigned long long)i + 1ull));
+    double a = st_operand(r1, dist), b = st_operand(r2, dist);
+    bool ok = true;
+    double f, ref;
+    if (op == 0) { f = div_fast(a, b, ok); ref = __ddiv_rn(a, b); }
+    else if (op == 1) { f = rcp_fast(b, ok); ref = __ddiv_rn(1.0, b); }
+    else { if (dist == 0) a = fabs(a); f = sqrt_fast(a, ok); ref = __dsqrt_rn(a); }
+    ++tot;
+    if (!ok) ++slow;
+    else if (__double_as_longlong(f) != __double_as_longlong(ref)) ++bad;
+  }
+  atomicAdd(counts + 0, bad);
+  atomicAdd(counts + 1, slow);
+  atomicAdd(counts + 2, tot);
+}
 }  // namespace hk

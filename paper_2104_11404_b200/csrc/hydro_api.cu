@@ -121,27 +121,20 @@ std::pair<cudaEvent_t, cudaEvent_t> prof_pair() {
   return p;
 }
 
-template <int DIM, int K, int Q>
-hydro_status launch_force_t(int mode, bool visc, const hk::Params &P, cudaStream_t s) {
-  using G = hk::Geo<DIM, K, Q>;
-  const int64_t grid = (P.n_units + G::EPB - 1) / G::EPB;
+template <int DIM, int K, int Q, bool VISC, int MODE, bool BATCHED, bool HAS_W>
+hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
+  constexpr int NF = MODE == hk::MODE_MQ ? 1 : (HAS_W ? 3 : 2);
+  using G = hk::Geo<DIM, K, Q, NF>;
+  const int64_t grid = ((int64_t)P.n_units + G::EPB - 1) / G::EPB;
   if (grid <= 0) return HYDRO_OK;
-  void (*kern)(const hk::Params);
-  if (mode == hk::MODE_FORCE)
-    kern = visc ? hk::force_kernel<DIM, K, Q, true, hk::MODE_FORCE>
-                : hk::force_kernel<DIM, K, Q, false, hk::MODE_FORCE>;
-  else if (mode == hk::MODE_DT)
-    kern = visc ? hk::force_kernel<DIM, K, Q, true, hk::MODE_DT>
-                : hk::force_kernel<DIM, K, Q, false, hk::MODE_DT>;
-  else
-    kern = hk::force_kernel<DIM, K, Q, false, hk::MODE_MQ>;
-  static bool attr_set[3][2] = {{false, false}, {false, false}, {false, false}};
-  if (!attr_set[mode][visc ? 1 : 0]) {
+  auto kern = hk::force_kernel<DIM, K, Q, VISC, MODE, BATCHED, HAS_W>;
+  static bool attr_set = false;  // one flag per instantiation
+  if (!attr_set) {
     CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-    attr_set[mode][visc ? 1 : 0] = true;
+    attr_set = true;
   }
   std::pair<cudaEvent_t, cudaEvent_t> ev;
-  const bool prof = g_prof.on && mode != hk::MODE_MQ;
+  const bool prof = g_prof.on && MODE != hk::MODE_MQ;
   if (prof) {
     ev = prof_pair();
     cudaEventRecord(ev.first, s);
@@ -156,12 +149,34 @@ hydro_status launch_force_t(int mode, bool visc, const hk::Params &P, cudaStream
   return HYDRO_OK;
 }
 
-hydro_status launch_force(int dim, int k, int mode, bool visc, const hk::Params &P,
-                          cudaStream_t s) {
-  if (dim == 2 && k == 2) return launch_force_t<2, 2, 4>(mode, visc, P, s);
-  if (dim == 3 && k == 2) return launch_force_t<3, 2, 4>(mode, visc, P, s);
-  if (dim == 2 && k == 3) return launch_force_t<2, 3, 6>(mode, visc, P, s);
-  if (dim == 3 && k == 3) return launch_force_t<3, 3, 6>(mode, visc, P, s);
+// Instantiated variants: FORCE x {visc} x {batched} x {w given}; DT x {visc} (full mode,
+// no w); MQ (setup).
+template <int DIM, int K, int Q>
+hydro_status launch_force_t(int mode, bool visc, bool batched, bool has_w, const hk::Params &P,
+                            cudaStream_t s) {
+  using namespace hk;
+  if (mode == MODE_MQ) return launch_force_k<DIM, K, Q, false, MODE_MQ, false, false>(P, s);
+  if (mode == MODE_DT) {
+    if (batched || has_w) return HYDRO_ERR_ARG;
+    return visc ? launch_force_k<DIM, K, Q, true, MODE_DT, false, false>(P, s)
+                : launch_force_k<DIM, K, Q, false, MODE_DT, false, false>(P, s);
+  }
+#define HK_F(V, BA, W) launch_force_k<DIM, K, Q, V, MODE_FORCE, BA, W>(P, s)
+  if (visc) {
+    if (batched) return has_w ? HK_F(true, true, true) : HK_F(true, true, false);
+    return has_w ? HK_F(true, false, true) : HK_F(true, false, false);
+  }
+  if (batched) return has_w ? HK_F(false, true, true) : HK_F(false, true, false);
+  return has_w ? HK_F(false, false, true) : HK_F(false, false, false);
+#undef HK_F
+}
+
+hydro_status launch_force(int dim, int k, int mode, bool visc, bool batched, bool has_w,
+                          const hk::Params &P, cudaStream_t s) {
+  if (dim == 2 && k == 2) return launch_force_t<2, 2, 4>(mode, visc, batched, has_w, P, s);
+  if (dim == 3 && k == 2) return launch_force_t<3, 2, 4>(mode, visc, batched, has_w, P, s);
+  if (dim == 2 && k == 3) return launch_force_t<2, 3, 6>(mode, visc, batched, has_w, P, s);
+  if (dim == 3 && k == 3) return launch_force_t<3, 3, 6>(mode, visc, batched, has_w, P, s);
   return HYDRO_ERR_UNSUPPORTED;
 }
 
@@ -211,6 +226,15 @@ hydro_status hydro_profile_read(double *total_ms, int64_t *count) {
   g_prof.pending.clear();
   if (total_ms) *total_ms = tot;
   if (count) *count = n;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_selftest_ieee_fast(uint64_t seed, int64_t n, int op, int dist,
+                                      unsigned long long *counts, hydro_stream_t stream) {
+  if (n < 0 || op < 0 || op > 2 || dist < 0 || dist > 1 || !counts) return HYDRO_ERR_ARG;
+  hk::selftest_ieee_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(seed, n, op, dist, counts);
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
   return HYDRO_OK;
 }
 
@@ -306,7 +330,7 @@ hydro_status hydro_ctx_create(const hydro_mesh_desc *desc, void *workspace, size
   // m_q = rho0_K detJ0 (density elimination) with the contract formulas
   hk::Params P;
   std::memset(&P, 0, sizeof(P));
-  P.n_units = E;
+  P.n_units = (int32_t)E;
   P.B = 1;
   P.ld_nodes = NN;
   P.elem_nodes = desc->elem_nodes;
@@ -315,7 +339,7 @@ hydro_status hydro_ctx_create(const hydro_mesh_desc *desc, void *workspace, size
   P.mq_out = c->mq;
   P.st = c->st;
   fill_tables_ptrs(P, c);
-  hydro_status r = launch_force(desc->dim, desc->order_h1, hk::MODE_MQ, false, P, s);
+  hydro_status r = launch_force(desc->dim, desc->order_h1, hk::MODE_MQ, false, false, false, P, s);
   if (r != HYDRO_OK) return fail(r);
   if (cudaStreamSynchronize(s) != cudaSuccess) return fail(HYDRO_ERR_CUDA);
   *out = c;
@@ -335,7 +359,7 @@ static hydro_status force_common(hydro_ctx *c, int mode, const double *x, const 
   if (mode == hk::MODE_FORCE && (!F1 || !FTw)) return HYDRO_ERR_ARG;
   hk::Params P;
   std::memset(&P, 0, sizeof(P));
-  P.n_units = c->d.n_elem;
+  P.n_units = (int32_t)c->d.n_elem;
   P.B = 1;
   P.ld_nodes = c->d.n_nodes;
   P.elem_nodes = c->d.elem_nodes;
@@ -347,7 +371,7 @@ static hydro_status force_common(hydro_ctx *c, int mode, const double *x, const 
   P.FTw = FTw;
   P.st = c->st;
   fill_tables_ptrs(P, c);
-  hydro_status r = launch_force(c->d.dim, c->d.order_h1, mode, visc.enabled != 0, P, s);
+  hydro_status r = launch_force(c->d.dim, c->d.order_h1, mode, visc.enabled != 0, false, w != nullptr, P, s);
   if (r != HYDRO_OK) return r;
   if (mode == hk::MODE_FORCE)
     return launch_assemble(c->d.dim, c->d.n_nodes, 1, c->off, c->evec, F1, c->st, dt, s);
@@ -521,7 +545,8 @@ hydro_status hydro_force_sampled(hydro_sample *p, const double *x_S, const doubl
   cudaStream_t s = (cudaStream_t)stream;
   hk::Params P;
   std::memset(&P, 0, sizeof(P));
-  P.n_units = p->n_cl * p->B;
+  if (p->n_cl * (int64_t)p->B >= ((int64_t)1 << 31)) return HYDRO_ERR_ARG;
+  P.n_units = (int32_t)(p->n_cl * p->B);
   P.B = p->B;
   P.ld_nodes = p->n_cl_nodes;
   P.elem_nodes = p->elem_nodes;
@@ -535,7 +560,7 @@ hydro_status hydro_force_sampled(hydro_sample *p, const double *x_S, const doubl
   P.ftw_row = p->ftw_row;
   P.st = p->st;
   fill_tables_ptrs(P, c);
-  hydro_status r = launch_force(c->d.dim, c->d.order_h1, hk::MODE_FORCE, visc.enabled != 0, P, s);
+  hydro_status r = launch_force(c->d.dim, c->d.order_h1, hk::MODE_FORCE, visc.enabled != 0, p->B > 1, w_S != nullptr, P, s);
   if (r != HYDRO_OK) return r;
   return launch_assemble(c->d.dim, p->n_s0_nodes, p->B, p->off, p->evec, F1_rows, p->st, dt, s);
 }

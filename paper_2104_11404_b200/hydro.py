@@ -27,7 +27,7 @@ EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy"
             "hydro_sample_destroy", "hydro_sample_info", "hydro_sample_lists", "hydro_rom_lift",
             "hydro_force_sampled", "hydro_sample_status_sync", "hydro_rom_project_workspace_bytes",
             "hydro_rom_project", "hydro_basis_tables", "hydro_launch_count", "hydro_version",
-            "hydro_profile_enable", "hydro_profile_read"]
+            "hydro_profile_enable", "hydro_profile_read", "hydro_selftest_ieee_fast"]
 
 
 class HydroError(RuntimeError):
@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
         L.hydro_rom_lift.argtypes = [i64, i32, i32, vp, vp, i32, vp, vp, vp]
         L.hydro_force_sampled.argtypes = [vp, vp, vp, vp, vp, vp, _Visc, _Cfl, vp, vp, vp, vp]
         L.hydro_sample_status_sync.argtypes = [vp, vp, ctypes.POINTER(i64)]
+        L.hydro_selftest_ieee_fast.argtypes = [ctypes.c_uint64, i64, i32, i32, vp, vp]
         L.hydro_rom_project_workspace_bytes.restype = ctypes.c_size_t
         L.hydro_rom_project_workspace_bytes.argtypes = [i32, i64, i32]
         L.hydro_rom_project.argtypes = [i32, i64, i32, vp, vp, vp, vp, ctypes.c_size_t, vp]
@@ -95,7 +96,7 @@ def _ptr(t: Optional[torch.Tensor]):
         return None
     if not t.is_cuda:
         raise ValueError("hydro: tensors must live on the CUDA device")
-    if t.dtype not in (torch.float64, torch.int32, torch.uint8):
+    if t.dtype not in (torch.float64, torch.int32, torch.int64, torch.uint8):
         raise ValueError(f"hydro: unexpected dtype {t.dtype}")
     if not t.is_contiguous():
         raise ValueError("hydro: tensors must be contiguous")
@@ -139,6 +140,14 @@ def basis_tables(k: int, q: int) -> dict:
     p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
     _check(lib().hydro_basis_tables(k, q, p(xi), p(w), p(B), p(G), p(Bl)), "hydro_basis_tables")
     return dict(xi=xi, w=w, B=B, G=G, Bl=Bl)
+
+
+def selftest_ieee_fast(seed: int, n: int, op: int, dist: int, stream=None):
+    """(mismatches, slow-path operands, total) of the fast div/rcp/sqrt paths vs IEEE."""
+    counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+    _check(lib().hydro_selftest_ieee_fast(seed, n, op, dist, _ptr(counts), _stream(stream)),
+           "hydro_selftest_ieee_fast")
+    return tuple(int(x) for x in counts.cpu().tolist())
 
 
 def launch_count() -> int:
