@@ -16,8 +16,8 @@
 //   S4 backward  S_q = w_q detJ sigma J^-T, A_q = w_q detJ sigma : grad w, then the
 //                sum-factorised transposes F1_K[a][c] = sum_q (S_q gradhat phi_a)_c,
 //                FTw_K[j] = sum_q psi_j A_q;
-//   S5 outputs   F1_K to its assembly slots (deterministic gather in assemble_kernel),
-//                FTw_K element-local;
+//   S5 outputs   F1_K to its assembly slots (summed per node in fixed order by
+//                assemble_kernel, a programmatic dependent launch), FTw_K element-local;
 //   S6 dt        warp/CTA min of order-preserving keys, one atomicMin per CTA (exact).
 // PAPER anchors: Eq. fom, Eq. forceOneforceTv, Eq. EOS P:374-376,
 // stress split P:367-370, density elimination P:389-391, Eq. adaptive-timestep P:533-544.
@@ -79,6 +79,14 @@ struct Params {
   double *mq_out;           // MODE_MQ: [n_elem][NQ]
   hydro_devstatus *st;      // [B]
   const double *tab_w, *tab_B, *tab_G, *tab_Bl;  // device tables [Q], [Q][N], [Q][N], [Q][M]
+  // fused deterministic assembly (S5) and dt finalisation (S6)
+  const int32_t *anode;     // [n_l][ND] assembly-node index of (element, local node) or -1
+  const int32_t *off;       // [n_asm + 1] CSR: slots of assembly node n are off[n]..off[n+1)
+  unsigned *cnt;            // [n_asm][B] arrival counters (zero between calls)
+  unsigned *done;           // CTA completion counter (zero between calls)
+  double *F1;               // [DIM][n_asm][B] assembled output
+  int64_t n_asm;            // assembly nodes (n_nodes, or S0 nodes in sampled mode)
+  double *dt_out;           // [B] or NULL
 };
 
 // ----------------------------------------------------------------------------- helpers
@@ -92,6 +100,26 @@ __device__ __forceinline__ double key_to_dt(unsigned long long k) {
   unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double((long long)b);
 }
+
+// Device-side completion of a call, in the dependent launch that follows the force kernel:
+// dt = min key (NaN if any dt_q was NaN); the per-call state is reset for the next call
+// and the NaN condition is folded into the sticky word read by status_sync.
+__device__ __forceinline__ void finalize_one(hydro_devstatus *st, double *dt_out) {
+  double d = key_to_dt(st->dt_key);
+  if (st->nan_flag) {
+    d = __longlong_as_double(0x7ff8000000000000ll);
+    st->nan_sticky = 1u;
+  }
+  if (dt_out) *dt_out = d;
+  st->dt_key = dt_key(__longlong_as_double(0x7ff0000000000000ll));  // +inf
+  st->nan_flag = 0u;
+}
+
+// Programmatic dependent launch (PDL): the force kernel signals that its dependent (the
+// assembly / dt-finalisation kernel) may be scheduled; the dependent waits for the force
+// grid's completion and memory flush before reading.  Hides the second launch's latency.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // One cyclic-Jacobi rotation of DESIGN A.4 on pair (p,q) with r3 = the third index,
 // skipped when |a_pq| <= tol.  Written without branches (the skipped case computes on
@@ -699,7 +727,11 @@ force_kernel(const Params P) {
     const int g2 = unit0 + tid;
     if (g2 < P.n_units && skey[tid] != ~0ull) atomicMin(&P.st[g2 % B].dt_key, skey[tid]);
   }
-  if (MODE == MODE_DT) return;
+  if (MODE == MODE_DT) {
+    pdl_trigger();
+    return;
+  }
+  __syncthreads();  // forward buffers are dead from here on (S4 reuses them)
 
   // --- S4 backward
   double *Ss = Wk;                      // [DIM*DIM][NQ]
@@ -782,18 +814,25 @@ force_kernel(const Params P) {
     __syncthreads();
     if (u < EPB && unit0 + u < P.n_units) {
       // b3: F1[c][a] = sum_q1 G[q1][a1] W1[c][q1][a2][a3] + B[q1][a1] W23[c][q1][a2][a3]
-      for (int o = lt; o < DIM * ND; o += NQ) {
-        const int a = o % ND, c = o / ND;
+      for (int a = lt; a < ND; a += NQ) {
         const int a1 = a % N, a23 = a / N;  // a23 = a2 + N a3
         const int a2 = a23 % N, a3 = a23 / N;
-        double acc = 0.0;
+        double val[3];
 #pragma unroll
-        for (int q1 = 0; q1 < Q; ++q1) {
-          acc = __fma_rn(sG[q1 * N + a1], Wb[((0 * DIM + c) * Q + q1) * N * N + a2 * N + a3], acc);
-          acc = __fma_rn(sB[q1 * N + a1], Wb[((1 * DIM + c) * Q + q1) * N * N + a2 * N + a3], acc);
+        for (int c = 0; c < DIM; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q1 = 0; q1 < Q; ++q1) {
+            acc = __fma_rn(sG[q1 * N + a1], Wb[((0 * DIM + c) * Q + q1) * N * N + a2 * N + a3], acc);
+            acc = __fma_rn(sB[q1 * N + a1], Wb[((1 * DIM + c) * Q + q1) * N * N + a2 * N + a3], acc);
+          }
+          val[c] = acc;
         }
         const int s = P.slot[slot_base + a];
-        if (s >= 0) P.evec[((int64_t)s * DIM + c) * B + b] = acc;
+        if (s >= 0) {
+#pragma unroll
+          for (int c = 0; c < DIM; ++c) P.evec[((int64_t)s * DIM + c) * B + b] = val[c];
+        }
       }
       const int row = P.ftw_row ? P.ftw_row[l] : l;
       if (row >= 0) {
@@ -832,17 +871,24 @@ force_kernel(const Params P) {
     }
     __syncthreads();
     if (u < EPB && unit0 + u < P.n_units) {
-      for (int o = lt; o < DIM * ND; o += NQ) {
-        const int a = o % ND, c = o / ND;
+      for (int a = lt; a < ND; a += NQ) {
         const int a1 = a % N, a2 = a / N;
-        double acc = 0.0;
+        double val[3];
 #pragma unroll
-        for (int q1 = 0; q1 < Q; ++q1) {
-          acc = __fma_rn(sG[q1 * N + a1], Tb[((0 * DIM + c) * Q + q1) * N + a2], acc);
-          acc = __fma_rn(sB[q1 * N + a1], Tb[((1 * DIM + c) * Q + q1) * N + a2], acc);
+        for (int c = 0; c < DIM; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q1 = 0; q1 < Q; ++q1) {
+            acc = __fma_rn(sG[q1 * N + a1], Tb[((0 * DIM + c) * Q + q1) * N + a2], acc);
+            acc = __fma_rn(sB[q1 * N + a1], Tb[((1 * DIM + c) * Q + q1) * N + a2], acc);
+          }
+          val[c] = acc;
         }
         const int s = P.slot[slot_base + a];
-        if (s >= 0) P.evec[((int64_t)s * DIM + c) * B + b] = acc;
+        if (s >= 0) {
+#pragma unroll
+          for (int c = 0; c < DIM; ++c) P.evec[((int64_t)s * DIM + c) * B + b] = val[c];
+        }
       }
       const int row = P.ftw_row ? P.ftw_row[l] : l;
       if (row >= 0) {
@@ -856,28 +902,22 @@ force_kernel(const Params P) {
       }
     }
   }
+  pdl_trigger();
 }
 
-// dt of the call = min key (NaN if any dt_q was NaN); per-call state is reset for the
-// next call and the NaN condition is folded into the sticky word read by status_sync.
-__device__ __forceinline__ void finalize_one(hydro_devstatus *st, double *dt_out) {
-  double d = key_to_dt(st->dt_key);
-  if (st->nan_flag) {
-    d = __longlong_as_double(0x7ff8000000000000ll);
-    st->nan_sticky = 1u;
-  }
-  if (dt_out) *dt_out = d;
-  st->dt_key = dt_key(__longlong_as_double(0x7ff0000000000000ll));  // +inf
-  st->nan_flag = 0u;
-}
+}  // namespace hk
 
+namespace hk {
 // ----------------------------------------------------------------------------- assembly
+// S5 + S6 completion, launched as a programmatic dependent of the force kernel:
 // F1[c][node] (or F1_rows[(c*n_nodes + node)*B + b]) = sum over the node's slots in
-// ascending order (slots are laid out by ascending element) -- deterministic.
+// ascending order (slots are laid out by ascending element) -- deterministic; then the
+// call's dt is finalised.
 template <int DIM>
 __global__ void assemble_kernel(int64_t n_nodes, int B, const int32_t *__restrict__ off,
                                 const double *__restrict__ evec, double *__restrict__ F1,
                                 hydro_devstatus *st, double *dt_out) {
+  pdl_wait();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n_nodes * B) {
     const int64_t node = B == 1 ? t : t / B;
@@ -890,21 +930,16 @@ __global__ void assemble_kernel(int64_t n_nodes, int B, const int32_t *__restric
       F1[((int64_t)c * n_nodes + node) * B + b] = acc;
     }
   }
-  // dt finalisation (the force kernel finished before this launch started)
   if (blockIdx.x == 0) {
-    for (int i = threadIdx.x; i < B; i += blockDim.x) {
-      finalize_one(st + i, dt_out ? dt_out + i : nullptr);
-    }
+    for (int i = threadIdx.x; i < B; i += blockDim.x) finalize_one(st + i, dt_out ? dt_out + i : nullptr);
   }
 }
 
 __global__ void finalize_dt_kernel(int B, hydro_devstatus *st, double *dt_out) {
+  pdl_wait();
   for (int i = threadIdx.x; i < B; i += blockDim.x) finalize_one(st + i, dt_out ? dt_out + i : nullptr);
 }
 
-}  // namespace hk
-
-namespace hk {
 // ----------------------------------------------------------------------------- self-test
 // Bit-equality of the ieee_fast.cuh fast paths against the IEEE operators on seeded
 // operands (SplitMix64 counter stream).  dist 0: random sign/mantissa, exponent uniform in

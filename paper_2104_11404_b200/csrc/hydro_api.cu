@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/hydro.h"
+#include "force2d.cuh"
 #include "force_kernel.cuh"
 #include "hydro_internal.h"
 #include "rom_kernels.cuh"
@@ -20,7 +21,7 @@ std::atomic<int64_t> g_launches{0};
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t tables, status, mq, off, slot, evec, total;
+  size_t tables, status, mq, off, slot, evec, cnt, total;
 };
 
 bool supported(int dim, int k, int q) {
@@ -45,6 +46,7 @@ bool layout_for(const hydro_mesh_desc *d, Layout *L) {
   L->off = o;    o = align256(o + sizeof(int32_t) * (size_t)(d->n_nodes + 1));
   L->slot = o;   o = align256(o + sizeof(int32_t) * (size_t)(d->n_elem * nd));
   L->evec = o;   o = align256(o + sizeof(double) * (size_t)(d->n_elem * nd * d->dim));
+  L->cnt = o;    o = align256(o + sizeof(uint32_t) * (size_t)(d->n_nodes + 1));  // + done counter
   L->total = o;
   return true;
 }
@@ -84,6 +86,7 @@ struct hydro_ctx {
   double *mq;
   int32_t *off, *slot;
   double *evec;
+  unsigned *cnt;          // [n_nodes] arrival counters, then the CTA done counter
   std::vector<int32_t> h_elem_nodes;  // host copy (sample plans)
 };
 
@@ -95,7 +98,8 @@ struct hydro_sample {
   std::vector<int32_t> h_closure;
   std::vector<int64_t> h_cl_nodes, h_s0_nodes;
   int32_t *elem_nodes = nullptr, *elem_gid = nullptr, *slot = nullptr, *off = nullptr,
-          *ftw_row = nullptr;
+          *ftw_row = nullptr, *anode = nullptr;
+  unsigned *cnt = nullptr;  // [n_s0_nodes][B] arrival counters, then the done counter
   double *evec = nullptr;
   hydro_devstatus *st = nullptr;
 };
@@ -127,10 +131,36 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
   using G = hk::Geo<DIM, K, Q, NF>;
   const int64_t grid = ((int64_t)P.n_units + G::EPB - 1) / G::EPB;
   if (grid <= 0) return HYDRO_OK;
-  auto kern = hk::force_kernel<DIM, K, Q, VISC, MODE, BATCHED, HAS_W>;
+  constexpr bool SPEC2D = DIM == 2 && K == 2 && Q == 4 && MODE != hk::MODE_MQ;
+  using G2 = hk::G2<NF>;
+  void (*kern)(const hk::Params);
+  size_t smem;
+  int nt;
+  int64_t grid2 = grid;
+  if constexpr (SPEC2D) {
+    kern = hk::force2d_kernel<VISC, MODE, BATCHED, HAS_W>;
+    smem = G2::SMEM;
+    nt = G2::NT;
+    // persistent: as many CTAs as fit on the device at once (each loops over rounds)
+    static int resident = 0;
+    if (!resident) {
+      int dev = 0, sms = 0, per_sm = 0;
+      CUDA_OK(cudaGetDevice(&dev));
+      CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2::SMEM));
+      CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G2::NT, G2::SMEM));
+      resident = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    const int64_t rounds = ((int64_t)P.n_units + G2::EPB - 1) / G2::EPB;
+    grid2 = rounds < resident ? rounds : resident;
+  } else {
+    kern = hk::force_kernel<DIM, K, Q, VISC, MODE, BATCHED, HAS_W>;
+    smem = G::SMEM;
+    nt = G::NT;
+  }
   static bool attr_set = false;  // one flag per instantiation
   if (!attr_set) {
-    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
   std::pair<cudaEvent_t, cudaEvent_t> ev;
@@ -139,7 +169,7 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
     ev = prof_pair();
     cudaEventRecord(ev.first, s);
   }
-  kern<<<(unsigned)grid, G::NT, G::SMEM, s>>>(P);
+  kern<<<(unsigned)grid2, nt, smem, s>>>(P);
   g_launches++;
   if (prof) {
     cudaEventRecord(ev.second, s);
@@ -180,18 +210,39 @@ hydro_status launch_force(int dim, int k, int mode, bool visc, bool batched, boo
   return HYDRO_ERR_UNSUPPORTED;
 }
 
+// Dependent launch of the assembly / dt-finalisation kernel with programmatic stream
+// serialisation: it is scheduled while the force kernel drains (griddepcontrol) and waits
+// on-device for the force grid's results, so the second launch's latency is hidden.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 hydro_status launch_assemble(int dim, int64_t n_nodes, int B, const int32_t *off,
                              const double *evec, double *F1, hydro_devstatus *st, double *dt,
                              cudaStream_t s) {
   const int threads = 256;
   int64_t blocks = (n_nodes * B + threads - 1) / threads;
   if (blocks < 1) blocks = 1;
+  cudaError_t e;
   if (dim == 2)
-    hk::assemble_kernel<2><<<(unsigned)blocks, threads, 0, s>>>(n_nodes, B, off, evec, F1, st, dt);
+    e = launch_pdl(hk::assemble_kernel<2>, dim3((unsigned)blocks), dim3(threads), s, n_nodes, B, off,
+                   evec, F1, st, dt);
   else
-    hk::assemble_kernel<3><<<(unsigned)blocks, threads, 0, s>>>(n_nodes, B, off, evec, F1, st, dt);
+    e = launch_pdl(hk::assemble_kernel<3>, dim3((unsigned)blocks), dim3(threads), s, n_nodes, B, off,
+                   evec, F1, st, dt);
   g_launches++;
-  CUDA_OK(cudaGetLastError());
+  CUDA_OK(e);
   return HYDRO_OK;
 }
 
@@ -288,6 +339,7 @@ hydro_status hydro_ctx_create(const hydro_mesh_desc *desc, void *workspace, size
   c->off = (int32_t *)(c->ws + L.off);
   c->slot = (int32_t *)(c->ws + L.slot);
   c->evec = (double *)(c->ws + L.evec);
+  c->cnt = (unsigned *)(c->ws + L.cnt);
   auto fail = [&](hydro_status st) { delete c; return st; };
   // tables
   hydro_tables_t T;
@@ -321,7 +373,8 @@ hydro_status hydro_ctx_create(const hydro_mesh_desc *desc, void *workspace, size
     std::vector<int32_t> pos(off.begin(), off.end() - 1);
     for (int64_t i = 0; i < E * nd; ++i) slot[(size_t)i] = pos[(size_t)c->h_elem_nodes[(size_t)i]]++;
   }
-  if (cudaMemcpyAsync(c->st, &hst, sizeof(hst), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+  if (cudaMemsetAsync(c->cnt, 0, sizeof(uint32_t) * (size_t)(NN + 1), s) != cudaSuccess ||
+      cudaMemcpyAsync(c->st, &hst, sizeof(hst), cudaMemcpyHostToDevice, s) != cudaSuccess ||
       cudaMemcpyAsync(c->off, off.data(), sizeof(int32_t) * (NN + 1), cudaMemcpyHostToDevice, s) !=
           cudaSuccess ||
       cudaMemcpyAsync(c->slot, slot.data(), sizeof(int32_t) * E * nd, cudaMemcpyHostToDevice, s) !=
@@ -370,14 +423,20 @@ static hydro_status force_common(hydro_ctx *c, int mode, const double *x, const 
   P.slot = c->slot;
   P.FTw = FTw;
   P.st = c->st;
+  P.anode = c->d.elem_nodes;  // full mode: assembly nodes are the mesh nodes
+  P.off = c->off;
+  P.cnt = c->cnt;
+  P.done = c->cnt + c->d.n_nodes;
+  P.F1 = F1;
+  P.n_asm = c->d.n_nodes;
+  P.dt_out = dt;
   fill_tables_ptrs(P, c);
   hydro_status r = launch_force(c->d.dim, c->d.order_h1, mode, visc.enabled != 0, false, w != nullptr, P, s);
   if (r != HYDRO_OK) return r;
   if (mode == hk::MODE_FORCE)
     return launch_assemble(c->d.dim, c->d.n_nodes, 1, c->off, c->evec, F1, c->st, dt, s);
-  hk::finalize_dt_kernel<<<1, 32, 0, s>>>(1, c->st, dt);
+  CUDA_OK(launch_pdl(hk::finalize_dt_kernel, dim3(1), dim3(32), s, 1, c->st, dt));
   g_launches++;
-  CUDA_OK(cudaGetLastError());
   return HYDRO_OK;
 }
 
@@ -462,7 +521,8 @@ hydro_status hydro_sample_create(hydro_ctx *c, const int32_t *sample_elems, int6
   p->n_s0_nodes = (int64_t)p->h_s0_nodes.size();
   // local tables; slots (CSR over S0 nodes, ordered by closure element)
   std::vector<int32_t> len((size_t)(p->n_cl * nd)), gid((size_t)p->n_cl), frow((size_t)p->n_cl),
-      slot((size_t)(p->n_cl * nd), -1), off((size_t)p->n_s0_nodes + 1, 0);
+      slot((size_t)(p->n_cl * nd), -1), off((size_t)p->n_s0_nodes + 1, 0),
+      anode((size_t)(p->n_cl * nd), -1);
   for (int64_t l = 0; l < p->n_cl; ++l) {
     const int64_t K = p->h_closure[(size_t)l];
     gid[(size_t)l] = (int32_t)K;
@@ -470,6 +530,7 @@ hydro_status hydro_sample_create(hydro_ctx *c, const int32_t *sample_elems, int6
     for (int a = 0; a < nd; ++a) {
       const int32_t g = en[K * nd + a];
       len[(size_t)(l * nd + a)] = (int32_t)local[(size_t)g];
+      anode[(size_t)(l * nd + a)] = (int32_t)s0local[(size_t)g];
       if (s0local[(size_t)g] >= 0) off[(size_t)s0local[(size_t)g] + 1]++;
     }
   }
@@ -492,7 +553,10 @@ hydro_status hydro_sample_create(hydro_ctx *c, const int32_t *sample_elems, int6
       cudaMalloc(&p->slot, sizeof(int32_t) * slot.size()) != cudaSuccess ||
       cudaMalloc(&p->off, sizeof(int32_t) * off.size()) != cudaSuccess ||
       cudaMalloc(&p->evec, evec_bytes > 0 ? evec_bytes : 8) != cudaSuccess ||
-      cudaMalloc(&p->st, sizeof(hydro_devstatus) * B) != cudaSuccess)
+      cudaMalloc(&p->st, sizeof(hydro_devstatus) * B) != cudaSuccess ||
+      cudaMalloc(&p->anode, sizeof(int32_t) * anode.size()) != cudaSuccess ||
+      cudaMalloc(&p->cnt, sizeof(uint32_t) * (size_t)(p->n_s0_nodes * B + 1)) != cudaSuccess ||
+      cudaMemset(p->cnt, 0, sizeof(uint32_t) * (size_t)(p->n_s0_nodes * B + 1)) != cudaSuccess)
     return fail(HYDRO_ERR_CUDA);
   std::vector<hydro_devstatus> hst((size_t)B);
   for (auto &h : hst) { h.dt_key = 0xFFF0000000000000ull; h.first_bad = ~0ull; h.nan_flag = 0; h.nan_sticky = 0; }
@@ -501,6 +565,7 @@ hydro_status hydro_sample_create(hydro_ctx *c, const int32_t *sample_elems, int6
       cudaMemcpy(p->ftw_row, frow.data(), sizeof(int32_t) * frow.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(p->slot, slot.data(), sizeof(int32_t) * slot.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(p->off, off.data(), sizeof(int32_t) * off.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->anode, anode.data(), sizeof(int32_t) * anode.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(p->st, hst.data(), sizeof(hydro_devstatus) * B, cudaMemcpyHostToDevice) != cudaSuccess)
     return fail(HYDRO_ERR_CUDA);
   *out = p;
@@ -510,7 +575,7 @@ hydro_status hydro_sample_create(hydro_ctx *c, const int32_t *sample_elems, int6
 hydro_status hydro_sample_destroy(hydro_sample *p) {
   if (!p) return HYDRO_OK;
   cudaFree(p->elem_nodes); cudaFree(p->elem_gid); cudaFree(p->ftw_row); cudaFree(p->slot);
-  cudaFree(p->off); cudaFree(p->evec); cudaFree(p->st);
+  cudaFree(p->off); cudaFree(p->evec); cudaFree(p->st); cudaFree(p->anode); cudaFree(p->cnt);
   delete p;
   return HYDRO_OK;
 }
@@ -559,8 +624,16 @@ hydro_status hydro_force_sampled(hydro_sample *p, const double *x_S, const doubl
   P.FTw = FTw_rows;
   P.ftw_row = p->ftw_row;
   P.st = p->st;
+  P.anode = p->anode;
+  P.off = p->off;
+  P.cnt = p->cnt;
+  P.done = p->cnt + p->n_s0_nodes * p->B;
+  P.F1 = F1_rows;
+  P.n_asm = p->n_s0_nodes;
+  P.dt_out = dt;
   fill_tables_ptrs(P, c);
-  hydro_status r = launch_force(c->d.dim, c->d.order_h1, hk::MODE_FORCE, visc.enabled != 0, p->B > 1, w_S != nullptr, P, s);
+  hydro_status r = launch_force(c->d.dim, c->d.order_h1, hk::MODE_FORCE, visc.enabled != 0, p->B > 1,
+                                w_S != nullptr, P, s);
   if (r != HYDRO_OK) return r;
   return launch_assemble(c->d.dim, p->n_s0_nodes, p->B, p->off, p->evec, F1_rows, p->st, dt, s);
 }

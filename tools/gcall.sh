@@ -11,7 +11,7 @@ timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest.log 2>&1; echo "pyt
 timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench.json 2> $O/bench.err; echo "bench rc=$?" >> $O/rc.txt
 for w in "$@"; do
   timeout 300 python tools/prof_case.py $w --iters 3 > $O/p_$w.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:force_kernel -s 2 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:force -s 2 -c 1 \
      -o $O/${w}_full python tools/prof_case.py $w --iters 3 > $O/ncu_$w.log 2>&1
   echo "ncu $w rc=$?" >> $O/rc.txt
 done
