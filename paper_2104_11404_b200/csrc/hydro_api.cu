@@ -141,18 +141,7 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
     kern = hk::force2d_kernel<VISC, MODE, BATCHED, HAS_W>;
     smem = G2::SMEM;
     nt = G2::NT;
-    // persistent: as many CTAs as fit on the device at once (each loops over rounds)
-    static int resident = 0;
-    if (!resident) {
-      int dev = 0, sms = 0, per_sm = 0;
-      CUDA_OK(cudaGetDevice(&dev));
-      CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2::SMEM));
-      CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G2::NT, G2::SMEM));
-      resident = sms * (per_sm > 0 ? per_sm : 1);
-    }
-    const int64_t rounds = ((int64_t)P.n_units + G2::EPB - 1) / G2::EPB;
-    grid2 = rounds < resident ? rounds : resident;
+    grid2 = ((int64_t)P.n_units + G2::NT - 1) / G2::NT;  // one thread per unit
   } else {
     kern = hk::force_kernel<DIM, K, Q, VISC, MODE, BATCHED, HAS_W>;
     smem = G::SMEM;
@@ -346,6 +335,13 @@ hydro_status hydro_ctx_create(const hydro_mesh_desc *desc, void *workspace, size
   if (hydro_make_tables(desc->order_h1, desc->nq1d, &T)) return fail(HYDRO_ERR_ARG);
   std::vector<double> packed;
   pack_tables(T, packed);
+  if (desc->order_h1 == 2 && desc->nq1d == 4) {
+    // __constant__ copy for the one-thread-per-element 2D kernel (same packed order)
+    static_assert(sizeof(hk::Tab24) == sizeof(double) * (4 + 12 + 12 + 8), "Tab24 layout");
+    if (cudaMemcpyToSymbolAsync(hk::c_t24, packed.data(), sizeof(hk::Tab24), 0,
+                                cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return fail(HYDRO_ERR_CUDA);
+  }
   if (cudaMemcpyAsync(c->tab, packed.data(), sizeof(double) * HYDRO_TAB_DOUBLES, cudaMemcpyHostToDevice, s) !=
       cudaSuccess)
     return fail(HYDRO_ERR_CUDA);
