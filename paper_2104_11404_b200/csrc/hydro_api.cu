@@ -10,6 +10,7 @@
 
 #include "../../include/hydro.h"
 #include "force2d.cuh"
+#include "force3d.cuh"
 #include "force_kernel.cuh"
 #include "hydro_internal.h"
 #include "rom_kernels.cuh"
@@ -132,6 +133,10 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
   const int64_t grid = ((int64_t)P.n_units + G::EPB - 1) / G::EPB;
   if (grid <= 0) return HYDRO_OK;
   constexpr bool SPEC2D = DIM == 2 && K == 2 && Q == 4 && MODE != hk::MODE_MQ;
+  // the persistent 3D kernel wins for Q2 (C2, C4); for Q3 (224-thread CTAs) its 80-register
+  // budget spills and barrier waits grow, so Q3 keeps the one-element-per-CTA kernel
+  constexpr bool SPEC3D = DIM == 3 && K == 2 && MODE != hk::MODE_MQ;
+  using G3 = hk::G3<K, Q, NF>;
   using G2 = hk::G2<NF>;
   void (*kern)(const hk::Params);
   size_t smem;
@@ -142,16 +147,29 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
     smem = G2::SMEM;
     nt = G2::NT;
     grid2 = ((int64_t)P.n_units + G2::NT - 1) / G2::NT;  // one thread per unit
+  } else if constexpr (SPEC3D) {
+    kern = hk::force3d_kernel<K, Q, VISC, MODE, BATCHED, HAS_W>;
+    smem = G3::SMEM;
+    nt = G3::NT;
   } else {
     kern = hk::force_kernel<DIM, K, Q, VISC, MODE, BATCHED, HAS_W>;
     smem = G::SMEM;
     nt = G::NT;
   }
   static bool attr_set = false;  // one flag per instantiation
+  static int resident = 0;       // persistent 3D kernel: CTAs resident on the device
   if (!attr_set) {
     CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (SPEC3D) {
+      int dev = 0, sms = 0, per_sm = 0;
+      CUDA_OK(cudaGetDevice(&dev));
+      CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
+      resident = sms * (per_sm > 0 ? per_sm : 1);
+    }
     attr_set = true;
   }
+  if (SPEC3D) grid2 = P.n_units < resident ? P.n_units : resident;
   std::pair<cudaEvent_t, cudaEvent_t> ev;
   const bool prof = g_prof.on && MODE != hk::MODE_MQ;
   if (prof) {
