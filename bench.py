@@ -54,23 +54,44 @@ def contraction_flops(dim, k, q, nfield=2, visc=True):
     return 2 * macs
 
 
-def pointwise_ops(dim, visc, rot_per_lmin3):
-    """(flops, div+sqrt count) of the contract pointwise stage per qp (DESIGN A.3/A.4)."""
+# FP64-pipe instruction cost of the IEEE operations on sm_100a, from the fast paths the
+# kernels issue (csrc/ieee_fast.cuh, identical to nvcc's): a/b = 5 DFMA + DMUL + 2 DFMA,
+# sqrt = 3 DMUL + 5 DFMA, 1/b = 5 DFMA (the MUFU seeds run on the XU pipe).
+DIV_I, SQRT_I, RCP_I = 8, 8, 5
+ROT_I = 2 + 3 + SQRT_I + 1 + DIV_I + 2 + SQRT_I + RCP_I + 1 + 10   # one Jacobi rotation (A.4) = 48
+
+
+def pointwise_instr(dim, visc, rot_per_lmin3):
+    """FP64-pipe instructions of the contract pointwise stage per quadrature point
+    (DESIGN A.3/A.4 as the kernels evaluate it; mul, add and fma count 1 each).
+    rot_per_lmin3: executed (non-skipped) Jacobi rotations per 3x3 eigen-solve."""
     if dim == 3:
-        flops, ds = 42 + 3 + 3 + 30 + 2 + 4 + 12, 5 + 2     # det/inv, rho, p, cs, J^T J, den, inv_dt, sigma
-        lm = lambda r: (6 + 19 * r + (12 - r) + 2, 4 * r)
-        f, d = lm(rot_per_lmin3)
-        flops += f; ds += d
+        n = 27 + 5 + RCP_I + 9                   # cofactors, det, 1/det, J^-1
+        n += DIV_I + 3 + 3 + SQRT_I              # rho, p, cs
+        n += 30 + 1 + ROT_I * rot_per_lmin3 + SQRT_I   # J^T J, lmin3 (tol), h
         if visc:
-            flops += 45 + 6 + 6
-            f, d = lm(rot_per_lmin3)
-            flops += f; ds += d
+            n += 45 + 6                          # grad v, eps
+            n += 1 + ROT_I * rot_per_lmin3       # lmin3(eps)
+            n += 5 + 1 + DIV_I + 1 + DIV_I + 1   # mu, den, cs/h, alpha_mu mu, / den, +
+            n += 12 + 10                         # sigma, A = sigma : eps
+        else:
+            n += 17 + 1 + DIV_I + 1 + 2          # tr grad v, den, cs/h, +, A
+        n += DIV_I                               # dt_q
+        n += 36 + 1 + 2                          # S = w detJ sigma J^-T, w detJ, w_q
     else:
-        flops, ds = 8 + 3 + 3 + 12 + 2 + 4 + 6, 6 + 3
+        n = 3 + RCP_I + 4                        # det, 1/det, J^-1
+        n += DIV_I + 3 + 3 + SQRT_I              # rho, p, cs
+        n += 9 + 2 + 3 + SQRT_I + 2 + 1 + SQRT_I + DIV_I   # h = det / sigma_max(J)
         if visc:
-            flops += 12 + 3 + 8 + 6
-            ds += 1
-    return flops, ds
+            n += 12 + 2                          # grad v, eps
+            n += 2 + 3 + SQRT_I + 2 + 1          # lambda_min(eps)
+            n += 5 + 2 + DIV_I + 1 + DIV_I + 1   # mu, den, cs/h, alpha_mu mu, / den, +
+            n += 6 + 5                           # sigma, A
+        else:
+            n += 7 + 2 + DIV_I + 1 + 2           # tr grad v, den, cs/h, +, A
+        n += DIV_I                               # dt_q
+        n += 12 + 1 + 1                          # S, w detJ, w_q
+    return n
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -128,7 +149,6 @@ def measured_peaks():
 # FP64 pipe peak: DFMA microbenchmark on this pool's B200 (tools/microbench/fp64_peak.cu,
 # profiles/r01_fp64_peak.txt): 34.2 TFLOP/s sustained; IEEE div 1.43e12/s, sqrt 1.29e12/s.
 FP64_PEAK_TFLOPS = 34.2
-DIVSQRT_WEIGHT = 24.0     # flop-equivalents of one IEEE FP64 div/sqrt on the FP64 pipe (12 DFMA slots)
 
 
 # ----------------------------------------------------------------------------- workloads
@@ -318,12 +338,16 @@ def _rotations_per_lmin3(name, prob):
 
 
 def roofline(name, base, m, n_units, kern_ms, prob):
+    """Roofline of the force kernel.  It is bound by the FP64 pipe (arithmetic intensity
+    ~50 flop/B, DESIGN "Kernels"), so the work is counted in FP64-pipe instructions of the
+    algorithm (contraction multiply-adds + the contract's pointwise operations, IEEE
+    div/sqrt/rcp at their instruction cost) and reported as DFMA-equivalent TFLOP/s
+    (2 per instruction) against the measured DFMA peak."""
     rot = _rotations_per_lmin3(name, prob)
     nq = m.nq ** m.dim
-    cflops = contraction_flops(m.dim, m.k, m.nq)
-    pf, pds = pointwise_ops(m.dim, base.visc, rot)
-    nominal = n_units * (cflops + nq * (pf + pds))
-    weighted = n_units * (cflops + nq * (pf + DIVSQRT_WEIGHT * pds))
+    c_instr = contraction_flops(m.dim, m.k, m.nq) // 2
+    p_instr = pointwise_instr(m.dim, base.visc, rot)
+    instr = n_units * (c_instr + nq * p_instr)
     # algorithmic bytes: x, v [N_V], e [N_E], m_q [Q], elem_nodes, gamma; write F1 [N_V], FTw [N_E]
     if name == "c4":
         B = prob.B
@@ -336,41 +360,57 @@ def roofline(name, base, m, n_units, kern_ms, prob):
         byts = (8 * (2 * m.N_V + m.N_E + m.n_elem * nq + m.n_elem) + 4 * m.n_elem * m.nd
                 + 8 * (m.N_V + m.N_E))
     t = kern_ms * 1e-3
-    ach = weighted / t / 1e12
+    ach = 2.0 * instr / t / 1e12
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6650.0)
+    traffic = measured_traffic(name)
     return {"bound": "alu", "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": None,
-            "kernel": "force_kernel", "flops_weighted_per_launch": weighted,
-            "flops_nominal_per_launch": nominal, "divsqrt_weight": DIVSQRT_WEIGHT,
+            "frac": round(ach / FP64_PEAK_TFLOPS, 4),
+            "traffic": traffic["bytes_per_launch"] if traffic else None,
+            "kernel": "force kernel (hydro_force_full / hydro_force_sampled)",
+            "fp64_instr_per_launch": instr, "flop_eq_per_instr": 2,
+            "contraction_instr_per_unit": c_instr, "pointwise_instr_per_qp": p_instr,
             "rotations_per_lmin3": round(rot, 3),
             "hbm_bytes_alg": byts, "hbm_frac": round(byts / t / 1e9 / hbm, 4),
-            "peak_source": "FP64 DFMA microbenchmark on B200 (profiles/r01_fp64_peak.txt); "
-                           "HBM from MEASURED_PEAKS.json"}
+            "traffic_source": traffic["source"] if traffic else None,
+            "peak_source": "FP64 DFMA microbenchmark on B200, sustained "
+                           "(profiles/r01_fp64_peak.txt); HBM from MEASURED_PEAKS.json"}
+
+
+def measured_traffic(name):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the force kernel for this workload
+    from the latest committed ncu --set full capture (profiles/traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    return json.load(open(p)).get(name)
 
 
 # ----------------------------------------------------------------------------- cpu baseline
 def cpu_baseline(name, target_s=12.0):
-    """The oracle as it stands, on a bounded seeded sample of the workload's elements."""
+    """The oracle as it stands (oracle/, OpenMP over the host cores) on a bounded seeded
+    sample of the workload: a random subset of elements, or the whole mesh repeated, sized
+    to ~target_s seconds of CPU work.  Quadrature points processed / wall time."""
     import oracle
     prob = build_problem(name) if name != "c4" else build_problem("c2")
     m = prob.mesh
     nq = m.nq ** m.dim
     cores = os.cpu_count() or 1
     rng = np.random.default_rng(1)
-    n = min(m.n_elem, 256)
-    el = np.sort(rng.choice(m.n_elem, n, replace=False)).astype(np.int32)
-    t0 = time.perf_counter()
-    oracle.force(prob, elist=el)
-    dt1 = time.perf_counter() - t0
-    n2 = int(min(m.n_elem, max(n, n * target_s / max(dt1, 1e-3))))
+    oracle.force(prob, elist=np.arange(min(m.n_elem, 8), dtype=np.int32))  # tables, threads
+    n2 = int(min(m.n_elem, 16384 if m.dim == 3 else 65536))
     el = np.sort(rng.choice(m.n_elem, n2, replace=False)).astype(np.int32)
-    t0 = time.perf_counter()
-    oracle.force(prob, elist=el)
-    wall = time.perf_counter() - t0
-    return {"value": n2 * nq / wall, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{n2} of {m.n_elem} elements of {name} ({n2 * nq} quad points), F.1+F^T.v+dt, "
-                      f"OpenMP over {cores} host threads, {wall:.1f} s"}
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.force(prob, elist=el)
+        reps += 1
+        wall = time.perf_counter() - t0
+        if wall >= target_s:
+            break
+    return {"value": reps * n2 * nq / wall, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n2} seeded elements of {name} ({m.n_elem} in the mesh) evaluated "
+                      f"{reps}x = {reps * n2 * nq} quad points, F.1+F^T.v+dt, OpenMP over "
+                      f"{cores} host threads, {wall:.1f} s"}
 
 
 # ----------------------------------------------------------------------------- main
