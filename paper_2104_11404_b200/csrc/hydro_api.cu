@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -138,27 +139,35 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
   constexpr bool SPEC3D = DIM == 3 && K == 2 && MODE != hk::MODE_MQ;
   using G3 = hk::G3<K, Q, NF>;
   using G2 = hk::G2<NF>;
-  void (*kern)(const hk::Params);
-  size_t smem;
-  int nt;
+  // one-thread-per-element 2D kernel only when there are enough elements to fill the GPU;
+  // small meshes (C0: 64 elements) run the point-per-thread kernel (16x the threads)
+  // (HYDRO_2D_KERNEL=element|point overrides the choice; the tests run both paths)
+  bool use2d = SPEC2D && P.n_units >= 148 * G2::NT * 2;
+  if (SPEC2D) {
+    const char *env = getenv("HYDRO_2D_KERNEL");
+    if (env && !strcmp(env, "element")) use2d = true;
+    if (env && !strcmp(env, "point")) use2d = false;
+  }
+  void (*kern)(const hk::Params) = hk::force_kernel<DIM, K, Q, VISC, MODE, BATCHED, HAS_W>;
+  size_t smem = G::SMEM;
+  int nt = G::NT;
   int64_t grid2 = grid;
   if constexpr (SPEC2D) {
-    kern = hk::force2d_kernel<VISC, MODE, BATCHED, HAS_W>;
-    smem = G2::SMEM;
-    nt = G2::NT;
-    grid2 = ((int64_t)P.n_units + G2::NT - 1) / G2::NT;  // one thread per unit
+    if (use2d) {
+      kern = hk::force2d_kernel<VISC, MODE, BATCHED, HAS_W>;
+      smem = G2::SMEM;
+      nt = G2::NT;
+      grid2 = ((int64_t)P.n_units + G2::NT - 1) / G2::NT;  // one thread per unit
+    }
   } else if constexpr (SPEC3D) {
     kern = hk::force3d_kernel<K, Q, VISC, MODE, BATCHED, HAS_W>;
     smem = G3::SMEM;
     nt = G3::NT;
-  } else {
-    kern = hk::force_kernel<DIM, K, Q, VISC, MODE, BATCHED, HAS_W>;
-    smem = G::SMEM;
-    nt = G::NT;
   }
-  static bool attr_set = false;  // one flag per instantiation
-  static int resident = 0;       // persistent 3D kernel: CTAs resident on the device
-  if (!attr_set) {
+  static bool attr_set[2] = {false, false};  // per instantiation: [generic/2D-or-3D kernel]
+  static int resident = 0;                    // persistent 3D kernel: CTAs resident on the device
+  const int which = (use2d || SPEC3D) ? 1 : 0;
+  if (!attr_set[which]) {
     CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (SPEC3D) {
       int dev = 0, sms = 0, per_sm = 0;
@@ -167,7 +176,7 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
       CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
       resident = sms * (per_sm > 0 ? per_sm : 1);
     }
-    attr_set = true;
+    attr_set[which] = true;
   }
   if (SPEC3D) grid2 = P.n_units < resident ? P.n_units : resident;
   std::pair<cudaEvent_t, cudaEvent_t> ev;
