@@ -54,8 +54,9 @@ struct G3 {
   static constexpr int TABD = G::TABD;
   static constexpr int WORK = G::WORK;
   static constexpr size_t SMEM = sizeof(double) * (size_t)(TABD + 2 * XE + WORK);
-  // occupancy target (registers): ~96/thread for Q=4 (10 CTAs of 64), ~96 for Q=6 (3 x 224)
-  static constexpr int MINB = NT >= 224 ? 3 : 10;
+  // occupancy target (registers): ~96/thread for Q=4 (10 CTAs of 64); Q=6: 2 x 224 threads
+  // (~144 registers: the 3 x 224 budget of 80 registers spilled heavily)
+  static constexpr int MINB = NT >= 224 ? 2 : 10;
 };
 
 template <int K, int Q, bool VISC, int MODE, bool BATCHED, bool HAS_W>

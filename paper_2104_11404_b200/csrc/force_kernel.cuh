@@ -179,15 +179,36 @@ __device__ __forceinline__ void lmin3_pair(AR &ar, double a00, double a11, doubl
 #pragma unroll 1
   for (int sweep = 0; sweep < 4; ++sweep) {
     if (EARLY) {
-      const bool live = offdiag_live(a01, a02, a12, ta) || offdiag_live(e01, e02, e12, te);
-      if (!__any_sync(0xffffffffu, live)) break;
+      // warp-uniform scheduling: a rotation slot of a matrix is executed only if some lane
+      // needs it (skipped lanes keep their entries), and the two matrices' rotations are
+      // interleaved only when both are live -- a converged matrix costs nothing
+      const bool la = offdiag_live(a01, a02, a12, ta), le = offdiag_live(e01, e02, e12, te);
+      const bool wa = __any_sync(0xffffffffu, la), we = __any_sync(0xffffffffu, le);
+      if (!(wa || we)) break;
+      if (wa && we) {
+        jacobi_rot(ar, a00, a11, a01, a02, a12, ta);  // (0,1), r3 = 2
+        jacobi_rot(ar, e00, e11, e01, e02, e12, te);
+        jacobi_rot(ar, a00, a22, a02, a01, a12, ta);  // (0,2), r3 = 1
+        jacobi_rot(ar, e00, e22, e02, e01, e12, te);
+        jacobi_rot(ar, a11, a22, a12, a01, a02, ta);  // (1,2), r3 = 0
+        jacobi_rot(ar, e11, e22, e12, e01, e02, te);
+      } else if (wa) {
+        jacobi_rot(ar, a00, a11, a01, a02, a12, ta);
+        jacobi_rot(ar, a00, a22, a02, a01, a12, ta);
+        jacobi_rot(ar, a11, a22, a12, a01, a02, ta);
+      } else {
+        jacobi_rot(ar, e00, e11, e01, e02, e12, te);
+        jacobi_rot(ar, e00, e22, e02, e01, e12, te);
+        jacobi_rot(ar, e11, e22, e12, e01, e02, te);
+      }
+    } else {
+      jacobi_rot(ar, a00, a11, a01, a02, a12, ta);  // (0,1), r3 = 2
+      jacobi_rot(ar, e00, e11, e01, e02, e12, te);
+      jacobi_rot(ar, a00, a22, a02, a01, a12, ta);  // (0,2), r3 = 1
+      jacobi_rot(ar, e00, e22, e02, e01, e12, te);
+      jacobi_rot(ar, a11, a22, a12, a01, a02, ta);  // (1,2), r3 = 0
+      jacobi_rot(ar, e11, e22, e12, e01, e02, te);
     }
-    jacobi_rot(ar, a00, a11, a01, a02, a12, ta);  // (0,1), r3 = 2
-    jacobi_rot(ar, e00, e11, e01, e02, e12, te);
-    jacobi_rot(ar, a00, a22, a02, a01, a12, ta);  // (0,2), r3 = 1
-    jacobi_rot(ar, e00, e22, e02, e01, e12, te);
-    jacobi_rot(ar, a11, a22, a12, a01, a02, ta);  // (1,2), r3 = 0
-    jacobi_rot(ar, e11, e22, e12, e01, e02, te);
   }
   la = fmin(fmin(a00, a11), a22);
   le = fmin(fmin(e00, e11), e22);

@@ -136,7 +136,13 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
   constexpr bool SPEC2D = DIM == 2 && K == 2 && Q == 4 && MODE != hk::MODE_MQ;
   // the persistent 3D kernel wins for Q2 (C2, C4); for Q3 (224-thread CTAs) its 80-register
   // budget spills and barrier waits grow, so Q3 keeps the one-element-per-CTA kernel
-  constexpr bool SPEC3D = DIM == 3 && K == 2 && MODE != hk::MODE_MQ;
+  constexpr bool SPEC3D_OK = DIM == 3 && MODE != hk::MODE_MQ;
+  bool use3d = SPEC3D_OK && K == 2;  // (HYDRO_3D_KERNEL=persistent|element overrides)
+  if (SPEC3D_OK) {
+    const char *env = getenv("HYDRO_3D_KERNEL");
+    if (env && !strcmp(env, "persistent")) use3d = true;
+    if (env && !strcmp(env, "element")) use3d = false;
+  }
   using G3 = hk::G3<K, Q, NF>;
   using G2 = hk::G2<NF>;
   // one-thread-per-element 2D kernel only when there are enough elements to fill the GPU;
@@ -159,17 +165,19 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
       nt = G2::NT;
       grid2 = ((int64_t)P.n_units + G2::NT - 1) / G2::NT;  // one thread per unit
     }
-  } else if constexpr (SPEC3D) {
-    kern = hk::force3d_kernel<K, Q, VISC, MODE, BATCHED, HAS_W>;
-    smem = G3::SMEM;
-    nt = G3::NT;
+  } else if constexpr (SPEC3D_OK) {
+    if (use3d) {
+      kern = hk::force3d_kernel<K, Q, VISC, MODE, BATCHED, HAS_W>;
+      smem = G3::SMEM;
+      nt = G3::NT;
+    }
   }
   static bool attr_set[2] = {false, false};  // per instantiation: [generic/2D-or-3D kernel]
   static int resident = 0;                    // persistent 3D kernel: CTAs resident on the device
-  const int which = (use2d || SPEC3D) ? 1 : 0;
+  const int which = (use2d || use3d) ? 1 : 0;
   if (!attr_set[which]) {
     CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (SPEC3D) {
+    if (use3d) {
       int dev = 0, sms = 0, per_sm = 0;
       CUDA_OK(cudaGetDevice(&dev));
       CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -178,7 +186,7 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
     }
     attr_set[which] = true;
   }
-  if (SPEC3D) grid2 = P.n_units < resident ? P.n_units : resident;
+  if (use3d) grid2 = P.n_units < resident ? P.n_units : resident;
   std::pair<cudaEvent_t, cudaEvent_t> ev;
   const bool prof = g_prof.on && MODE != hk::MODE_MQ;
   if (prof) {
