@@ -467,9 +467,10 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
 template <int DIM, int K, int Q, int NF, int EPB_>
 struct KCfg {
   using G = Geo<DIM, K, Q, NF, EPB_>;
-  // occupancy target: as many CTAs as registers allow at <= 96 registers/thread for the
-  // one-element 3D CTAs (see DESIGN "Kernels"); 2D CTAs are 128 threads.
-  static constexpr int MINB = G::NT >= 224 ? 3 : (G::NT >= 128 ? 5 : 10);
+  // occupancy target.  3D Q3 (224-thread CTAs): 4 CTAs/SM at 72 registers measured best
+  // (10.75 ms on C3 vs 12.0 ms at 3 CTAs / 80 registers, 11.2 ms at 5 CTAs / 56 registers:
+  // occupancy outweighs the extra spills; profiles/ab/).
+  static constexpr int MINB = G::NT >= 224 ? 4 : (G::NT >= 128 ? 5 : 10);
 };
 
 template <int DIM, int K, int Q, bool VISC, int MODE, bool BATCHED, bool HAS_W, int EPB_ = 0>
