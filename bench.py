@@ -294,31 +294,108 @@ def bench_one(name, args, dev, flush, rank, world):
                force_kernel_share=kern_avg / ms if ms > 0 else None,
                gpu_launches=launches, timing="CUDA-graph replay of the step, CUDA events",
                clocks=clk.summary())
-    # end to end through the public API with host buffers (pinned), c0..c3
+    # end to end through the public API with host buffers (pinned): every step copies its
+    # inputs host->device, runs the hot path and copies its results device->host.  Steps
+    # are software-pipelined over three streams with double-buffered device and host
+    # tensors (step i+1's upload and step i-1's download overlap step i's compute), as a
+    # serving loop would; the timed region spans the first upload to the last download.
     if name != "c4":
-        hx = torch.as_tensor(prob.x).pin_memory(); hv = torch.as_tensor(prob.v).pin_memory()
-        he = torch.as_tensor(prob.e).pin_memory(); hg = torch.as_tensor(base.gamma).pin_memory()
-        oF1 = torch.empty(F1.shape, dtype=torch.float64).pin_memory()
-        oFT = torch.empty(FTw.shape, dtype=torch.float64).pin_memory()
-        odt = torch.empty(1, dtype=torch.float64).pin_memory()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        for it in range(args.warmup + args.steps):
-            if it == args.warmup:
-                torch.cuda.synchronize(); e0.record()
-            x.copy_(hx, non_blocking=True); v.copy_(hv, non_blocking=True)
-            e.copy_(he, non_blocking=True); gamma.copy_(hg, non_blocking=True)
-            step()
-            oF1.copy_(F1, non_blocking=True); oFT.copy_(FTw, non_blocking=True)
-            odt.copy_(dt, non_blocking=True)
-        e1.record(); torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1) / args.steps
-        h2d = sum(t.numel() * 8 for t in (hx, hv, he, hg))
-        d2h = sum(t.numel() * 8 for t in (oF1, oFT, odt))
-        out["e2e"] = {"value": n_qp / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                      "d2h_bytes_per_step": d2h, "ms_per_step": ems}
+        out["e2e"] = e2e_full(ctx, prob, base, visc, cfl, n_qp, args, dev)
+    else:
+        out["e2e"] = e2e_rom(step_inputs=(Yx, Yv, Ye), step_outputs=(rv, re_, rx, dt), step=step,
+                             n_qp=n_qp, args=args)
     # roofline of the dominant kernel (force kernel)
     out["roofline"] = roofline(name, base, m, n_units, kern_avg, prob)
     return out
+
+
+def e2e_full(ctx, prob, base, visc, cfl, n_qp, args, dev):
+    import torch
+    m = base.mesh
+    host_in = [torch.as_tensor(np.ascontiguousarray(a)).pin_memory()
+               for a in (prob.x, prob.v, prob.e, base.gamma)]
+    dbuf, hout = [], []
+    for _ in range(2):
+        dbuf.append(dict(inp=[torch.empty_like(h, device=dev) for h in host_in],
+                         F1=torch.empty((m.dim, m.n_nodes), dtype=torch.float64, device=dev),
+                         FTw=torch.empty((m.n_elem, m.ne), dtype=torch.float64, device=dev),
+                         dt=torch.empty(1, dtype=torch.float64, device=dev)))
+        hout.append([torch.empty((m.dim, m.n_nodes), dtype=torch.float64).pin_memory(),
+                     torch.empty((m.n_elem, m.ne), dtype=torch.float64).pin_memory(),
+                     torch.empty(1, dtype=torch.float64).pin_memory()])
+    s_in, s_cp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    ev = lambda: torch.cuda.Event()
+    in_done = [ev(), ev()]; cp_done = [ev(), ev()]; out_done = [ev(), ev()]
+    for e_ in out_done + cp_done:
+        e_.record(torch.cuda.current_stream())
+
+    def run(n):
+        for it in range(n):
+            k = it & 1
+            b = dbuf[k]
+            with torch.cuda.stream(s_in):
+                s_in.wait_event(cp_done[k])          # step it-2 finished reading inputs k
+                for d, h in zip(b["inp"], host_in):
+                    d.copy_(h, non_blocking=True)
+                in_done[k].record(s_in)
+            with torch.cuda.stream(s_cp):
+                s_cp.wait_event(in_done[k])
+                s_cp.wait_event(out_done[k])         # step it-2's download of outputs k done
+                x, v, e, g = b["inp"]
+                ctx.force_full(x, v, e, g, visc, cfl, F1=b["F1"], FTw=b["FTw"], dt=b["dt"])
+                cp_done[k].record(s_cp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(cp_done[k])
+                for h, d in zip(hout[k], (b["F1"], b["FTw"], b["dt"])):
+                    h.copy_(d, non_blocking=True)
+                out_done[k].record(s_out)
+
+    run(args.warmup)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s_in)
+    run(args.steps)
+    for s_ in (s_in, s_cp):
+        s_out.wait_stream(s_)
+    e1.record(s_out)
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1) / args.steps
+    st = ctx.status_sync()
+    if st[0] != 0:
+        raise RuntimeError(f"e2e: device status {st}")
+    h2d = sum(t.numel() * 8 for t in host_in)
+    d2h = sum(t.numel() * 8 for t in hout[0])
+    return {"value": n_qp / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ems,
+            "method": "public API (hydro_force_full) with pinned host buffers; uploads, "
+                      "compute and downloads of consecutive steps overlapped on 3 streams"}
+
+
+def e2e_rom(step_inputs, step_outputs, step, n_qp, args):
+    """C4: the step's inputs are the reduced coordinates (Yhat_x, Yhat_v, Yhat_e), its
+    results the reduced right-hand sides (r_v, r_e, r_x) and dt per instance."""
+    import torch
+    host_in = [t.cpu().pin_memory() for t in step_inputs]
+    host_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in step_outputs]
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        for d, h in zip(step_inputs, host_in):
+            d.copy_(h, non_blocking=True)
+        step()
+        for h, d in zip(host_out, step_outputs):
+            h.copy_(d, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1) / args.steps
+    return {"value": n_qp / (ems * 1e-3), "unit": UNIT,
+            "h2d_bytes_per_step": sum(t.numel() * t.element_size() for t in host_in),
+            "d2h_bytes_per_step": sum(t.numel() * t.element_size() for t in host_out),
+            "ms_per_step": ems,
+            "method": "public API (lift, force_sampled, project) with pinned host buffers"}
 
 
 def _rotations_per_lmin3(name, prob):
