@@ -272,10 +272,7 @@ def bench_one(name, args, dev, flush, rank, world):
         raise RuntimeError(f"{name}: device status {st} after the timed region")
     step_ms = [a.elapsed_time(b) for a, b in evs]
     ms = sum(step_ms) / len(step_ms)
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, dev, world)
     # dominant-kernel time: a separate eager pass of K steps with the library's CUDA events
     # around the force kernel on the launching stream (not mixed into the step timing)
     hydro.profile_enable(True)
@@ -307,6 +304,24 @@ def bench_one(name, args, dev, flush, rank, world):
     # roofline of the dominant kernel (force kernel)
     out["roofline"] = roofline(name, base, m, n_units, kern_avg, prob)
     return out
+
+
+def max_over_ranks(value, dev, world):
+    """Max of a per-rank time over all ranks (the bench reports the slowest replica).
+    dev: the rank's device (CUDA under NCCL, CPU under gloo)."""
+    if world <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_value(per_rank_units, ms_max, world):
+    """Whole-job throughput: units processed by all ranks / the slowest rank's time
+    (weak scaling: every rank processes the full workload)."""
+    return per_rank_units * world / (ms_max * 1e-3)
 
 
 def e2e_full(ctx, prob, base, visc, cfl, n_qp, args, dev):
@@ -536,7 +551,8 @@ def main():
     head = res[args.workload]
     if rank == 0:
         line = {
-            "metric": METRIC, "value": head["qp_per_s"] * world, "unit": UNIT, "n_gpus": world,
+            "metric": METRIC, "value": whole_job_value(head["n_qp"], head["ms_per_step"], world),
+            "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (workloads/: seeded SplitMix64, shapes of BASELINE.json configs)",
