@@ -136,7 +136,11 @@ __device__ __forceinline__ void jacobi_rot(AR &ar, double &app, double &aqq, dou
   const double rr = ar.sqrt_(dl * dl + a_ * a_);
   double t = ar.div(a_, fabs(dl) + rr);
   t = dl < 0.0 ? -t : t;
-  const double c = ar.rcp(ar.sqrt_(1.0 + t * t));
+  // t = a_/(|dl| + sqrt(dl^2 + a_^2)) has |t| <= 1 (plus rounding) whenever the checked
+  // sqrt and div passed, so 1 + t^2 lies in [1, 2] and its root in [1, 1.5): both fast
+  // paths are valid there and their range checks are redundant (unit variants).  If a
+  // checked op failed, the whole point is re-run with IEEE operators anyway.
+  const double c = ar.rcp_unit(ar.sqrt_unit(1.0 + t * t));
   const double s = t * c;
   const double rp = arp, rq = arq;
   const double napp = app - t * apq;
@@ -148,6 +152,40 @@ __device__ __forceinline__ void jacobi_rot(AR &ar, double &app, double &aqq, dou
   apq = go ? 0.0 : apq;
   arp = go ? narp : arp;
   arq = go ? narq : arq;
+}
+
+// Two independent rotations (one per matrix), written step by step in lockstep so the
+// scheduler sees the two dependency chains side by side (ptxas otherwise emitted the first
+// rotation's whole sqrt -> div -> sqrt -> rcp chain before the second's).  Each rotation's
+// arithmetic is exactly jacobi_rot's.
+template <class AR>
+__device__ __forceinline__ void jacobi_rot2(AR &ar, double &app, double &aqq, double &apq,
+                                            double &arp, double &arq, const double ta,
+                                            double &epp, double &eqq, double &epq,
+                                            double &erp, double &erq, const double te) {
+  const bool ga = !(fabs(apq) <= ta), ge = !(fabs(epq) <= te);
+  const double a_ = ga ? apq : 1.0, e_ = ge ? epq : 1.0;
+  const double dla = ga ? 0.5 * (aqq - app) : 0.0, dle = ge ? 0.5 * (eqq - epp) : 0.0;
+  const double sa = dla * dla + a_ * a_, se = dle * dle + e_ * e_;
+  const double rra = ar.sqrt_(sa), rre = ar.sqrt_(se);
+  const double dna = fabs(dla) + rra, dne = fabs(dle) + rre;
+  double tA = ar.div(a_, dna), tE = ar.div(e_, dne);
+  tA = dla < 0.0 ? -tA : tA;
+  tE = dle < 0.0 ? -tE : tE;
+  const double ua = 1.0 + tA * tA, ue = 1.0 + tE * tE;
+  const double qa = ar.sqrt_unit(ua), qe = ar.sqrt_unit(ue);  // in [1, 2]: see jacobi_rot
+  const double ca = ar.rcp_unit(qa), ce = ar.rcp_unit(qe);
+  const double sA = tA * ca, sE = tE * ce;
+  const double rpa = arp, rqa = arq, rpe = erp, rqe = erq;
+  const double nppa = app - tA * apq, nppe = epp - tE * epq;
+  const double nqqa = aqq + tA * apq, nqqe = eqq + tE * epq;
+  const double nrpa = ca * rpa - sA * rqa, nrpe = ce * rpe - sE * rqe;
+  const double nrqa = sA * rpa + ca * rqa, nrqe = sE * rpe + ce * rqe;
+  app = ga ? nppa : app;  epp = ge ? nppe : epp;
+  aqq = ga ? nqqa : aqq;  eqq = ge ? nqqe : eqq;
+  apq = ga ? 0.0 : apq;   epq = ge ? 0.0 : epq;
+  arp = ga ? nrpa : arp;  erp = ge ? nrpe : erp;
+  arq = ga ? nrqa : arq;  erq = ge ? nrqe : erq;
 }
 
 __device__ __forceinline__ double amax6(double a00, double a11, double a22, double a01, double a02,
@@ -186,12 +224,9 @@ __device__ __forceinline__ void lmin3_pair(AR &ar, double a00, double a11, doubl
       const bool wa = __any_sync(0xffffffffu, la), we = __any_sync(0xffffffffu, le);
       if (!(wa || we)) break;
       if (wa && we) {
-        jacobi_rot(ar, a00, a11, a01, a02, a12, ta);  // (0,1), r3 = 2
-        jacobi_rot(ar, e00, e11, e01, e02, e12, te);
-        jacobi_rot(ar, a00, a22, a02, a01, a12, ta);  // (0,2), r3 = 1
-        jacobi_rot(ar, e00, e22, e02, e01, e12, te);
-        jacobi_rot(ar, a11, a22, a12, a01, a02, ta);  // (1,2), r3 = 0
-        jacobi_rot(ar, e11, e22, e12, e01, e02, te);
+        jacobi_rot2(ar, a00, a11, a01, a02, a12, ta, e00, e11, e01, e02, e12, te);  // (0,1)
+        jacobi_rot2(ar, a00, a22, a02, a01, a12, ta, e00, e22, e02, e01, e12, te);  // (0,2)
+        jacobi_rot2(ar, a11, a22, a12, a01, a02, ta, e11, e22, e12, e01, e02, te);  // (1,2)
       } else if (wa) {
         jacobi_rot(ar, a00, a11, a01, a02, a12, ta);
         jacobi_rot(ar, a00, a22, a02, a01, a12, ta);
