@@ -51,3 +51,35 @@ def test_unsupported_combination_rejected():
     import ctypes
     d = hydro._MeshDesc(3, 4, 8, 1, 1, None, None, None)
     assert hydro.lib().hydro_ctx_workspace_bytes(ctypes.byref(d)) == 0
+
+
+def _desc(dim, k, q, n_elem, n_nodes):
+    from paper_2104_11404_b200 import hydro
+    return hydro._MeshDesc(dim, k, q, n_elem, n_nodes, None, None, None)
+
+
+def test_empty_and_oversized_meshes_rejected():
+    """Edge cases of the boundary (no GPU needed): an empty mesh and a mesh whose
+    element->node slot count overflows the int32 indexing are rejected up front
+    (workspace size 0 = invalid description); valid sizes return a positive size."""
+    import ctypes
+    from paper_2104_11404_b200 import hydro
+    L = hydro.lib()
+    ws = lambda d: L.hydro_ctx_workspace_bytes(ctypes.byref(d))
+    assert ws(_desc(3, 2, 4, 0, 10)) == 0                        # no elements
+    assert ws(_desc(3, 2, 4, 10, 0)) == 0                        # no nodes
+    assert ws(_desc(3, 2, 4, (1 << 31) // 27 + 1, 1000)) == 0    # n_elem * 27 >= 2^31
+    assert ws(_desc(3, 2, 4, 262144, 129 ** 3)) > 0              # C2 size
+    assert ws(_desc(3, 3, 6, 258048, 337 * 145 * 145)) > 0       # C3 size
+    assert ws(_desc(2, 2, 5, 10, 100)) == 0                      # unsupported q for k = 2
+
+
+def test_null_arguments_rejected_without_gpu():
+    """Argument errors return synchronously, before any device work."""
+    from paper_2104_11404_b200 import hydro
+    L = hydro.lib()
+    assert L.hydro_force_full(None, None, None, None, None, None, hydro.Visc(0.5, 2.0, 1).c(),
+                              hydro.Cfl(0.5, 2.5).c(), None, None, None, None) == hydro.HYDRO_ERR_ARG
+    assert L.hydro_sample_create(None, None, 0, 1, None) == hydro.HYDRO_ERR_ARG
+    assert L.hydro_rom_lift(10, 0, 4, None, None, 0, None, None, None) == hydro.HYDRO_ERR_ARG
+    assert L.hydro_selftest_ieee_fast(1, -1, 0, 0, None, None) == hydro.HYDRO_ERR_ARG
