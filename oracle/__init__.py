@@ -9,6 +9,9 @@ Contents:
   hydro_oracle.c  -- plain C implementation of F.1, F^T.w, dt (see its header for
                      the PAPER.md citations), the ROM lift and projection as naive
                      loops. Built with gcc -O2 -ffp-contract=off (explicit fma()).
+  fom.py          -- the full-order RK2-average step: mass matrices by
+                     their definition (np.kron tables, scipy.sparse assembly), sparse
+                     direct solves, the force via hydro_oracle.c.
 Parity pins for every function live in tests/test_oracle_pins.py.  Nothing here is
 "parity unpinned" except the physical fidelity of readings R3/R5 to Dobrev 2012
 (DESIGN.md), which no available source can check.
