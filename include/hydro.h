@@ -158,6 +158,48 @@ hydro_status hydro_rom_project(int n, int64_t s_rows, int B, const double *P, co
                                double *r, void *workspace, size_t ws_bytes,
                                hydro_stream_t stream);
 
+/* ------------------------------------------------------------------ FOM time step (NEXT-1) */
+/* The full-order RK2-average step of PAPER Eq. RK2-avg around the force:
+ *   v^{n+1/2} = v^n - dt/2 M_V^-1 F(U^n).1,   e^{n+1/2} = e^n + dt/2 M_E^-1 F(U^n)^T v^{n+1/2},
+ *   x^{n+1/2} = x^n + dt/2 v^{n+1/2},
+ *   v^{n+1}   = v^n - dt M_V^-1 F(U^{n+1/2}).1, e^{n+1} = e^n + dt M_E^-1 F(U^{n+1/2})^T vbar,
+ *   x^{n+1}   = x^n + dt vbar,   vbar = (v^n + v^{n+1})/2.
+ * M_V (kinematic mass, constant in time: P:389-391) is applied matrix-free and
+ * inverted by Jacobi-preconditioned CG on the free dofs; M_E is block diagonal and inverted
+ * exactly per element.  The boundary condition v.n = g with g = 0 is given as
+ * the list of constrained velocity dofs (flat index c*n_nodes + node, host array); those
+ * components of v are held at 0.  The scheme conserves 1/2 v^T M_V v + 1^T M_E e
+ * up to the CG tolerance.  All reductions are fixed-order (deterministic).
+ * hydro_fom_create allocates device memory (setup, never on the hot path) and
+ * synchronises `stream`; it keeps `ctx` (which must outlive it).                          */
+typedef struct hydro_fom hydro_fom;
+hydro_status hydro_fom_create(hydro_ctx *ctx, const int64_t *bc_dofs /* host */, int64_t n_bc,
+                              hydro_stream_t stream, hydro_fom **out /* host */);
+hydro_status hydro_fom_destroy(hydro_fom *fom);
+/* out = M_V in   (in, out: device [dim][n_nodes]; no boundary condition applied).         */
+hydro_status hydro_mass_v_apply(hydro_fom *fom, const double *in, double *out,
+                                hydro_stream_t stream);
+/* sol = M_V^-1 rhs on the free dofs (0 on the constrained ones), PCG to the relative
+ * preconditioned residual rel_tol or max_iter iterations; *iters, *relres (host, may be
+ * NULL) report what was reached.  Synchronises `stream` (host-checked convergence).      */
+hydro_status hydro_mass_v_solve(hydro_fom *fom, const double *rhs, double *sol, double rel_tol,
+                                int max_iter, int *iters, double *relres, hydro_stream_t stream);
+/* sol = M_E^-1 rhs  (device [n_elem][k^dim]).                                               */
+hydro_status hydro_mass_e_solve(hydro_fom *fom, const double *rhs, double *sol,
+                                hydro_stream_t stream);
+/* Kinetic 1/2 v^T M_V v and internal 1^T M_E e energies (host outputs).  Synchronises.     */
+hydro_status hydro_fom_energy(hydro_fom *fom, const double *v, const double *e,
+                              double *kinetic, double *internal, hydro_stream_t stream);
+/* One RK2-average step of size dt, in place on the device state (x, v, e); four force
+ * evaluations (F.1 and F^T w of each stage), two CG solves.  *dt_est (host) = the min of
+ * the two stages' time-step estimates for the caller's controller;
+ * *cg_iters (host) = CG iterations used.  Device conditions (tangled, NaN) are reported by
+ * hydro_status_sync on the context.  Synchronises `stream`.                                 */
+hydro_status hydro_rk2avg_step(hydro_fom *fom, double *x, double *v, double *e,
+                               const double *gamma, hydro_visc visc, hydro_cfl cfl, double dt,
+                               double cg_tol, int cg_max_iter, double *dt_est /* host */,
+                               int *cg_iters /* host */, hydro_stream_t stream);
+
 /* ------------------------------------------------------------------ profiling (host) */
 /* When enabled, every hydro_force_full / hydro_dt_estimate / hydro_force_sampled call
  * records a pair of CUDA events around its force kernel on the call's stream (the

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -12,6 +13,7 @@
 #include "../../include/hydro.h"
 #include "force2d.cuh"
 #include "force3d.cuh"
+#include "fom.cuh"
 #include "force_kernel.cuh"
 #include "hydro_internal.h"
 #include "rom_kernels.cuh"
@@ -719,6 +721,278 @@ hydro_status hydro_rom_project(int n, int64_t s_rows, int B, const double *P, co
   hk::project_reduce_kernel<<<(n * B + 255) / 256, 256, 0, s>>>(n, B, G, (const double *)workspace, r);
   g_launches++;
   CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
+
+// ------------------------------------------------------------------------------ FOM step
+}  // extern "C"
+
+struct hydro_fom {
+  hydro_ctx *c = nullptr;
+  int64_t n = 0;  // dim * n_nodes
+  double *mask = nullptr, *dinv = nullptr, *Minv = nullptr, *csum = nullptr;
+  double *r = nullptr, *z = nullptr, *p = nullptr, *Ap = nullptr, *part = nullptr, *sc = nullptr;
+  double *F1 = nullptr, *F1x = nullptr, *FTw = nullptr, *FTx = nullptr, *dv = nullptr;
+  double *vh = nullptr, *eh = nullptr, *xh = nullptr, *v1 = nullptr, *vbar = nullptr,
+         *dts = nullptr;
+  std::vector<void *> allocs;
+};
+
+namespace {
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+template <int DIM, int K, int Q>
+hydro_status mass_apply_t(hydro_fom *f, const double *in, double *out, const double *mask, int mode,
+                          int invert, cudaStream_t s) {
+  hydro_ctx *c = f->c;
+  hk::MassParams P;
+  P.n_elem = (int32_t)c->d.n_elem;
+  P.n_nodes = c->d.n_nodes;
+  P.elem_nodes = c->d.elem_nodes;
+  P.slot = c->slot;
+  P.mq = c->mq;
+  P.in = in;
+  P.evec = c->evec;
+  P.mode = mode;
+  P.tab_w = c->tab;
+  P.tab_B = c->tab + Q;
+  constexpr int NT = DIM == 3 ? (Q == 4 ? 64 : 224) : 64;
+  hk::mass_apply_kernel<DIM, K, Q><<<(unsigned)c->d.n_elem, NT, 0, s>>>(P);
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  hk::assemble_masked_kernel<DIM><<<blocks_for(c->d.n_nodes, 256), 256, 0, s>>>(
+      c->d.n_nodes, c->off, c->evec, mask, out, invert);
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
+hydro_status mass_apply(hydro_fom *f, const double *in, double *out, const double *mask, int mode,
+                        int invert, cudaStream_t s) {
+  const hydro_mesh_desc &d = f->c->d;
+  if (d.dim == 2 && d.order_h1 == 2) return mass_apply_t<2, 2, 4>(f, in, out, mask, mode, invert, s);
+  if (d.dim == 3 && d.order_h1 == 2) return mass_apply_t<3, 2, 4>(f, in, out, mask, mode, invert, s);
+  if (d.dim == 2 && d.order_h1 == 3) return mass_apply_t<2, 3, 6>(f, in, out, mask, mode, invert, s);
+  if (d.dim == 3 && d.order_h1 == 3) return mass_apply_t<3, 3, 6>(f, in, out, mask, mode, invert, s);
+  return HYDRO_ERR_UNSUPPORTED;
+}
+
+hydro_status dot(hydro_fom *f, int64_t n, const double *a, const double *b, double *out,
+                 cudaStream_t s) {
+  hk::dot_partial_kernel<<<hk::DOT_BLOCKS, hk::DOT_THREADS, 0, s>>>(n, a, b, f->part);
+  hk::dot_final_kernel<<<1, 32, 0, s>>>(f->part, out);
+  g_launches += 2;
+  CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
+hydro_status mass_e_update(hydro_fom *f, const double *a, const double *rhs, double scale,
+                           double *out, cudaStream_t s) {
+  const hydro_ctx *c = f->c;
+  const int ne = c->ne;
+  const int64_t n = c->d.n_elem * ne;
+  const unsigned g = blocks_for(n, 256);
+  const int32_t E = (int32_t)c->d.n_elem;
+  if (ne == 4) hk::mass_e_update_kernel<4><<<g, 256, 0, s>>>(E, f->Minv, a, rhs, scale, out);
+  else if (ne == 8) hk::mass_e_update_kernel<8><<<g, 256, 0, s>>>(E, f->Minv, a, rhs, scale, out);
+  else if (ne == 9) hk::mass_e_update_kernel<9><<<g, 256, 0, s>>>(E, f->Minv, a, rhs, scale, out);
+  else if (ne == 27) hk::mass_e_update_kernel<27><<<g, 256, 0, s>>>(E, f->Minv, a, rhs, scale, out);
+  else return HYDRO_ERR_UNSUPPORTED;
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
+// PCG with the Jacobi preconditioner on the free dofs; rel. preconditioned residual.
+hydro_status pcg(hydro_fom *f, const double *b, double *x, double tol, int max_iter, int *iters,
+                 double *relres, cudaStream_t s) {
+  const int64_t n = f->n;
+  const unsigned g = blocks_for(n, 256);
+  hk::cg_init_kernel<<<g, 256, 0, s>>>(n, b, f->mask, f->dinv, x, f->r, f->z, f->p);
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  hydro_status st = dot(f, n, f->r, f->z, f->sc + 0, s);
+  if (st != HYDRO_OK) return st;
+  double rz0 = 0.0;
+  CUDA_OK(cudaMemcpyAsync(&rz0, f->sc + 0, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+  int it = 0;
+  double rel = 0.0;
+  if (rz0 > 0.0) {
+    rel = 1.0;
+    while (it < max_iter) {
+      if ((st = mass_apply(f, f->p, f->Ap, f->mask, 0, 0, s)) != HYDRO_OK) return st;
+      if ((st = dot(f, n, f->p, f->Ap, f->sc + 1, s)) != HYDRO_OK) return st;
+      hk::cg_alpha_kernel<<<1, 1, 0, s>>>(f->sc);
+      hk::cg_xr_kernel<<<g, 256, 0, s>>>(n, f->sc, f->p, f->Ap, f->dinv, x, f->r, f->z);
+      if ((st = dot(f, n, f->r, f->z, f->sc + 3, s)) != HYDRO_OK) return st;
+      hk::cg_beta_kernel<<<1, 1, 0, s>>>(f->sc);
+      hk::cg_p_kernel<<<g, 256, 0, s>>>(n, f->sc, f->z, f->p);
+      g_launches += 4;
+      CUDA_OK(cudaGetLastError());
+      ++it;
+      if (it % 4 == 0 || it == max_iter) {
+        double rz = 0.0;
+        CUDA_OK(cudaMemcpyAsync(&rz, f->sc + 0, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        rel = sqrt(rz / rz0);
+        if (!(rel > tol)) break;
+      }
+    }
+  }
+  if (iters) *iters = it;
+  if (relres) *relres = rel;
+  return HYDRO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hydro_status hydro_fom_create(hydro_ctx *c, const int64_t *bc_dofs, int64_t n_bc,
+                              hydro_stream_t stream, hydro_fom **out) {
+  if (!c || !out || n_bc < 0 || (n_bc > 0 && !bc_dofs)) return HYDRO_ERR_ARG;
+  *out = nullptr;
+  cudaStream_t s = (cudaStream_t)stream;
+  hydro_fom *f = new hydro_fom();
+  f->c = c;
+  const int dim = c->d.dim;
+  const int64_t NN = c->d.n_nodes, E = c->d.n_elem, ne = c->ne;
+  f->n = dim * NN;
+  std::vector<double> mask((size_t)f->n, 1.0);
+  for (int64_t i = 0; i < n_bc; ++i) {
+    if (bc_dofs[i] < 0 || bc_dofs[i] >= f->n) { delete f; return HYDRO_ERR_ARG; }
+    mask[(size_t)bc_dofs[i]] = 0.0;
+  }
+  auto fail = [&](hydro_status st) { hydro_fom_destroy(f); return st; };
+  auto alloc = [&](double **ptr, size_t count) {
+    void *q = nullptr;
+    if (cudaMalloc(&q, sizeof(double) * (count > 0 ? count : 1)) != cudaSuccess) return false;
+    f->allocs.push_back(q);
+    *ptr = (double *)q;
+    return true;
+  };
+  const size_t n = (size_t)f->n, nE = (size_t)(E * ne);
+  if (!alloc(&f->mask, n) || !alloc(&f->dinv, n) || !alloc(&f->Minv, nE * ne) ||
+      !alloc(&f->csum, nE) || !alloc(&f->r, n) || !alloc(&f->z, n) || !alloc(&f->p, n) ||
+      !alloc(&f->Ap, n) || !alloc(&f->part, hk::DOT_BLOCKS) || !alloc(&f->sc, 8) ||
+      !alloc(&f->F1, n) || !alloc(&f->F1x, n) || !alloc(&f->FTw, nE) || !alloc(&f->FTx, nE) ||
+      !alloc(&f->dv, n) || !alloc(&f->vh, n) || !alloc(&f->eh, nE) || !alloc(&f->xh, n) ||
+      !alloc(&f->v1, n) || !alloc(&f->vbar, n) || !alloc(&f->dts, 2))
+    return fail(HYDRO_ERR_CUDA);
+  if (cudaMemcpyAsync(f->mask, mask.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return fail(HYDRO_ERR_CUDA);
+  // Jacobi preconditioner: 1 / diag(M_V) on the free dofs, 0 on the constrained ones
+  hydro_status st = mass_apply(f, nullptr, f->dinv, f->mask, 1, 1, s);
+  if (st != HYDRO_OK) return fail(st);
+  // M_E,K^{-1} and the internal-energy weights
+  const int q = c->d.nq1d, nn = c->d.order_h1 + 1;
+  const double *tw = c->tab, *tBl = c->tab + q + 2 * q * nn;
+  const unsigned g = blocks_for(E, 64);
+  if (dim == 2 && c->d.order_h1 == 2)
+    hk::mass_e_setup_kernel<2, 2, 4><<<g, 64, 0, s>>>((int32_t)E, c->mq, tw, tBl, f->Minv, f->csum);
+  else if (dim == 3 && c->d.order_h1 == 2)
+    hk::mass_e_setup_kernel<3, 2, 4><<<g, 64, 0, s>>>((int32_t)E, c->mq, tw, tBl, f->Minv, f->csum);
+  else if (dim == 2 && c->d.order_h1 == 3)
+    hk::mass_e_setup_kernel<2, 3, 6><<<g, 64, 0, s>>>((int32_t)E, c->mq, tw, tBl, f->Minv, f->csum);
+  else
+    hk::mass_e_setup_kernel<3, 3, 6><<<g, 64, 0, s>>>((int32_t)E, c->mq, tw, tBl, f->Minv, f->csum);
+  g_launches++;
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+    return fail(HYDRO_ERR_CUDA);
+  *out = f;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_fom_destroy(hydro_fom *f) {
+  if (!f) return HYDRO_OK;
+  for (void *q : f->allocs) cudaFree(q);
+  delete f;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_mass_v_apply(hydro_fom *f, const double *in, double *out, hydro_stream_t stream) {
+  if (!f || !in || !out) return HYDRO_ERR_ARG;
+  return mass_apply(f, in, out, nullptr, 0, 0, (cudaStream_t)stream);
+}
+
+hydro_status hydro_mass_v_solve(hydro_fom *f, const double *rhs, double *sol, double rel_tol,
+                                int max_iter, int *iters, double *relres, hydro_stream_t stream) {
+  if (!f || !rhs || !sol || max_iter < 0 || !(rel_tol >= 0.0)) return HYDRO_ERR_ARG;
+  return pcg(f, rhs, sol, rel_tol, max_iter, iters, relres, (cudaStream_t)stream);
+}
+
+hydro_status hydro_mass_e_solve(hydro_fom *f, const double *rhs, double *sol, hydro_stream_t stream) {
+  if (!f || !rhs || !sol) return HYDRO_ERR_ARG;
+  hydro_status st;
+  cudaStream_t s = (cudaStream_t)stream;
+  // sol = 0 + 1 * Minv rhs  (the zero vector: FTx scratch cleared first)
+  const size_t nE = (size_t)(f->c->d.n_elem * f->c->ne);
+  CUDA_OK(cudaMemsetAsync(f->FTx, 0, sizeof(double) * nE, s));
+  if ((st = mass_e_update(f, f->FTx, rhs, 1.0, sol, s)) != HYDRO_OK) return st;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_fom_energy(hydro_fom *f, const double *v, const double *e, double *kinetic,
+                              double *internal, hydro_stream_t stream) {
+  if (!f || !v || !e) return HYDRO_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  hydro_status st;
+  if ((st = mass_apply(f, v, f->Ap, nullptr, 0, 0, s)) != HYDRO_OK) return st;
+  if ((st = dot(f, f->n, v, f->Ap, f->sc + 6, s)) != HYDRO_OK) return st;
+  if ((st = dot(f, f->c->d.n_elem * f->c->ne, f->csum, e, f->sc + 7, s)) != HYDRO_OK) return st;
+  double h[2];
+  CUDA_OK(cudaMemcpyAsync(h, f->sc + 6, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+  if (kinetic) *kinetic = 0.5 * h[0];
+  if (internal) *internal = h[1];
+  return HYDRO_OK;
+}
+
+hydro_status hydro_rk2avg_step(hydro_fom *f, double *x, double *v, double *e, const double *gamma,
+                               hydro_visc visc, hydro_cfl cfl, double dt, double cg_tol,
+                               int cg_max_iter, double *dt_est, int *cg_iters,
+                               hydro_stream_t stream) {
+  if (!f || !x || !v || !e || !gamma || !(dt > 0.0)) return HYDRO_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  hydro_ctx *c = f->c;
+  const int64_t n = f->n, nE = c->d.n_elem * c->ne;
+  const unsigned g = blocks_for(n, 256);
+  hydro_status st;
+  int it1 = 0, it2 = 0;
+  // ---- stage 1: F(U^n)
+  if ((st = force_common(c, hk::MODE_FORCE, x, v, e, nullptr, gamma, visc, cfl, f->F1, f->FTx,
+                         f->dts + 0, s)) != HYDRO_OK) return st;
+  if ((st = pcg(f, f->F1, f->dv, cg_tol, cg_max_iter, &it1, nullptr, s)) != HYDRO_OK) return st;
+  hk::axpy_kernel<<<g, 256, 0, s>>>(n, v, -0.5 * dt, f->dv, f->mask, f->vh);    // v^{n+1/2}
+  g_launches++;
+  if ((st = force_common(c, hk::MODE_FORCE, x, v, e, f->vh, gamma, visc, cfl, f->F1x, f->FTw,
+                         nullptr, s)) != HYDRO_OK) return st;                       // F(U^n)^T v^{n+1/2}
+  if ((st = mass_e_update(f, e, f->FTw, 0.5 * dt, f->eh, s)) != HYDRO_OK) return st;
+  hk::axpy_kernel<<<g, 256, 0, s>>>(n, x, 0.5 * dt, f->vh, nullptr, f->xh);    // x^{n+1/2}
+  g_launches++;
+  // ---- stage 2: F(U^{n+1/2})
+  if ((st = force_common(c, hk::MODE_FORCE, f->xh, f->vh, f->eh, nullptr, gamma, visc, cfl, f->F1,
+                         f->FTx, f->dts + 1, s)) != HYDRO_OK) return st;
+  if ((st = pcg(f, f->F1, f->dv, cg_tol, cg_max_iter, &it2, nullptr, s)) != HYDRO_OK) return st;
+  hk::axpy_kernel<<<g, 256, 0, s>>>(n, v, -dt, f->dv, f->mask, f->v1);         // v^{n+1}
+  hk::avg_kernel<<<g, 256, 0, s>>>(n, v, f->v1, f->vbar);                       // vbar
+  g_launches += 2;
+  if ((st = force_common(c, hk::MODE_FORCE, f->xh, f->vh, f->eh, f->vbar, gamma, visc, cfl, f->F1x,
+                         f->FTw, nullptr, s)) != HYDRO_OK) return st;               // F(U^{n+1/2})^T vbar
+  if ((st = mass_e_update(f, e, f->FTw, dt, e, s)) != HYDRO_OK) return st;     // e^{n+1}
+  hk::axpy_kernel<<<g, 256, 0, s>>>(n, x, dt, f->vbar, nullptr, x);            // x^{n+1}
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaMemcpyAsync(v, f->v1, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  double h[2];
+  CUDA_OK(cudaMemcpyAsync(h, f->dts, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+  if (dt_est) *dt_est = h[0] < h[1] ? h[0] : h[1];  // (a NaN estimate propagates via status)
+  if (cg_iters) *cg_iters = it1 + it2;
+  (void)nE;
   return HYDRO_OK;
 }
 

@@ -27,7 +27,9 @@ EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy"
             "hydro_sample_destroy", "hydro_sample_info", "hydro_sample_lists", "hydro_rom_lift",
             "hydro_force_sampled", "hydro_sample_status_sync", "hydro_rom_project_workspace_bytes",
             "hydro_rom_project", "hydro_basis_tables", "hydro_launch_count", "hydro_version",
-            "hydro_profile_enable", "hydro_profile_read", "hydro_selftest_ieee_fast"]
+            "hydro_profile_enable", "hydro_profile_read", "hydro_selftest_ieee_fast",
+            "hydro_fom_create", "hydro_fom_destroy", "hydro_mass_v_apply", "hydro_mass_v_solve",
+            "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step"]
 
 
 class HydroError(RuntimeError):
@@ -79,6 +81,15 @@ def lib() -> ctypes.CDLL:
         L.hydro_force_sampled.argtypes = [vp, vp, vp, vp, vp, vp, _Visc, _Cfl, vp, vp, vp, vp]
         L.hydro_sample_status_sync.argtypes = [vp, vp, ctypes.POINTER(i64)]
         L.hydro_selftest_ieee_fast.argtypes = [ctypes.c_uint64, i64, i32, i32, vp, vp]
+        L.hydro_fom_create.argtypes = [vp, vp, i64, vp, ctypes.POINTER(vp)]
+        L.hydro_fom_destroy.argtypes = [vp]
+        L.hydro_mass_v_apply.argtypes = [vp, vp, vp, vp]
+        L.hydro_mass_v_solve.argtypes = [vp, vp, vp, dbl, i32, ctypes.POINTER(i32),
+                                         ctypes.POINTER(dbl), vp]
+        L.hydro_mass_e_solve.argtypes = [vp, vp, vp, vp]
+        L.hydro_fom_energy.argtypes = [vp, vp, vp, ctypes.POINTER(dbl), ctypes.POINTER(dbl), vp]
+        L.hydro_rk2avg_step.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, dbl, dbl, i32,
+                                        ctypes.POINTER(dbl), ctypes.POINTER(i32), vp]
         L.hydro_rom_project_workspace_bytes.restype = ctypes.c_size_t
         L.hydro_rom_project_workspace_bytes.argtypes = [i32, i64, i32]
         L.hydro_rom_project.argtypes = [i32, i64, i32, vp, vp, vp, vp, ctypes.c_size_t, vp]
@@ -323,3 +334,57 @@ def rom_project(P: torch.Tensor, f: torch.Tensor, out: Optional[torch.Tensor] = 
     _check(lib().hydro_rom_project(n, s_rows, B, _ptr(P), _ptr(f), _ptr(out), _ptr(workspace),
                                    workspace.numel(), _stream(stream)), "hydro_rom_project")
     return out
+
+
+class Fom:
+    """Full-order RK2-average stepper (hydro_fom_*; PAPER Eq. RK2-avg) on a context.
+    bc_dofs: constrained velocity dofs (flat c*n_nodes + node) of v.n = 0."""
+
+    def __init__(self, ctx: HydroContext, bc_dofs, stream=None):
+        import numpy as np
+        L = lib()
+        bc = np.ascontiguousarray(np.asarray(bc_dofs, dtype=np.int64))
+        h = ctypes.c_void_p()
+        _check(L.hydro_fom_create(ctx.handle, bc.ctypes.data_as(ctypes.c_void_p) if bc.size else None,
+                                  bc.size, _stream(stream), ctypes.byref(h)), "hydro_fom_create")
+        self._h, self.ctx = h, ctx
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) and self._h.value:
+                lib().hydro_fom_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def mass_v(self, v, out=None, stream=None):
+        out = torch.empty_like(v) if out is None else out
+        _check(lib().hydro_mass_v_apply(self._h, _ptr(v), _ptr(out), _stream(stream)), "hydro_mass_v_apply")
+        return out
+
+    def solve_v(self, rhs, tol=1e-12, max_iter=500, out=None, stream=None):
+        out = torch.empty_like(rhs) if out is None else out
+        it, rel = ctypes.c_int(0), ctypes.c_double(0.0)
+        _check(lib().hydro_mass_v_solve(self._h, _ptr(rhs), _ptr(out), tol, max_iter, ctypes.byref(it),
+                                        ctypes.byref(rel), _stream(stream)), "hydro_mass_v_solve")
+        return out, it.value, rel.value
+
+    def solve_e(self, rhs, out=None, stream=None):
+        out = torch.empty_like(rhs) if out is None else out
+        _check(lib().hydro_mass_e_solve(self._h, _ptr(rhs), _ptr(out), _stream(stream)), "hydro_mass_e_solve")
+        return out
+
+    def energy(self, v, e, stream=None):
+        k, i = ctypes.c_double(0.0), ctypes.c_double(0.0)
+        _check(lib().hydro_fom_energy(self._h, _ptr(v), _ptr(e), ctypes.byref(k), ctypes.byref(i),
+                                      _stream(stream)), "hydro_fom_energy")
+        return k.value, i.value
+
+    def step(self, x, v, e, gamma, visc: Visc, cfl: Cfl, dt: float, cg_tol=1e-12, cg_max_iter=500,
+             stream=None):
+        """In-place RK2-average step; returns (dt_estimate, cg_iterations)."""
+        d, it = ctypes.c_double(0.0), ctypes.c_int(0)
+        _check(lib().hydro_rk2avg_step(self._h, _ptr(x), _ptr(v), _ptr(e), _ptr(gamma), visc.c(), cfl.c(),
+                                       dt, cg_tol, cg_max_iter, ctypes.byref(d), ctypes.byref(it),
+                                       _stream(stream)), "hydro_rk2avg_step")
+        return d.value, it.value

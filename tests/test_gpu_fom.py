@@ -1,0 +1,121 @@
+"""GPU parity of the full-order RK2-average step (PAPER Eq. RK2-avg
+P:463-508) against oracle/fom.py: the matrix-free M_V apply, the PCG mass solve, the
+M_E block solve, one and several full steps, and discrete total-energy conservation
+(P:506-508).  Tolerances: mass apply 1e-13 of the |terms| scale; solves to the CG
+tolerance (1e-13); a step's state within 1e-11 relative (the four force evaluations
+see states that differ at the CG-tolerance level, so dt is compared to 1e-10, not
+bitwise); energy conserved to 1e-11 relative over 5 steps."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from tests import gpu_helpers as H  # noqa: E402
+from paper_2104_11404_b200 import hydro  # noqa: E402
+from oracle import fom as ofom  # noqa: E402
+
+
+def _box(dim, k, shape, delta=0.08, cfg=41):
+    nq = 4 if k == 2 else 6
+    hi = tuple(0.1 * s for s in shape)
+    p = W.sedov_like(cfg, dim, shape, (0.0,) * dim, hi, delta=delta, e_floor=1e-2,
+                     vmode="uniform", vscale=0.1, k=k, nq=nq, name="fombox")
+    rng = np.random.default_rng(cfg)
+    p.e[:] = 1.0 + 0.5 * rng.random(p.e.shape)
+    return p
+
+
+CASES = [(2, 2, (7, 5)), (3, 2, (3, 3, 2)), (2, 3, (3, 2)), (3, 3, (2, 2, 1))]
+
+
+@pytest.mark.parametrize("dim,k,shape", CASES)
+def test_mass_apply_and_solves(dim, k, shape):
+    prob = _box(dim, k, shape)
+    m = prob.mesh
+    bc = ofom.bc_dofs_box(m)
+    ref = ofom.Fom(m, bc)
+    ctx = H.context(prob)
+    f = hydro.Fom(ctx, bc)
+    rng = np.random.default_rng(7)
+    u = rng.standard_normal((dim, m.n_nodes))
+    Mu = f.mass_v(H.dev(u)).cpu().numpy()
+    Mu_ref = np.stack([ref.M @ u[c] for c in range(dim)])
+    scale = np.stack([abs(ref.M) @ abs(u[c]) for c in range(dim)])
+    H.assert_close(Mu, Mu_ref, scale, 1e-13, "M_V u")
+    rhs = rng.standard_normal((dim, m.n_nodes))
+    sol, it, rel = f.solve_v(H.dev(rhs), tol=1e-14, max_iter=2000)
+    want = ref.solve_v(rhs)
+    assert rel <= 1e-14 and it < 2000
+    assert np.abs(sol.cpu().numpy() - want).max() <= 1e-11 * np.abs(want).max()
+    re = rng.standard_normal((m.n_elem, m.ne))
+    se = f.solve_e(H.dev(re)).cpu().numpy()
+    H.assert_close(se, ref.solve_e(re), np.abs(ref.solve_e(re)) + 1e-300, 1e-11, "M_E^-1 r")
+
+
+@pytest.mark.parametrize("dim,k,shape", CASES)
+def test_rk2avg_steps_match_oracle(dim, k, shape):
+    prob = _box(dim, k, shape)
+    m = prob.mesh
+    bc = ofom.bc_dofs_box(m)
+    prob.v.reshape(-1)[bc] = 0.0
+    ref = ofom.Fom(m, bc)
+    ctx = H.context(prob)
+    f = hydro.Fom(ctx, bc)
+    x, v, e, g = H.dev(prob.x), H.dev(prob.v), H.dev(prob.e), H.dev(prob.gamma)
+    visc, cfl = hydro.Visc(prob.q1, prob.q2, prob.visc), hydro.Cfl(prob.alpha, prob.alpha_mu)
+    xr, vr, er = prob.x.copy(), prob.v.copy(), prob.e.copy()
+    import oracle
+    dt = 0.25 * oracle.force(prob)["dt"]
+    for _ in range(2):
+        dt_g, iters = f.step(x, v, e, g, visc, cfl, dt, cg_tol=1e-14, cg_max_iter=2000)
+        xr, vr, er, dt_r = ofom.rk2avg_step(ref, prob, xr, vr, er, dt)
+        assert ctx.status_sync()[0] == 0
+        assert dt_g == pytest.approx(dt_r, rel=1e-10)
+    for got, want, what in ((x, xr, "x"), (v, vr, "v"), (e, er, "e")):
+        g_ = got.cpu().numpy()
+        assert np.abs(g_ - want).max() <= 1e-11 * max(np.abs(want).max(), 1e-300), what
+    assert np.array_equal(v.cpu().numpy().reshape(-1)[bc], np.zeros(bc.size))
+
+
+def test_energy_conservation_gpu():
+    prob = _box(3, 2, (4, 3, 3))
+    m = prob.mesh
+    bc = ofom.bc_dofs_box(m)
+    prob.v.reshape(-1)[bc] = 0.0
+    ctx = H.context(prob)
+    f = hydro.Fom(ctx, bc)
+    x, v, e, g = H.dev(prob.x), H.dev(prob.v), H.dev(prob.e), H.dev(prob.gamma)
+    visc, cfl = hydro.Visc(prob.q1, prob.q2, prob.visc), hydro.Cfl(prob.alpha, prob.alpha_mu)
+    k0, i0 = f.energy(v, e)
+    import oracle
+    dt = 0.25 * oracle.force(prob)["dt"]
+    for _ in range(5):
+        dt_est, _ = f.step(x, v, e, g, visc, cfl, dt, cg_tol=1e-14, cg_max_iter=2000)
+        dt = min(dt, 0.5 * dt_est)
+    k1, i1 = f.energy(v, e)
+    assert ctx.status_sync()[0] == 0
+    assert abs((k1 + i1) - (k0 + i0)) <= 1e-11 * (k0 + i0)
+    assert k1 != k0   # the state actually evolved
+
+
+def test_step_deterministic():
+    prob = _box(2, 2, (7, 5))
+    m = prob.mesh
+    bc = ofom.bc_dofs_box(m)
+    prob.v.reshape(-1)[bc] = 0.0
+    outs = []
+    for _ in range(2):
+        ctx = H.context(prob)
+        f = hydro.Fom(ctx, bc)
+        x, v, e, g = H.dev(prob.x), H.dev(prob.v), H.dev(prob.e), H.dev(prob.gamma)
+        f.step(x, v, e, g, hydro.Visc(prob.q1, prob.q2, prob.visc), hydro.Cfl(0.5, 2.5), 1e-4)
+        outs.append([t.cpu().numpy() for t in (x, v, e)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
