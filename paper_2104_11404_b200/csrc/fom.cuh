@@ -158,6 +158,109 @@ mass_apply_kernel(const MassParams P) {
   }
 }
 
+// M_V apply for 3D Q2/Q1 with 4^3 points (C2/C4 meshes), one thread per (element,
+// component, q1): the lane's slice of the sum-factorised interpolation / projection lives in
+// registers (tables are compile-time constant-bank operands), the final q1 contraction
+// exchanges the four lanes' partial sums through shared memory (fixed order, deterministic).
+// wm: precomputed w_q m_q [E][64].  evec: [slot][3].
+__constant__ double c_mB24[4][3];  // Q2 GLL basis at the 4 GL points (filled at FOM setup)
+
+__global__ void __launch_bounds__(256) mass_apply3_q2_kernel(int32_t n_elem, int64_t n_nodes,
+                                                            const int32_t *__restrict__ elem_nodes,
+                                                            const int32_t *__restrict__ slot,
+                                                            const double *__restrict__ wm,
+                                                            const double *__restrict__ in,
+                                                            double *__restrict__ evec) {
+  // CTA = 64 (element, component) groups of 4 lanes (q1); elements [e0, e0 + 22) overlap it
+  __shared__ int sNode[23][27];
+  __shared__ double sX[64][27];
+  __shared__ double sP2[64][4][9];  // [group][q1][a2 + 3 a3]
+  const int tid = threadIdx.x;
+  const int q1 = tid & 3, grp = tid >> 2;
+  const int ec0 = blockIdx.x * 64;
+  const int e0 = ec0 / 3;
+  const int ec = ec0 + grp;
+  const bool valid = ec < n_elem * 3;
+  const int e = valid ? ec / 3 : 0, c = valid ? ec % 3 : 0;
+  const int le = e - e0;                       // element within the CTA window (0..22)
+  // (1) node ids of the window's elements (coalesced rows)
+  const int ne_win = min(23, n_elem - e0);
+  for (int i = tid; i < ne_win * 27; i += 256) sNode[i / 27][i % 27] = __ldg(elem_nodes + (int64_t)e0 * 27 + i);
+  __syncthreads();
+  // (2) each lane gathers a quarter of its group's 27 dofs
+  const double *src = in + (int64_t)c * n_nodes;
+  if (valid)
+    for (int a = q1; a < 27; a += 4) sX[grp][a] = __ldg(src + sNode[le][a]);
+  __syncthreads();
+  const double *X = sX[grp];
+  // stage 1: U1[a2][a3] = sum_a1 B[q1][a1] X[a1, a2, a3]
+  double b0, b1, b2;
+  if (q1 == 0) { b0 = c_mB24[0][0]; b1 = c_mB24[0][1]; b2 = c_mB24[0][2]; }
+  else if (q1 == 1) { b0 = c_mB24[1][0]; b1 = c_mB24[1][1]; b2 = c_mB24[1][2]; }
+  else if (q1 == 2) { b0 = c_mB24[2][0]; b1 = c_mB24[2][1]; b2 = c_mB24[2][2]; }
+  else { b0 = c_mB24[3][0]; b1 = c_mB24[3][1]; b2 = c_mB24[3][2]; }
+  double U1[9];
+#pragma unroll
+  for (int r = 0; r < 9; ++r) U1[r] = __fma_rn(b2, X[3 * r + 2], __fma_rn(b1, X[3 * r + 1], b0 * X[3 * r]));
+  // stage 2: U2[q2][a3] = sum_a2 B[q2][a2] U1[a2][a3]
+  double U2[4][3];
+#pragma unroll
+  for (int q2 = 0; q2 < 4; ++q2)
+#pragma unroll
+    for (int a3 = 0; a3 < 3; ++a3)
+      U2[q2][a3] = __fma_rn(c_mB24[q2][2], U1[2 + 3 * a3],
+                            __fma_rn(c_mB24[q2][1], U1[1 + 3 * a3], c_mB24[q2][0] * U1[3 * a3]));
+  // stage 3 + weights + first projection: P1[q2][a3] = sum_q3 B[q3][a3] wm V
+  const double *w = wm + (int64_t)e * 64 + q1;
+  double P1[4][3];
+#pragma unroll
+  for (int q2 = 0; q2 < 4; ++q2) {
+    P1[q2][0] = P1[q2][1] = P1[q2][2] = 0.0;
+#pragma unroll
+    for (int q3 = 0; q3 < 4; ++q3) {
+      double vq = __fma_rn(c_mB24[q3][2], U2[q2][2],
+                           __fma_rn(c_mB24[q3][1], U2[q2][1], c_mB24[q3][0] * U2[q2][0]));
+      vq = vq * __ldg(w + 4 * q2 + 16 * q3);
+#pragma unroll
+      for (int a3 = 0; a3 < 3; ++a3) P1[q2][a3] = __fma_rn(c_mB24[q3][a3], vq, P1[q2][a3]);
+    }
+  }
+  // P2[a2][a3] = sum_q2 B[q2][a2] P1[q2][a3]  -> shared, per lane q1
+#pragma unroll
+  for (int a2 = 0; a2 < 3; ++a2)
+#pragma unroll
+    for (int a3 = 0; a3 < 3; ++a3) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q2 = 0; q2 < 4; ++q2) acc = __fma_rn(c_mB24[q2][a2], P1[q2][a3], acc);
+      sP2[grp][q1][a2 + 3 * a3] = acc;
+    }
+  __syncwarp();
+  // Y[a1, a2, a3] = sum_q1 B[q1][a1] P2[q1][a2][a3]: lane q1 writes nodes a = q1, q1+4, ...
+  if (valid) {
+    const int32_t *sl = slot + (int64_t)e * 27;
+    for (int a = q1; a < 27; a += 4) {
+      const int a1 = a % 3, r = a / 3;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc = __fma_rn(c_mB24[k][a1], sP2[grp][k][r], acc);
+      evec[(int64_t)__ldg(sl + a) * 3 + c] = acc;
+    }
+  }
+}
+
+__global__ void wm_setup_kernel(int64_t n, int Q, int dim, const double *__restrict__ tab_w,
+                                const double *__restrict__ mq, double *__restrict__ wm) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nq = dim == 3 ? Q * Q * Q : Q * Q;
+  if (t >= n * nq) return;
+  const int q = (int)(t % nq);
+  const int q1 = q % Q, q2 = (q / Q) % Q, q3 = q / (Q * Q);
+  double w = tab_w[q1] * tab_w[q2];
+  if (dim == 3) w = w * tab_w[q3];
+  wm[t] = w * mq[t];
+}
+
 // y[c][node] = mask * sum over the node's slots (ascending) -- deterministic assembly
 template <int DIM>
 __global__ void assemble_masked_kernel(int64_t n_nodes, const int32_t *__restrict__ off,
@@ -242,7 +345,7 @@ __global__ void mass_e_update_kernel(int32_t n_elem, const double *__restrict__ 
 }
 
 // ---- deterministic dot product: fixed grid, fixed-order block trees, one final block
-constexpr int DOT_BLOCKS = 296, DOT_THREADS = 256;
+constexpr int DOT_BLOCKS = 148 * 8, DOT_THREADS = 256;
 
 __global__ void __launch_bounds__(DOT_THREADS) dot_partial_kernel(int64_t n, const double *__restrict__ a,
                                                                   const double *__restrict__ b,
@@ -262,11 +365,104 @@ __global__ void __launch_bounds__(DOT_THREADS) dot_partial_kernel(int64_t n, con
   if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
 }
 
-__global__ void dot_final_kernel(const double *__restrict__ part, double *__restrict__ out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double acc = 0.0;
-    for (int i = 0; i < DOT_BLOCKS; ++i) acc += part[i];
-    *out = acc;
+
+
+// Block-partial of a dot product inside another kernel's grid: each block writes the
+// fixed-order tree sum of its threads' values to part[blockIdx.x] (grid = DOT_BLOCKS
+// blocks of DOT_THREADS threads, each covering one contiguous chunk: deterministic).
+__device__ __forceinline__ void block_partial(double v, double *part) {
+  __shared__ double sh[DOT_THREADS];
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = DOT_THREADS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+// Ap = mask * assemble(evec) and part = block partials of p . Ap  (fused)
+template <int DIM>
+__global__ void __launch_bounds__(DOT_THREADS) assemble_dot_kernel(
+    int64_t n_nodes, const int32_t *__restrict__ off, const double *__restrict__ evec,
+    const double *__restrict__ mask, const double *__restrict__ p, double *__restrict__ Ap,
+    double *__restrict__ part) {
+  const int64_t chunk = (n_nodes + DOT_BLOCKS - 1) / DOT_BLOCKS;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < n_nodes ? lo + chunk : n_nodes;
+  double acc = 0.0;
+  for (int64_t node = lo + threadIdx.x; node < hi; node += DOT_THREADS) {
+    const int s0 = off[node], s1 = off[node + 1];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+      double y = 0.0;
+      for (int s = s0; s < s1; ++s) y += evec[(int64_t)s * DIM + c];
+      const int64_t i = (int64_t)c * n_nodes + node;
+      y = mask[i] * y;
+      Ap[i] = y;
+      acc = __fma_rn(p[i], y, acc);
+    }
+  }
+  block_partial(acc, part);
+}
+
+// x += alpha p; r -= alpha Ap; z = Dinv r;  part = block partials of r . z  (fused)
+__global__ void __launch_bounds__(DOT_THREADS) cg_xr_dot_kernel(
+    int64_t n, const double *__restrict__ sc, const double *__restrict__ p,
+    const double *__restrict__ Ap, const double *__restrict__ dinv, double *__restrict__ x,
+    double *__restrict__ r, double *__restrict__ z, double *__restrict__ part) {
+  const int64_t chunk = (n + DOT_BLOCKS - 1) / DOT_BLOCKS;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < n ? lo + chunk : n;
+  const double al = sc[2];
+  double acc = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) {
+    x[i] = __fma_rn(al, p[i], x[i]);
+    const double ri = __fma_rn(-al, Ap[i], r[i]);
+    r[i] = ri;
+    const double zi = dinv[i] * ri;
+    z[i] = zi;
+    acc = __fma_rn(ri, zi, acc);
+  }
+  block_partial(acc, part);
+}
+
+// Fixed-order sum of the DOT_BLOCKS partials by one 256-thread block: thread t adds
+// partials t, t+256, ... in order, then a fixed tree (deterministic, ~2 us instead of a
+// serial loop's ~40 us).
+__device__ __forceinline__ double sum_partials(const double *__restrict__ part) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < DOT_BLOCKS; i += 256) acc += part[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  return sh[0];
+}
+
+__global__ void __launch_bounds__(256) dot_final_kernel(const double *__restrict__ part,
+                                                        double *__restrict__ out) {
+  const double s_ = sum_partials(part);
+  if (threadIdx.x == 0) *out = s_;
+}
+
+// sc[1] = p.Ap ; alpha = rz / pAp      and      sc[3] = r.z ; beta = rz_new / rz ; rz = rz_new
+__global__ void __launch_bounds__(256) dot_final_alpha_kernel(const double *__restrict__ part, double *sc) {
+  const double s_ = sum_partials(part);
+  if (threadIdx.x == 0) {
+    sc[1] = s_;
+    sc[2] = sc[0] / s_;
+  }
+}
+__global__ void __launch_bounds__(256) dot_final_beta_kernel(const double *__restrict__ part, double *sc) {
+  const double s_ = sum_partials(part);
+  if (threadIdx.x == 0) {
+    sc[3] = s_;
+    sc[4] = s_ / sc[0];
+    sc[0] = s_;
   }
 }
 

@@ -731,7 +731,7 @@ hydro_status hydro_rom_project(int n, int64_t s_rows, int B, const double *P, co
 struct hydro_fom {
   hydro_ctx *c = nullptr;
   int64_t n = 0;  // dim * n_nodes
-  double *mask = nullptr, *dinv = nullptr, *Minv = nullptr, *csum = nullptr;
+  double *mask = nullptr, *dinv = nullptr, *Minv = nullptr, *csum = nullptr, *wm = nullptr;
   double *r = nullptr, *z = nullptr, *p = nullptr, *Ap = nullptr, *part = nullptr, *sc = nullptr;
   double *F1 = nullptr, *F1x = nullptr, *FTw = nullptr, *FTx = nullptr, *dv = nullptr;
   double *vh = nullptr, *eh = nullptr, *xh = nullptr, *v1 = nullptr, *vbar = nullptr,
@@ -769,9 +769,55 @@ hydro_status mass_apply_t(hydro_fom *f, const double *in, double *out, const dou
   return HYDRO_OK;
 }
 
+// Element part of M_V in (contributions into the context's slot buffer), 3D Q2 fast kernel
+// or the generic one.
+hydro_status mass_apply_elements(hydro_fom *f, const double *in, cudaStream_t s) {
+  const hydro_mesh_desc &d = f->c->d;
+  hydro_ctx *c = f->c;
+  if (d.dim == 3 && d.order_h1 == 2 && f->wm) {
+    const int64_t threads = d.n_elem * 3 * 4;
+    hk::mass_apply3_q2_kernel<<<blocks_for(threads, 256), 256, 0, s>>>(
+        (int32_t)d.n_elem, d.n_nodes, d.elem_nodes, c->slot, f->wm, in, c->evec);
+    g_launches++;
+    CUDA_OK(cudaGetLastError());
+    return HYDRO_OK;
+  }
+  hk::MassParams P;
+  P.n_elem = (int32_t)d.n_elem;
+  P.n_nodes = d.n_nodes;
+  P.elem_nodes = d.elem_nodes;
+  P.slot = c->slot;
+  P.mq = c->mq;
+  P.in = in;
+  P.evec = c->evec;
+  P.mode = 0;
+  P.tab_w = c->tab;
+  P.tab_B = c->tab + d.nq1d;
+  if (d.dim == 2 && d.order_h1 == 2) hk::mass_apply_kernel<2, 2, 4><<<(unsigned)d.n_elem, 64, 0, s>>>(P);
+  else if (d.dim == 3 && d.order_h1 == 2) hk::mass_apply_kernel<3, 2, 4><<<(unsigned)d.n_elem, 64, 0, s>>>(P);
+  else if (d.dim == 2 && d.order_h1 == 3) hk::mass_apply_kernel<2, 3, 6><<<(unsigned)d.n_elem, 64, 0, s>>>(P);
+  else hk::mass_apply_kernel<3, 3, 6><<<(unsigned)d.n_elem, 224, 0, s>>>(P);
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
 hydro_status mass_apply(hydro_fom *f, const double *in, double *out, const double *mask, int mode,
                         int invert, cudaStream_t s) {
   const hydro_mesh_desc &d = f->c->d;
+  if (mode == 0 && d.dim == 3 && d.order_h1 == 2 && f->wm) {
+    hydro_ctx *c = f->c;
+    const int64_t threads = d.n_elem * 3 * 4;
+    hk::mass_apply3_q2_kernel<<<blocks_for(threads, 256), 256, 0, s>>>(
+        (int32_t)d.n_elem, d.n_nodes, d.elem_nodes, c->slot, f->wm, in, c->evec);
+    g_launches++;
+    CUDA_OK(cudaGetLastError());
+    hk::assemble_masked_kernel<3><<<blocks_for(d.n_nodes, 256), 256, 0, s>>>(d.n_nodes, c->off, c->evec,
+                                                                             mask, out, invert);
+    g_launches++;
+    CUDA_OK(cudaGetLastError());
+    return HYDRO_OK;
+  }
   if (d.dim == 2 && d.order_h1 == 2) return mass_apply_t<2, 2, 4>(f, in, out, mask, mode, invert, s);
   if (d.dim == 3 && d.order_h1 == 2) return mass_apply_t<3, 2, 4>(f, in, out, mask, mode, invert, s);
   if (d.dim == 2 && d.order_h1 == 3) return mass_apply_t<2, 3, 6>(f, in, out, mask, mode, invert, s);
@@ -782,7 +828,7 @@ hydro_status mass_apply(hydro_fom *f, const double *in, double *out, const doubl
 hydro_status dot(hydro_fom *f, int64_t n, const double *a, const double *b, double *out,
                  cudaStream_t s) {
   hk::dot_partial_kernel<<<hk::DOT_BLOCKS, hk::DOT_THREADS, 0, s>>>(n, a, b, f->part);
-  hk::dot_final_kernel<<<1, 32, 0, s>>>(f->part, out);
+  hk::dot_final_kernel<<<1, 256, 0, s>>>(f->part, out);
   g_launches += 2;
   CUDA_OK(cudaGetLastError());
   return HYDRO_OK;
@@ -822,15 +868,22 @@ hydro_status pcg(hydro_fom *f, const double *b, double *x, double tol, int max_i
   double rel = 0.0;
   if (rz0 > 0.0) {
     rel = 1.0;
+    const hydro_mesh_desc &d = f->c->d;
     while (it < max_iter) {
-      if ((st = mass_apply(f, f->p, f->Ap, f->mask, 0, 0, s)) != HYDRO_OK) return st;
-      if ((st = dot(f, n, f->p, f->Ap, f->sc + 1, s)) != HYDRO_OK) return st;
-      hk::cg_alpha_kernel<<<1, 1, 0, s>>>(f->sc);
-      hk::cg_xr_kernel<<<g, 256, 0, s>>>(n, f->sc, f->p, f->Ap, f->dinv, x, f->r, f->z);
-      if ((st = dot(f, n, f->r, f->z, f->sc + 3, s)) != HYDRO_OK) return st;
-      hk::cg_beta_kernel<<<1, 1, 0, s>>>(f->sc);
+      // Ap = M p (element kernel into the slots, then fused masked assembly + p.Ap partials)
+      if ((st = mass_apply_elements(f, f->p, s)) != HYDRO_OK) return st;
+      if (d.dim == 3)
+        hk::assemble_dot_kernel<3><<<hk::DOT_BLOCKS, hk::DOT_THREADS, 0, s>>>(
+            d.n_nodes, f->c->off, f->c->evec, f->mask, f->p, f->Ap, f->part);
+      else
+        hk::assemble_dot_kernel<2><<<hk::DOT_BLOCKS, hk::DOT_THREADS, 0, s>>>(
+            d.n_nodes, f->c->off, f->c->evec, f->mask, f->p, f->Ap, f->part);
+      hk::dot_final_alpha_kernel<<<1, 256, 0, s>>>(f->part, f->sc);
+      hk::cg_xr_dot_kernel<<<hk::DOT_BLOCKS, hk::DOT_THREADS, 0, s>>>(n, f->sc, f->p, f->Ap, f->dinv,
+                                                                     x, f->r, f->z, f->part);
+      hk::dot_final_beta_kernel<<<1, 256, 0, s>>>(f->part, f->sc);
       hk::cg_p_kernel<<<g, 256, 0, s>>>(n, f->sc, f->z, f->p);
-      g_launches += 4;
+      g_launches += 5;
       CUDA_OK(cudaGetLastError());
       ++it;
       if (it % 4 == 0 || it == max_iter) {
@@ -884,6 +937,18 @@ hydro_status hydro_fom_create(hydro_ctx *c, const int64_t *bc_dofs, int64_t n_bc
     return fail(HYDRO_ERR_CUDA);
   if (cudaMemcpyAsync(f->mask, mask.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return fail(HYDRO_ERR_CUDA);
+  if (dim == 3 && c->d.order_h1 == 2) {
+    // w_q m_q for the register-resident 3D Q2 mass kernel, and its constant table
+    const int64_t nq = 64;
+    if (!alloc(&f->wm, (size_t)(E * nq))) return fail(HYDRO_ERR_CUDA);
+    hk::wm_setup_kernel<<<blocks_for(E * nq, 256), 256, 0, s>>>(E, 4, 3, c->tab, c->mq, f->wm);
+    g_launches++;
+    double hB[12];
+    if (cudaMemcpyAsync(hB, c->tab + 4, sizeof(hB), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess ||
+        cudaMemcpyToSymbolAsync(hk::c_mB24, hB, sizeof(hB), 0, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return fail(HYDRO_ERR_CUDA);
+  }
   // Jacobi preconditioner: 1 / diag(M_V) on the free dofs, 0 on the constrained ones
   hydro_status st = mass_apply(f, nullptr, f->dinv, f->mask, 1, 1, s);
   if (st != HYDRO_OK) return fail(st);
