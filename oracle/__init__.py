@@ -12,6 +12,8 @@ Contents:
   fom.py          -- the full-order RK2-average step: mass matrices by
                      their definition (np.kron tables, scipy.sparse assembly), sparse
                      direct solves, the force via hydro_oracle.c.
+  rom.py          -- the hyper-reduced ROM RK2-average online step: naive
+                     lifts and projections around the sampled force (NEXT-2).
 Parity pins for every function live in tests/test_oracle_pins.py.  Nothing here is
 "parity unpinned" except the physical fidelity of readings R3/R5 to Dobrev 2012
 (DESIGN.md), which no available source can check.

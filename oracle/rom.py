@@ -1,0 +1,92 @@
+"""CPU oracle of the hyper-reduced ROM online step -- TEST INFRASTRUCTURE ONLY
+(same import rules as oracle/__init__.py).
+
+PAPER.md Eq. RK2-avg-rom-hr with the lifted approximation
+Eq. discretesolrepresentation and the hyper-reduced projection
+Eq. sol-ls-hyper:
+
+    vhat^{n+1/2} = vhat^n - (dt/2) R_v f1(U~^n)_S            U~ = (v_os + Phi_v vhat, e_os + Phi_e ehat,
+    ehat^{n+1/2} = ehat^n + (dt/2) R_e ftv(U~^n; v~^{n+1/2})_S        x_os + Phi_x xhat)
+    xhat^{n+1/2} = xhat^n + (dt/2) (c_x + C_xv vhat^{n+1/2})
+    vhat^{n+1}   = vhat^n - dt R_v f1(U~^{n+1/2})_S
+    ehat^{n+1}   = ehat^n + dt R_e ftv(U~^{n+1/2}; v~bar)_S,    v~bar = v_os + Phi_v (vhat^n + vhat^{n+1})/2
+    xhat^{n+1}   = xhat^n + dt (c_x + C_xv vbarhat)
+
+R_v = Mhat_V^{-1} Phi_v^T Phi_F1 (Z^T Phi_F1)^+ and R_e likewise, C_xv = Phi_x^T Phi_v,
+c_x = Phi_x^T v_os are offline operators given to the step; the
+subscript S denotes the sampled rows (H1 dofs of the S0 nodes, L2 dofs of the S0
+elements; the lifting only on the sample-mesh closure).  Each instance b of a
+batch is an independent simulation with its own offsets, coordinates and dt.
+
+The force rows come from oracle.force on the closure elements with the lifted state
+written into a full-size state (outside the closure the values are irrelevant: those
+elements are not evaluated).  Pinned by tests/test_rom_oracle_pins.py (with full bases
+and a full sample, the ROM step is the FOM step of oracle/fom.py).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import force as _force
+
+
+def lift(Phi, os_, Y):
+    """os + Phi Y, os [rows] or [rows][B]."""
+    os2 = os_[:, None] if os_.ndim == 1 else os_
+    return os2 + Phi @ Y
+
+
+def sampled_force(batch_base, closure_elems, closure_nodes, s0_nodes, sample_elems, xS, vS, eS,
+                  wS, b):
+    """F.1 rows at the S0 nodes and F^T w rows of the S0 elements for instance b."""
+    m = batch_base.mesh
+    d, ncl, ne = m.dim, closure_nodes.size, m.ne
+    x = m.x0.copy()
+    x[:, closure_nodes] = xS[:, b].reshape(d, ncl)
+    v = np.zeros_like(m.x0)
+    v[:, closure_nodes] = vS[:, b].reshape(d, ncl)
+    w = np.zeros_like(m.x0)
+    w[:, closure_nodes] = wS[:, b].reshape(d, ncl)
+    e = batch_base.e.copy()
+    e[closure_elems] = eS[:, b].reshape(-1, ne)
+    r = _force(batch_base, elist=closure_elems, x=x, v=v, e=e, w=w)
+    F1 = r["F1"][:, s0_nodes].reshape(-1)
+    FT = r["FTw"][sample_elems].reshape(-1)
+    return F1, FT, r["dt"]
+
+
+def rom_rk2avg_step(op, Yx, Yv, Ye, dt):
+    """One hyper-reduced RK2-average step for every instance.  op: dict with keys
+    base, closure_elems, closure_nodes, s0_nodes, sample_elems, Phi_x, Phi_v, Phi_e
+    (closure rows), x_os, v_os, e_os, R_v, R_e, C_xv, c_x.  dt: [B].
+    Returns (Yx1, Yv1, Ye1, dt_est[B])."""
+    B = Yv.shape[1]
+    dt = np.asarray(dt, dtype=np.float64)
+    args = (op["base"], op["closure_elems"], op["closure_nodes"], op["s0_nodes"], op["sample_elems"])
+
+    def forces(xS, vS, eS, wS):
+        res = [sampled_force(*args, xS, vS, eS, wS, b) for b in range(B)]
+        F1 = np.stack([r[0] for r in res], axis=1)
+        FT = np.stack([r[1] for r in res], axis=1)
+        dts = np.array([r[2] for r in res])
+        return F1, FT, dts
+
+    xS = lift(op["Phi_x"], op["x_os"], Yx)
+    vS = lift(op["Phi_v"], op["v_os"], Yv)
+    eS = lift(op["Phi_e"], op["e_os"], Ye)
+    F1, _, dt1 = forces(xS, vS, eS, vS)
+    Yv_h = Yv - 0.5 * dt * (op["R_v"] @ F1)
+    vS_h = lift(op["Phi_v"], op["v_os"], Yv_h)
+    _, FT, _ = forces(xS, vS, eS, vS_h)
+    Ye_h = Ye + 0.5 * dt * (op["R_e"] @ FT)
+    Yx_h = Yx + 0.5 * dt * (op["c_x"][:, None] + op["C_xv"] @ Yv_h)
+    xS_h = lift(op["Phi_x"], op["x_os"], Yx_h)
+    eS_h = lift(op["Phi_e"], op["e_os"], Ye_h)
+    F1h, _, dt2 = forces(xS_h, vS_h, eS_h, vS_h)
+    Yv1 = Yv - dt * (op["R_v"] @ F1h)
+    Yvb = 0.5 * (Yv + Yv1)
+    vS_b = lift(op["Phi_v"], op["v_os"], Yvb)
+    _, FTh, _ = forces(xS_h, vS_h, eS_h, vS_b)
+    Ye1 = Ye + dt * (op["R_e"] @ FTh)
+    Yx1 = Yx + dt * (op["c_x"][:, None] + op["C_xv"] @ Yvb)
+    return Yx1, Yv1, Ye1, np.minimum(dt1, dt2)

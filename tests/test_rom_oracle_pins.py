@@ -1,0 +1,63 @@
+"""Pins of the hyper-reduced ROM-step oracle (oracle/rom.py):
+
+P21 with full bases (Phi = I), a full sample (every element, every row) and the exact
+    reduced operators R_v = M_V^{-1}, R_e = M_E^{-1}, C_xv = I, the hyper-reduced
+    RK2-average step IS the full-order RK2-average step:
+    compared with oracle/fom.py (independent formulation: sparse direct solves, no lift,
+    no sampling) over two steps;
+P22 lifting with a zero reduced coordinate returns the offset; a unit coordinate returns
+    the offset plus that basis column.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytest.importorskip("scipy")
+
+
+def test_P21_full_basis_rom_step_is_fom_step(oracle_lib):
+    from oracle import fom, rom
+    prob = W.sedov_like(51, 2, (3, 2), (0.0, 0.0), (0.3, 0.2), delta=0.08, e_floor=1e-2,
+                        vmode="uniform", vscale=0.1, name="romfull")
+    rng = np.random.default_rng(3)
+    prob.e[:] = 1.0 + 0.5 * rng.random(prob.e.shape)
+    m = prob.mesh
+    F = fom.Fom(m, np.zeros(0, dtype=np.int64))          # no boundary condition
+    d, n, E, ne = m.dim, m.n_nodes, m.n_elem, m.ne
+    Minv = np.linalg.inv(F.M.toarray())
+    R_v = np.kron(np.eye(d), Minv)                       # rows c*n + i (= F1 rows order)
+    R_e = np.zeros((E * ne, E * ne))
+    for k in range(E):
+        R_e[k * ne:(k + 1) * ne, k * ne:(k + 1) * ne] = np.linalg.inv(F.ME[k])
+    op = dict(base=prob, closure_elems=np.arange(E, dtype=np.int32),
+              closure_nodes=np.arange(n, dtype=np.int64), s0_nodes=np.arange(n, dtype=np.int64),
+              sample_elems=np.arange(E, dtype=np.int32),
+              Phi_x=np.eye(d * n), Phi_v=np.eye(d * n), Phi_e=np.eye(E * ne),
+              x_os=np.zeros(d * n), v_os=np.zeros(d * n), e_os=np.zeros((E * ne, 1)),
+              R_v=R_v, R_e=R_e, C_xv=np.eye(d * n), c_x=np.zeros(d * n))
+    Yx, Yv, Ye = (prob.x.reshape(-1, 1).copy(), prob.v.reshape(-1, 1).copy(),
+                  prob.e.reshape(-1, 1).copy())
+    x, v, e = prob.x.copy(), prob.v.copy(), prob.e.copy()
+    dt = 0.25 * oracle_lib.force(prob)["dt"]
+    for _ in range(2):
+        Yx, Yv, Ye, dt_rom = rom.rom_rk2avg_step(op, Yx, Yv, Ye, np.array([dt]))
+        x, v, e, dt_fom = fom.rk2avg_step(F, prob, x, v, e, dt)
+        assert dt_rom[0] == dt_fom or abs(dt_rom[0] - dt_fom) <= 1e-12 * dt_fom
+    assert np.abs(Yx[:, 0] - x.reshape(-1)).max() <= 1e-14 * np.abs(x).max()
+    assert np.abs(Yv[:, 0] - v.reshape(-1)).max() <= 1e-12 * np.abs(v).max()
+    assert np.abs(Ye[:, 0] - e.reshape(-1)).max() <= 1e-12 * np.abs(e).max()
+
+
+def test_P22_lift_basis_columns():
+    from oracle import rom
+    rng = np.random.default_rng(5)
+    Phi = rng.standard_normal((30, 4))
+    os_ = rng.standard_normal(30)
+    Y = np.zeros((4, 3))
+    assert np.array_equal(rom.lift(Phi, os_, Y), np.repeat(os_[:, None], 3, axis=1))
+    Y[2, 1] = 1.0
+    out = rom.lift(Phi, os_, Y)
+    assert np.array_equal(out[:, 1], os_ + Phi[:, 2])
