@@ -303,6 +303,9 @@ def bench_one(name, args, dev, flush, rank, world):
     else:
         out["e2e"] = e2e_rom(step_inputs=(Yx, Yv, Ye), step_outputs=(rv, re_, rx, dt), step=step,
                              n_qp=n_qp, args=args)
+        out["rom_rk2avg_step"] = bench_rom_step(plan, b, Phi_x, Phi_v, Phi_e, x_os, v_os, e_os,
+                                                Pv, Pe, Cxv, cx, Yx, Yv, Ye, gamma, visc, cfl, n_qp,
+                                                args, flush)
     # roofline of the dominant kernel (force kernel)
     out["roofline"] = roofline(name, base, m, n_units, kern_avg, prob)
     return out
@@ -324,6 +327,40 @@ def whole_job_value(per_rank_units, ms_max, world):
     """Whole-job throughput: units processed by all ranks / the slowest rank's time
     (weak scaling: every rank processes the full workload)."""
     return per_rank_units * world / (ms_max * 1e-3)
+
+
+def bench_rom_step(plan, b, Phi_x, Phi_v, Phi_e, x_os, v_os, e_os, Pv, Pe, Cxv, cx, Yx, Yv, Ye,
+                   gamma, visc, cfl, n_qp, args, flush):
+    """the full hyper-reduced RK2-average online step for the
+    64 instances of C4 (6 lifts, 4 sampled force passes, 4 projections, reduced updates),
+    captured as one CUDA graph (the step has no host synchronisation).  Offline operators:
+    the M-orthonormal-basis option, R = (Z^T Phi)^+."""
+    import torch
+    from paper_2104_11404_b200 import hydro
+    st = hydro.RomStepper(plan, Phi_x, Phi_v, Phi_e, x_os, v_os, e_os, Pv, Pe, Cxv, cx)
+    Y = [t.clone() for t in (Yx, Yv, Ye)]
+    dt = torch.full((b.B,), 1e-6, dtype=torch.float64, device=Yx.device)
+    dte = torch.empty_like(dt)
+    for _ in range(2):
+        st.step(*Y, gamma, visc, cfl, dt, dt_est=dte)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        st.step(*Y, gamma, visc, cfl, dt, dt_est=dte)
+    ms = []
+    for _ in range(max(2, args.steps // 4)):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    status = plan.status_sync()[0]
+    step_ms = float(np.median(ms))
+    return {"ms_per_step": step_ms, "instances": b.B, "sampled_force_passes": 4,
+            "qp_per_s": 4 * n_qp / (step_ms * 1e-3), "status": status,
+            "what": "hyper-reduced RK2-average step, 64 instances, CUDA-graph replay"}
 
 
 def e2e_full(ctx, prob, base, visc, cfl, n_qp, args, dev):

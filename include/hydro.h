@@ -200,6 +200,32 @@ hydro_status hydro_rk2avg_step(hydro_fom *fom, double *x, double *v, double *e,
                                double cg_tol, int cg_max_iter, double *dt_est /* host */,
                                int *cg_iters /* host */, hydro_stream_t stream);
 
+/* ------------------------------------------------------------------ ROM online step (NEXT-2) */
+/* The hyper-reduced RK2-average step of PAPER Eq. RK2-avg-rom-hr for the B
+ * instances of a sample plan, on device, in place on the reduced coordinates
+ * Yx [nx][B], Yv [nv][B], Ye [ne][B]:
+ *   vhat^{n+1/2} = vhat^n - dt/2 R_v f1(U~^n)_S,   ehat^{n+1/2} = ehat^n + dt/2 R_e ftv(U~^n; v~^{n+1/2})_S,
+ *   xhat^{n+1/2} = xhat^n + dt/2 (c_x + C_xv vhat^{n+1/2}),  and the second stage at U~^{n+1/2}
+ *   with vbarhat = (vhat^n + vhat^{n+1})/2,
+ * where U~ is lifted on the sample-mesh closure only through
+ * Phi_{x,v,e}_S (closure rows, [rows][n] row-major) and the offsets (os_batched_flags bit 0/1/2:
+ * x/v/e offset is [rows][B] instead of [rows]).  The offline operators are given:
+ * R_v = Mhat_V^-1 Phi_v^T Phi_F1 (Z^T Phi_F1)^+ [nv][s_v], R_e likewise [ne][s_e] (Eq.
+ * sol-ls-hyper), C_xv = Phi_x^T Phi_v [nx][nv], c_x = Phi_x^T v_os [nx].
+ * dt: device [B] per-instance step; dt_est (device [B] or NULL) = min over both stages'
+ * estimates.  Four sampled force evaluations per step.  All device pointers are
+ * kept by the object and must outlive it; buffers are allocated at create (setup).       */
+typedef struct hydro_rom hydro_rom;
+hydro_status hydro_rom_create(hydro_sample *plan, int nx, int nv, int ne, const double *Phi_x_S,
+                              const double *Phi_v_S, const double *Phi_e_S, const double *x_os_S,
+                              const double *v_os_S, const double *e_os_S, int os_batched_flags,
+                              const double *R_v, const double *R_e, const double *C_xv,
+                              const double *c_x, hydro_rom **out /* host */);
+hydro_status hydro_rom_destroy(hydro_rom *rom);
+hydro_status hydro_rom_rk2avg_step(hydro_rom *rom, double *Yx, double *Yv, double *Ye,
+                                   const double *gamma, hydro_visc visc, hydro_cfl cfl,
+                                   const double *dt, double *dt_est, hydro_stream_t stream);
+
 /* ------------------------------------------------------------------ profiling (host) */
 /* When enabled, every hydro_force_full / hydro_dt_estimate / hydro_force_sampled call
  * records a pair of CUDA events around its force kernel on the call's stream (the

@@ -522,4 +522,21 @@ __global__ void avg_kernel(int64_t n, const double *__restrict__ a, const double
   out[i] = 0.5 * (a[i] + b[i]);
 }
 
+// ---- hyper-reduced ROM step vector ops on [n][B] arrays (instance fastest), per-instance dt
+// out[i][b] = a[i][b] + s * dt[b] * r[i][b]
+__global__ void rom_axpy_kernel(int64_t n, int B, const double *__restrict__ a, double s,
+                                const double *__restrict__ dt, const double *__restrict__ r,
+                                double *__restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * B) return;
+  const int b = (int)(t % B);
+  out[t] = a[t] + (s * dt[b]) * r[t];
+}
+
+__global__ void min2_kernel(int B, const double *__restrict__ a, const double *__restrict__ b,
+                            double *__restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < B) out[i] = (a[i] < b[i] || b[i] != b[i]) ? a[i] : b[i];  // NaN in b propagates
+}
+
 }  // namespace hk

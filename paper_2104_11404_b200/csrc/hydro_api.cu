@@ -1061,4 +1061,139 @@ hydro_status hydro_rk2avg_step(hydro_fom *f, double *x, double *v, double *e, co
   return HYDRO_OK;
 }
 
+
+// ------------------------------------------------------------------------------ ROM step
+}  // extern "C"
+
+struct hydro_rom {
+  hydro_sample *p = nullptr;
+  int B = 0, nx = 0, nv = 0, ne = 0, os_flags = 0;
+  int64_t rows_h1 = 0, rows_l2 = 0, s_v = 0, s_e = 0;
+  const double *Phi_x = nullptr, *Phi_v = nullptr, *Phi_e = nullptr;
+  const double *x_os = nullptr, *v_os = nullptr, *e_os = nullptr;
+  const double *R_v = nullptr, *R_e = nullptr, *C_xv = nullptr, *c_x = nullptr;
+  double *xS = nullptr, *vS = nullptr, *eS = nullptr, *wS = nullptr, *F1r = nullptr,
+         *F1x = nullptr, *FTr = nullptr, *FTx = nullptr, *rv = nullptr, *re = nullptr,
+         *rx = nullptr, *Yv_h = nullptr, *Ye_h = nullptr, *Yx_h = nullptr, *Yv1 = nullptr,
+         *Yvb = nullptr, *dt1 = nullptr, *dt2 = nullptr, *wsv = nullptr, *wse = nullptr;
+  size_t wsv_bytes = 0, wse_bytes = 0;
+  std::vector<void *> allocs;
+};
+
+extern "C" {
+
+hydro_status hydro_rom_create(hydro_sample *p, int nx, int nv, int ne, const double *Phi_x_S,
+                              const double *Phi_v_S, const double *Phi_e_S, const double *x_os_S,
+                              const double *v_os_S, const double *e_os_S, int os_batched_flags,
+                              const double *R_v, const double *R_e, const double *C_xv,
+                              const double *c_x, hydro_rom **out) {
+  if (!p || !out || nx <= 0 || nv <= 0 || ne <= 0 || nx > 256 || nv > hk::PROJ_MAXN ||
+      ne > hk::PROJ_MAXN || nv > 256 || !Phi_x_S || !Phi_v_S || !Phi_e_S || !x_os_S || !v_os_S ||
+      !e_os_S || !R_v || !R_e || !C_xv || !c_x || p->B > hk::PROJ_MAXB)
+    return HYDRO_ERR_ARG;
+  *out = nullptr;
+  hydro_rom *r = new hydro_rom();
+  r->p = p;
+  r->B = p->B;
+  r->nx = nx; r->nv = nv; r->ne = ne;
+  r->os_flags = os_batched_flags;
+  const hydro_ctx *c = p->ctx;
+  r->rows_h1 = (int64_t)c->d.dim * p->n_cl_nodes;
+  r->rows_l2 = p->n_cl * c->ne;
+  r->s_v = p->n_s0_nodes * c->d.dim;
+  r->s_e = p->n_s0 * c->ne;
+  r->Phi_x = Phi_x_S; r->Phi_v = Phi_v_S; r->Phi_e = Phi_e_S;
+  r->x_os = x_os_S; r->v_os = v_os_S; r->e_os = e_os_S;
+  r->R_v = R_v; r->R_e = R_e; r->C_xv = C_xv; r->c_x = c_x;
+  auto fail = [&](hydro_status st) { hydro_rom_destroy(r); return st; };
+  auto alloc = [&](double **ptr, size_t count) {
+    void *q = nullptr;
+    if (cudaMalloc(&q, sizeof(double) * (count > 0 ? count : 1)) != cudaSuccess) return false;
+    r->allocs.push_back(q);
+    *ptr = (double *)q;
+    return true;
+  };
+  const size_t B = (size_t)r->B, h1 = (size_t)r->rows_h1 * B, l2 = (size_t)r->rows_l2 * B;
+  r->wsv_bytes = hydro_rom_project_workspace_bytes(nv, r->s_v, r->B);
+  r->wse_bytes = hydro_rom_project_workspace_bytes(ne, r->s_e, r->B);
+  if (!alloc(&r->xS, h1) || !alloc(&r->vS, h1) || !alloc(&r->eS, l2) || !alloc(&r->wS, h1) ||
+      !alloc(&r->F1r, (size_t)r->s_v * B) || !alloc(&r->F1x, (size_t)r->s_v * B) ||
+      !alloc(&r->FTr, (size_t)r->s_e * B) || !alloc(&r->FTx, (size_t)r->s_e * B) ||
+      !alloc(&r->rv, (size_t)nv * B) || !alloc(&r->re, (size_t)ne * B) || !alloc(&r->rx, (size_t)nx * B) ||
+      !alloc(&r->Yv_h, (size_t)nv * B) || !alloc(&r->Ye_h, (size_t)ne * B) ||
+      !alloc(&r->Yx_h, (size_t)nx * B) || !alloc(&r->Yv1, (size_t)nv * B) ||
+      !alloc(&r->Yvb, (size_t)nv * B) || !alloc(&r->dt1, B) || !alloc(&r->dt2, B) ||
+      !alloc(&r->wsv, r->wsv_bytes / 8 + 1) || !alloc(&r->wse, r->wse_bytes / 8 + 1))
+    return fail(HYDRO_ERR_CUDA);
+  *out = r;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_rom_destroy(hydro_rom *r) {
+  if (!r) return HYDRO_OK;
+  for (void *q : r->allocs) cudaFree(q);
+  delete r;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_rom_rk2avg_step(hydro_rom *r, double *Yx, double *Yv, double *Ye,
+                                   const double *gamma, hydro_visc visc, hydro_cfl cfl,
+                                   const double *dt, double *dt_est, hydro_stream_t stream) {
+  if (!r || !Yx || !Yv || !Ye || !gamma || !dt) return HYDRO_ERR_ARG;
+  const int B = r->B;
+  hydro_status st;
+  auto lift = [&](const double *Phi, const double *os, int batched, int64_t rows, int n,
+                  const double *Y, double *o) {
+    return hydro_rom_lift(rows, n, B, Phi, os, batched, Y, o, stream);
+  };
+  auto proj = [&](const double *P, int n, int64_t s_rows, const double *f, double *o, double *ws,
+                  size_t wsb) {
+    return hydro_rom_project(n, s_rows, B, P, f, o, ws, wsb, stream);
+  };
+  auto axpy = [&](int64_t n, const double *a, double sc, const double *rr, double *o) {
+    hk::rom_axpy_kernel<<<blocks_for(n * B, 256), 256, 0, (cudaStream_t)stream>>>(n, B, a, sc, dt, rr, o);
+    g_launches++;
+    return cudaGetLastError() == cudaSuccess ? HYDRO_OK : HYDRO_ERR_CUDA;
+  };
+  const int fx = r->os_flags & 1, fv = (r->os_flags >> 1) & 1, fe = (r->os_flags >> 2) & 1;
+#define RS(call) do { if ((st = (call)) != HYDRO_OK) return st; } while (0)
+  // ---- stage 1 at the lifted U~^n
+  RS(lift(r->Phi_x, r->x_os, fx, r->rows_h1, r->nx, Yx, r->xS));
+  RS(lift(r->Phi_v, r->v_os, fv, r->rows_h1, r->nv, Yv, r->vS));
+  RS(lift(r->Phi_e, r->e_os, fe, r->rows_l2, r->ne, Ye, r->eS));
+  RS(hydro_force_sampled(r->p, r->xS, r->vS, r->eS, nullptr, gamma, visc, cfl, r->F1r, r->FTx, r->dt1, stream));
+  RS(proj(r->R_v, r->nv, r->s_v, r->F1r, r->rv, r->wsv, r->wsv_bytes));
+  RS(axpy(r->nv, Yv, -0.5, r->rv, r->Yv_h));                                   // vhat^{n+1/2}
+  RS(lift(r->Phi_v, r->v_os, fv, r->rows_h1, r->nv, r->Yv_h, r->wS));          // v~^{n+1/2}
+  RS(hydro_force_sampled(r->p, r->xS, r->vS, r->eS, r->wS, gamma, visc, cfl, r->F1x, r->FTr, nullptr, stream));
+  RS(proj(r->R_e, r->ne, r->s_e, r->FTr, r->re, r->wse, r->wse_bytes));
+  RS(axpy(r->ne, Ye, 0.5, r->re, r->Ye_h));                                    // ehat^{n+1/2}
+  RS(lift(r->C_xv, r->c_x, 0, r->nx, r->nv, r->Yv_h, r->rx));                  // c_x + C_xv vhat
+  RS(axpy(r->nx, Yx, 0.5, r->rx, r->Yx_h));                                    // xhat^{n+1/2}
+  // ---- stage 2 at U~^{n+1/2} (its velocity is wS)
+  RS(lift(r->Phi_x, r->x_os, fx, r->rows_h1, r->nx, r->Yx_h, r->xS));
+  RS(lift(r->Phi_e, r->e_os, fe, r->rows_l2, r->ne, r->Ye_h, r->eS));
+  RS(hydro_force_sampled(r->p, r->xS, r->wS, r->eS, nullptr, gamma, visc, cfl, r->F1r, r->FTx, r->dt2, stream));
+  RS(proj(r->R_v, r->nv, r->s_v, r->F1r, r->rv, r->wsv, r->wsv_bytes));
+  RS(axpy(r->nv, Yv, -1.0, r->rv, r->Yv1));                                    // vhat^{n+1}
+  hk::avg_kernel<<<blocks_for((int64_t)r->nv * B, 256), 256, 0, (cudaStream_t)stream>>>(
+      (int64_t)r->nv * B, Yv, r->Yv1, r->Yvb);
+  g_launches++;
+  RS(lift(r->Phi_v, r->v_os, fv, r->rows_h1, r->nv, r->Yvb, r->vS));           // v~bar
+  RS(hydro_force_sampled(r->p, r->xS, r->wS, r->eS, r->vS, gamma, visc, cfl, r->F1x, r->FTr, nullptr, stream));
+  RS(proj(r->R_e, r->ne, r->s_e, r->FTr, r->re, r->wse, r->wse_bytes));
+  RS(axpy(r->ne, Ye, 1.0, r->re, Ye));                                         // ehat^{n+1}
+  RS(lift(r->C_xv, r->c_x, 0, r->nx, r->nv, r->Yvb, r->rx));
+  RS(axpy(r->nx, Yx, 1.0, r->rx, Yx));                                         // xhat^{n+1}
+  CUDA_OK(cudaMemcpyAsync(Yv, r->Yv1, sizeof(double) * (size_t)r->nv * B, cudaMemcpyDeviceToDevice,
+                          (cudaStream_t)stream));
+  if (dt_est) {
+    hk::min2_kernel<<<blocks_for(B, 128), 128, 0, (cudaStream_t)stream>>>(B, r->dt1, r->dt2, dt_est);
+    g_launches++;
+  }
+#undef RS
+  CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
 }  // extern "C"

@@ -29,7 +29,8 @@ EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy"
             "hydro_rom_project", "hydro_basis_tables", "hydro_launch_count", "hydro_version",
             "hydro_profile_enable", "hydro_profile_read", "hydro_selftest_ieee_fast",
             "hydro_fom_create", "hydro_fom_destroy", "hydro_mass_v_apply", "hydro_mass_v_solve",
-            "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step"]
+            "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_rom_create",
+            "hydro_rom_destroy", "hydro_rom_rk2avg_step"]
 
 
 class HydroError(RuntimeError):
@@ -90,6 +91,10 @@ def lib() -> ctypes.CDLL:
         L.hydro_fom_energy.argtypes = [vp, vp, vp, ctypes.POINTER(dbl), ctypes.POINTER(dbl), vp]
         L.hydro_rk2avg_step.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, dbl, dbl, i32,
                                         ctypes.POINTER(dbl), ctypes.POINTER(i32), vp]
+        L.hydro_rom_create.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp,
+                                       vp, ctypes.POINTER(vp)]
+        L.hydro_rom_destroy.argtypes = [vp]
+        L.hydro_rom_rk2avg_step.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, vp, vp, vp]
         L.hydro_rom_project_workspace_bytes.restype = ctypes.c_size_t
         L.hydro_rom_project_workspace_bytes.argtypes = [i32, i64, i32]
         L.hydro_rom_project.argtypes = [i32, i64, i32, vp, vp, vp, vp, ctypes.c_size_t, vp]
@@ -388,3 +393,36 @@ class Fom:
                                        dt, cg_tol, cg_max_iter, ctypes.byref(d), ctypes.byref(it),
                                        _stream(stream)), "hydro_rk2avg_step")
         return d.value, it.value
+
+
+class RomStepper:
+    """Hyper-reduced RK2-average online step (hydro_rom_*; PAPER Eq. RK2-avg-rom-hr
+    P:847-906) for the B instances of a SamplePlan.  Keeps references to its operands."""
+
+    def __init__(self, plan: SamplePlan, Phi_x, Phi_v, Phi_e, x_os, v_os, e_os, R_v, R_e, C_xv, c_x):
+        self._keep = [t.contiguous() for t in (Phi_x, Phi_v, Phi_e, x_os, v_os, e_os, R_v, R_e, C_xv, c_x)]
+        Phi_x, Phi_v, Phi_e, x_os, v_os, e_os, R_v, R_e, C_xv, c_x = self._keep
+        flags = (1 if x_os.dim() == 2 else 0) | (2 if v_os.dim() == 2 else 0) | (4 if e_os.dim() == 2 else 0)
+        h = ctypes.c_void_p()
+        _check(lib().hydro_rom_create(plan._h, Phi_x.shape[1], Phi_v.shape[1], Phi_e.shape[1], _ptr(Phi_x),
+                                      _ptr(Phi_v), _ptr(Phi_e), _ptr(x_os), _ptr(v_os), _ptr(e_os), flags,
+                                      _ptr(R_v), _ptr(R_e), _ptr(C_xv), _ptr(c_x), ctypes.byref(h)),
+               "hydro_rom_create")
+        self._h, self.plan = h, plan
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) and self._h.value:
+                lib().hydro_rom_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def step(self, Yx, Yv, Ye, gamma, visc: Visc, cfl: Cfl, dt, dt_est=None, stream=None):
+        """In place on (Yx, Yv, Ye); dt: device [B]; returns dt_est (device [B])."""
+        if dt_est is None:
+            dt_est = torch.empty_like(dt)
+        _check(lib().hydro_rom_rk2avg_step(self._h, _ptr(Yx), _ptr(Yv), _ptr(Ye), _ptr(gamma), visc.c(),
+                                           cfl.c(), _ptr(dt), _ptr(dt_est), _stream(stream)),
+               "hydro_rom_rk2avg_step")
+        return dt_est

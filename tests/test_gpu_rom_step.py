@@ -1,0 +1,86 @@
+"""GPU parity of the hyper-reduced ROM RK2-average online step (SURVEY 8(f) NEXT-2,
+PAPER Eq. RK2-avg-rom-hr) against oracle/rom.py on a C4-shaped batch (3D Q2
+sample mesh, B instances with their own energy offsets and per-instance dt): reduced
+coordinates after two steps within 1e-10 (relative to their scale), stage dt estimates
+within 1e-10 (the lifted states differ at the rounding level of the two GEMM orders, so
+dt is not compared bitwise here; the sampled force itself is bit-exact in dt given equal
+inputs, tests/test_gpu_rom.py).  The offline operators use the M-orthonormal-basis option
+of P:716-723 (Mhat = I): R_v = (Z^T Phi_v)^+, R_e = (Z^T Phi_e)^+."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from tests import gpu_helpers as H  # noqa: E402
+from paper_2104_11404_b200 import hydro  # noqa: E402
+from oracle import rom as orom  # noqa: E402
+
+
+@pytest.mark.parametrize("dim", [3, 2])
+def test_rom_step_matches_oracle(dim):
+    if dim == 3:
+        batch = W.c4(n_sample=6, B=3, small_mesh=True)
+    else:
+        batch = W.rom_batch(W.small("c0"), B=3, n_sample=5, n_red=8)
+    base = batch.base
+    P_v, P_e, C_xv, c_x = W.offline_projectors(batch)
+    ctx = H.context(base)
+    plan = hydro.SamplePlan(ctx, batch.sample_elems, batch.B)
+    st = hydro.RomStepper(plan, H.dev(batch.Phi_x), H.dev(batch.Phi_v), H.dev(batch.Phi_e),
+                          H.dev(batch.x_os), H.dev(batch.v_os), H.dev(batch.e_os), H.dev(P_v),
+                          H.dev(P_e), H.dev(C_xv), H.dev(c_x))
+    op = dict(base=base, closure_elems=batch.closure_elems, closure_nodes=batch.closure_nodes,
+              s0_nodes=batch.s0_nodes, sample_elems=batch.sample_elems, Phi_x=batch.Phi_x,
+              Phi_v=batch.Phi_v, Phi_e=batch.Phi_e, x_os=batch.x_os, v_os=batch.v_os,
+              e_os=batch.e_os, R_v=P_v, R_e=P_e, C_xv=C_xv, c_x=c_x)
+    Yx, Yv, Ye = H.dev(batch.Yx), H.dev(batch.Yv), H.dev(batch.Ye)
+    rx, rv, re = batch.Yx.copy(), batch.Yv.copy(), batch.Ye.copy()
+    visc, cfl = hydro.Visc(base.q1, base.q2, base.visc), hydro.Cfl(base.alpha, base.alpha_mu)
+    g = H.dev(base.gamma)
+    # per-instance steps: a fraction of each instance's own stability estimate
+    _, _, _, dt0 = orom.rom_rk2avg_step(op, rx, rv, re, np.zeros(batch.B))
+    dt = 0.2 * dt0 * (1.0 + 0.1 * np.arange(batch.B))
+    for _ in range(2):
+        dte = st.step(Yx, Yv, Ye, g, visc, cfl, H.dev(dt))
+        rx, rv, re, dte_ref = orom.rom_rk2avg_step(op, rx, rv, re, dt)
+        assert plan.status_sync()[0] == 0
+        np.testing.assert_allclose(dte.cpu().numpy(), dte_ref, rtol=1e-10)
+    for got, want, what in ((Yx, rx, "xhat"), (Yv, rv, "vhat"), (Ye, re, "ehat")):
+        g_ = got.cpu().numpy()
+        assert np.abs(g_ - want).max() <= 1e-10 * np.abs(want).max(), what
+    # the state moved
+    assert np.abs(rv - batch.Yv).max() > 0
+
+
+def test_rom_step_instances_independent():
+    """Instance b of a batch steps exactly like a B = 1 plan of that instance."""
+    batch = W.c4(n_sample=4, B=3, small_mesh=True)
+    base = batch.base
+    P_v, P_e, C_xv, c_x = W.offline_projectors(batch)
+    ctx = H.context(base)
+    visc, cfl = hydro.Visc(base.q1, base.q2, base.visc), hydro.Cfl(base.alpha, base.alpha_mu)
+    g = H.dev(base.gamma)
+    dt = np.full(batch.B, 2e-5)
+
+    def run(B, sl):
+        plan = hydro.SamplePlan(ctx, batch.sample_elems, B)
+        st = hydro.RomStepper(plan, H.dev(batch.Phi_x), H.dev(batch.Phi_v), H.dev(batch.Phi_e),
+                              H.dev(batch.x_os), H.dev(batch.v_os),
+                              H.dev(np.ascontiguousarray(batch.e_os[:, sl])), H.dev(P_v), H.dev(P_e),
+                              H.dev(C_xv), H.dev(c_x))
+        Y = [H.dev(np.ascontiguousarray(a[:, sl])) for a in (batch.Yx, batch.Yv, batch.Ye)]
+        st.step(*Y, g, visc, cfl, H.dev(np.ascontiguousarray(dt[sl])))
+        torch.cuda.synchronize()
+        return [y.cpu().numpy() for y in Y]
+
+    full = run(batch.B, slice(0, batch.B))
+    one = run(1, slice(1, 2))
+    for a, b in zip(full, one):
+        assert np.array_equal(a[:, 1], b[:, 0])
