@@ -358,8 +358,8 @@ def bench_rom_step(plan, b, Phi_x, Phi_v, Phi_e, x_os, v_os, e_os, Pv, Pe, Cxv, 
         ms.append(e0.elapsed_time(e1))
     status = plan.status_sync()[0]
     step_ms = float(np.median(ms))
-    return {"ms_per_step": step_ms, "instances": b.B, "sampled_force_passes": 4,
-            "qp_per_s": 4 * n_qp / (step_ms * 1e-3), "status": status,
+    return {"ms_per_step": step_ms, "instances": b.B, "sampled_force_passes": 2,
+            "transpose_passes": 2, "qp_per_s": 2 * n_qp / (step_ms * 1e-3), "status": status,
             "what": "hyper-reduced RK2-average step, 64 instances, CUDA-graph replay"}
 
 
@@ -508,12 +508,13 @@ def bench_fom(name, args, dev):
     E1 = sum(fom.energy(v, e))
     step_ms = float(np.median(ms))
     return {"workload": f"fom_{name}", "ms_per_step": step_ms,
-            "force_evals_per_step": 4, "force_ms_per_step": kern_ms / max(kern_n, 1) * 4,
+            "force_evals_per_step": 2, "transpose_passes_per_step": 2,
+            "force_ms_per_step": kern_ms / max(len(ms), 1),
             "cg_iterations_per_step": float(np.mean(iters)), "cg_tol": 1e-12,
-            "qp_per_s_force": 4 * m.n_elem * m.nq ** m.dim / (step_ms * 1e-3),
+            "qp_per_s_force": 2 * m.n_elem * m.nq ** m.dim / (step_ms * 1e-3),
             "rel_energy_drift": abs(E1 - E0) / E0, "status": st[0],
-            "what": "RK2-average step (PAPER P:463-508): 4 force evaluations, 2 PCG solves of "
-                    "M_V, 2 M_E block solves, v.n=0 on the box"}
+            "what": "RK2-average step (PAPER P:463-508): 2 force evaluations storing S_q + 2 "
+                    "F^T w passes from S_q, 2 PCG solves of M_V, 2 M_E block solves, v.n=0"}
 
 
 def _rotations_per_lmin3(name, prob):

@@ -102,6 +102,19 @@ hydro_status hydro_force_full(hydro_ctx *ctx, const double *x, const double *v, 
 hydro_status hydro_dt_estimate(hydro_ctx *ctx, const double *x, const double *v, const double *e,
                                const double *gamma, hydro_visc visc, hydro_cfl cfl, double *dt,
                                hydro_stream_t stream);
+/* Two-pass form of F^T w for time integrators whose w depends on F.1 (RK2-average: w =
+ * v^{n+1/2} = v^n - dt/2 M_V^-1 F.1).  hydro_force_full_store is hydro_force_full
+ * with w = v that also stores the point stresses S_q = w_q detJ sigma J^-T in S (device,
+ * hydro_force_stress_bytes(ctx) bytes, [n_elem][dim*dim][q^dim]); hydro_force_transpose then
+ * evaluates FTw = F^T w = sum_q psi_j (S_q : gradhat w_q) for any w from the stored S without
+ * repeating the pointwise stage (FTw within the element-local tolerance of hydro_force_full
+ * with the same w).                                                                          */
+size_t hydro_force_stress_bytes(const hydro_ctx *ctx);
+hydro_status hydro_force_full_store(hydro_ctx *ctx, const double *x, const double *v, const double *e,
+                                    const double *gamma, hydro_visc visc, hydro_cfl cfl, double *F1,
+                                    double *FTw, double *dt, double *S, hydro_stream_t stream);
+hydro_status hydro_force_transpose(hydro_ctx *ctx, const double *S, const double *w, double *FTw,
+                                   hydro_stream_t stream);
 /* Synchronises `stream`, returns the sticky device condition (TANGLED before NONFINITE)
  * and clears it.  *first_bad_elem (host, may be NULL) = lowest tangled element or -1.    */
 hydro_status hydro_status_sync(hydro_ctx *ctx, hydro_stream_t stream, int64_t *first_bad_elem);
@@ -145,6 +158,15 @@ hydro_status hydro_force_sampled(hydro_sample *s, const double *x_S, const doubl
                                  const double *e_S, const double *w_S, const double *gamma,
                                  hydro_visc visc, hydro_cfl cfl, double *F1_rows,
                                  double *FTw_rows, double *dt, hydro_stream_t stream);
+/* The sampled two-pass form (see hydro_force_full_store): S [n_closure_elem*B][dim*dim][q^dim]
+ * of hydro_sample_stress_bytes(plan) bytes; w_S: closure H1 rows [dim*n_cl_nodes][B].          */
+size_t hydro_sample_stress_bytes(const hydro_sample *s);
+hydro_status hydro_force_sampled_store(hydro_sample *s, const double *x_S, const double *v_S,
+                                       const double *e_S, const double *gamma, hydro_visc visc,
+                                       hydro_cfl cfl, double *F1_rows, double *FTw_rows, double *dt,
+                                       double *S, hydro_stream_t stream);
+hydro_status hydro_sample_force_transpose(hydro_sample *s, const double *S, const double *w_S,
+                                          double *FTw_rows, hydro_stream_t stream);
 /* Sticky status of the sample plan (same semantics as hydro_status_sync; the element
  * index is global).                                                                        */
 hydro_status hydro_sample_status_sync(hydro_sample *s, hydro_stream_t stream,

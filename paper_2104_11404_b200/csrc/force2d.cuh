@@ -49,7 +49,7 @@ template <bool VISC, bool HAS_W, class AR>
 __device__ __forceinline__ void column2d(AR &ar, int q1, const double (&UB)[6][3],
                                          const double (&UG)[6][3], const double (&E1)[2],
                                          const double *__restrict__ mqp, double gam,
-                                         const PhysIn &ph, ColOut &o) {
+                                         const PhysIn &ph, ColOut &o, double *Sst) {
 #pragma unroll
   for (int c = 0; c < 2; ++c)
 #pragma unroll
@@ -90,6 +90,12 @@ __device__ __forceinline__ void column2d(AR &ar, int q1, const double (&UB)[6][3
     PointOut po;
     pointwise<2, VISC, HAS_W, false>(ar, J, Gv, Gw, eq, __ldg(mqp + 4 * q2), gam, wq1 * c_t24.w[q2],
                                      ph, po);
+    if (Sst) {  // stored S_q = w_q detJ sigma J^-T, [cd][q] with q = q1 + 4 q2
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int d = 0; d < 2; ++d) Sst[(c * 2 + d) * 16 + q1 + 4 * q2] = po.S[c][d];
+    }
     o.tangled = o.tangled || !(po.det > 0.0);
     if (isnan(po.dtq)) o.nan = true;
     else {
@@ -164,6 +170,7 @@ __global__ void __maxnreg__(128) force2d_kernel(const Params P) {
   const PhysIn ph{P.q1, P.q2, P.alpha, P.alpha_mu};
   unsigned long long kmin = ~0ull;
   bool tangled = false, nan = false;
+  double *Sst = (MODE == MODE_FORCE && P.S_store && valid) ? P.S_store + (int64_t)g * 4 * NQ : nullptr;
 
 #pragma unroll 1
   for (int q1 = 0; q1 < 4; ++q1) {
@@ -196,10 +203,10 @@ __global__ void __maxnreg__(128) force2d_kernel(const Params P) {
     ColOut co;
     {
       ArithFast af;
-      column2d<VISC, HAS_W>(af, q1, UB, UG, E1, mqp, gam, ph, co);
+      column2d<VISC, HAS_W>(af, q1, UB, UG, E1, mqp, gam, ph, co, Sst);
       if (!af.ok) {
         ArithIeee ai;
-        column2d<VISC, HAS_W>(ai, q1, UB, UG, E1, mqp, gam, ph, co);
+        column2d<VISC, HAS_W>(ai, q1, UB, UG, E1, mqp, gam, ph, co, Sst);
       }
     }
     kmin = co.kmin < kmin ? co.kmin : kmin;

@@ -253,6 +253,12 @@ force3d_kernel(const Params P) {
     }
     // ---- S6 dt: flags; key min per thread (full) or per unit (batched)
     const bool pt = lt < NQ;
+    if (MODE == MODE_FORCE && P.S_store && pt) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) P.S_store[((int64_t)u * 9 + c * 3 + d) * NQ + lt] = po.S[c][d];
+    }
     if (pt) {
       if (!(po.det > 0.0)) atomicMin(&P.st[b].first_bad, (unsigned long long)sc.gid);
       if (isnan(po.dtq)) atomicOr(&P.st[b].nan_flag, 1u);

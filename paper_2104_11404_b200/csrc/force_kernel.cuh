@@ -31,7 +31,9 @@
 
 namespace hk {
 
-enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2 };
+enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2, MODE_FTW = 3 };
+// MODE_FTW: F^T w from stored S_q (no pointwise stage): gather w, its reference gradient,
+// A_q = S_q : gradhat w, the L2 backward contraction.
 
 // EPB_: units per CTA (0 = default: 8 for 16-point 2D elements, else 1).
 template <int DIM_, int K_, int Q_, int NF_, int EPB_ = 0>
@@ -87,6 +89,9 @@ struct Params {
   double *F1;               // [DIM][n_asm][B] assembled output
   int64_t n_asm;            // assembly nodes (n_nodes, or S0 nodes in sampled mode)
   double *dt_out;           // [B] or NULL
+  // stored point stresses S_q = w_q detJ sigma J^-T (optional): [unit][DIM*DIM][NQ]
+  double *S_store;          // written by MODE_FORCE when non-NULL
+  const double *S_load;     // read by MODE_FTW
 };
 
 // ----------------------------------------------------------------------------- helpers
@@ -508,11 +513,15 @@ struct KCfg {
   static constexpr int MINB = G::NT >= 224 ? 4 : (G::NT >= 128 ? 5 : 10);
 };
 
+template <int MODE, bool HAS_W>
+__host__ __device__ constexpr int nfields() { return (MODE == MODE_MQ || MODE == MODE_FTW) ? 1 : (HAS_W ? 3 : 2); }
+
 template <int DIM, int K, int Q, bool VISC, int MODE, bool BATCHED, bool HAS_W, int EPB_ = 0>
-__global__ void __launch_bounds__(KCfg<DIM, K, Q, (MODE == MODE_MQ ? 1 : (HAS_W ? 3 : 2)), EPB_>::G::NT,
-                                  KCfg<DIM, K, Q, (MODE == MODE_MQ ? 1 : (HAS_W ? 3 : 2)), EPB_>::MINB)
+__global__ void __launch_bounds__(KCfg<DIM, K, Q, nfields<MODE, HAS_W>(), EPB_>::G::NT,
+                                  KCfg<DIM, K, Q, nfields<MODE, HAS_W>(), EPB_>::MINB)
 force_kernel(const Params P) {
-  constexpr int NF = MODE == MODE_MQ ? 1 : (HAS_W ? 3 : 2);
+  constexpr int NF = nfields<MODE, HAS_W>();
+  constexpr bool WANT_E = MODE != MODE_MQ && MODE != MODE_FTW;
   using G = Geo<DIM, K, Q, NF, EPB_>;
   constexpr int N = G::N, M = G::M, ND = G::ND, NE = G::NE, NQ = G::NQ, EPB = G::EPB,
                 NT = G::NT;
@@ -559,12 +568,12 @@ force_kernel(const Params P) {
       if (gu < P.n_units) {
         const int b = BATCHED ? gu % B : 0;
         const int64_t idx = ((int64_t)c * P.ld_nodes + snode[uu * ND + a]) * B + b;
-        const double *src = MODE == MODE_MQ ? P.x : (f == 0 ? P.x : (f == 1 ? P.v : P.w));
+        const double *src = NF == 1 ? P.x : (f == 0 ? P.x : (f == 1 ? P.v : P.w));
         val = __ldg(src + idx);
       }
       units[uu * G::UNIT + (f * DIM + c) * ND + a] = val;
     }
-    if (MODE != MODE_MQ) {
+    if (WANT_E) {
       for (int i = tid; i < EPB * NE; i += NT) {
         const int uu = i % EPB, j = i / EPB;
         const int gu = unit0 + uu;
@@ -620,7 +629,7 @@ force_kernel(const Params P) {
         for (int a1 = 1; a1 < N; ++a1) acc = __fma_rn(tab[a1], src[a1], acc);
         S1b[((fc * 2 + bg) * Q + q1) * N * N + a2 * N + a3] = acc;
       }
-      if (MODE != MODE_MQ) {
+      if (WANT_E) {
         for (int o = lt; o < Q * M * M; o += NQ) {
           int r = o;
           const int j3 = r % M; r /= M;
@@ -659,7 +668,7 @@ force_kernel(const Params P) {
         S2b[((fc * 3 + 1) * Q + q1) * Q * N + q2 * N + a3] = d2;
         S2b[((fc * 3 + 2) * Q + q1) * Q * N + q2 * N + a3] = d3;
       }
-      if (MODE != MODE_MQ) {
+      if (WANT_E) {
         for (int o = lt; o < Q * Q * M; o += NQ) {
           int r = o;
           const int j3 = r % M; r /= M;
@@ -694,7 +703,7 @@ force_kernel(const Params P) {
         for (int a1 = 1; a1 < N; ++a1) acc = __fma_rn(tab[a1], src[a1], acc);
         S1b[((fc * 2 + bg) * Q + q1) * N + a2] = acc;
       }
-      if (MODE != MODE_MQ) {
+      if (WANT_E) {
         for (int o = lt; o < Q * M; o += NQ) {
           const int j2 = o % M, q1 = o / M;
           const double *tab = sBl + q1 * M;
@@ -708,7 +717,73 @@ force_kernel(const Params P) {
     }
     __syncthreads();
   }
-  forward_point<DIM, K, Q, NF, MODE != MODE_MQ>(sB, sG, sBl, Wk, q1i, q2i, q3i, J, Gv, Gw, eq);
+  forward_point<DIM, K, Q, NF, WANT_E>(sB, sG, sBl, Wk, q1i, q2i, q3i, J, Gv, Gw, eq);
+
+  // --- MODE_FTW: FTw[j] = sum_q psi_j(xi_q) (S_q : gradhat w_q) from the stored S_q
+  if (MODE == MODE_FTW) {
+    __syncthreads();                      // forward buffers dead
+    double *As = Wk;                      // [NQ]
+    double *F1b = As + NQ;                // f1
+    double *F2b = F1b + G::F1B;           // f2 (3D)
+    if (u < EPB && lt < NQ) {
+      const double *S = P.S_load + (int64_t)(unit0 + uc) * DIM * DIM * NQ + lt;
+      double A = 0.0;
+#pragma unroll
+      for (int c = 0; c < DIM; ++c)
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) A = __fma_rn(S[(c * DIM + d) * NQ], J[c][d], A);
+      As[lt] = A;
+    }
+    __syncthreads();
+    const int row = (u < EPB && unit0 + u < P.n_units) ? (P.ftw_row ? P.ftw_row[l] : l) : -1;
+    if (DIM == 3) {
+      if (u < EPB)
+        for (int o = lt; o < Q * Q * M; o += NQ) {
+          const int j3 = o % M, q2 = (o / M) % Q, q1 = o / (M * Q);
+          double acc = 0.0;
+#pragma unroll
+          for (int q3 = 0; q3 < Q; ++q3) acc = __fma_rn(sBl[q3 * M + j3], As[q1 + Q * q2 + Q * Q * q3], acc);
+          F1b[o] = acc;
+        }
+      __syncthreads();
+      if (u < EPB)
+        for (int o = lt; o < Q * M * M; o += NQ) {
+          const int j3 = o % M, j2 = (o / M) % M, q1 = o / (M * M);
+          double acc = 0.0;
+#pragma unroll
+          for (int q2 = 0; q2 < Q; ++q2) acc = __fma_rn(sBl[q2 * M + j2], F1b[(q1 * Q + q2) * M + j3], acc);
+          F2b[o] = acc;
+        }
+      __syncthreads();
+      if (row >= 0)
+        for (int o = lt; o < NE; o += NQ) {
+          const int j1 = o % M, j2 = (o / M) % M, j3 = o / (M * M);
+          double acc = 0.0;
+#pragma unroll
+          for (int q1 = 0; q1 < Q; ++q1) acc = __fma_rn(sBl[q1 * M + j1], F2b[(q1 * M + j2) * M + j3], acc);
+          P.FTw[((int64_t)row * NE + o) * B + b] = acc;
+        }
+    } else {
+      if (u < EPB)
+        for (int o = lt; o < Q * M; o += NQ) {
+          const int j2 = o % M, q1 = o / M;
+          double acc = 0.0;
+#pragma unroll
+          for (int q2 = 0; q2 < Q; ++q2) acc = __fma_rn(sBl[q2 * M + j2], As[q1 + Q * q2], acc);
+          F1b[o] = acc;
+        }
+      __syncthreads();
+      if (row >= 0)
+        for (int o = lt; o < NE; o += NQ) {
+          const int j1 = o % M, j2 = o / M;
+          double acc = 0.0;
+#pragma unroll
+          for (int q1 = 0; q1 < Q; ++q1) acc = __fma_rn(sBl[q1 * M + j1], F1b[q1 * M + j2], acc);
+          P.FTw[((int64_t)row * NE + o) * B + b] = acc;
+        }
+    }
+    return;
+  }
 
   // --- MODE_MQ: m_q = rho0_K detJ0 (density elimination)
   if (MODE == MODE_MQ) {
@@ -749,6 +824,14 @@ force_kernel(const Params P) {
       pointwise<DIM, VISC, HAS_W, false>(ai, J, Gv, Gw, eq, __ldg(P.mq + (int64_t)gid * NQ + lq),
                                          __ldg(P.gamma + gid), wq, ph, po);
     }
+  }
+
+  if (MODE == MODE_FORCE && P.S_store && active) {
+#pragma unroll
+    for (int c = 0; c < DIM; ++c)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d)
+        P.S_store[((int64_t)(unit0 + u) * DIM * DIM + c * DIM + d) * NQ + lt] = po.S[c][d];
   }
 
   // --- S6 dt: status flags, then min of order-preserving keys

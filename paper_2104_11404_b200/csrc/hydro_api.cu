@@ -131,14 +131,14 @@ std::pair<cudaEvent_t, cudaEvent_t> prof_pair() {
 
 template <int DIM, int K, int Q, bool VISC, int MODE, bool BATCHED, bool HAS_W>
 hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
-  constexpr int NF = MODE == hk::MODE_MQ ? 1 : (HAS_W ? 3 : 2);
+  constexpr int NF = hk::nfields<MODE, HAS_W>();
   using G = hk::Geo<DIM, K, Q, NF>;
   const int64_t grid = ((int64_t)P.n_units + G::EPB - 1) / G::EPB;
   if (grid <= 0) return HYDRO_OK;
-  constexpr bool SPEC2D = DIM == 2 && K == 2 && Q == 4 && MODE != hk::MODE_MQ;
+  constexpr bool SPEC2D = DIM == 2 && K == 2 && Q == 4 && MODE != hk::MODE_MQ && MODE != hk::MODE_FTW;
   // the persistent 3D kernel wins for Q2 (C2, C4); for Q3 (224-thread CTAs) its 80-register
   // budget spills and barrier waits grow, so Q3 keeps the one-element-per-CTA kernel
-  constexpr bool SPEC3D_OK = DIM == 3 && MODE != hk::MODE_MQ;
+  constexpr bool SPEC3D_OK = DIM == 3 && MODE != hk::MODE_MQ && MODE != hk::MODE_FTW;
   bool use3d = SPEC3D_OK && K == 2;  // (HYDRO_3D_KERNEL=persistent|element overrides)
   if (SPEC3D_OK) {
     const char *env = getenv("HYDRO_3D_KERNEL");
@@ -190,7 +190,7 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
   }
   if (use3d) grid2 = P.n_units < resident ? P.n_units : resident;
   std::pair<cudaEvent_t, cudaEvent_t> ev;
-  const bool prof = g_prof.on && MODE != hk::MODE_MQ;
+  const bool prof = g_prof.on && (MODE == hk::MODE_FORCE || MODE == hk::MODE_DT);
   if (prof) {
     ev = prof_pair();
     cudaEventRecord(ev.first, s);
@@ -212,6 +212,9 @@ hydro_status launch_force_t(int mode, bool visc, bool batched, bool has_w, const
                             cudaStream_t s) {
   using namespace hk;
   if (mode == MODE_MQ) return launch_force_k<DIM, K, Q, false, MODE_MQ, false, false>(P, s);
+  if (mode == MODE_FTW)
+    return batched ? launch_force_k<DIM, K, Q, false, MODE_FTW, true, false>(P, s)
+                   : launch_force_k<DIM, K, Q, false, MODE_FTW, false, false>(P, s);
   if (mode == MODE_DT) {
     if (batched || has_w) return HYDRO_ERR_ARG;
     return visc ? launch_force_k<DIM, K, Q, true, MODE_DT, false, false>(P, s)
@@ -440,7 +443,7 @@ hydro_status hydro_ctx_destroy(hydro_ctx *ctx) {
 static hydro_status force_common(hydro_ctx *c, int mode, const double *x, const double *v,
                                  const double *e, const double *w, const double *gamma,
                                  hydro_visc visc, hydro_cfl cfl, double *F1, double *FTw,
-                                 double *dt, cudaStream_t s) {
+                                 double *dt, cudaStream_t s, double *S_store = nullptr) {
   if (!c || !x || !v || !e || !gamma) return HYDRO_ERR_ARG;
   if (mode == hk::MODE_FORCE && (!F1 || !FTw)) return HYDRO_ERR_ARG;
   hk::Params P;
@@ -463,6 +466,7 @@ static hydro_status force_common(hydro_ctx *c, int mode, const double *x, const 
   P.F1 = F1;
   P.n_asm = c->d.n_nodes;
   P.dt_out = dt;
+  P.S_store = S_store;
   fill_tables_ptrs(P, c);
   hydro_status r = launch_force(c->d.dim, c->d.order_h1, mode, visc.enabled != 0, false, w != nullptr, P, s);
   if (r != HYDRO_OK) return r;
@@ -486,6 +490,35 @@ hydro_status hydro_dt_estimate(hydro_ctx *ctx, const double *x, const double *v,
                                hydro_stream_t stream) {
   return force_common(ctx, hk::MODE_DT, x, v, e, nullptr, gamma, visc, cfl, nullptr, nullptr, dt,
                       (cudaStream_t)stream);
+}
+
+size_t hydro_force_stress_bytes(const hydro_ctx *c) {
+  if (!c) return 0;
+  return sizeof(double) * (size_t)c->d.n_elem * c->d.dim * c->d.dim * c->nq;
+}
+
+hydro_status hydro_force_full_store(hydro_ctx *ctx, const double *x, const double *v, const double *e,
+                                    const double *gamma, hydro_visc visc, hydro_cfl cfl, double *F1,
+                                    double *FTw, double *dt, double *S, hydro_stream_t stream) {
+  if (!S) return HYDRO_ERR_ARG;
+  return force_common(ctx, hk::MODE_FORCE, x, v, e, nullptr, gamma, visc, cfl, F1, FTw, dt,
+                      (cudaStream_t)stream, S);
+}
+
+hydro_status hydro_force_transpose(hydro_ctx *c, const double *S, const double *w, double *FTw,
+                                   hydro_stream_t stream) {
+  if (!c || !S || !w || !FTw) return HYDRO_ERR_ARG;
+  hk::Params P;
+  std::memset(&P, 0, sizeof(P));
+  P.n_units = (int32_t)c->d.n_elem;
+  P.B = 1;
+  P.ld_nodes = c->d.n_nodes;
+  P.elem_nodes = c->d.elem_nodes;
+  P.x = w;
+  P.FTw = FTw;
+  P.S_load = S;
+  fill_tables_ptrs(P, c);
+  return launch_force(c->d.dim, c->d.order_h1, hk::MODE_FTW, false, false, false, P, (cudaStream_t)stream);
 }
 
 static hydro_status status_sync_impl(hydro_devstatus *st, int B, cudaStream_t s,
@@ -634,10 +667,11 @@ hydro_status hydro_sample_lists(const hydro_sample *p, int32_t *closure_elems,
   return HYDRO_OK;
 }
 
-hydro_status hydro_force_sampled(hydro_sample *p, const double *x_S, const double *v_S,
-                                 const double *e_S, const double *w_S, const double *gamma,
-                                 hydro_visc visc, hydro_cfl cfl, double *F1_rows,
-                                 double *FTw_rows, double *dt, hydro_stream_t stream) {
+static hydro_status sampled_common(hydro_sample *p, const double *x_S, const double *v_S,
+                                   const double *e_S, const double *w_S, const double *gamma,
+                                   hydro_visc visc, hydro_cfl cfl, double *F1_rows,
+                                   double *FTw_rows, double *dt, hydro_stream_t stream,
+                                   double *S_store) {
   if (!p || !x_S || !v_S || !e_S || !gamma || !F1_rows || !FTw_rows) return HYDRO_ERR_ARG;
   hydro_ctx *c = p->ctx;
   cudaStream_t s = (cudaStream_t)stream;
@@ -664,11 +698,55 @@ hydro_status hydro_force_sampled(hydro_sample *p, const double *x_S, const doubl
   P.F1 = F1_rows;
   P.n_asm = p->n_s0_nodes;
   P.dt_out = dt;
+  P.S_store = S_store;
   fill_tables_ptrs(P, c);
   hydro_status r = launch_force(c->d.dim, c->d.order_h1, hk::MODE_FORCE, visc.enabled != 0, p->B > 1,
                                 w_S != nullptr, P, s);
   if (r != HYDRO_OK) return r;
   return launch_assemble(c->d.dim, p->n_s0_nodes, p->B, p->off, p->evec, F1_rows, p->st, dt, s);
+}
+
+hydro_status hydro_force_sampled(hydro_sample *p, const double *x_S, const double *v_S,
+                                 const double *e_S, const double *w_S, const double *gamma,
+                                 hydro_visc visc, hydro_cfl cfl, double *F1_rows,
+                                 double *FTw_rows, double *dt, hydro_stream_t stream) {
+  return sampled_common(p, x_S, v_S, e_S, w_S, gamma, visc, cfl, F1_rows, FTw_rows, dt, stream,
+                        nullptr);
+}
+
+size_t hydro_sample_stress_bytes(const hydro_sample *p) {
+  if (!p) return 0;
+  const hydro_ctx *c = p->ctx;
+  return sizeof(double) * (size_t)p->n_cl * p->B * c->d.dim * c->d.dim * c->nq;
+}
+
+hydro_status hydro_force_sampled_store(hydro_sample *p, const double *x_S, const double *v_S,
+                                       const double *e_S, const double *gamma, hydro_visc visc,
+                                       hydro_cfl cfl, double *F1_rows, double *FTw_rows, double *dt,
+                                       double *S, hydro_stream_t stream) {
+  if (!S) return HYDRO_ERR_ARG;
+  return sampled_common(p, x_S, v_S, e_S, nullptr, gamma, visc, cfl, F1_rows, FTw_rows, dt, stream, S);
+}
+
+hydro_status hydro_sample_force_transpose(hydro_sample *p, const double *S, const double *w_S,
+                                          double *FTw_rows, hydro_stream_t stream) {
+  if (!p || !S || !w_S || !FTw_rows) return HYDRO_ERR_ARG;
+  hydro_ctx *c = p->ctx;
+  if (p->n_cl * (int64_t)p->B >= ((int64_t)1 << 31)) return HYDRO_ERR_ARG;
+  hk::Params P;
+  std::memset(&P, 0, sizeof(P));
+  P.n_units = (int32_t)(p->n_cl * p->B);
+  P.B = p->B;
+  P.ld_nodes = p->n_cl_nodes;
+  P.elem_nodes = p->elem_nodes;
+  P.elem_gid = p->elem_gid;
+  P.x = w_S;
+  P.FTw = FTw_rows;
+  P.ftw_row = p->ftw_row;
+  P.S_load = S;
+  fill_tables_ptrs(P, c);
+  return launch_force(c->d.dim, c->d.order_h1, hk::MODE_FTW, false, p->B > 1, false, P,
+                      (cudaStream_t)stream);
 }
 
 hydro_status hydro_sample_status_sync(hydro_sample *p, hydro_stream_t stream,
@@ -735,7 +813,7 @@ struct hydro_fom {
   double *r = nullptr, *z = nullptr, *p = nullptr, *Ap = nullptr, *part = nullptr, *sc = nullptr;
   double *F1 = nullptr, *F1x = nullptr, *FTw = nullptr, *FTx = nullptr, *dv = nullptr;
   double *vh = nullptr, *eh = nullptr, *xh = nullptr, *v1 = nullptr, *vbar = nullptr,
-         *dts = nullptr;
+         *dts = nullptr, *S = nullptr;
   std::vector<void *> allocs;
 };
 
@@ -933,7 +1011,8 @@ hydro_status hydro_fom_create(hydro_ctx *c, const int64_t *bc_dofs, int64_t n_bc
       !alloc(&f->Ap, n) || !alloc(&f->part, hk::DOT_BLOCKS) || !alloc(&f->sc, 8) ||
       !alloc(&f->F1, n) || !alloc(&f->F1x, n) || !alloc(&f->FTw, nE) || !alloc(&f->FTx, nE) ||
       !alloc(&f->dv, n) || !alloc(&f->vh, n) || !alloc(&f->eh, nE) || !alloc(&f->xh, n) ||
-      !alloc(&f->v1, n) || !alloc(&f->vbar, n) || !alloc(&f->dts, 2))
+      !alloc(&f->v1, n) || !alloc(&f->vbar, n) || !alloc(&f->dts, 2) ||
+      !alloc(&f->S, hydro_force_stress_bytes(c) / sizeof(double)))
     return fail(HYDRO_ERR_CUDA);
   if (cudaMemcpyAsync(f->mask, mask.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return fail(HYDRO_ERR_CUDA);
@@ -1027,26 +1106,24 @@ hydro_status hydro_rk2avg_step(hydro_fom *f, double *x, double *v, double *e, co
   const unsigned g = blocks_for(n, 256);
   hydro_status st;
   int it1 = 0, it2 = 0;
-  // ---- stage 1: F(U^n)
+  // ---- stage 1: F(U^n) (F.1, dt, and the point stresses S_q for the transposed product)
   if ((st = force_common(c, hk::MODE_FORCE, x, v, e, nullptr, gamma, visc, cfl, f->F1, f->FTx,
-                         f->dts + 0, s)) != HYDRO_OK) return st;
+                         f->dts + 0, s, f->S)) != HYDRO_OK) return st;
   if ((st = pcg(f, f->F1, f->dv, cg_tol, cg_max_iter, &it1, nullptr, s)) != HYDRO_OK) return st;
   hk::axpy_kernel<<<g, 256, 0, s>>>(n, v, -0.5 * dt, f->dv, f->mask, f->vh);    // v^{n+1/2}
   g_launches++;
-  if ((st = force_common(c, hk::MODE_FORCE, x, v, e, f->vh, gamma, visc, cfl, f->F1x, f->FTw,
-                         nullptr, s)) != HYDRO_OK) return st;                       // F(U^n)^T v^{n+1/2}
+  if ((st = hydro_force_transpose(c, f->S, f->vh, f->FTw, stream)) != HYDRO_OK) return st;  // F(U^n)^T v^{n+1/2}
   if ((st = mass_e_update(f, e, f->FTw, 0.5 * dt, f->eh, s)) != HYDRO_OK) return st;
   hk::axpy_kernel<<<g, 256, 0, s>>>(n, x, 0.5 * dt, f->vh, nullptr, f->xh);    // x^{n+1/2}
   g_launches++;
   // ---- stage 2: F(U^{n+1/2})
   if ((st = force_common(c, hk::MODE_FORCE, f->xh, f->vh, f->eh, nullptr, gamma, visc, cfl, f->F1,
-                         f->FTx, f->dts + 1, s)) != HYDRO_OK) return st;
+                         f->FTx, f->dts + 1, s, f->S)) != HYDRO_OK) return st;
   if ((st = pcg(f, f->F1, f->dv, cg_tol, cg_max_iter, &it2, nullptr, s)) != HYDRO_OK) return st;
   hk::axpy_kernel<<<g, 256, 0, s>>>(n, v, -dt, f->dv, f->mask, f->v1);         // v^{n+1}
   hk::avg_kernel<<<g, 256, 0, s>>>(n, v, f->v1, f->vbar);                       // vbar
   g_launches += 2;
-  if ((st = force_common(c, hk::MODE_FORCE, f->xh, f->vh, f->eh, f->vbar, gamma, visc, cfl, f->F1x,
-                         f->FTw, nullptr, s)) != HYDRO_OK) return st;               // F(U^{n+1/2})^T vbar
+  if ((st = hydro_force_transpose(c, f->S, f->vbar, f->FTw, stream)) != HYDRO_OK) return st;  // F(U^{n+1/2})^T vbar
   if ((st = mass_e_update(f, e, f->FTw, dt, e, s)) != HYDRO_OK) return st;     // e^{n+1}
   hk::axpy_kernel<<<g, 256, 0, s>>>(n, x, dt, f->vbar, nullptr, x);            // x^{n+1}
   g_launches++;
@@ -1075,7 +1152,8 @@ struct hydro_rom {
   double *xS = nullptr, *vS = nullptr, *eS = nullptr, *wS = nullptr, *F1r = nullptr,
          *F1x = nullptr, *FTr = nullptr, *FTx = nullptr, *rv = nullptr, *re = nullptr,
          *rx = nullptr, *Yv_h = nullptr, *Ye_h = nullptr, *Yx_h = nullptr, *Yv1 = nullptr,
-         *Yvb = nullptr, *dt1 = nullptr, *dt2 = nullptr, *wsv = nullptr, *wse = nullptr;
+         *Yvb = nullptr, *dt1 = nullptr, *dt2 = nullptr, *wsv = nullptr, *wse = nullptr,
+         *S = nullptr;
   size_t wsv_bytes = 0, wse_bytes = 0;
   std::vector<void *> allocs;
 };
@@ -1123,7 +1201,8 @@ hydro_status hydro_rom_create(hydro_sample *p, int nx, int nv, int ne, const dou
       !alloc(&r->Yv_h, (size_t)nv * B) || !alloc(&r->Ye_h, (size_t)ne * B) ||
       !alloc(&r->Yx_h, (size_t)nx * B) || !alloc(&r->Yv1, (size_t)nv * B) ||
       !alloc(&r->Yvb, (size_t)nv * B) || !alloc(&r->dt1, B) || !alloc(&r->dt2, B) ||
-      !alloc(&r->wsv, r->wsv_bytes / 8 + 1) || !alloc(&r->wse, r->wse_bytes / 8 + 1))
+      !alloc(&r->wsv, r->wsv_bytes / 8 + 1) || !alloc(&r->wse, r->wse_bytes / 8 + 1) ||
+      !alloc(&r->S, hydro_sample_stress_bytes(p) / sizeof(double)))
     return fail(HYDRO_ERR_CUDA);
   *out = r;
   return HYDRO_OK;
@@ -1161,11 +1240,11 @@ hydro_status hydro_rom_rk2avg_step(hydro_rom *r, double *Yx, double *Yv, double 
   RS(lift(r->Phi_x, r->x_os, fx, r->rows_h1, r->nx, Yx, r->xS));
   RS(lift(r->Phi_v, r->v_os, fv, r->rows_h1, r->nv, Yv, r->vS));
   RS(lift(r->Phi_e, r->e_os, fe, r->rows_l2, r->ne, Ye, r->eS));
-  RS(hydro_force_sampled(r->p, r->xS, r->vS, r->eS, nullptr, gamma, visc, cfl, r->F1r, r->FTx, r->dt1, stream));
+  RS(hydro_force_sampled_store(r->p, r->xS, r->vS, r->eS, gamma, visc, cfl, r->F1r, r->FTx, r->dt1, r->S, stream));
   RS(proj(r->R_v, r->nv, r->s_v, r->F1r, r->rv, r->wsv, r->wsv_bytes));
   RS(axpy(r->nv, Yv, -0.5, r->rv, r->Yv_h));                                   // vhat^{n+1/2}
   RS(lift(r->Phi_v, r->v_os, fv, r->rows_h1, r->nv, r->Yv_h, r->wS));          // v~^{n+1/2}
-  RS(hydro_force_sampled(r->p, r->xS, r->vS, r->eS, r->wS, gamma, visc, cfl, r->F1x, r->FTr, nullptr, stream));
+  RS(hydro_sample_force_transpose(r->p, r->S, r->wS, r->FTr, stream));
   RS(proj(r->R_e, r->ne, r->s_e, r->FTr, r->re, r->wse, r->wse_bytes));
   RS(axpy(r->ne, Ye, 0.5, r->re, r->Ye_h));                                    // ehat^{n+1/2}
   RS(lift(r->C_xv, r->c_x, 0, r->nx, r->nv, r->Yv_h, r->rx));                  // c_x + C_xv vhat
@@ -1173,14 +1252,14 @@ hydro_status hydro_rom_rk2avg_step(hydro_rom *r, double *Yx, double *Yv, double 
   // ---- stage 2 at U~^{n+1/2} (its velocity is wS)
   RS(lift(r->Phi_x, r->x_os, fx, r->rows_h1, r->nx, r->Yx_h, r->xS));
   RS(lift(r->Phi_e, r->e_os, fe, r->rows_l2, r->ne, r->Ye_h, r->eS));
-  RS(hydro_force_sampled(r->p, r->xS, r->wS, r->eS, nullptr, gamma, visc, cfl, r->F1r, r->FTx, r->dt2, stream));
+  RS(hydro_force_sampled_store(r->p, r->xS, r->wS, r->eS, gamma, visc, cfl, r->F1r, r->FTx, r->dt2, r->S, stream));
   RS(proj(r->R_v, r->nv, r->s_v, r->F1r, r->rv, r->wsv, r->wsv_bytes));
   RS(axpy(r->nv, Yv, -1.0, r->rv, r->Yv1));                                    // vhat^{n+1}
   hk::avg_kernel<<<blocks_for((int64_t)r->nv * B, 256), 256, 0, (cudaStream_t)stream>>>(
       (int64_t)r->nv * B, Yv, r->Yv1, r->Yvb);
   g_launches++;
   RS(lift(r->Phi_v, r->v_os, fv, r->rows_h1, r->nv, r->Yvb, r->vS));           // v~bar
-  RS(hydro_force_sampled(r->p, r->xS, r->wS, r->eS, r->vS, gamma, visc, cfl, r->F1x, r->FTr, nullptr, stream));
+  RS(hydro_sample_force_transpose(r->p, r->S, r->vS, r->FTr, stream));
   RS(proj(r->R_e, r->ne, r->s_e, r->FTr, r->re, r->wse, r->wse_bytes));
   RS(axpy(r->ne, Ye, 1.0, r->re, Ye));                                         // ehat^{n+1}
   RS(lift(r->C_xv, r->c_x, 0, r->nx, r->nv, r->Yvb, r->rx));

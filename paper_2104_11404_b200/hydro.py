@@ -30,7 +30,9 @@ EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy"
             "hydro_profile_enable", "hydro_profile_read", "hydro_selftest_ieee_fast",
             "hydro_fom_create", "hydro_fom_destroy", "hydro_mass_v_apply", "hydro_mass_v_solve",
             "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_rom_create",
-            "hydro_rom_destroy", "hydro_rom_rk2avg_step"]
+            "hydro_rom_destroy", "hydro_rom_rk2avg_step", "hydro_force_stress_bytes",
+            "hydro_force_full_store", "hydro_force_transpose", "hydro_sample_stress_bytes",
+            "hydro_force_sampled_store", "hydro_sample_force_transpose"]
 
 
 class HydroError(RuntimeError):
@@ -95,6 +97,14 @@ def lib() -> ctypes.CDLL:
                                        vp, ctypes.POINTER(vp)]
         L.hydro_rom_destroy.argtypes = [vp]
         L.hydro_rom_rk2avg_step.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, vp, vp, vp]
+        L.hydro_force_stress_bytes.restype = ctypes.c_size_t
+        L.hydro_force_stress_bytes.argtypes = [vp]
+        L.hydro_force_full_store.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, vp, vp, vp, vp, vp]
+        L.hydro_force_transpose.argtypes = [vp, vp, vp, vp, vp]
+        L.hydro_sample_stress_bytes.restype = ctypes.c_size_t
+        L.hydro_sample_stress_bytes.argtypes = [vp]
+        L.hydro_force_sampled_store.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, vp, vp, vp, vp, vp]
+        L.hydro_sample_force_transpose.argtypes = [vp, vp, vp, vp, vp]
         L.hydro_rom_project_workspace_bytes.restype = ctypes.c_size_t
         L.hydro_rom_project_workspace_bytes.argtypes = [i32, i64, i32]
         L.hydro_rom_project.argtypes = [i32, i64, i32, vp, vp, vp, vp, ctypes.c_size_t, vp]
@@ -241,6 +251,30 @@ class HydroContext:
                                       visc.c(), cfl.c(), _ptr(F1), _ptr(FTw), _ptr(dt),
                                       _stream(stream)), "hydro_force_full")
         return F1, FTw, dt
+
+    def force_full_store(self, x, v, e, gamma, visc: Visc, cfl: Cfl, F1=None, FTw=None, dt=None,
+                         S=None, stream=None):
+        """hydro_force_full (w = v) that also stores S_q; returns (F1, FTw, dt, S)."""
+        dev = x.device
+        if F1 is None:
+            F1 = torch.empty((self.dim, self.n_nodes), dtype=torch.float64, device=dev)
+        if FTw is None:
+            FTw = torch.empty((self.n_elem, self.ne), dtype=torch.float64, device=dev)
+        if dt is None:
+            dt = torch.empty(1, dtype=torch.float64, device=dev)
+        if S is None:
+            S = torch.empty(lib().hydro_force_stress_bytes(self._h) // 8, dtype=torch.float64, device=dev)
+        _check(lib().hydro_force_full_store(self._h, _ptr(x), _ptr(v), _ptr(e), _ptr(gamma), visc.c(),
+                                            cfl.c(), _ptr(F1), _ptr(FTw), _ptr(dt), _ptr(S),
+                                            _stream(stream)), "hydro_force_full_store")
+        return F1, FTw, dt, S
+
+    def force_transpose(self, S, w, FTw=None, stream=None):
+        if FTw is None:
+            FTw = torch.empty((self.n_elem, self.ne), dtype=torch.float64, device=w.device)
+        _check(lib().hydro_force_transpose(self._h, _ptr(S), _ptr(w), _ptr(FTw), _stream(stream)),
+               "hydro_force_transpose")
+        return FTw
 
     def dt_estimate(self, x, v, e, gamma, visc: Visc, cfl: Cfl, dt=None, stream=None):
         if dt is None:
