@@ -96,48 +96,86 @@ def pointwise_instr(dim, visc, rot_per_lmin3):
 
 # ----------------------------------------------------------------------------- helpers
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region.
+
+    NVML is polled every ~0.5 ms from a thread (the timed regions of the small configs last
+    about a millisecond, too short for nvidia-smi's ~50 ms per query); nvidia-smi is the
+    fallback.  The GPU is identified by PCI bus id, so CUDA_VISIBLE_DEVICES remapping does
+    not pick the wrong board.  One sample is always taken at entry and one at exit."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, gpu_index=0):
-        self.gpu = gpu_index
-        self.samples = []
+    def __init__(self, dev):
+        self.samples = []            # (sm_mhz, max_mhz, {reason names})
+        self.source = None
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nvml = None
+        self._smi_id = str(getattr(dev, "index", 0) or 0)
+        try:
+            import torch
+            props = torch.cuda.get_device_properties(dev)
+            bus = "%08x:%02x:%02x.0" % (props.pci_domain_id, props.pci_bus_id, props.pci_device_id)
+            self._smi_id = bus
+            import pynvml as N
+            N.nvmlInit()
+            self._nvml = (N, N.nvmlDeviceGetHandleByPciBusId(bus.encode()))
+            self.source = "nvml"
+        except Exception:
+            self._nvml = None
+            self.source = "nvidia-smi"
+
+    def _sample(self):
+        if self._nvml is not None:
+            N, h = self._nvml
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                        N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+                self.samples.append((float(sm), float(mx),
+                                     {n for n, b in zip(self.NAMES, bits) if r & b}))
+            except Exception:
+                pass
+            return
+        try:
+            out = subprocess.run(["nvidia-smi", f"--id={self._smi_id}", f"--query-gpu={self.Q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True,
+                                 text=True, timeout=5).stdout.strip()
+            s = [t.strip() for t in out.split(",")]
+            if len(s) >= 9 and s[1].replace(".", "").isdigit():
+                self.samples.append((float(s[1]), float(s[2]) if s[2].replace(".", "").isdigit() else None,
+                                     {self.NAMES[i] for i in range(4) if s[5 + i].lower().startswith("active")}))
+        except Exception:
+            pass
 
     def _run(self):
         while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+            self._sample()
+            self._stop.wait(0.0005 if self._nvml is not None else 0.2)
 
     def __enter__(self):
+        self._sample()
         self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        self._sample()
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 5 + i and s[5 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock query unavailable"]}
+        sm = [s[0] for s in self.samples]
+        mx = [s[1] for s in self.samples if s[1] is not None]
+        reasons = sorted(set().union(*[s[2] for s in self.samples]))
+        return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm),
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "source": self.source}
 
 
 def measured_peaks():
@@ -260,7 +298,7 @@ def bench_one(name, args, dev, flush, rank, world):
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(dev.index) as clk:
+    with ClockSampler(dev) as clk:
         for i in range(args.steps):
             flush.zero_()                      # L2 flush (256 MiB > 126 MB), outside the events
             evs[i][0].record()

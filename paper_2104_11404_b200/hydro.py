@@ -15,7 +15,9 @@ from typing import Optional
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhydro.so")
+# HYDRO_LIB_PATH: load another in-tree build of the same library (A/B of kernel variants,
+# tools/ab_lib.py); never a substitute implementation.
+LIB_PATH = os.environ.get("HYDRO_LIB_PATH") or os.path.join(_HERE, "libhydro.so")
 
 HYDRO_OK, HYDRO_ERR_ARG, HYDRO_ERR_UNSUPPORTED, HYDRO_ERR_CUDA = 0, 1, 2, 3
 HYDRO_ERR_TANGLED, HYDRO_ERR_NONFINITE, HYDRO_ERR_WORKSPACE = 4, 5, 6

@@ -1,0 +1,28 @@
+#!/usr/bin/env python
+"""A/B timing of two builds of libhydro.so on the same box: each (library, config) pair
+runs in its own process (tools/ab.py's timing loop, default kernel selection), the
+libraries alternating, ROUNDS times.
+
+    python tools/ab_lib.py ROUNDS LIB_A LIB_B c1 c2 c3
+"""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def main():
+    rounds, la, lb, cfgs = int(sys.argv[1]), sys.argv[2], sys.argv[3], sys.argv[4:]
+    for r in range(rounds):
+        for c in cfgs:
+            for lib in (la, lb) if r % 2 == 0 else (lb, la):
+                env = dict(os.environ, HYDRO_LIB_PATH=os.path.abspath(lib))
+                out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ab.py"), c,
+                                      "HYDRO_AB=1"], env=env, capture_output=True, text=True)
+                line = (out.stdout.strip().splitlines() or [out.stderr.strip()[-300:]])[-1]
+                print(f"round {r} {os.path.basename(lib)}: {line}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
