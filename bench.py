@@ -621,12 +621,13 @@ def measured_traffic(name):
 
 
 # ----------------------------------------------------------------------------- cpu baseline
-def cpu_baseline(name, target_s=12.0):
+def cpu_baseline(name, target_s=12.0, prob=None):
     """The oracle as it stands (oracle/, OpenMP over the host cores) on a bounded seeded
     sample of the workload: a random subset of elements, or the whole mesh repeated, sized
     to ~target_s seconds of CPU work.  Quadrature points processed / wall time."""
     import oracle
-    prob = build_problem(name) if name != "c4" else build_problem("c2")
+    if prob is None:
+        prob = build_problem(name) if name != "c4" else build_problem("c2")
     m = prob.mesh
     nq = m.nq ** m.dim
     cores = os.cpu_count() or 1
@@ -648,6 +649,13 @@ def cpu_baseline(name, target_s=12.0):
 
 
 # ----------------------------------------------------------------------------- main
+def bench_config(name, n_qp, world):
+    """The workload description shared by both arms' JSON lines."""
+    return {"workload": f"{name} (BASELINE.json configs[{name[1]}])", "quad_points": n_qp,
+            "l2": "flushed before every timed step (256 MiB write; GPU arm)",
+            "parallelism": f"replicas x{world}"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -664,21 +672,25 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
 
     if args.impl == "reference":
+        # the oracle arm: rank 0 only, on the host cores; each step is a bounded sample of
+        # the same workload (bench.cpu_baseline), warm-up steps shorter and untimed
         if rank != 0:
             return 0
-        import oracle
-        cb = []
+        prob = build_problem(args.workload if args.workload != "c4" else "c2")
+        m = prob.mesh
+        n_qp = m.n_elem * m.nq ** m.dim
         for _ in range(args.warmup):
-            pass
+            cpu_baseline(args.workload, target_s=0.2, prob=prob)
         vals = []
         for _ in range(args.steps):
-            r = cpu_baseline(args.workload, target_s=max(2.0, 60.0 / max(args.steps, 1)))
+            r = cpu_baseline(args.workload, target_s=max(1.0, 60.0 / max(args.steps, 1)), prob=prob)
             vals.append(r["value"])
         v = float(np.median(vals))
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 1,
-                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-                "dtype": "f64", "data": "synthetic",
-                "config": {"workload": args.workload},
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": n_qp / v * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (workloads/: seeded SplitMix64, shapes of BASELINE.json configs)",
+                "config": bench_config(args.workload, n_qp, 1),
                 "cpu_baseline": {**r, "value": v},
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
@@ -698,10 +710,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (workloads/: seeded SplitMix64, shapes of BASELINE.json configs)",
-            "config": {"workload": f"{args.workload} (BASELINE.json configs[{args.workload[1]}])",
-                       "elements_per_s": head["elements_per_s"] * world, "quad_points": head["n_qp"],
-                       "l2": "flushed before every timed step (256 MiB write)",
-                       "parallelism": f"replicas x{world}"},
+            "config": bench_config(args.workload, head["n_qp"], world),
+            "elements_per_s": head["elements_per_s"] * world,
             "e2e": head.get("e2e"), "gpu_launches": head["gpu_launches"],
             "roofline": head["roofline"], "clocks": head["clocks"],
             "force_kernel_ms": head["force_kernel_ms"], "force_kernel_share": head["force_kernel_share"],
