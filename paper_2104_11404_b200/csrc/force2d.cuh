@@ -45,11 +45,39 @@ struct ColOut {
 };
 
 // The q2 loop of one q1 column: forward last stage, pointwise, first backward stage.
+constexpr int F2D_NT = 64;
+
+// U rows of the xi_1 contraction (canonical order): ub = sum_a1 B[q1][a1] X[fc][a1,a2],
+// ug = sum_a1 G[q1][a1] X[fc][a1,a2]; Xs is the thread's lane-interleaved dof column.
+__device__ __forceinline__ void u_row(int q1, const double *Xs, int fc, int a2, double &ub,
+                                      double &ug) {
+  const double x0 = Xs[(fc * 9 + a2 * 3 + 0) * F2D_NT];
+  const double x1 = Xs[(fc * 9 + a2 * 3 + 1) * F2D_NT];
+  const double x2 = Xs[(fc * 9 + a2 * 3 + 2) * F2D_NT];
+  ub = c_t24.B[q1][0] * x0;
+  ug = c_t24.G[q1][0] * x0;
+  ub = __fma_rn(c_t24.B[q1][1], x1, ub);
+  ug = __fma_rn(c_t24.G[q1][1], x1, ug);
+  ub = __fma_rn(c_t24.B[q1][2], x2, ub);
+  ug = __fma_rn(c_t24.G[q1][2], x2, ug);
+}
+
+// F2D_KEEP: how many of the (field, component) rows of U stay in registers across the q2
+// loop (the position rows, 2); the velocity (and w) rows are re-contracted from the gathered
+// dofs in shared memory at every point -- the same canonical FMA chain, so the same bits --
+// trading ~27 FP64 instructions per point for ~24 registers, which removes the local-memory
+// spills the all-register version had (they missed L1: profiles/r01_ab14_*).
+#ifndef F2D_KEEP
+#define F2D_KEEP 2
+#endif
+
 template <bool VISC, bool HAS_W, class AR>
 __device__ __forceinline__ void column2d(AR &ar, int q1, const double (&UB)[6][3],
-                                         const double (&UG)[6][3], const double (&E1)[2],
-                                         const double *__restrict__ mqp, double gam,
-                                         const PhysIn &ph, ColOut &o, double *Sst) {
+                                         const double (&UG)[6][3], const double *Xs,
+                                         const double (&E1)[2],
+                                         const double *__restrict__ mqp, double mq0,
+                                         double &mq_next, double gam, const PhysIn &ph,
+                                         ColOut &o, double *Sst) {
 #pragma unroll
   for (int c = 0; c < 2; ++c)
 #pragma unroll
@@ -60,8 +88,14 @@ __device__ __forceinline__ void column2d(AR &ar, int q1, const double (&UB)[6][3
   o.kmin = ~0ull;
   o.tangled = o.nan = false;
   const double wq1 = c_t24.w[q1];
+  // m_q is software-prefetched one point ahead (a rotating register, no indexed array):
+  // the global load's latency hides behind the previous point's pointwise stage.  After
+  // the last point mq_next holds m_q(q1 + 1, 0) (mqp[1]; a harmless re-read for q1 = 3).
+  double mq_cur = mq0;
 #pragma unroll 1
   for (int q2 = 0; q2 < 4; ++q2) {
+    const double mq = mq_cur;
+    mq_cur = __ldg(q2 < 3 ? mqp + 4 * (q2 + 1) : mqp + (q1 < 3 ? 1 : 0));
     double J[3][3], Gv[3][3], Gw[3][3];
     constexpr int NF = HAS_W ? 3 : 2;
 #pragma unroll
@@ -69,11 +103,21 @@ __device__ __forceinline__ void column2d(AR &ar, int q1, const double (&UB)[6][3
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int fc = f * 2 + c;
-        double d0 = c_t24.B[q2][0] * UG[fc][0], d1 = c_t24.G[q2][0] * UB[fc][0];
+        double ugv[3], ubv[3];
+#pragma unroll
+        for (int a2 = 0; a2 < 3; ++a2) {
+          if (fc < F2D_KEEP) {
+            ugv[a2] = UG[fc][a2];
+            ubv[a2] = UB[fc][a2];
+          } else {
+            u_row(q1, Xs, fc, a2, ubv[a2], ugv[a2]);
+          }
+        }
+        double d0 = c_t24.B[q2][0] * ugv[0], d1 = c_t24.G[q2][0] * ubv[0];
 #pragma unroll
         for (int a2 = 1; a2 < 3; ++a2) {
-          d0 = __fma_rn(c_t24.B[q2][a2], UG[fc][a2], d0);
-          d1 = __fma_rn(c_t24.G[q2][a2], UB[fc][a2], d1);
+          d0 = __fma_rn(c_t24.B[q2][a2], ugv[a2], d0);
+          d1 = __fma_rn(c_t24.G[q2][a2], ubv[a2], d1);
         }
         double *dst = f == 0 ? J[c] : (f == 1 ? Gv[c] : Gw[c]);
         dst[0] = d0;
@@ -88,8 +132,7 @@ __device__ __forceinline__ void column2d(AR &ar, int q1, const double (&UB)[6][3
     double eq = c_t24.Bl[q2][0] * E1[0];
     eq = __fma_rn(c_t24.Bl[q2][1], E1[1], eq);
     PointOut po;
-    pointwise<2, VISC, HAS_W, false>(ar, J, Gv, Gw, eq, __ldg(mqp + 4 * q2), gam, wq1 * c_t24.w[q2],
-                                     ph, po);
+    pointwise<2, VISC, HAS_W, false>(ar, J, Gv, Gw, eq, mq, gam, wq1 * c_t24.w[q2], ph, po);
     if (Sst) {  // stored S_q = w_q detJ sigma J^-T, [cd][q] with q = q1 + 4 q2
 #pragma unroll
       for (int c = 0; c < 2; ++c)
@@ -112,14 +155,13 @@ __device__ __forceinline__ void column2d(AR &ar, int q1, const double (&UB)[6][3
     o.f1[0] = __fma_rn(c_t24.Bl[q2][0], po.A, o.f1[0]);
     o.f1[1] = __fma_rn(c_t24.Bl[q2][1], po.A, o.f1[1]);
   }
+  mq_next = mq_cur;
 }
-
-constexpr int F2D_NT = 64;
 
 template <int NF>
 struct G2 {
   static constexpr int NT = F2D_NT;
-  static constexpr size_t SMEM = sizeof(double) * (size_t)(NF * 2 * 9 + 18) * NT;
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(NF * 2 * 9 + 18 + 4) * NT;
 };
 
 template <bool VISC, int MODE, bool BATCHED, bool HAS_W>
@@ -130,6 +172,7 @@ __global__ void __maxnreg__(128) force2d_kernel(const Params P) {
   extern __shared__ __align__(16) double smem[];
   double *Xs = smem + threadIdx.x;              // [NX][NT]   gathered x, v (, w)
   double *Fs = smem + NX * NT + threadIdx.x;    // [18][NT]   F1 accumulators [c][a2][a1]
+  double *Es = Fs + 18 * NT;                    // [4][NT]    e dofs (off the register budget)
   __shared__ unsigned long long skey[NT / 32];
 
   const int tid = threadIdx.x;
@@ -157,9 +200,8 @@ __global__ void __maxnreg__(128) force2d_kernel(const Params P) {
           Xs[((f * 2 + c) * ND + a) * NT] = __ldg(src + ((int64_t)c * P.ld_nodes + nd[a]) * B + b);
     }
   }
-  double E[NE];
 #pragma unroll
-  for (int j = 0; j < NE; ++j) E[j] = __ldg(P.e + ((int64_t)l * NE + j) * B + b);
+  for (int j = 0; j < NE; ++j) Es[j * NT] = __ldg(P.e + ((int64_t)l * NE + j) * B + b);
   double FT[2][2];  // FTw[j1][j2] accumulators
 #pragma unroll
   for (int j = 0; j < 2; ++j) FT[j][0] = FT[j][1] = 0.0;
@@ -171,31 +213,24 @@ __global__ void __maxnreg__(128) force2d_kernel(const Params P) {
   unsigned long long kmin = ~0ull;
   bool tangled = false, nan = false;
   double *Sst = (MODE == MODE_FORCE && P.S_store && valid) ? P.S_store + (int64_t)g * 4 * NQ : nullptr;
+  double mq0 = __ldg(P.mq + (int64_t)gid * NQ);  // m_q(0, 0); then prefetched point by point
 
 #pragma unroll 1
   for (int q1 = 0; q1 < 4; ++q1) {
     // S2a: contract xi_1 for this q1 (canonical order)
     double UB[6][3], UG[6][3];
-    const double b0 = c_t24.B[q1][0], b1 = c_t24.B[q1][1], b2 = c_t24.B[q1][2];
-    const double h0 = c_t24.G[q1][0], h1 = c_t24.G[q1][1], h2 = c_t24.G[q1][2];
 #pragma unroll
     for (int fc = 0; fc < NF * 2; ++fc)
 #pragma unroll
       for (int a2 = 0; a2 < 3; ++a2) {
-        const double x0 = Xs[(fc * ND + a2 * 3 + 0) * NT];
-        const double x1 = Xs[(fc * ND + a2 * 3 + 1) * NT];
-        const double x2 = Xs[(fc * ND + a2 * 3 + 2) * NT];
-        double ub = b0 * x0, ug = h0 * x0;
-        ub = __fma_rn(b1, x1, ub); ug = __fma_rn(h1, x1, ug);
-        ub = __fma_rn(b2, x2, ub); ug = __fma_rn(h2, x2, ug);
-        UB[fc][a2] = ub;
-        UG[fc][a2] = ug;
+        if (fc < F2D_KEEP) u_row(q1, Xs, fc, a2, UB[fc][a2], UG[fc][a2]);
+        else UB[fc][a2] = UG[fc][a2] = 0.0;  // unused: re-contracted per point
       }
     double E1[2];
 #pragma unroll
     for (int j2 = 0; j2 < 2; ++j2) {
-      const double acc = c_t24.Bl[q1][0] * E[j2 * 2 + 0];
-      E1[j2] = __fma_rn(c_t24.Bl[q1][1], E[j2 * 2 + 1], acc);
+      const double acc = c_t24.Bl[q1][0] * Es[(j2 * 2 + 0) * NT];
+      E1[j2] = __fma_rn(c_t24.Bl[q1][1], Es[(j2 * 2 + 1) * NT], acc);
     }
     const double *mqp = P.mq + (int64_t)gid * NQ + q1;  // m_q at (q1, q2) = mqp[4 q2]
 
@@ -203,11 +238,13 @@ __global__ void __maxnreg__(128) force2d_kernel(const Params P) {
     ColOut co;
     {
       ArithFast af;
-      column2d<VISC, HAS_W>(af, q1, UB, UG, E1, mqp, gam, ph, co, Sst);
+      double mqn;
+      column2d<VISC, HAS_W>(af, q1, UB, UG, Xs, E1, mqp, mq0, mqn, gam, ph, co, Sst);
       if (!af.ok) {
         ArithIeee ai;
-        column2d<VISC, HAS_W>(ai, q1, UB, UG, E1, mqp, gam, ph, co, Sst);
+        column2d<VISC, HAS_W>(ai, q1, UB, UG, Xs, E1, mqp, mq0, mqn, gam, ph, co, Sst);
       }
+      mq0 = mqn;
     }
     kmin = co.kmin < kmin ? co.kmin : kmin;
     tangled = tangled || co.tangled;

@@ -33,7 +33,7 @@ def main():
             F1, FTw, dt = ctx.force_full(x, v, e, g, visc, cfl)
         torch.cuda.synchronize()
         ts = []
-        for _ in range(10):
+        for _ in range(int(os.environ.get("AB_ITERS", "40"))):
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
@@ -45,7 +45,7 @@ def main():
         out = (F1.cpu().numpy(), FTw.cpu().numpy(), float(dt.item()))
         same = None if ref is None else (np.array_equal(out[1], ref[1]) and out[2] == ref[2])
         ref = ref or out
-        print(f"{name} {var}: median {np.median(ts):.3f} ms  min {min(ts):.3f}  status {st[0]}  "
+        print(f"{name} {var}: median {np.median(ts) * 1e3:.1f} us  min {min(ts) * 1e3:.1f}  status {st[0]}  "
               f"dt {out[2]!r}  FTw/dt identical to first variant: {same}")
 
 
