@@ -256,6 +256,13 @@ hydro_status hydro_rom_rk2avg_step(hydro_rom *rom, double *Yx, double *Yv, doubl
  * last read, then clears them.  Profiling is global to the library (not per context). */
 hydro_status hydro_profile_enable(int on);
 hydro_status hydro_profile_read(double *total_ms /* host */, int64_t *count /* host */);
+/* A call made while its stream is being captured into a CUDA graph records the pair as
+ * external event-record nodes (cudaEventRecordExternal), so every replay of the graph
+ * re-times the kernel.  hydro_profile_read_captured synchronises those events and returns
+ * the summed kernel time of the most recent replay (they are kept, not cleared);
+ * hydro_profile_release_captured returns them to the library once the graph is gone. */
+hydro_status hydro_profile_read_captured(double *total_ms /* host */, int64_t *count /* host */);
+hydro_status hydro_profile_release_captured(void);
 
 /* ------------------------------------------------------------------ introspection (host) */
 /* The library's own correctly rounded 1D tables for (k, q) (DESIGN R5, R6): xi[q], w[q],

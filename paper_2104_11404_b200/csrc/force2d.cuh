@@ -62,6 +62,11 @@ __device__ __forceinline__ void u_row(int q1, const double *Xs, int fc, int a2, 
   ug = __fma_rn(c_t24.G[q1][2], x2, ug);
 }
 
+#ifndef F2D_Q2_UNROLL
+#define F2D_Q2_UNROLL 2
+#endif
+constexpr int F2D_Q2_UNROLL_K = F2D_Q2_UNROLL;
+
 // F2D_KEEP: how many of the (field, component) rows of U stay in registers across the q2
 // loop (the position rows, 2); the velocity (and w) rows are re-contracted from the gathered
 // dofs in shared memory at every point -- the same canonical FMA chain, so the same bits --
@@ -92,7 +97,7 @@ __device__ __forceinline__ void column2d(AR &ar, int q1, const double (&UB)[6][3
   // the global load's latency hides behind the previous point's pointwise stage.  After
   // the last point mq_next holds m_q(q1 + 1, 0) (mqp[1]; a harmless re-read for q1 = 3).
   double mq_cur = mq0;
-#pragma unroll 1
+#pragma unroll (F2D_Q2_UNROLL_K)
   for (int q2 = 0; q2 < 4; ++q2) {
     const double mq = mq_cur;
     mq_cur = __ldg(q2 < 3 ? mqp + 4 * (q2 + 1) : mqp + (q1 < 3 ? 1 : 0));

@@ -111,9 +111,11 @@ struct hydro_sample {
 namespace {
 
 // --- profiling: event pairs around the force kernel (bench.py's live roofline)
+// While a stream is being captured into a CUDA graph the pair is recorded as external
+// event-record nodes (they then time every replay of the graph) and kept in `captured`.
 struct ProfState {
   bool on = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending, pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending, pool, captured;
 };
 ProfState g_prof;
 
@@ -191,15 +193,25 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
   if (use3d) grid2 = P.n_units < resident ? P.n_units : resident;
   std::pair<cudaEvent_t, cudaEvent_t> ev;
   const bool prof = g_prof.on && (MODE == hk::MODE_FORCE || MODE == hk::MODE_DT);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (prof) {
     ev = prof_pair();
-    cudaEventRecord(ev.first, s);
+    CUDA_OK(cudaStreamIsCapturing(s, &cap));
+    if (cap == cudaStreamCaptureStatusActive)
+      CUDA_OK(cudaEventRecordWithFlags(ev.first, s, cudaEventRecordExternal));
+    else
+      CUDA_OK(cudaEventRecord(ev.first, s));
   }
   kern<<<(unsigned)grid2, nt, smem, s>>>(P);
   g_launches++;
   if (prof) {
-    cudaEventRecord(ev.second, s);
-    g_prof.pending.push_back(ev);
+    if (cap == cudaStreamCaptureStatusActive) {
+      CUDA_OK(cudaEventRecordWithFlags(ev.second, s, cudaEventRecordExternal));
+      g_prof.captured.push_back(ev);
+    } else {
+      CUDA_OK(cudaEventRecord(ev.second, s));
+      g_prof.pending.push_back(ev);
+    }
   }
   CUDA_OK(cudaGetLastError());
   return HYDRO_OK;
@@ -306,6 +318,27 @@ hydro_status hydro_profile_read(double *total_ms, int64_t *count) {
   g_prof.pending.clear();
   if (total_ms) *total_ms = tot;
   if (count) *count = n;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_profile_read_captured(double *total_ms, int64_t *count) {
+  double tot = 0.0;
+  int64_t n = 0;
+  for (auto &p : g_prof.captured) {
+    CUDA_OK(cudaEventSynchronize(p.second));
+    float ms = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&ms, p.first, p.second));
+    tot += ms;
+    ++n;
+  }
+  if (total_ms) *total_ms = tot;
+  if (count) *count = n;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_profile_release_captured(void) {
+  for (auto &p : g_prof.captured) g_prof.pool.push_back(p);
+  g_prof.captured.clear();
   return HYDRO_OK;
 }
 

@@ -29,7 +29,8 @@ EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy"
             "hydro_sample_destroy", "hydro_sample_info", "hydro_sample_lists", "hydro_rom_lift",
             "hydro_force_sampled", "hydro_sample_status_sync", "hydro_rom_project_workspace_bytes",
             "hydro_rom_project", "hydro_basis_tables", "hydro_launch_count", "hydro_version",
-            "hydro_profile_enable", "hydro_profile_read", "hydro_selftest_ieee_fast",
+            "hydro_profile_enable", "hydro_profile_read", "hydro_profile_read_captured",
+            "hydro_profile_release_captured", "hydro_selftest_ieee_fast",
             "hydro_fom_create", "hydro_fom_destroy", "hydro_mass_v_apply", "hydro_mass_v_solve",
             "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_rom_create",
             "hydro_rom_destroy", "hydro_rom_rk2avg_step", "hydro_force_stress_bytes",
@@ -114,6 +115,8 @@ def lib() -> ctypes.CDLL:
         L.hydro_launch_count.restype = i64
         L.hydro_profile_enable.argtypes = [i32]
         L.hydro_profile_read.argtypes = [ctypes.POINTER(dbl), ctypes.POINTER(i64)]
+        L.hydro_profile_read_captured.argtypes = [ctypes.POINTER(dbl), ctypes.POINTER(i64)]
+        L.hydro_profile_release_captured.argtypes = []
         L.hydro_version.restype = ctypes.c_char_p
         _lib = L
     return _lib
@@ -191,6 +194,19 @@ def profile_read():
     ms, n = ctypes.c_double(0.0), ctypes.c_int64(0)
     _check(lib().hydro_profile_read(ctypes.byref(ms), ctypes.byref(n)), "hydro_profile_read")
     return ms.value, n.value
+
+
+def profile_read_captured():
+    """(summed force-kernel ms, launches) of the most recent replay of a graph captured with
+    profiling enabled (the events stay attached to the graph)."""
+    ms, n = ctypes.c_double(0.0), ctypes.c_int64(0)
+    _check(lib().hydro_profile_read_captured(ctypes.byref(ms), ctypes.byref(n)),
+           "hydro_profile_read_captured")
+    return ms.value, n.value
+
+
+def profile_release_captured() -> None:
+    _check(lib().hydro_profile_release_captured(), "hydro_profile_release_captured")
 
 
 class HydroContext:

@@ -1,9 +1,9 @@
 #!/usr/bin/env python
-"""A/B timing of two builds of libhydro.so on the same box: each (library, config) pair
-runs in its own process (tools/ab.py's timing loop, default kernel selection), the
-libraries alternating, ROUNDS times.
+"""A/B timing of several builds of libhydro.so on the same box: each (library, config)
+pair runs in its own process (tools/ab.py's timing loop, default kernel selection), the
+library order rotating every round.
 
-    python tools/ab_lib.py ROUNDS LIB_A LIB_B c1 c2 c3
+    python tools/ab_lib.py ROUNDS c1,c2 LIB_A LIB_B [LIB_C ...]
 """
 import os
 import subprocess
@@ -13,10 +13,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def main():
-    rounds, la, lb, cfgs = int(sys.argv[1]), sys.argv[2], sys.argv[3], sys.argv[4:]
+    rounds, cfgs, libs = int(sys.argv[1]), sys.argv[2].split(","), sys.argv[3:]
     for r in range(rounds):
+        order = libs[r % len(libs):] + libs[:r % len(libs)]
         for c in cfgs:
-            for lib in (la, lb) if r % 2 == 0 else (lb, la):
+            for lib in order:
                 env = dict(os.environ, HYDRO_LIB_PATH=os.path.abspath(lib))
                 out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ab.py"), c,
                                       "HYDRO_AB=1"], env=env, capture_output=True, text=True)
