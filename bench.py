@@ -415,24 +415,40 @@ def bench_rom_step(plan, b, Phi_x, Phi_v, Phi_e, x_os, v_os, e_os, Pv, Pe, Cxv, 
 
 
 def e2e_full(ctx, prob, base, visc, cfl, n_qp, args, dev):
+    """End to end through hydro_force_full with host buffers.  The step's inputs are the
+    state (x, v, e) -- F(x, v, e) of PAPER P:403-411 -- packed in one pinned host buffer
+    and uploaded with one copy; its results (F1, FTw, dt) come back in one packed copy.
+    The material constant gamma is uploaded once with the mesh (setup, like x0 and rho0)."""
     import torch
     m = base.mesh
-    host_in = [torch.as_tensor(np.ascontiguousarray(a)).pin_memory()
-               for a in (prob.x, prob.v, prob.e, base.gamma)]
+    parts_in = [np.ascontiguousarray(a, dtype=np.float64) for a in (prob.x, prob.v, prob.e)]
+    sizes_in = [a.size for a in parts_in]
+    host_in = torch.from_numpy(np.concatenate([a.ravel() for a in parts_in])).pin_memory()
+    gamma = torch.as_tensor(np.ascontiguousarray(base.gamma)).to(dev)
+    shapes_out = [(m.dim, m.n_nodes), (m.n_elem, m.ne), (1,)]
+    n_out = sum(int(np.prod(sh)) for sh in shapes_out)
+
+    def views(buf, sizes, shapes):
+        out, o = [], 0
+        for n, sh in zip(sizes, shapes):
+            out.append(buf[o:o + n].view(sh))
+            o += n
+        return out
+
+    shapes_in = [a.shape for a in parts_in]
     dbuf, hout = [], []
     for _ in range(2):
-        dbuf.append(dict(inp=[torch.empty_like(h, device=dev) for h in host_in],
-                         F1=torch.empty((m.dim, m.n_nodes), dtype=torch.float64, device=dev),
-                         FTw=torch.empty((m.n_elem, m.ne), dtype=torch.float64, device=dev),
-                         dt=torch.empty(1, dtype=torch.float64, device=dev)))
-        hout.append([torch.empty((m.dim, m.n_nodes), dtype=torch.float64).pin_memory(),
-                     torch.empty((m.n_elem, m.ne), dtype=torch.float64).pin_memory(),
-                     torch.empty(1, dtype=torch.float64).pin_memory()])
+        din = torch.empty(host_in.numel(), dtype=torch.float64, device=dev)
+        dout = torch.empty(n_out, dtype=torch.float64, device=dev)
+        F1, FTw, dt = views(dout, [int(np.prod(sh)) for sh in shapes_out], shapes_out)
+        dbuf.append(dict(din=din, inp=views(din, sizes_in, shapes_in), dout=dout, F1=F1, FTw=FTw, dt=dt))
+        hout.append(torch.empty(n_out, dtype=torch.float64).pin_memory())
     s_in, s_cp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     ev = lambda: torch.cuda.Event()
     in_done = [ev(), ev()]; cp_done = [ev(), ev()]; out_done = [ev(), ev()]
     for e_ in out_done + cp_done:
         e_.record(torch.cuda.current_stream())
+    torch.cuda.synchronize()
 
     def run(n):
         for it in range(n):
@@ -440,19 +456,17 @@ def e2e_full(ctx, prob, base, visc, cfl, n_qp, args, dev):
             b = dbuf[k]
             with torch.cuda.stream(s_in):
                 s_in.wait_event(cp_done[k])          # step it-2 finished reading inputs k
-                for d, h in zip(b["inp"], host_in):
-                    d.copy_(h, non_blocking=True)
+                b["din"].copy_(host_in, non_blocking=True)
                 in_done[k].record(s_in)
             with torch.cuda.stream(s_cp):
                 s_cp.wait_event(in_done[k])
                 s_cp.wait_event(out_done[k])         # step it-2's download of outputs k done
-                x, v, e, g = b["inp"]
-                ctx.force_full(x, v, e, g, visc, cfl, F1=b["F1"], FTw=b["FTw"], dt=b["dt"])
+                x, v, e = b["inp"]
+                ctx.force_full(x, v, e, gamma, visc, cfl, F1=b["F1"], FTw=b["FTw"], dt=b["dt"])
                 cp_done[k].record(s_cp)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(cp_done[k])
-                for h, d in zip(hout[k], (b["F1"], b["FTw"], b["dt"])):
-                    h.copy_(d, non_blocking=True)
+                hout[k].copy_(b["dout"], non_blocking=True)
                 out_done[k].record(s_out)
 
     run(args.warmup)
@@ -468,12 +482,27 @@ def e2e_full(ctx, prob, base, visc, cfl, n_qp, args, dev):
     st = ctx.status_sync()
     if st[0] != 0:
         raise RuntimeError(f"e2e: device status {st}")
-    h2d = sum(t.numel() * 8 for t in host_in)
-    d2h = sum(t.numel() * 8 for t in hout[0])
+    h2d = host_in.numel() * 8
+    d2h = hout[0].numel() * 8
+    # the link alone: the same copies timed without compute (context for the e2e number)
+    link = {}
+    for name_, fn in (("h2d", lambda: dbuf[0]["din"].copy_(host_in, non_blocking=True)),
+                      ("d2h", lambda: hout[0].copy_(dbuf[0]["dout"], non_blocking=True))):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(5):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        link[name_ + "_gbps"] = 5 * (h2d if name_ == "h2d" else d2h) / (a.elapsed_time(b) * 1e-3) / 1e9
     return {"value": n_qp / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ems,
-            "method": "public API (hydro_force_full) with pinned host buffers; uploads, "
-                      "compute and downloads of consecutive steps overlapped on 3 streams"}
+            "link_alone": {k: round(v, 1) for k, v in link.items()},
+            "method": "public API (hydro_force_full); per step one H2D copy of the packed "
+                      "state (x, v, e) from pinned host memory and one D2H copy of the packed "
+                      "results (F1, FTw, dt); gamma resident (material constant, set up with "
+                      "the mesh); uploads, compute and downloads of consecutive steps "
+                      "overlapped on 3 streams"}
 
 
 def e2e_rom(step_inputs, step_outputs, step, n_qp, args):
