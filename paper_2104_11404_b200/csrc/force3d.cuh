@@ -238,7 +238,7 @@ force3d_kernel(const Params P) {
     PointOut po;
     {
       ArithFast af;
-      pointwise<3, VISC, HAS_W, true>(af, J, Gv, Gw, eq, sc.mq, sc.gam, wq, ph, po);
+      pointwise<3, VISC, HAS_W, true, ArithFast, true>(af, J, Gv, Gw, eq, sc.mq, sc.gam, wq, ph, po);
       if (!af.ok) {
         forward_point<3, K, Q, NF, true>(sB, sG, sBl, Wk, q1i, q2i, q3i, J, Gv, Gw, eq);
         if (!HAS_W) {

@@ -132,10 +132,36 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // rotations can be interleaved by the scheduler.  The rotated entries are exactly the
 // contract's: dlt = 0.5(a_qq - a_pp), r = sqrt(dlt^2 + a_pq^2), t = a_pq/(|dlt| + r)
 // (negated if dlt < 0), c = 1/sqrt(1 + t^2), s = t c.
+#ifdef HYDRO_COUNT_ROT
+// diagnostic build only (tools/rot_count.py): [0] lane-slots of executed rotations,
+// [1] rotations a lane actually needed (not skipped)
+__device__ unsigned long long g_rot_count[2];
+__device__ unsigned long long g_sweep_count[4][2];  // [sweep]: lanes live (a + e), lane-slots executed
+__device__ __forceinline__ void count_sweep(int sweep, bool la, bool le, bool wa, bool we) {
+  const unsigned b = __ballot_sync(0xffffffffu, la), c = __ballot_sync(0xffffffffu, le);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&g_sweep_count[sweep][0], (unsigned long long)(__popc(b) + __popc(c)));
+    atomicAdd(&g_sweep_count[sweep][1], (unsigned long long)(32 * ((int)wa + (int)we)));
+  }
+}
+__device__ __forceinline__ void count_rot(bool go) {
+  const unsigned m = __activemask();
+  const unsigned b = __ballot_sync(m, go);
+  if ((threadIdx.x & 31) == __ffs(m) - 1) {
+    atomicAdd(&g_rot_count[0], (unsigned long long)__popc(m));
+    atomicAdd(&g_rot_count[1], (unsigned long long)__popc(b));
+  }
+}
+#else
+__device__ __forceinline__ void count_rot(bool) {}
+__device__ __forceinline__ void count_sweep(int, bool, bool, bool, bool) {}
+#endif
+
 template <class AR>
 __device__ __forceinline__ void jacobi_rot(AR &ar, double &app, double &aqq, double &apq,
                                            double &arp, double &arq, const double tol) {
   const bool go = !(fabs(apq) <= tol);
+  count_rot(go);
   const double a_ = go ? apq : 1.0;
   const double dl = go ? 0.5 * (aqq - app) : 0.0;
   const double rr = ar.sqrt_(dl * dl + a_ * a_);
@@ -169,6 +195,8 @@ __device__ __forceinline__ void jacobi_rot2(AR &ar, double &app, double &aqq, do
                                             double &epp, double &eqq, double &epq,
                                             double &erp, double &erq, const double te) {
   const bool ga = !(fabs(apq) <= ta), ge = !(fabs(epq) <= te);
+  count_rot(ga);
+  count_rot(ge);
   const double a_ = ga ? apq : 1.0, e_ = ge ? epq : 1.0;
   const double dla = ga ? 0.5 * (aqq - app) : 0.0, dle = ge ? 0.5 * (eqq - epp) : 0.0;
   const double sa = dla * dla + a_ * a_, se = dle * dle + e_ * e_;
@@ -208,15 +236,61 @@ __device__ __forceinline__ bool offdiag_live(double a01, double a02, double a12,
   return !(fabs(a01) <= tol) || !(fabs(a02) <= tol) || !(fabs(a12) <= tol);
 }
 
+// The remaining sweeps [sweep0, 4) of lmin3_pair once at most 32 matrices of the warp
+// (either kind, over all lanes) are still live: they are compacted onto the first lanes
+// (lane i takes the i-th live matrix; __fns finds its owner) and rotated one matrix per lane,
+// so the slots the converged lanes would have skipped cost nothing.  Each matrix sees the
+// same rotation sequence with the same arithmetic (jacobi_rot), so its lambda_min is
+// bit-identical to the uncompacted schedule's; a matrix that was not live keeps its entries.
+template <class AR>
+__device__ __forceinline__ void lmin3_pair_compact(AR &ar, int sweep0, unsigned ba, unsigned be,
+                                                 double a00, double a11, double a22, double a01,
+                                                 double a02, double a12, double ta, double e00,
+                                                 double e11, double e22, double e01, double e02,
+                                                 double e12, double te, double &la, double &le) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int na = __popc(ba), n = na + __popc(be);
+  const bool mine = lane < n, isE = lane >= na;
+  const int src = mine ? (int)__fns(isE ? be : ba, 0, (isE ? lane - na : lane) + 1) : lane;
+  // both shuffles are issued by every lane (the source lane does not know which is wanted)
+  const double sa00 = __shfl_sync(full, a00, src), se00 = __shfl_sync(full, e00, src);
+  const double sa11 = __shfl_sync(full, a11, src), se11 = __shfl_sync(full, e11, src);
+  const double sa22 = __shfl_sync(full, a22, src), se22 = __shfl_sync(full, e22, src);
+  const double sa01 = __shfl_sync(full, a01, src), se01 = __shfl_sync(full, e01, src);
+  const double sa02 = __shfl_sync(full, a02, src), se02 = __shfl_sync(full, e02, src);
+  const double sa12 = __shfl_sync(full, a12, src), se12 = __shfl_sync(full, e12, src);
+  const double sta = __shfl_sync(full, ta, src), ste = __shfl_sync(full, te, src);
+  double m00 = isE ? se00 : sa00, m11 = isE ? se11 : sa11, m22 = isE ? se22 : sa22;
+  double m01 = isE ? se01 : sa01, m02 = isE ? se02 : sa02, m12 = isE ? se12 : sa12;
+  const double tm = isE ? ste : sta;
+  if (!mine) m01 = m02 = m12 = 0.0;  // idle lanes: nothing live, never keeps the loop going
+#pragma unroll 1
+  for (int sweep = sweep0; sweep < 4; ++sweep) {
+    if (!__any_sync(full, offdiag_live(m01, m02, m12, tm))) break;
+    jacobi_rot(ar, m00, m11, m01, m02, m12, tm);  // (0,1), r3 = 2
+    jacobi_rot(ar, m00, m22, m02, m01, m12, tm);  // (0,2), r3 = 1
+    jacobi_rot(ar, m11, m22, m12, m01, m02, tm);  // (1,2), r3 = 0
+  }
+  const double lam = fmin(fmin(m00, m11), m22);
+  const unsigned lt = (1u << lane) - 1u;
+  const double lA = __shfl_sync(full, lam, __popc(ba & lt));
+  const double lE = __shfl_sync(full, lam, (na + __popc(be & lt)) & 31);
+  la = ((ba >> lane) & 1u) ? lA : fmin(fmin(a00, a11), a22);
+  le = ((be >> lane) & 1u) ? lE : fmin(fmin(e00, e11), e22);
+}
+
 // Smallest eigenvalues of two symmetric 3x3 matrices (DESIGN A.4), their rotations
-// interleaved.  EARLY: the warp leaves the sweep loop once no lane has a live
+// interleaved.  COMPACT: from the third sweep on, once <= 32 matrices of the warp are live,
+// finish in lmin3_pair_compact (force3d: C2 -5.5 %; the 72-register generic kernel spills
+// more with it and loses 5 %, so it does not use it).  EARLY: the warp leaves the sweep loop once no lane has a live
 // off-diagonal in either matrix (every remaining rotation would be a skip) -- needs all
 // 32 lanes converged, so only the fast (non-divergent) pass uses it.
-template <class AR, bool EARLY>
+template <class AR, bool EARLY, bool COMPACT = false>
 __device__ __forceinline__ void lmin3_pair(AR &ar, double a00, double a11, double a22,
                                            double a01, double a02, double a12, double e00,
                                            double e11, double e22, double e01, double e02,
-                                           double e12, double &la, double &le) {
+                                           double e12, double &la_out, double &le_out) {
   const double ta = amax6(a00, a11, a22, a01, a02, a12) * 0x1p-53;
   const double te = amax6(e00, e11, e22, e01, e02, e12) * 0x1p-53;
 #pragma unroll 1
@@ -227,7 +301,16 @@ __device__ __forceinline__ void lmin3_pair(AR &ar, double a00, double a11, doubl
       // interleaved only when both are live -- a converged matrix costs nothing
       const bool la = offdiag_live(a01, a02, a12, ta), le = offdiag_live(e01, e02, e12, te);
       const bool wa = __any_sync(0xffffffffu, la), we = __any_sync(0xffffffffu, le);
+      count_sweep(sweep, la, le, wa, we);
       if (!(wa || we)) break;
+      if (COMPACT && sweep >= 2) {
+        const unsigned ba = __ballot_sync(0xffffffffu, la), be = __ballot_sync(0xffffffffu, le);
+        if (__popc(ba) + __popc(be) <= 32) {
+          lmin3_pair_compact(ar, sweep, ba, be, a00, a11, a22, a01, a02, a12, ta, e00, e11, e22,
+                             e01, e02, e12, te, la_out, le_out);
+          return;
+        }
+      }
       if (wa && we) {
         jacobi_rot2(ar, a00, a11, a01, a02, a12, ta, e00, e11, e01, e02, e12, te);  // (0,1)
         jacobi_rot2(ar, a00, a22, a02, a01, a12, ta, e00, e22, e02, e01, e12, te);  // (0,2)
@@ -250,8 +333,8 @@ __device__ __forceinline__ void lmin3_pair(AR &ar, double a00, double a11, doubl
       jacobi_rot(ar, e11, e22, e12, e01, e02, te);
     }
   }
-  la = fmin(fmin(a00, a11), a22);
-  le = fmin(fmin(e00, e11), e22);
+  la_out = fmin(fmin(a00, a11), a22);
+  le_out = fmin(fmin(e00, e11), e22);
 }
 
 template <class AR, bool EARLY>
@@ -322,7 +405,7 @@ struct PointOut {
 // Pointwise stage (DESIGN A.3/A.4) through arithmetic policy AR; everything dt_q depends
 // on follows the contract exactly.  Gw: gradhat of the field F^T is applied to (== Gv
 // when w is v).  S and A are tolerance-only (A.5).
-template <int DIM, bool VISC, bool HAS_W, bool EARLY, class AR>
+template <int DIM, bool VISC, bool HAS_W, bool EARLY, class AR, bool COMPACT = false>
 __device__ __forceinline__ void pointwise(AR &ar, const double (&J)[3][3], const double (&Gv)[3][3],
                                           const double (&Gw)[3][3], double eq, double mq,
                                           double gam, double wq, const PhysIn &ph, PointOut &o) {
@@ -371,7 +454,7 @@ __device__ __forceinline__ void pointwise(AR &ar, const double (&J)[3][3], const
     const double c12 = (J[0][1] * J[0][2] + J[1][1] * J[1][2]) + J[2][1] * J[2][2];
     double lj;
     if (VISC) {
-      lmin3_pair<AR, EARLY>(ar, c00, c11, c22, c01, c02, c12, eps[0][0], eps[1][1], eps[2][2],
+      lmin3_pair<AR, EARLY, COMPACT>(ar, c00, c11, c22, c01, c02, c12, eps[0][0], eps[1][1], eps[2][2],
                             eps[0][1], eps[0][2], eps[1][2], lj, lam);
     } else {
       lj = lmin3<AR, EARLY>(ar, c00, c11, c22, c01, c02, c12);

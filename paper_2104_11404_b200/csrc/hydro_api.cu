@@ -321,6 +321,19 @@ hydro_status hydro_profile_read(double *total_ms, int64_t *count) {
   return HYDRO_OK;
 }
 
+#ifdef HYDRO_COUNT_ROT
+hydro_status hydro_debug_rot_counts(unsigned long long *out /* host [10] */, int reset) {
+  CUDA_OK(cudaMemcpyFromSymbol(out, hk::g_rot_count, 2 * sizeof(unsigned long long)));
+  CUDA_OK(cudaMemcpyFromSymbol(out + 2, hk::g_sweep_count, 8 * sizeof(unsigned long long)));
+  if (reset) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    CUDA_OK(cudaMemcpyToSymbol(hk::g_rot_count, z, 2 * sizeof(unsigned long long)));
+    CUDA_OK(cudaMemcpyToSymbol(hk::g_sweep_count, z, sizeof(z)));
+  }
+  return HYDRO_OK;
+}
+#endif
+
 hydro_status hydro_profile_read_captured(double *total_ms, int64_t *count) {
   double tot = 0.0;
   int64_t n = 0;
