@@ -239,6 +239,7 @@ force3d_kernel(const Params P) {
     {
       ArithFast af;
       pointwise<3, VISC, HAS_W, true, ArithFast, true>(af, J, Gv, Gw, eq, sc.mq, sc.gam, wq, ph, po);
+      count_rerun(!af.ok);
       if (!af.ok) {
         forward_point<3, K, Q, NF, true>(sB, sG, sBl, Wk, q1i, q2i, q3i, J, Gv, Gw, eq);
         if (!HAS_W) {

@@ -137,6 +137,15 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // [1] rotations a lane actually needed (not skipped)
 __device__ unsigned long long g_rot_count[2];
 __device__ unsigned long long g_sweep_count[4][2];  // [sweep]: lanes live (a + e), lane-slots executed
+__device__ unsigned long long g_rerun_count[2];     // points re-run with IEEE ops, warps affected
+__device__ __forceinline__ void count_rerun(bool rerun) {
+  const unsigned m = __activemask();
+  const unsigned b = __ballot_sync(m, rerun);
+  if ((threadIdx.x & 31) == __ffs(m) - 1 && b) {
+    atomicAdd(&g_rerun_count[0], (unsigned long long)__popc(b));
+    atomicAdd(&g_rerun_count[1], 1ull);
+  }
+}
 __device__ __forceinline__ void count_sweep(int sweep, bool la, bool le, bool wa, bool we) {
   const unsigned b = __ballot_sync(0xffffffffu, la), c = __ballot_sync(0xffffffffu, le);
   if ((threadIdx.x & 31) == 0) {
@@ -155,6 +164,7 @@ __device__ __forceinline__ void count_rot(bool go) {
 #else
 __device__ __forceinline__ void count_rot(bool) {}
 __device__ __forceinline__ void count_sweep(int, bool, bool, bool, bool) {}
+__device__ __forceinline__ void count_rerun(bool) {}
 #endif
 
 template <class AR>

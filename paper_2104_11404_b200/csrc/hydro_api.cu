@@ -322,13 +322,15 @@ hydro_status hydro_profile_read(double *total_ms, int64_t *count) {
 }
 
 #ifdef HYDRO_COUNT_ROT
-hydro_status hydro_debug_rot_counts(unsigned long long *out /* host [10] */, int reset) {
+hydro_status hydro_debug_rot_counts(unsigned long long *out /* host [12] */, int reset) {
   CUDA_OK(cudaMemcpyFromSymbol(out, hk::g_rot_count, 2 * sizeof(unsigned long long)));
   CUDA_OK(cudaMemcpyFromSymbol(out + 2, hk::g_sweep_count, 8 * sizeof(unsigned long long)));
+  CUDA_OK(cudaMemcpyFromSymbol(out + 10, hk::g_rerun_count, 2 * sizeof(unsigned long long)));
   if (reset) {
     const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     CUDA_OK(cudaMemcpyToSymbol(hk::g_rot_count, z, 2 * sizeof(unsigned long long)));
     CUDA_OK(cudaMemcpyToSymbol(hk::g_sweep_count, z, sizeof(z)));
+    CUDA_OK(cudaMemcpyToSymbol(hk::g_rerun_count, z, 2 * sizeof(unsigned long long)));
   }
   return HYDRO_OK;
 }
