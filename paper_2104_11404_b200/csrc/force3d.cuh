@@ -59,6 +59,25 @@ struct G3 {
   static constexpr int MINB = NT >= 224 ? 2 : 10;
 };
 
+// The exact IEEE re-run of one point (rare: a fast-path range check failed), out of line so
+// that its ~1 500 instructions do not sit inside the unit loop's instruction footprint.
+template <int K, int Q, int NF, bool VISC, bool HAS_W>
+__device__ __noinline__ void rerun_point_ieee(const double *sB, const double *sG, const double *sBl,
+                                              const double *Wk, int q1i, int q2i, int q3i,
+                                              double mq, double gam, double wq, PhysIn ph,
+                                              PointOut *po) {
+  double J[3][3], Gv[3][3], Gw[3][3], eq = 0.0;
+  forward_point<3, K, Q, NF, true>(sB, sG, sBl, Wk, q1i, q2i, q3i, J, Gv, Gw, eq);
+  if (!HAS_W) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) Gw[c][d] = 0.0;
+  }
+  ArithIeee ai;
+  pointwise<3, VISC, HAS_W, false>(ai, J, Gv, Gw, eq, mq, gam, wq, ph, *po);
+}
+
 template <int K, int Q, bool VISC, int MODE, bool BATCHED, bool HAS_W>
 __global__ void __launch_bounds__(G3<K, Q, HAS_W ? 3 : 2>::NT, G3<K, Q, HAS_W ? 3 : 2>::MINB)
 force3d_kernel(const Params P) {
@@ -240,17 +259,8 @@ force3d_kernel(const Params P) {
       ArithFast af;
       pointwise<3, VISC, HAS_W, true, ArithFast, true>(af, J, Gv, Gw, eq, sc.mq, sc.gam, wq, ph, po);
       count_rerun(!af.ok);
-      if (!af.ok) {
-        forward_point<3, K, Q, NF, true>(sB, sG, sBl, Wk, q1i, q2i, q3i, J, Gv, Gw, eq);
-        if (!HAS_W) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int d = 0; d < 3; ++d) Gw[c][d] = 0.0;
-        }
-        ArithIeee ai;
-        pointwise<3, VISC, HAS_W, false>(ai, J, Gv, Gw, eq, sc.mq, sc.gam, wq, ph, po);
-      }
+      if (!af.ok) rerun_point_ieee<K, Q, NF, VISC, HAS_W>(sB, sG, sBl, Wk, q1i, q2i, q3i, sc.mq,
+                                                           sc.gam, wq, ph, &po);
     }
     // ---- S6 dt: flags; key min per thread (full) or per unit (batched)
     const bool pt = lt < NQ;

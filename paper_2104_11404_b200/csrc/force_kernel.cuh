@@ -313,7 +313,9 @@ __device__ __forceinline__ void lmin3_pair(AR &ar, double a00, double a11, doubl
       const bool wa = __any_sync(0xffffffffu, la), we = __any_sync(0xffffffffu, le);
       count_sweep(sweep, la, le, wa, we);
       if (!(wa || we)) break;
-      if (COMPACT && sweep >= 2) {
+      // (a sweep with only one kind live always fits: its single-matrix code paths below
+      // are then dead and compiled out, which keeps the kernel's hot loop smaller)
+      if (COMPACT && (sweep >= 2 || !(wa && we))) {
         const unsigned ba = __ballot_sync(0xffffffffu, la), be = __ballot_sync(0xffffffffu, le);
         if (__popc(ba) + __popc(be) <= 32) {
           lmin3_pair_compact(ar, sweep, ba, be, a00, a11, a22, a01, a02, a12, ta, e00, e11, e22,
@@ -325,6 +327,8 @@ __device__ __forceinline__ void lmin3_pair(AR &ar, double a00, double a11, doubl
         jacobi_rot2(ar, a00, a11, a01, a02, a12, ta, e00, e11, e01, e02, e12, te);  // (0,1)
         jacobi_rot2(ar, a00, a22, a02, a01, a12, ta, e00, e22, e02, e01, e12, te);  // (0,2)
         jacobi_rot2(ar, a11, a22, a12, a01, a02, ta, e11, e22, e12, e01, e02, te);  // (1,2)
+      } else if (COMPACT) {
+        __builtin_unreachable();  // handled by lmin3_pair_compact above
       } else if (wa) {
         jacobi_rot(ar, a00, a11, a01, a02, a12, ta);
         jacobi_rot(ar, a00, a22, a02, a01, a12, ta);
