@@ -45,6 +45,10 @@ __device__ __forceinline__ int opaque_tid() {
   return t;
 }
 
+#ifndef F3D_MINB
+#define F3D_MINB 10
+#endif
+
 template <int K, int Q, int NF>
 struct G3 {
   using G = Geo<3, K, Q, NF>;
@@ -56,7 +60,7 @@ struct G3 {
   static constexpr size_t SMEM = sizeof(double) * (size_t)(TABD + 2 * XE + WORK);
   // occupancy target (registers): ~96/thread for Q=4 (10 CTAs of 64); Q=6: 2 x 224 threads
   // (~144 registers: the 3 x 224 budget of 80 registers spilled heavily)
-  static constexpr int MINB = NT >= 224 ? 2 : 10;
+  static constexpr int MINB = NT >= 224 ? 2 : F3D_MINB;
 };
 
 // The exact IEEE re-run of one point (rare: a fast-path range check failed), out of line so
