@@ -486,6 +486,18 @@ __global__ void cg_init_kernel(int64_t n, const double *__restrict__ b, const do
   z[i] = zi;
   p[i] = zi;
 }
+// warm start: r = mask b - Ap (Ap = mask M x0, r = mask b on entry), z = D^-1 r, p = z
+__global__ void cg_residual_kernel(int64_t n, const double *__restrict__ Ap,
+                                   const double *__restrict__ dinv, double *__restrict__ r,
+                                   double *__restrict__ z, double *__restrict__ p) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double ri = r[i] - Ap[i];
+  r[i] = ri;
+  const double zi = dinv[i] * ri;
+  z[i] = zi;
+  p[i] = zi;
+}
 __global__ void cg_xr_kernel(int64_t n, const double *__restrict__ sc, const double *__restrict__ p,
                              const double *__restrict__ Ap, const double *__restrict__ dinv,
                              double *__restrict__ x, double *__restrict__ r, double *__restrict__ z) {

@@ -862,6 +862,7 @@ struct hydro_fom {
   double *F1 = nullptr, *F1x = nullptr, *FTw = nullptr, *FTx = nullptr, *dv = nullptr;
   double *vh = nullptr, *eh = nullptr, *xh = nullptr, *v1 = nullptr, *vbar = nullptr,
          *dts = nullptr, *S = nullptr;
+  bool have_dv = false;  // dv holds the previous solve's solution (warm start of the step's CG)
   std::vector<void *> allocs;
 };
 
@@ -977,22 +978,42 @@ hydro_status mass_e_update(hydro_fom *f, const double *a, const double *rhs, dou
   return HYDRO_OK;
 }
 
-// PCG with the Jacobi preconditioner on the free dofs; rel. preconditioned residual.
+// PCG with the Jacobi preconditioner on the free dofs.  Stops when the preconditioned
+// residual norm relative to the right-hand side's, sqrt(r.z / b.D^-1 b), is <= tol.
+// warm: x holds the initial guess (constrained components zero), else x0 = 0 -- the two
+// coincide in their first residual when x = 0.
 hydro_status pcg(hydro_fom *f, const double *b, double *x, double tol, int max_iter, int *iters,
-                 double *relres, cudaStream_t s) {
+                 double *relres, cudaStream_t s, bool warm = false) {
   const int64_t n = f->n;
   const unsigned g = blocks_for(n, 256);
-  hk::cg_init_kernel<<<g, 256, 0, s>>>(n, b, f->mask, f->dinv, x, f->r, f->z, f->p);
+  // r = mask b, z = D^-1 r (= p), x = 0; the reference norm b.D^-1 b is r.z of this state
+  hk::cg_init_kernel<<<g, 256, 0, s>>>(n, b, f->mask, f->dinv, warm ? f->Ap : x, f->r, f->z, f->p);
   g_launches++;
   CUDA_OK(cudaGetLastError());
-  hydro_status st = dot(f, n, f->r, f->z, f->sc + 0, s);
+  hydro_status st = dot(f, n, f->r, f->z, f->sc + 5, s);
   if (st != HYDRO_OK) return st;
-  double rz0 = 0.0;
-  CUDA_OK(cudaMemcpyAsync(&rz0, f->sc + 0, sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (warm) {
+    // r = mask (b - M x), z = D^-1 r, p = z
+    const hydro_mesh_desc &d = f->c->d;
+    if ((st = mass_apply_elements(f, x, s)) != HYDRO_OK) return st;
+    if (d.dim == 3)
+      hk::assemble_dot_kernel<3><<<hk::DOT_BLOCKS, hk::DOT_THREADS, 0, s>>>(
+          d.n_nodes, f->c->off, f->c->evec, f->mask, x, f->Ap, f->part);
+    else
+      hk::assemble_dot_kernel<2><<<hk::DOT_BLOCKS, hk::DOT_THREADS, 0, s>>>(
+          d.n_nodes, f->c->off, f->c->evec, f->mask, x, f->Ap, f->part);
+    hk::cg_residual_kernel<<<g, 256, 0, s>>>(n, f->Ap, f->dinv, f->r, f->z, f->p);
+    g_launches += 2;
+    CUDA_OK(cudaGetLastError());
+  }
+  if ((st = dot(f, n, f->r, f->z, f->sc + 0, s)) != HYDRO_OK) return st;
+  double h[6];
+  CUDA_OK(cudaMemcpyAsync(h, f->sc, 6 * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_OK(cudaStreamSynchronize(s));
+  const double rz0 = h[0], bz = h[5];
   int it = 0;
-  double rel = 0.0;
-  if (rz0 > 0.0) {
+  double rel = bz > 0.0 ? sqrt(rz0 / bz) : 0.0;
+  if (rz0 > 0.0 && rel > tol) {
     rel = 1.0;
     const hydro_mesh_desc &d = f->c->d;
     while (it < max_iter) {
@@ -1016,7 +1037,7 @@ hydro_status pcg(hydro_fom *f, const double *b, double *x, double tol, int max_i
         double rz = 0.0;
         CUDA_OK(cudaMemcpyAsync(&rz, f->sc + 0, sizeof(double), cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaStreamSynchronize(s));
-        rel = sqrt(rz / rz0);
+        rel = sqrt(rz / bz);
         if (!(rel > tol)) break;
       }
     }
@@ -1157,7 +1178,11 @@ hydro_status hydro_rk2avg_step(hydro_fom *f, double *x, double *v, double *e, co
   // ---- stage 1: F(U^n) (F.1, dt, and the point stresses S_q for the transposed product)
   if ((st = force_common(c, hk::MODE_FORCE, x, v, e, nullptr, gamma, visc, cfl, f->F1, f->FTx,
                          f->dts + 0, s, f->S)) != HYDRO_OK) return st;
-  if ((st = pcg(f, f->F1, f->dv, cg_tol, cg_max_iter, &it1, nullptr, s)) != HYDRO_OK) return st;
+  // the CG of each stage starts from the previous solve's solution (the accelerations of
+  // consecutive stages differ by O(dt)); the stopping test is relative to the rhs either way
+  if ((st = pcg(f, f->F1, f->dv, cg_tol, cg_max_iter, &it1, nullptr, s, f->have_dv)) != HYDRO_OK)
+    return st;
+  f->have_dv = true;
   hk::axpy_kernel<<<g, 256, 0, s>>>(n, v, -0.5 * dt, f->dv, f->mask, f->vh);    // v^{n+1/2}
   g_launches++;
   if ((st = hydro_force_transpose(c, f->S, f->vh, f->FTw, stream)) != HYDRO_OK) return st;  // F(U^n)^T v^{n+1/2}
@@ -1167,7 +1192,7 @@ hydro_status hydro_rk2avg_step(hydro_fom *f, double *x, double *v, double *e, co
   // ---- stage 2: F(U^{n+1/2})
   if ((st = force_common(c, hk::MODE_FORCE, f->xh, f->vh, f->eh, nullptr, gamma, visc, cfl, f->F1,
                          f->FTx, f->dts + 1, s, f->S)) != HYDRO_OK) return st;
-  if ((st = pcg(f, f->F1, f->dv, cg_tol, cg_max_iter, &it2, nullptr, s)) != HYDRO_OK) return st;
+  if ((st = pcg(f, f->F1, f->dv, cg_tol, cg_max_iter, &it2, nullptr, s, true)) != HYDRO_OK) return st;
   hk::axpy_kernel<<<g, 256, 0, s>>>(n, v, -dt, f->dv, f->mask, f->v1);         // v^{n+1}
   hk::avg_kernel<<<g, 256, 0, s>>>(n, v, f->v1, f->vbar);                       // vbar
   g_launches += 2;
