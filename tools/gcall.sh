@@ -15,3 +15,9 @@ for w in "$@"; do
      -o $O/${w}_full python tools/prof_case.py $w --iters 3 > $O/ncu_$w.log 2>&1
   echo "ncu $w rc=$?" >> $O/rc.txt
 done
+# launch list of the bench command itself (ncu's per-launch durations; first 400 launches)
+if [ -n "$LAUNCHES" ]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --only --no-cpu > $O/ncu_launch.log 2>&1
+  echo "ncu launches rc=$?" >> $O/rc.txt
+fi
