@@ -29,13 +29,7 @@
 
 namespace hk {
 
-struct Tab24 {
-  double w[4];
-  double B[4][3];
-  double G[4][3];
-  double Bl[4][2];
-};
-__constant__ Tab24 c_t24;
+// (Tab24 / c_t24 are defined in force_kernel.cuh, shared with the blocked 3D stages)
 
 struct ColOut {
   double T[2][2][3];  // T[c][d][a2] of this q1

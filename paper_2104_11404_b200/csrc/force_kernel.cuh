@@ -600,6 +600,46 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
   }
 }
 
+// Warp-compacted final Jacobi sweeps in the generic kernel (3D Q2 only; Q3 at 72 registers
+// spills more with it): see lmin3_pair.  Off by default: on the blocked generic kernel it is
+// neutral (C2 +0.8 %, C4 -0.3 %: profiles/ab/r01_ab23_*); force3d keeps it.
+#ifndef F3_COMPACT
+#define F3_COMPACT 0
+#endif
+
+// ----------------------------------------------------------------------------- tables
+// The 1D tables in __constant__ memory (filled at context creation, packed order w, B, G, Bl):
+// in the register-blocked 3D stages below every table index is a compile-time constant, so the
+// entries are read as uniform constant-bank operands (no shared-memory loads).
+struct Tab24 {
+  double w[4];
+  double B[4][3];
+  double G[4][3];
+  double Bl[4][2];
+};
+struct Tab36 {
+  double w[6];
+  double B[6][4];
+  double G[6][4];
+  double Bl[6][3];
+};
+__constant__ Tab24 c_t24;
+__constant__ Tab36 c_t36;
+template <int K, int Q>
+struct CTab;
+template <>
+struct CTab<2, 4> {
+  static __device__ __forceinline__ double B(int q, int a) { return c_t24.B[q][a]; }
+  static __device__ __forceinline__ double G(int q, int a) { return c_t24.G[q][a]; }
+  static __device__ __forceinline__ double Bl(int q, int j) { return c_t24.Bl[q][j]; }
+};
+template <>
+struct CTab<3, 6> {
+  static __device__ __forceinline__ double B(int q, int a) { return c_t36.B[q][a]; }
+  static __device__ __forceinline__ double G(int q, int a) { return c_t36.G[q][a]; }
+  static __device__ __forceinline__ double Bl(int q, int j) { return c_t36.Bl[q][j]; }
+};
+
 // ----------------------------------------------------------------------------- kernel
 template <int DIM, int K, int Q, int NF, int EPB_>
 struct KCfg {
@@ -709,74 +749,89 @@ force_kernel(const Params P) {
     double *S2b = Wk + G::NF * DIM * 2 * G::S1;    // [NF*DIM][3][Q][Q][N]
     double *E1b = S2b + G::NF * DIM * 3 * G::S2;   // [Q][M][M]
     double *E2b = E1b + G::E1;                     // [Q][Q][M]
+    using CT = CTab<K, Q>;
     if (u < EPB) {
-      // stage 1: contract a1
-      constexpr int cnt1 = NF * DIM * 2 * Q * N * N;
-      for (int o = lt; o < cnt1; o += NQ) {
-        int r = o;
-        const int a3 = r % N; r /= N;
-        const int a2 = r % N; r /= N;
-        const int q1 = r % Q; r /= Q;
-        const int bg = r % 2;
-        const int fc = r / 2;
-        const double *tab = (bg ? sG : sB) + q1 * N;
+      // stage 1: contract a1.  One task per (field comp, a2, a3) line: its N dofs are loaded
+      // once and give all Q x {B, G} outputs (canonical FMA order per output, DESIGN A.2).
+      for (int t = lt; t < NF * DIM * N * N; t += NQ) {
+        const int a23 = t % (N * N), fc = t / (N * N);
+        const int a2 = a23 % N, a3 = a23 / N;
         const double *src = Xs + fc * ND + (a3 * N + a2) * N;
-        double acc = tab[0] * src[0];
+        double x[N];
 #pragma unroll
-        for (int a1 = 1; a1 < N; ++a1) acc = __fma_rn(tab[a1], src[a1], acc);
-        S1b[((fc * 2 + bg) * Q + q1) * N * N + a2 * N + a3] = acc;
+        for (int a1 = 0; a1 < N; ++a1) x[a1] = src[a1];
+        double *dB = S1b + ((fc * 2 + 0) * Q) * N * N + a2 * N + a3;
+        double *dG = S1b + ((fc * 2 + 1) * Q) * N * N + a2 * N + a3;
+#pragma unroll
+        for (int q1 = 0; q1 < Q; ++q1) {
+          double ab = CT::B(q1, 0) * x[0], ag = CT::G(q1, 0) * x[0];
+#pragma unroll
+          for (int a1 = 1; a1 < N; ++a1) {
+            ab = __fma_rn(CT::B(q1, a1), x[a1], ab);
+            ag = __fma_rn(CT::G(q1, a1), x[a1], ag);
+          }
+          dB[q1 * N * N] = ab;
+          dG[q1 * N * N] = ag;
+        }
       }
-      if (WANT_E) {
-        for (int o = lt; o < Q * M * M; o += NQ) {
-          int r = o;
-          const int j3 = r % M; r /= M;
-          const int j2 = r % M;
-          const int q1 = r / M;
-          const double *tab = sBl + q1 * M;
+      if (WANT_E) {  // (j2, j3) lines, on the highest lanes
+        for (int t = NQ - 1 - lt; t < M * M; t += NQ) {
+          const int j2 = t % M, j3 = t / M;
           const double *src = Es + (j3 * M + j2) * M;
-          double acc = tab[0] * src[0];
+          double ev[M];
 #pragma unroll
-          for (int j1 = 1; j1 < M; ++j1) acc = __fma_rn(tab[j1], src[j1], acc);
-          E1b[(q1 * M + j2) * M + j3] = acc;
+          for (int j1 = 0; j1 < M; ++j1) ev[j1] = src[j1];
+#pragma unroll
+          for (int q1 = 0; q1 < Q; ++q1) {
+            double acc = CT::Bl(q1, 0) * ev[0];
+#pragma unroll
+            for (int j1 = 1; j1 < M; ++j1) acc = __fma_rn(CT::Bl(q1, j1), ev[j1], acc);
+            E1b[(q1 * M + j2) * M + j3] = acc;
+          }
         }
       }
     }
     __syncthreads();
     if (u < EPB) {
-      // stage 2: contract a2 ; kind 0: B.UG (d/dxi1), 1: G.UB (d/dxi2), 2: B.UB (d/dxi3)
-      constexpr int cnt2 = NF * DIM * Q * Q * N;
-      for (int o = lt; o < cnt2; o += NQ) {
-        int r = o;
-        const int a3 = r % N; r /= N;
-        const int q2 = r % Q; r /= Q;
-        const int q1 = r % Q;
-        const int fc = r / Q;
-        const double *tB = sB + q2 * N, *tG = sG + q2 * N;
-        const double *uB = S1b + ((fc * 2 + 0) * Q + q1) * N * N + a3;
-        const double *uG = S1b + ((fc * 2 + 1) * Q + q1) * N * N + a3;
-        double d1 = tB[0] * uG[0], d2 = tG[0] * uB[0], d3 = tB[0] * uB[0];
+      // stage 2: contract a2 ; kind 0: B.UG (d/dxi1), 1: G.UB (d/dxi2), 2: B.UB (d/dxi3).
+      // One task per (field comp, q1, a3): its 2N stage-1 values give all Q x 3 outputs.
+      for (int t = lt; t < NF * DIM * Q * N; t += NQ) {
+        const int a3 = t % N, r = t / N;
+        const int q1 = r % Q, fc = r / Q;
+        const double *pB = S1b + ((fc * 2 + 0) * Q + q1) * N * N + a3;
+        const double *pG = S1b + ((fc * 2 + 1) * Q + q1) * N * N + a3;
+        double uB[N], uG[N];
 #pragma unroll
-        for (int a2 = 1; a2 < N; ++a2) {
-          d1 = __fma_rn(tB[a2], uG[a2 * N], d1);
-          d2 = __fma_rn(tG[a2], uB[a2 * N], d2);
-          d3 = __fma_rn(tB[a2], uB[a2 * N], d3);
+        for (int a2 = 0; a2 < N; ++a2) { uB[a2] = pB[a2 * N]; uG[a2] = pG[a2 * N]; }
+        double *dst = S2b + ((fc * 3) * Q + q1) * Q * N + a3;
+#pragma unroll
+        for (int q2 = 0; q2 < Q; ++q2) {
+          double d1 = CT::B(q2, 0) * uG[0], d2 = CT::G(q2, 0) * uB[0], d3 = CT::B(q2, 0) * uB[0];
+#pragma unroll
+          for (int a2 = 1; a2 < N; ++a2) {
+            d1 = __fma_rn(CT::B(q2, a2), uG[a2], d1);
+            d2 = __fma_rn(CT::G(q2, a2), uB[a2], d2);
+            d3 = __fma_rn(CT::B(q2, a2), uB[a2], d3);
+          }
+          dst[(0 * Q) * Q * N + q2 * N] = d1;
+          dst[(1 * Q) * Q * N + q2 * N] = d2;
+          dst[(2 * Q) * Q * N + q2 * N] = d3;
         }
-        S2b[((fc * 3 + 0) * Q + q1) * Q * N + q2 * N + a3] = d1;
-        S2b[((fc * 3 + 1) * Q + q1) * Q * N + q2 * N + a3] = d2;
-        S2b[((fc * 3 + 2) * Q + q1) * Q * N + q2 * N + a3] = d3;
       }
-      if (WANT_E) {
-        for (int o = lt; o < Q * Q * M; o += NQ) {
-          int r = o;
-          const int j3 = r % M; r /= M;
-          const int q2 = r % Q;
-          const int q1 = r / Q;
-          const double *tab = sBl + q2 * M;
+      if (WANT_E) {  // (q1, j3) lines, on the highest lanes
+        for (int t = NQ - 1 - lt; t < Q * M; t += NQ) {
+          const int j3 = t % M, q1 = t / M;
           const double *src = E1b + q1 * M * M + j3;
-          double acc = tab[0] * src[0];
+          double ev[M];
 #pragma unroll
-          for (int j2 = 1; j2 < M; ++j2) acc = __fma_rn(tab[j2], src[j2 * M], acc);
-          E2b[(q1 * Q + q2) * M + j3] = acc;
+          for (int j2 = 0; j2 < M; ++j2) ev[j2] = src[j2 * M];
+#pragma unroll
+          for (int q2 = 0; q2 < Q; ++q2) {
+            double acc = CT::Bl(q2, 0) * ev[0];
+#pragma unroll
+            for (int j2 = 1; j2 < M; ++j2) acc = __fma_rn(CT::Bl(q2, j2), ev[j2], acc);
+            E2b[(q1 * Q + q2) * M + j3] = acc;
+          }
         }
       }
     }
@@ -906,7 +961,7 @@ force_kernel(const Params P) {
   PointOut po;
   {
     ArithFast af;
-    pointwise<DIM, VISC, HAS_W, true>(af, J, Gv, Gw, eq, mq, gam, wq, ph, po);
+    pointwise<DIM, VISC, HAS_W, true, ArithFast, F3_COMPACT && DIM == 3 && K == 2>(af, J, Gv, Gw, eq, mq, gam, wq, ph, po);
     if (!af.ok) {
       // rare: some fast div/sqrt left its exact range; recompute the inputs from shared
       // memory (not kept live across the fast pass) and re-run with IEEE operators.
@@ -988,97 +1043,128 @@ force_kernel(const Params P) {
   __syncthreads();
   const int64_t slot_base = (int64_t)l * ND;
   if (DIM == 3) {
+    using CT = CTab<K, Q>;
     if (u < EPB) {
-      // b1: T[dl][c][q1][q2][a3] = sum_q3 (dl==2 ? G : B)[q3][a3] S[c][dl](q1,q2,q3)
-      for (int o = lt; o < DIM * DIM * Q * Q * N; o += NQ) {
-        int r = o;
-        const int a3 = r % N; r /= N;
-        const int q2 = r % Q; r /= Q;
-        const int q1 = r % Q; r /= Q;
-        const int c = r % DIM;
-        const int dl = r / DIM;
-        const double *tab = dl == 2 ? sG : sB;
-        const double *src = Ss + (c * DIM + dl) * NQ + q1 + Q * q2;
-        double acc = 0.0;
+      // b1: T[dl][c][q1][q2][a3] = sum_q3 (dl==2 ? G : B)[q3][a3] S[c][dl](q1,q2,q3); one task
+      // per (c, q1, q2) pencil: its 3Q stresses give all 3 x N outputs
+      for (int t = lt; t < DIM * Q * Q; t += NQ) {
+        const int q12 = t % (Q * Q), c = t / (Q * Q);
+        const int q1 = q12 % Q, q2 = q12 / Q;
 #pragma unroll
-        for (int q3 = 0; q3 < Q; ++q3) acc = __fma_rn(tab[q3 * N + a3], src[q3 * Q * Q], acc);
-        Tb[o] = acc;
+        for (int dl = 0; dl < 3; ++dl) {
+          const double *src = Ss + (c * DIM + dl) * NQ + q12;
+          double sv[Q];
+#pragma unroll
+          for (int q3 = 0; q3 < Q; ++q3) sv[q3] = src[q3 * Q * Q];
+          double *dst = Tb + (((dl * DIM + c) * Q + q1) * Q + q2) * N;
+#pragma unroll
+          for (int a3 = 0; a3 < N; ++a3) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q3 = 0; q3 < Q; ++q3)
+              acc = __fma_rn(dl == 2 ? CT::G(q3, a3) : CT::B(q3, a3), sv[q3], acc);
+            dst[a3] = acc;
+          }
+        }
       }
-      // f1[q1][q2][j3] = sum_q3 Bl[q3][j3] A(q1,q2,q3)
-      for (int o = lt; o < Q * Q * M; o += NQ) {
-        const int j3 = o % M, q2 = (o / M) % Q, q1 = o / (M * Q);
-        double acc = 0.0;
+      // f1[q1][q2][j3] = sum_q3 Bl[q3][j3] A(q1,q2,q3), (q1, q2) pencils on the highest lanes
+      for (int t = NQ - 1 - lt; t < Q * Q; t += NQ) {
+        double av[Q];
 #pragma unroll
-        for (int q3 = 0; q3 < Q; ++q3) acc = __fma_rn(sBl[q3 * M + j3], As[q1 + Q * q2 + Q * Q * q3], acc);
-        F1b[o] = acc;
+        for (int q3 = 0; q3 < Q; ++q3) av[q3] = As[t + Q * Q * q3];
+        const int q1 = t % Q, q2 = t / Q;
+#pragma unroll
+        for (int j3 = 0; j3 < M; ++j3) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q3 = 0; q3 < Q; ++q3) acc = __fma_rn(CT::Bl(q3, j3), av[q3], acc);
+          F1b[(q1 * Q + q2) * M + j3] = acc;
+        }
       }
     }
     __syncthreads();
     if (u < EPB) {
-      // b2: W1[c][q1][a2][a3] = sum_q2 B[q2][a2] T0 ; W23 = sum_q2 G[q2][a2] T1 + B[q2][a2] T2
-      for (int o = lt; o < 2 * DIM * Q * N * N; o += NQ) {
-        int r = o;
-        const int a3 = r % N; r /= N;
-        const int a2 = r % N; r /= N;
-        const int q1 = r % Q; r /= Q;
-        const int c = r % DIM;
-        const int which = r / DIM;
-        double acc = 0.0;
-        if (which == 0) {
-          const double *t0 = Tb + ((0 * DIM + c) * Q + q1) * Q * N + a3;
+      // b2: W1[c][q1][a2][a3] = sum_q2 B[q2][a2] T0 ; W23 = sum_q2 G[q2][a2] T1 + B[q2][a2] T2;
+      // one task per (c, q1, a3) pencil
+      for (int t = lt; t < DIM * Q * N; t += NQ) {
+        const int a3 = t % N, r = t / N;
+        const int q1 = r % Q, c = r / Q;
+        const double *t0 = Tb + ((0 * DIM + c) * Q + q1) * Q * N + a3;
+        const double *t1 = Tb + ((1 * DIM + c) * Q + q1) * Q * N + a3;
+        const double *t2 = Tb + ((2 * DIM + c) * Q + q1) * Q * N + a3;
+        double v0[Q], v1[Q], v2[Q];
 #pragma unroll
-          for (int q2 = 0; q2 < Q; ++q2) acc = __fma_rn(sB[q2 * N + a2], t0[q2 * N], acc);
-        } else {
-          const double *t1 = Tb + ((1 * DIM + c) * Q + q1) * Q * N + a3;
-          const double *t2 = Tb + ((2 * DIM + c) * Q + q1) * Q * N + a3;
+        for (int q2 = 0; q2 < Q; ++q2) { v0[q2] = t0[q2 * N]; v1[q2] = t1[q2 * N]; v2[q2] = t2[q2 * N]; }
+        double *w1 = Wb + ((0 * DIM + c) * Q + q1) * N * N + a3;
+        double *w23 = Wb + ((1 * DIM + c) * Q + q1) * N * N + a3;
+#pragma unroll
+        for (int a2 = 0; a2 < N; ++a2) {
+          double acc1 = 0.0, acc23 = 0.0;
 #pragma unroll
           for (int q2 = 0; q2 < Q; ++q2) {
-            acc = __fma_rn(sG[q2 * N + a2], t1[q2 * N], acc);
-            acc = __fma_rn(sB[q2 * N + a2], t2[q2 * N], acc);
+            acc1 = __fma_rn(CT::B(q2, a2), v0[q2], acc1);
+            acc23 = __fma_rn(CT::G(q2, a2), v1[q2], acc23);
+            acc23 = __fma_rn(CT::B(q2, a2), v2[q2], acc23);
           }
+          w1[a2 * N] = acc1;
+          w23[a2 * N] = acc23;
         }
-        Wb[o] = acc;
       }
-      // f2[q1][j2][j3] = sum_q2 Bl[q2][j2] f1[q1][q2][j3]
-      for (int o = lt; o < Q * M * M; o += NQ) {
-        const int j3 = o % M, j2 = (o / M) % M, q1 = o / (M * M);
-        double acc = 0.0;
+      // f2[q1][j2][j3] = sum_q2 Bl[q2][j2] f1[q1][q2][j3], (q1, j3) pencils on the highest lanes
+      for (int t = NQ - 1 - lt; t < Q * M; t += NQ) {
+        const int j3 = t % M, q1 = t / M;
+        double fv[Q];
 #pragma unroll
-        for (int q2 = 0; q2 < Q; ++q2) acc = __fma_rn(sBl[q2 * M + j2], F1b[(q1 * Q + q2) * M + j3], acc);
-        F2b[o] = acc;
+        for (int q2 = 0; q2 < Q; ++q2) fv[q2] = F1b[(q1 * Q + q2) * M + j3];
+#pragma unroll
+        for (int j2 = 0; j2 < M; ++j2) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q2 = 0; q2 < Q; ++q2) acc = __fma_rn(CT::Bl(q2, j2), fv[q2], acc);
+          F2b[(q1 * M + j2) * M + j3] = acc;
+        }
       }
     }
     __syncthreads();
     if (u < EPB && unit0 + u < P.n_units) {
-      // b3: F1[c][a] = sum_q1 G[q1][a1] W1[c][q1][a2][a3] + B[q1][a1] W23[c][q1][a2][a3]
-      for (int a = lt; a < ND; a += NQ) {
-        const int a1 = a % N, a23 = a / N;  // a23 = a2 + N a3
-        const int a2 = a23 % N, a3 = a23 / N;
-        double val[3];
+      // b3: F1[c][a] = sum_q1 G[q1][a1] W1[c][q1][a2][a3] + B[q1][a1] W23[c][q1][a2][a3];
+      // one task per (c, a2, a3) pencil writes the N nodes a1 = 0..N-1 of component c
+      for (int t = lt; t < DIM * N * N; t += NQ) {
+        const int a23 = t % (N * N), c = t / (N * N);
+        double w1v[Q], w23v[Q];
 #pragma unroll
-        for (int c = 0; c < DIM; ++c) {
+        for (int q1 = 0; q1 < Q; ++q1) {
+          w1v[q1] = Wb[((0 * DIM + c) * Q + q1) * N * N + a23];
+          w23v[q1] = Wb[((1 * DIM + c) * Q + q1) * N * N + a23];
+        }
+        const int a2 = a23 / N, a3 = a23 % N;  // Wb index a2 * N + a3
+        const int a0 = (a3 * N + a2) * N;      // node a = a1 + N a2 + N^2 a3
+#pragma unroll
+        for (int a1 = 0; a1 < N; ++a1) {
           double acc = 0.0;
 #pragma unroll
           for (int q1 = 0; q1 < Q; ++q1) {
-            acc = __fma_rn(sG[q1 * N + a1], Wb[((0 * DIM + c) * Q + q1) * N * N + a2 * N + a3], acc);
-            acc = __fma_rn(sB[q1 * N + a1], Wb[((1 * DIM + c) * Q + q1) * N * N + a2 * N + a3], acc);
+            acc = __fma_rn(CT::G(q1, a1), w1v[q1], acc);
+            acc = __fma_rn(CT::B(q1, a1), w23v[q1], acc);
           }
-          val[c] = acc;
-        }
-        const int s = P.slot[slot_base + a];
-        if (s >= 0) {
-#pragma unroll
-          for (int c = 0; c < DIM; ++c) P.evec[((int64_t)s * DIM + c) * B + b] = val[c];
+          const int s = P.slot[slot_base + a0 + a1];
+          if (s >= 0) P.evec[((int64_t)s * DIM + c) * B + b] = acc;
         }
       }
       const int row = P.ftw_row ? P.ftw_row[l] : l;
-      if (row >= 0) {
-        for (int o = lt; o < NE; o += NQ) {
-          const int j1 = o % M, j2 = (o / M) % M, j3 = o / (M * M);
-          double acc = 0.0;
+      if (row >= 0) {  // (j2, j3) pencils on the highest lanes
+        for (int t = NQ - 1 - lt; t < M * M; t += NQ) {
+          const int j2 = t % M, j3 = t / M;
+          double fv[Q];
 #pragma unroll
-          for (int q1 = 0; q1 < Q; ++q1) acc = __fma_rn(sBl[q1 * M + j1], F2b[(q1 * M + j2) * M + j3], acc);
-          P.FTw[((int64_t)row * NE + o) * B + b] = acc;
+          for (int q1 = 0; q1 < Q; ++q1) fv[q1] = F2b[(q1 * M + j2) * M + j3];
+#pragma unroll
+          for (int j1 = 0; j1 < M; ++j1) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q1 = 0; q1 < Q; ++q1) acc = __fma_rn(CT::Bl(q1, j1), fv[q1], acc);
+            P.FTw[((int64_t)row * NE + (j3 * M + j2) * M + j1) * B + b] = acc;
+          }
         }
       }
     }

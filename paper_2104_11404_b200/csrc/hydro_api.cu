@@ -138,10 +138,12 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
   const int64_t grid = ((int64_t)P.n_units + G::EPB - 1) / G::EPB;
   if (grid <= 0) return HYDRO_OK;
   constexpr bool SPEC2D = DIM == 2 && K == 2 && Q == 4 && MODE != hk::MODE_MQ && MODE != hk::MODE_FTW;
-  // the persistent 3D kernel wins for Q2 (C2, C4); for Q3 (224-thread CTAs) its 80-register
-  // budget spills and barrier waits grow, so Q3 keeps the one-element-per-CTA kernel
+  // 3D: the one-element-per-CTA kernel with register-blocked contraction stages (tables as
+  // constant-bank operands) beats the persistent cp.async kernel since r01 v22 (C2 2.57 vs
+  // 2.80 ms, C4 69.2 vs 77.8 ms: profiles/ab/r01_ab23_*); force3d stays selectable with
+  // HYDRO_3D_KERNEL=persistent (and is covered by the kernel-path tests)
   constexpr bool SPEC3D_OK = DIM == 3 && MODE != hk::MODE_MQ && MODE != hk::MODE_FTW;
-  bool use3d = SPEC3D_OK && K == 2;  // (HYDRO_3D_KERNEL=persistent|element overrides)
+  bool use3d = false;
   if (SPEC3D_OK) {
     const char *env = getenv("HYDRO_3D_KERNEL");
     if (env && !strcmp(env, "persistent")) use3d = true;
@@ -424,9 +426,16 @@ hydro_status hydro_ctx_create(const hydro_mesh_desc *desc, void *workspace, size
   std::vector<double> packed;
   pack_tables(T, packed);
   if (desc->order_h1 == 2 && desc->nq1d == 4) {
-    // __constant__ copy for the one-thread-per-element 2D kernel (same packed order)
+    // __constant__ copy for the one-thread-per-element 2D kernel and the blocked 3D stages
     static_assert(sizeof(hk::Tab24) == sizeof(double) * (4 + 12 + 12 + 8), "Tab24 layout");
     if (cudaMemcpyToSymbolAsync(hk::c_t24, packed.data(), sizeof(hk::Tab24), 0,
+                                cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return fail(HYDRO_ERR_CUDA);
+  }
+  if (desc->order_h1 == 3 && desc->nq1d == 6) {
+    // __constant__ copy for the register-blocked 3D stages of force_kernel (Q3/Q2)
+    static_assert(sizeof(hk::Tab36) == sizeof(double) * (6 + 24 + 24 + 18), "Tab36 layout");
+    if (cudaMemcpyToSymbolAsync(hk::c_t36, packed.data(), sizeof(hk::Tab36), 0,
                                 cudaMemcpyHostToDevice, s) != cudaSuccess)
       return fail(HYDRO_ERR_CUDA);
   }

@@ -33,6 +33,14 @@ def kernel2d(request, monkeypatch):
     return request.param
 
 
+@pytest.fixture(params=["element", "persistent"])
+def kernel3d(request, monkeypatch):
+    """3D: the one-element-per-CTA kernel with blocked stages (default) and the persistent
+    cp.async kernel (force3d, Q2 only; Q3 falls back to the element kernel's code)."""
+    monkeypatch.setenv("HYDRO_3D_KERNEL", request.param)
+    return request.param
+
+
 def check(prob, oracle_lib, w=None, ctx=None, what=""):
     if w is not None:
         prob.w = w
@@ -114,16 +122,46 @@ def test_2d_ragged_counts(oracle_lib, monkeypatch, shape):
 
 
 @pytest.mark.parametrize("shape", [(5, 1, 1), (13, 11, 11)])
-def test_3d_ragged_counts(oracle_lib, shape):
+def test_3d_ragged_counts(oracle_lib, kernel3d, shape):
     """Small 3D element counts (fewer elements than persistent CTAs; and several
     elements per CTA with a ragged last round)."""
     n = shape
     prob = W.sedov_like(9, 3, n, (0.0,) * 3, tuple(0.01875 * s for s in n), delta=0.05,
                         e_floor=1e-6, vmode="radial", vscale=0.5, name="ragged3d")
-    check(prob, oracle_lib, what=f"3D {shape}")
+    check(prob, oracle_lib, what=f"3D {shape} {kernel3d}")
 
 
-def test_3d_inviscid(oracle_lib):
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_3d_paths_match_oracle(oracle_lib, kernel3d, name):
+    check(W.small(name), oracle_lib, what=f"{name}/{kernel3d}")
+
+
+def test_3d_paths_bitwise_identical(monkeypatch):
+    """Both 3D Q2 kernels evaluate the same contract and the same backward FMA order."""
+    prob = W.small("c2")
+    monkeypatch.setenv("HYDRO_3D_KERNEL", "element")
+    a = H.run_full(prob)
+    monkeypatch.setenv("HYDRO_3D_KERNEL", "persistent")
+    b = H.run_full(prob)
+    assert np.array_equal(a["F1"], b["F1"]) and np.array_equal(a["FTw"], b["FTw"])
+    assert H.dt_bitwise(a["dt"], b["dt"])
+
+
+def test_3d_batched_sampled_matches_oracle(oracle_lib, kernel3d):
+    """hydro_force_sampled on a C2-shaped mesh with B = 3 instances, both 3D kernels."""
+    from tests.test_gpu_rom import gpu_step, oracle_instance
+    base = W.small("c2")
+    batch = W.rom_batch(base, B=3, n_sample=4, n_red=8)
+    g = gpu_step(batch)
+    assert g["status"][0] == 0
+    for b in range(batch.B):
+        F1, F1m, FT, FTm, dt = oracle_instance(oracle_lib, batch, g["xS"], g["vS"], g["eS"], b)
+        H.assert_close(g["F1"][:, b], F1, F1m, H.TOL_LOCAL, f"F1_rows b={b}")
+        H.assert_close(g["FT"][:, b], FT, FTm, H.TOL_LOCAL, f"FTw_rows b={b}")
+        assert H.dt_bitwise(g["dt"][b], dt)
+
+
+def test_3d_inviscid(oracle_lib, kernel3d):
     prob = W.small("c2")
     prob.visc = False
-    check(prob, oracle_lib, what="3D inviscid")
+    check(prob, oracle_lib, what=f"3D inviscid {kernel3d}")
