@@ -606,6 +606,10 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
 #ifndef F3_COMPACT
 #define F3_COMPACT 0
 #endif
+// CTAs per SM targeted for the 224-thread (3D Q3) generic kernel (registers: 4 -> 72)
+#ifndef GEN_MINB224
+#define GEN_MINB224 4
+#endif
 
 // ----------------------------------------------------------------------------- tables
 // The 1D tables in __constant__ memory (filled at context creation, packed order w, B, G, Bl):
@@ -647,7 +651,7 @@ struct KCfg {
   // occupancy target.  3D Q3 (224-thread CTAs): 4 CTAs/SM at 72 registers measured best
   // (10.75 ms on C3 vs 12.0 ms at 3 CTAs / 80 registers, 11.2 ms at 5 CTAs / 56 registers:
   // occupancy outweighs the extra spills; profiles/ab/).
-  static constexpr int MINB = G::NT >= 224 ? 4 : (G::NT >= 128 ? 5 : 10);
+  static constexpr int MINB = G::NT >= 224 ? GEN_MINB224 : (G::NT >= 128 ? 5 : 10);
 };
 
 template <int MODE, bool HAS_W>
