@@ -158,8 +158,11 @@ hydro_status hydro_force_sampled(hydro_sample *s, const double *x_S, const doubl
                                  const double *e_S, const double *w_S, const double *gamma,
                                  hydro_visc visc, hydro_cfl cfl, double *F1_rows,
                                  double *FTw_rows, double *dt, hydro_stream_t stream);
-/* The sampled two-pass form (see hydro_force_full_store): S [n_closure_elem*B][dim*dim][q^dim]
- * of hydro_sample_stress_bytes(plan) bytes; w_S: closure H1 rows [dim*n_cl_nodes][B].          */
+/* The sampled two-pass form (see hydro_force_full_store).  F^T w is needed only at the L2
+ * rows of the S0 elements, so only their point stresses are kept: S [s_e/k^dim rows * B]
+ * [dim*dim][q^dim] (S0 row r, instance b at r*B + b) of hydro_sample_stress_bytes(plan)
+ * bytes, and the transposed pass runs over those S0 units only.  w_S: closure H1 rows
+ * [dim*n_cl_nodes][B].                                                                         */
 size_t hydro_sample_stress_bytes(const hydro_sample *s);
 hydro_status hydro_force_sampled_store(hydro_sample *s, const double *x_S, const double *v_S,
                                        const double *e_S, const double *gamma, hydro_visc visc,

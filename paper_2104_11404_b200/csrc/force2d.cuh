@@ -211,7 +211,11 @@ __global__ void __maxnreg__(128) force2d_kernel(const Params P) {
   const PhysIn ph{P.q1, P.q2, P.alpha, P.alpha_mu};
   unsigned long long kmin = ~0ull;
   bool tangled = false, nan = false;
-  double *Sst = (MODE == MODE_FORCE && P.S_store && valid) ? P.S_store + (int64_t)g * 4 * NQ : nullptr;
+  double *Sst = nullptr;
+  if (MODE == MODE_FORCE && P.S_store && valid) {
+    const int64_t si = s_index(P, g, l, b);
+    if (si >= 0) Sst = P.S_store + si * 4 * NQ;
+  }
   double mq0 = __ldg(P.mq + (int64_t)gid * NQ);  // m_q(0, 0); then prefetched point by point
 
 #pragma unroll 1

@@ -282,10 +282,13 @@ force3d_kernel(const Params P) {
     // ---- S6 dt: flags; key min per thread (full) or per unit (batched)
     const bool pt = lt < NQ;
     if (MODE == MODE_FORCE && P.S_store && pt) {
+      const int64_t si = s_index(P, u, l, b);
+      if (si >= 0) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
+        for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) P.S_store[((int64_t)u * 9 + c * 3 + d) * NQ + lt] = po.S[c][d];
+          for (int d = 0; d < 3; ++d) P.S_store[(si * 9 + c * 3 + d) * NQ + lt] = po.S[c][d];
+      }
     }
     if (pt) {
       if (!(po.det > 0.0)) atomicMin(&P.st[b].first_bad, (unsigned long long)sc.gid);

@@ -92,7 +92,17 @@ struct Params {
   // stored point stresses S_q = w_q detJ sigma J^-T (optional): [unit][DIM*DIM][NQ]
   double *S_store;          // written by MODE_FORCE when non-NULL
   const double *S_load;     // read by MODE_FTW
+  // S index of unit (l, b): sampled mode (ftw_row != NULL) keeps only the S0 elements,
+  // compacted to ftw_row[l] * B + b (-1: not stored); full mode: the unit index itself.
+  // MODE_FTW over compacted units: unit_elem[row] = the closure element of S0 row `row`.
+  const int32_t *unit_elem;
 };
+
+__device__ __forceinline__ int64_t s_index(const Params &P, int unit, int l, int b) {
+  if (!P.ftw_row) return unit;
+  const int row = __ldg(P.ftw_row + l);
+  return row < 0 ? -1 : (int64_t)row * P.B + b;
+}
 
 // ----------------------------------------------------------------------------- helpers
 __device__ __forceinline__ unsigned long long dt_key(double d) {
@@ -692,7 +702,10 @@ force_kernel(const Params P) {
     const int uu = i % EPB, a = i / EPB;
     const int gu = unit0 + uu;
     int nd = 0;
-    if (gu < P.n_units) nd = P.elem_nodes[(BATCHED ? gu / B : gu) * ND + a];
+    if (gu < P.n_units) {
+      const int lr = BATCHED ? gu / B : gu;
+      nd = P.elem_nodes[(P.unit_elem ? P.unit_elem[lr] : lr) * ND + a];
+    }
     snode[uu * ND + a] = nd;
   }
   __syncthreads();
@@ -736,7 +749,8 @@ force_kernel(const Params P) {
   double *Es = U + G::NF * DIM * ND;      // [NE]
   double *Wk = Es + NE;                   // work region
   const int gu = (unit0 + uc < P.n_units) ? unit0 + uc : 0;  // safe unit for reads
-  const int l = BATCHED ? gu / B : gu;
+  const int lraw = BATCHED ? gu / B : gu;  // element (or, over compacted units, S0 row)
+  const int l = P.unit_elem ? P.unit_elem[lraw] : lraw;
   const int b = BATCHED ? gu % B : 0;
   const int gid = P.elem_gid ? P.elem_gid[l] : l;
 
@@ -891,7 +905,8 @@ force_kernel(const Params P) {
       As[lt] = A;
     }
     __syncthreads();
-    const int row = (u < EPB && unit0 + u < P.n_units) ? (P.ftw_row ? P.ftw_row[l] : l) : -1;
+    const int row = (u < EPB && unit0 + u < P.n_units)
+                        ? (P.unit_elem ? lraw : (P.ftw_row ? P.ftw_row[l] : l)) : -1;
     if (DIM == 3) {
       if (u < EPB)
         for (int o = lt; o < Q * Q * M; o += NQ) {
@@ -983,11 +998,14 @@ force_kernel(const Params P) {
   }
 
   if (MODE == MODE_FORCE && P.S_store && active) {
+    const int64_t si = s_index(P, unit0 + u, l, b);
+    if (si >= 0) {
 #pragma unroll
-    for (int c = 0; c < DIM; ++c)
+      for (int c = 0; c < DIM; ++c)
 #pragma unroll
-      for (int d = 0; d < DIM; ++d)
-        P.S_store[((int64_t)(unit0 + u) * DIM * DIM + c * DIM + d) * NQ + lt] = po.S[c][d];
+        for (int d = 0; d < DIM; ++d)
+          P.S_store[(si * DIM * DIM + c * DIM + d) * NQ + lt] = po.S[c][d];
+    }
   }
 
   // --- S6 dt: status flags, then min of order-preserving keys

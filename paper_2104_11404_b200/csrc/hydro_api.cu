@@ -103,6 +103,7 @@ struct hydro_sample {
   std::vector<int64_t> h_cl_nodes, h_s0_nodes;
   int32_t *elem_nodes = nullptr, *elem_gid = nullptr, *slot = nullptr, *off = nullptr,
           *ftw_row = nullptr, *anode = nullptr;
+  int32_t *s0_elem = nullptr;  // [n_s0] closure-local element of each S0 row (inverse of ftw_row)
   unsigned *cnt = nullptr;  // [n_s0_nodes][B] arrival counters, then the done counter
   double *evec = nullptr;
   hydro_devstatus *st = nullptr;
@@ -668,6 +669,9 @@ hydro_status hydro_sample_create(hydro_ctx *c, const int32_t *sample_elems, int6
       }
   }
   (void)ne;
+  std::vector<int32_t> s0el((size_t)(p->n_s0 > 0 ? p->n_s0 : 1), 0);
+  for (int64_t l = 0; l < p->n_cl; ++l)
+    if (frow[(size_t)l] >= 0) s0el[(size_t)frow[(size_t)l]] = (int32_t)l;
   auto fail = [&](hydro_status st) { hydro_sample_destroy(p); return st; };
   const size_t evec_bytes = sizeof(double) * (size_t)p->n_slots * c->d.dim * B;
   if (cudaMalloc(&p->elem_nodes, sizeof(int32_t) * len.size()) != cudaSuccess ||
@@ -678,6 +682,7 @@ hydro_status hydro_sample_create(hydro_ctx *c, const int32_t *sample_elems, int6
       cudaMalloc(&p->evec, evec_bytes > 0 ? evec_bytes : 8) != cudaSuccess ||
       cudaMalloc(&p->st, sizeof(hydro_devstatus) * B) != cudaSuccess ||
       cudaMalloc(&p->anode, sizeof(int32_t) * anode.size()) != cudaSuccess ||
+      cudaMalloc(&p->s0_elem, sizeof(int32_t) * s0el.size()) != cudaSuccess ||
       cudaMalloc(&p->cnt, sizeof(uint32_t) * (size_t)(p->n_s0_nodes * B + 1)) != cudaSuccess ||
       cudaMemset(p->cnt, 0, sizeof(uint32_t) * (size_t)(p->n_s0_nodes * B + 1)) != cudaSuccess)
     return fail(HYDRO_ERR_CUDA);
@@ -689,6 +694,7 @@ hydro_status hydro_sample_create(hydro_ctx *c, const int32_t *sample_elems, int6
       cudaMemcpy(p->slot, slot.data(), sizeof(int32_t) * slot.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(p->off, off.data(), sizeof(int32_t) * off.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(p->anode, anode.data(), sizeof(int32_t) * anode.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->s0_elem, s0el.data(), sizeof(int32_t) * s0el.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(p->st, hst.data(), sizeof(hydro_devstatus) * B, cudaMemcpyHostToDevice) != cudaSuccess)
     return fail(HYDRO_ERR_CUDA);
   *out = p;
@@ -699,6 +705,7 @@ hydro_status hydro_sample_destroy(hydro_sample *p) {
   if (!p) return HYDRO_OK;
   cudaFree(p->elem_nodes); cudaFree(p->elem_gid); cudaFree(p->ftw_row); cudaFree(p->slot);
   cudaFree(p->off); cudaFree(p->evec); cudaFree(p->st); cudaFree(p->anode); cudaFree(p->cnt);
+  cudaFree(p->s0_elem);
   delete p;
   return HYDRO_OK;
 }
@@ -774,7 +781,8 @@ hydro_status hydro_force_sampled(hydro_sample *p, const double *x_S, const doubl
 size_t hydro_sample_stress_bytes(const hydro_sample *p) {
   if (!p) return 0;
   const hydro_ctx *c = p->ctx;
-  return sizeof(double) * (size_t)p->n_cl * p->B * c->d.dim * c->d.dim * c->nq;
+  // only the S0 elements' point stresses are kept: F^T w is needed at their L2 rows only
+  return sizeof(double) * (size_t)(p->n_s0 > 0 ? p->n_s0 : 1) * p->B * c->d.dim * c->d.dim * c->nq;
 }
 
 hydro_status hydro_force_sampled_store(hydro_sample *p, const double *x_S, const double *v_S,
@@ -792,14 +800,15 @@ hydro_status hydro_sample_force_transpose(hydro_sample *p, const double *S, cons
   if (p->n_cl * (int64_t)p->B >= ((int64_t)1 << 31)) return HYDRO_ERR_ARG;
   hk::Params P;
   std::memset(&P, 0, sizeof(P));
-  P.n_units = (int32_t)(p->n_cl * p->B);
+  if (p->n_s0 == 0) return HYDRO_OK;
+  P.n_units = (int32_t)(p->n_s0 * p->B);  // units: (S0 row, instance)
   P.B = p->B;
   P.ld_nodes = p->n_cl_nodes;
   P.elem_nodes = p->elem_nodes;
   P.elem_gid = p->elem_gid;
+  P.unit_elem = p->s0_elem;
   P.x = w_S;
   P.FTw = FTw_rows;
-  P.ftw_row = p->ftw_row;
   P.S_load = S;
   fill_tables_ptrs(P, c);
   return launch_force(c->d.dim, c->d.order_h1, hk::MODE_FTW, false, p->B > 1, false, P,
