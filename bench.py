@@ -31,7 +31,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "force-eval quad-points/sec (F·1 + F^T·v) at 1 B200"
+METRIC = "force-eval quad-points/sec (F·1 + F^T·v) at 1 B200; % of FP64/HBM roofline"  # BASELINE.json
 UNIT = "quad-points/s"
 
 
