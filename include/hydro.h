@@ -215,6 +215,9 @@ hydro_status hydro_mass_e_solve(hydro_fom *fom, const double *rhs, double *sol,
 /* Kinetic 1/2 v^T M_V v and internal 1^T M_E e energies (host outputs).  Synchronises.     */
 hydro_status hydro_fom_energy(hydro_fom *fom, const double *v, const double *e,
                               double *kinetic, double *internal, hydro_stream_t stream);
+/* The time-step controller of PAPER P:549-566 (defaults beta1 = 0.85, beta2 = 1.02,
+ * gamma = 0.8).                                                                             */
+typedef struct { double beta1, beta2, gamma; } hydro_dt_ctrl;
 /* One RK2-average step of size dt, in place on the device state (x, v, e); four force
  * evaluations (F.1 and F^T w of each stage), two CG solves.  *dt_est (host) = the min of
  * the two stages' time-step estimates for the caller's controller;
@@ -224,6 +227,18 @@ hydro_status hydro_rk2avg_step(hydro_fom *fom, double *x, double *v, double *e,
                                const double *gamma, hydro_visc visc, hydro_cfl cfl, double dt,
                                double cg_tol, int cg_max_iter, double *dt_est /* host */,
                                int *cg_iters /* host */, hydro_stream_t stream);
+/* Advance (x, v, e) in place from t0 to t_final with hydro_rk2avg_step under the controller
+ * of P:549-566: a step with dt >= its estimate is undone (state restored from an internal
+ * copy) and retried with beta1*dt; after an accepted step dt <- beta2*dt when
+ * dt <= gamma*estimate; the step reaching t_final is shortened to land on it.  *dt (host,
+ * in/out): the first trial step, returned as the controller's next step.  At most max_steps
+ * accepted steps; *t_out (host) = the time reached, *steps / *rejected (host) = accepted and
+ * rejected steps.  HYDRO_ERR_NONFINITE on a NaN estimate.  Synchronises `stream`.             */
+hydro_status hydro_fom_advance(hydro_fom *fom, double *x, double *v, double *e,
+                               const double *gamma, hydro_visc visc, hydro_cfl cfl,
+                               hydro_dt_ctrl ctrl, double t0, double t_final, double *dt,
+                               int max_steps, double cg_tol, int cg_max_iter, double *t_out,
+                               int *steps, int *rejected, hydro_stream_t stream);
 
 /* ------------------------------------------------------------------ ROM online step (NEXT-2) */
 /* The hyper-reduced RK2-average step of PAPER Eq. RK2-avg-rom-hr for the B

@@ -140,3 +140,35 @@ def rk2avg_step(fom: Fom, prob, x, v, e, dt: float):
     e1 = e + dt * fom.solve_e(s2w["FTw"])
     x1 = x + dt * vbar
     return x1, v1, e1, min(s1["dt"], s2["dt"])
+
+
+def advance(fom: Fom, prob, x, v, e, t0: float, t_final: float, dt: float, beta1=0.85,
+            beta2=1.02, gamma=0.8, max_steps=10**6, step=None):
+    """Time loop t0 -> t_final under the time-step controller of PAPER P:549-566:
+
+      1. with dt and the state U^n, evaluate U^{n+1} and the estimate dt_est;
+      2. if dt >= dt_est: dt <- beta1 dt and go to 1 (from U^n);
+      3. if dt <= gamma dt_est: dt <- beta2 dt;
+      4. accept, n <- n + 1.
+
+    The step that reaches t_final is shortened to land on it (reading: the paper runs to a
+    final time t_f).  `step(x, v, e, dt) -> (x1, v1, e1, dt_est)` defaults to
+    rk2avg_step on (fom, prob).  Returns (x, v, e, t, next_dt, accepted, rejected)."""
+    if step is None:
+        def step(x_, v_, e_, h_):
+            return rk2avg_step(fom, prob, x_, v_, e_, h_)
+    t, h, ns, nr = t0, dt, 0, 0
+    while t < t_final and ns < max_steps:
+        h_try = t_final - t if t_final - t < h else h
+        x1, v1, e1, est = step(x, v, e, h_try)
+        if np.isnan(est):
+            raise FloatingPointError("NaN time-step estimate")
+        if h_try >= est:
+            h = beta1 * h_try
+            nr += 1
+            continue
+        x, v, e = x1, v1, e1
+        t = t_final if h_try == t_final - t else t + h_try
+        ns += 1
+        h = beta2 * h_try if h_try <= gamma * est else h_try
+    return x, v, e, t, h, ns, nr

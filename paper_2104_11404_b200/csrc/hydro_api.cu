@@ -880,6 +880,7 @@ struct hydro_fom {
   double *F1 = nullptr, *F1x = nullptr, *FTw = nullptr, *FTx = nullptr, *dv = nullptr;
   double *vh = nullptr, *eh = nullptr, *xh = nullptr, *v1 = nullptr, *vbar = nullptr,
          *dts = nullptr, *S = nullptr;
+  double *xb = nullptr, *vb = nullptr, *eb = nullptr;  // state backup of the step controller
   bool have_dv = false;  // dv holds the previous solve's solution (warm start of the step's CG)
   std::vector<void *> allocs;
 };
@@ -1099,6 +1100,7 @@ hydro_status hydro_fom_create(hydro_ctx *c, const int64_t *bc_dofs, int64_t n_bc
       !alloc(&f->F1, n) || !alloc(&f->F1x, n) || !alloc(&f->FTw, nE) || !alloc(&f->FTx, nE) ||
       !alloc(&f->dv, n) || !alloc(&f->vh, n) || !alloc(&f->eh, nE) || !alloc(&f->xh, n) ||
       !alloc(&f->v1, n) || !alloc(&f->vbar, n) || !alloc(&f->dts, 2) ||
+      !alloc(&f->xb, n) || !alloc(&f->vb, n) || !alloc(&f->eb, nE) ||
       !alloc(&f->S, hydro_force_stress_bytes(c) / sizeof(double)))
     return fail(HYDRO_ERR_CUDA);
   if (cudaMemcpyAsync(f->mask, mask.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
@@ -1229,6 +1231,53 @@ hydro_status hydro_rk2avg_step(hydro_fom *f, double *x, double *v, double *e, co
   return HYDRO_OK;
 }
 
+
+hydro_status hydro_fom_advance(hydro_fom *f, double *x, double *v, double *e, const double *gamma,
+                               hydro_visc visc, hydro_cfl cfl, hydro_dt_ctrl ctrl, double t0,
+                               double t_final, double *dt, int max_steps, double cg_tol,
+                               int cg_max_iter, double *t_out, int *steps, int *rejected,
+                               hydro_stream_t stream) {
+  if (!f || !x || !v || !e || !gamma || !dt || !(*dt > 0.0) || !(t_final >= t0) || max_steps < 0 ||
+      !(ctrl.beta1 > 0.0 && ctrl.beta1 < 1.0) || !(ctrl.beta2 >= 1.0) || !(ctrl.gamma > 0.0))
+    return HYDRO_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = f->n, nE = f->c->d.n_elem * f->c->ne;
+  double t = t0, h = *dt;
+  int ns = 0, nr = 0;
+  hydro_status st = HYDRO_OK;
+  // (1) advance with dt, get the estimate; (2) dt >= estimate: dt <- beta1 dt,
+  // redo the step from the saved state; (3) dt <= gamma * estimate: dt <- beta2 dt; (4) next.
+  // The step that reaches t_final is shortened to land on it.
+  while (t < t_final && ns < max_steps) {
+    const double h_try = (t_final - t < h) ? t_final - t : h;
+    CUDA_OK(cudaMemcpyAsync(f->xb, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(f->vb, v, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(f->eb, e, sizeof(double) * nE, cudaMemcpyDeviceToDevice, s));
+    double est = 0.0;
+    if ((st = hydro_rk2avg_step(f, x, v, e, gamma, visc, cfl, h_try, cg_tol, cg_max_iter, &est,
+                                nullptr, stream)) != HYDRO_OK)
+      break;
+    if (!(est == est)) { st = HYDRO_ERR_NONFINITE; break; }
+    if (h_try >= est) {  // rejected: restore and retry with a smaller step
+      CUDA_OK(cudaMemcpyAsync(x, f->xb, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+      CUDA_OK(cudaMemcpyAsync(v, f->vb, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+      CUDA_OK(cudaMemcpyAsync(e, f->eb, sizeof(double) * nE, cudaMemcpyDeviceToDevice, s));
+      h = ctrl.beta1 * h_try;
+      ++nr;
+      if (nr > 1000000) { st = HYDRO_ERR_NONFINITE; break; }
+      continue;
+    }
+    t = (h_try == t_final - t) ? t_final : t + h_try;
+    ++ns;
+    h = (h_try <= ctrl.gamma * est) ? ctrl.beta2 * h_try : h_try;
+  }
+  CUDA_OK(cudaStreamSynchronize(s));
+  *dt = h;
+  if (t_out) *t_out = t;
+  if (steps) *steps = ns;
+  if (rejected) *rejected = nr;
+  return st;
+}
 
 // ------------------------------------------------------------------------------ ROM step
 }  // extern "C"

@@ -32,7 +32,7 @@ EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy"
             "hydro_profile_enable", "hydro_profile_read", "hydro_profile_read_captured",
             "hydro_profile_release_captured", "hydro_selftest_ieee_fast",
             "hydro_fom_create", "hydro_fom_destroy", "hydro_mass_v_apply", "hydro_mass_v_solve",
-            "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_rom_create",
+            "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_fom_advance", "hydro_rom_create",
             "hydro_rom_destroy", "hydro_rom_rk2avg_step", "hydro_force_stress_bytes",
             "hydro_force_full_store", "hydro_force_transpose", "hydro_sample_stress_bytes",
             "hydro_force_sampled_store", "hydro_sample_force_transpose"]
@@ -58,6 +58,10 @@ class _Visc(ctypes.Structure):
 
 class _Cfl(ctypes.Structure):
     _fields_ = [("alpha", ctypes.c_double), ("alpha_mu", ctypes.c_double)]
+
+
+class _DtCtrl(ctypes.Structure):
+    _fields_ = [("beta1", ctypes.c_double), ("beta2", ctypes.c_double), ("gamma", ctypes.c_double)]
 
 
 _lib = None
@@ -96,6 +100,9 @@ def lib() -> ctypes.CDLL:
         L.hydro_fom_energy.argtypes = [vp, vp, vp, ctypes.POINTER(dbl), ctypes.POINTER(dbl), vp]
         L.hydro_rk2avg_step.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, dbl, dbl, i32,
                                         ctypes.POINTER(dbl), ctypes.POINTER(i32), vp]
+        L.hydro_fom_advance.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, _DtCtrl, dbl, dbl,
+                                        ctypes.POINTER(dbl), i32, dbl, i32, ctypes.POINTER(dbl),
+                                        ctypes.POINTER(i32), ctypes.POINTER(i32), vp]
         L.hydro_rom_create.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp,
                                        vp, ctypes.POINTER(vp)]
         L.hydro_rom_destroy.argtypes = [vp]
@@ -161,6 +168,17 @@ class Cfl:
 
     def c(self):
         return _Cfl(self.alpha, self.alpha_mu)
+
+
+@dataclass
+class DtCtrl:
+    """Time-step controller constants (PAPER P:549-566 defaults)."""
+    beta1: float = 0.85
+    beta2: float = 1.02
+    gamma: float = 0.8
+
+    def c(self):
+        return _DtCtrl(self.beta1, self.beta2, self.gamma)
 
 
 def basis_tables(k: int, q: int) -> dict:
@@ -445,6 +463,19 @@ class Fom:
                                        dt, cg_tol, cg_max_iter, ctypes.byref(d), ctypes.byref(it),
                                        _stream(stream)), "hydro_rk2avg_step")
         return d.value, it.value
+
+    def advance(self, x, v, e, gamma, visc: Visc, cfl: Cfl, t0: float, t_final: float, dt: float,
+                ctrl: DtCtrl = DtCtrl(), max_steps=1000000, cg_tol=1e-12, cg_max_iter=500,
+                stream=None):
+        """In-place time loop t0 -> t_final under the controller of P:549-566.
+        Returns (t_reached, next_dt, accepted_steps, rejected_steps)."""
+        h, t = ctypes.c_double(dt), ctypes.c_double(0.0)
+        ns, nr = ctypes.c_int(0), ctypes.c_int(0)
+        _check(lib().hydro_fom_advance(self._h, _ptr(x), _ptr(v), _ptr(e), _ptr(gamma), visc.c(),
+                                       cfl.c(), ctrl.c(), t0, t_final, ctypes.byref(h), max_steps,
+                                       cg_tol, cg_max_iter, ctypes.byref(t), ctypes.byref(ns),
+                                       ctypes.byref(nr), _stream(stream)), "hydro_fom_advance")
+        return t.value, h.value, ns.value, nr.value
 
 
 class RomStepper:

@@ -119,3 +119,41 @@ def test_P20_solve_manufactured():
     rhs = np.stack([F.M @ u[c] for c in range(2)])
     got = F.solve_v(rhs)
     assert np.abs(got - u).max() <= 1e-12 * np.abs(u).max()
+
+
+def test_P23_dt_controller_worked_example():
+    """The controller of PAPER P:549-566 (beta1 = 0.85, beta2 = 1.02, gamma = 0.8) on a step
+    whose estimate is a constant 1.0, from dt = 2.0 over [0, 3]: the trace worked by hand
+    from the algorithm's four steps -- rejections 2.0, 1.7, 1.445, 1.22825, 1.0440125
+    (each >= 1.0), then 0.887410625 accepted three times (not <= 0.8, so no growth), then
+    the shortened last step 3 - 3 * 0.887410625 = 0.337768125 lands on t = 3 and, being
+    <= 0.8 * 1.0, grows the next step to 1.02 * 0.337768125."""
+    fom = _fom()
+    calls = []
+
+    def step(x, v, e, h):
+        calls.append(h)
+        return x, v, e, 1.0
+    x, v, e, t, h, ns, nr = fom.advance(None, None, 0, 0, 0, 0.0, 3.0, 2.0, step=step)
+    assert (ns, nr) == (4, 5)
+    assert t == 3.0
+    want = [2.0, 1.7, 1.445, 1.22825, 1.0440125, 0.887410625, 0.887410625, 0.887410625]
+    assert np.allclose(calls[:8], want, rtol=1e-15, atol=0)
+    assert np.isclose(calls[8], 3.0 - 3 * 0.887410625, rtol=1e-13)
+    assert np.isclose(h, 1.02 * (3.0 - 3 * 0.887410625), rtol=1e-13)
+
+
+def test_P23_dt_controller_growth_and_max_steps():
+    """Estimate 10 x the step: never rejected; every accepted step is <= 0.8 * estimate, so
+    the step grows by beta2 = 1.02 each time (h_n = 1.02^n h_0); max_steps stops the loop."""
+    fom = _fom()
+    hs = []
+
+    def step(x, v, e, h):
+        hs.append(h)
+        return x, v, e, 10.0 * h
+    *_, t, h, ns, nr = fom.advance(None, None, 0, 0, 0, 0.0, 1e9, 0.5, step=step, max_steps=6)
+    assert (ns, nr) == (6, 0)
+    assert np.allclose(hs, [0.5 * 1.02 ** i for i in range(6)], rtol=1e-15, atol=0)
+    assert np.isclose(t, sum(hs), rtol=1e-15)
+    assert np.isclose(h, 0.5 * 1.02 ** 6, rtol=1e-15)

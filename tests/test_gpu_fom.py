@@ -119,3 +119,32 @@ def test_step_deterministic():
         outs.append([t.cpu().numpy() for t in (x, v, e)])
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("dim,k,shape", [(2, 2, (7, 5)), (3, 2, (3, 3, 2))])
+def test_advance_controller_matches_oracle(dim, k, shape):
+    """hydro_fom_advance (PAPER P:549-566 controller) against oracle/fom.advance from a first
+    step 3x the stable estimate: the same accepted/rejected counts, the same time reached,
+    and the final state within 1e-10 relative."""
+    prob = _box(dim, k, shape)
+    m = prob.mesh
+    bc = ofom.bc_dofs_box(m)
+    prob.v.reshape(-1)[bc] = 0.0
+    ref = ofom.Fom(m, bc)
+    ctx = H.context(prob)
+    f = hydro.Fom(ctx, bc)
+    x, v, e, g = H.dev(prob.x), H.dev(prob.v), H.dev(prob.e), H.dev(prob.gamma)
+    visc, cfl = hydro.Visc(prob.q1, prob.q2, prob.visc), hydro.Cfl(prob.alpha, prob.alpha_mu)
+    import oracle
+    dt0 = 3.0 * oracle.force(prob)["dt"]
+    t_final = 4.0 * dt0
+    tg, hg, nsg, nrg = f.advance(x, v, e, g, visc, cfl, 0.0, t_final, dt0, max_steps=6,
+                                 cg_tol=1e-14, cg_max_iter=2000)
+    xr, vr, er, tr, hr, nsr, nrr = ofom.advance(ref, prob, prob.x.copy(), prob.v.copy(),
+                                                prob.e.copy(), 0.0, t_final, dt0, max_steps=6)
+    assert ctx.status_sync()[0] == 0
+    assert (nsg, nrg) == (nsr, nrr) and nrg > 0
+    assert tg == pytest.approx(tr, rel=1e-12) and hg == pytest.approx(hr, rel=1e-10)
+    for got, want, what in ((x, xr, "x"), (v, vr, "v"), (e, er, "e")):
+        g_ = got.cpu().numpy()
+        assert np.abs(g_ - want).max() <= 1e-10 * max(np.abs(want).max(), 1e-300), what
