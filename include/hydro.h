@@ -253,8 +253,9 @@ hydro_status hydro_fom_advance(hydro_fom *fom, double *x, double *v, double *e,
  * R_v = Mhat_V^-1 Phi_v^T Phi_F1 (Z^T Phi_F1)^+ [nv][s_v], R_e likewise [ne][s_e] (Eq.
  * sol-ls-hyper), C_xv = Phi_x^T Phi_v [nx][nv], c_x = Phi_x^T v_os [nx].
  * dt: device [B] per-instance step; dt_est (device [B] or NULL) = min over both stages'
- * estimates.  Four sampled force evaluations per step.  All device pointers are
- * kept by the object and must outlive it; buffers are allocated at create (setup).       */
+ * estimates.  Two sampled force evaluations per step (storing the S0 elements'
+ * point stresses) and two transposed F^T w passes.  All device pointers are kept by the
+ * object and must outlive it; buffers are allocated at create (setup).                   */
 typedef struct hydro_rom hydro_rom;
 hydro_status hydro_rom_create(hydro_sample *plan, int nx, int nv, int ne, const double *Phi_x_S,
                               const double *Phi_v_S, const double *Phi_e_S, const double *x_os_S,
@@ -265,6 +266,18 @@ hydro_status hydro_rom_destroy(hydro_rom *rom);
 hydro_status hydro_rom_rk2avg_step(hydro_rom *rom, double *Yx, double *Yv, double *Ye,
                                    const double *gamma, hydro_visc visc, hydro_cfl cfl,
                                    const double *dt, double *dt_est, hydro_stream_t stream);
+/* The online time loop t0 -> t_final for every instance under the controller of P:549-566
+ * (as hydro_fom_advance, per instance: each instance is an independent simulation with its
+ * own step).  dt (host [B], in/out): first trial steps, returned as the next steps.  The
+ * instances step together; rejected and finished instances are restored from an internal
+ * copy after each batched step.  At most max_iters batched steps; t_out, steps, rejected
+ * (host [B] or NULL) per instance, *iters (host or NULL) = batched steps run.
+ * HYDRO_ERR_NONFINITE on a NaN estimate.  Synchronises `stream`.                          */
+hydro_status hydro_rom_advance(hydro_rom *rom, double *Yx, double *Yv, double *Ye,
+                               const double *gamma, hydro_visc visc, hydro_cfl cfl,
+                               hydro_dt_ctrl ctrl, double t0, double t_final, double *dt,
+                               int max_iters, double *t_out, int *steps, int *rejected,
+                               int *iters, hydro_stream_t stream);
 
 /* ------------------------------------------------------------------ profiling (host) */
 /* When enabled, every hydro_force_full / hydro_dt_estimate / hydro_force_sampled call

@@ -139,6 +139,8 @@ def rk2avg_step(fom: Fom, prob, x, v, e, dt: float):
     s2w = _force(prob, x=x_h, v=v_h, e=e_h, w=vbar)
     e1 = e + dt * fom.solve_e(s2w["FTw"])
     x1 = x + dt * vbar
+    if s1["status"] or s2["status"]:   # tangled or non-finite stage: the step is invalid
+        return x1, v1, e1, float("nan")
     return x1, v1, e1, min(s1["dt"], s2["dt"])
 
 
@@ -147,7 +149,9 @@ def advance(fom: Fom, prob, x, v, e, t0: float, t_final: float, dt: float, beta1
     """Time loop t0 -> t_final under the time-step controller of PAPER P:549-566:
 
       1. with dt and the state U^n, evaluate U^{n+1} and the estimate dt_est;
-      2. if dt >= dt_est: dt <- beta1 dt and go to 1 (from U^n);
+      2. if dt >= dt_est: dt <- beta1 dt and go to 1 (from U^n) -- also when the trial step
+         is invalid (a stage tangles an element or its estimate is NaN, e.g. a negative
+         energy, R12): dt_est = NaN then, read as "too large" (DESIGN R26);
       3. if dt <= gamma dt_est: dt <- beta2 dt;
       4. accept, n <- n + 1.
 
@@ -161,11 +165,11 @@ def advance(fom: Fom, prob, x, v, e, t0: float, t_final: float, dt: float, beta1
     while t < t_final and ns < max_steps:
         h_try = t_final - t if t_final - t < h else h
         x1, v1, e1, est = step(x, v, e, h_try)
-        if np.isnan(est):
-            raise FloatingPointError("NaN time-step estimate")
-        if h_try >= est:
+        if np.isnan(est) or h_try >= est:
             h = beta1 * h_try
             nr += 1
+            if nr > 10000:
+                raise FloatingPointError("no admissible step found")
             continue
         x, v, e = x1, v1, e1
         t = t_final if h_try == t_final - t else t + h_try

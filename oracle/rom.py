@@ -52,7 +52,8 @@ def sampled_force(batch_base, closure_elems, closure_nodes, s0_nodes, sample_ele
     r = _force(batch_base, elist=closure_elems, x=x, v=v, e=e, w=w)
     F1 = r["F1"][:, s0_nodes].reshape(-1)
     FT = r["FTw"][sample_elems].reshape(-1)
-    return F1, FT, r["dt"]
+    # a tangled or non-finite evaluation makes the instance's estimate NaN (DESIGN R26)
+    return F1, FT, (float("nan") if r["status"] else r["dt"])
 
 
 def rom_rk2avg_step(op, Yx, Yv, Ye, dt):
@@ -90,3 +91,49 @@ def rom_rk2avg_step(op, Yx, Yv, Ye, dt):
     Ye1 = Ye + dt * (op["R_e"] @ FTh)
     Yx1 = Yx + dt * (op["c_x"][:, None] + op["C_xv"] @ Yvb)
     return Yx1, Yv1, Ye1, np.minimum(dt1, dt2)
+
+
+def advance(op, Yx, Yv, Ye, t0, t_final, dt, beta1=0.85, beta2=1.02, gamma=0.8,
+            max_iters=10**6, step=None):
+    """Online time loop t0 -> t_final for every instance under the time-step controller of
+    PAPER P:549-566, applied to each instance independently (each is its own simulation):
+    all instances take one batched step with their own trial dt (0 once finished); an
+    instance whose dt >= its estimate keeps its previous coordinates and retries with
+    beta1 dt; an accepted one advances, growing dt by beta2 when dt <= gamma * estimate; the
+    step that reaches t_final is shortened to land on it.  `step(Yx, Yv, Ye, dt[B]) ->
+    (Yx1, Yv1, Ye1, dt_est[B])` defaults to rom_rk2avg_step(op, ...).
+    Returns (Yx, Yv, Ye, t[B], next_dt[B], accepted[B], rejected[B], batched_steps)."""
+    if step is None:
+        def step(a, b_, c, h_):
+            return rom_rk2avg_step(op, a, b_, c, h_)
+    B = Yv.shape[1]
+    t = np.full(B, float(t0))
+    h = np.array(dt, dtype=np.float64).copy()
+    ns = np.zeros(B, dtype=np.int64)
+    nr = np.zeros(B, dtype=np.int64)
+    it = 0
+    while it < max_iters:
+        act = t < t_final
+        if not act.any():
+            break
+        htry = np.where(act, np.where(t_final - t < h, t_final - t, h), 0.0)
+        Yx1, Yv1, Ye1, est = step(Yx, Yv, Ye, htry)
+        it += 1
+        keep = np.zeros(B, dtype=bool)
+        for b in range(B):
+            if htry[b] == 0.0:
+                continue
+            if np.isnan(est[b]) or htry[b] >= est[b]:   # invalid or too large (R26)
+                h[b] = beta1 * htry[b]
+                nr[b] += 1
+                if nr[b] > 10000:
+                    raise FloatingPointError(f"no admissible step found, instance {b}")
+                continue
+            keep[b] = True
+            t[b] = t_final if htry[b] == t_final - t[b] else t[b] + htry[b]
+            ns[b] += 1
+            h[b] = beta2 * htry[b] if htry[b] <= gamma * est[b] else htry[b]
+        Yx = np.where(keep[None, :], Yx1, Yx)
+        Yv = np.where(keep[None, :], Yv1, Yv)
+        Ye = np.where(keep[None, :], Ye1, Ye)
+    return Yx, Yv, Ye, t, h, ns, nr, it

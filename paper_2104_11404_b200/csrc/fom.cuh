@@ -545,6 +545,14 @@ __global__ void rom_axpy_kernel(int64_t n, int B, const double *__restrict__ a, 
   out[t] = a[t] + (s * dt[b]) * r[t];
 }
 
+// Per-instance accept/restore of the step controller: Y[:, b] = keep[b] ? Y : Ybak (layout [n][B])
+__global__ void rom_select_kernel(int64_t n, int B, const double *__restrict__ keep,
+                                  const double *__restrict__ bak, double *__restrict__ Y) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * B) return;
+  if (keep[t % B] == 0.0) Y[t] = bak[t];
+}
+
 __global__ void min2_kernel(int B, const double *__restrict__ a, const double *__restrict__ b,
                             double *__restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;

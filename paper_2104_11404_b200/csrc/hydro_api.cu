@@ -1232,6 +1232,29 @@ hydro_status hydro_rk2avg_step(hydro_fom *f, double *x, double *v, double *e, co
 }
 
 
+// Per-instance validity of the last evaluation(s) since the previous read (tangled element or
+// non-finite estimate), then the status words are reset: a rejected trial step must not
+// leave its condition behind.  bad[b] = 1 for an invalid instance.
+static hydro_status read_reset_status(hydro_devstatus *st, int B, cudaStream_t s,
+                                      std::vector<char> &bad) {
+  std::vector<hydro_devstatus> h((size_t)B);
+  CUDA_OK(cudaMemcpyAsync(h.data(), st, sizeof(hydro_devstatus) * B, cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+  bad.assign((size_t)B, 0);
+  bool any = false;
+  for (int b = 0; b < B; ++b) {
+    hydro_devstatus &x = h[(size_t)b];
+    if (x.first_bad != ~0ull || x.nan_sticky || x.nan_flag) { bad[(size_t)b] = 1; any = true; }
+    x.first_bad = ~0ull;
+    x.nan_sticky = 0;
+  }
+  if (any) {
+    CUDA_OK(cudaMemcpyAsync(st, h.data(), sizeof(hydro_devstatus) * B, cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+  }
+  return HYDRO_OK;
+}
+
 hydro_status hydro_fom_advance(hydro_fom *f, double *x, double *v, double *e, const double *gamma,
                                hydro_visc visc, hydro_cfl cfl, hydro_dt_ctrl ctrl, double t0,
                                double t_final, double *dt, int max_steps, double cg_tol,
@@ -1257,14 +1280,19 @@ hydro_status hydro_fom_advance(hydro_fom *f, double *x, double *v, double *e, co
     if ((st = hydro_rk2avg_step(f, x, v, e, gamma, visc, cfl, h_try, cg_tol, cg_max_iter, &est,
                                 nullptr, stream)) != HYDRO_OK)
       break;
-    if (!(est == est)) { st = HYDRO_ERR_NONFINITE; break; }
-    if (h_try >= est) {  // rejected: restore and retry with a smaller step
+    std::vector<char> bad;
+    if ((st = read_reset_status(f->c->st, 1, s, bad)) != HYDRO_OK) break;
+#ifdef HYDRO_DEBUG_ADV
+    fprintf(stderr, "adv t=%.17g h_try=%.17g est=%.17g bad=%d ns=%d nr=%d\n", t, h_try, est, (int)bad[0], ns, nr);
+#endif
+    // rejected (too large, or invalid: tangled / NaN estimate, DESIGN R26): restore, retry
+    if (bad[0] || !(est == est) || h_try >= est) {
       CUDA_OK(cudaMemcpyAsync(x, f->xb, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
       CUDA_OK(cudaMemcpyAsync(v, f->vb, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
       CUDA_OK(cudaMemcpyAsync(e, f->eb, sizeof(double) * nE, cudaMemcpyDeviceToDevice, s));
       h = ctrl.beta1 * h_try;
       ++nr;
-      if (nr > 1000000) { st = HYDRO_ERR_NONFINITE; break; }
+      if (nr > 10000) { st = HYDRO_ERR_NONFINITE; break; }  // no admissible step found
       continue;
     }
     t = (h_try == t_final - t) ? t_final : t + h_try;
@@ -1294,6 +1322,8 @@ struct hydro_rom {
          *rx = nullptr, *Yv_h = nullptr, *Ye_h = nullptr, *Yx_h = nullptr, *Yv1 = nullptr,
          *Yvb = nullptr, *dt1 = nullptr, *dt2 = nullptr, *wsv = nullptr, *wse = nullptr,
          *S = nullptr;
+  double *Yxb = nullptr, *Yvb_ = nullptr, *Yeb = nullptr, *hdev = nullptr, *est = nullptr,
+         *keep = nullptr;  // step-controller state (backup of the reduced coordinates)
   size_t wsv_bytes = 0, wse_bytes = 0;
   std::vector<void *> allocs;
 };
@@ -1342,6 +1372,9 @@ hydro_status hydro_rom_create(hydro_sample *p, int nx, int nv, int ne, const dou
       !alloc(&r->Yx_h, (size_t)nx * B) || !alloc(&r->Yv1, (size_t)nv * B) ||
       !alloc(&r->Yvb, (size_t)nv * B) || !alloc(&r->dt1, B) || !alloc(&r->dt2, B) ||
       !alloc(&r->wsv, r->wsv_bytes / 8 + 1) || !alloc(&r->wse, r->wse_bytes / 8 + 1) ||
+      !alloc(&r->Yxb, (size_t)nx * B) || !alloc(&r->Yvb_, (size_t)nv * B) ||
+      !alloc(&r->Yeb, (size_t)ne * B) || !alloc(&r->hdev, B) || !alloc(&r->est, B) ||
+      !alloc(&r->keep, B) ||
       !alloc(&r->S, hydro_sample_stress_bytes(p) / sizeof(double)))
     return fail(HYDRO_ERR_CUDA);
   *out = r;
@@ -1413,6 +1446,85 @@ hydro_status hydro_rom_rk2avg_step(hydro_rom *r, double *Yx, double *Yv, double 
 #undef RS
   CUDA_OK(cudaGetLastError());
   return HYDRO_OK;
+}
+
+hydro_status hydro_rom_advance(hydro_rom *r, double *Yx, double *Yv, double *Ye,
+                               const double *gamma, hydro_visc visc, hydro_cfl cfl,
+                               hydro_dt_ctrl ctrl, double t0, double t_final, double *dt,
+                               int max_iters, double *t_out, int *steps, int *rejected,
+                               int *iters, hydro_stream_t stream) {
+  if (!r || !Yx || !Yv || !Ye || !gamma || !dt || !(t_final >= t0) || max_iters < 0 ||
+      !(ctrl.beta1 > 0.0 && ctrl.beta1 < 1.0) || !(ctrl.beta2 >= 1.0) || !(ctrl.gamma > 0.0))
+    return HYDRO_ERR_ARG;
+  const int B = r->B;
+  for (int b = 0; b < B; ++b)
+    if (!(dt[b] > 0.0)) return HYDRO_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<double> t((size_t)B, t0), h(dt, dt + B), htry((size_t)B), est((size_t)B),
+      keep((size_t)B);
+  std::vector<int> ns((size_t)B, 0), nr((size_t)B, 0);
+  int it = 0;
+  hydro_status st = HYDRO_OK;
+  const size_t bx = sizeof(double) * (size_t)r->nx * B, bv = sizeof(double) * (size_t)r->nv * B,
+               be = sizeof(double) * (size_t)r->ne * B;
+  // PAPER P:549-566 per instance (each instance is an independent simulation): instances
+  // step together with their own trial dt; a rejected instance (dt >= its estimate) is
+  // restored from the copy and retried with beta1*dt; finished instances ride along with a
+  // zero step and are restored too, so their coordinates stay bit-identical.
+  while (it < max_iters) {
+    bool any = false;
+    for (int b = 0; b < B; ++b) {
+      const bool act = t[(size_t)b] < t_final;
+      any = any || act;
+      htry[(size_t)b] = act ? ((t_final - t[(size_t)b] < h[(size_t)b]) ? t_final - t[(size_t)b]
+                                                                       : h[(size_t)b])
+                            : 0.0;
+    }
+    if (!any) break;
+    CUDA_OK(cudaMemcpyAsync(r->Yxb, Yx, bx, cudaMemcpyDeviceToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(r->Yvb_, Yv, bv, cudaMemcpyDeviceToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(r->Yeb, Ye, be, cudaMemcpyDeviceToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(r->hdev, htry.data(), sizeof(double) * B, cudaMemcpyHostToDevice, s));
+    if ((st = hydro_rom_rk2avg_step(r, Yx, Yv, Ye, gamma, visc, cfl, r->hdev, r->est, stream)) !=
+        HYDRO_OK)
+      break;
+    CUDA_OK(cudaMemcpyAsync(est.data(), r->est, sizeof(double) * B, cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    std::vector<char> bad;
+    if ((st = read_reset_status(r->p->st, B, s, bad)) != HYDRO_OK) break;
+    ++it;
+    for (int b = 0; b < B; ++b) {
+      const size_t i = (size_t)b;
+      keep[i] = 0.0;
+      if (htry[i] == 0.0) continue;  // finished instance
+      if (bad[i] || !(est[i] == est[i]) || htry[i] >= est[i]) {  // too large or invalid (R26)
+        if (nr[i] >= 10000) st = HYDRO_ERR_NONFINITE;               // no admissible step found
+        h[i] = ctrl.beta1 * htry[i];
+        ++nr[i];
+        continue;
+      }
+      keep[i] = 1.0;
+      t[i] = (htry[i] == t_final - t[i]) ? t_final : t[i] + htry[i];
+      ++ns[i];
+      h[i] = (htry[i] <= ctrl.gamma * est[i]) ? ctrl.beta2 * htry[i] : htry[i];
+    }
+    CUDA_OK(cudaMemcpyAsync(r->keep, keep.data(), sizeof(double) * B, cudaMemcpyHostToDevice, s));
+    hk::rom_select_kernel<<<blocks_for((int64_t)r->nx * B, 256), 256, 0, s>>>(r->nx, B, r->keep, r->Yxb, Yx);
+    hk::rom_select_kernel<<<blocks_for((int64_t)r->nv * B, 256), 256, 0, s>>>(r->nv, B, r->keep, r->Yvb_, Yv);
+    hk::rom_select_kernel<<<blocks_for((int64_t)r->ne * B, 256), 256, 0, s>>>(r->ne, B, r->keep, r->Yeb, Ye);
+    g_launches += 3;
+    CUDA_OK(cudaGetLastError());
+    if (st != HYDRO_OK) break;
+  }
+  CUDA_OK(cudaStreamSynchronize(s));
+  for (int b = 0; b < B; ++b) {
+    dt[b] = h[(size_t)b];
+    if (t_out) t_out[b] = t[(size_t)b];
+    if (steps) steps[b] = ns[(size_t)b];
+    if (rejected) rejected[b] = nr[(size_t)b];
+  }
+  if (iters) *iters = it;
+  return st;
 }
 
 }  // extern "C"

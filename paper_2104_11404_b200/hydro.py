@@ -32,7 +32,7 @@ EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy"
             "hydro_profile_enable", "hydro_profile_read", "hydro_profile_read_captured",
             "hydro_profile_release_captured", "hydro_selftest_ieee_fast",
             "hydro_fom_create", "hydro_fom_destroy", "hydro_mass_v_apply", "hydro_mass_v_solve",
-            "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_fom_advance", "hydro_rom_create",
+            "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_fom_advance", "hydro_rom_advance", "hydro_rom_create",
             "hydro_rom_destroy", "hydro_rom_rk2avg_step", "hydro_force_stress_bytes",
             "hydro_force_full_store", "hydro_force_transpose", "hydro_sample_stress_bytes",
             "hydro_force_sampled_store", "hydro_sample_force_transpose"]
@@ -107,6 +107,10 @@ def lib() -> ctypes.CDLL:
                                        vp, ctypes.POINTER(vp)]
         L.hydro_rom_destroy.argtypes = [vp]
         L.hydro_rom_rk2avg_step.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, vp, vp, vp]
+        L.hydro_rom_advance.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, _DtCtrl, dbl, dbl,
+                                        ctypes.POINTER(dbl), i32, ctypes.POINTER(dbl),
+                                        ctypes.POINTER(i32), ctypes.POINTER(i32),
+                                        ctypes.POINTER(i32), vp]
         L.hydro_force_stress_bytes.restype = ctypes.c_size_t
         L.hydro_force_stress_bytes.argtypes = [vp]
         L.hydro_force_full_store.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, vp, vp, vp, vp, vp]
@@ -509,3 +513,19 @@ class RomStepper:
                                            cfl.c(), _ptr(dt), _ptr(dt_est), _stream(stream)),
                "hydro_rom_rk2avg_step")
         return dt_est
+
+    def advance(self, Yx, Yv, Ye, gamma, visc: Visc, cfl: Cfl, t0: float, t_final: float, dt,
+                ctrl: DtCtrl = DtCtrl(), max_iters=1000000, stream=None):
+        """In-place online time loop t0 -> t_final for every instance under the controller
+        of P:549-566.  dt: host sequence [B] of first trial steps.  Returns (t [B], next dt [B],
+        accepted [B], rejected [B], batched steps run) as numpy arrays / int."""
+        import numpy as _np
+        B = self.plan.B
+        h = (ctypes.c_double * B)(*[float(d) for d in dt])
+        t = (ctypes.c_double * B)()
+        ns, nr = (ctypes.c_int * B)(), (ctypes.c_int * B)()
+        it = ctypes.c_int(0)
+        _check(lib().hydro_rom_advance(self._h, _ptr(Yx), _ptr(Yv), _ptr(Ye), _ptr(gamma), visc.c(),
+                                       cfl.c(), ctrl.c(), t0, t_final, h, max_iters, t, ns, nr,
+                                       ctypes.byref(it), _stream(stream)), "hydro_rom_advance")
+        return (_np.array(t[:]), _np.array(h[:]), _np.array(ns[:]), _np.array(nr[:]), it.value)

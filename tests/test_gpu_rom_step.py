@@ -84,3 +84,40 @@ def test_rom_step_instances_independent():
     one = run(1, slice(1, 2))
     for a, b in zip(full, one):
         assert np.array_equal(a[:, 1], b[:, 0])
+
+
+def test_rom_advance_controller_matches_oracle():
+    """hydro_rom_advance (P:549-566 controller per instance) against oracle/rom.advance on a
+    C4-shaped batch whose instances start from 3x / 0.5x / 1.5x their stability estimates:
+    the same per-instance accepted/rejected counts and times, reduced coordinates within
+    1e-10 of their scale."""
+    batch = W.c4(n_sample=6, B=3, small_mesh=True)
+    base = batch.base
+    P_v, P_e, C_xv, c_x = W.offline_projectors(batch)
+    ctx = H.context(base)
+    plan = hydro.SamplePlan(ctx, batch.sample_elems, batch.B)
+    st = hydro.RomStepper(plan, H.dev(batch.Phi_x), H.dev(batch.Phi_v), H.dev(batch.Phi_e),
+                          H.dev(batch.x_os), H.dev(batch.v_os), H.dev(batch.e_os), H.dev(P_v),
+                          H.dev(P_e), H.dev(C_xv), H.dev(c_x))
+    op = dict(base=base, closure_elems=batch.closure_elems, closure_nodes=batch.closure_nodes,
+              s0_nodes=batch.s0_nodes, sample_elems=batch.sample_elems, Phi_x=batch.Phi_x,
+              Phi_v=batch.Phi_v, Phi_e=batch.Phi_e, x_os=batch.x_os, v_os=batch.v_os,
+              e_os=batch.e_os, R_v=P_v, R_e=P_e, C_xv=C_xv, c_x=c_x)
+    _, _, _, est0 = orom.rom_rk2avg_step(op, batch.Yx, batch.Yv, batch.Ye, np.zeros(batch.B))
+    dt0 = est0 * np.array([3.0, 0.5, 1.5])
+    t_final = 2.5 * float(est0.max())
+    Yx, Yv, Ye = H.dev(batch.Yx), H.dev(batch.Yv), H.dev(batch.Ye)
+    visc, cfl = hydro.Visc(base.q1, base.q2, base.visc), hydro.Cfl(base.alpha, base.alpha_mu)
+    tg, hg, nsg, nrg, itg = st.advance(Yx, Yv, Ye, H.dev(base.gamma), visc, cfl, 0.0, t_final,
+                                       dt0, max_iters=12)
+    rx, rv, re, tr, hr, nsr, nrr, itr = orom.advance(op, batch.Yx.copy(), batch.Yv.copy(),
+                                                     batch.Ye.copy(), 0.0, t_final, dt0,
+                                                     max_iters=12)
+    assert plan.status_sync()[0] == 0
+    assert itg == itr and list(nsg) == list(nsr) and list(nrg) == list(nrr)
+    assert nrg.sum() > 0 and nsg.sum() > 0
+    np.testing.assert_allclose(tg, tr, rtol=1e-12)
+    np.testing.assert_allclose(hg, hr, rtol=1e-10)
+    for got, want, what in ((Yx, rx, "xhat"), (Yv, rv, "vhat"), (Ye, re, "ehat")):
+        g_ = got.cpu().numpy()
+        assert np.abs(g_ - want).max() <= 1e-10 * np.abs(want).max(), what

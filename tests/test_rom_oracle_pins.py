@@ -61,3 +61,36 @@ def test_P22_lift_basis_columns():
     Y[2, 1] = 1.0
     out = rom.lift(Phi, os_, Y)
     assert np.array_equal(out[:, 1], os_ + Phi[:, 2])
+
+
+def test_P24_rom_controller_is_per_instance():
+    """The batched online loop applies the controller of P:549-566 to each instance as if it
+    ran alone: with a scripted step whose estimate differs per instance, every instance's
+    trial-step sequence, counts and final time equal oracle/fom.advance on that instance
+    alone (whose controller trace is pinned by hand in P23); coordinates of a rejected or
+    finished instance are left untouched."""
+    from oracle import fom, rom
+    ests = np.array([1.0, 0.3, 5.0])
+    seen = {b: [] for b in range(3)}
+
+    def step(Yx, Yv, Ye, h):
+        for b in range(3):
+            if h[b] > 0:
+                seen[b].append(h[b])
+        return Yx + h[None, :], Yv + 2 * h[None, :], Ye - h[None, :], ests.copy()
+    Y0 = np.zeros((2, 3))
+    Yx, Yv, Ye, t, hn, ns, nr, it = rom.advance(None, Y0, Y0, Y0, 0.0, 3.0, [2.0, 2.0, 2.0],
+                                                step=step)
+    for b in range(3):
+        calls = []
+
+        def one(x, v, e, h):
+            calls.append(h)
+            return x, v, e, ests[b]
+        *_, tb, hb, nsb, nrb = fom.advance(None, None, 0, 0, 0, 0.0, 3.0, 2.0, step=one)
+        assert seen[b] == calls
+        assert (ns[b], nr[b], t[b], hn[b]) == (nsb, nrb, tb, hb)
+        # accepted increments only: x advanced by exactly the accepted steps
+        acc = [c for c, nxt in zip(calls, calls[1:] + [None]) if c < ests[b]]
+        assert np.isclose(Yx[0, b], sum(acc), rtol=1e-14)
+        assert np.isclose(Ye[1, b], -sum(acc), rtol=1e-14)
