@@ -137,3 +137,34 @@ def advance(op, Yx, Yv, Ye, t0, t_final, dt, beta1=0.85, beta2=1.02, gamma=0.8,
         Yv = np.where(keep[None, :], Yv1, Yv)
         Ye = np.where(keep[None, :], Ye1, Ye)
     return Yx, Yv, Ye, t, h, ns, nr, it
+
+
+def window_transition(T, c, Y):
+    """Initial reduced coordinates of time window w from those of window w-1, PAPER Eq.
+    ic-tw: yhat_w = T yhat_{w-1} + c with the offline T = Phi_w^T Phi_{w-1} and
+    c = Phi_w^T (os_{w-1} - os_w) (the oblique Eq. ic2-tw only changes T and c).  Plain
+    product: Y_new[i][b] = c[i] (or c[i][b]) + sum_k T[i][k] Y[k][b]."""
+    return lift(T, c, Y)
+
+
+def windowed_advance(windows, Yx, Yv, Ye, t0, dt, beta1=0.85, beta2=1.02, gamma=0.8,
+                     max_iters=10**6):
+    """The time-windowing online phase: for each window, `advance` with its
+    own operators up to its end time, then map the reduced coordinates into the next
+    window's bases (window_transition).  windows: list of dicts with keys op (the
+    rom_rk2avg_step operators), t_end and, except for the last, trans = ((Tx, cx), (Tv, cv),
+    (Te, ce)).  Returns (Yx, Yv, Ye, t[B], next_dt[B], per-window (accepted, rejected))."""
+    t = t0
+    h = np.array(dt, dtype=np.float64)
+    stats = []
+    tB = None
+    for w in windows:
+        Yx, Yv, Ye, tB, h, ns, nr, _ = advance(w["op"], Yx, Yv, Ye, t, w["t_end"], h, beta1, beta2,
+                                               gamma, max_iters)
+        stats.append((ns, nr))
+        t = w["t_end"]
+        if w.get("trans") is not None:
+            (Tx, cx), (Tv, cv), (Te, ce) = w["trans"]
+            Yx, Yv, Ye = window_transition(Tx, cx, Yx), window_transition(Tv, cv, Yv), \
+                window_transition(Te, ce, Ye)
+    return Yx, Yv, Ye, tB, h, stats

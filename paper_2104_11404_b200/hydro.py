@@ -396,6 +396,36 @@ def rom_lift(Phi: torch.Tensor, os_: torch.Tensor, Y: torch.Tensor, out: Optiona
     return out
 
 
+def rom_window_transition(T: torch.Tensor, c: torch.Tensor, Y: torch.Tensor,
+                          out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Initial reduced coordinates of time window w, PAPER Eq. ic-tw / ic2-tw
+    (P:1223-1264): Y_w = T Y_{w-1} + c with the offline T [n_w][n_{w-1}] and c ([n_w] or
+    [n_w][B]) -- the lift primitive (hydro_rom_lift) on reduced dimensions."""
+    return rom_lift(T, c, Y, out=out, stream=stream)
+
+
+def rom_windowed_advance(windows, Yx, Yv, Ye, gamma, visc: Visc, cfl: Cfl, t0: float, dt,
+                         ctrl: DtCtrl = DtCtrl(), max_iters=1000000, stream=None):
+    """The time-windowing online phase: for each window advance with its own
+    RomStepper to its end time (hydro_rom_advance), then map the reduced coordinates into
+    the next window's bases (rom_window_transition).  windows: list of dicts with keys
+    stepper, t_end and, except for the last, trans = ((Tx, cx), (Tv, cv), (Te, ce)) as
+    device tensors.  Returns (Yx, Yv, Ye, t[B], next_dt[B], per-window (accepted, rejected));
+    the returned coordinates are new tensors where a transition changed their dimension."""
+    t, h, stats, tB = t0, list(dt), [], None
+    for w in windows:
+        tB, h, ns, nr, _ = w["stepper"].advance(Yx, Yv, Ye, gamma, visc, cfl, t, w["t_end"], h,
+                                                ctrl, max_iters, stream)
+        stats.append((ns, nr))
+        t = w["t_end"]
+        if w.get("trans") is not None:
+            (Tx, cx), (Tv, cv), (Te, ce) = w["trans"]
+            Yx = rom_window_transition(Tx, cx, Yx, stream=stream)
+            Yv = rom_window_transition(Tv, cv, Yv, stream=stream)
+            Ye = rom_window_transition(Te, ce, Ye, stream=stream)
+    return Yx, Yv, Ye, tB, h, stats
+
+
 def rom_project_workspace(n: int, s_rows: int, B: int, device="cuda") -> torch.Tensor:
     nb = lib().hydro_rom_project_workspace_bytes(n, s_rows, B)
     return torch.empty(max(nb, 8), dtype=torch.uint8, device=device)

@@ -121,3 +121,51 @@ def test_rom_advance_controller_matches_oracle():
     for got, want, what in ((Yx, rx, "xhat"), (Yv, rv, "vhat"), (Ye, re, "ehat")):
         g_ = got.cpu().numpy()
         assert np.abs(g_ - want).max() <= 1e-10 * np.abs(want).max(), what
+
+
+def test_rom_windowed_advance_matches_oracle():
+    """Two time windows: window 1 with the batch's bases up to t1, the
+    transition Eq. ic-tw into window 2's bases (W.next_window: 24 shared directions), then
+    window 2 up to t2 -- against oracle/rom.windowed_advance: per-window step counts, times,
+    and the final reduced coordinates within 1e-10 of their scale."""
+    b1 = W.c4(n_sample=6, B=3, small_mesh=True)
+    b2 = W.next_window(b1)
+    base = b1.base
+    ctx = H.context(base)
+    plan = hydro.SamplePlan(ctx, b1.sample_elems, b1.B)
+    g = H.dev(base.gamma)
+    visc, cfl = hydro.Visc(base.q1, base.q2, base.visc), hydro.Cfl(base.alpha, base.alpha_mu)
+
+    def ops(b):
+        P_v, P_e, C_xv, c_x = W.offline_projectors(b)
+        op = dict(base=base, closure_elems=b.closure_elems, closure_nodes=b.closure_nodes,
+                  s0_nodes=b.s0_nodes, sample_elems=b.sample_elems, Phi_x=b.Phi_x, Phi_v=b.Phi_v,
+                  Phi_e=b.Phi_e, x_os=b.x_os, v_os=b.v_os, e_os=b.e_os, R_v=P_v, R_e=P_e,
+                  C_xv=C_xv, c_x=c_x)
+        st = hydro.RomStepper(plan, H.dev(b.Phi_x), H.dev(b.Phi_v), H.dev(b.Phi_e), H.dev(b.x_os),
+                              H.dev(b.v_os), H.dev(b.e_os), H.dev(P_v), H.dev(P_e), H.dev(C_xv),
+                              H.dev(c_x))
+        return op, st
+    op1, st1 = ops(b1)
+    op2, st2 = ops(b2)
+    trans = tuple(W.window_transition_ops(getattr(b2, f"Phi_{f}"), getattr(b1, f"Phi_{f}"),
+                                          getattr(b2, f"{f}_os"), getattr(b1, f"{f}_os"))
+                  for f in ("x", "v", "e"))
+    _, _, _, est0 = orom.rom_rk2avg_step(op1, b1.Yx, b1.Yv, b1.Ye, np.zeros(b1.B))
+    dt0 = 0.7 * est0
+    t1, t2 = 2.0 * float(est0.max()), 4.0 * float(est0.max())
+    ref = orom.windowed_advance([dict(op=op1, t_end=t1, trans=trans), dict(op=op2, t_end=t2)],
+                                b1.Yx.copy(), b1.Yv.copy(), b1.Ye.copy(), 0.0, dt0, max_iters=20)
+    dtr = tuple((H.dev(T), H.dev(c)) for T, c in trans)
+    got = hydro.rom_windowed_advance([dict(stepper=st1, t_end=t1, trans=dtr),
+                                      dict(stepper=st2, t_end=t2)],
+                                     H.dev(b1.Yx), H.dev(b1.Yv), H.dev(b1.Ye), g, visc, cfl, 0.0,
+                                     dt0, max_iters=20)
+    assert plan.status_sync()[0] == 0
+    for (nsg, nrg), (nsr, nrr) in zip(got[5], ref[5]):
+        assert list(nsg) == list(nsr) and list(nrg) == list(nrr)
+    np.testing.assert_allclose(got[3], ref[3], rtol=1e-12)
+    np.testing.assert_allclose(got[4], ref[4], rtol=1e-10)
+    for gt, want, what in zip(got[:3], ref[:3], ("xhat", "vhat", "ehat")):
+        g_ = gt.cpu().numpy()
+        assert np.abs(g_ - want).max() <= 1e-10 * np.abs(want).max(), what

@@ -523,3 +523,34 @@ def offline_projectors(batch: RomBatch):
     C_xv = np.ascontiguousarray(batch.Phi_x.T @ batch.Phi_v)
     c_x = np.ascontiguousarray(batch.Phi_x.T @ batch.v_os)
     return P_v, P_e, C_xv, c_x
+
+
+def window_transition_ops(Phi_new, Phi_old, os_new, os_old):
+    """Offline operators of the time-window transition, PAPER Eq. ic-tw:
+    yhat_w = Phi_w^T (os_{w-1} + Phi_{w-1} yhat_{w-1} - os_w) = T yhat_{w-1} + c with
+    T = Phi_w^T Phi_{w-1} [n_w][n_{w-1}] and c = Phi_w^T (os_{w-1} - os_w) ([n_w] or
+    [n_w][B] for per-instance offsets).  The synthetic bases exist on the sample-mesh
+    closure rows only, so the products run over those rows."""
+    T = np.ascontiguousarray(Phi_new.T @ Phi_old)
+    c = np.ascontiguousarray(Phi_new.T @ (os_old - os_new))
+    return T, c
+
+
+def next_window(batch: RomBatch, keep: int = 24, seed: int = 77):
+    """A second time window for a ROM batch (same mesh, sample and offsets): each field's
+    basis keeps its first `keep` columns and replaces the rest by fresh seeded directions,
+    re-orthonormalised (CholQR2), so consecutive windows share a subspace (as bases built
+    from overlapping snapshot windows do) but are not equal."""
+    import copy
+    nb = copy.copy(batch)
+    rng = np.random.default_rng(seed)
+    for name in ("Phi_x", "Phi_v", "Phi_e"):
+        P = getattr(batch, name)
+        fresh = rng.uniform(-1.0, 1.0, size=(P.shape[0], P.shape[1] - keep))
+        fresh -= P[:, :keep] @ (P[:, :keep].T @ fresh)
+        Q = np.concatenate([P[:, :keep], fresh], axis=1)
+        for _ in range(2):   # CholQR2
+            R = np.linalg.cholesky(Q.T @ Q).T
+            Q = np.linalg.solve(R.T, Q.T).T
+        setattr(nb, name, np.ascontiguousarray(Q))
+    return nb
