@@ -279,6 +279,30 @@ hydro_status hydro_rom_advance(hydro_rom *rom, double *Yx, double *Yv, double *Y
                                int max_iters, double *t_out, int *steps, int *rejected,
                                int *iters, hydro_stream_t stream);
 
+/* ------------------------------------------------------------------ offline phase (NEXT-3) */
+/* The half-stage state (x, v, e)^{n+1/2} of the last hydro_rk2avg_step (device copies; any
+ * pointer may be NULL): the intermediate Runge-Kutta stages belong to the POD snapshot set
+ * (P:921-943).                                                                              */
+hydro_status hydro_fom_stage_state(hydro_fom *fom, double *x_half, double *v_half,
+                                   double *e_half, hydro_stream_t stream);
+/* POD of the snapshot matrix S (device, [ns][N] row-major: ONE SNAPSHOT PER ROW,
+ * offsets already subtracted) by the method of snapshots: the Gram matrix S S^T on the GPU
+ * (fixed-order split-K), its symmetric eigen-decomposition on the host (cyclic Jacobi,
+ * ns x ns), sigma_i = sqrt(lambda_i), the energy criterion sum_{i<=k} sigma_i / sum sigma_i
+ * >= eps (paper default 0.9999) with k <= max_k, and the basis
+ * Phi = S^T V_k Sigma_k^-1 on the GPU followed by one CholQR pass (Phi <- Phi R^-1,
+ * R^T R = Phi^T Phi: the Gram route alone is orthonormal only to ~eps (sigma_1/sigma_k)^2)
+ * (device out [N][max_k] row-major, first k columns written; column c has the sign that
+ * makes the largest-magnitude entry of the c-th Gram eigenvector positive).  sigma (host [ns] or NULL), *k_out (host).  Allocates its own
+ * scratch (offline routine).  Synchronises `stream`.                                       */
+hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k, double *Phi,
+                       double *sigma, int *k_out, hydro_stream_t stream);
+/* Greedy DEIM interpolation indices (Algorithm 1 of Chaturantabut-Sorensen) of
+ * the basis U (device, [N][m] row-major): p_1 = argmax |u_1|; p_j = argmax |u_j - U_{<j} c|
+ * with (P^T U_{<j}) c = P^T u_j (LU with partial pivoting, host).  Ties: the lowest row.
+ * idx: host [m].  HYDRO_ERR_NONFINITE if some P^T U_{<j} is singular.  Synchronises.        */
+hydro_status hydro_deim(const double *U, int64_t N, int m, int64_t *idx, hydro_stream_t stream);
+
 /* ------------------------------------------------------------------ profiling (host) */
 /* When enabled, every hydro_force_full / hydro_dt_estimate / hydro_force_sampled call
  * records a pair of CUDA events around its force kernel on the call's stream (the

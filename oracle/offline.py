@@ -1,0 +1,55 @@
+"""CPU oracle of the ROM offline phase -- TEST INFRASTRUCTURE ONLY (same
+import rules as oracle/__init__.py).
+
+PAPER Sec. 4.3 (POD) and 4.5 (DEIM):
+
+* pod(S, eps): the thin SVD of the snapshot matrix (here S holds one snapshot per row, so the
+  paper's snapshot matrix is S^T) by a library SVD (a primitive as a step), the leading k left
+  singular vectors with k the smallest integer such that sum_{i<=k} sigma_i / sum_i sigma_i
+  >= eps (Eq. energy_criteria), each column signed so that the largest-magnitude entry of
+  the matching right singular vector is positive (the convention hydro_pod documents).
+* deim(U): Algorithm 1 of Chaturantabut-Sorensen as the paper describes it: p_1 = argmax
+  |u_1|; for j >= 2, c solves (P^T U_{<j}) c = P^T u_j and p_j = argmax |u_j - U_{<j} c|
+  (numpy.argmax: the first maximum, i.e. the lowest row on ties).
+
+Pinned by tests/test_offline_oracle_pins.py (closed-form low-rank snapshots, the DEIM
+interpolation property, permutation bases)."""
+from __future__ import annotations
+
+import numpy as np
+
+
+def pod(S: np.ndarray, eps: float = 0.9999, max_k: int | None = None):
+    """(Phi [N][k], sigma [ns]) of the snapshots S [ns][N]."""
+    ns = S.shape[0]
+    U, sig, Vt = np.linalg.svd(S.T, full_matrices=False)   # S^T = U diag(sig) Vt
+    tot = sig.sum()
+    k = ns
+    run = 0.0
+    for i in range(ns):
+        run += sig[i]
+        if tot > 0 and run / tot >= eps:
+            k = i + 1
+            break
+    if max_k is not None:
+        k = min(k, max_k)
+    while k > 0 and not sig[k - 1] > 0:
+        k -= 1
+    V = Vt.T
+    for c in range(k):
+        imax = int(np.argmax(np.abs(V[:, c])))
+        if V[imax, c] < 0:
+            U[:, c] = -U[:, c]
+    return U[:, :k].copy(), sig
+
+
+def deim(U: np.ndarray) -> np.ndarray:
+    """Greedy DEIM indices [m] of the basis U [N][m]."""
+    N, m = U.shape
+    p = [int(np.argmax(np.abs(U[:, 0])))]
+    for j in range(1, m):
+        A = U[p, :j]
+        c = np.linalg.solve(A, U[p, j])
+        r = U[:, j] - U[:, :j] @ c
+        p.append(int(np.argmax(np.abs(r))))
+    return np.array(p, dtype=np.int64)

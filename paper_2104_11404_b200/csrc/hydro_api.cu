@@ -14,6 +14,7 @@
 #include "force2d.cuh"
 #include "force3d.cuh"
 #include "fom.cuh"
+#include "offline.cuh"
 #include "force_kernel.cuh"
 #include "hydro_internal.h"
 #include "rom_kernels.cuh"
@@ -1307,6 +1308,17 @@ hydro_status hydro_fom_advance(hydro_fom *f, double *x, double *v, double *e, co
   return st;
 }
 
+hydro_status hydro_fom_stage_state(hydro_fom *f, double *x_half, double *v_half, double *e_half,
+                                   hydro_stream_t stream) {
+  if (!f) return HYDRO_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = f->n, nE = f->c->d.n_elem * f->c->ne;
+  if (x_half) CUDA_OK(cudaMemcpyAsync(x_half, f->xh, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  if (v_half) CUDA_OK(cudaMemcpyAsync(v_half, f->vh, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  if (e_half) CUDA_OK(cudaMemcpyAsync(e_half, f->eh, sizeof(double) * nE, cudaMemcpyDeviceToDevice, s));
+  return HYDRO_OK;
+}
+
 // ------------------------------------------------------------------------------ ROM step
 }  // extern "C"
 
@@ -1524,6 +1536,261 @@ hydro_status hydro_rom_advance(hydro_rom *r, double *Yx, double *Yv, double *Ye,
     if (rejected) rejected[b] = nr[(size_t)b];
   }
   if (iters) *iters = it;
+  return st;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------ offline (NEXT-3)
+namespace {
+
+// Symmetric eigen-decomposition of a small dense matrix (host, cyclic Jacobi to full
+// convergence): A [n][n] row-major in, eigenvalues lam[n] descending, eigenvectors V [n][n]
+// (column c = eigenvector c), each with its largest-magnitude component positive.
+void sym_eig_host(int n, std::vector<double> A, std::vector<double> &lam, std::vector<double> &V) {
+  V.assign((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0;
+  auto a = [&](int i, int j) -> double & { return A[(size_t)i * n + j]; };
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) { tot += a(i, j) * a(i, j); if (i != j) off += a(i, j) * a(i, j); }
+    if (off <= 1e-30 * tot || off == 0.0) break;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = a(p, q);
+        if (apq == 0.0) continue;
+        const double theta = (a(q, q) - a(p, p)) / (2.0 * apq);
+        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
+        for (int k = 0; k < n; ++k) {  // A <- A J (columns p, q)
+          const double akp = a(k, p), akq = a(k, q);
+          a(k, p) = c * akp - sn * akq;
+          a(k, q) = sn * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {  // A <- J^T A (rows p, q)
+          const double apk = a(p, k), aqk = a(q, k);
+          a(p, k) = c * apk - sn * aqk;
+          a(q, k) = sn * apk + c * aqk;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double vkp = V[(size_t)k * n + p], vkq = V[(size_t)k * n + q];
+          V[(size_t)k * n + p] = c * vkp - sn * vkq;
+          V[(size_t)k * n + q] = sn * vkp + c * vkq;
+        }
+      }
+  }
+  std::vector<int> order((size_t)n);
+  for (int i = 0; i < n; ++i) order[(size_t)i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return a(x, x) > a(y, y); });
+  std::vector<double> Vs((size_t)n * n);
+  lam.resize((size_t)n);
+  for (int c = 0; c < n; ++c) {
+    const int o = order[(size_t)c];
+    lam[(size_t)c] = a(o, o);
+    int imax = 0;
+    for (int k = 1; k < n; ++k)
+      if (std::fabs(V[(size_t)k * n + o]) > std::fabs(V[(size_t)imax * n + o])) imax = k;
+    const double sg = V[(size_t)imax * n + o] < 0.0 ? -1.0 : 1.0;
+    for (int k = 0; k < n; ++k) Vs[(size_t)k * n + c] = sg * V[(size_t)k * n + o];
+  }
+  V.swap(Vs);
+}
+
+// Solve A x = b (n x n, row-major) by LU with partial pivoting (host; DEIM's small systems).
+bool lu_solve_host(int n, std::vector<double> A, std::vector<double> &b) {
+  for (int k = 0; k < n; ++k) {
+    int p = k;
+    for (int i = k + 1; i < n; ++i)
+      if (std::fabs(A[(size_t)i * n + k]) > std::fabs(A[(size_t)p * n + k])) p = i;
+    if (A[(size_t)p * n + k] == 0.0) return false;
+    if (p != k) {
+      for (int j = 0; j < n; ++j) std::swap(A[(size_t)k * n + j], A[(size_t)p * n + j]);
+      std::swap(b[(size_t)k], b[(size_t)p]);
+    }
+    for (int i = k + 1; i < n; ++i) {
+      const double l = A[(size_t)i * n + k] / A[(size_t)k * n + k];
+      for (int j = k; j < n; ++j) A[(size_t)i * n + j] -= l * A[(size_t)k * n + j];
+      b[(size_t)i] -= l * b[(size_t)k];
+    }
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double acc = b[(size_t)i];
+    for (int j = i + 1; j < n; ++j) acc -= A[(size_t)i * n + j] * b[(size_t)j];
+    b[(size_t)i] = acc / A[(size_t)i * n + i];
+  }
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k, double *Phi,
+                       double *sigma, int *k_out, hydro_stream_t stream) {
+  if (!S || ns <= 0 || ns > 4096 || N <= 0 || !(eps > 0.0 && eps <= 1.0) || max_k <= 0 || !Phi ||
+      !k_out)
+    return HYDRO_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int chunks = (int)std::min<int64_t>(hk::GRAM_CHUNKS, (N + hk::GRAM_KT - 1) / hk::GRAM_KT);
+  const int64_t chunk = (N + chunks - 1) / chunks;
+  const int tiles = (ns + hk::GRAM_T - 1) / hk::GRAM_T;
+  double *part = nullptr, *G = nullptr, *W = nullptr;
+  hydro_status st = HYDRO_OK;
+  auto cleanup = [&]() { cudaFree(part); cudaFree(G); cudaFree(W); };
+  if (cudaMalloc(&part, sizeof(double) * (size_t)chunks * ns * ns) != cudaSuccess ||
+      cudaMalloc(&G, sizeof(double) * (size_t)ns * ns) != cudaSuccess) {
+    cleanup();
+    return HYDRO_ERR_CUDA;
+  }
+  // G = S S^T (the snapshot Gram matrix; S holds one snapshot per row)
+  hk::gram_partial_kernel<<<dim3((unsigned)chunks, (unsigned)tiles, (unsigned)tiles), hk::GRAM_T * hk::GRAM_T, 0, s>>>(
+      ns, N, chunk, S, part);
+  hk::gram_reduce_kernel<<<(ns * ns + 255) / 256, 256, 0, s>>>(ns, chunks, part, G);
+  g_launches += 2;
+  std::vector<double> hG((size_t)ns * ns), lam, V;
+  if (cudaGetLastError() != cudaSuccess ||
+      cudaMemcpyAsync(hG.data(), G, sizeof(double) * hG.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess) {
+    cleanup();
+    return HYDRO_ERR_CUDA;
+  }
+  // G = V Lambda V^T; singular values of S^T: sigma = sqrt(lambda)
+  sym_eig_host(ns, hG, lam, V);
+  std::vector<double> sg((size_t)ns);
+  double tot = 0.0;
+  for (int i = 0; i < ns; ++i) { sg[(size_t)i] = std::sqrt(std::max(lam[(size_t)i], 0.0)); tot += sg[(size_t)i]; }
+  if (sigma) std::copy(sg.begin(), sg.end(), sigma);
+  // energy criterion: the smallest k with sum_{i<=k} sigma_i / sum sigma_i >= eps
+  int k = ns;
+  double run = 0.0;
+  for (int i = 0; i < ns; ++i) {
+    run += sg[(size_t)i];
+    if (tot > 0.0 && run / tot >= eps) { k = i + 1; break; }
+  }
+  if (k > max_k) k = max_k;
+  while (k > 0 && !(sg[(size_t)k - 1] > 0.0)) --k;
+  *k_out = k;
+  if (k == 0) { cleanup(); return HYDRO_OK; }
+  // Phi = S^T V_k Sigma_k^-1  ([N][k]; the left singular vectors)
+  std::vector<double> hW((size_t)ns * k);
+  for (int j = 0; j < ns; ++j)
+    for (int c = 0; c < k; ++c) hW[(size_t)j * k + c] = V[(size_t)j * ns + c] / sg[(size_t)c];
+  if (cudaMalloc(&W, sizeof(double) * hW.size()) != cudaSuccess ||
+      cudaMemcpyAsync(W, hW.data(), sizeof(double) * hW.size(), cudaMemcpyHostToDevice, s) != cudaSuccess) {
+    cleanup();
+    return HYDRO_ERR_CUDA;
+  }
+  hk::snapshot_combine_kernel<<<blocks_for(N, 128), 128, 0, s>>>(ns, N, k, max_k, S, W, Phi);
+  g_launches++;
+  if (cudaGetLastError() != cudaSuccess) { cleanup(); return HYDRO_ERR_CUDA; }
+  // One CholQR pass: the Gram route leaves Phi orthonormal only to ~eps (sigma_1/sigma_k)^2;
+  // Phi <- Phi R^-1 with R^T R = Phi^T Phi restores it to rounding (same span).
+  {
+    double *P2 = nullptr, *Rinv = nullptr, *Tmp = nullptr;
+    const int ch = (int)std::min<int64_t>(hk::GRAM_CHUNKS, N);
+    const int64_t chs = (N + ch - 1) / ch;
+    bool ok = cudaMalloc(&P2, sizeof(double) * (size_t)ch * k * k) == cudaSuccess &&
+              cudaMalloc(&Rinv, sizeof(double) * (size_t)k * k) == cudaSuccess &&
+              cudaMalloc(&Tmp, sizeof(double) * (size_t)N * k) == cudaSuccess;
+    std::vector<double> hP((size_t)ch * k * k);
+    if (ok) {
+      hk::gram_cols_partial_kernel<<<ch, 256, 0, s>>>(N, k, max_k, chs, Phi, P2);
+      g_launches++;
+      ok = cudaGetLastError() == cudaSuccess &&
+           cudaMemcpyAsync(hP.data(), P2, sizeof(double) * hP.size(), cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+           cudaStreamSynchronize(s) == cudaSuccess;
+    }
+    std::vector<double> C((size_t)k * k, 0.0), Ri((size_t)k * k, 0.0);
+    if (ok) {
+      for (int c0 = 0; c0 < ch; ++c0)  // fixed-order chunk sum, upper triangle
+        for (int i = 0; i < k; ++i)
+          for (int j = i; j < k; ++j) C[(size_t)i * k + j] += hP[((size_t)c0 * k + i) * k + j];
+      // upper Cholesky R (C = R^T R), then R^-1 by back substitution
+      std::vector<double> R((size_t)k * k, 0.0);
+      for (int i = 0; i < k && ok; ++i) {
+        double d = C[(size_t)i * k + i];
+        for (int p = 0; p < i; ++p) d -= R[(size_t)p * k + i] * R[(size_t)p * k + i];
+        if (!(d > 0.0)) { ok = false; break; }
+        R[(size_t)i * k + i] = std::sqrt(d);
+        for (int j = i + 1; j < k; ++j) {
+          double v = C[(size_t)i * k + j];
+          for (int p = 0; p < i; ++p) v -= R[(size_t)p * k + i] * R[(size_t)p * k + j];
+          R[(size_t)i * k + j] = v / R[(size_t)i * k + i];
+        }
+      }
+      for (int c = 0; c < k && ok; ++c) {  // column c of R^-1: R x = e_c
+        for (int i = c; i >= 0; --i) {
+          double v = (i == c) ? 1.0 : 0.0;
+          for (int j = i + 1; j <= c; ++j) v -= R[(size_t)i * k + j] * Ri[(size_t)j * k + c];
+          Ri[(size_t)i * k + c] = v / R[(size_t)i * k + i];
+        }
+      }
+    }
+    if (ok) {
+      ok = cudaMemcpyAsync(Rinv, Ri.data(), sizeof(double) * Ri.size(), cudaMemcpyHostToDevice, s) == cudaSuccess;
+      hk::right_mult_kernel<<<blocks_for(N, 128), 128, 0, s>>>(N, k, max_k, Rinv, Tmp, Phi);
+      g_launches++;
+      ok = ok && cudaGetLastError() == cudaSuccess && cudaStreamSynchronize(s) == cudaSuccess;
+    }
+    cudaFree(P2); cudaFree(Rinv); cudaFree(Tmp);
+    if (!ok) st = HYDRO_ERR_CUDA;
+  }
+  cleanup();
+  return st;
+}
+
+hydro_status hydro_deim(const double *U, int64_t N, int m, int64_t *idx, hydro_stream_t stream) {
+  if (!U || N <= 0 || m <= 0 || m > N || m > 4096 || !idx) return HYDRO_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  double *c = nullptr, *bval = nullptr;
+  int64_t *bidx = nullptr;
+  auto cleanup = [&]() { cudaFree(c); cudaFree(bval); cudaFree(bidx); };
+  if (cudaMalloc(&c, sizeof(double) * (size_t)m) != cudaSuccess ||
+      cudaMalloc(&bval, sizeof(double) * hk::DEIM_BLOCKS) != cudaSuccess ||
+      cudaMalloc(&bidx, sizeof(int64_t) * hk::DEIM_BLOCKS) != cudaSuccess) {
+    cleanup();
+    return HYDRO_ERR_CUDA;
+  }
+  std::vector<double> rows((size_t)m * m), hv(hk::DEIM_BLOCKS), hc((size_t)m);
+  std::vector<int64_t> hi(hk::DEIM_BLOCKS);
+  hydro_status st = HYDRO_OK;
+  for (int j = 0; j < m; ++j) {
+    if (j > 0) {  // c = (P^T U_{<j})^-1 P^T u_j
+      std::vector<double> A((size_t)j * j), b((size_t)j);
+      for (int a = 0; a < j; ++a) {
+        for (int q = 0; q < j; ++q) A[(size_t)a * j + q] = rows[(size_t)a * m + q];
+        b[(size_t)a] = rows[(size_t)a * m + j];
+      }
+      if (!lu_solve_host(j, A, b)) { st = HYDRO_ERR_NONFINITE; break; }
+      std::copy(b.begin(), b.end(), hc.begin());
+      if (cudaMemcpyAsync(c, hc.data(), sizeof(double) * j, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+        st = HYDRO_ERR_CUDA;
+        break;
+      }
+    }
+    hk::deim_residual_kernel<<<hk::DEIM_BLOCKS, hk::DEIM_THREADS, 0, s>>>(N, m, j, U, c, bval, bidx);
+    g_launches++;
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(hv.data(), bval, sizeof(double) * hk::DEIM_BLOCKS, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(hi.data(), bidx, sizeof(int64_t) * hk::DEIM_BLOCKS, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+      st = HYDRO_ERR_CUDA;
+      break;
+    }
+    double best = -1.0;
+    int64_t p = -1;
+    for (int q = 0; q < hk::DEIM_BLOCKS; ++q)  // blocks cover ascending row ranges
+      if (hi[(size_t)q] >= 0 && hv[(size_t)q] > best) { best = hv[(size_t)q]; p = hi[(size_t)q]; }
+    if (p < 0) { st = HYDRO_ERR_NONFINITE; break; }
+    idx[j] = p;
+    if (cudaMemcpyAsync(rows.data() + (size_t)j * m, U + p * m, sizeof(double) * m, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+      st = HYDRO_ERR_CUDA;
+      break;
+    }
+  }
+  cleanup();
   return st;
 }
 

@@ -1,0 +1,145 @@
+// offline.cuh -- the ROM offline phase on the GPU (PAPER Sec. 4.3-4.5,
+// P:908-1051): the snapshot Gram matrix for POD by the method of snapshots, the basis
+// formation Phi = S^T V Sigma^-1, and the greedy DEIM index selection (Algorithm 1 of
+// Chaturantabut-Sorensen, as described at P:1003-1016).  All reductions are fixed-order
+// (split over fixed row chunks, then a fixed-order sum), so results are run-to-run
+// deterministic.  The small dense pieces (the ns x ns eigenproblem, the j x j DEIM solves)
+// run on the host in hydro_api.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hk {
+
+constexpr int GRAM_T = 16;        // output tile (GRAM_T x GRAM_T per block)
+constexpr int GRAM_KT = 64;       // rows staged per smem tile
+constexpr int GRAM_CHUNKS = 148 * 2;
+
+// partial[c][i][j] = sum over rows k of chunk c of S[i][k] S[j][k]  (S: [ns][N] row-major),
+// for the upper-triangle tile (blockIdx.y, blockIdx.z) with tile_i <= tile_j.
+__global__ void __launch_bounds__(GRAM_T *GRAM_T) gram_partial_kernel(
+    int ns, int64_t N, int64_t chunk, const double *__restrict__ S, double *__restrict__ partial) {
+  const int ti = blockIdx.y, tj = blockIdx.z;
+  if (ti > tj) return;
+  __shared__ double si[GRAM_T][GRAM_KT + 1], sj[GRAM_T][GRAM_KT + 1];
+  const int tx = threadIdx.x % GRAM_T, ty = threadIdx.x / GRAM_T;
+  const int i = ti * GRAM_T + ty, j = tj * GRAM_T + tx;
+  const int64_t k0 = (int64_t)blockIdx.x * chunk;
+  const int64_t k1 = k0 + chunk < N ? k0 + chunk : N;
+  double acc = 0.0;
+  for (int64_t kb = k0; kb < k1; kb += GRAM_KT) {
+    for (int t = threadIdx.x; t < GRAM_T * GRAM_KT; t += GRAM_T * GRAM_T) {
+      const int r = t / GRAM_KT, kk = t % GRAM_KT;
+      const int64_t k = kb + kk;
+      const int ri = ti * GRAM_T + r, rj = tj * GRAM_T + r;
+      si[r][kk] = (ri < ns && k < k1) ? S[(int64_t)ri * N + k] : 0.0;
+      sj[r][kk] = (rj < ns && k < k1) ? S[(int64_t)rj * N + k] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < GRAM_KT; ++kk) acc = __fma_rn(si[ty][kk], sj[tx][kk], acc);
+    __syncthreads();
+  }
+  if (i < ns && j < ns) partial[((int64_t)blockIdx.x * ns + i) * ns + j] = acc;
+}
+
+// G[i][j] = G[j][i] = sum over chunks (ascending) of partial[c][min][max]
+__global__ void gram_reduce_kernel(int ns, int chunks, const double *__restrict__ partial,
+                                   double *__restrict__ G) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ns * ns) return;
+  int i = t / ns, j = t % ns;
+  if (i > j) { const int x = i; i = j; j = x; }
+  double acc = 0.0;
+  for (int c = 0; c < chunks; ++c) acc += partial[((int64_t)c * ns + i) * ns + j];
+  G[t] = acc;
+}
+
+// Phi[r][c] = sum_j S[j][r] W[j][c]  (S: [ns][N], W: [ns][k], Phi: [N][ldp], c < k); one
+// thread per row r, output columns in groups of 8 registers.
+__global__ void snapshot_combine_kernel(int ns, int64_t N, int k, int ldp, const double *__restrict__ S,
+                                        const double *__restrict__ W, double *__restrict__ Phi) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  for (int c0 = 0; c0 < k; c0 += 8) {
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    for (int j = 0; j < ns; ++j) {
+      const double sv = S[(int64_t)j * N + r];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (c0 + q < k) acc[q] = __fma_rn(sv, W[j * k + c0 + q], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (c0 + q < k) Phi[r * ldp + c0 + q] = acc[q];
+  }
+}
+
+// Column Gram of a row-major basis: partial[c][i][j] = sum over rows r of chunk c of
+// Phi[r][i] Phi[r][j] (i <= j; Phi: [N][ldp], k columns), one block per chunk.
+__global__ void gram_cols_partial_kernel(int64_t N, int k, int ldp, int64_t chunk,
+                                         const double *__restrict__ Phi, double *__restrict__ partial) {
+  const int64_t r0 = (int64_t)blockIdx.x * chunk;
+  const int64_t r1 = r0 + chunk < N ? r0 + chunk : N;
+  for (int pq = threadIdx.x; pq < k * k; pq += blockDim.x) {
+    const int i = pq / k, j = pq % k;
+    double acc = 0.0;
+    if (i <= j)
+      for (int64_t r = r0; r < r1; ++r) acc = __fma_rn(Phi[r * ldp + i], Phi[r * ldp + j], acc);
+    partial[((int64_t)blockIdx.x * k + i) * k + j] = acc;
+  }
+}
+
+// Phi[r][:k] <- Phi[r][:k] R^{-1} (Rinv: [k][k] upper triangular), one thread per row;
+// the row is first copied to Tmp so the update can be done in place.
+__global__ void right_mult_kernel(int64_t N, int k, int ldp, const double *__restrict__ Rinv,
+                                  double *__restrict__ Tmp, double *__restrict__ Phi) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  double *row = Phi + r * ldp, *t = Tmp + r * k;
+  for (int j = 0; j < k; ++j) t[j] = row[j];
+  for (int c = 0; c < k; ++c) {
+    double acc = 0.0;
+    for (int j = 0; j <= c; ++j) acc = __fma_rn(t[j], Rinv[j * k + c], acc);
+    row[c] = acc;
+  }
+}
+
+// DEIM residual of basis column j: res[r] = U[r][j] - sum_{i<j} U[r][i] c[i]  (U: [N][m]),
+// with per-block argmax of |res| (ties: lowest row) written to (bval, bidx).
+constexpr int DEIM_BLOCKS = 148 * 4, DEIM_THREADS = 256;
+__global__ void __launch_bounds__(DEIM_THREADS) deim_residual_kernel(
+    int64_t N, int m, int j, const double *__restrict__ U, const double *__restrict__ c,
+    double *__restrict__ bval, int64_t *__restrict__ bidx) {
+  __shared__ double sv[DEIM_THREADS];
+  __shared__ int64_t si[DEIM_THREADS];
+  const int64_t chunk = (N + DEIM_BLOCKS - 1) / DEIM_BLOCKS;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < N ? lo + chunk : N;
+  double best = -1.0;
+  int64_t bi = -1;
+  for (int64_t r = lo + threadIdx.x; r < hi; r += DEIM_THREADS) {
+    const double *row = U + r * m;
+    double acc = 0.0;
+    for (int i = 0; i < j; ++i) acc = __fma_rn(row[i], c[i], acc);
+    const double v = fabs(row[j] - acc);
+    if (v > best) { best = v; bi = r; }   // ascending r per thread: first maximum kept
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int w = DEIM_THREADS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const double a = sv[threadIdx.x], b = sv[threadIdx.x + w];
+      const int64_t ia = si[threadIdx.x], ib = si[threadIdx.x + w];
+      if (b > a || (b == a && ib >= 0 && (ia < 0 || ib < ia))) { sv[threadIdx.x] = b; si[threadIdx.x] = ib; }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { bval[blockIdx.x] = sv[0]; bidx[blockIdx.x] = si[0]; }
+}
+
+}  // namespace hk

@@ -33,6 +33,7 @@ EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy"
             "hydro_profile_release_captured", "hydro_selftest_ieee_fast",
             "hydro_fom_create", "hydro_fom_destroy", "hydro_mass_v_apply", "hydro_mass_v_solve",
             "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_fom_advance", "hydro_rom_advance", "hydro_rom_create",
+            "hydro_fom_stage_state", "hydro_pod", "hydro_deim",
             "hydro_rom_destroy", "hydro_rom_rk2avg_step", "hydro_force_stress_bytes",
             "hydro_force_full_store", "hydro_force_transpose", "hydro_sample_stress_bytes",
             "hydro_force_sampled_store", "hydro_sample_force_transpose"]
@@ -107,6 +108,10 @@ def lib() -> ctypes.CDLL:
                                        vp, ctypes.POINTER(vp)]
         L.hydro_rom_destroy.argtypes = [vp]
         L.hydro_rom_rk2avg_step.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, vp, vp, vp]
+        L.hydro_fom_stage_state.argtypes = [vp, vp, vp, vp, vp]
+        L.hydro_pod.argtypes = [vp, i32, i64, dbl, i32, vp, ctypes.POINTER(dbl),
+                                ctypes.POINTER(i32), vp]
+        L.hydro_deim.argtypes = [vp, i64, i32, ctypes.POINTER(i64), vp]
         L.hydro_rom_advance.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, _DtCtrl, dbl, dbl,
                                         ctypes.POINTER(dbl), i32, ctypes.POINTER(dbl),
                                         ctypes.POINTER(i32), ctypes.POINTER(i32),
@@ -426,6 +431,30 @@ def rom_windowed_advance(windows, Yx, Yv, Ye, gamma, visc: Visc, cfl: Cfl, t0: f
     return Yx, Yv, Ye, tB, h, stats
 
 
+def pod(S: torch.Tensor, eps: float = 0.9999, max_k: Optional[int] = None, stream=None):
+    """POD basis of the snapshots S (device [ns][N], one snapshot per row): (Phi [N][k],
+    sigma [ns] numpy) -- hydro_pod (energy criterion of P:955-963)."""
+    import numpy as _np
+    ns, N = S.shape
+    max_k = ns if max_k is None else max_k
+    S = S.contiguous()
+    Phi = torch.empty((N, max_k), dtype=torch.float64, device=S.device)
+    sig = (ctypes.c_double * ns)()
+    k = ctypes.c_int(0)
+    _check(lib().hydro_pod(_ptr(S), ns, N, eps, max_k, _ptr(Phi), sig, ctypes.byref(k),
+                           _stream(stream)), "hydro_pod")
+    return Phi[:, :k.value].contiguous(), _np.array(sig[:])
+
+
+def deim(U: torch.Tensor, stream=None):
+    """Greedy DEIM indices (numpy int64 [m]) of the basis U (device [N][m]) -- hydro_deim."""
+    import numpy as _np
+    N, m = U.shape
+    idx = (ctypes.c_int64 * m)()
+    _check(lib().hydro_deim(_ptr(U.contiguous()), N, m, idx, _stream(stream)), "hydro_deim")
+    return _np.array(idx[:], dtype=_np.int64)
+
+
 def rom_project_workspace(n: int, s_rows: int, B: int, device="cuda") -> torch.Tensor:
     nb = lib().hydro_rom_project_workspace_bytes(n, s_rows, B)
     return torch.empty(max(nb, 8), dtype=torch.uint8, device=device)
@@ -497,6 +526,11 @@ class Fom:
                                        dt, cg_tol, cg_max_iter, ctypes.byref(d), ctypes.byref(it),
                                        _stream(stream)), "hydro_rk2avg_step")
         return d.value, it.value
+
+    def stage_state(self, x_half=None, v_half=None, e_half=None, stream=None):
+        """Copy the last step's half-stage state (x, v, e)^{n+1/2} into the given tensors."""
+        _check(lib().hydro_fom_stage_state(self._h, _ptr(x_half), _ptr(v_half), _ptr(e_half),
+                                           _stream(stream)), "hydro_fom_stage_state")
 
     def advance(self, x, v, e, gamma, visc: Visc, cfl: Cfl, t0: float, t_final: float, dt: float,
                 ctrl: DtCtrl = DtCtrl(), max_steps=1000000, cg_tol=1e-12, cg_max_iter=500,

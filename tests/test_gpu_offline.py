@@ -1,0 +1,98 @@
+"""GPU parity of the ROM offline phase against
+oracle/offline.py: POD by the method of snapshots (hydro_pod) against a library SVD, greedy
+DEIM (hydro_deim) index for index, and the pipeline FOM snapshots (incl. the half stages,
+P:921-943) -> POD velocity basis -> SNS force basis M_V Phi_v -> DEIM indices.
+Tolerances: the Gram route squares the condition number, so a singular value sigma_i is
+compared to 1e-13 sigma_1^2 / sigma_i + 1e-12 sigma_i and basis columns only where sigma_i is
+well separated; DEIM indices exactly."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from tests import gpu_helpers as H  # noqa: E402
+from paper_2104_11404_b200 import hydro  # noqa: E402
+from oracle import offline as ooff  # noqa: E402
+from oracle import fom as ofom  # noqa: E402
+
+
+def _sig_close(sg, so):
+    tol = 1e-13 * so[0] ** 2 / np.maximum(so, 1e-300) + 1e-12 * so
+    assert np.all(np.abs(sg - so) <= tol), np.max(np.abs(sg - so) / tol)
+
+
+def test_pod_known_svd_matches_oracle():
+    rng = np.random.default_rng(10)
+    N, ns = 100_003, 24
+    Q1, _ = np.linalg.qr(rng.standard_normal((N, ns)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((ns, ns)))
+    s = np.array([3.0 / 1.6 ** i for i in range(ns)])
+    S = np.ascontiguousarray(((Q1 * s) @ Q2.T).T)
+    for eps in (0.9, 0.9999):
+        Phi_g, sg = hydro.pod(H.dev(S), eps=eps)
+        Phi_o, so = ooff.pod(S, eps=eps)
+        assert Phi_g.shape == Phi_o.shape
+        _sig_close(sg, so)
+        Pg = Phi_g.cpu().numpy()
+        k = Pg.shape[1]
+        np.testing.assert_allclose(Pg.T @ Pg, np.eye(k), atol=1e-9)
+        good = so[:k] >= 1e-3 * so[0]
+        np.testing.assert_allclose(Pg[:, good], Phi_o[:, good], atol=1e-8)
+
+
+@pytest.mark.parametrize("N,m", [(50_000, 20), (7, 7), (1_000, 1)])
+def test_deim_matches_oracle(N, m):
+    rng = np.random.default_rng(11 + m)
+    U, _ = np.linalg.qr(rng.standard_normal((N, m)))
+    U = np.ascontiguousarray(U)
+    np.testing.assert_array_equal(hydro.deim(H.dev(U)), ooff.deim(U))
+
+
+def test_fom_snapshots_pod_sns_deim_pipeline():
+    prob = W.sedov_like(41, 2, (9, 7), (0.0, 0.0), (0.9, 0.7), delta=0.08, e_floor=1e-2,
+                        vmode="uniform", vscale=0.1, name="offline")
+    rng = np.random.default_rng(41)
+    prob.e[:] = 1.0 + 0.5 * rng.random(prob.e.shape)
+    m = prob.mesh
+    bc = ofom.bc_dofs_box(m)
+    prob.v.reshape(-1)[bc] = 0.0
+    ctx = H.context(prob)
+    f = hydro.Fom(ctx, bc)
+    x, v, e, g = H.dev(prob.x), H.dev(prob.v), H.dev(prob.e), H.dev(prob.gamma)
+    visc, cfl = hydro.Visc(prob.q1, prob.q2, prob.visc), hydro.Cfl(prob.alpha, prob.alpha_mu)
+    import oracle
+    dt = 0.2 * oracle.force(prob)["dt"]
+    v_os = v.clone()
+    snaps = []
+    vh = torch.empty_like(v)
+    for _ in range(6):   # snapshots: every half stage and every full step
+        f.step(x, v, e, g, visc, cfl, dt, cg_tol=1e-14, cg_max_iter=2000)
+        f.stage_state(v_half=vh)
+        snaps += [(vh - v_os).reshape(-1).clone(), (v - v_os).reshape(-1).clone()]
+    S = torch.stack(snaps).contiguous()          # [ns][N_V]
+    Phi_g, sg = hydro.pod(S, eps=0.9999)
+    Phi_o, so = ooff.pod(S.cpu().numpy(), eps=0.9999)
+    assert Phi_g.shape == Phi_o.shape
+    _sig_close(sg, so)
+    k = Phi_g.shape[1]
+    # SNS: the force basis is M_V Phi_v, column by column through the device mass
+    # operator, against the oracle's assembled M_V on the oracle basis
+    MV = ofom.mass_v(m)
+    F_g = torch.stack([f.mass_v(Phi_g[:, c].contiguous().reshape(m.dim, m.n_nodes)).reshape(-1)
+                       for c in range(k)], dim=1).contiguous()
+    F_o = np.stack([np.concatenate([MV @ Phi_o[c0 * m.n_nodes:(c0 + 1) * m.n_nodes, c]
+                                    for c0 in range(m.dim)]) for c in range(k)], axis=1)
+    good = so[:k] >= 1e-3 * so[0]
+    np.testing.assert_allclose(F_g.cpu().numpy()[:, good], F_o[:, good],
+                               atol=1e-8 * np.abs(F_o).max())
+    # DEIM on the SNS basis: the same sampled rows (restricted to the well-separated modes)
+    kk = int(good.sum())
+    np.testing.assert_array_equal(hydro.deim(F_g[:, :kk].contiguous()),
+                                  ooff.deim(np.ascontiguousarray(F_o[:, :kk])))

@@ -1,0 +1,76 @@
+"""Pins of the offline-phase oracle (oracle/offline.py) against what the
+paper and the mathematics fix, independently of its own formulas:
+
+P26 POD of snapshots with a known SVD (S^T = Q1 diag(s) Q2^T from random orthogonal factors):
+    the singular values are s, the energy criterion picks the closed-form k for thresholds on
+    either side of each partial sum, and the basis spans Q1's leading columns;
+P27 the POD basis is orthonormal and reproduces every snapshot of an exactly rank-r set;
+P28 DEIM on a permuted identity basis returns the permutation (each column's only nonzero);
+P29 the DEIM interpolation property: f in span(U) is reproduced exactly from its sampled
+    rows, U (P^T U)^-1 P^T f = f, and the indices are distinct;
+P30 the first DEIM index is the position of the largest |u_1| entry (Algorithm 1, step 1).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import offline
+
+
+def _known_svd(N=300, ns=12, seed=0):
+    rng = np.random.default_rng(seed)
+    Q1, _ = np.linalg.qr(rng.standard_normal((N, ns)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((ns, ns)))
+    s = np.array([10.0 / 2 ** i for i in range(ns)])
+    return (Q1 * s) @ Q2.T, Q1, s   # S^T [N][ns]
+
+
+def test_P26_pod_known_svd_and_energy_criterion():
+    St, Q1, s = _known_svd()
+    S = np.ascontiguousarray(St.T)
+    Phi, sig = offline.pod(S, eps=1.0)
+    np.testing.assert_allclose(sig, s, rtol=1e-12)
+    part = np.cumsum(s) / s.sum()
+    for k in (1, 3, 6):
+        # a threshold just below the k-th partial sum selects k, just above selects k + 1
+        assert offline.pod(S, eps=part[k - 1] - 1e-12)[0].shape[1] == k
+        assert offline.pod(S, eps=part[k - 1] + 1e-12)[0].shape[1] == k + 1
+    Phi, _ = offline.pod(S, eps=part[4] - 1e-12)
+    P1 = Q1[:, :5] @ Q1[:, :5].T
+    np.testing.assert_allclose(Phi @ Phi.T, P1, atol=1e-12)
+
+
+def test_P27_pod_orthonormal_and_reproduces_rank_r():
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((500, 4))
+    S = np.ascontiguousarray((A @ rng.standard_normal((4, 9))).T)   # 9 snapshots of rank 4
+    Phi, sig = offline.pod(S, eps=1.0 - 1e-14, max_k=4)
+    assert Phi.shape[1] == 4
+    np.testing.assert_allclose(Phi.T @ Phi, np.eye(4), atol=1e-13)
+    np.testing.assert_allclose(Phi @ (Phi.T @ S.T), S.T, atol=1e-11 * np.abs(S).max())
+    assert sig[4:].max() <= 1e-12 * sig[0]
+
+
+def test_P28_deim_permutation_basis():
+    rng = np.random.default_rng(2)
+    N, m = 40, 7
+    perm = rng.permutation(N)[:m]
+    U = np.zeros((N, m))
+    U[perm, np.arange(m)] = rng.uniform(0.5, 2.0, m)
+    np.testing.assert_array_equal(offline.deim(U), perm)
+
+
+def test_P29_deim_interpolates_span():
+    rng = np.random.default_rng(3)
+    U, _ = np.linalg.qr(rng.standard_normal((200, 9)))
+    p = offline.deim(U)
+    assert len(set(p.tolist())) == 9
+    f = U @ rng.standard_normal(9)
+    rec = U @ np.linalg.solve(U[p], f[p])
+    np.testing.assert_allclose(rec, f, atol=1e-12)
+
+
+def test_P30_deim_first_index():
+    rng = np.random.default_rng(4)
+    U = rng.standard_normal((100, 5))
+    assert offline.deim(U)[0] == int(np.argmax(np.abs(U[:, 0])))
