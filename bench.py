@@ -213,6 +213,7 @@ def run_ours(args, rank, world):
         results[name] = bench_one(name, args, dev, flush, rank, world)
     if args.all:
         results["fom_c2"] = bench_fom("c2", args, dev)
+        results["offline_c2"] = bench_offline(args, dev)
     return results
 
 
@@ -595,6 +596,49 @@ def bench_fom(name, args, dev):
             "rel_energy_drift": abs(E1 - E0) / E0, "status": st[0],
             "what": "RK2-average step (PAPER P:463-508): 2 force evaluations storing S_q + 2 "
                     "F^T w passes from S_q, 2 PCG solves of M_V, 2 M_E block solves, v.n=0"}
+
+
+def bench_offline(args, dev, ns=64, m=40):
+    """SURVEY 8(f) NEXT-3 on C2-sized vectors (N = 3 * 129^3 velocity dofs): POD of ns seeded
+    synthetic snapshots (hydro_pod: Gram + host eigen + basis + CholQR) and greedy DEIM of an
+    m-column basis (hydro_deim), wall time per call with CUDA events (both synchronise)."""
+    import torch
+    from paper_2104_11404_b200 import hydro
+    N = 3 * 129 ** 3
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(2104)
+    # low-rank-plus-noise snapshots, so the energy criterion selects a nontrivial k
+    A = torch.randn((ns, 24), generator=gen, device=dev, dtype=torch.float64)
+    Bm = torch.randn((24, N), generator=gen, device=dev, dtype=torch.float64)
+    S = A @ Bm    # (input generation only)
+    S += 1e-3 * torch.randn((ns, N), generator=gen, device=dev, dtype=torch.float64)
+    del Bm
+    hydro.pod(S, eps=0.9999)    # warm-up
+    t = []
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        Phi, sig = hydro.pod(S, eps=0.9999)
+        b.record()
+        torch.cuda.synchronize()
+        t.append(a.elapsed_time(b))
+    pod_ms = float(np.median(t))
+    U = Phi[:, :m].contiguous() if Phi.shape[1] >= m else torch.linalg.qr(
+        torch.randn((N, m), generator=gen, device=dev, dtype=torch.float64))[0].contiguous()
+    del S
+    hydro.deim(U)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    idx = hydro.deim(U)
+    b.record()
+    torch.cuda.synchronize()
+    deim_ms = a.elapsed_time(b)
+    gram_flop = 2.0 * ns * ns * N / 2
+    return {"workload": "offline_c2", "N": N, "snapshots": ns, "pod_ms": pod_ms,
+            "pod_k": int(Phi.shape[1]), "gram_tflops": gram_flop / (pod_ms * 1e-3) / 1e12,
+            "deim_ms": deim_ms, "deim_m": m, "deim_distinct": int(len(set(idx.tolist()))),
+            "what": "POD (method of snapshots, energy criterion 0.9999, CholQR) of seeded "
+                    "low-rank+noise snapshots and greedy DEIM (P:908-1016)"}
 
 
 def _rotations_per_lmin3(name, prob):

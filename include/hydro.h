@@ -289,7 +289,7 @@ hydro_status hydro_fom_stage_state(hydro_fom *fom, double *x_half, double *v_hal
  * offsets already subtracted) by the method of snapshots: the Gram matrix S S^T on the GPU
  * (fixed-order split-K), its symmetric eigen-decomposition on the host (cyclic Jacobi,
  * ns x ns), sigma_i = sqrt(lambda_i), the energy criterion sum_{i<=k} sigma_i / sum sigma_i
- * >= eps (paper default 0.9999) with k <= max_k, and the basis
+ * >= eps (paper default 0.9999) with k <= max_k <= 128, and the basis
  * Phi = S^T V_k Sigma_k^-1 on the GPU followed by one CholQR pass (Phi <- Phi R^-1,
  * R^T R = Phi^T Phi: the Gram route alone is orthonormal only to ~eps (sigma_1/sigma_k)^2)
  * (device out [N][max_k] row-major, first k columns written; column c has the sign that

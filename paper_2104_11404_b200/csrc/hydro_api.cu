@@ -1628,8 +1628,8 @@ extern "C" {
 
 hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k, double *Phi,
                        double *sigma, int *k_out, hydro_stream_t stream) {
-  if (!S || ns <= 0 || ns > 4096 || N <= 0 || !(eps > 0.0 && eps <= 1.0) || max_k <= 0 || !Phi ||
-      !k_out)
+  if (!S || ns <= 0 || ns > 4096 || N <= 0 || !(eps > 0.0 && eps <= 1.0) || max_k <= 0 ||
+      max_k > hk::POD_MAXK || !Phi || !k_out)
     return HYDRO_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const int chunks = (int)std::min<int64_t>(hk::GRAM_CHUNKS, (N + hk::GRAM_KT - 1) / hk::GRAM_KT);
@@ -1645,7 +1645,7 @@ hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k
   }
   // G = S S^T (the snapshot Gram matrix; S holds one snapshot per row)
   hk::gram_partial_kernel<<<dim3((unsigned)chunks, (unsigned)tiles, (unsigned)tiles), hk::GRAM_T * hk::GRAM_T, 0, s>>>(
-      ns, N, chunk, S, part);
+      ns, N, chunk, N, 1, S, part);
   hk::gram_reduce_kernel<<<(ns * ns + 255) / 256, 256, 0, s>>>(ns, chunks, part, G);
   g_launches += 2;
   std::vector<double> hG((size_t)ns * ns), lam, V;
@@ -1687,25 +1687,24 @@ hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k
   // One CholQR pass: the Gram route leaves Phi orthonormal only to ~eps (sigma_1/sigma_k)^2;
   // Phi <- Phi R^-1 with R^T R = Phi^T Phi restores it to rounding (same span).
   {
-    double *P2 = nullptr, *Rinv = nullptr, *Tmp = nullptr;
-    const int ch = (int)std::min<int64_t>(hk::GRAM_CHUNKS, N);
+    double *P2 = nullptr, *Rinv = nullptr, *G2 = nullptr;
+    const int ch = (int)std::min<int64_t>(hk::GRAM_CHUNKS, (N + hk::GRAM_KT - 1) / hk::GRAM_KT);
     const int64_t chs = (N + ch - 1) / ch;
+    const int kt = (k + hk::GRAM_T - 1) / hk::GRAM_T;
     bool ok = cudaMalloc(&P2, sizeof(double) * (size_t)ch * k * k) == cudaSuccess &&
-              cudaMalloc(&Rinv, sizeof(double) * (size_t)k * k) == cudaSuccess &&
-              cudaMalloc(&Tmp, sizeof(double) * (size_t)N * k) == cudaSuccess;
-    std::vector<double> hP((size_t)ch * k * k);
-    if (ok) {
-      hk::gram_cols_partial_kernel<<<ch, 256, 0, s>>>(N, k, max_k, chs, Phi, P2);
-      g_launches++;
+              cudaMalloc(&G2, sizeof(double) * (size_t)k * k) == cudaSuccess &&
+              cudaMalloc(&Rinv, sizeof(double) * (size_t)k * k) == cudaSuccess;
+    std::vector<double> C((size_t)k * k, 0.0), Ri((size_t)k * k, 0.0);
+    if (ok) {  // Phi^T Phi: the same tiled Gram kernel on the columns of the row-major basis
+      hk::gram_partial_kernel<<<dim3((unsigned)ch, (unsigned)kt, (unsigned)kt), hk::GRAM_T * hk::GRAM_T, 0, s>>>(
+          k, N, chs, 1, max_k, Phi, P2);
+      hk::gram_reduce_kernel<<<(k * k + 255) / 256, 256, 0, s>>>(k, ch, P2, G2);
+      g_launches += 2;
       ok = cudaGetLastError() == cudaSuccess &&
-           cudaMemcpyAsync(hP.data(), P2, sizeof(double) * hP.size(), cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+           cudaMemcpyAsync(C.data(), G2, sizeof(double) * C.size(), cudaMemcpyDeviceToHost, s) == cudaSuccess &&
            cudaStreamSynchronize(s) == cudaSuccess;
     }
-    std::vector<double> C((size_t)k * k, 0.0), Ri((size_t)k * k, 0.0);
     if (ok) {
-      for (int c0 = 0; c0 < ch; ++c0)  // fixed-order chunk sum, upper triangle
-        for (int i = 0; i < k; ++i)
-          for (int j = i; j < k; ++j) C[(size_t)i * k + j] += hP[((size_t)c0 * k + i) * k + j];
       // upper Cholesky R (C = R^T R), then R^-1 by back substitution
       std::vector<double> R((size_t)k * k, 0.0);
       for (int i = 0; i < k && ok; ++i) {
@@ -1729,11 +1728,11 @@ hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k
     }
     if (ok) {
       ok = cudaMemcpyAsync(Rinv, Ri.data(), sizeof(double) * Ri.size(), cudaMemcpyHostToDevice, s) == cudaSuccess;
-      hk::right_mult_kernel<<<blocks_for(N, 128), 128, 0, s>>>(N, k, max_k, Rinv, Tmp, Phi);
+      hk::right_mult_kernel<<<blocks_for(N, 128), 128, 0, s>>>(N, k, max_k, Rinv, Phi);
       g_launches++;
       ok = ok && cudaGetLastError() == cudaSuccess && cudaStreamSynchronize(s) == cudaSuccess;
     }
-    cudaFree(P2); cudaFree(Rinv); cudaFree(Tmp);
+    cudaFree(P2); cudaFree(Rinv); cudaFree(G2);
     if (!ok) st = HYDRO_ERR_CUDA;
   }
   cleanup();

@@ -16,10 +16,13 @@ constexpr int GRAM_T = 16;        // output tile (GRAM_T x GRAM_T per block)
 constexpr int GRAM_KT = 64;       // rows staged per smem tile
 constexpr int GRAM_CHUNKS = 148 * 2;
 
-// partial[c][i][j] = sum over rows k of chunk c of S[i][k] S[j][k]  (S: [ns][N] row-major),
-// for the upper-triangle tile (blockIdx.y, blockIdx.z) with tile_i <= tile_j.
+// partial[c][i][j] = sum over k in chunk c of A(i, k) A(j, k), A(i, k) = A[i * si + k * sk]
+// (snapshots S [ns][N]: si = N, sk = 1; the columns of a row-major basis Phi [N][ldp]:
+// si = 1, sk = ldp), for the upper-triangle tile (blockIdx.y, blockIdx.z), tile_i <= tile_j.
+// The smem loader walks the unit-stride index fastest so the loads coalesce either way.
 __global__ void __launch_bounds__(GRAM_T *GRAM_T) gram_partial_kernel(
-    int ns, int64_t N, int64_t chunk, const double *__restrict__ S, double *__restrict__ partial) {
+    int ns, int64_t N, int64_t chunk, int64_t si_, int64_t sk_, const double *__restrict__ S,
+    double *__restrict__ partial) {
   const int ti = blockIdx.y, tj = blockIdx.z;
   if (ti > tj) return;
   __shared__ double si[GRAM_T][GRAM_KT + 1], sj[GRAM_T][GRAM_KT + 1];
@@ -27,14 +30,16 @@ __global__ void __launch_bounds__(GRAM_T *GRAM_T) gram_partial_kernel(
   const int i = ti * GRAM_T + ty, j = tj * GRAM_T + tx;
   const int64_t k0 = (int64_t)blockIdx.x * chunk;
   const int64_t k1 = k0 + chunk < N ? k0 + chunk : N;
+  const bool kfast = sk_ == 1;
   double acc = 0.0;
   for (int64_t kb = k0; kb < k1; kb += GRAM_KT) {
     for (int t = threadIdx.x; t < GRAM_T * GRAM_KT; t += GRAM_T * GRAM_T) {
-      const int r = t / GRAM_KT, kk = t % GRAM_KT;
+      const int r = kfast ? t / GRAM_KT : t % GRAM_T;
+      const int kk = kfast ? t % GRAM_KT : t / GRAM_T;
       const int64_t k = kb + kk;
       const int ri = ti * GRAM_T + r, rj = tj * GRAM_T + r;
-      si[r][kk] = (ri < ns && k < k1) ? S[(int64_t)ri * N + k] : 0.0;
-      sj[r][kk] = (rj < ns && k < k1) ? S[(int64_t)rj * N + k] : 0.0;
+      si[r][kk] = (ri < ns && k < k1) ? S[ri * si_ + k * sk_] : 0.0;
+      sj[r][kk] = (rj < ns && k < k1) ? S[rj * si_ + k * sk_] : 0.0;
     }
     __syncthreads();
 #pragma unroll 8
@@ -78,28 +83,16 @@ __global__ void snapshot_combine_kernel(int ns, int64_t N, int k, int ldp, const
   }
 }
 
-// Column Gram of a row-major basis: partial[c][i][j] = sum over rows r of chunk c of
-// Phi[r][i] Phi[r][j] (i <= j; Phi: [N][ldp], k columns), one block per chunk.
-__global__ void gram_cols_partial_kernel(int64_t N, int k, int ldp, int64_t chunk,
-                                         const double *__restrict__ Phi, double *__restrict__ partial) {
-  const int64_t r0 = (int64_t)blockIdx.x * chunk;
-  const int64_t r1 = r0 + chunk < N ? r0 + chunk : N;
-  for (int pq = threadIdx.x; pq < k * k; pq += blockDim.x) {
-    const int i = pq / k, j = pq % k;
-    double acc = 0.0;
-    if (i <= j)
-      for (int64_t r = r0; r < r1; ++r) acc = __fma_rn(Phi[r * ldp + i], Phi[r * ldp + j], acc);
-    partial[((int64_t)blockIdx.x * k + i) * k + j] = acc;
-  }
-}
+constexpr int POD_MAXK = 128;
 
-// Phi[r][:k] <- Phi[r][:k] R^{-1} (Rinv: [k][k] upper triangular), one thread per row;
-// the row is first copied to Tmp so the update can be done in place.
+// Phi[r][:k] <- Phi[r][:k] R^{-1} (Rinv: [k][k] upper triangular), one thread per row, the
+// row held in a per-thread array (k <= POD_MAXK).
 __global__ void right_mult_kernel(int64_t N, int k, int ldp, const double *__restrict__ Rinv,
-                                  double *__restrict__ Tmp, double *__restrict__ Phi) {
+                                  double *__restrict__ Phi) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= N) return;
-  double *row = Phi + r * ldp, *t = Tmp + r * k;
+  double t[POD_MAXK];
+  double *row = Phi + r * ldp;
   for (int j = 0; j < k; ++j) t[j] = row[j];
   for (int c = 0; c < k; ++c) {
     double acc = 0.0;

@@ -436,7 +436,7 @@ def pod(S: torch.Tensor, eps: float = 0.9999, max_k: Optional[int] = None, strea
     sigma [ns] numpy) -- hydro_pod (energy criterion of P:955-963)."""
     import numpy as _np
     ns, N = S.shape
-    max_k = ns if max_k is None else max_k
+    max_k = min(ns, 128) if max_k is None else max_k
     S = S.contiguous()
     Phi = torch.empty((N, max_k), dtype=torch.float64, device=S.device)
     sig = (ctypes.c_double * ns)()
