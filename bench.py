@@ -206,13 +206,14 @@ def run_ours(args, rank, world):
     torch.cuda.set_device(dev)
     hydro.lib()
     results = {}
-    names = [args.workload] + ([c for c in ("c0", "c2", "c3", "c4") if c != args.workload]
+    names = [args.workload] + ([c for c in ("c0", "c2", "c3", "c4", "tg") if c != args.workload]
                                if args.all else [])
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     for name in names:
         results[name] = bench_one(name, args, dev, flush, rank, world)
     if args.all:
         results["fom_c2"] = bench_fom("c2", args, dev)
+        results["fom_tg"] = bench_fom("tg", args, dev)
         results["offline_c2"] = bench_offline(args, dev)
     return results
 

@@ -378,6 +378,12 @@ def config(name: str) -> Problem:
         p = triple_point(3, (112, 48, 48))
         p.name = "c3_triple3d"
         return p
+    if name == "tg":
+        # not a BASELINE.json config: the Taylor-Green state the north star lists (SURVEY
+        # 8(f) NEXT-4), on a C2-sized 64^3 Q2/Q1 mesh of the unit cube
+        p = taylor_green(5, (64, 64, 64))
+        p.name = "tg_3d"
+        return p
     raise ValueError(name)
 
 
