@@ -83,3 +83,29 @@ def test_null_arguments_rejected_without_gpu():
     assert L.hydro_sample_create(None, None, 0, 1, None) == hydro.HYDRO_ERR_ARG
     assert L.hydro_rom_lift(10, 0, 4, None, None, 0, None, None, None) == hydro.HYDRO_ERR_ARG
     assert L.hydro_selftest_ieee_fast(1, -1, 0, 0, None, None) == hydro.HYDRO_ERR_ARG
+
+
+def test_time_loop_and_offline_arguments_rejected_without_gpu():
+    """The time loops, the offline routines and the stage-state export validate their
+    arguments before any device work: NULL objects, non-positive steps, reversed time
+    intervals, out-of-range controller constants, empty bases."""
+    import ctypes
+    from paper_2104_11404_b200 import hydro
+    L = hydro.lib()
+    ERR = hydro.HYDRO_ERR_ARG
+    visc, cfl, ctrl = hydro.Visc().c(), hydro.Cfl().c(), hydro.DtCtrl().c()
+    dt = ctypes.c_double(1e-3)
+    assert L.hydro_fom_advance(None, None, None, None, None, visc, cfl, ctrl, 0.0, 1.0,
+                               ctypes.byref(dt), 10, 1e-12, 100, None, None, None, None) == ERR
+    bad = hydro.DtCtrl(beta1=1.5).c()   # beta1 must lie in (0, 1)
+    assert L.hydro_fom_advance(None, None, None, None, None, visc, cfl, bad, 0.0, 1.0,
+                               ctypes.byref(dt), 10, 1e-12, 100, None, None, None, None) == ERR
+    h = (ctypes.c_double * 2)(1e-3, 1e-3)
+    assert L.hydro_rom_advance(None, None, None, None, None, visc, cfl, ctrl, 1.0, 0.0, h, 10,
+                               None, None, None, None, None) == ERR
+    k = ctypes.c_int(0)
+    assert L.hydro_pod(None, 4, 100, 0.9999, 4, None, None, ctypes.byref(k), None) == ERR
+    assert L.hydro_pod(None, 4, 100, 1.5, 4, None, None, ctypes.byref(k), None) == ERR
+    idx = (ctypes.c_int64 * 4)()
+    assert L.hydro_deim(None, 100, 4, idx, None) == ERR
+    assert L.hydro_fom_stage_state(None, None, None, None, None) == ERR

@@ -149,3 +149,25 @@ def test_advance_controller_matches_oracle(dim, k, shape):
     for got, want, what in ((x, xr, "x"), (v, vr, "v"), (e, er, "e")):
         g_ = got.cpu().numpy()
         assert np.abs(g_ - want).max() <= 1e-10 * max(np.abs(want).max(), 1e-300), what
+
+
+def test_advance_degenerate_intervals():
+    """t_final == t0 and max_steps == 0 take no step and leave the state bit-identical; a
+    first trial step longer than the interval lands exactly on t_final in one step."""
+    prob = _box(2, 2, (5, 4))
+    m = prob.mesh
+    bc = ofom.bc_dofs_box(m)
+    prob.v.reshape(-1)[bc] = 0.0
+    ctx = H.context(prob)
+    f = hydro.Fom(ctx, bc)
+    x, v, e, g = H.dev(prob.x), H.dev(prob.v), H.dev(prob.e), H.dev(prob.gamma)
+    visc, cfl = hydro.Visc(prob.q1, prob.q2, prob.visc), hydro.Cfl(prob.alpha, prob.alpha_mu)
+    import oracle
+    est = oracle.force(prob)["dt"]
+    assert f.advance(x, v, e, g, visc, cfl, 0.5, 0.5, est)[2:] == (0, 0)
+    assert f.advance(x, v, e, g, visc, cfl, 0.0, 1.0, est, max_steps=0)[2:] == (0, 0)
+    for got, want in ((x, prob.x), (v, prob.v), (e, prob.e)):
+        assert np.array_equal(got.cpu().numpy(), want)
+    t, h, ns, nr = f.advance(x, v, e, g, visc, cfl, 0.0, 0.05 * est, 0.5 * est)
+    assert (t, ns, nr) == (0.05 * est, 1, 0)
+    assert ctx.status_sync()[0] == 0

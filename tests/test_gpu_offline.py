@@ -96,3 +96,20 @@ def test_fom_snapshots_pod_sns_deim_pipeline():
     kk = int(good.sum())
     np.testing.assert_array_equal(hydro.deim(F_g[:, :kk].contiguous()),
                                   ooff.deim(np.ascontiguousarray(F_o[:, :kk])))
+
+
+def test_pod_degenerate_cases():
+    """One snapshot: k = 1 and Phi = s / |s| (sign: the 1x1 eigenvector is +1); a zero
+    snapshot set: k = 0; DEIM of a square orthonormal basis selects every row once."""
+    rng = np.random.default_rng(12)
+    s = rng.standard_normal(1001)
+    Phi, sig = hydro.pod(H.dev(s[None, :].copy()), eps=0.9999)
+    assert Phi.shape == (1001, 1)
+    np.testing.assert_allclose(Phi.cpu().numpy()[:, 0], s / np.linalg.norm(s), rtol=1e-13)
+    np.testing.assert_allclose(sig[0], np.linalg.norm(s), rtol=1e-13)
+    Phi0, _ = hydro.pod(H.dev(np.zeros((3, 50))), eps=0.9999)
+    assert Phi0.shape[1] == 0
+    Q, _ = np.linalg.qr(rng.standard_normal((12, 12)))
+    idx = hydro.deim(H.dev(np.ascontiguousarray(Q)))
+    assert sorted(idx.tolist()) == list(range(12))
+    np.testing.assert_array_equal(idx, ooff.deim(np.ascontiguousarray(Q)))
