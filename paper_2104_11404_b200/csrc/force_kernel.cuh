@@ -620,6 +620,14 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
 #ifndef GEN_MINB224
 #define GEN_MINB224 4
 #endif
+// ... and for the 64-thread (3D Q2) one: 14 -> 72 registers, 28 warps/SM; with the blocked
+// stages the occupancy pays for the extra spills (10/12/13/14/16 measured: profiles/ab/r01_ab30_*)
+#ifndef GEN_MINB64
+#define GEN_MINB64 14
+#endif
+#ifndef F3_COMPACT_Q3
+#define F3_COMPACT_Q3 0
+#endif
 
 // ----------------------------------------------------------------------------- tables
 // The 1D tables in __constant__ memory (filled at context creation, packed order w, B, G, Bl):
@@ -661,7 +669,7 @@ struct KCfg {
   // occupancy target.  3D Q3 (224-thread CTAs): 4 CTAs/SM at 72 registers measured best
   // (10.75 ms on C3 vs 12.0 ms at 3 CTAs / 80 registers, 11.2 ms at 5 CTAs / 56 registers:
   // occupancy outweighs the extra spills; profiles/ab/).
-  static constexpr int MINB = G::NT >= 224 ? GEN_MINB224 : (G::NT >= 128 ? 5 : 10);
+  static constexpr int MINB = G::NT >= 224 ? GEN_MINB224 : (G::NT >= 128 ? 5 : GEN_MINB64);
 };
 
 template <int MODE, bool HAS_W>
@@ -980,7 +988,9 @@ force_kernel(const Params P) {
   PointOut po;
   {
     ArithFast af;
-    pointwise<DIM, VISC, HAS_W, true, ArithFast, F3_COMPACT && DIM == 3 && K == 2>(af, J, Gv, Gw, eq, mq, gam, wq, ph, po);
+    pointwise<DIM, VISC, HAS_W, true, ArithFast,
+              DIM == 3 && ((F3_COMPACT && K == 2) || (F3_COMPACT_Q3 && K == 3))>(
+        af, J, Gv, Gw, eq, mq, gam, wq, ph, po);
     if (!af.ok) {
       // rare: some fast div/sqrt left its exact range; recompute the inputs from shared
       // memory (not kept live across the fast pass) and re-run with IEEE operators.
