@@ -11,9 +11,11 @@
  * P:864-871), sampled force evaluation ("the lifting is computed only for the
  * sampled degrees of freedom") and the least-squares projection
  * (Eq. sol-ls-hyper).  The entries of F are not written in the paper
- * (it defers to Dobrev et al. 2012); R1-R25 give the
+ * (it defers to Dobrev et al. 2012); R1-R26 give the
  * reading implemented here, and DESIGN.md "Evaluation contract" fixes the
- * operation order that makes dt bit-reproducible.
+ * operation order that makes dt bit-reproducible.  Around the hot path:
+ * the full-order RK2-average step and time loop, the ROM online step, loop
+ * and time windows and the offline POD/DEIM.
  *
  * Conventions (all entry points):
  *   - FP64 everywhere; indices int32 (element->node table) / int64 (sizes).
@@ -218,8 +220,9 @@ hydro_status hydro_fom_energy(hydro_fom *fom, const double *v, const double *e,
 /* The time-step controller of PAPER P:549-566 (defaults beta1 = 0.85, beta2 = 1.02,
  * gamma = 0.8).                                                                             */
 typedef struct { double beta1, beta2, gamma; } hydro_dt_ctrl;
-/* One RK2-average step of size dt, in place on the device state (x, v, e); four force
- * evaluations (F.1 and F^T w of each stage), two CG solves.  *dt_est (host) = the min of
+/* One RK2-average step of size dt, in place on the device state (x, v, e); per stage one
+ * force evaluation storing S_q and one transposed F^T w pass, and a CG solve of M_V started
+ * from the previous solve's solution (stopping test relative to the right-hand side).  *dt_est (host) = the min of
  * the two stages' time-step estimates for the caller's controller;
  * *cg_iters (host) = CG iterations used.  Device conditions (tangled, NaN) are reported by
  * hydro_status_sync on the context.  Synchronises `stream`.                                 */
