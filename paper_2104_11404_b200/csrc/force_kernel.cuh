@@ -36,6 +36,14 @@ enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2, MODE_FTW = 3 };
 // A_q = S_q : gradhat w, the L2 backward contraction.
 
 // EPB_: units per CTA (0 = default: 8 for 16-point 2D elements, else 1).
+#ifndef GEN_SEPS
+#define GEN_SEPS 0
+#endif
+// one dt-key atomic per warp instead of a CTA-wide shared-memory reduction and barrier
+#ifndef GEN_WARP_KEY
+#define GEN_WARP_KEY 1
+#endif
+
 template <int DIM_, int K_, int Q_, int NF_, int EPB_ = 0>
 struct Geo {
   static constexpr int DIM = DIM_, K = K_, Q = Q_;
@@ -57,7 +65,13 @@ struct Geo {
   static constexpr int F1B = DIM == 3 ? Q * Q * M : Q * M;
   static constexpr int F2B = DIM == 3 ? Q * M * M : 0;
   static constexpr int BWD = DIM * DIM * NQ + NQ + TB + WB + F1B + F2B;
-  static constexpr int WORK = FWD > BWD ? FWD : BWD;
+  // SEPS (3D Q3 and larger): the point stresses S_q, A_q get their own region after the
+  // forward buffers, so they can be written without waiting for every warp to finish its
+  // forward reads (one barrier fewer per element); the backward work arrays still overlap
+  // the forward buffers.  Costs 2 160 doubles per C3 element (4 CTAs/SM still fit).
+  static constexpr bool SEPS = DIM == 3 && NQ >= 128 && GEN_SEPS;
+  static constexpr int WORK = SEPS ? FWD + DIM * DIM * NQ + NQ : (FWD > BWD ? FWD : BWD);
+  static_assert(!SEPS || TB + WB + F1B + F2B <= FWD, "SEPS layout");
   static constexpr int UNIT = NF * DIM * ND + NE + WORK;
   static constexpr int TABD = Q + Q * N * 2 + Q * M;             // w, B, G, Bl
   static constexpr size_t SMEM =
@@ -1025,6 +1039,16 @@ force_kernel(const Params P) {
     if (isnan(po.dtq)) atomicOr(&P.st[b].nan_flag, 1u);
     else key = dt_key(po.dtq);
   }
+  if (GEN_WARP_KEY && DIM == 3 && EPB == 1) {
+    // one unit per CTA: each warp's minimum goes straight to the unit's status word (no
+    // shared-memory reduction, no CTA barrier before the backward pass)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, key, off);
+      key = o < key ? o : key;
+    }
+    if ((tid & 31) == 0 && key != ~0ull && unit0 < P.n_units) atomicMin(&P.st[b].dt_key, key);
+  } else {
   {
     constexpr bool WARP_IN_UNIT = (NQ % 32 == 0) || (EPB == 1);
     constexpr bool HALF = (NQ == 16);
@@ -1051,16 +1075,17 @@ force_kernel(const Params P) {
     const int g2 = unit0 + tid;
     if (g2 < P.n_units && skey[tid] != ~0ull) atomicMin(&P.st[g2 % B].dt_key, skey[tid]);
   }
+  }
   if (MODE == MODE_DT) {
     pdl_trigger();
     return;
   }
-  __syncthreads();  // forward buffers are dead from here on (S4 reuses them)
+  if (!G::SEPS) __syncthreads();  // forward buffers are dead from here on (S4 reuses them)
 
   // --- S4 backward
-  double *Ss = Wk;                      // [DIM*DIM][NQ]
-  double *As = Ss + DIM * DIM * NQ;     // [NQ]
-  double *Tb = As + NQ;
+  double *Ss = G::SEPS ? Wk + G::FWD : Wk;  // [DIM*DIM][NQ]
+  double *As = Ss + DIM * DIM * NQ;         // [NQ]
+  double *Tb = G::SEPS ? Wk : As + NQ;
   double *Wb = Tb + G::TB;
   double *F1b = Wb + G::WB;
   double *F2b = F1b + G::F1B;
