@@ -43,6 +43,10 @@ enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2, MODE_FTW = 3 };
 #ifndef GEN_WARP_KEY
 #define GEN_WARP_KEY 1
 #endif
+// one-unit 3D CTAs gather node ids and values in the same thread (no barrier in between)
+#ifndef GEN_GATHER1
+#define GEN_GATHER1 1
+#endif
 
 template <int DIM_, int K_, int Q_, int NF_, int EPB_ = 0>
 struct Geo {
@@ -719,7 +723,34 @@ force_kernel(const Params P) {
   for (int i = tid; i < Q * M; i += NT) sBl[i] = P.tab_Bl[i];
   for (int i = tid; i < EPB; i += NT) skey[i] = ~0ull;
 
-  // --- S1 gather: node ids, then fields (unit fastest for coalescing across instances)
+  // --- S1 gather
+  constexpr bool GATHER1 = GEN_GATHER1 && DIM == 3 && EPB == 1 && NT >= ND + NE;
+  if constexpr (GATHER1) {
+    // one unit per CTA: thread a < ND loads node a's id and then its NF x DIM values (no
+    // barrier between the two), threads ND .. ND+NE-1 load the e dofs
+    const int gu = unit0;
+    if (gu < P.n_units) {
+      const int lr = BATCHED ? gu / B : gu;
+      const int l0 = P.unit_elem ? P.unit_elem[lr] : lr;
+      const int b0 = BATCHED ? gu - lr * B : 0;
+      if (tid < ND) {
+        const int nd = __ldg(P.elem_nodes + (int64_t)l0 * ND + tid);
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          const double *src = NF == 1 ? P.x : (f == 0 ? P.x : (f == 1 ? P.v : P.w));
+#pragma unroll
+          for (int c = 0; c < DIM; ++c)
+            units[(f * DIM + c) * ND + tid] = __ldg(src + ((int64_t)c * P.ld_nodes + nd) * B + b0);
+        }
+      } else if (WANT_E && tid < ND + NE) {
+        const int j = tid - ND;
+        units[G::NF * DIM * ND + j] = __ldg(P.e + ((int64_t)l0 * NE + j) * B + b0);
+      }
+    } else {
+      for (int i = tid; i < G::NF * DIM * ND + NE; i += NT) units[i] = 0.0;
+    }
+  } else {
+  // node ids, then fields (unit fastest for coalescing across instances)
   for (int i = tid; i < EPB * ND; i += NT) {
     const int uu = i % EPB, a = i / EPB;
     const int gu = unit0 + uu;
@@ -762,6 +793,7 @@ force_kernel(const Params P) {
       }
     }
   }
+  }  // !GATHER1
   __syncthreads();
 
   const bool active = (u < EPB) && (unit0 + u < P.n_units) && (lt < NQ);
