@@ -735,6 +735,8 @@ force_kernel(const Params P) {
       const int b0 = BATCHED ? gu - lr * B : 0;
       if (tid < ND) {
         const int nd = __ldg(P.elem_nodes + (int64_t)l0 * ND + tid);
+        // the node's assembly slot, for the F.1 write-out at the end (snode is free here)
+        if (MODE == MODE_FORCE) snode[tid] = __ldg(P.slot + (int64_t)l0 * ND + tid);
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
           const double *src = NF == 1 ? P.x : (f == 0 ? P.x : (f == 1 ? P.v : P.w));
@@ -1236,7 +1238,7 @@ force_kernel(const Params P) {
             acc = __fma_rn(CT::G(q1, a1), w1v[q1], acc);
             acc = __fma_rn(CT::B(q1, a1), w23v[q1], acc);
           }
-          const int s = P.slot[slot_base + a0 + a1];
+          const int s = GATHER1 && MODE == MODE_FORCE ? snode[a0 + a1] : P.slot[slot_base + a0 + a1];
           if (s >= 0) P.evec[((int64_t)s * DIM + c) * B + b] = acc;
         }
       }
