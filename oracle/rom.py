@@ -139,32 +139,41 @@ def advance(op, Yx, Yv, Ye, t0, t_final, dt, beta1=0.85, beta2=1.02, gamma=0.8,
     return Yx, Yv, Ye, t, h, ns, nr, it
 
 
-def window_transition(T, c, Y):
+def window_transition(Phi_new, Phi_old, os_new, os_old, Y):
     """Initial reduced coordinates of time window w from those of window w-1, PAPER Eq.
-    ic-tw: yhat_w = T yhat_{w-1} + c with the offline T = Phi_w^T Phi_{w-1} and
-    c = Phi_w^T (os_{w-1} - os_w) (the oblique Eq. ic2-tw only changes T and c).  Plain
-    product: Y_new[i][b] = c[i] (or c[i][b]) + sum_k T[i][k] Y[k][b]."""
-    return lift(T, c, Y)
+    ic-tw, written out as the paper states it:
+        yhat_w = Phi_w^T (os_{w-1} + Phi_{w-1} yhat_{w-1} - os_w)
+    (lift with the old window's basis and offset, subtract the new offset, project on the new
+    basis); offsets [rows] or [rows][B].  Evaluated as Phi_w^T (os_{w-1} - os_w) +
+    Phi_w^T (Phi_{w-1} yhat): the offsets are differenced first (lifting and then
+    subtracting a large offset would cancel catastrophically for the e field's spike).
+    Independent of the factored T, c form the GPU path uses (workloads.window_transition_ops)."""
+    d = os_old - os_new
+    d = d[:, None] if d.ndim == 1 else d
+    return Phi_new.T @ d + Phi_new.T @ (Phi_old @ Y)
 
 
 def windowed_advance(windows, Yx, Yv, Ye, t0, dt, beta1=0.85, beta2=1.02, gamma=0.8,
                      max_iters=10**6):
     """The time-windowing online phase: for each window, `advance` with its
     own operators up to its end time, then map the reduced coordinates into the next
-    window's bases (window_transition).  windows: list of dicts with keys op (the
-    rom_rk2avg_step operators), t_end and, except for the last, trans = ((Tx, cx), (Tv, cv),
-    (Te, ce)).  Returns (Yx, Yv, Ye, t[B], next_dt[B], per-window (accepted, rejected))."""
+    window's bases (window_transition, from the two windows' bases and offsets in `op`).
+    windows: list of dicts with keys op (the rom_rk2avg_step operators, incl. Phi_x/v/e and
+    x_os/v_os/e_os) and t_end.  Returns (Yx, Yv, Ye, t[B], next_dt[B], per-window
+    (accepted, rejected))."""
     t = t0
     h = np.array(dt, dtype=np.float64)
     stats = []
     tB = None
-    for w in windows:
+    for wi, w in enumerate(windows):
         Yx, Yv, Ye, tB, h, ns, nr, _ = advance(w["op"], Yx, Yv, Ye, t, w["t_end"], h, beta1, beta2,
                                                gamma, max_iters)
         stats.append((ns, nr))
         t = w["t_end"]
-        if w.get("trans") is not None:
-            (Tx, cx), (Tv, cv), (Te, ce) = w["trans"]
-            Yx, Yv, Ye = window_transition(Tx, cx, Yx), window_transition(Tv, cv, Yv), \
-                window_transition(Te, ce, Ye)
+        nxt = wi + 1
+        if nxt < len(windows):
+            o, n = w["op"], windows[nxt]["op"]
+            Yx = window_transition(n["Phi_x"], o["Phi_x"], n["x_os"], o["x_os"], Yx)
+            Yv = window_transition(n["Phi_v"], o["Phi_v"], n["v_os"], o["v_os"], Yv)
+            Ye = window_transition(n["Phi_e"], o["Phi_e"], n["e_os"], o["e_os"], Ye)
     return Yx, Yv, Ye, tB, h, stats

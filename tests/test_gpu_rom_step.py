@@ -154,7 +154,7 @@ def test_rom_windowed_advance_matches_oracle():
     _, _, _, est0 = orom.rom_rk2avg_step(op1, b1.Yx, b1.Yv, b1.Ye, np.zeros(b1.B))
     dt0 = 0.7 * est0
     t1, t2 = 2.0 * float(est0.max()), 4.0 * float(est0.max())
-    ref = orom.windowed_advance([dict(op=op1, t_end=t1, trans=trans), dict(op=op2, t_end=t2)],
+    ref = orom.windowed_advance([dict(op=op1, t_end=t1), dict(op=op2, t_end=t2)],
                                 b1.Yx.copy(), b1.Yv.copy(), b1.Ye.copy(), 0.0, dt0, max_iters=20)
     dtr = tuple((H.dev(T), H.dev(c)) for T, c in trans)
     got = hydro.rom_windowed_advance([dict(stepper=st1, t_end=t1, trans=dtr),

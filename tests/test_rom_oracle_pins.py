@@ -97,24 +97,24 @@ def test_P24_rom_controller_is_per_instance():
 
 
 def test_P25_window_transition():
-    """Eq. ic-tw with the offline T = Phi_w^T Phi_{w-1}, c = Phi_w^T(os_{w-1} -
-    os_w): (a) the same orthonormal basis and offset in both windows -> identity; (b) a
-    next-window basis that contains the previous one's span and the same offset -> the
-    lifted state is reproduced exactly (up to rounding): os + Phi_w yhat_w = os + Phi_{w-1}
-    yhat_{w-1}; (c) different offsets whose difference lies in span(Phi_w) -> the lifted
-    state is again reproduced (the offset shift is absorbed by c)."""
+    """Eq. ic-tw: (a) the same orthonormal basis and offset in both windows ->
+    identity; (b) a next-window basis that contains the previous one's span and the same
+    offset -> the lifted state is reproduced exactly (up to rounding): os + Phi_w yhat_w =
+    os + Phi_{w-1} yhat_{w-1}; (c) different offsets whose difference lies in span(Phi_w) ->
+    the lifted state is again reproduced; (d) the factored offline form the GPU path uses,
+    T = Phi_w^T Phi_{w-1}, c = Phi_w^T (os_{w-1} - os_w) (workloads.window_transition_ops),
+    agrees with the direct formula."""
     from oracle import rom
     rng = np.random.default_rng(3)
     Q, _ = np.linalg.qr(rng.standard_normal((50, 8)))
     Y = rng.standard_normal((8, 3))
     os_ = rng.standard_normal(50)
-    T, c = W.window_transition_ops(Q, Q, os_, os_)
-    np.testing.assert_allclose(rom.window_transition(T, c, Y), Y, atol=1e-14)
+    np.testing.assert_allclose(rom.window_transition(Q, Q, os_, os_, Y), Y, atol=1e-14)
     Q2, _ = np.linalg.qr(np.concatenate([Q, rng.standard_normal((50, 4))], axis=1))
-    T, c = W.window_transition_ops(Q2, Q, os_, os_)
-    Y2 = rom.window_transition(T, c, Y)
+    Y2 = rom.window_transition(Q2, Q, os_, os_, Y)
     np.testing.assert_allclose(os_[:, None] + Q2 @ Y2, os_[:, None] + Q @ Y, atol=1e-13)
     os2 = os_ + Q2 @ rng.standard_normal(12)
-    T, c = W.window_transition_ops(Q2, Q, os2, os_)
-    Y2 = rom.window_transition(T, c, Y)
+    Y2 = rom.window_transition(Q2, Q, os2, os_, Y)
     np.testing.assert_allclose(os2[:, None] + Q2 @ Y2, os_[:, None] + Q @ Y, atol=1e-12)
+    T, c = W.window_transition_ops(Q2, Q, os2, os_)
+    np.testing.assert_allclose(T @ Y + c[:, None], Y2, atol=1e-12)
