@@ -33,7 +33,10 @@ RAW = ["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
        "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
        "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
        "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
-       "smsp__inst_executed.sum", "launch__registers_per_thread"]
+       "smsp__inst_executed.sum", "launch__registers_per_thread",
+       "dram__bytes.sum.per_second",
+       "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+       "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"]
 
 
 def _csv(args):
