@@ -184,9 +184,12 @@ def measured_peaks():
     return d
 
 
-# FP64 pipe peak: DFMA microbenchmark on this pool's B200 (tools/microbench/fp64_peak.cu,
-# profiles/r01_fp64_peak.txt): 34.2 TFLOP/s sustained; IEEE div 1.43e12/s, sqrt 1.29e12/s.
-FP64_PEAK_TFLOPS = 34.2
+# FP64 pipe peak, derived from unit counts and clock: 64 FP64 FMA/clk/SM x 2 flop x 148 SMs x
+# 1965 MHz = 37.2 TFLOP/s; measured 37.1 TFLOP/s with DMMA and 36.5 with independent DFMA
+# chains (tools/microbench/dmma_rate.cu, profiles/r01_fp64_dmma_rate.txt; DMMA and DFMA share
+# the pipe: 35.2 TF mixed).  The first DFMA microbenchmark (fp64_peak.cu, 34.2 TF) was
+# chain-limited and under-stated the peak.  IEEE div 1.43e12/s, sqrt 1.29e12/s.
+FP64_PEAK_TFLOPS = 37.2
 
 
 # ----------------------------------------------------------------------------- workloads
@@ -694,8 +697,9 @@ def roofline(name, base, m, n_units, kern_ms, prob):
             "rotations_per_lmin3": round(rot, 3),
             "hbm_bytes_alg": byts, "hbm_frac": round(byts / t / 1e9 / hbm, 4),
             "traffic_source": traffic["source"] if traffic else None,
-            "peak_source": "FP64 DFMA microbenchmark on B200, sustained "
-                           "(profiles/r01_fp64_peak.txt); HBM from MEASURED_PEAKS.json"}
+            "peak_source": "FP64: 64 FMA/clk/SM x 2 x 148 SMs x 1965 MHz = 37.2 TF/s (measured "
+                           "37.1 DMMA / 36.5 DFMA, profiles/r01_fp64_dmma_rate.txt); HBM from "
+                           "MEASURED_PEAKS.json"}
 
 
 def measured_traffic(name):
