@@ -637,12 +637,18 @@ def bench_offline(args, dev, ns=64, m=40):
     b.record()
     torch.cuda.synchronize()
     deim_ms = a.elapsed_time(b)
+    a.record()
+    qidx = hydro.qdeim(U)
+    b.record()
+    torch.cuda.synchronize()
+    qdeim_ms = a.elapsed_time(b)
     gram_flop = 2.0 * ns * ns * N / 2
     return {"workload": "offline_c2", "N": N, "snapshots": ns, "pod_ms": pod_ms,
             "pod_k": int(Phi.shape[1]), "gram_tflops": gram_flop / (pod_ms * 1e-3) / 1e12,
             "deim_ms": deim_ms, "deim_m": m, "deim_distinct": int(len(set(idx.tolist()))),
+            "qdeim_ms": qdeim_ms, "qdeim_distinct": int(len(set(qidx.tolist()))),
             "what": "POD (method of snapshots, energy criterion 0.9999, CholQR) of seeded "
-                    "low-rank+noise snapshots and greedy DEIM (P:908-1016)"}
+                    "low-rank+noise snapshots, greedy DEIM and Q-DEIM (P:908-1026)"}
 
 
 def _rotations_per_lmin3(name, prob):

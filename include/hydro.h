@@ -305,6 +305,13 @@ hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k
  * with (P^T U_{<j}) c = P^T u_j (LU with partial pivoting, host).  Ties: the lowest row.
  * idx: host [m].  HYDRO_ERR_NONFINITE if some P^T U_{<j} is singular.  Synchronises.        */
 hydro_status hydro_deim(const double *U, int64_t N, int m, int64_t *idx, hydro_stream_t stream);
+/* Q-DEIM indices (Drmac-Gugercin): the first m pivots of a QR factorisation with
+ * column pivoting of U^T, computed as pivoted Gram-Schmidt on the rows of U (device,
+ * [N][m] row-major): pivot = the row with the largest residual norm (ties: the lowest row),
+ * then every residual row loses its component along the pivot's normalised residual.
+ * idx: host [m].  Allocates its own scratch (an [m][N] transposed copy of U).  Synchronises
+ * `stream`.  HYDRO_ERR_NONFINITE if a residual vanishes before m pivots (U rank-deficient).  */
+hydro_status hydro_qdeim(const double *U, int64_t N, int m, int64_t *idx, hydro_stream_t stream);
 
 /* ------------------------------------------------------------------ profiling (host) */
 /* When enabled, every hydro_force_full / hydro_dt_estimate / hydro_force_sampled call

@@ -12,6 +12,10 @@ PAPER Sec. 4.3 (POD) and 4.5 (DEIM):
   |u_1|; for j >= 2, c solves (P^T U_{<j}) c = P^T u_j and p_j = argmax |u_j - U_{<j} c|
   (numpy.argmax: the first maximum, i.e. the lowest row on ties).
 
+* qdeim(U): Q-DEIM (Drmac-Gugercin): the first m column pivots of a QR
+  factorisation with column pivoting of U^T, by a library pivoted QR (scipy.linalg.qr,
+  pivoting=True -- LAPACK dgeqp3, a primitive as a step).
+
 Pinned by tests/test_offline_oracle_pins.py (closed-form low-rank snapshots, the DEIM
 interpolation property, permutation bases)."""
 from __future__ import annotations
@@ -53,3 +57,11 @@ def deim(U: np.ndarray) -> np.ndarray:
         r = U[:, j] - U[:, :j] @ c
         p.append(int(np.argmax(np.abs(r))))
     return np.array(p, dtype=np.int64)
+
+
+def qdeim(U: np.ndarray) -> np.ndarray:
+    """Q-DEIM indices [m] of the basis U [N][m]: the first m pivots of U^T P = Q R."""
+    import scipy.linalg
+    m = U.shape[1]
+    _, _, piv = scipy.linalg.qr(U.T, mode="economic", pivoting=True)
+    return np.asarray(piv[:m], dtype=np.int64)

@@ -1794,3 +1794,64 @@ hydro_status hydro_deim(const double *U, int64_t N, int m, int64_t *idx, hydro_s
 }
 
 }  // extern "C"
+
+extern "C" {
+
+hydro_status hydro_qdeim(const double *U, int64_t N, int m, int64_t *idx, hydro_stream_t stream) {
+  if (!U || N <= 0 || m <= 0 || m > N || m > 4096 || !idx) return HYDRO_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  double *Rt = nullptr, *q = nullptr, *bval = nullptr;
+  int64_t *bidx = nullptr;
+  auto cleanup = [&]() { cudaFree(Rt); cudaFree(q); cudaFree(bval); cudaFree(bidx); };
+  if (cudaMalloc(&Rt, sizeof(double) * (size_t)N * m) != cudaSuccess ||
+      cudaMalloc(&q, sizeof(double) * (size_t)m) != cudaSuccess ||
+      cudaMalloc(&bval, sizeof(double) * hk::DEIM_BLOCKS) != cudaSuccess ||
+      cudaMalloc(&bidx, sizeof(int64_t) * hk::DEIM_BLOCKS) != cudaSuccess) {
+    cleanup();
+    return HYDRO_ERR_CUDA;
+  }
+  hk::transpose_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((m + 31) / 32)), dim3(32, 8), 0, s>>>(
+      N, m, U, Rt);
+  g_launches++;
+  std::vector<double> hv(hk::DEIM_BLOCKS), row((size_t)m);
+  std::vector<int64_t> hi(hk::DEIM_BLOCKS);
+  hydro_status st = HYDRO_OK;
+  for (int k = 0; k < m; ++k) {
+    hk::qdeim_step_kernel<<<hk::DEIM_BLOCKS, hk::DEIM_THREADS, 0, s>>>(N, m, q, Rt, bval, bidx, k == 0);
+    g_launches++;
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(hv.data(), bval, sizeof(double) * hk::DEIM_BLOCKS, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(hi.data(), bidx, sizeof(int64_t) * hk::DEIM_BLOCKS, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+      st = HYDRO_ERR_CUDA;
+      break;
+    }
+    double best = -1.0;
+    int64_t p = -1;
+    for (int b = 0; b < hk::DEIM_BLOCKS; ++b)  // blocks cover ascending row ranges
+      if (hi[(size_t)b] >= 0 && hv[(size_t)b] > best) { best = hv[(size_t)b]; p = hi[(size_t)b]; }
+    if (p < 0 || !(best > 0.0)) { st = HYDRO_ERR_NONFINITE; break; }
+    idx[k] = p;
+    if (k + 1 == m) break;
+    // q = R[p] / |R[p]| for the next step (row p of the column-major residual: stride N)
+    if (cudaMemcpy2DAsync(row.data(), sizeof(double), Rt + p, sizeof(double) * (size_t)N, sizeof(double),
+                          (size_t)m, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+      st = HYDRO_ERR_CUDA;
+      break;
+    }
+    double n2 = 0.0;
+    for (int j = 0; j < m; ++j) n2 += row[(size_t)j] * row[(size_t)j];
+    const double inv = 1.0 / std::sqrt(n2);
+    for (int j = 0; j < m; ++j) row[(size_t)j] *= inv;
+    if (cudaMemcpyAsync(q, row.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+      st = HYDRO_ERR_CUDA;
+      break;
+    }
+  }
+  cudaStreamSynchronize(s);
+  cleanup();
+  return st;
+}
+
+}  // extern "C"

@@ -135,4 +135,71 @@ __global__ void __launch_bounds__(DEIM_THREADS) deim_residual_kernel(
   if (threadIdx.x == 0) { bval[blockIdx.x] = sv[0]; bidx[blockIdx.x] = si[0]; }
 }
 
+// Q-DEIM (QR with column pivoting of U^T = pivoted Gram-Schmidt on the rows of U), one
+// step on the residual Rt held column-major ([m][N], so every access below is coalesced
+// across rows): every residual row r loses its component along the unit vector q (the last
+// pivot's normalised residual), R[r] -= (R[r].q) q, and its squared norm nu[r] is recomputed
+// from the updated entries; the block-wise arg-max of nu (ties: the lowest row) is written
+// for the next pivot.  Rows already chosen keep a zero residual and are never picked again.
+__global__ void __launch_bounds__(DEIM_THREADS) qdeim_step_kernel(
+    int64_t N, int m, const double *__restrict__ q, double *__restrict__ Rt,
+    double *__restrict__ bval, int64_t *__restrict__ bidx, int first) {
+  __shared__ double sv[DEIM_THREADS];
+  __shared__ int64_t si[DEIM_THREADS];
+  const int64_t chunk = (N + DEIM_BLOCKS - 1) / DEIM_BLOCKS;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < N ? lo + chunk : N;
+  double best = -1.0;
+  int64_t bi = -1;
+  for (int64_t r = lo + threadIdx.x; r < hi; r += DEIM_THREADS) {
+    double n2 = 0.0;
+    if (first) {
+      for (int j = 0; j < m; ++j) {
+        const double v = Rt[(int64_t)j * N + r];
+        n2 = __fma_rn(v, v, n2);
+      }
+    } else {
+      double c = 0.0;
+      for (int j = 0; j < m; ++j) c = __fma_rn(Rt[(int64_t)j * N + r], q[j], c);
+      for (int j = 0; j < m; ++j) {
+        const double v = __fma_rn(-c, q[j], Rt[(int64_t)j * N + r]);
+        Rt[(int64_t)j * N + r] = v;
+        n2 = __fma_rn(v, v, n2);
+      }
+    }
+    if (n2 > best) { best = n2; bi = r; }
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int w = DEIM_THREADS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const double a = sv[threadIdx.x], b = sv[threadIdx.x + w];
+      const int64_t ia = si[threadIdx.x], ib = si[threadIdx.x + w];
+      if (b > a || (b == a && ib >= 0 && (ia < 0 || ib < ia))) { sv[threadIdx.x] = b; si[threadIdx.x] = ib; }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { bval[blockIdx.x] = sv[0]; bidx[blockIdx.x] = si[0]; }
+}
+
+// [N][m] row-major -> [m][N] (Q-DEIM's working layout), 32x32 tiles through shared memory.
+__global__ void transpose_kernel(int64_t N, int m, const double *__restrict__ A,
+                                 double *__restrict__ At) {
+  __shared__ double t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int j0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int64_t r = r0 + i;
+    const int j = j0 + threadIdx.x;
+    if (r < N && j < m) t[i][threadIdx.x] = A[r * m + j];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int j = j0 + i;
+    const int64_t r = r0 + threadIdx.x;
+    if (r < N && j < m) At[(int64_t)j * N + r] = t[threadIdx.x][i];
+  }
+}
+
 }  // namespace hk

@@ -108,4 +108,5 @@ def test_time_loop_and_offline_arguments_rejected_without_gpu():
     assert L.hydro_pod(None, 4, 100, 1.5, 4, None, None, ctypes.byref(k), None) == ERR
     idx = (ctypes.c_int64 * 4)()
     assert L.hydro_deim(None, 100, 4, idx, None) == ERR
+    assert L.hydro_qdeim(None, 100, 4, idx, None) == ERR
     assert L.hydro_fom_stage_state(None, None, None, None, None) == ERR

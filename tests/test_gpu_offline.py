@@ -55,6 +55,14 @@ def test_deim_matches_oracle(N, m):
     np.testing.assert_array_equal(hydro.deim(H.dev(U)), ooff.deim(U))
 
 
+@pytest.mark.parametrize("N,m", [(50_000, 20), (9, 5), (1_000, 1), (200_000, 40)])
+def test_qdeim_matches_oracle(N, m):
+    rng = np.random.default_rng(21 + m)
+    U, _ = np.linalg.qr(rng.standard_normal((N, m)))
+    U = np.ascontiguousarray(U)
+    np.testing.assert_array_equal(hydro.qdeim(H.dev(U)), ooff.qdeim(U))
+
+
 def test_fom_snapshots_pod_sns_deim_pipeline():
     prob = W.sedov_like(41, 2, (9, 7), (0.0, 0.0), (0.9, 0.7), delta=0.08, e_floor=1e-2,
                         vmode="uniform", vscale=0.1, name="offline")

@@ -74,3 +74,35 @@ def test_P30_deim_first_index():
     rng = np.random.default_rng(4)
     U = rng.standard_normal((100, 5))
     assert offline.deim(U)[0] == int(np.argmax(np.abs(U[:, 0])))
+
+
+def test_P31_qdeim_scaled_permutation_basis():
+    """Rows that are scaled unit vectors: the pivoted QR takes them in decreasing norm order
+    (each pivot leaves the other rows' residuals untouched, they are orthogonal)."""
+    rng = np.random.default_rng(5)
+    N, m = 40, 7
+    rows = rng.permutation(N)[:m]
+    scale = np.sort(rng.uniform(0.5, 2.0, m))[::-1]
+    U = np.zeros((N, m))
+    U[rows, rng.permutation(m)] = scale
+    np.testing.assert_array_equal(offline.qdeim(U), rows)
+
+
+def test_P32_qdeim_matches_brute_force_pivoted_gram_schmidt():
+    """Brute force on a small case: pivoted Gram-Schmidt on the rows of U written out (the
+    textbook definition of QR with column pivoting applied to U^T), and the interpolation
+    property of the selected rows."""
+    rng = np.random.default_rng(6)
+    U, _ = np.linalg.qr(rng.standard_normal((30, 6)))
+    R = U.copy()
+    piv = []
+    for _ in range(6):
+        nrm = [float(R[r] @ R[r]) for r in range(30)]
+        p = max(range(30), key=lambda r: (nrm[r], -r))
+        piv.append(p)
+        q = R[p] / np.sqrt(nrm[p])
+        for r in range(30):
+            R[r] = R[r] - (R[r] @ q) * q
+    np.testing.assert_array_equal(offline.qdeim(U), piv)
+    f = U @ rng.standard_normal(6)
+    np.testing.assert_allclose(U @ np.linalg.solve(U[piv], f[piv]), f, atol=1e-12)
