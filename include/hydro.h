@@ -312,6 +312,15 @@ hydro_status hydro_deim(const double *U, int64_t N, int m, int64_t *idx, hydro_s
  * idx: host [m].  Allocates its own scratch (an [m][N] transposed copy of U).  Synchronises
  * `stream`.  HYDRO_ERR_NONFINITE if a residual vanishes before m pivots (U rank-deficient).  */
 hydro_status hydro_qdeim(const double *U, int64_t N, int m, int64_t *idx, hydro_stream_t stream);
+/* Oversampled greedy DEIM (gappy POD, the greedy of Carlberg et al. that allows
+ * n_s >= m sample rows; R28 for the reading): basis column j (j = 0..m-1) adds
+ * floor(n_s/m) (+1 while j < n_s mod m) rows: those outside the current set I with the largest
+ * |u_j - U_{<j} c|, c the least-squares fit of U[I, <j] c ~ U[I, j] (host Householder QR),
+ * taken one at a time in decreasing order (ties: the lowest row).  n_s = m is DEIM exactly.
+ * U: device [N][m] row-major; idx: host [n_s] in selection order.  m <= n_s <= N.
+ * Allocates its own scratch; synchronises `stream`.  HYDRO_ERR_NONFINITE on a rank-deficient fit. */
+hydro_status hydro_deim_oversampled(const double *U, int64_t N, int m, int n_s, int64_t *idx,
+                                    hydro_stream_t stream);
 
 /* ------------------------------------------------------------------ profiling (host) */
 /* When enabled, every hydro_force_full / hydro_dt_estimate / hydro_force_sampled call

@@ -16,6 +16,11 @@ PAPER Sec. 4.3 (POD) and 4.5 (DEIM):
   factorisation with column pivoting of U^T, by a library pivoted QR (scipy.linalg.qr,
   pivoting=True -- LAPACK dgeqp3, a primitive as a step).
 
+* deim_oversampled(U, n_s): the greedy that allows over-sampling (DESIGN.md
+  R28): basis column j adds floor(n_s/m) (+1 while j < n_s mod m) rows, those outside the
+  sample set I with the largest |u_j - U_{<j} c| (c = numpy.linalg.lstsq of U[I,<j] c ~
+  U[I,j]), one at a time in decreasing order (ties: the lowest row).
+
 Pinned by tests/test_offline_oracle_pins.py (closed-form low-rank snapshots, the DEIM
 interpolation property, permutation bases)."""
 from __future__ import annotations
@@ -65,3 +70,22 @@ def qdeim(U: np.ndarray) -> np.ndarray:
     m = U.shape[1]
     _, _, piv = scipy.linalg.qr(U.T, mode="economic", pivoting=True)
     return np.asarray(piv[:m], dtype=np.int64)
+
+
+def deim_oversampled(U: np.ndarray, n_s: int) -> np.ndarray:
+    """Oversampled greedy indices [n_s] of the basis U [N][m], in selection order."""
+    N, m = U.shape
+    I: list[int] = []
+    for j in range(m):
+        if j == 0:
+            r = U[:, 0]
+        else:
+            c = np.linalg.lstsq(U[I, :j], U[I, j], rcond=None)[0]
+            r = U[:, j] - U[:, :j] @ c
+        a = np.abs(r)
+        n_add = n_s // m + (1 if j < n_s % m else 0)
+        for _ in range(n_add):
+            am = a.copy()
+            am[I] = -1.0                      # rows already in I are not candidates
+            I.append(int(np.argmax(am)))      # the first maximum: the lowest row on ties
+    return np.array(I, dtype=np.int64)

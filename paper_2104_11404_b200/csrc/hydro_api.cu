@@ -1622,6 +1622,42 @@ bool lu_solve_host(int n, std::vector<double> A, std::vector<double> &b) {
   return true;
 }
 
+// Least squares min |A x - b|_2 (rows x n, row-major, rows >= n) by Householder QR (host; the
+// oversampled greedy's small gappy fits).  x = first n entries of b on return.
+bool lstsq_host(int rows, int n, std::vector<double> A, std::vector<double> &b) {
+  for (int k = 0; k < n; ++k) {
+    double nrm = 0.0;
+    for (int i = k; i < rows; ++i) nrm += A[(size_t)i * n + k] * A[(size_t)i * n + k];
+    nrm = std::sqrt(nrm);
+    if (nrm == 0.0) return false;
+    const double a = A[(size_t)k * n + k] > 0 ? -nrm : nrm;   // R_kk
+    std::vector<double> w((size_t)rows, 0.0);
+    for (int i = k; i < rows; ++i) w[(size_t)i] = A[(size_t)i * n + k];
+    w[(size_t)k] -= a;
+    double ww = 0.0;
+    for (int i = k; i < rows; ++i) ww += w[(size_t)i] * w[(size_t)i];
+    if (ww > 0.0) {
+      for (int j = k; j < n; ++j) {
+        double d = 0.0;
+        for (int i = k; i < rows; ++i) d += w[(size_t)i] * A[(size_t)i * n + j];
+        const double f = 2.0 * d / ww;
+        for (int i = k; i < rows; ++i) A[(size_t)i * n + j] -= f * w[(size_t)i];
+      }
+      double d = 0.0;
+      for (int i = k; i < rows; ++i) d += w[(size_t)i] * b[(size_t)i];
+      const double f = 2.0 * d / ww;
+      for (int i = k; i < rows; ++i) b[(size_t)i] -= f * w[(size_t)i];
+    }
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double acc = b[(size_t)i];
+    for (int j = i + 1; j < n; ++j) acc -= A[(size_t)i * n + j] * b[(size_t)j];
+    if (A[(size_t)i * n + i] == 0.0) return false;
+    b[(size_t)i] = acc / A[(size_t)i * n + i];
+  }
+  return true;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1847,6 +1883,74 @@ hydro_status hydro_qdeim(const double *U, int64_t N, int m, int64_t *idx, hydro_
     if (cudaMemcpyAsync(q, row.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s) != cudaSuccess) {
       st = HYDRO_ERR_CUDA;
       break;
+    }
+  }
+  cudaStreamSynchronize(s);
+  cleanup();
+  return st;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+hydro_status hydro_deim_oversampled(const double *U, int64_t N, int m, int n_s, int64_t *idx,
+                                    hydro_stream_t stream) {
+  if (!U || N <= 0 || m <= 0 || m > 4096 || n_s < m || n_s > N || n_s > 65536 || !idx) return HYDRO_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  double *c = nullptr, *bval = nullptr;
+  int64_t *bidx = nullptr;
+  unsigned char *mask = nullptr;
+  auto cleanup = [&]() { cudaFree(c); cudaFree(bval); cudaFree(bidx); cudaFree(mask); };
+  if (cudaMalloc(&c, sizeof(double) * (size_t)m) != cudaSuccess ||
+      cudaMalloc(&bval, sizeof(double) * hk::DEIM_BLOCKS) != cudaSuccess ||
+      cudaMalloc(&bidx, sizeof(int64_t) * hk::DEIM_BLOCKS) != cudaSuccess ||
+      cudaMalloc(&mask, (size_t)N) != cudaSuccess || cudaMemsetAsync(mask, 0, (size_t)N, s) != cudaSuccess) {
+    cleanup();
+    return HYDRO_ERR_CUDA;
+  }
+  std::vector<double> rows((size_t)n_s * m), hv(hk::DEIM_BLOCKS);
+  std::vector<int64_t> hi(hk::DEIM_BLOCKS);
+  const unsigned char one = 1;
+  hydro_status st = HYDRO_OK;
+  int got = 0;
+  for (int j = 0; j < m && st == HYDRO_OK; ++j) {
+    if (j > 0) {  // c = argmin |U[I, <j] c - U[I, j]|_2 over the current sample set I
+      std::vector<double> A((size_t)got * j), b((size_t)got);
+      for (int a = 0; a < got; ++a) {
+        for (int q = 0; q < j; ++q) A[(size_t)a * j + q] = rows[(size_t)a * m + q];
+        b[(size_t)a] = rows[(size_t)a * m + j];
+      }
+      if (!lstsq_host(got, j, A, b)) { st = HYDRO_ERR_NONFINITE; break; }
+      if (cudaMemcpyAsync(c, b.data(), sizeof(double) * j, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+        st = HYDRO_ERR_CUDA;
+        break;
+      }
+    }
+    const int n_add = n_s / m + (j < n_s % m ? 1 : 0);
+    for (int t = 0; t < n_add; ++t) {  // the n_add largest |residual| rows outside I, in order
+      hk::deim_residual_kernel<<<hk::DEIM_BLOCKS, hk::DEIM_THREADS, 0, s>>>(N, m, j, U, c, bval, bidx, mask);
+      g_launches++;
+      if (cudaGetLastError() != cudaSuccess ||
+          cudaMemcpyAsync(hv.data(), bval, sizeof(double) * hk::DEIM_BLOCKS, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+          cudaMemcpyAsync(hi.data(), bidx, sizeof(int64_t) * hk::DEIM_BLOCKS, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+          cudaStreamSynchronize(s) != cudaSuccess) {
+        st = HYDRO_ERR_CUDA;
+        break;
+      }
+      double best = -1.0;
+      int64_t p = -1;
+      for (int q = 0; q < hk::DEIM_BLOCKS; ++q)  // blocks cover ascending row ranges
+        if (hi[(size_t)q] >= 0 && hv[(size_t)q] > best) { best = hv[(size_t)q]; p = hi[(size_t)q]; }
+      if (p < 0) { st = HYDRO_ERR_NONFINITE; break; }
+      idx[got] = p;
+      if (cudaMemcpyAsync(mask + p, &one, 1, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+          cudaMemcpyAsync(rows.data() + (size_t)got * m, U + p * m, sizeof(double) * m, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+          cudaStreamSynchronize(s) != cudaSuccess) {
+        st = HYDRO_ERR_CUDA;
+        break;
+      }
+      ++got;
     }
   }
   cudaStreamSynchronize(s);

@@ -104,9 +104,11 @@ __global__ void right_mult_kernel(int64_t N, int k, int ldp, const double *__res
 // DEIM residual of basis column j: res[r] = U[r][j] - sum_{i<j} U[r][i] c[i]  (U: [N][m]),
 // with per-block argmax of |res| (ties: lowest row) written to (bval, bidx).
 constexpr int DEIM_BLOCKS = 148 * 4, DEIM_THREADS = 256;
+// mask (optional): rows with mask[r] != 0 are skipped (the oversampled greedy's chosen set).
 __global__ void __launch_bounds__(DEIM_THREADS) deim_residual_kernel(
     int64_t N, int m, int j, const double *__restrict__ U, const double *__restrict__ c,
-    double *__restrict__ bval, int64_t *__restrict__ bidx) {
+    double *__restrict__ bval, int64_t *__restrict__ bidx,
+    const unsigned char *__restrict__ mask = nullptr) {
   __shared__ double sv[DEIM_THREADS];
   __shared__ int64_t si[DEIM_THREADS];
   const int64_t chunk = (N + DEIM_BLOCKS - 1) / DEIM_BLOCKS;
@@ -115,6 +117,7 @@ __global__ void __launch_bounds__(DEIM_THREADS) deim_residual_kernel(
   double best = -1.0;
   int64_t bi = -1;
   for (int64_t r = lo + threadIdx.x; r < hi; r += DEIM_THREADS) {
+    if (mask && mask[r]) continue;
     const double *row = U + r * m;
     double acc = 0.0;
     for (int i = 0; i < j; ++i) acc = __fma_rn(row[i], c[i], acc);

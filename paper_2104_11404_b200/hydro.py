@@ -33,7 +33,7 @@ EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy"
             "hydro_profile_release_captured", "hydro_selftest_ieee_fast",
             "hydro_fom_create", "hydro_fom_destroy", "hydro_mass_v_apply", "hydro_mass_v_solve",
             "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_fom_advance", "hydro_rom_advance", "hydro_rom_create",
-            "hydro_fom_stage_state", "hydro_pod", "hydro_deim", "hydro_qdeim",
+            "hydro_fom_stage_state", "hydro_pod", "hydro_deim", "hydro_qdeim", "hydro_deim_oversampled",
             "hydro_rom_destroy", "hydro_rom_rk2avg_step", "hydro_force_stress_bytes",
             "hydro_force_full_store", "hydro_force_transpose", "hydro_sample_stress_bytes",
             "hydro_force_sampled_store", "hydro_sample_force_transpose"]
@@ -113,6 +113,7 @@ def lib() -> ctypes.CDLL:
                                 ctypes.POINTER(i32), vp]
         L.hydro_deim.argtypes = [vp, i64, i32, ctypes.POINTER(i64), vp]
         L.hydro_qdeim.argtypes = [vp, i64, i32, ctypes.POINTER(i64), vp]
+        L.hydro_deim_oversampled.argtypes = [vp, i64, i32, i32, ctypes.POINTER(i64), vp]
         L.hydro_rom_advance.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, _DtCtrl, dbl, dbl,
                                         ctypes.POINTER(dbl), i32, ctypes.POINTER(dbl),
                                         ctypes.POINTER(i32), ctypes.POINTER(i32),
@@ -462,6 +463,16 @@ def qdeim(U: torch.Tensor, stream=None):
     N, m = U.shape
     idx = (ctypes.c_int64 * m)()
     _check(lib().hydro_qdeim(_ptr(U.contiguous()), N, m, idx, _stream(stream)), "hydro_qdeim")
+    return _np.array(idx[:], dtype=_np.int64)
+
+
+def deim_oversampled(U: torch.Tensor, n_s: int, stream=None):
+    """Oversampled greedy DEIM indices (numpy int64 [n_s]) -- hydro_deim_oversampled."""
+    import numpy as _np
+    N, m = U.shape
+    idx = (ctypes.c_int64 * n_s)()
+    _check(lib().hydro_deim_oversampled(_ptr(U.contiguous()), N, m, n_s, idx, _stream(stream)),
+           "hydro_deim_oversampled")
     return _np.array(idx[:], dtype=_np.int64)
 
 

@@ -109,4 +109,6 @@ def test_time_loop_and_offline_arguments_rejected_without_gpu():
     idx = (ctypes.c_int64 * 4)()
     assert L.hydro_deim(None, 100, 4, idx, None) == ERR
     assert L.hydro_qdeim(None, 100, 4, idx, None) == ERR
+    assert L.hydro_deim_oversampled(None, 100, 4, 8, idx, None) == ERR
+    assert L.hydro_deim_oversampled(ctypes.c_void_p(8), 100, 4, 3, idx, None) == ERR   # n_s < m
     assert L.hydro_fom_stage_state(None, None, None, None, None) == ERR

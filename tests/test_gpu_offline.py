@@ -63,6 +63,14 @@ def test_qdeim_matches_oracle(N, m):
     np.testing.assert_array_equal(hydro.qdeim(H.dev(U)), ooff.qdeim(U))
 
 
+@pytest.mark.parametrize("N,m,n_s", [(50_000, 20, 40), (50_000, 20, 53), (1_000, 4, 4), (12, 3, 12)])
+def test_deim_oversampled_matches_oracle(N, m, n_s):
+    rng = np.random.default_rng(31 + n_s)
+    U, _ = np.linalg.qr(rng.standard_normal((N, m)))
+    U = np.ascontiguousarray(U)
+    np.testing.assert_array_equal(hydro.deim_oversampled(H.dev(U), n_s), ooff.deim_oversampled(U, n_s))
+
+
 def test_fom_snapshots_pod_sns_deim_pipeline():
     prob = W.sedov_like(41, 2, (9, 7), (0.0, 0.0), (0.9, 0.7), delta=0.08, e_floor=1e-2,
                         vmode="uniform", vscale=0.1, name="offline")

@@ -106,3 +106,25 @@ def test_P32_qdeim_matches_brute_force_pivoted_gram_schmidt():
     np.testing.assert_array_equal(offline.qdeim(U), piv)
     f = U @ rng.standard_normal(6)
     np.testing.assert_allclose(U @ np.linalg.solve(U[piv], f[piv]), f, atol=1e-12)
+
+
+def test_P33_oversampled_with_ns_equal_m_is_deim():
+    rng = np.random.default_rng(7)
+    U, _ = np.linalg.qr(rng.standard_normal((300, 8)))
+    np.testing.assert_array_equal(offline.deim_oversampled(U, 8), offline.deim(U))
+
+
+def test_P34_oversampled_first_rows_and_gappy_reconstruction():
+    """Column 0 adds the rows of largest |u_0| in decreasing order (closed form); with
+    n_s > m the sampled rows give an exact gappy (least-squares) reconstruction of anything
+    in span(U), and no row is chosen twice."""
+    rng = np.random.default_rng(8)
+    N, m, n_s = 250, 6, 15
+    U, _ = np.linalg.qr(rng.standard_normal((N, m)))
+    I = offline.deim_oversampled(U, n_s)
+    assert len(I) == n_s and len(set(I.tolist())) == n_s
+    n0 = n_s // m + 1                      # column 0 gets the remainder's extra row
+    np.testing.assert_array_equal(I[:n0], np.argsort(-np.abs(U[:, 0]), kind="stable")[:n0])
+    f = U @ rng.standard_normal(m)
+    c = np.linalg.lstsq(U[I], f[I], rcond=None)[0]
+    np.testing.assert_allclose(U @ c, f, atol=1e-12)
