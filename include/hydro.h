@@ -214,6 +214,8 @@ hydro_status hydro_mass_v_solve(hydro_fom *fom, const double *rhs, double *sol, 
 /* sol = M_E^-1 rhs  (device [n_elem][k^dim]).                                               */
 hydro_status hydro_mass_e_solve(hydro_fom *fom, const double *rhs, double *sol,
                                 hydro_stream_t stream);
+/* out = M_E in (block-diagonal energy mass matrix; in/out device [n_elem][ne]).   */
+hydro_status hydro_mass_e_apply(hydro_fom *fom, const double *in, double *out, hydro_stream_t stream);
 /* Kinetic 1/2 v^T M_V v and internal 1^T M_E e energies (host outputs).  Synchronises.     */
 hydro_status hydro_fom_energy(hydro_fom *fom, const double *v, const double *e,
                               double *kinetic, double *internal, hydro_stream_t stream);
@@ -321,6 +323,19 @@ hydro_status hydro_qdeim(const double *U, int64_t N, int m, int64_t *idx, hydro_
  * Allocates its own scratch; synchronises `stream`.  HYDRO_ERR_NONFINITE on a rank-deficient fit. */
 hydro_status hydro_deim_oversampled(const double *U, int64_t N, int m, int n_s, int64_t *idx,
                                     hydro_stream_t stream);
+/* Time-window transition operators, so that yhat_w = T yhat_{w-1} + c:
+ *   orthogonal, Eq. ic-tw (fom NULL or field 0 -- and always for the position field):
+ *     T = Phi_w^T Phi_{w-1},  c = Phi_w^T (os_{w-1} - os_w);
+ *   M-oblique, Eq. ic2-tw (fom given, field 1 = velocity with M_V, field 2 = energy with M_E):
+ *     T = Mhat^-1 Phi_w^T M Phi_{w-1},  c = Mhat^-1 Phi_w^T M (os_{w-1} - os_w),
+ *     Mhat = Phi_w^T M Phi_w  (n_w x n_w, LU-solved on the host).
+ * Phi_new device [N][n_new], Phi_old device [N][n_old], os_new / os_old device [N][B] (B = 1 for
+ * shared offsets), all row-major over the full FOM rows (N must match the field's size when
+ * oblique).  T: device [n_new][n_old], c: device [n_new][B].  The products over N rows are
+ * fixed-order split-K reductions (deterministic).  Allocates its own scratch; synchronises. */
+hydro_status hydro_window_ops(hydro_fom *fom, int field, int64_t N, int n_new, int n_old, int B,
+                              const double *Phi_new, const double *Phi_old, const double *os_new,
+                              const double *os_old, double *T, double *c, hydro_stream_t stream);
 
 /* ------------------------------------------------------------------ profiling (host) */
 /* When enabled, every hydro_force_full / hydro_dt_estimate / hydro_force_sampled call

@@ -153,6 +153,19 @@ def window_transition(Phi_new, Phi_old, os_new, os_old, Y):
     return Phi_new.T @ d + Phi_new.T @ (Phi_old @ Y)
 
 
+def window_transition_oblique(Phi_new, Phi_old, os_new, os_old, Y, M):
+    """The M-oblique variant, PAPER Eq. ic2-tw, as written:
+        yhat_w = (Phi_w^T M Phi_w)^{-1} Phi_w^T M (os_{w-1} + Phi_{w-1} yhat_{w-1} - os_w)
+    with M the field's FOM mass matrix (M_V for velocity, M_E for energy; the position keeps
+    Eq. ic-tw).  M: a function applying the mass matrix to a [N][k] array.  The offsets are
+    differenced first, as in window_transition."""
+    d = os_old - os_new
+    d = d[:, None] if d.ndim == 1 else d
+    Mhat = Phi_new.T @ M(Phi_new)
+    rhs = Phi_new.T @ M(d) + Phi_new.T @ M(Phi_old @ Y)
+    return np.linalg.solve(Mhat, rhs)
+
+
 def windowed_advance(windows, Yx, Yv, Ye, t0, dt, beta1=0.85, beta2=1.02, gamma=0.8,
                      max_iters=10**6):
     """The time-windowing online phase: for each window, `advance` with its

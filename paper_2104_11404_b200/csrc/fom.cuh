@@ -280,13 +280,13 @@ __global__ void assemble_masked_kernel(int64_t n_nodes, const int32_t *__restric
   }
 }
 
-// M_E,K, its inverse (Gauss-Jordan on the SPD block, no pivoting needed) and its row sums
+// M_E,K (kept in Mblk for hydro_mass_e_apply), its inverse (Gauss-Jordan on the SPD block, no pivoting needed) and its row sums
 // (c_K[j] = 1^T M_E,K e_j, the internal-energy weights).  One thread per element.
 template <int DIM, int K, int Q>
 __global__ void mass_e_setup_kernel(int32_t n_elem, const double *__restrict__ mq,
                                     const double *__restrict__ tab_w,
                                     const double *__restrict__ tab_Bl, double *__restrict__ Minv,
-                                    double *__restrict__ csum) {
+                                    double *__restrict__ csum, double *__restrict__ Mblk) {
   constexpr int M = K, NE = DIM == 3 ? M * M * M : M * M, NQ = DIM == 3 ? Q * Q * Q : Q * Q;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_elem) return;
@@ -312,6 +312,8 @@ __global__ void mass_e_setup_kernel(int32_t n_elem, const double *__restrict__ m
     double s = 0.0;
     for (int j = 0; j < NE; ++j) s += A[i][j];
     csum[(int64_t)e * NE + i] = s;
+    if (Mblk)
+      for (int j = 0; j < NE; ++j) Mblk[((int64_t)e * NE + i) * NE + j] = A[i][j];
   }
   for (int p = 0; p < NE; ++p) {
     const double inv = 1.0 / A[p][p];

@@ -877,6 +877,7 @@ struct hydro_fom {
   hydro_ctx *c = nullptr;
   int64_t n = 0;  // dim * n_nodes
   double *mask = nullptr, *dinv = nullptr, *Minv = nullptr, *csum = nullptr, *wm = nullptr;
+  double *Mblk = nullptr;  // M_E,K blocks (hydro_mass_e_apply)
   double *r = nullptr, *z = nullptr, *p = nullptr, *Ap = nullptr, *part = nullptr, *sc = nullptr;
   double *F1 = nullptr, *F1x = nullptr, *FTw = nullptr, *FTx = nullptr, *dv = nullptr;
   double *vh = nullptr, *eh = nullptr, *xh = nullptr, *v1 = nullptr, *vbar = nullptr,
@@ -982,16 +983,17 @@ hydro_status dot(hydro_fom *f, int64_t n, const double *a, const double *b, doub
 }
 
 hydro_status mass_e_update(hydro_fom *f, const double *a, const double *rhs, double scale,
-                           double *out, cudaStream_t s) {
+                           double *out, cudaStream_t s, const double *blocks = nullptr) {
+  const double *Mb = blocks ? blocks : f->Minv;
   const hydro_ctx *c = f->c;
   const int ne = c->ne;
   const int64_t n = c->d.n_elem * ne;
   const unsigned g = blocks_for(n, 256);
   const int32_t E = (int32_t)c->d.n_elem;
-  if (ne == 4) hk::mass_e_update_kernel<4><<<g, 256, 0, s>>>(E, f->Minv, a, rhs, scale, out);
-  else if (ne == 8) hk::mass_e_update_kernel<8><<<g, 256, 0, s>>>(E, f->Minv, a, rhs, scale, out);
-  else if (ne == 9) hk::mass_e_update_kernel<9><<<g, 256, 0, s>>>(E, f->Minv, a, rhs, scale, out);
-  else if (ne == 27) hk::mass_e_update_kernel<27><<<g, 256, 0, s>>>(E, f->Minv, a, rhs, scale, out);
+  if (ne == 4) hk::mass_e_update_kernel<4><<<g, 256, 0, s>>>(E, Mb, a, rhs, scale, out);
+  else if (ne == 8) hk::mass_e_update_kernel<8><<<g, 256, 0, s>>>(E, Mb, a, rhs, scale, out);
+  else if (ne == 9) hk::mass_e_update_kernel<9><<<g, 256, 0, s>>>(E, Mb, a, rhs, scale, out);
+  else if (ne == 27) hk::mass_e_update_kernel<27><<<g, 256, 0, s>>>(E, Mb, a, rhs, scale, out);
   else return HYDRO_ERR_UNSUPPORTED;
   g_launches++;
   CUDA_OK(cudaGetLastError());
@@ -1102,7 +1104,7 @@ hydro_status hydro_fom_create(hydro_ctx *c, const int64_t *bc_dofs, int64_t n_bc
       !alloc(&f->dv, n) || !alloc(&f->vh, n) || !alloc(&f->eh, nE) || !alloc(&f->xh, n) ||
       !alloc(&f->v1, n) || !alloc(&f->vbar, n) || !alloc(&f->dts, 2) ||
       !alloc(&f->xb, n) || !alloc(&f->vb, n) || !alloc(&f->eb, nE) ||
-      !alloc(&f->S, hydro_force_stress_bytes(c) / sizeof(double)))
+      !alloc(&f->S, hydro_force_stress_bytes(c) / sizeof(double)) || !alloc(&f->Mblk, nE * (size_t)c->ne))
     return fail(HYDRO_ERR_CUDA);
   if (cudaMemcpyAsync(f->mask, mask.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return fail(HYDRO_ERR_CUDA);
@@ -1126,13 +1128,13 @@ hydro_status hydro_fom_create(hydro_ctx *c, const int64_t *bc_dofs, int64_t n_bc
   const double *tw = c->tab, *tBl = c->tab + q + 2 * q * nn;
   const unsigned g = blocks_for(E, 64);
   if (dim == 2 && c->d.order_h1 == 2)
-    hk::mass_e_setup_kernel<2, 2, 4><<<g, 64, 0, s>>>((int32_t)E, c->mq, tw, tBl, f->Minv, f->csum);
+    hk::mass_e_setup_kernel<2, 2, 4><<<g, 64, 0, s>>>((int32_t)E, c->mq, tw, tBl, f->Minv, f->csum, f->Mblk);
   else if (dim == 3 && c->d.order_h1 == 2)
-    hk::mass_e_setup_kernel<3, 2, 4><<<g, 64, 0, s>>>((int32_t)E, c->mq, tw, tBl, f->Minv, f->csum);
+    hk::mass_e_setup_kernel<3, 2, 4><<<g, 64, 0, s>>>((int32_t)E, c->mq, tw, tBl, f->Minv, f->csum, f->Mblk);
   else if (dim == 2 && c->d.order_h1 == 3)
-    hk::mass_e_setup_kernel<2, 3, 6><<<g, 64, 0, s>>>((int32_t)E, c->mq, tw, tBl, f->Minv, f->csum);
+    hk::mass_e_setup_kernel<2, 3, 6><<<g, 64, 0, s>>>((int32_t)E, c->mq, tw, tBl, f->Minv, f->csum, f->Mblk);
   else
-    hk::mass_e_setup_kernel<3, 3, 6><<<g, 64, 0, s>>>((int32_t)E, c->mq, tw, tBl, f->Minv, f->csum);
+    hk::mass_e_setup_kernel<3, 3, 6><<<g, 64, 0, s>>>((int32_t)E, c->mq, tw, tBl, f->Minv, f->csum, f->Mblk);
   g_launches++;
   if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
     return fail(HYDRO_ERR_CUDA);
@@ -1167,6 +1169,14 @@ hydro_status hydro_mass_e_solve(hydro_fom *f, const double *rhs, double *sol, hy
   CUDA_OK(cudaMemsetAsync(f->FTx, 0, sizeof(double) * nE, s));
   if ((st = mass_e_update(f, f->FTx, rhs, 1.0, sol, s)) != HYDRO_OK) return st;
   return HYDRO_OK;
+}
+
+hydro_status hydro_mass_e_apply(hydro_fom *f, const double *in, double *out, hydro_stream_t stream) {
+  if (!f || !in || !out) return HYDRO_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t nE = (size_t)(f->c->d.n_elem * f->c->ne);
+  CUDA_OK(cudaMemsetAsync(f->FTx, 0, sizeof(double) * nE, s));
+  return mass_e_update(f, f->FTx, in, 1.0, out, s, f->Mblk);
 }
 
 hydro_status hydro_fom_energy(hydro_fom *f, const double *v, const double *e, double *kinetic,
@@ -1951,6 +1961,119 @@ hydro_status hydro_deim_oversampled(const double *U, int64_t N, int m, int n_s, 
         break;
       }
       ++got;
+    }
+  }
+  cudaStreamSynchronize(s);
+  cleanup();
+  return st;
+}
+
+}  // extern "C"
+
+namespace {
+
+// G (device [na][nx]) = A^T X over N rows; A, X row-major with leading dimensions lda, ldx.
+hydro_status xprod(int64_t N, int na, const double *A, int64_t lda, int nx, const double *X, int64_t ldx,
+                   double *G, cudaStream_t s) {
+  const int chunks = (int)std::min<int64_t>(hk::GRAM_CHUNKS, (N + hk::GRAM_KT - 1) / hk::GRAM_KT);
+  const int64_t chunk = (N + chunks - 1) / chunks;
+  double *part = nullptr;
+  if (cudaMalloc(&part, sizeof(double) * (size_t)chunks * na * nx) != cudaSuccess) return HYDRO_ERR_CUDA;
+  hk::xprod_partial_kernel<<<dim3((unsigned)chunks, (unsigned)((na + hk::GRAM_T - 1) / hk::GRAM_T),
+                                  (unsigned)((nx + hk::GRAM_T - 1) / hk::GRAM_T)),
+                             hk::GRAM_T * hk::GRAM_T, 0, s>>>(na, nx, N, chunk, A, lda, X, ldx, part);
+  hk::xprod_reduce_kernel<<<(na * nx + 255) / 256, 256, 0, s>>>(na, nx, chunks, part, G);
+  g_launches += 2;
+  const bool ok = cudaGetLastError() == cudaSuccess && cudaStreamSynchronize(s) == cudaSuccess;
+  cudaFree(part);
+  return ok ? HYDRO_OK : HYDRO_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+hydro_status hydro_window_ops(hydro_fom *fom, int field, int64_t N, int n_new, int n_old, int B,
+                              const double *Phi_new, const double *Phi_old, const double *os_new,
+                              const double *os_old, double *T, double *c, hydro_stream_t stream) {
+  if (N <= 0 || n_new <= 0 || n_old <= 0 || B <= 0 || n_new > 1024 || n_old > 1024 || B > 65536 ||
+      !Phi_new || !Phi_old || !os_new || !os_old || !T || !c || field < 0 || field > 2)
+    return HYDRO_ERR_ARG;
+  const bool oblique = fom && field > 0;
+  if (oblique) {
+    const int64_t want = field == 1 ? fom->n : fom->c->d.n_elem * fom->c->ne;
+    if (N != want) return HYDRO_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  double *W = nullptr, *d = nullptr, *G = nullptr, *tmp = nullptr;
+  auto cleanup = [&]() { cudaFree(W); cudaFree(d); cudaFree(G); cudaFree(tmp); };
+  const size_t gsz = (size_t)n_new * (n_new + n_old + B);
+  if (cudaMalloc(&d, sizeof(double) * (size_t)N * B) != cudaSuccess ||
+      cudaMalloc(&G, sizeof(double) * gsz) != cudaSuccess) {
+    cleanup();
+    return HYDRO_ERR_CUDA;
+  }
+  hydro_status st = HYDRO_OK;
+  const double *Wp = Phi_new;
+  if (oblique) {  // W = M Phi_new, column by column through the FOM's own mass operators
+    if (cudaMalloc(&W, sizeof(double) * (size_t)N * n_new) != cudaSuccess ||
+        cudaMalloc(&tmp, sizeof(double) * (size_t)N * 2) != cudaSuccess) {
+      cleanup();
+      return HYDRO_ERR_CUDA;
+    }
+    const unsigned g = blocks_for(N, 256);
+    for (int j = 0; j < n_new && st == HYDRO_OK; ++j) {
+      hk::col_copy_kernel<<<g, 256, 0, s>>>(N, Phi_new + j, n_new, tmp, 1);
+      g_launches++;
+      st = field == 1 ? mass_apply(fom, tmp, tmp + N, nullptr, 0, 0, s)
+                      : hydro_mass_e_apply(fom, tmp, tmp + N, stream);
+      if (st != HYDRO_OK) break;
+      hk::col_copy_kernel<<<g, 256, 0, s>>>(N, tmp + N, 1, W + j, n_new);
+      g_launches++;
+      if (cudaGetLastError() != cudaSuccess) st = HYDRO_ERR_CUDA;
+    }
+    Wp = W;
+  }
+  if (st == HYDRO_OK) {
+    hk::sub_kernel<<<blocks_for(N * B, 256), 256, 0, s>>>(N * B, os_old, os_new, d);
+    g_launches++;
+    if (cudaGetLastError() != cudaSuccess) st = HYDRO_ERR_CUDA;
+  }
+  // G = [W^T Phi_old | W^T d | W^T Phi_new]
+  double *G2 = G, *G3 = G + (size_t)n_new * n_old, *G1 = G3 + (size_t)n_new * B;
+  if (st == HYDRO_OK) st = xprod(N, n_new, Wp, n_new, n_old, Phi_old, n_old, G2, s);
+  if (st == HYDRO_OK) st = xprod(N, n_new, Wp, n_new, B, d, B, G3, s);
+  if (st == HYDRO_OK && oblique) st = xprod(N, n_new, Wp, n_new, n_new, Phi_new, n_new, G1, s);
+  if (st == HYDRO_OK && !oblique) {
+    if (cudaMemcpyAsync(T, G2, sizeof(double) * (size_t)n_new * n_old, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(c, G3, sizeof(double) * (size_t)n_new * B, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      st = HYDRO_ERR_CUDA;
+  } else if (st == HYDRO_OK) {  // T = Mhat^-1 (W^T Phi_old), c = Mhat^-1 (W^T d), Mhat = W^T Phi_new
+    std::vector<double> h(gsz);
+    if (cudaMemcpyAsync(h.data(), G, sizeof(double) * gsz, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+      st = HYDRO_ERR_CUDA;
+    } else {
+      const double *h1 = h.data() + (size_t)n_new * (n_old + B);
+      std::vector<double> A(h1, h1 + (size_t)n_new * n_new), out((size_t)n_new * (n_old + B)), b((size_t)n_new);
+      const int nr = n_old + B;
+      for (int col = 0; col < nr && st == HYDRO_OK; ++col) {
+        const double *src = col < n_old ? h.data() : h.data() + (size_t)n_new * n_old;
+        const int ld = col < n_old ? n_old : B, cc = col < n_old ? col : col - n_old;
+        for (int i = 0; i < n_new; ++i) b[(size_t)i] = src[(size_t)i * ld + cc];
+        if (!lu_solve_host(n_new, A, b)) { st = HYDRO_ERR_NONFINITE; break; }
+        for (int i = 0; i < n_new; ++i) out[(size_t)i * nr + col] = b[(size_t)i];
+      }
+      if (st == HYDRO_OK) {
+        std::vector<double> hT((size_t)n_new * n_old), hc((size_t)n_new * B);
+        for (int i = 0; i < n_new; ++i) {
+          for (int j = 0; j < n_old; ++j) hT[(size_t)i * n_old + j] = out[(size_t)i * nr + j];
+          for (int j = 0; j < B; ++j) hc[(size_t)i * B + j] = out[(size_t)i * nr + n_old + j];
+        }
+        if (cudaMemcpyAsync(T, hT.data(), sizeof(double) * hT.size(), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+            cudaMemcpyAsync(c, hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
+          st = HYDRO_ERR_CUDA;
+      }
     }
   }
   cudaStreamSynchronize(s);

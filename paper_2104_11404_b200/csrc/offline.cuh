@@ -205,4 +205,56 @@ __global__ void transpose_kernel(int64_t N, int m, const double *__restrict__ A,
   }
 }
 
+// Cross products G = A^T X over N rows (A: [N][lda] first na columns, X: [N][ldx] first nx
+// columns), split-K over row chunks like the Gram kernel: one GRAM_T x GRAM_T output tile per
+// block (y, z) and row chunk (x), staged through shared memory; partial[chunk][na][nx].
+__global__ void __launch_bounds__(GRAM_T *GRAM_T) xprod_partial_kernel(
+    int na, int nx, int64_t N, int64_t chunk, const double *__restrict__ A, int64_t lda,
+    const double *__restrict__ X, int64_t ldx, double *__restrict__ partial) {
+  __shared__ double sa[GRAM_KT][GRAM_T + 1], sx[GRAM_KT][GRAM_T + 1];
+  const int tx = threadIdx.x % GRAM_T, ty = threadIdx.x / GRAM_T;
+  const int i = blockIdx.y * GRAM_T + ty, j = blockIdx.z * GRAM_T + tx;
+  const int64_t k0 = (int64_t)blockIdx.x * chunk;
+  const int64_t k1 = k0 + chunk < N ? k0 + chunk : N;
+  double acc = 0.0;
+  for (int64_t kb = k0; kb < k1; kb += GRAM_KT) {
+    for (int t = threadIdx.x; t < GRAM_T * GRAM_KT; t += GRAM_T * GRAM_T) {
+      const int c = t % GRAM_T, kk = t / GRAM_T;   // consecutive threads: consecutive columns
+      const int64_t k = kb + kk;
+      const int ca = blockIdx.y * GRAM_T + c, cx = blockIdx.z * GRAM_T + c;
+      sa[kk][c] = (ca < na && k < k1) ? A[k * lda + ca] : 0.0;
+      sx[kk][c] = (cx < nx && k < k1) ? X[k * ldx + cx] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < GRAM_KT; ++kk) acc = __fma_rn(sa[kk][ty], sx[kk][tx], acc);
+    __syncthreads();
+  }
+  if (i < na && j < nx) partial[((int64_t)blockIdx.x * na + i) * nx + j] = acc;
+}
+
+// G[i][j] = sum over chunks (ascending) of partial[c][i][j]
+__global__ void xprod_reduce_kernel(int na, int nx, int chunks, const double *__restrict__ partial,
+                                    double *__restrict__ G) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= na * nx) return;
+  double acc = 0.0;
+  for (int c = 0; c < chunks; ++c) acc += partial[(int64_t)c * na * nx + t];
+  G[t] = acc;
+}
+
+// dst[r * ldd] = src[r * lds] (one column of a row-major matrix to / from a vector)
+__global__ void col_copy_kernel(int64_t N, const double *__restrict__ src, int64_t lds,
+                                double *__restrict__ dst, int64_t ldd) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < N) dst[r * ldd] = src[r * lds];
+}
+
+// d = a - b (elementwise; the offset difference of a window transition)
+__global__ void sub_kernel(int64_t n, const double *__restrict__ a, const double *__restrict__ b,
+                           double *__restrict__ d) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = a[i] - b[i];
+}
+
 }  // namespace hk

@@ -33,7 +33,7 @@ EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy"
             "hydro_profile_release_captured", "hydro_selftest_ieee_fast",
             "hydro_fom_create", "hydro_fom_destroy", "hydro_mass_v_apply", "hydro_mass_v_solve",
             "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_fom_advance", "hydro_rom_advance", "hydro_rom_create",
-            "hydro_fom_stage_state", "hydro_pod", "hydro_deim", "hydro_qdeim", "hydro_deim_oversampled",
+            "hydro_fom_stage_state", "hydro_pod", "hydro_deim", "hydro_qdeim", "hydro_deim_oversampled", "hydro_mass_e_apply", "hydro_window_ops",
             "hydro_rom_destroy", "hydro_rom_rk2avg_step", "hydro_force_stress_bytes",
             "hydro_force_full_store", "hydro_force_transpose", "hydro_sample_stress_bytes",
             "hydro_force_sampled_store", "hydro_sample_force_transpose"]
@@ -98,6 +98,8 @@ def lib() -> ctypes.CDLL:
         L.hydro_mass_v_solve.argtypes = [vp, vp, vp, dbl, i32, ctypes.POINTER(i32),
                                          ctypes.POINTER(dbl), vp]
         L.hydro_mass_e_solve.argtypes = [vp, vp, vp, vp]
+        L.hydro_mass_e_apply.argtypes = [vp, vp, vp, vp]
+        L.hydro_window_ops.argtypes = [vp, i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
         L.hydro_fom_energy.argtypes = [vp, vp, vp, ctypes.POINTER(dbl), ctypes.POINTER(dbl), vp]
         L.hydro_rk2avg_step.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, dbl, dbl, i32,
                                         ctypes.POINTER(dbl), ctypes.POINTER(i32), vp]
@@ -411,6 +413,25 @@ def rom_window_transition(T: torch.Tensor, c: torch.Tensor, Y: torch.Tensor,
     return rom_lift(T, c, Y, out=out, stream=stream)
 
 
+def window_ops(Phi_new: torch.Tensor, Phi_old: torch.Tensor, os_new: torch.Tensor,
+               os_old: torch.Tensor, fom: Optional["Fom"] = None, field: int = 0, stream=None):
+    """(T, c) of the time-window transition (hydro_window_ops): Eq. ic-tw when fom is None or
+    field == 0, the M-oblique Eq. ic2-tw with M_V (field 1) or M_E (field 2) otherwise.
+    Offsets [N] or [N][B]; returns device T [n_new][n_old], c [n_new][B]."""
+    N, n_new = Phi_new.shape
+    n_old = Phi_old.shape[1]
+    osn = (os_new if os_new.dim() == 2 else os_new.reshape(N, 1)).contiguous()
+    oso = (os_old if os_old.dim() == 2 else os_old.reshape(N, 1)).contiguous()
+    B = osn.shape[1]
+    T = torch.empty((n_new, n_old), dtype=torch.float64, device=Phi_new.device)
+    c = torch.empty((n_new, B), dtype=torch.float64, device=Phi_new.device)
+    Pn, Po = Phi_new.contiguous(), Phi_old.contiguous()
+    _check(lib().hydro_window_ops(fom._h if fom is not None else None, field, N, n_new, n_old, B, _ptr(Pn),
+                                  _ptr(Po), _ptr(osn), _ptr(oso), _ptr(T), _ptr(c), _stream(stream)),
+           "hydro_window_ops")
+    return T, c
+
+
 def rom_windowed_advance(windows, Yx, Yv, Ye, gamma, visc: Visc, cfl: Cfl, t0: float, dt,
                          ctrl: DtCtrl = DtCtrl(), max_iters=1000000, stream=None):
     """The time-windowing online phase: for each window advance with its own
@@ -527,6 +548,11 @@ class Fom:
         _check(lib().hydro_mass_v_solve(self._h, _ptr(rhs), _ptr(out), tol, max_iter, ctypes.byref(it),
                                         ctypes.byref(rel), _stream(stream)), "hydro_mass_v_solve")
         return out, it.value, rel.value
+
+    def mass_e(self, e, out=None, stream=None):
+        out = torch.empty_like(e) if out is None else out
+        _check(lib().hydro_mass_e_apply(self._h, _ptr(e), _ptr(out), _stream(stream)), "hydro_mass_e_apply")
+        return out
 
     def solve_e(self, rhs, out=None, stream=None):
         out = torch.empty_like(rhs) if out is None else out

@@ -110,5 +110,9 @@ def test_time_loop_and_offline_arguments_rejected_without_gpu():
     assert L.hydro_deim(None, 100, 4, idx, None) == ERR
     assert L.hydro_qdeim(None, 100, 4, idx, None) == ERR
     assert L.hydro_deim_oversampled(None, 100, 4, 8, idx, None) == ERR
+    assert L.hydro_mass_e_apply(None, None, None, None) == ERR
+    assert L.hydro_window_ops(None, 0, 100, 4, 4, 1, None, None, None, None, None, None, None) == ERR
+    vp8 = ctypes.c_void_p(8)
+    assert L.hydro_window_ops(None, 3, 100, 4, 4, 1, vp8, vp8, vp8, vp8, vp8, vp8, None) == ERR  # field
     assert L.hydro_deim_oversampled(ctypes.c_void_p(8), 100, 4, 3, idx, None) == ERR   # n_s < m
     assert L.hydro_fom_stage_state(None, None, None, None, None) == ERR

@@ -118,3 +118,54 @@ def test_P25_window_transition():
     np.testing.assert_allclose(os2[:, None] + Q2 @ Y2, os_[:, None] + Q @ Y, atol=1e-12)
     T, c = W.window_transition_ops(Q2, Q, os2, os_)
     np.testing.assert_allclose(T @ Y + c[:, None], Y2, atol=1e-12)
+
+
+def _orth(rng, N, k):
+    return np.linalg.qr(rng.standard_normal((N, k)))[0]
+
+
+def test_P35_oblique_transition_with_identity_mass_is_ic_tw():
+    """Eq. ic2-tw with M = I and an orthonormal new basis reduces to Eq. ic-tw."""
+    from oracle import rom
+    rng = np.random.default_rng(35)
+    N = 60
+    Pn, Po = _orth(rng, N, 5), _orth(rng, N, 4)
+    osn, oso = rng.standard_normal((N, 3)), rng.standard_normal((N, 3))
+    Y = rng.standard_normal((4, 3))
+    np.testing.assert_allclose(rom.window_transition_oblique(Pn, Po, osn, oso, Y, lambda a: a),
+                               rom.window_transition(Pn, Po, osn, oso, Y), atol=1e-13)
+
+
+def test_P36_oblique_transition_is_an_m_projector():
+    """For an SPD M (here a random SPD matrix, and the oracle's own FOM M_V and M_E): a lifted
+    state already in os_w + span(Phi_w) maps to its exact coordinates, and in general the
+    residual of the new window's lift is M-orthogonal to Phi_w (the Galerkin condition that
+    defines an oblique projection) -- a transposed operand or a dropped M fails one of them."""
+    from oracle import fom, rom
+    rng = np.random.default_rng(36)
+    prob = W.sedov_like(36, 2, (3, 2), (0.0, 0.0), (0.3, 0.2), delta=0.08, e_floor=1e-2,
+                        vmode="uniform", vscale=0.1, name="obl")
+    m = prob.mesh
+    Mv = fom.mass_v(m)
+    Me = fom.mass_e(m)
+    A = rng.standard_normal((40, 40))
+    cases = [(40, lambda a: (A @ A.T + 40 * np.eye(40)) @ a),
+             (Mv.shape[0], lambda a: Mv @ a),
+             (m.n_elem * m.ne, lambda a: np.einsum("eij,ejk->eik", Me,
+                                                   a.reshape(m.n_elem, m.ne, -1)).reshape(a.shape))]
+    for N, M in cases:
+        Pn, Po = _orth(rng, N, 6), _orth(rng, N, 5)
+        osn, oso = rng.standard_normal((N, 2)), rng.standard_normal((N, 2))
+        z = rng.standard_normal((6, 2))
+        # choose Y so that os_old + Phi_old Y - os_new = Phi_new z + (a part outside span(Phi_old))
+        Y = rng.standard_normal((5, 2))
+        lifted = oso + Po @ Y - osn
+        y = rom.window_transition_oblique(Pn, Po, osn, oso, Y, M)
+        r = lifted - Pn @ y
+        scale = np.abs(Pn.T @ M(lifted)).max()
+        np.testing.assert_allclose(Pn.T @ M(r), 0.0, atol=1e-12 * scale)
+        # exact reproduction: the old window is the new basis with an offset shifted inside
+        # its span, os_old = os_new + Phi_w w, so the lifted state is os_w + Phi_w (w + z)
+        w = rng.standard_normal((6, 1))
+        y2 = rom.window_transition_oblique(Pn, Pn, osn, osn + Pn @ w, z, M)
+        np.testing.assert_allclose(y2, z + w, atol=1e-12 * np.abs(z + w).max())
