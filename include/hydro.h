@@ -336,6 +336,21 @@ hydro_status hydro_deim_oversampled(const double *U, int64_t N, int m, int n_s, 
 hydro_status hydro_window_ops(hydro_fom *fom, int field, int64_t N, int n_new, int n_old, int B,
                               const double *Phi_new, const double *Phi_old, const double *os_new,
                               const double *os_old, double *T, double *c, hydro_stream_t stream);
+/* The integrands of the a-posteriori bound, Theorem 2 Eq. aposteriori-semi, at
+ * one (lifted) state (x, v, e) of a ROM trajectory (DESIGN R29):
+ *   eta[0] = | (I - M_V Phi_v Mhat_V^-1 Phi_v^T P_F1) F.1(x, v, e) |_2,
+ *   eta[1] = | (I - M_E Phi_e Mhat_E^-1 Phi_e^T P_Ftv) F^T.v(x, v, e) |_2,
+ * Mhat = Phi^T M Phi, P f = U (U[Z,:])^+ f[Z] the (gappy, least-squares when s > m) DEIM
+ * projector of the force basis U with sample rows Z.  The full-order force evaluation (w = v)
+ * runs on all elements; M_V without boundary masking.  Device: x, v, e, gamma (the fom's
+ * layouts), Phi_v [N_V][nv], Phi_e [N_E][ne], U1 [N_V][m1], U2 [N_E][m2]; host: Z1 [s1],
+ * Z2 [s2] (s >= m), eta [2].  HYDRO_ERR_TANGLED / _NONFINITE if the state is invalid or a
+ * small solve is singular.  Allocates its own scratch; synchronises `stream`.               */
+hydro_status hydro_rom_indicator(hydro_fom *fom, const double *x, const double *v, const double *e,
+                                 const double *gamma, hydro_visc visc, hydro_cfl cfl, int nv,
+                                 const double *Phi_v, int ne, const double *Phi_e, int m1, const double *U1,
+                                 int s1, const int64_t *Z1, int m2, const double *U2, int s2,
+                                 const int64_t *Z2, double *eta, hydro_stream_t stream);
 
 /* ------------------------------------------------------------------ profiling (host) */
 /* When enabled, every hydro_force_full / hydro_dt_estimate / hydro_force_sampled call

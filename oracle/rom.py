@@ -190,3 +190,38 @@ def windowed_advance(windows, Yx, Yv, Ye, t0, dt, beta1=0.85, beta2=1.02, gamma=
             Yv = window_transition(n["Phi_v"], o["Phi_v"], n["v_os"], o["v_os"], Yv)
             Ye = window_transition(n["Phi_e"], o["Phi_e"], n["e_os"], o["e_os"], Ye)
     return Yx, Yv, Ye, tB, h, stats
+
+
+def indicator_term(f, Phi, M, U, Z):
+    """One field of the Theorem-2 integrand (Eq. aposteriori-semi), as written:
+        | (I - M Phi Mhat^{-1} Phi^T P) f |_2,   Mhat = Phi^T M Phi,
+    with the DEIM projector P f = U (Z^T U)^+ Z^T f (numpy lstsq; the inverse when the
+    sample count equals the basis size).  M: function applying the field's mass
+    matrix to a [N][k] array."""
+    Z = np.asarray(Z, dtype=np.int64)
+    a = np.linalg.lstsq(U[Z], f[Z], rcond=None)[0]
+    Pf = U @ a
+    MPhi = M(Phi)
+    Mhat = Phi.T @ MPhi
+    z = np.linalg.solve(Mhat, Phi.T @ Pf)
+    return float(np.linalg.norm(f - MPhi @ z))
+
+
+def aposteriori_integrand(prob, x, v, e, Phi_v, Phi_e, U1, Z1, U2, Z2):
+    """(eta_v, eta_e): the two Theorem-2 integrands at the state (x, v, e) -- the full-order
+    F.1 and F^T.v (w = v) by the force oracle, M_V = I_dim (x) the scalar kinematic mass
+    matrix (velocity dofs c * n_nodes + node), M_E the element blocks (DESIGN R29)."""
+    from . import force as _f
+    from . import fom as _fom
+    m = prob.mesh
+    out = _f(prob, x=x, v=v, e=e, w=v)
+    F1 = np.asarray(out["F1"]).reshape(-1)
+    FTv = np.asarray(out["FTw"]).reshape(-1)
+    Mv, Me, n = _fom.mass_v(m), _fom.mass_e(m), m.n_nodes
+
+    def MV(a):
+        return np.concatenate([Mv @ a[c * n:(c + 1) * n] for c in range(m.dim)])
+
+    def ME(a):
+        return np.einsum("eij,ejk->eik", Me, a.reshape(m.n_elem, m.ne, -1)).reshape(a.shape)
+    return (indicator_term(F1, Phi_v, MV, U1, Z1), indicator_term(FTv, Phi_e, ME, U2, Z2))

@@ -2082,3 +2082,116 @@ hydro_status hydro_window_ops(hydro_fom *fom, int field, int64_t N, int n_new, i
 }
 
 }  // extern "C"
+
+namespace {
+
+// eta = | (I - M Phi Mhat^-1 Phi^T P) f |_2 with P f = U (U[Z,:])^+ f[Z]  (one field of the
+// Theorem-2 integrand).  f: device [N]; Phi [N][n]; U [N][m]; Z host [s].
+hydro_status indicator_field(hydro_fom *F, int field, int64_t N, const double *f, int n, const double *Phi,
+                             int m, const double *U, int s_rows, const int64_t *Z, double *eta,
+                             cudaStream_t s) {
+  double *W = nullptr, *tmp = nullptr, *G = nullptr, *gat = nullptr, *y = nullptr;
+  int64_t *dZ = nullptr;
+  auto cleanup = [&]() { cudaFree(W); cudaFree(tmp); cudaFree(G); cudaFree(gat); cudaFree(y); cudaFree(dZ); };
+  if (cudaMalloc(&W, sizeof(double) * (size_t)N * n) != cudaSuccess ||
+      cudaMalloc(&tmp, sizeof(double) * (size_t)N * 2) != cudaSuccess ||
+      cudaMalloc(&G, sizeof(double) * std::max<size_t>((size_t)n * (n + 1), (size_t)N)) != cudaSuccess ||
+      cudaMalloc(&gat, sizeof(double) * (size_t)s_rows * (m + 1)) != cudaSuccess ||
+      cudaMalloc(&y, sizeof(double) * (size_t)(m > n ? m : n)) != cudaSuccess ||
+      cudaMalloc(&dZ, sizeof(int64_t) * (size_t)s_rows) != cudaSuccess) {
+    cleanup();
+    return HYDRO_ERR_CUDA;
+  }
+  hydro_status st = HYDRO_OK;
+  const unsigned g = blocks_for(N, 256);
+  // P f: least-squares fit of the sampled rows
+  std::vector<double> hU((size_t)s_rows * m), hf((size_t)s_rows);
+  if (cudaMemcpyAsync(dZ, Z, sizeof(int64_t) * s_rows, cudaMemcpyHostToDevice, s) != cudaSuccess) st = HYDRO_ERR_CUDA;
+  if (st == HYDRO_OK) {
+    hk::gather_rows_kernel<<<(s_rows * m + 255) / 256, 256, 0, s>>>(s_rows, m, dZ, U, m, gat);
+    hk::gather_rows_kernel<<<(s_rows + 255) / 256, 256, 0, s>>>(s_rows, 1, dZ, f, 1, gat + (size_t)s_rows * m);
+    g_launches += 2;
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(hU.data(), gat, sizeof(double) * hU.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(hf.data(), gat + (size_t)s_rows * m, sizeof(double) * s_rows, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      st = HYDRO_ERR_CUDA;
+  }
+  if (st == HYDRO_OK && !lstsq_host(s_rows, m, hU, hf)) st = HYDRO_ERR_NONFINITE;
+  if (st == HYDRO_OK) {  // tmp = U a
+    if (cudaMemcpyAsync(y, hf.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s) != cudaSuccess) st = HYDRO_ERR_CUDA;
+    hk::gemv_kernel<<<g, 256, 0, s>>>(N, m, U, m, y, nullptr, -1.0, tmp);
+    g_launches++;
+  }
+  // W = M Phi, column by column
+  for (int j = 0; j < n && st == HYDRO_OK; ++j) {
+    // column j -> contiguous scratch -> mass apply -> column j of W
+    hk::col_copy_kernel<<<g, 256, 0, s>>>(N, Phi + j, n, tmp + N, 1);
+    g_launches++;
+    st = field == 1 ? mass_apply(F, tmp + N, G, nullptr, 0, 0, s) : hydro_mass_e_apply(F, tmp + N, G, s);
+    if (st == HYDRO_OK) {
+      hk::col_copy_kernel<<<g, 256, 0, s>>>(N, G, 1, W + j, n);
+      g_launches++;
+      if (cudaGetLastError() != cudaSuccess) st = HYDRO_ERR_CUDA;
+    }
+  }
+  // [Mhat | b] = Phi^T [W | U a]
+  if (st == HYDRO_OK) st = xprod(N, n, Phi, n, n, W, n, G, s);
+  if (st == HYDRO_OK) st = xprod(N, n, Phi, n, 1, tmp, 1, G + (size_t)n * n, s);
+  std::vector<double> hG((size_t)n * (n + 1));
+  if (st == HYDRO_OK &&
+      (cudaMemcpyAsync(hG.data(), G, sizeof(double) * hG.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+       cudaStreamSynchronize(s) != cudaSuccess))
+    st = HYDRO_ERR_CUDA;
+  if (st == HYDRO_OK) {
+    std::vector<double> A(hG.begin(), hG.begin() + (size_t)n * n), b(hG.begin() + (size_t)n * n, hG.end());
+    if (!lu_solve_host(n, A, b)) st = HYDRO_ERR_NONFINITE;
+    else if (cudaMemcpyAsync(y, b.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      st = HYDRO_ERR_CUDA;
+  }
+  if (st == HYDRO_OK) {  // r = f - W z;  eta = |r|
+    hk::gemv_kernel<<<g, 256, 0, s>>>(N, n, W, n, y, f, 1.0, tmp + N);
+    g_launches++;
+    st = dot(F, N, tmp + N, tmp + N, F->sc + 5, s);
+  }
+  double h = 0.0;
+  if (st == HYDRO_OK &&
+      (cudaMemcpyAsync(&h, F->sc + 5, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+       cudaStreamSynchronize(s) != cudaSuccess))
+    st = HYDRO_ERR_CUDA;
+  if (st == HYDRO_OK) *eta = std::sqrt(h);
+  cudaStreamSynchronize(s);
+  cleanup();
+  return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+hydro_status hydro_rom_indicator(hydro_fom *fom, const double *x, const double *v, const double *e,
+                                 const double *gamma, hydro_visc visc, hydro_cfl cfl, int nv,
+                                 const double *Phi_v, int ne, const double *Phi_e, int m1, const double *U1,
+                                 int s1, const int64_t *Z1, int m2, const double *U2, int s2,
+                                 const int64_t *Z2, double *eta, hydro_stream_t stream) {
+  if (!fom || !x || !v || !e || !gamma || !Phi_v || !Phi_e || !U1 || !U2 || !Z1 || !Z2 || !eta ||
+      nv <= 0 || ne <= 0 || m1 <= 0 || m2 <= 0 || s1 < m1 || s2 < m2 || nv > 1024 || ne > 1024 ||
+      m1 > 4096 || m2 > 4096)
+    return HYDRO_ERR_ARG;
+  const int64_t NV = fom->n, NE = fom->c->d.n_elem * fom->c->ne;
+  for (int i = 0; i < s1; ++i)
+    if (Z1[i] < 0 || Z1[i] >= NV) return HYDRO_ERR_ARG;
+  for (int i = 0; i < s2; ++i)
+    if (Z2[i] < 0 || Z2[i] >= NE) return HYDRO_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  hydro_status st = force_common(fom->c, hk::MODE_FORCE, x, v, e, v, gamma, visc, cfl, fom->F1, fom->FTw,
+                                 fom->dts, s);
+  if (st != HYDRO_OK) return st;
+  std::vector<char> bad;
+  if ((st = read_reset_status(fom->c->st, 1, s, bad)) != HYDRO_OK) return st;
+  if (bad[0]) return HYDRO_ERR_TANGLED;
+  if ((st = indicator_field(fom, 1, NV, fom->F1, nv, Phi_v, m1, U1, s1, Z1, &eta[0], s)) != HYDRO_OK) return st;
+  return indicator_field(fom, 2, NE, fom->FTw, ne, Phi_e, m2, U2, s2, Z2, &eta[1], s);
+}
+
+}  // extern "C"

@@ -257,4 +257,25 @@ __global__ void sub_kernel(int64_t n, const double *__restrict__ a, const double
   if (i < n) d[i] = a[i] - b[i];
 }
 
+// out[r] = (f ? f[r] : 0) - sgn * sum_j A[r][j] y[j]   (A: [N][lda], first n columns)
+__global__ void gemv_kernel(int64_t N, int n, const double *__restrict__ A, int64_t lda,
+                            const double *__restrict__ y, const double *__restrict__ f, double sgn,
+                            double *__restrict__ out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  const double *a = A + r * lda;
+  double acc = 0.0;
+  for (int j = 0; j < n; ++j) acc = __fma_rn(a[j], y[j], acc);
+  out[r] = (f ? f[r] : 0.0) - sgn * acc;
+}
+
+// out[i][j] = A[idx[i]][j]  (i < s, j < n; A: [N][lda])
+__global__ void gather_rows_kernel(int s, int n, const int64_t *__restrict__ idx,
+                                   const double *__restrict__ A, int64_t lda, double *__restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= s * n) return;
+  const int i = t / n, j = t % n;
+  out[t] = A[idx[i] * lda + j];
+}
+
 }  // namespace hk

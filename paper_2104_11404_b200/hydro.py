@@ -33,7 +33,7 @@ EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy"
             "hydro_profile_release_captured", "hydro_selftest_ieee_fast",
             "hydro_fom_create", "hydro_fom_destroy", "hydro_mass_v_apply", "hydro_mass_v_solve",
             "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_fom_advance", "hydro_rom_advance", "hydro_rom_create",
-            "hydro_fom_stage_state", "hydro_pod", "hydro_deim", "hydro_qdeim", "hydro_deim_oversampled", "hydro_mass_e_apply", "hydro_window_ops",
+            "hydro_fom_stage_state", "hydro_pod", "hydro_deim", "hydro_qdeim", "hydro_deim_oversampled", "hydro_mass_e_apply", "hydro_window_ops", "hydro_rom_indicator",
             "hydro_rom_destroy", "hydro_rom_rk2avg_step", "hydro_force_stress_bytes",
             "hydro_force_full_store", "hydro_force_transpose", "hydro_sample_stress_bytes",
             "hydro_force_sampled_store", "hydro_sample_force_transpose"]
@@ -100,6 +100,9 @@ def lib() -> ctypes.CDLL:
         L.hydro_mass_e_solve.argtypes = [vp, vp, vp, vp]
         L.hydro_mass_e_apply.argtypes = [vp, vp, vp, vp]
         L.hydro_window_ops.argtypes = [vp, i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
+        L.hydro_rom_indicator.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, i32, vp, i32, vp, i32, vp, i32,
+                                          ctypes.POINTER(i64), i32, vp, i32, ctypes.POINTER(i64),
+                                          ctypes.POINTER(ctypes.c_double), vp]
         L.hydro_fom_energy.argtypes = [vp, vp, vp, ctypes.POINTER(dbl), ctypes.POINTER(dbl), vp]
         L.hydro_rk2avg_step.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, dbl, dbl, i32,
                                         ctypes.POINTER(dbl), ctypes.POINTER(i32), vp]
@@ -553,6 +556,20 @@ class Fom:
         out = torch.empty_like(e) if out is None else out
         _check(lib().hydro_mass_e_apply(self._h, _ptr(e), _ptr(out), _stream(stream)), "hydro_mass_e_apply")
         return out
+
+    def indicator(self, x, v, e, gamma, visc: Visc, cfl: Cfl, Phi_v, Phi_e, U1, Z1, U2, Z2, stream=None):
+        """Theorem-2 integrands (eta_v, eta_e) at the state (x, v, e) -- hydro_rom_indicator."""
+        Z1 = [int(i) for i in Z1]
+        Z2 = [int(i) for i in Z2]
+        z1, z2 = (ctypes.c_int64 * len(Z1))(*Z1), (ctypes.c_int64 * len(Z2))(*Z2)
+        eta = (ctypes.c_double * 2)()
+        ops = [t.contiguous() for t in (Phi_v, Phi_e, U1, U2)]
+        _check(lib().hydro_rom_indicator(self._h, _ptr(x), _ptr(v), _ptr(e), _ptr(gamma), visc.c(), cfl.c(),
+                                         ops[0].shape[1], _ptr(ops[0]), ops[1].shape[1], _ptr(ops[1]),
+                                         ops[2].shape[1], _ptr(ops[2]), len(Z1), z1, ops[3].shape[1],
+                                         _ptr(ops[3]), len(Z2), z2, eta, _stream(stream)),
+               "hydro_rom_indicator")
+        return eta[0], eta[1]
 
     def solve_e(self, rhs, out=None, stream=None):
         out = torch.empty_like(rhs) if out is None else out

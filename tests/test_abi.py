@@ -111,6 +111,10 @@ def test_time_loop_and_offline_arguments_rejected_without_gpu():
     assert L.hydro_qdeim(None, 100, 4, idx, None) == ERR
     assert L.hydro_deim_oversampled(None, 100, 4, 8, idx, None) == ERR
     assert L.hydro_mass_e_apply(None, None, None, None) == ERR
+    z = (ctypes.c_int64 * 2)(0, 1)
+    eta = (ctypes.c_double * 2)()
+    assert L.hydro_rom_indicator(None, None, None, None, None, visc, cfl, 2, None, 2, None, 2, None, 2, z,
+                                 2, None, 2, z, eta, None) == ERR
     assert L.hydro_window_ops(None, 0, 100, 4, 4, 1, None, None, None, None, None, None, None) == ERR
     vp8 = ctypes.c_void_p(8)
     assert L.hydro_window_ops(None, 3, 100, 4, 4, 1, vp8, vp8, vp8, vp8, vp8, vp8, None) == ERR  # field

@@ -169,3 +169,43 @@ def test_P36_oblique_transition_is_an_m_projector():
         w = rng.standard_normal((6, 1))
         y2 = rom.window_transition_oblique(Pn, Pn, osn, osn + Pn @ w, z, M)
         np.testing.assert_allclose(y2, z + w, atol=1e-12 * np.abs(z + w).max())
+
+
+def test_P37_indicator_vanishes_for_full_bases(oracle_lib):
+    """Theorem 2's integrands vanish when the ROM is the FOM: Phi = I, U = I with every row
+    sampled (P = I, M Phi Mhat^-1 Phi^T = M M^-1 = I) -- at a real state, through the force
+    oracle."""
+    from oracle import rom
+    prob = W.sedov_like(37, 2, (3, 2), (0.0, 0.0), (0.3, 0.2), delta=0.08, e_floor=1e-2,
+                        vmode="uniform", vscale=0.1, name="ind")
+    m = prob.mesh
+    NV, NE = m.dim * m.n_nodes, m.n_elem * m.ne
+    ev, ee = rom.aposteriori_integrand(prob, prob.x, prob.v, prob.e, np.eye(NV), np.eye(NE),
+                                       np.eye(NV), np.arange(NV), np.eye(NE), np.arange(NE))
+    import oracle
+    out = oracle.force(prob, w=prob.v)
+    assert ev <= 1e-12 * np.abs(out["F1"]).sum() and ee <= 1e-12 * np.abs(out["FTw"]).sum()
+
+
+def test_P38_indicator_with_sns_basis_is_the_distance_to_its_span():
+    """With the SNS force basis U = M Phi sampled on every row, P is the
+    orthogonal projector onto span(M Phi) and M Phi Mhat^-1 Phi^T P = P, so the integrand is
+    the Euclidean distance of f from span(M Phi) -- computed independently from an
+    orthonormal basis of that span (QR); zero for f inside it."""
+    from oracle import rom
+    rng = np.random.default_rng(38)
+    N, n = 50, 6
+    A = rng.standard_normal((N, N))
+    Mmat = A @ A.T + N * np.eye(N)
+    M = lambda a: Mmat @ a  # noqa: E731
+    Phi = np.linalg.qr(rng.standard_normal((N, n)))[0]
+    U = Mmat @ Phi
+    f = rng.standard_normal(N)
+    Q = np.linalg.qr(U)[0]
+    dist = np.linalg.norm(f - Q @ (Q.T @ f))
+    assert abs(rom.indicator_term(f, Phi, M, U, np.arange(N)) - dist) <= 1e-12 * np.linalg.norm(f)
+    g = U @ rng.standard_normal(n)
+    assert rom.indicator_term(g, Phi, M, U, np.arange(N)) <= 1e-12 * np.linalg.norm(g)
+    # DEIM sampling (n rows) of an SNS basis still reproduces anything in its span exactly
+    from oracle import offline
+    assert rom.indicator_term(g, Phi, M, U, offline.deim(U)) <= 1e-11 * np.linalg.norm(g)
