@@ -592,7 +592,8 @@ def bench_fom(name, args, dev):
     st = ctx.status_sync()
     E1 = sum(fom.energy(v, e))
     step_ms = float(np.median(ms))
-    return {"workload": f"fom_{name}", "ms_per_step": step_ms,
+    extra = _bench_rom_fullrow_ops(fom, x, v, e, g, visc, cfl, dev) if name == "c2" else {}
+    return {"workload": f"fom_{name}", "ms_per_step": step_ms, **extra,
             "force_evals_per_step": 2, "transpose_passes_per_step": 2,
             "force_ms_per_step": kern_ms / max(len(ms), 1),
             "cg_iterations_per_step": float(np.mean(iters)), "cg_tol": 1e-12,
@@ -600,6 +601,41 @@ def bench_fom(name, args, dev):
             "rel_energy_drift": abs(E1 - E0) / E0, "status": st[0],
             "what": "RK2-average step (PAPER P:463-508): 2 force evaluations storing S_q + 2 "
                     "F^T w passes from S_q, 2 PCG solves of M_V, 2 M_E block solves, v.n=0"}
+
+
+def _bench_rom_fullrow_ops(fom, x, v, e, g, visc, cfl, dev, n=20, m=40):
+    """Full-row ROM operators on the FOM mesh (seeded random orthonormal bases, n state and m
+    force columns per field, DEIM rows): the Theorem-2 integrands (hydro_rom_indicator, one
+    full force evaluation + 2n mass applications + products) and the M-oblique window
+    transition operators of the velocity (hydro_window_ops, Eq. ic2-tw).  Wall time per
+    call with CUDA events (both synchronise)."""
+    import torch
+    from paper_2104_11404_b200 import hydro
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(2104)
+
+    def orth(N, k):
+        return torch.linalg.qr(torch.randn((N, k), generator=gen, device=dev, dtype=torch.float64))[0].contiguous()
+    NV, NE = v.numel(), e.numel()
+    Pv, Pe, U1, U2 = orth(NV, n), orth(NE, n), orth(NV, m), orth(NE, m)
+    Z1, Z2 = hydro.deim(U1), hydro.deim(U2)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fom.indicator(x, v, e, g, visc, cfl, Pv, Pe, U1, Z1, U2, Z2)
+    a.record()
+    eta = fom.indicator(x, v, e, g, visc, cfl, Pv, Pe, U1, Z1, U2, Z2)
+    b.record()
+    torch.cuda.synchronize()
+    ind_ms = a.elapsed_time(b)
+    Po = orth(NV, n)
+    osn = torch.randn((NV, 1), generator=gen, device=dev, dtype=torch.float64)
+    oso = torch.randn((NV, 1), generator=gen, device=dev, dtype=torch.float64)
+    a.record()
+    hydro.window_ops(Pv, Po, osn, oso, fom=fom, field=1)
+    b.record()
+    torch.cuda.synchronize()
+    return {"indicator_ms": ind_ms, "indicator_eta": [float(eta[0]), float(eta[1])],
+            "window_ops_oblique_v_ms": a.elapsed_time(b), "fullrow_basis_cols": n,
+            "fullrow_force_basis_cols": m}
 
 
 def bench_offline(args, dev, ns=64, m=40):
