@@ -346,6 +346,13 @@ hydro_status hydro_window_ops(hydro_fom *fom, int field, int64_t N, int n_new, i
  * layouts), Phi_v [N_V][nv], Phi_e [N_E][ne], U1 [N_V][m1], U2 [N_E][m2]; host: Z1 [s1],
  * Z2 [s2] (s >= m), eta [2].  HYDRO_ERR_TANGLED / _NONFINITE if the state is invalid or a
  * small solve is singular.  Allocates its own scratch; synchronises `stream`.               */
+/* dst[c * ld_dst + dst_idx[i]] = (add ? that + : ) src[c * ld_src + src_idx[i]], i < n, c < dim
+ * (NULL index = identity): the gather, fixed-order accumulate and scatter steps of the
+ * slab-sharded force's halo sum (paper_2104_11404_b200/shard.py).  Device
+ * pointers; the dst indices of one call must be distinct.  Asynchronous on `stream`.        */
+hydro_status hydro_index_copy_add(int64_t n, int dim, const double *src, int64_t ld_src,
+                                  const int64_t *src_idx, double *dst, int64_t ld_dst,
+                                  const int64_t *dst_idx, int add, hydro_stream_t stream);
 hydro_status hydro_rom_indicator(hydro_fom *fom, const double *x, const double *v, const double *e,
                                  const double *gamma, hydro_visc visc, hydro_cfl cfl, int nv,
                                  const double *Phi_v, int ne, const double *Phi_e, int m1, const double *U1,

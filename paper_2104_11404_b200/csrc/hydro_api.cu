@@ -2195,3 +2195,20 @@ hydro_status hydro_rom_indicator(hydro_fom *fom, const double *x, const double *
 }
 
 }  // extern "C"
+
+extern "C" {
+
+hydro_status hydro_index_copy_add(int64_t n, int dim, const double *src, int64_t ld_src,
+                                  const int64_t *src_idx, double *dst, int64_t ld_dst,
+                                  const int64_t *dst_idx, int add, hydro_stream_t stream) {
+  if (n < 0 || dim <= 0 || dim > 3 || ld_src < 0 || ld_dst < 0) return HYDRO_ERR_ARG;
+  if (n == 0) return HYDRO_OK;
+  if (!src || !dst) return HYDRO_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  hk::index_copy_add_kernel<<<blocks_for(n * dim, 256), 256, 0, s>>>(n, dim, src, ld_src, src_idx, dst, ld_dst,
+                                                                      dst_idx, add);
+  g_launches++;
+  return cudaGetLastError() == cudaSuccess ? HYDRO_OK : HYDRO_ERR_CUDA;
+}
+
+}  // extern "C"

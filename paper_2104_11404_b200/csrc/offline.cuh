@@ -278,4 +278,20 @@ __global__ void gather_rows_kernel(int s, int n, const int64_t *__restrict__ idx
   out[t] = A[idx[i] * lda + j];
 }
 
+// dst[c * ld_dst + di] (+)= src[c * ld_src + si] for i < n, c < dim, with si = src_idx[i] (or
+// i) and di = dst_idx[i] (or i) -- the gather / fixed-order accumulate / scatter of the
+// sharded force's halo sum.  Indices within one call are distinct (no write conflicts).
+__global__ void index_copy_add_kernel(int64_t n, int dim, const double *__restrict__ src, int64_t ld_src,
+                                      const int64_t *__restrict__ src_idx, double *__restrict__ dst,
+                                      int64_t ld_dst, const int64_t *__restrict__ dst_idx, int add) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * dim) return;
+  const int c = (int)(t / n);
+  const int64_t i = t % n;
+  const int64_t si = src_idx ? src_idx[i] : i, di = dst_idx ? dst_idx[i] : i;
+  const double v = src[c * ld_src + si];
+  double *d = dst + c * ld_dst + di;
+  *d = add ? *d + v : v;
+}
+
 }  // namespace hk

@@ -33,7 +33,7 @@ EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy"
             "hydro_profile_release_captured", "hydro_selftest_ieee_fast",
             "hydro_fom_create", "hydro_fom_destroy", "hydro_mass_v_apply", "hydro_mass_v_solve",
             "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_fom_advance", "hydro_rom_advance", "hydro_rom_create",
-            "hydro_fom_stage_state", "hydro_pod", "hydro_deim", "hydro_qdeim", "hydro_deim_oversampled", "hydro_mass_e_apply", "hydro_window_ops", "hydro_rom_indicator",
+            "hydro_fom_stage_state", "hydro_pod", "hydro_deim", "hydro_qdeim", "hydro_deim_oversampled", "hydro_mass_e_apply", "hydro_window_ops", "hydro_rom_indicator", "hydro_index_copy_add",
             "hydro_rom_destroy", "hydro_rom_rk2avg_step", "hydro_force_stress_bytes",
             "hydro_force_full_store", "hydro_force_transpose", "hydro_sample_stress_bytes",
             "hydro_force_sampled_store", "hydro_sample_force_transpose"]
@@ -100,6 +100,7 @@ def lib() -> ctypes.CDLL:
         L.hydro_mass_e_solve.argtypes = [vp, vp, vp, vp]
         L.hydro_mass_e_apply.argtypes = [vp, vp, vp, vp]
         L.hydro_window_ops.argtypes = [vp, i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
+        L.hydro_index_copy_add.argtypes = [i64, i32, vp, i64, vp, vp, i64, vp, i32, vp]
         L.hydro_rom_indicator.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, i32, vp, i32, vp, i32, vp, i32,
                                           ctypes.POINTER(i64), i32, vp, i32, ctypes.POINTER(i64),
                                           ctypes.POINTER(ctypes.c_double), vp]
@@ -414,6 +415,14 @@ def rom_window_transition(T: torch.Tensor, c: torch.Tensor, Y: torch.Tensor,
     (P:1223-1264): Y_w = T Y_{w-1} + c with the offline T [n_w][n_{w-1}] and c ([n_w] or
     [n_w][B]) -- the lift primitive (hydro_rom_lift) on reduced dimensions."""
     return rom_lift(T, c, Y, out=out, stream=stream)
+
+
+def index_copy_add(n: int, dim: int, src: torch.Tensor, ld_src: int, src_idx, dst: torch.Tensor,
+                   ld_dst: int, dst_idx, add: bool, stream=None):
+    """dst[c, dst_idx[i]] (+)= src[c, src_idx[i]] over [dim][ld] row blocks -- hydro_index_copy_add.
+    Index tensors: device int64 or None (identity)."""
+    _check(lib().hydro_index_copy_add(n, dim, _ptr(src), ld_src, _ptr(src_idx), _ptr(dst), ld_dst,
+                                      _ptr(dst_idx), 1 if add else 0, _stream(stream)), "hydro_index_copy_add")
 
 
 def window_ops(Phi_new: torch.Tensor, Phi_old: torch.Tensor, os_new: torch.Tensor,
