@@ -1337,12 +1337,18 @@ __global__ void assemble_kernel(int64_t n_nodes, int B, const int32_t *__restric
     const int64_t node = B == 1 ? t : t / B;
     const int b = B == 1 ? 0 : (int)(t % B);
     const int s0 = off[node], s1 = off[node + 1];
+    // one pass over the node's slots for all components (each component still summed in
+    // ascending slot order: the same bits as a per-component pass)
+    double acc[DIM];
 #pragma unroll
-    for (int c = 0; c < DIM; ++c) {
-      double acc = 0.0;
-      for (int s = s0; s < s1; ++s) acc += evec[((int64_t)s * DIM + c) * B + b];
-      F1[((int64_t)c * n_nodes + node) * B + b] = acc;
+    for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
+    for (int s = s0; s < s1; ++s) {
+      const double *e = evec + (int64_t)s * DIM * B + b;
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) acc[c] += e[(int64_t)c * B];
     }
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) F1[((int64_t)c * n_nodes + node) * B + b] = acc[c];
   }
   if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < B; i += blockDim.x) finalize_one(st + i, dt_out ? dt_out + i : nullptr);
