@@ -163,8 +163,11 @@ struct G2 {
   static constexpr size_t SMEM = sizeof(double) * (size_t)(NF * 2 * 9 + 18 + 4) * NT;
 };
 
+#ifndef F2D_MAXNREG
+#define F2D_MAXNREG 128
+#endif
 template <bool VISC, int MODE, bool BATCHED, bool HAS_W>
-__global__ void __maxnreg__(128) force2d_kernel(const Params P) {
+__global__ void __maxnreg__(F2D_MAXNREG) force2d_kernel(const Params P) {
   constexpr int NF = HAS_W ? 3 : 2;
   constexpr int ND = 9, NE = 4, NQ = 16, NT = F2D_NT;
   constexpr int NX = NF * 2 * ND;
