@@ -15,7 +15,10 @@
  * reading implemented here, and DESIGN.md "Evaluation contract" fixes the
  * operation order that makes dt bit-reproducible.  Around the hot path:
  * the full-order RK2-average step and time loop, the ROM online step, loop
- * and time windows and the offline POD/DEIM.
+ * and time windows with the orthogonal and M-oblique transitions (P:847-906,
+ * P:1175-1264), the offline POD / DEIM / Q-DEIM / oversampled sampling, the
+ * Theorem-2 a-posteriori integrands and the index primitive of the
+ * slab-sharded force's halo sum.  DESIGN.md R1-R29 list the readings.
  *
  * Conventions (all entry points):
  *   - FP64 everywhere; indices int32 (element->node table) / int64 (sizes).
