@@ -1841,6 +1841,38 @@ hydro_status hydro_deim(const double *U, int64_t N, int m, int64_t *idx, hydro_s
 
 }  // extern "C"
 
+namespace {
+
+// [N][m] row-major -> [m][N] (tiled, coalesced both ways)
+void transpose(int64_t N, int64_t m, const double *A, double *At, cudaStream_t s) {
+  const int64_t tiles = ((N + 31) / 32) * ((m + 31) / 32);
+  hk::transpose_kernel<<<(unsigned)tiles, dim3(32, 8), 0, s>>>(N, m, A, At);
+  g_launches++;
+}
+
+// W = M Phi for the n columns of Phi [N][n] (field 1: M_V, 2: M_E): one tiled transpose to
+// [n][N] so every column is a contiguous vector for the mass operator, n applications into
+// a second [n][N] buffer, one transpose back.  (Column-by-column strided copies read a
+// 32-byte sector per 8-byte value: 110 us per C2 column, profiles/fom/r01_fom_step_v3_*.)
+hydro_status mass_columns(hydro_fom *F, int field, int64_t N, int n, const double *Phi, double *W,
+                          cudaStream_t s) {
+  double *T = nullptr;
+  if (cudaMalloc(&T, sizeof(double) * (size_t)N * n * 2) != cudaSuccess) return HYDRO_ERR_CUDA;
+  double *T2 = T + (size_t)N * n;
+  transpose(N, n, Phi, T, s);
+  hydro_status st = HYDRO_OK;
+  for (int j = 0; j < n && st == HYDRO_OK; ++j)
+    st = field == 1 ? mass_apply(F, T + (size_t)j * N, T2 + (size_t)j * N, nullptr, 0, 0, s)
+                    : hydro_mass_e_apply(F, T + (size_t)j * N, T2 + (size_t)j * N, s);
+  if (st == HYDRO_OK) transpose(n, N, T2, W, s);
+  if (st == HYDRO_OK && cudaGetLastError() != cudaSuccess) st = HYDRO_ERR_CUDA;
+  cudaStreamSynchronize(s);
+  cudaFree(T);
+  return st;
+}
+
+}  // namespace
+
 extern "C" {
 
 hydro_status hydro_qdeim(const double *U, int64_t N, int m, int64_t *idx, hydro_stream_t stream) {
@@ -1856,8 +1888,7 @@ hydro_status hydro_qdeim(const double *U, int64_t N, int m, int64_t *idx, hydro_
     cleanup();
     return HYDRO_ERR_CUDA;
   }
-  hk::transpose_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((m + 31) / 32)), dim3(32, 8), 0, s>>>(
-      N, m, U, Rt);
+  transpose(N, m, U, Rt, s);
   g_launches++;
   std::vector<double> hv(hk::DEIM_BLOCKS), row((size_t)m);
   std::vector<int64_t> hi(hk::DEIM_BLOCKS);
@@ -2016,22 +2047,11 @@ hydro_status hydro_window_ops(hydro_fom *fom, int field, int64_t N, int n_new, i
   hydro_status st = HYDRO_OK;
   const double *Wp = Phi_new;
   if (oblique) {  // W = M Phi_new, column by column through the FOM's own mass operators
-    if (cudaMalloc(&W, sizeof(double) * (size_t)N * n_new) != cudaSuccess ||
-        cudaMalloc(&tmp, sizeof(double) * (size_t)N * 2) != cudaSuccess) {
+    if (cudaMalloc(&W, sizeof(double) * (size_t)N * n_new) != cudaSuccess) {
       cleanup();
       return HYDRO_ERR_CUDA;
     }
-    const unsigned g = blocks_for(N, 256);
-    for (int j = 0; j < n_new && st == HYDRO_OK; ++j) {
-      hk::col_copy_kernel<<<g, 256, 0, s>>>(N, Phi_new + j, n_new, tmp, 1);
-      g_launches++;
-      st = field == 1 ? mass_apply(fom, tmp, tmp + N, nullptr, 0, 0, s)
-                      : hydro_mass_e_apply(fom, tmp, tmp + N, stream);
-      if (st != HYDRO_OK) break;
-      hk::col_copy_kernel<<<g, 256, 0, s>>>(N, tmp + N, 1, W + j, n_new);
-      g_launches++;
-      if (cudaGetLastError() != cudaSuccess) st = HYDRO_ERR_CUDA;
-    }
+    st = mass_columns(fom, field, N, n_new, Phi_new, W, s);
     Wp = W;
   }
   if (st == HYDRO_OK) {
@@ -2123,18 +2143,8 @@ hydro_status indicator_field(hydro_fom *F, int field, int64_t N, const double *f
     hk::gemv_kernel<<<g, 256, 0, s>>>(N, m, U, m, y, nullptr, -1.0, tmp);
     g_launches++;
   }
-  // W = M Phi, column by column
-  for (int j = 0; j < n && st == HYDRO_OK; ++j) {
-    // column j -> contiguous scratch -> mass apply -> column j of W
-    hk::col_copy_kernel<<<g, 256, 0, s>>>(N, Phi + j, n, tmp + N, 1);
-    g_launches++;
-    st = field == 1 ? mass_apply(F, tmp + N, G, nullptr, 0, 0, s) : hydro_mass_e_apply(F, tmp + N, G, s);
-    if (st == HYDRO_OK) {
-      hk::col_copy_kernel<<<g, 256, 0, s>>>(N, G, 1, W + j, n);
-      g_launches++;
-      if (cudaGetLastError() != cudaSuccess) st = HYDRO_ERR_CUDA;
-    }
-  }
+  // W = M Phi
+  if (st == HYDRO_OK) st = mass_columns(F, field, N, n, Phi, W, s);
   // [Mhat | b] = Phi^T [W | U a]
   if (st == HYDRO_OK) st = xprod(N, n, Phi, n, n, W, n, G, s);
   if (st == HYDRO_OK) st = xprod(N, n, Phi, n, 1, tmp, 1, G + (size_t)n * n, s);

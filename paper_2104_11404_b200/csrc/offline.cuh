@@ -186,22 +186,24 @@ __global__ void __launch_bounds__(DEIM_THREADS) qdeim_step_kernel(
   if (threadIdx.x == 0) { bval[blockIdx.x] = sv[0]; bidx[blockIdx.x] = si[0]; }
 }
 
-// [N][m] row-major -> [m][N] (Q-DEIM's working layout), 32x32 tiles through shared memory.
-__global__ void transpose_kernel(int64_t N, int m, const double *__restrict__ A,
+// [N][m] row-major -> [m][N], 32x32 tiles through shared memory; a 1D grid of
+// ceil(N/32) * ceil(m/32) tiles (row tile fastest), so either extent may be large.
+__global__ void transpose_kernel(int64_t N, int64_t m, const double *__restrict__ A,
                                  double *__restrict__ At) {
   __shared__ double t[32][33];
-  const int64_t r0 = (int64_t)blockIdx.x * 32;
-  const int j0 = blockIdx.y * 32;
+  const int64_t tiles_r = (N + 31) / 32;
+  const int64_t r0 = ((int64_t)blockIdx.x % tiles_r) * 32;
+  const int64_t j0 = ((int64_t)blockIdx.x / tiles_r) * 32;
   for (int i = threadIdx.y; i < 32; i += 8) {
     const int64_t r = r0 + i;
-    const int j = j0 + threadIdx.x;
+    const int64_t j = j0 + threadIdx.x;
     if (r < N && j < m) t[i][threadIdx.x] = A[r * m + j];
   }
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += 8) {
-    const int j = j0 + i;
+    const int64_t j = j0 + i;
     const int64_t r = r0 + threadIdx.x;
-    if (r < N && j < m) At[(int64_t)j * N + r] = t[threadIdx.x][i];
+    if (r < N && j < m) At[j * N + r] = t[threadIdx.x][i];
   }
 }
 
