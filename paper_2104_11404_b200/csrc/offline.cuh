@@ -245,13 +245,6 @@ __global__ void xprod_reduce_kernel(int na, int nx, int chunks, const double *__
   G[t] = acc;
 }
 
-// dst[r * ldd] = src[r * lds] (one column of a row-major matrix to / from a vector)
-__global__ void col_copy_kernel(int64_t N, const double *__restrict__ src, int64_t lds,
-                                double *__restrict__ dst, int64_t ldd) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < N) dst[r * ldd] = src[r * lds];
-}
-
 // d = a - b (elementwise; the offset difference of a window transition)
 __global__ void sub_kernel(int64_t n, const double *__restrict__ a, const double *__restrict__ b,
                            double *__restrict__ d) {
