@@ -125,18 +125,25 @@ class Fom:
         return kin, inte
 
 
-def rk2avg_step(fom: Fom, prob, x, v, e, dt: float):
+def rk2avg_step(fom: Fom, prob, x, v, e, dt: float, force=None):
     """One RK2-average step from (x, v, e); returns (x1, v1, e1, dt_est) with
-    dt_est the minimum of the two stages' estimates."""
-    s1 = _force(prob, x=x, v=v, e=e)
+    dt_est the minimum of the two stages' estimates.
+
+    force(x, v, e, w) -> {"F1", "FTw", "dt", "status"} defaults to the corner force of
+    oracle.force (w = None means w = v); the pins substitute closed-form force fields
+    (tests/test_fom_oracle_pins.py P39-P41)."""
+    if force is None:
+        def force(x_, v_, e_, w_=None):
+            return _force(prob, x=x_, v=v_, e=e_, w=w_)
+    s1 = force(x, v, e)
     v_h = v - 0.5 * dt * fom.solve_v(s1["F1"])
-    s1w = _force(prob, x=x, v=v, e=e, w=v_h)
+    s1w = force(x, v, e, v_h)
     e_h = e + 0.5 * dt * fom.solve_e(s1w["FTw"])
     x_h = x + 0.5 * dt * v_h
-    s2 = _force(prob, x=x_h, v=v_h, e=e_h)
+    s2 = force(x_h, v_h, e_h)
     v1 = v - dt * fom.solve_v(s2["F1"])
     vbar = 0.5 * (v + v1)
-    s2w = _force(prob, x=x_h, v=v_h, e=e_h, w=vbar)
+    s2w = force(x_h, v_h, e_h, vbar)
     e1 = e + dt * fom.solve_e(s2w["FTw"])
     x1 = x + dt * vbar
     if s1["status"] or s2["status"]:   # tangled or non-finite stage: the step is invalid
