@@ -60,7 +60,9 @@ typedef enum {
   HYDRO_ERR_CUDA = 3,        /* a CUDA runtime call or launch failed                      */
   HYDRO_ERR_TANGLED = 4,     /* detJ <= 0 at some quadrature point (DESIGN R16)            */
   HYDRO_ERR_NONFINITE = 5,   /* some dt_q is NaN (DESIGN R15)                              */
-  HYDRO_ERR_WORKSPACE = 6    /* workspace too small or misaligned                          */
+  HYDRO_ERR_WORKSPACE = 6,   /* workspace too small or misaligned                          */
+  HYDRO_ERR_NOT_CONVERGED = 7 /* an iterative solve (CG of M_V) stopped at its iteration cap
+                                 with a finite residual above its tolerance                 */
 } hydro_status;
 
 /* Mesh description (kinematic H1 Q_k, thermodynamic L2 Q_{k-1}). */
@@ -230,7 +232,9 @@ typedef struct { double beta1, beta2, gamma; } hydro_dt_ctrl;
  * from the previous solve's solution (stopping test relative to the right-hand side).  *dt_est (host) = the min of
  * the two stages' time-step estimates for the caller's controller;
  * *cg_iters (host) = CG iterations used.  Device conditions (tangled, NaN) are reported by
- * hydro_status_sync on the context.  Synchronises `stream`.                                 */
+ * hydro_status_sync on the context; a NaN CG residual (an invalid state) makes *dt_est NaN.
+ * HYDRO_ERR_NOT_CONVERGED if a CG solve reaches cg_max_iter with a finite residual above
+ * cg_tol (the state is then updated with that solve).  Synchronises `stream`.               */
 hydro_status hydro_rk2avg_step(hydro_fom *fom, double *x, double *v, double *e,
                                const double *gamma, hydro_visc visc, hydro_cfl cfl, double dt,
                                double cg_tol, int cg_max_iter, double *dt_est /* host */,
@@ -241,7 +245,10 @@ hydro_status hydro_rk2avg_step(hydro_fom *fom, double *x, double *v, double *e,
  * dt <= gamma*estimate; the step reaching t_final is shortened to land on it.  *dt (host,
  * in/out): the first trial step, returned as the controller's next step.  At most max_steps
  * accepted steps; *t_out (host) = the time reached, *steps / *rejected (host) = accepted and
- * rejected steps.  HYDRO_ERR_NONFINITE on a NaN estimate.  Synchronises `stream`.             */
+ * rejected steps.  A trial step that tangles an element or whose estimate is NaN is rejected
+ * like dt >= estimate (DESIGN R26) and retried with beta1*dt; after 10 000 rejections in a row
+ * the loop stops with HYDRO_ERR_NONFINITE.  Errors of hydro_rk2avg_step (incl.
+ * HYDRO_ERR_NOT_CONVERGED) end the loop and are returned.  Synchronises `stream`.            */
 hydro_status hydro_fom_advance(hydro_fom *fom, double *x, double *v, double *e,
                                const double *gamma, hydro_visc visc, hydro_cfl cfl,
                                hydro_dt_ctrl ctrl, double t0, double t_final, double *dt,
@@ -339,6 +346,16 @@ hydro_status hydro_deim_oversampled(const double *U, int64_t N, int m, int n_s, 
 hydro_status hydro_window_ops(hydro_fom *fom, int field, int64_t N, int n_new, int n_old, int B,
                               const double *Phi_new, const double *Phi_old, const double *os_new,
                               const double *os_old, double *T, double *c, hydro_stream_t stream);
+/* Least-squares (gappy) pseudo-inverse of sampled basis rows, the offline factor of the
+ * hyper-reduction (P:778-799 Eq. sol-ls-hyper; P:985-1000 SNS with M = I, DESIGN R21):
+ *   P = (U[rows, :])^+ = (Z^T U)^+   [m][s]  (device out, row-major),
+ * with U device [N][m] row-major and rows host [s] (0 <= rows[i] < N, s >= m).  Computed as
+ * CholQR2 of the gathered rows (Q R = U[rows], two Cholesky-QR passes on the GPU with the
+ * m x m Cholesky factorisations on the host) followed by P = R^-1 Q^T on the GPU.
+ * HYDRO_ERR_NONFINITE if U[rows] is numerically rank-deficient.  Allocates its own scratch
+ * (offline routine); synchronises `stream`.                                                */
+hydro_status hydro_gappy_pinv(const double *U, int64_t N, int m, const int64_t *rows, int64_t s_rows,
+                              double *P, hydro_stream_t stream);
 /* The integrands of the a-posteriori bound, Theorem 2 Eq. aposteriori-semi, at
  * one (lifted) state (x, v, e) of a ROM trajectory (DESIGN R29):
  *   eta[0] = | (I - M_V Phi_v Mhat_V^-1 Phi_v^T P_F1) F.1(x, v, e) |_2,
@@ -349,6 +366,11 @@ hydro_status hydro_window_ops(hydro_fom *fom, int field, int64_t N, int n_new, i
  * layouts), Phi_v [N_V][nv], Phi_e [N_E][ne], U1 [N_V][m1], U2 [N_E][m2]; host: Z1 [s1],
  * Z2 [s2] (s >= m), eta [2].  HYDRO_ERR_TANGLED / _NONFINITE if the state is invalid or a
  * small solve is singular.  Allocates its own scratch; synchronises `stream`.               */
+hydro_status hydro_rom_indicator(hydro_fom *fom, const double *x, const double *v, const double *e,
+                                 const double *gamma, hydro_visc visc, hydro_cfl cfl, int nv,
+                                 const double *Phi_v, int ne, const double *Phi_e, int m1, const double *U1,
+                                 int s1, const int64_t *Z1, int m2, const double *U2, int s2,
+                                 const int64_t *Z2, double *eta, hydro_stream_t stream);
 /* dst[c * ld_dst + dst_idx[i]] = (add ? that + : ) src[c * ld_src + src_idx[i]], i < n, c < dim
  * (NULL index = identity): the gather, fixed-order accumulate and scatter steps of the
  * slab-sharded force's halo sum (paper_2104_11404_b200/shard.py).  Device
@@ -356,11 +378,7 @@ hydro_status hydro_window_ops(hydro_fom *fom, int field, int64_t N, int n_new, i
 hydro_status hydro_index_copy_add(int64_t n, int dim, const double *src, int64_t ld_src,
                                   const int64_t *src_idx, double *dst, int64_t ld_dst,
                                   const int64_t *dst_idx, int add, hydro_stream_t stream);
-hydro_status hydro_rom_indicator(hydro_fom *fom, const double *x, const double *v, const double *e,
-                                 const double *gamma, hydro_visc visc, hydro_cfl cfl, int nv,
-                                 const double *Phi_v, int ne, const double *Phi_e, int m1, const double *U1,
-                                 int s1, const int64_t *Z1, int m2, const double *U2, int s2,
-                                 const int64_t *Z2, double *eta, hydro_stream_t stream);
+
 
 /* ------------------------------------------------------------------ profiling (host) */
 /* When enabled, every hydro_force_full / hydro_dt_estimate / hydro_force_sampled call
@@ -383,10 +401,24 @@ hydro_status hydro_profile_release_captured(void);
  * B[q][k+1], G[q][k+1], Bl[q][k] (host outputs).  Pure host computation, no GPU needed. */
 hydro_status hydro_basis_tables(int k, int q, double *xi, double *w, double *B, double *G,
                                 double *Bl);
+/* Kernel choice for 2D Q2/Q1 force evaluations (process-wide, all devices): 0 = by size
+ * (default: one thread per element with >= 18 944 units, else one thread per point),
+ * 1 = always one thread per element (force2d_kernel), 2 = always one thread per point
+ * (force_kernel).  Both evaluate the same contract with the same backward FMA order, so
+ * results are bitwise identical; this is a test and A/B knob.  HYDRO_ERR_ARG otherwise.   */
+hydro_status hydro_set_2d_kernel(int choice);
 /* Number of kernel launches issued by this library since load (host counter).            */
 int64_t hydro_launch_count(void);
 /* Library version string.                                                                  */
 const char *hydro_version(void);
+
+#ifdef HYDRO_COUNT_ROT
+/* Diagnostic builds only (-DHYDRO_COUNT_ROT, tools/rot_count.py): device counters of the
+ * Jacobi fallback of the 3x3 eigen-solve -- out (host [12]): [0] lane-slots of executed
+ * rotations, [1] rotations a lane needed, [2..9] per-sweep live lanes / executed lane-slots,
+ * [10] points re-run with IEEE operators, [11] warps affected.  reset != 0 zeroes them.   */
+hydro_status hydro_debug_rot_counts(unsigned long long *out, int reset);
+#endif
 
 /* ------------------------------------------------------------------ self-test (device) */
 /* Checks the branch-free FP64 division / reciprocal / square-root fast paths the force

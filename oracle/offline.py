@@ -42,7 +42,10 @@ def pod(S: np.ndarray, eps: float = 0.9999, max_k: int | None = None):
             break
     if max_k is not None:
         k = min(k, max_k)
-    while k > 0 and not sig[k - 1] > 0:
+    # numerical rank (DESIGN R31): directions with sigma_i^2 <= ns eps_mach sigma_1^2 are
+    # rounding noise of the snapshot set (the Gram route the GPU takes cannot resolve them)
+    floor = ns * np.finfo(np.float64).eps * sig[0] ** 2 if sig.size else 0.0
+    while k > 0 and not sig[k - 1] ** 2 > floor:
         k -= 1
     V = Vt.T
     for c in range(k):

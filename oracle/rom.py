@@ -56,6 +56,30 @@ def sampled_force(batch_base, closure_elems, closure_nodes, s0_nodes, sample_ele
     return F1, FT, (float("nan") if r["status"] else r["dt"])
 
 
+def offline_projectors(batch):
+    """The offline operators of the hyper-reduced step over the sample-mesh rows,
+    by their definitions with library primitives (numpy pinv = SVD, matrix products):
+    P_v = (Z_v^T Phi_v)^+ [nv][s_v], P_e = (Z_e^T Phi_e)^+ [ne][s_e] (Eq. sol-ls-hyper
+    P:778-799, SNS with M = I P:985-1000), C_xv = Phi_x^T Phi_v [nx][nv], c_x = Phi_x^T v_os
+    [nx].  The GPU path forms them with hydro_gappy_pinv / hydro_window_ops."""
+    import workloads as W
+    h1, l2 = W.sampled_row_maps(batch)
+    P_v = np.ascontiguousarray(np.linalg.pinv(batch.Phi_v[h1]))
+    P_e = np.ascontiguousarray(np.linalg.pinv(batch.Phi_e[l2]))
+    C_xv = np.ascontiguousarray(batch.Phi_x.T @ batch.Phi_v)
+    c_x = np.ascontiguousarray(batch.Phi_x.T @ batch.v_os)
+    return P_v, P_e, C_xv, c_x
+
+
+def window_transition_ops(Phi_new, Phi_old, os_new, os_old):
+    """The factored form of Eq. ic-tw: yhat_w = T yhat_{w-1} + c with
+    T = Phi_w^T Phi_{w-1} [n_w][n_{w-1}] and c = Phi_w^T (os_{w-1} - os_w) ([n_w] or [n_w][B]),
+    by plain matrix products (pinned against window_transition, P25)."""
+    T = np.ascontiguousarray(Phi_new.T @ Phi_old)
+    c = np.ascontiguousarray(Phi_new.T @ (os_old - os_new))
+    return T, c
+
+
 def rom_rk2avg_step(op, Yx, Yv, Ye, dt):
     """One hyper-reduced RK2-average step for every instance.  op: dict with keys
     base, closure_elems, closure_nodes, s0_nodes, sample_elems, Phi_x, Phi_v, Phi_e
@@ -147,7 +171,7 @@ def window_transition(Phi_new, Phi_old, os_new, os_old, Y):
     basis); offsets [rows] or [rows][B].  Evaluated as Phi_w^T (os_{w-1} - os_w) +
     Phi_w^T (Phi_{w-1} yhat): the offsets are differenced first (lifting and then
     subtracting a large offset would cancel catastrophically for the e field's spike).
-    Independent of the factored T, c form the GPU path uses (workloads.window_transition_ops)."""
+    Independent of the factored T, c form (window_transition_ops; hydro_window_ops on the GPU)."""
     d = os_old - os_new
     d = d[:, None] if d.ndim == 1 else d
     return Phi_new.T @ d + Phi_new.T @ (Phi_old @ Y)

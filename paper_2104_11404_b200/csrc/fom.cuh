@@ -456,24 +456,25 @@ __global__ void __launch_bounds__(256) dot_final_alpha_kernel(const double *__re
   const double s_ = sum_partials(part);
   if (threadIdx.x == 0) {
     sc[1] = s_;
-    sc[2] = sc[0] / s_;
+    // a zero residual (rz = 0) or a vanishing p.Ap would give 0/0: the iterate is final
+    sc[2] = (sc[0] == 0.0 || s_ == 0.0) ? 0.0 : sc[0] / s_;
   }
 }
 __global__ void __launch_bounds__(256) dot_final_beta_kernel(const double *__restrict__ part, double *sc) {
   const double s_ = sum_partials(part);
   if (threadIdx.x == 0) {
     sc[3] = s_;
-    sc[4] = s_ / sc[0];
+    sc[4] = sc[0] == 0.0 ? 0.0 : s_ / sc[0];
     sc[0] = s_;
   }
 }
 
 // ---- PCG (Jacobi) pieces.  sc: [0] rz, [1] pAp, [2] alpha, [3] rz_new, [4] beta, [5] rz0
 __global__ void cg_alpha_kernel(double *sc) {
-  sc[2] = sc[0] / sc[1];
+  sc[2] = (sc[0] == 0.0 || sc[1] == 0.0) ? 0.0 : sc[0] / sc[1];
 }
 __global__ void cg_beta_kernel(double *sc) {
-  sc[4] = sc[3] / sc[0];
+  sc[4] = sc[0] == 0.0 ? 0.0 : sc[3] / sc[0];
   sc[0] = sc[3];
 }
 __global__ void cg_init_kernel(int64_t n, const double *__restrict__ b, const double *__restrict__ mask,
@@ -558,7 +559,10 @@ __global__ void rom_select_kernel(int64_t n, int B, const double *__restrict__ k
 __global__ void min2_kernel(int B, const double *__restrict__ a, const double *__restrict__ b,
                             double *__restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < B) out[i] = (a[i] < b[i] || b[i] != b[i]) ? a[i] : b[i];  // NaN in b propagates
+  if (i < B) {
+    const double x = a[i], y = b[i];
+    out[i] = (x != x || y != y) ? __longlong_as_double(0x7ff8000000000000ll) : fmin(x, y);  // NaN in either propagates
+  }
 }
 
 }  // namespace hk

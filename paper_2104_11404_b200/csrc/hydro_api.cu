@@ -8,11 +8,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
+#include <mutex>
 #include <vector>
 
 #include "../../include/hydro.h"
 #include "force2d.cuh"
-#include "force3d.cuh"
 #include "fom.cuh"
 #include "offline.cuh"
 #include "force_kernel.cuh"
@@ -116,12 +117,17 @@ namespace {
 // While a stream is being captured into a CUDA graph the pair is recorded as external
 // event-record nodes (they then time every replay of the graph) and kept in `captured`.
 struct ProfState {
-  bool on = false;
+  std::atomic<bool> on{false};
+  std::mutex mu;  // guards the three lists (calls may come from several host threads)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending, pool, captured;
 };
 ProfState g_prof;
 
+// 2D Q2 kernel choice (hydro_set_2d_kernel): 0 size-based, 1 element per thread, 2 point per thread
+std::atomic<int> g_kernel_2d{0};
+
 std::pair<cudaEvent_t, cudaEvent_t> prof_pair() {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
   if (!g_prof.pool.empty()) {
     auto p = g_prof.pool.back();
     g_prof.pool.pop_back();
@@ -140,28 +146,12 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
   const int64_t grid = ((int64_t)P.n_units + G::EPB - 1) / G::EPB;
   if (grid <= 0) return HYDRO_OK;
   constexpr bool SPEC2D = DIM == 2 && K == 2 && Q == 4 && MODE != hk::MODE_MQ && MODE != hk::MODE_FTW;
-  // 3D: the one-element-per-CTA kernel with register-blocked contraction stages (tables as
-  // constant-bank operands) beats the persistent cp.async kernel since r01 v22 (C2 2.57 vs
-  // 2.80 ms, C4 69.2 vs 77.8 ms: profiles/ab/r01_ab23_*); force3d stays selectable with
-  // HYDRO_3D_KERNEL=persistent (and is covered by the kernel-path tests)
-  constexpr bool SPEC3D_OK = DIM == 3 && MODE != hk::MODE_MQ && MODE != hk::MODE_FTW;
-  bool use3d = false;
-  if (SPEC3D_OK) {
-    const char *env = getenv("HYDRO_3D_KERNEL");
-    if (env && !strcmp(env, "persistent")) use3d = true;
-    if (env && !strcmp(env, "element")) use3d = false;
-  }
-  using G3 = hk::G3<K, Q, NF>;
   using G2 = hk::G2<NF>;
   // one-thread-per-element 2D kernel only when there are enough elements to fill the GPU;
-  // small meshes (C0: 64 elements) run the point-per-thread kernel (16x the threads)
-  // (HYDRO_2D_KERNEL=element|point overrides the choice; the tests run both paths)
-  bool use2d = SPEC2D && P.n_units >= 148 * G2::NT * 2;
-  if (SPEC2D) {
-    const char *env = getenv("HYDRO_2D_KERNEL");
-    if (env && !strcmp(env, "element")) use2d = true;
-    if (env && !strcmp(env, "point")) use2d = false;
-  }
+  // small meshes (C0: 64 elements) run the point-per-thread kernel (16x the threads);
+  // hydro_set_2d_kernel overrides the choice (the tests run both paths)
+  const int k2d = g_kernel_2d.load(std::memory_order_relaxed);
+  const bool use2d = SPEC2D && (k2d == 1 || (k2d == 0 && P.n_units >= 148 * G2::NT * 2));
   void (*kern)(const hk::Params) = hk::force_kernel<DIM, K, Q, VISC, MODE, BATCHED, HAS_W>;
   size_t smem = G::SMEM;
   int nt = G::NT;
@@ -173,28 +163,19 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
       nt = G2::NT;
       grid2 = ((int64_t)P.n_units + G2::NT - 1) / G2::NT;  // one thread per unit
     }
-  } else if constexpr (SPEC3D_OK) {
-    if (use3d) {
-      kern = hk::force3d_kernel<K, Q, VISC, MODE, BATCHED, HAS_W>;
-      smem = G3::SMEM;
-      nt = G3::NT;
+  }
+  // the dynamic shared-memory opt-in is a per-device function attribute: once per device
+  // and kernel (bit d of the mask for device d)
+  static std::atomic<unsigned long long> attr_done[2];
+  {
+    int dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_done[use2d ? 1 : 0].load(std::memory_order_acquire) & bit)) {
+      CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_done[use2d ? 1 : 0].fetch_or(bit, std::memory_order_acq_rel);
     }
   }
-  static bool attr_set[2] = {false, false};  // per instantiation: [generic/2D-or-3D kernel]
-  static int resident = 0;                    // persistent 3D kernel: CTAs resident on the device
-  const int which = (use2d || use3d) ? 1 : 0;
-  if (!attr_set[which]) {
-    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (use3d) {
-      int dev = 0, sms = 0, per_sm = 0;
-      CUDA_OK(cudaGetDevice(&dev));
-      CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
-      resident = sms * (per_sm > 0 ? per_sm : 1);
-    }
-    attr_set[which] = true;
-  }
-  if (use3d) grid2 = P.n_units < resident ? P.n_units : resident;
   std::pair<cudaEvent_t, cudaEvent_t> ev;
   const bool prof = g_prof.on && (MODE == hk::MODE_FORCE || MODE == hk::MODE_DT);
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -211,9 +192,11 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
   if (prof) {
     if (cap == cudaStreamCaptureStatusActive) {
       CUDA_OK(cudaEventRecordWithFlags(ev.second, s, cudaEventRecordExternal));
+      std::lock_guard<std::mutex> lk(g_prof.mu);
       g_prof.captured.push_back(ev);
     } else {
       CUDA_OK(cudaEventRecord(ev.second, s));
+      std::lock_guard<std::mutex> lk(g_prof.mu);
       g_prof.pending.push_back(ev);
     }
   }
@@ -309,6 +292,7 @@ hydro_status hydro_profile_enable(int on) {
 }
 
 hydro_status hydro_profile_read(double *total_ms, int64_t *count) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
   double tot = 0.0;
   int64_t n = 0;
   for (auto &p : g_prof.pending) {
@@ -341,6 +325,7 @@ hydro_status hydro_debug_rot_counts(unsigned long long *out /* host [12] */, int
 #endif
 
 hydro_status hydro_profile_read_captured(double *total_ms, int64_t *count) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
   double tot = 0.0;
   int64_t n = 0;
   for (auto &p : g_prof.captured) {
@@ -356,6 +341,7 @@ hydro_status hydro_profile_read_captured(double *total_ms, int64_t *count) {
 }
 
 hydro_status hydro_profile_release_captured(void) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
   for (auto &p : g_prof.captured) g_prof.pool.push_back(p);
   g_prof.captured.clear();
   return HYDRO_OK;
@@ -367,6 +353,12 @@ hydro_status hydro_selftest_ieee_fast(uint64_t seed, int64_t n, int op, int dist
   hk::selftest_ieee_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(seed, n, op, dist, counts);
   g_launches++;
   CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
+hydro_status hydro_set_2d_kernel(int choice) {
+  if (choice < 0 || choice > 2) return HYDRO_ERR_ARG;
+  g_kernel_2d.store(choice);
   return HYDRO_OK;
 }
 
@@ -885,6 +877,8 @@ struct hydro_fom {
   double *xb = nullptr, *vb = nullptr, *eb = nullptr;  // state backup of the step controller
   bool have_dv = false;  // dv holds the previous solve's solution (warm start of the step's CG)
   std::vector<void *> allocs;
+  double *colbuf = nullptr;  // mass_columns' transpose scratch, grown on demand (freed on destroy)
+  size_t colbuf_doubles = 0;
 };
 
 namespace {
@@ -1145,6 +1139,7 @@ hydro_status hydro_fom_create(hydro_ctx *c, const int64_t *bc_dofs, int64_t n_bc
 hydro_status hydro_fom_destroy(hydro_fom *f) {
   if (!f) return HYDRO_OK;
   for (void *q : f->allocs) cudaFree(q);
+  cudaFree(f->colbuf);
   delete f;
   return HYDRO_OK;
 }
@@ -1206,12 +1201,13 @@ hydro_status hydro_rk2avg_step(hydro_fom *f, double *x, double *v, double *e, co
   const unsigned g = blocks_for(n, 256);
   hydro_status st;
   int it1 = 0, it2 = 0;
+  double rel1 = 0.0, rel2 = 0.0;
   // ---- stage 1: F(U^n) (F.1, dt, and the point stresses S_q for the transposed product)
   if ((st = force_common(c, hk::MODE_FORCE, x, v, e, nullptr, gamma, visc, cfl, f->F1, f->FTx,
                          f->dts + 0, s, f->S)) != HYDRO_OK) return st;
   // the CG of each stage starts from the previous solve's solution (the accelerations of
   // consecutive stages differ by O(dt)); the stopping test is relative to the rhs either way
-  if ((st = pcg(f, f->F1, f->dv, cg_tol, cg_max_iter, &it1, nullptr, s, f->have_dv)) != HYDRO_OK)
+  if ((st = pcg(f, f->F1, f->dv, cg_tol, cg_max_iter, &it1, &rel1, s, f->have_dv)) != HYDRO_OK)
     return st;
   f->have_dv = true;
   hk::axpy_kernel<<<g, 256, 0, s>>>(n, v, -0.5 * dt, f->dv, f->mask, f->vh);    // v^{n+1/2}
@@ -1223,7 +1219,7 @@ hydro_status hydro_rk2avg_step(hydro_fom *f, double *x, double *v, double *e, co
   // ---- stage 2: F(U^{n+1/2})
   if ((st = force_common(c, hk::MODE_FORCE, f->xh, f->vh, f->eh, nullptr, gamma, visc, cfl, f->F1,
                          f->FTx, f->dts + 1, s, f->S)) != HYDRO_OK) return st;
-  if ((st = pcg(f, f->F1, f->dv, cg_tol, cg_max_iter, &it2, nullptr, s, true)) != HYDRO_OK) return st;
+  if ((st = pcg(f, f->F1, f->dv, cg_tol, cg_max_iter, &it2, &rel2, s, true)) != HYDRO_OK) return st;
   hk::axpy_kernel<<<g, 256, 0, s>>>(n, v, -dt, f->dv, f->mask, f->v1);         // v^{n+1}
   hk::avg_kernel<<<g, 256, 0, s>>>(n, v, f->v1, f->vbar);                       // vbar
   g_launches += 2;
@@ -1236,9 +1232,12 @@ hydro_status hydro_rk2avg_step(hydro_fom *f, double *x, double *v, double *e, co
   double h[2];
   CUDA_OK(cudaMemcpyAsync(h, f->dts, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_OK(cudaStreamSynchronize(s));
-  if (dt_est) *dt_est = h[0] < h[1] ? h[0] : h[1];  // (a NaN estimate propagates via status)
+  // min of the stage estimates, NaN if either is NaN (or a CG residual is: an invalid state)
+  const bool nan = h[0] != h[0] || h[1] != h[1] || rel1 != rel1 || rel2 != rel2;
+  if (dt_est) *dt_est = nan ? std::numeric_limits<double>::quiet_NaN() : std::fmin(h[0], h[1]);
   if (cg_iters) *cg_iters = it1 + it2;
   (void)nE;
+  if (!nan && (rel1 > cg_tol || rel2 > cg_tol)) return HYDRO_ERR_NOT_CONVERGED;
   return HYDRO_OK;
 }
 
@@ -1715,7 +1714,11 @@ hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k
     if (tot > 0.0 && run / tot >= eps) { k = i + 1; break; }
   }
   if (k > max_k) k = max_k;
-  while (k > 0 && !(sg[(size_t)k - 1] > 0.0)) --k;
+  // Directions the Gram route cannot resolve are dropped: lambda_i <= ns eps lambda_1 is
+  // rounding noise of S S^T (a rank-deficient snapshot set gives ~1e-16 lambda_1 there, not
+  // 0), and S^T v_i / sigma_i would be garbage.  eps = 1 keeps the numerically nonzero ones.
+  const double lam_floor = (double)ns * std::numeric_limits<double>::epsilon() * std::max(lam[0], 0.0);
+  while (k > 0 && !(lam[(size_t)k - 1] > lam_floor)) --k;
   *k_out = k;
   if (k == 0) { cleanup(); return HYDRO_OK; }
   // Phi = S^T V_k Sigma_k^-1  ([N][k]; the left singular vectors)
@@ -1734,6 +1737,7 @@ hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k
   // Phi <- Phi R^-1 with R^T R = Phi^T Phi restores it to rounding (same span).
   {
     double *P2 = nullptr, *Rinv = nullptr, *G2 = nullptr;
+    bool chol_fail = false;
     const int ch = (int)std::min<int64_t>(hk::GRAM_CHUNKS, (N + hk::GRAM_KT - 1) / hk::GRAM_KT);
     const int64_t chs = (N + ch - 1) / ch;
     const int kt = (k + hk::GRAM_T - 1) / hk::GRAM_T;
@@ -1756,7 +1760,7 @@ hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k
       for (int i = 0; i < k && ok; ++i) {
         double d = C[(size_t)i * k + i];
         for (int p = 0; p < i; ++p) d -= R[(size_t)p * k + i] * R[(size_t)p * k + i];
-        if (!(d > 0.0)) { ok = false; break; }
+        if (!(d > 0.0)) { ok = false; chol_fail = true; break; }
         R[(size_t)i * k + i] = std::sqrt(d);
         for (int j = i + 1; j < k; ++j) {
           double v = C[(size_t)i * k + j];
@@ -1779,7 +1783,7 @@ hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k
       ok = ok && cudaGetLastError() == cudaSuccess && cudaStreamSynchronize(s) == cudaSuccess;
     }
     cudaFree(P2); cudaFree(Rinv); cudaFree(G2);
-    if (!ok) st = HYDRO_ERR_CUDA;
+    if (!ok) st = chol_fail ? HYDRO_ERR_NONFINITE : HYDRO_ERR_CUDA;
   }
   cleanup();
   return st;
@@ -1856,8 +1860,16 @@ void transpose(int64_t N, int64_t m, const double *A, double *At, cudaStream_t s
 // 32-byte sector per 8-byte value: 110 us per C2 column, profiles/fom/r01_fom_step_v3_*.)
 hydro_status mass_columns(hydro_fom *F, int field, int64_t N, int n, const double *Phi, double *W,
                           cudaStream_t s) {
-  double *T = nullptr;
-  if (cudaMalloc(&T, sizeof(double) * (size_t)N * n * 2) != cudaSuccess) return HYDRO_ERR_CUDA;
+  const size_t need = (size_t)N * n * 2;
+  if (F->colbuf_doubles < need) {  // grow the FOM's scratch (kept for the next call)
+    cudaStreamSynchronize(s);
+    cudaFree(F->colbuf);
+    F->colbuf = nullptr;
+    F->colbuf_doubles = 0;
+    if (cudaMalloc(&F->colbuf, sizeof(double) * need) != cudaSuccess) return HYDRO_ERR_CUDA;
+    F->colbuf_doubles = need;
+  }
+  double *T = F->colbuf;
   double *T2 = T + (size_t)N * n;
   transpose(N, n, Phi, T, s);
   hydro_status st = HYDRO_OK;
@@ -1866,8 +1878,6 @@ hydro_status mass_columns(hydro_fom *F, int field, int64_t N, int n, const doubl
                     : hydro_mass_e_apply(F, T + (size_t)j * N, T2 + (size_t)j * N, s);
   if (st == HYDRO_OK) transpose(n, N, T2, W, s);
   if (st == HYDRO_OK && cudaGetLastError() != cudaSuccess) st = HYDRO_ERR_CUDA;
-  cudaStreamSynchronize(s);
-  cudaFree(T);
   return st;
 }
 
@@ -1889,7 +1899,6 @@ hydro_status hydro_qdeim(const double *U, int64_t N, int m, int64_t *idx, hydro_
     return HYDRO_ERR_CUDA;
   }
   transpose(N, m, U, Rt, s);
-  g_launches++;
   std::vector<double> hv(hk::DEIM_BLOCKS), row((size_t)m);
   std::vector<int64_t> hi(hk::DEIM_BLOCKS);
   hydro_status st = HYDRO_OK;
@@ -2020,6 +2029,37 @@ hydro_status xprod(int64_t N, int na, const double *A, int64_t lda, int nx, cons
   return ok ? HYDRO_OK : HYDRO_ERR_CUDA;
 }
 
+// Ri = R^-1 of an upper triangular k x k R (row-major, host), by back substitution.
+void upper_inv(int k, const std::vector<double> &R, std::vector<double> &Ri) {
+  Ri.assign((size_t)k * k, 0.0);
+  for (int c = 0; c < k; ++c)  // column c of R^-1: R x = e_c
+    for (int i = c; i >= 0; --i) {
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int j = i + 1; j <= c; ++j) v -= R[(size_t)i * k + j] * Ri[(size_t)j * k + c];
+      Ri[(size_t)i * k + c] = v / R[(size_t)i * k + i];
+    }
+}
+
+// Upper Cholesky factor R of the SPD k x k matrix C (C = R^T R) and its inverse Ri (both
+// row-major, host).  false if a pivot is not positive (C not numerically SPD).
+bool chol_upper_inv(int k, const std::vector<double> &C, std::vector<double> &R, std::vector<double> &Ri) {
+  R.assign((size_t)k * k, 0.0);
+  Ri.assign((size_t)k * k, 0.0);
+  for (int i = 0; i < k; ++i) {
+    double d = C[(size_t)i * k + i];
+    for (int p = 0; p < i; ++p) d -= R[(size_t)p * k + i] * R[(size_t)p * k + i];
+    if (!(d > 0.0)) return false;
+    R[(size_t)i * k + i] = std::sqrt(d);
+    for (int j = i + 1; j < k; ++j) {
+      double v = C[(size_t)i * k + j];
+      for (int p = 0; p < i; ++p) v -= R[(size_t)p * k + i] * R[(size_t)p * k + j];
+      R[(size_t)i * k + j] = v / R[(size_t)i * k + i];
+    }
+  }
+  upper_inv(k, R, Ri);
+  return true;
+}
+
 }  // namespace
 
 extern "C" {
@@ -2097,6 +2137,70 @@ hydro_status hydro_window_ops(hydro_fom *fom, int field, int64_t N, int n_new, i
     }
   }
   cudaStreamSynchronize(s);
+  cleanup();
+  return st;
+}
+
+hydro_status hydro_gappy_pinv(const double *U, int64_t N, int m, const int64_t *rows, int64_t s_rows,
+                              double *P, hydro_stream_t stream) {
+  if (!U || N <= 0 || m <= 0 || m > hk::POD_MAXK || !rows || s_rows < m || s_rows > INT32_MAX || !P)
+    return HYDRO_ERR_ARG;
+  for (int64_t i = 0; i < s_rows; ++i)
+    if (rows[i] < 0 || rows[i] >= N) return HYDRO_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t *d_rows = nullptr;
+  double *Q = nullptr, *G = nullptr, *Rinv = nullptr;
+  auto cleanup = [&]() { cudaFree(d_rows); cudaFree(Q); cudaFree(G); cudaFree(Rinv); };
+  if (cudaMalloc(&d_rows, sizeof(int64_t) * (size_t)s_rows) != cudaSuccess ||
+      cudaMalloc(&Q, sizeof(double) * (size_t)s_rows * m) != cudaSuccess ||
+      cudaMalloc(&G, sizeof(double) * (size_t)m * m) != cudaSuccess ||
+      cudaMalloc(&Rinv, sizeof(double) * (size_t)m * m) != cudaSuccess ||
+      cudaMemcpyAsync(d_rows, rows, sizeof(int64_t) * (size_t)s_rows, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+    cleanup();
+    return HYDRO_ERR_CUDA;
+  }
+  // Q = U[rows, :]
+  hk::gather_rows_kernel<<<blocks_for(s_rows * m, 256), 256, 0, s>>>((int)s_rows, m, d_rows, U, m, Q);
+  g_launches++;
+  // CholQR2: Q <- Q R1^-1, Q <- Q R2^-1 (Q^T Q = R^T R each pass), R = R2 R1
+  std::vector<double> C((size_t)m * m), R, Ri, Racc((size_t)m * m, 0.0);
+  for (int i = 0; i < m; ++i) Racc[(size_t)i * m + i] = 1.0;
+  hydro_status st = cudaGetLastError() == cudaSuccess ? HYDRO_OK : HYDRO_ERR_CUDA;
+  for (int pass = 0; pass < 2 && st == HYDRO_OK; ++pass) {
+    st = xprod(s_rows, m, Q, m, m, Q, m, G, s);
+    if (st != HYDRO_OK) break;
+    if (cudaMemcpyAsync(C.data(), G, sizeof(double) * C.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+      st = HYDRO_ERR_CUDA;
+      break;
+    }
+    if (!chol_upper_inv(m, C, R, Ri)) { st = HYDRO_ERR_NONFINITE; break; }  // U[rows] rank-deficient
+    std::vector<double> Rn((size_t)m * m, 0.0);  // R_pass * Racc (both upper triangular)
+    for (int i = 0; i < m; ++i)
+      for (int j = i; j < m; ++j) {
+        double acc = 0.0;
+        for (int k = i; k <= j; ++k) acc += R[(size_t)i * m + k] * Racc[(size_t)k * m + j];
+        Rn[(size_t)i * m + j] = acc;
+      }
+    Racc.swap(Rn);
+    if (cudaMemcpyAsync(Rinv, Ri.data(), sizeof(double) * Ri.size(), cudaMemcpyHostToDevice, s) != cudaSuccess) {
+      st = HYDRO_ERR_CUDA;
+      break;
+    }
+    hk::right_mult_kernel<<<blocks_for(s_rows, 128), 128, 0, s>>>(s_rows, m, m, Rinv, Q);
+    g_launches++;
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) st = HYDRO_ERR_CUDA;
+  }
+  if (st == HYDRO_OK) {  // P = R^-1 Q^T
+    upper_inv(m, Racc, Ri);
+    if (cudaMemcpyAsync(Rinv, Ri.data(), sizeof(double) * Ri.size(), cudaMemcpyHostToDevice, s) != cudaSuccess) {
+      st = HYDRO_ERR_CUDA;
+    } else {
+      hk::pinv_apply_kernel<<<blocks_for(s_rows, 128), 128, 0, s>>>(s_rows, m, Rinv, Q, P);
+      g_launches++;
+      if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) st = HYDRO_ERR_CUDA;
+    }
+  }
   cleanup();
   return st;
 }

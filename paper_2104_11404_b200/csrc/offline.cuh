@@ -101,6 +101,22 @@ __global__ void right_mult_kernel(int64_t N, int k, int ldp, const double *__res
   }
 }
 
+// P[i][j] = sum_{k >= i} Rinv[i][k] Q[j][k]  (P = R^-1 Q^T: [m][s]; Q [s][m] row-major, Rinv
+// [m][m] upper triangular), one thread per column j of P -- consecutive threads write
+// consecutive entries of every row of P (hydro_gappy_pinv).
+__global__ void pinv_apply_kernel(int64_t s, int m, const double *__restrict__ Rinv,
+                                  const double *__restrict__ Q, double *__restrict__ P) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= s) return;
+  double q[POD_MAXK];
+  for (int k = 0; k < m; ++k) q[k] = Q[j * m + k];
+  for (int i = 0; i < m; ++i) {
+    double acc = 0.0;
+    for (int k = i; k < m; ++k) acc = __fma_rn(Rinv[i * m + k], q[k], acc);
+    P[(int64_t)i * s + j] = acc;
+  }
+}
+
 // DEIM residual of basis column j: res[r] = U[r][j] - sum_{i<j} U[r][i] c[i]  (U: [N][m]),
 // with per-block argmax of |res| (ties: lowest row) written to (bval, bidx).
 constexpr int DEIM_BLOCKS = 148 * 4, DEIM_THREADS = 256;

@@ -20,20 +20,20 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HYDRO_LIB_PATH") or os.path.join(_HERE, "libhydro.so")
 
 HYDRO_OK, HYDRO_ERR_ARG, HYDRO_ERR_UNSUPPORTED, HYDRO_ERR_CUDA = 0, 1, 2, 3
-HYDRO_ERR_TANGLED, HYDRO_ERR_NONFINITE, HYDRO_ERR_WORKSPACE = 4, 5, 6
+HYDRO_ERR_TANGLED, HYDRO_ERR_NONFINITE, HYDRO_ERR_WORKSPACE, HYDRO_ERR_NOT_CONVERGED = 4, 5, 6, 7
 STATUS_NAMES = {0: "OK", 1: "ERR_ARG", 2: "ERR_UNSUPPORTED", 3: "ERR_CUDA", 4: "ERR_TANGLED",
-                5: "ERR_NONFINITE", 6: "ERR_WORKSPACE"}
+                5: "ERR_NONFINITE", 6: "ERR_WORKSPACE", 7: "ERR_NOT_CONVERGED"}
 
 EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy",
             "hydro_force_full", "hydro_dt_estimate", "hydro_status_sync", "hydro_sample_create",
             "hydro_sample_destroy", "hydro_sample_info", "hydro_sample_lists", "hydro_rom_lift",
             "hydro_force_sampled", "hydro_sample_status_sync", "hydro_rom_project_workspace_bytes",
-            "hydro_rom_project", "hydro_basis_tables", "hydro_launch_count", "hydro_version",
+            "hydro_rom_project", "hydro_basis_tables", "hydro_launch_count", "hydro_version", "hydro_set_2d_kernel",
             "hydro_profile_enable", "hydro_profile_read", "hydro_profile_read_captured",
             "hydro_profile_release_captured", "hydro_selftest_ieee_fast",
             "hydro_fom_create", "hydro_fom_destroy", "hydro_mass_v_apply", "hydro_mass_v_solve",
             "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_fom_advance", "hydro_rom_advance", "hydro_rom_create",
-            "hydro_fom_stage_state", "hydro_pod", "hydro_deim", "hydro_qdeim", "hydro_deim_oversampled", "hydro_mass_e_apply", "hydro_window_ops", "hydro_rom_indicator", "hydro_index_copy_add",
+            "hydro_fom_stage_state", "hydro_pod", "hydro_deim", "hydro_qdeim", "hydro_deim_oversampled", "hydro_mass_e_apply", "hydro_window_ops", "hydro_gappy_pinv", "hydro_rom_indicator", "hydro_index_copy_add",
             "hydro_rom_destroy", "hydro_rom_rk2avg_step", "hydro_force_stress_bytes",
             "hydro_force_full_store", "hydro_force_transpose", "hydro_sample_stress_bytes",
             "hydro_force_sampled_store", "hydro_sample_force_transpose"]
@@ -100,6 +100,7 @@ def lib() -> ctypes.CDLL:
         L.hydro_mass_e_solve.argtypes = [vp, vp, vp, vp]
         L.hydro_mass_e_apply.argtypes = [vp, vp, vp, vp]
         L.hydro_window_ops.argtypes = [vp, i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
+        L.hydro_gappy_pinv.argtypes = [vp, i64, i32, ctypes.POINTER(i64), i64, vp, vp]
         L.hydro_index_copy_add.argtypes = [i64, i32, vp, i64, vp, vp, i64, vp, i32, vp]
         L.hydro_rom_indicator.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, i32, vp, i32, vp, i32, vp, i32,
                                           ctypes.POINTER(i64), i32, vp, i32, ctypes.POINTER(i64),
@@ -142,6 +143,7 @@ def lib() -> ctypes.CDLL:
         L.hydro_profile_read_captured.argtypes = [ctypes.POINTER(dbl), ctypes.POINTER(i64)]
         L.hydro_profile_release_captured.argtypes = []
         L.hydro_version.restype = ctypes.c_char_p
+        L.hydro_set_2d_kernel.argtypes = [i32]
         _lib = L
     return _lib
 
@@ -214,6 +216,14 @@ def selftest_ieee_fast(seed: int, n: int, op: int, dist: int, stream=None):
     _check(lib().hydro_selftest_ieee_fast(seed, n, op, dist, _ptr(counts), _stream(stream)),
            "hydro_selftest_ieee_fast")
     return tuple(int(x) for x in counts.cpu().tolist())
+
+
+_K2D = {"auto": 0, "element": 1, "point": 2}
+
+
+def set_kernel_2d(choice: str) -> None:
+    """hydro_set_2d_kernel: "auto" (by size), "element" (one thread per element) or "point"."""
+    _check(lib().hydro_set_2d_kernel(_K2D[choice]), "hydro_set_2d_kernel")
 
 
 def launch_count() -> int:
@@ -442,6 +452,34 @@ def window_ops(Phi_new: torch.Tensor, Phi_old: torch.Tensor, os_new: torch.Tenso
                                   _ptr(Po), _ptr(osn), _ptr(oso), _ptr(T), _ptr(c), _stream(stream)),
            "hydro_window_ops")
     return T, c
+
+
+def gappy_pinv(U: torch.Tensor, rows, stream=None) -> torch.Tensor:
+    """P = (U[rows, :])^+ [m][s] (device) -- hydro_gappy_pinv, the offline factor of the
+    hyper-reduced projection.  U device [N][m]; rows: host int64 [s]."""
+    import numpy as _np
+    N, m = U.shape
+    r = _np.ascontiguousarray(_np.asarray(rows, dtype=_np.int64))
+    P = torch.empty((m, r.size), dtype=torch.float64, device=U.device)
+    _check(lib().hydro_gappy_pinv(_ptr(U.contiguous()), N, m,
+                                  r.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), r.size, _ptr(P),
+                                  _stream(stream)), "hydro_gappy_pinv")
+    return P
+
+
+def offline_projectors(Phi_x: torch.Tensor, Phi_v: torch.Tensor, Phi_e: torch.Tensor,
+                       v_os: torch.Tensor, rows_v, rows_e, stream=None):
+    """Offline operators of the hyper-reduced online step over the sample-mesh rows (SURVEY
+    R21), all on the GPU: P_v = (Z_v^T Phi_v)^+ [nv][s_v], P_e = (Z_e^T Phi_e)^+ [ne][s_e]
+    (Eq. sol-ls-hyper, SNS with M = I P:985-1000; hydro_gappy_pinv), and
+    C_xv = Phi_x^T Phi_v [nx][nv], c_x = Phi_x^T v_os [nx] (hydro_window_ops with
+    os_new = 0, os_old = v_os).  rows_v / rows_e: host indices of the sampled rows among the
+    basis rows, in the order of hydro_force_sampled's F1_rows / FTw_rows."""
+    P_v = gappy_pinv(Phi_v, rows_v, stream)
+    P_e = gappy_pinv(Phi_e, rows_e, stream)
+    zero = torch.zeros_like(v_os)
+    C_xv, c_x = window_ops(Phi_x, Phi_v, zero, v_os, stream=stream)
+    return P_v, P_e, C_xv, c_x.reshape(-1).contiguous()
 
 
 def rom_windowed_advance(windows, Yx, Yv, Ye, gamma, visc: Visc, cfl: Cfl, t0: float, dt,

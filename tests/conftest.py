@@ -26,3 +26,12 @@ def oracle_lib():
     import oracle
     oracle.build()
     return oracle
+
+
+@pytest.fixture
+def set_kernel_2d():
+    """Force the 2D Q2 force kernel for the test (hydro_set_2d_kernel: "element" = one thread
+    per element, "point" = one thread per point); back to the size-based choice afterwards."""
+    from paper_2104_11404_b200 import hydro
+    yield hydro.set_kernel_2d
+    hydro.set_kernel_2d("auto")

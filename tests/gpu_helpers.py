@@ -48,3 +48,12 @@ def assert_close(got, ref, mag, tol, what=""):
 
 def dt_bitwise(a: float, b: float) -> bool:
     return np.float64(a).tobytes() == np.float64(b).tobytes()
+
+
+def gpu_offline_ops(batch):
+    """The offline operators of a ROM batch formed by the library on the GPU
+    (hydro.offline_projectors: hydro_gappy_pinv + hydro_window_ops) -- device tensors
+    (P_v, P_e, C_xv, c_x).  The oracle side uses oracle.rom.offline_projectors."""
+    h1, l2 = W.sampled_row_maps(batch)
+    return hydro.offline_projectors(dev(batch.Phi_x), dev(batch.Phi_v), dev(batch.Phi_e),
+                                    dev(batch.v_os), h1, l2)

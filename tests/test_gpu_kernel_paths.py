@@ -1,10 +1,10 @@
 """GPU parity of every kernel path against the oracle (DESIGN "Kernels"):
 
 * 2D Q2: the one-thread-per-element kernel (force2d) and the point-per-thread kernel
-  (force_kernel) -- forced with HYDRO_2D_KERNEL -- on C0/C1-shaped meshes, w != v,
+  (force_kernel) -- forced with hydro_set_2d_kernel -- on C0/C1-shaped meshes, w != v,
   dt_estimate, and a batched sample plan (hydro_force_sampled with B > 1);
 * degenerate and ragged meshes: one element (every dim/order), and element counts just
-  below / at / above the CTA and persistent-grid multiples;
+  below / at / above the CTA multiples;
 * inviscid 3D (no config uses it, the API allows it).
 
 Bars: F.1 within 1e-11, F^T.w within 1e-12 of max(|ref|, M), dt bit-exact
@@ -28,16 +28,8 @@ from paper_2104_11404_b200 import hydro  # noqa: E402
 
 
 @pytest.fixture(params=["element", "point"])
-def kernel2d(request, monkeypatch):
-    monkeypatch.setenv("HYDRO_2D_KERNEL", request.param)
-    return request.param
-
-
-@pytest.fixture(params=["element", "persistent"])
-def kernel3d(request, monkeypatch):
-    """3D: the one-element-per-CTA kernel with blocked stages (default) and the persistent
-    cp.async kernel (force3d, Q2 only; Q3 falls back to the element kernel's code)."""
-    monkeypatch.setenv("HYDRO_3D_KERNEL", request.param)
+def kernel2d(request, set_kernel_2d):
+    set_kernel_2d(request.param)
     return request.param
 
 
@@ -66,12 +58,12 @@ def test_2d_paths_w_distinct(oracle_lib, kernel2d, name):
     check(prob, oracle_lib, w=w, what=f"{name}/{kernel2d} w")
 
 
-def test_2d_paths_bitwise_identical(monkeypatch):
+def test_2d_paths_bitwise_identical(set_kernel_2d):
     """Both 2D kernels evaluate the same contract and the same backward FMA order."""
     prob = W.small("c0")
-    monkeypatch.setenv("HYDRO_2D_KERNEL", "element")
+    set_kernel_2d("element")
     a = H.run_full(prob)
-    monkeypatch.setenv("HYDRO_2D_KERNEL", "point")
+    set_kernel_2d("point")
     b = H.run_full(prob)
     assert np.array_equal(a["F1"], b["F1"]) and np.array_equal(a["FTw"], b["FTw"])
     assert H.dt_bitwise(a["dt"], b["dt"])
@@ -103,9 +95,9 @@ def test_2d_batched_sampled_matches_oracle(oracle_lib, kernel2d):
 
 
 @pytest.mark.parametrize("dim,k", [(2, 2), (2, 3), (3, 2), (3, 3)])
-def test_single_element(oracle_lib, monkeypatch, dim, k):
+def test_single_element(oracle_lib, set_kernel_2d, dim, k):
     """The degenerate mesh of one element (every node on the boundary)."""
-    monkeypatch.setenv("HYDRO_2D_KERNEL", "element")
+    set_kernel_2d("element")
     nq = 4 if k == 2 else 6
     prob = W.sedov_like(7, dim, (1,) * dim, (0.0,) * dim, (1.0,) * dim, delta=0.0, e_floor=1e-3,
                         vmode="uniform", vscale=0.1, k=k, nq=nq, name="one")
@@ -113,42 +105,30 @@ def test_single_element(oracle_lib, monkeypatch, dim, k):
 
 
 @pytest.mark.parametrize("shape", [(63,), (64,), (65,), (127,), (129,)])
-def test_2d_ragged_counts(oracle_lib, monkeypatch, shape):
+def test_2d_ragged_counts(oracle_lib, set_kernel_2d, shape):
     """Element counts around the 64-thread CTA of the element kernel."""
-    monkeypatch.setenv("HYDRO_2D_KERNEL", "element")
+    set_kernel_2d("element")
     prob = W.sedov_like(8, 2, (shape[0], 1), (0.0, 0.0), (shape[0] / 8.0, 0.125), delta=0.1,
                         e_floor=1e-4, vmode="uniform", vscale=0.1, name="ragged2d")
     check(prob, oracle_lib, what=f"2D {shape}")
 
 
 @pytest.mark.parametrize("shape", [(5, 1, 1), (13, 11, 11)])
-def test_3d_ragged_counts(oracle_lib, kernel3d, shape):
-    """Small 3D element counts (fewer elements than persistent CTAs; and several
-    elements per CTA with a ragged last round)."""
+def test_3d_ragged_counts(oracle_lib, shape):
+    """Small 3D element counts (fewer elements than SMs; and a 13x11x11 mesh)."""
     n = shape
     prob = W.sedov_like(9, 3, n, (0.0,) * 3, tuple(0.01875 * s for s in n), delta=0.05,
                         e_floor=1e-6, vmode="radial", vscale=0.5, name="ragged3d")
-    check(prob, oracle_lib, what=f"3D {shape} {kernel3d}")
+    check(prob, oracle_lib, what=f"3D {shape}")
 
 
 @pytest.mark.parametrize("name", ["c2", "c3"])
-def test_3d_paths_match_oracle(oracle_lib, kernel3d, name):
-    check(W.small(name), oracle_lib, what=f"{name}/{kernel3d}")
+def test_3d_paths_match_oracle(oracle_lib, name):
+    check(W.small(name), oracle_lib, what=name)
 
 
-def test_3d_paths_bitwise_identical(monkeypatch):
-    """Both 3D Q2 kernels evaluate the same contract and the same backward FMA order."""
-    prob = W.small("c2")
-    monkeypatch.setenv("HYDRO_3D_KERNEL", "element")
-    a = H.run_full(prob)
-    monkeypatch.setenv("HYDRO_3D_KERNEL", "persistent")
-    b = H.run_full(prob)
-    assert np.array_equal(a["F1"], b["F1"]) and np.array_equal(a["FTw"], b["FTw"])
-    assert H.dt_bitwise(a["dt"], b["dt"])
-
-
-def test_3d_batched_sampled_matches_oracle(oracle_lib, kernel3d):
-    """hydro_force_sampled on a C2-shaped mesh with B = 3 instances, both 3D kernels."""
+def test_3d_batched_sampled_matches_oracle(oracle_lib):
+    """hydro_force_sampled on a C2-shaped mesh with B = 3 instances."""
     from tests.test_gpu_rom import gpu_step, oracle_instance
     base = W.small("c2")
     batch = W.rom_batch(base, B=3, n_sample=4, n_red=8)
@@ -161,7 +141,7 @@ def test_3d_batched_sampled_matches_oracle(oracle_lib, kernel3d):
         assert H.dt_bitwise(g["dt"][b], dt)
 
 
-def test_3d_inviscid(oracle_lib, kernel3d):
+def test_3d_inviscid(oracle_lib):
     prob = W.small("c2")
     prob.visc = False
-    check(prob, oracle_lib, what=f"3D inviscid {kernel3d}")
+    check(prob, oracle_lib, what="3D inviscid")

@@ -129,3 +129,47 @@ def test_pod_degenerate_cases():
     idx = hydro.deim(H.dev(np.ascontiguousarray(Q)))
     assert sorted(idx.tolist()) == list(range(12))
     np.testing.assert_array_equal(idx, ooff.deim(np.ascontiguousarray(Q)))
+
+
+@pytest.mark.parametrize("N,m,s", [(5_000, 8, 8), (50_001, 40, 1_337), (200_000, 40, 9_999)])
+def test_gappy_pinv_matches_oracle(N, m, s):
+    """hydro_gappy_pinv (CholQR2 on the GPU) against the oracle's library pseudo-inverse
+    (numpy SVD pinv, oracle.rom.offline_projectors' step) of the same sampled rows of a seeded
+    orthonormal basis; also P (U[rows]) = I."""
+    rng = np.random.default_rng(N + m)
+    U = np.linalg.qr(rng.standard_normal((N, m)))[0]
+    rows = np.sort(rng.choice(N, s, replace=False)).astype(np.int64)
+    P = hydro.gappy_pinv(H.dev(U), rows).cpu().numpy()
+    ref = np.linalg.pinv(U[rows])
+    scale = np.abs(ref).max()
+    assert np.abs(P - ref).max() <= 1e-11 * scale
+    assert np.abs(P @ U[rows] - np.eye(m)).max() <= 1e-11
+
+
+def test_offline_projectors_gpu_vs_oracle():
+    """The four offline operators of a small C4-shaped batch: GPU (hydro.offline_projectors)
+    against oracle.rom.offline_projectors."""
+    from oracle import rom as orom
+    batch = W.c4(n_sample=6, B=3, small_mesh=True)
+    got = [t.cpu().numpy() for t in H.gpu_offline_ops(batch)]
+    want = orom.offline_projectors(batch)
+    for g, w, what in zip(got, want, ("P_v", "P_e", "C_xv", "c_x")):
+        assert g.shape == w.shape, what
+        assert np.abs(g - w).max() <= 1e-11 * max(np.abs(w).max(), 1e-300), what
+
+
+def test_pod_eps_one_rank_deficient():
+    """eps = 1 on a rank-deficient, non-zero snapshot set (near-duplicate snapshots): the GPU
+    POD keeps the numerical rank (DESIGN R31), like the oracle, with an orthonormal basis --
+    no noise directions reach the CholQR pass."""
+    rng = np.random.default_rng(31)
+    r, ns, N = 5, 20, 80_001
+    A = rng.standard_normal((N, r))
+    S = (A @ rng.standard_normal((r, ns))).T
+    S = np.ascontiguousarray(np.concatenate([S, S[:3] * (1 + 1e-15)]))
+    Phi_g, sg = hydro.pod(H.dev(S), eps=1.0)
+    Phi_o, so = ooff.pod(S, eps=1.0)
+    assert Phi_g.shape[1] == Phi_o.shape[1] == r
+    P = Phi_g.cpu().numpy()
+    assert np.abs(P.T @ P - np.eye(r)).max() <= 1e-12
+    assert np.abs(P @ (P.T @ S.T) - S.T).max() <= 1e-10 * np.abs(S).max()

@@ -69,8 +69,9 @@ def test_rom_small_lift_force_project(oracle_lib):
         H.assert_close(g["F1"][:, b], F1, F1m, H.TOL_LOCAL, f"F1_rows b={b}")
         H.assert_close(g["FT"][:, b], FT, FTm, H.TOL_LOCAL, f"FTw_rows b={b}")
         assert H.dt_bitwise(g["dt"][b], dt)
-    # projection
-    P_v, P_e, C_xv, c_x = W.offline_projectors(batch)
+    # projection (the same oracle-formed operators on both sides: this checks the GEMMs)
+    from oracle import rom as orom
+    P_v, P_e, C_xv, c_x = orom.offline_projectors(batch)
     rv = hydro.rom_project(H.dev(P_v), g["F1_t"]).cpu().numpy()
     re_ = hydro.rom_project(H.dev(P_e), g["FT_t"]).cpu().numpy()
     H.assert_close(rv, oracle_lib.project(P_v, g["F1"]), np.abs(P_v) @ np.abs(g["F1"]), 1e-13, "r_v")

@@ -30,12 +30,12 @@ def test_rom_step_matches_oracle(dim):
     else:
         batch = W.rom_batch(W.small("c0"), B=3, n_sample=5, n_red=8)
     base = batch.base
-    P_v, P_e, C_xv, c_x = W.offline_projectors(batch)
+    P_v, P_e, C_xv, c_x = orom.offline_projectors(batch)
     ctx = H.context(base)
     plan = hydro.SamplePlan(ctx, batch.sample_elems, batch.B)
     st = hydro.RomStepper(plan, H.dev(batch.Phi_x), H.dev(batch.Phi_v), H.dev(batch.Phi_e),
-                          H.dev(batch.x_os), H.dev(batch.v_os), H.dev(batch.e_os), H.dev(P_v),
-                          H.dev(P_e), H.dev(C_xv), H.dev(c_x))
+                          H.dev(batch.x_os), H.dev(batch.v_os), H.dev(batch.e_os),
+                          *H.gpu_offline_ops(batch))
     op = dict(base=base, closure_elems=batch.closure_elems, closure_nodes=batch.closure_nodes,
               s0_nodes=batch.s0_nodes, sample_elems=batch.sample_elems, Phi_x=batch.Phi_x,
               Phi_v=batch.Phi_v, Phi_e=batch.Phi_e, x_os=batch.x_os, v_os=batch.v_os,
@@ -63,7 +63,7 @@ def test_rom_step_instances_independent():
     """Instance b of a batch steps exactly like a B = 1 plan of that instance."""
     batch = W.c4(n_sample=4, B=3, small_mesh=True)
     base = batch.base
-    P_v, P_e, C_xv, c_x = W.offline_projectors(batch)
+    P_v, P_e, C_xv, c_x = H.gpu_offline_ops(batch)
     ctx = H.context(base)
     visc, cfl = hydro.Visc(base.q1, base.q2, base.visc), hydro.Cfl(base.alpha, base.alpha_mu)
     g = H.dev(base.gamma)
@@ -73,8 +73,7 @@ def test_rom_step_instances_independent():
         plan = hydro.SamplePlan(ctx, batch.sample_elems, B)
         st = hydro.RomStepper(plan, H.dev(batch.Phi_x), H.dev(batch.Phi_v), H.dev(batch.Phi_e),
                               H.dev(batch.x_os), H.dev(batch.v_os),
-                              H.dev(np.ascontiguousarray(batch.e_os[:, sl])), H.dev(P_v), H.dev(P_e),
-                              H.dev(C_xv), H.dev(c_x))
+                              H.dev(np.ascontiguousarray(batch.e_os[:, sl])), P_v, P_e, C_xv, c_x)
         Y = [H.dev(np.ascontiguousarray(a[:, sl])) for a in (batch.Yx, batch.Yv, batch.Ye)]
         st.step(*Y, g, visc, cfl, H.dev(np.ascontiguousarray(dt[sl])))
         torch.cuda.synchronize()
@@ -93,12 +92,12 @@ def test_rom_advance_controller_matches_oracle():
     1e-10 of their scale."""
     batch = W.c4(n_sample=6, B=3, small_mesh=True)
     base = batch.base
-    P_v, P_e, C_xv, c_x = W.offline_projectors(batch)
+    P_v, P_e, C_xv, c_x = orom.offline_projectors(batch)
     ctx = H.context(base)
     plan = hydro.SamplePlan(ctx, batch.sample_elems, batch.B)
     st = hydro.RomStepper(plan, H.dev(batch.Phi_x), H.dev(batch.Phi_v), H.dev(batch.Phi_e),
-                          H.dev(batch.x_os), H.dev(batch.v_os), H.dev(batch.e_os), H.dev(P_v),
-                          H.dev(P_e), H.dev(C_xv), H.dev(c_x))
+                          H.dev(batch.x_os), H.dev(batch.v_os), H.dev(batch.e_os),
+                          *H.gpu_offline_ops(batch))
     op = dict(base=base, closure_elems=batch.closure_elems, closure_nodes=batch.closure_nodes,
               s0_nodes=batch.s0_nodes, sample_elems=batch.sample_elems, Phi_x=batch.Phi_x,
               Phi_v=batch.Phi_v, Phi_e=batch.Phi_e, x_os=batch.x_os, v_os=batch.v_os,
@@ -137,26 +136,27 @@ def test_rom_windowed_advance_matches_oracle():
     visc, cfl = hydro.Visc(base.q1, base.q2, base.visc), hydro.Cfl(base.alpha, base.alpha_mu)
 
     def ops(b):
-        P_v, P_e, C_xv, c_x = W.offline_projectors(b)
+        P_v, P_e, C_xv, c_x = orom.offline_projectors(b)
         op = dict(base=base, closure_elems=b.closure_elems, closure_nodes=b.closure_nodes,
                   s0_nodes=b.s0_nodes, sample_elems=b.sample_elems, Phi_x=b.Phi_x, Phi_v=b.Phi_v,
                   Phi_e=b.Phi_e, x_os=b.x_os, v_os=b.v_os, e_os=b.e_os, R_v=P_v, R_e=P_e,
                   C_xv=C_xv, c_x=c_x)
         st = hydro.RomStepper(plan, H.dev(b.Phi_x), H.dev(b.Phi_v), H.dev(b.Phi_e), H.dev(b.x_os),
-                              H.dev(b.v_os), H.dev(b.e_os), H.dev(P_v), H.dev(P_e), H.dev(C_xv),
-                              H.dev(c_x))
+                              H.dev(b.v_os), H.dev(b.e_os), *H.gpu_offline_ops(b))
         return op, st
     op1, st1 = ops(b1)
     op2, st2 = ops(b2)
-    trans = tuple(W.window_transition_ops(getattr(b2, f"Phi_{f}"), getattr(b1, f"Phi_{f}"),
-                                          getattr(b2, f"{f}_os"), getattr(b1, f"{f}_os"))
-                  for f in ("x", "v", "e"))
+    # the transition operators on the GPU (hydro_window_ops, Eq. ic-tw over the closure rows)
+    def trans_ops(f):
+        T, c = hydro.window_ops(H.dev(getattr(b2, f"Phi_{f}")), H.dev(getattr(b1, f"Phi_{f}")),
+                                H.dev(getattr(b2, f"{f}_os")), H.dev(getattr(b1, f"{f}_os")))
+        return T, (c.reshape(-1).contiguous() if getattr(b1, f"{f}_os").ndim == 1 else c)
+    dtr = tuple(trans_ops(f) for f in ("x", "v", "e"))
     _, _, _, est0 = orom.rom_rk2avg_step(op1, b1.Yx, b1.Yv, b1.Ye, np.zeros(b1.B))
     dt0 = 0.7 * est0
     t1, t2 = 2.0 * float(est0.max()), 4.0 * float(est0.max())
     ref = orom.windowed_advance([dict(op=op1, t_end=t1), dict(op=op2, t_end=t2)],
                                 b1.Yx.copy(), b1.Yv.copy(), b1.Ye.copy(), 0.0, dt0, max_iters=20)
-    dtr = tuple((H.dev(T), H.dev(c)) for T, c in trans)
     got = hydro.rom_windowed_advance([dict(stepper=st1, t_end=t1, trans=dtr),
                                       dict(stepper=st2, t_end=t2)],
                                      H.dev(b1.Yx), H.dev(b1.Yv), H.dev(b1.Ye), g, visc, cfl, 0.0,

@@ -20,8 +20,8 @@ from paper_2104_11404_b200 import hydro  # noqa: E402
 
 @pytest.mark.parametrize("name", ["c0", "c1", "c2", "c3"])
 @pytest.mark.parametrize("kern2d", ["element", "point"])
-def test_store_then_transpose(oracle_lib, monkeypatch, name, kern2d):
-    monkeypatch.setenv("HYDRO_2D_KERNEL", kern2d)
+def test_store_then_transpose(oracle_lib, set_kernel_2d, name, kern2d):
+    set_kernel_2d(kern2d)
     prob = W.small(name)
     rng = np.random.default_rng(11)
     w = np.ascontiguousarray(prob.v + 0.05 * rng.standard_normal(prob.v.shape))

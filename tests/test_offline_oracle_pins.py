@@ -5,6 +5,7 @@ P26 POD of snapshots with a known SVD (S^T = Q1 diag(s) Q2^T from random orthogo
     the singular values are s, the energy criterion picks the closed-form k for thresholds on
     either side of each partial sum, and the basis spans Q1's leading columns;
 P27 the POD basis is orthonormal and reproduces every snapshot of an exactly rank-r set;
+    with eps = 1 its size is the numerical rank r (DESIGN R31);
 P28 DEIM on a permuted identity basis returns the permutation (each column's only nonzero);
 P29 the DEIM interpolation property: f in span(U) is reproduced exactly from its sampled
     rows, U (P^T U)^-1 P^T f = f, and the indices are distinct;
@@ -49,6 +50,20 @@ def test_P27_pod_orthonormal_and_reproduces_rank_r():
     np.testing.assert_allclose(Phi.T @ Phi, np.eye(4), atol=1e-13)
     np.testing.assert_allclose(Phi @ (Phi.T @ S.T), S.T, atol=1e-11 * np.abs(S).max())
     assert sig[4:].max() <= 1e-12 * sig[0]
+
+
+def test_P27b_pod_eps_one_gives_numerical_rank():
+    """eps = 1 keeps every numerically nonzero direction (DESIGN R31): on a rank-r snapshot
+    set (near-duplicate snapshots included) the basis has exactly r columns, whose span holds
+    every snapshot."""
+    rng = np.random.default_rng(7)
+    for r, ns in ((3, 10), (6, 16)):
+        A = rng.standard_normal((700, r))
+        S = (A @ rng.standard_normal((r, ns))).T
+        S = np.ascontiguousarray(np.concatenate([S, S[:2] * (1 + 1e-15)]))   # near-duplicates
+        Phi, sig = offline.pod(S, eps=1.0)
+        assert Phi.shape[1] == r
+        np.testing.assert_allclose(Phi @ (Phi.T @ S.T), S.T, atol=1e-11 * np.abs(S).max())
 
 
 def test_P28_deim_permutation_basis():

@@ -102,7 +102,7 @@ def test_P25_window_transition():
     offset -> the lifted state is reproduced exactly (up to rounding): os + Phi_w yhat_w =
     os + Phi_{w-1} yhat_{w-1}; (c) different offsets whose difference lies in span(Phi_w) ->
     the lifted state is again reproduced; (d) the factored offline form the GPU path uses,
-    T = Phi_w^T Phi_{w-1}, c = Phi_w^T (os_{w-1} - os_w) (workloads.window_transition_ops),
+    T = Phi_w^T Phi_{w-1}, c = Phi_w^T (os_{w-1} - os_w) (oracle.rom.window_transition_ops),
     agrees with the direct formula."""
     from oracle import rom
     rng = np.random.default_rng(3)
@@ -116,7 +116,7 @@ def test_P25_window_transition():
     os2 = os_ + Q2 @ rng.standard_normal(12)
     Y2 = rom.window_transition(Q2, Q, os2, os_, Y)
     np.testing.assert_allclose(os2[:, None] + Q2 @ Y2, os_[:, None] + Q @ Y, atol=1e-12)
-    T, c = W.window_transition_ops(Q2, Q, os2, os_)
+    T, c = rom.window_transition_ops(Q2, Q, os2, os_)
     np.testing.assert_allclose(T @ Y + c[:, None], Y2, atol=1e-12)
 
 

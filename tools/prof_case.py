@@ -46,11 +46,10 @@ def main():
             F1, FTw, dt = ctx.force_full(x, v, e, gamma, visc, cfl)
     else:
         plan = hydro.SamplePlan(ctx, b.sample_elems, b.B)
-        P_v, P_e, C_xv, c_x = W.offline_projectors(b)
         Phi_x, Phi_v, Phi_e = t(b.Phi_x), t(b.Phi_v), t(b.Phi_e)
         x_os, v_os, e_os = t(b.x_os), t(b.v_os), t(b.e_os)
         Yx, Yv, Ye = t(b.Yx), t(b.Yv), t(b.Ye)
-        Pv, Pe, Cxv, cx = t(P_v), t(P_e), t(C_xv), t(c_x)
+        Pv, Pe, Cxv, cx = hydro.offline_projectors(Phi_x, Phi_v, Phi_e, v_os, *W.sampled_row_maps(b))
         wsv = hydro.rom_project_workspace(b.nv, plan.s_v, b.B, dev)
         wse = hydro.rom_project_workspace(b.ne, plan.s_e, b.B, dev)
         # the bench's C4 step: 3 lifts, the sampled force, 2 projections, the r_x lift

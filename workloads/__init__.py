@@ -518,30 +518,6 @@ def sampled_row_maps(batch: RomBatch):
     return h1, l2
 
 
-def offline_projectors(batch: RomBatch):
-    """Offline (untimed) inputs of the projection step: P_v =
-    (Z_v^T Phi_v)^dagger [nv][s_v], P_e = (Z_e^T Phi_e)^dagger [ne][s_e] (SNS with M = I,
-    PAPER P:985-1000), C_xv = Phi_x^T Phi_v [nx][nv], c_x = Phi_x^T v_os [nx] -- all
-    restricted to the sample mesh, as the online phase sees it."""
-    h1, l2 = sampled_row_maps(batch)
-    P_v = np.ascontiguousarray(np.linalg.pinv(batch.Phi_v[h1]))
-    P_e = np.ascontiguousarray(np.linalg.pinv(batch.Phi_e[l2]))
-    C_xv = np.ascontiguousarray(batch.Phi_x.T @ batch.Phi_v)
-    c_x = np.ascontiguousarray(batch.Phi_x.T @ batch.v_os)
-    return P_v, P_e, C_xv, c_x
-
-
-def window_transition_ops(Phi_new, Phi_old, os_new, os_old):
-    """Offline operators of the time-window transition, PAPER Eq. ic-tw:
-    yhat_w = Phi_w^T (os_{w-1} + Phi_{w-1} yhat_{w-1} - os_w) = T yhat_{w-1} + c with
-    T = Phi_w^T Phi_{w-1} [n_w][n_{w-1}] and c = Phi_w^T (os_{w-1} - os_w) ([n_w] or
-    [n_w][B] for per-instance offsets).  The synthetic bases exist on the sample-mesh
-    closure rows only, so the products run over those rows."""
-    T = np.ascontiguousarray(Phi_new.T @ Phi_old)
-    c = np.ascontiguousarray(Phi_new.T @ (os_old - os_new))
-    return T, c
-
-
 def next_window(batch: RomBatch, keep: int = 24, seed: int = 77):
     """A second time window for a ROM batch (same mesh, sample and offsets): each field's
     basis keeps its first `keep` columns and replaces the rest by fresh seeded directions,
