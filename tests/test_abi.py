@@ -15,6 +15,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared():
     src = open(os.path.join(ROOT, "include", "hydro.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    # declarations of diagnostic builds only (not exported by the production library)
+    src = re.sub(r"#ifdef HYDRO_COUNT_ROT.*?#endif", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(hydro_[a-z0-9_]+)\s*\(", src)))
 
 
