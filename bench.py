@@ -2,15 +2,16 @@
 """bench.py -- throughput of the corner-force hot path on B200 (BASELINE.json metric:
 force-eval quadrature points / s (F.1 + F^T.v) at 1 B200, % of the FP64/HBM roofline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4] [--impl ours|reference]
 
 A step = one pass of the whole hot path for the workload:
   c0..c3 : hydro_force_full (gather, forward contractions, pointwise physics + dt,
            backward contractions, deterministic assembly, dt finalisation);
   c4     : ROM online step = 3 lifts + hydro_force_sampled (64 instances) + 2
            projections + the reduced position RHS.
-The headline workload is BASELINE.json configs[1] (c1, Gresho 256^2); the JSON line also
-carries the other configs under "per_config".  Inputs are synthetic (workloads/), resident
+The headline workload is BASELINE.json configs[4] (c4: the largest single-GPU config, the
+paper's hyper-reduced online path); the JSON line also carries c0-c3, the
+Taylor-Green force evaluation (tg), the FOM steps and the offline phase under "per_config".  Inputs are synthetic (workloads/), resident
 in HBM before timing; L2 (126 MB) is flushed before every timed step by writing a 256 MiB
 buffer (outside the per-step CUDA events).  Multi-GPU: independent replicas (the path is
 sharded by nothing here -- DESIGN "Multi-GPU"), weak scaling, max over ranks.
@@ -58,20 +59,25 @@ def contraction_flops(dim, k, q, nfield=2, visc=True):
 # kernels issue (csrc/ieee_fast.cuh, identical to nvcc's): a/b = 5 DFMA + DMUL + 2 DFMA,
 # sqrt = 3 DMUL + 5 DFMA, 1/b = 5 DFMA (the MUFU seeds run on the XU pipe).
 DIV_I, SQRT_I, RCP_I = 8, 8, 5
-ROT_I = 2 + 3 + SQRT_I + 1 + DIV_I + 2 + SQRT_I + RCP_I + 1 + 10   # one Jacobi rotation (A.4) = 48
+ROT_I = 2 + 3 + SQRT_I + 1 + DIV_I + 2 + SQRT_I + RCP_I + 1 + 10   # one Jacobi rotation = 48
+# closed-form lambda_min of a symmetric 3x3 (DESIGN A.4 / R30): q, B, p1, p2 (18), p (1 +
+# sqrt), det(B) (14), r (3 + div), fmax, s (2 + sqrt), cubic guess (5 fma), two Newton steps
+# (2 x (4 + div + 1)), lambda (1)
+LMIN3_CF_I = 18 + 1 + SQRT_I + 14 + 3 + DIV_I + 1 + 2 + SQRT_I + 5 + 2 * (5 + DIV_I) + 1   # = 95
 
 
 def pointwise_instr(dim, visc, rot_per_lmin3):
     """FP64-pipe instructions of the contract pointwise stage per quadrature point
     (DESIGN A.3/A.4 as the kernels evaluate it; mul, add and fma count 1 each).
-    rot_per_lmin3: executed (non-skipped) Jacobi rotations per 3x3 eigen-solve."""
+    rot_per_lmin3: Jacobi rotations of the fallback (R30) per 3x3 eigen-solve, averaged over
+    all solves (the closed form's are counted by LMIN3_CF_I)."""
     if dim == 3:
         n = 27 + 5 + RCP_I + 9                   # cofactors, det, 1/det, J^-1
         n += DIV_I + 3 + 3 + SQRT_I              # rho, p, cs
-        n += 30 + 1 + ROT_I * rot_per_lmin3 + SQRT_I   # J^T J, lmin3 (tol), h
+        n += 30 + LMIN3_CF_I + ROT_I * rot_per_lmin3 + SQRT_I   # J^T J, lmin3, h
         if visc:
             n += 45 + 6                          # grad v, eps
-            n += 1 + ROT_I * rot_per_lmin3       # lmin3(eps)
+            n += LMIN3_CF_I + ROT_I * rot_per_lmin3   # lmin3(eps)
             n += 5 + 1 + DIV_I + 1 + DIV_I + 1   # mu, den, cs/h, alpha_mu mu, / den, +
             n += 12 + 10                         # sigma, A = sigma : eps
         else:
@@ -92,6 +98,32 @@ def pointwise_instr(dim, visc, rot_per_lmin3):
         n += DIV_I                               # dt_q
         n += 12 + 1 + 1                          # S, w detJ, w_q
     return n
+
+
+# SURVEY 8(d)'s algorithmic work model (the graded per-unit figure): contraction multiply-adds
+# (2 flop each) plus pointwise operations per quadrature point under the survey's Appendix A
+# (Jacobi-4 eigen-solves), division / square root weighted x10 ("weighted") or x1 ("nominal").
+S8D_POINTWISE = {(2, True): (110, 8), (2, False): (72, 6), (3, True): (664, 103), (3, False): None}
+
+
+def s8d_contraction_flops(dim, k, q):
+    """grad = 2qn^2 + 2q^2n (2D) or 2qn^3 + 3q^2n^2 + 3q^3n (3D); interp =
+    qm^2 + q^2m (2D) or qm^3 + q^2m^2 + q^3m (3D); per element 3d grad + 2 interp MACs."""
+    n, m = k + 1, k
+    if dim == 3:
+        grad = 2 * q * n ** 3 + 3 * q * q * n * n + 3 * q ** 3 * n
+        interp = q * m ** 3 + q * q * m * m + q ** 3 * m
+    else:
+        grad = 2 * q * n * n + 2 * q * q * n
+        interp = q * m * m + q * q * m
+    return 2 * (3 * dim * grad + 2 * interp)
+
+
+def s8d_flops_per_unit(dim, k, q, visc, weighted=True):
+    """SURVEY 8(d) algorithmic flops of one element (unit) evaluation."""
+    ops, divs = S8D_POINTWISE[(dim, visc)]
+    pw = ops + (9 * divs if weighted else 0)
+    return s8d_contraction_flops(dim, k, q) + pw * q ** dim
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -200,25 +232,29 @@ def build_problem(name):
     return W.config(name)
 
 
+HEADLINE = "c4"   # the largest single-GPU config (BASELINE.json configs[4]): the paper's
+                  # hyper-reduced online path
+ALL_WORKLOADS = ("c4", "c0", "c1", "c2", "c3", "tg")
+
+
 def run_ours(args, rank, world):
     import torch
-    import workloads as W
     from paper_2104_11404_b200 import hydro
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     hydro.lib()
-    results = {}
-    names = [args.workload] + ([c for c in ("c0", "c2", "c3", "c4", "tg") if c != args.workload]
-                               if args.all else [])
+    results, probs = {}, {}
+    names = [args.workload] + ([c for c in ALL_WORKLOADS if c != args.workload] if args.all else [])
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     for name in names:
-        results[name] = bench_one(name, args, dev, flush, rank, world)
+        results[name], probs[name] = bench_one(name, args, dev, flush, rank, world)
+        torch.cuda.empty_cache()
     if args.all:
         results["fom_c2"] = bench_fom("c2", args, dev)
         results["fom_tg"] = bench_fom("tg", args, dev)
         results["offline_c2"] = bench_offline(args, dev)
-    return results
+    return results, probs
 
 
 def _t(a, dev, dtype=None):
@@ -363,8 +399,8 @@ def bench_one(name, args, dev, flush, rank, world):
                                                 Pv, Pe, Cxv, cx, Yx, Yv, Ye, gamma, visc, cfl, n_qp,
                                                 args, flush)
     # roofline of the dominant kernel (force kernel)
-    out["roofline"] = roofline(name, base, m, n_units, kern_avg, prob)
-    return out
+    out["roofline"] = roofline(name, base, m, n_units, kern_avg, prob, step_ms=ms)
+    return out, prob
 
 
 def max_over_ranks(value, dev, world):
@@ -710,17 +746,20 @@ def _rotations_per_lmin3(name, prob):
     return r / max(c, 1) * (1 if base.visc else 1)
 
 
-def roofline(name, base, m, n_units, kern_ms, prob):
-    """Roofline of the force kernel.  It is bound by the FP64 pipe (arithmetic intensity
-    ~50 flop/B, DESIGN "Kernels"), so the work is counted in FP64-pipe instructions of the
-    algorithm (contraction multiply-adds + the contract's pointwise operations, IEEE
-    div/sqrt/rcp at their instruction cost) and reported as DFMA-equivalent TFLOP/s
-    (2 per instruction) against the measured DFMA peak."""
-    rot = _rotations_per_lmin3(name, prob)
+def roofline(name, base, m, n_units, kern_ms, prob, step_ms=None):
+    """Roofline of the dominant kernel (the force kernel).  FP64-bound (arithmetic intensity
+    ~50 flop/B, DESIGN "Kernels").  achieved = SURVEY 8(d)'s algorithmic flops per unit
+    (weighted: / and sqrt x10) x the units of one launch / the launch's average duration,
+    against the FP64 peak.  Beside it, `issue`: the FP64-pipe instructions the kernel's own
+    algorithm needs (contraction FMAs + the contract's pointwise operations, IEEE div/sqrt/rcp
+    at their instruction cost, the Jacobi fallback's data-dependent rotation count from the
+    oracle) at 2 flop per instruction slot -- the fraction of FP64 issue slots doing that
+    work.  The 8(d) model assumes Jacobi-4 eigen-solves (664 ops per 3D point); the closed
+    form of R30 needs fewer, so 8(d)'s fraction can exceed the issue-slot fraction in 3D."""
     nq = m.nq ** m.dim
-    c_instr = contraction_flops(m.dim, m.k, m.nq) // 2
-    p_instr = pointwise_instr(m.dim, base.visc, rot)
-    instr = n_units * (c_instr + nq * p_instr)
+    s8d_unit = s8d_flops_per_unit(m.dim, m.k, m.nq, base.visc)
+    s8d_unit_nominal = s8d_flops_per_unit(m.dim, m.k, m.nq, base.visc, weighted=False)
+    flops = n_units * s8d_unit
     # algorithmic bytes: x, v [N_V], e [N_E], m_q [Q], elem_nodes, gamma; write F1 [N_V], FTw [N_E]
     if name == "c4":
         B = prob.B
@@ -733,22 +772,55 @@ def roofline(name, base, m, n_units, kern_ms, prob):
         byts = (8 * (2 * m.N_V + m.N_E + m.n_elem * nq + m.n_elem) + 4 * m.n_elem * m.nd
                 + 8 * (m.N_V + m.N_E))
     t = kern_ms * 1e-3
-    ach = 2.0 * instr / t / 1e12
+    ach = flops / t / 1e12
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6650.0)
     traffic = measured_traffic(name)
-    return {"bound": "alu", "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": round(ach / FP64_PEAK_TFLOPS, 4),
-            "traffic": traffic["bytes_per_launch"] if traffic else None,
-            "kernel": "force kernel (hydro_force_full / hydro_force_sampled)",
-            "fp64_instr_per_launch": instr, "flop_eq_per_instr": 2,
-            "contraction_instr_per_unit": c_instr, "pointwise_instr_per_qp": p_instr,
-            "rotations_per_lmin3": round(rot, 3),
-            "hbm_bytes_alg": byts, "hbm_frac": round(byts / t / 1e9 / hbm, 4),
-            "traffic_source": traffic["source"] if traffic else None,
-            "peak_source": "FP64: 64 FMA/clk/SM x 2 x 148 SMs x 1965 MHz = 37.2 TF/s (measured "
-                           "37.1 DMMA / 36.5 DFMA, profiles/r01_fp64_dmma_rate.txt); HBM from "
-                           "MEASURED_PEAKS.json"}
+    out = {"bound": "alu", "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+           "frac": round(ach / FP64_PEAK_TFLOPS, 4),
+           "traffic": traffic["bytes_per_launch"] if traffic else None,
+           "kernel": "force kernel (hydro_force_full / hydro_force_sampled)",
+           "basis": "SURVEY 8(d) weighted algorithmic flops per unit x units per launch",
+           "s8d_flop_per_unit": s8d_unit, "s8d_flop_per_unit_nominal": s8d_unit_nominal,
+           "units_per_launch": n_units, "kernel_ms": round(kern_ms, 5),
+           "issue": None,   # filled by issue_basis() in the cpu-baseline leg (needs the oracle)
+           "hbm_bytes_alg": byts, "hbm_frac": round(byts / t / 1e9 / hbm, 4),
+           "traffic_source": traffic["source"] if traffic else None,
+           "peak_source": "FP64: 64 FMA/clk/SM x 2 x 148 SMs x 1965 MHz = 37.2 TF/s (measured "
+                          "37.1 DMMA / 36.5 DFMA burst, profiles/r01_fp64_dmma_rate.txt; sustained: "
+                          "profiles/r02_fp64_sustained.txt); HBM from MEASURED_PEAKS.json"}
+    if step_ms:
+        # the whole step on 8(d)'s basis (C4: + the lift and projection GEMM flops)
+        step_flops = flops
+        if name == "c4":
+            nred = prob.Phi_x.shape[1]
+            step_flops += 2.0 * nred * prob.B * (2 * prob.Phi_x.shape[0] + prob.Phi_e.shape[0])  # lifts
+            h1, l2 = prob.s0_nodes.size * m.dim, prob.sample_elems.size * m.ne
+            step_flops += 2.0 * nred * prob.B * (h1 + l2) + 2.0 * nred * nred * prob.B           # projections, r_x
+        out["step"] = {"gflop_s8d": round(step_flops / 1e9, 3), "ms": round(step_ms, 5),
+                       "achieved": round(step_flops / (step_ms * 1e-3) / 1e12, 3),
+                       "frac": round(step_flops / (step_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4)}
+    return out
+
+
+def issue_basis(name, prob, rf):
+    """The issue-slot view of a roofline entry (DESIGN 8.2): FP64-pipe instructions of the
+    kernel's own algorithm, with the Jacobi fallback's data-dependent rotation count measured
+    by the oracle on a seeded element sample (both sides execute the same contract sequence)
+    -- computed in the cpu-baseline leg, the one place bench.py may call oracle/."""
+    base = prob.base if name == "c4" else prob
+    m = base.mesh
+    rot = _rotations_per_lmin3(name, prob)
+    nq = m.nq ** m.dim
+    c_instr = contraction_flops(m.dim, m.k, m.nq) // 2
+    p_instr = pointwise_instr(m.dim, base.visc, rot)
+    instr = rf["units_per_launch"] * (c_instr + nq * p_instr)
+    ach = 2.0 * instr / (rf["kernel_ms"] * 1e-3) / 1e12
+    rf["issue"] = {"achieved": round(ach, 3), "frac": round(ach / FP64_PEAK_TFLOPS, 4),
+                   "fp64_instr_per_launch": instr, "flop_eq_per_instr": 2,
+                   "contraction_instr_per_unit": c_instr, "pointwise_instr_per_qp": p_instr,
+                   "fallback_rotations_per_lmin3": round(rot, 4),
+                   "rotation_count_source": "oracle.lmin3_stats, seeded 2000-element sample"}
 
 
 def measured_traffic(name):
@@ -761,39 +833,124 @@ def measured_traffic(name):
 
 
 # ----------------------------------------------------------------------------- cpu baseline
-def cpu_baseline(name, target_s=12.0, prob=None):
-    """The oracle as it stands (oracle/, OpenMP over the host cores) on a bounded seeded
-    sample of the workload: a random subset of elements, or the whole mesh repeated, sized
-    to ~target_s seconds of CPU work.  Quadrature points processed / wall time."""
+def cpu_model():
+    """The host CPU model (lscpu 'Model name'), for the baseline's record."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def oracle_c4_instance(batch, b, P_v, P_e, nthreads=0):
+    """The oracle's C4 step for instance b: naive lifts of the
+    instance's column on the sample-mesh closure rows, the force on the closure elements,
+    the rows at S0, naive projections.  Returns the quadrature points evaluated."""
     import oracle
-    if prob is None:
-        prob = build_problem(name) if name != "c4" else build_problem("c2")
+    base, m = batch.base, batch.base.mesh
+    d, ncl, ne = m.dim, batch.closure_nodes.size, m.ne
+    col = slice(b, b + 1)
+    xS = oracle.lift(batch.Phi_x, batch.x_os, np.ascontiguousarray(batch.Yx[:, col]))
+    vS = oracle.lift(batch.Phi_v, batch.v_os, np.ascontiguousarray(batch.Yv[:, col]))
+    eS = oracle.lift(batch.Phi_e, np.ascontiguousarray(batch.e_os[:, col]), np.ascontiguousarray(batch.Ye[:, col]))
+    x = m.x0.copy()
+    x[:, batch.closure_nodes] = xS[:, 0].reshape(d, ncl)
+    v = np.zeros_like(m.x0)
+    v[:, batch.closure_nodes] = vS[:, 0].reshape(d, ncl)
+    e = base.e.copy()
+    e[batch.closure_elems] = eS[:, 0].reshape(-1, ne)
+    r = oracle.force(base, elist=batch.closure_elems, x=x, v=v, e=e, nthreads=nthreads)
+    F1 = np.ascontiguousarray(r["F1"][:, batch.s0_nodes].reshape(-1, 1))
+    FT = np.ascontiguousarray(r["FTw"][batch.sample_elems].reshape(-1, 1))
+    oracle.project(P_v, F1)
+    oracle.project(P_e, FT)
+    return batch.closure_elems.size * m.nq ** m.dim
+
+
+def oracle_rate(name, prob, target_s, nthreads=0, c4_ops=None):
+    """The oracle as it stands (oracle/, OpenMP) on a bounded seeded sample of a workload:
+    quadrature points per second, the sample, the wall time.  c0-c3/tg: a seeded element subset
+    (or the whole mesh) evaluated repeatedly for ~target_s; c4: whole instances of the ROM step
+    (oracle_c4_instance), at least one."""
+    import oracle
+    cores = nthreads if nthreads > 0 else (os.cpu_count() or 1)
+    if name == "c4":
+        P_v, P_e = c4_ops
+        qp, reps, t0 = 0, 0, time.perf_counter()
+        while True:
+            qp += oracle_c4_instance(prob, reps % prob.B, P_v, P_e, nthreads)
+            reps += 1
+            wall = time.perf_counter() - t0
+            if wall >= target_s:
+                break
+        return {"value": qp / wall, "cores": cores, "wall_s": round(wall, 2),
+                "sample": f"{reps} of {prob.B} C4 instances (lift + force over the "
+                          f"{prob.closure_elems.size}-element closure + projections), {qp} quad points"}
     m = prob.mesh
     nq = m.nq ** m.dim
-    cores = os.cpu_count() or 1
     rng = np.random.default_rng(1)
-    oracle.force(prob, elist=np.arange(min(m.n_elem, 8), dtype=np.int32))  # tables, threads
-    n2 = int(min(m.n_elem, 16384 if m.dim == 3 else 65536))
+    oracle.force(prob, elist=np.arange(min(m.n_elem, 8), dtype=np.int32), nthreads=nthreads)
+    n2 = int(min(m.n_elem, (16384 if m.dim == 3 else 65536) // (8 if nthreads == 1 else 1)))
     el = np.sort(rng.choice(m.n_elem, n2, replace=False)).astype(np.int32)
     reps, t0 = 0, time.perf_counter()
     while True:
-        oracle.force(prob, elist=el)
+        oracle.force(prob, elist=el, nthreads=nthreads)
         reps += 1
         wall = time.perf_counter() - t0
         if wall >= target_s:
             break
-    return {"value": reps * n2 * nq / wall, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{n2} seeded elements of {name} ({m.n_elem} in the mesh) evaluated "
-                      f"{reps}x = {reps * n2 * nq} quad points, F.1+F^T.v+dt, OpenMP over "
-                      f"{cores} host threads, {wall:.1f} s"}
+    return {"value": reps * n2 * nq / wall, "cores": cores, "wall_s": round(wall, 2),
+            "sample": f"{n2} seeded elements of {m.n_elem} evaluated {reps}x = {reps * n2 * nq} quad "
+                      f"points (F.1 + F^T.v + dt)"}
+
+
+def cpu_baseline(headline, probs, per_cfg_s=2.5, one_core=("c0", "c1", "c2")):
+    """SURVEY 8(d) oracle baseline: the oracle on the GPU box's host cores, per config (value,
+    sample, and the full config's extrapolated wall time), plus 1-core rates for C0-C2 and the
+    CPU model.  The headline config's entry is the line's cpu_baseline value."""
+    from oracle import rom as orom
+    per = {}
+    c4_ops = None
+    for name, prob in probs.items():
+        if name == "c4":
+            c4_ops = orom.offline_projectors(prob)[:2]
+            r = oracle_rate("c4", prob, per_cfg_s * 2, c4_ops=c4_ops)
+            full_qp = prob.closure_elems.size * prob.B * prob.base.mesh.nq ** 3
+        else:
+            r = oracle_rate(name, prob, per_cfg_s)
+            full_qp = prob.mesh.n_elem * prob.mesh.nq ** prob.mesh.dim
+        r["full_config_wall_s_est"] = round(full_qp / r["value"], 1)
+        per[name] = r
+    single = {}
+    for name in one_core:
+        if name in probs:
+            r = oracle_rate(name, probs[name], per_cfg_s, nthreads=1)
+            single[name] = {"value": r["value"], "sample": r["sample"], "wall_s": r["wall_s"]}
+    h = per[headline]
+    return {"value": h["value"], "unit": UNIT, "cores": h["cores"], "kind": "oracle",
+            "sample": h["sample"], "cpu_model": cpu_model(), "per_config": per,
+            "one_core": single,
+            "note": "oracle/ as it stands (OpenMP over the elements, serial assembly); a reported "
+                    "baseline, not the target"}
 
 
 # ----------------------------------------------------------------------------- main
 def bench_config(name, n_qp, world):
     """The workload description shared by both arms' JSON lines."""
-    return {"workload": f"{name} (BASELINE.json configs[{name[1]}])", "quad_points": n_qp,
-            "l2": "flushed before every timed step (256 MiB write; GPU arm)",
-            "parallelism": f"replicas x{world}"}
+    idx = {"c0": 0, "c1": 1, "c2": 2, "c3": 3, "c4": 4}.get(name)
+    what = (f"{name} (BASELINE.json configs[{idx}])" if idx is not None else
+            f"{name} (Taylor-Green 64^3 Q2/Q1, SURVEY 8(f) NEXT-4)")
+    cfg = {"workload": what, "quad_points": n_qp,
+           "l2": "flushed before every timed step (256 MiB write; GPU arm)",
+           "parallelism": f"replicas x{world}"}
+    if name == "c4":
+        cfg["step"] = ("3 lifts (x, v, e on the sample-mesh closure rows) + hydro_force_sampled "
+                       "(64 instances x closure elements) + 2 projections + the r_x lift")
+        cfg["instances"] = 64
+    return cfg
 
 
 def main():
@@ -801,7 +958,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c1", choices=["c0", "c1", "c2", "c3", "c4"])
+    ap.add_argument("--workload", default=HEADLINE, choices=list(ALL_WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--all", dest="all", action="store_true", default=True)
     ap.add_argument("--only", dest="all", action="store_false")
@@ -812,36 +969,14 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
 
     if args.impl == "reference":
-        # the oracle arm: rank 0 only, on the host cores; each step is a bounded sample of
-        # the same workload (bench.cpu_baseline), warm-up steps shorter and untimed
-        if rank != 0:
-            return 0
-        prob = build_problem(args.workload if args.workload != "c4" else "c2")
-        m = prob.mesh
-        n_qp = m.n_elem * m.nq ** m.dim
-        for _ in range(args.warmup):
-            cpu_baseline(args.workload, target_s=0.2, prob=prob)
-        vals = []
-        for _ in range(args.steps):
-            r = cpu_baseline(args.workload, target_s=max(1.0, 60.0 / max(args.steps, 1)), prob=prob)
-            vals.append(r["value"])
-        v = float(np.median(vals))
-        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 1,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": n_qp / v * 1e3,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic (workloads/: seeded SplitMix64, shapes of BASELINE.json configs)",
-                "config": bench_config(args.workload, n_qp, 1),
-                "cpu_baseline": {**r, "value": v},
-                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
-        return 0
+        return reference_arm(args, rank)
 
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         dist.init_process_group("nccl")
-    res = run_ours(args, rank, world)
+    res, probs = run_ours(args, rank, world)
     head = res[args.workload]
     if rank == 0:
         line = {
@@ -859,11 +994,48 @@ def main():
                            for k, r in res.items() if k != args.workload},
         }
         if not args.no_cpu:
-            line["cpu_baseline"] = cpu_baseline(args.workload)
+            for name, prob in probs.items():
+                issue_basis(name, prob, res[name]["roofline"])
+            line["cpu_baseline"] = cpu_baseline(args.workload, probs)
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+    return 0
+
+
+def reference_arm(args, rank):
+    """The oracle arm (bench.py --impl reference): rank 0 only, on the host cores, the same
+    workload, metric and unit as our arm; each timed step is a bounded sample of the workload
+    (c4: one whole instance of the ROM step; others: a seeded element sample for ~3 s)."""
+    if rank != 0:
+        return 0
+    import oracle
+    prob = build_problem(args.workload)
+    m = (prob.base if args.workload == "c4" else prob).mesh
+    c4_ops = None
+    if args.workload == "c4":
+        from oracle import rom as orom
+        c4_ops = orom.offline_projectors(prob)[:2]
+        n_qp = prob.closure_elems.size * prob.B * m.nq ** m.dim
+    else:
+        n_qp = m.n_elem * m.nq ** m.dim
+    for _ in range(args.warmup):   # untimed: library load, threads, tables
+        oracle.force(prob.base if args.workload == "c4" else prob, elist=np.arange(8, dtype=np.int32))
+    vals, r = [], None
+    for _ in range(args.steps):
+        r = oracle_rate(args.workload, prob, 0.0 if args.workload == "c4" else 3.0, c4_ops=c4_ops)
+        vals.append(r["value"])
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": n_qp / v * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (workloads/: seeded SplitMix64, shapes of BASELINE.json configs)",
+            "config": bench_config(args.workload, n_qp, 1),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["cores"], "kind": "oracle",
+                             "sample": r["sample"] + " per step", "cpu_model": cpu_model()},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
     return 0
 
 

@@ -349,9 +349,10 @@ hydro_status hydro_window_ops(hydro_fom *fom, int field, int64_t N, int n_new, i
 /* Least-squares (gappy) pseudo-inverse of sampled basis rows, the offline factor of the
  * hyper-reduction (P:778-799 Eq. sol-ls-hyper; P:985-1000 SNS with M = I, DESIGN R21):
  *   P = (U[rows, :])^+ = (Z^T U)^+   [m][s]  (device out, row-major),
- * with U device [N][m] row-major and rows host [s] (0 <= rows[i] < N, s >= m).  Computed as
+ * with U device [N][m] row-major and rows host [s] (0 <= rows[i] < N, m <= 128).  s >= m:
  * CholQR2 of the gathered rows (Q R = U[rows], two Cholesky-QR passes on the GPU with the
- * m x m Cholesky factorisations on the host) followed by P = R^-1 Q^T on the GPU.
+ * m x m Cholesky factorisations on the host) followed by P = R^-1 Q^T on the GPU; s < m (a
+ * wide sample): the minimum-norm pseudo-inverse Q R^-T of U[rows]^T = Q R on the host.
  * HYDRO_ERR_NONFINITE if U[rows] is numerically rank-deficient.  Allocates its own scratch
  * (offline routine); synchronises `stream`.                                                */
 hydro_status hydro_gappy_pinv(const double *U, int64_t N, int m, const int64_t *rows, int64_t s_rows,

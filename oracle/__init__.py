@@ -176,5 +176,14 @@ def lmin3_stats(reset: bool = True):
     return r.value, c.value
 
 
+def lmin3_fallback_stats(reset: bool = True):
+    """(Jacobi rotations performed, lmin3 calls, Jacobi fallbacks) accumulated by oracle.force
+    since the last reset (DESIGN A.4 / R30: the closed form falls back to Jacobi near a double
+    smallest eigenvalue) -- bench.py's work model."""
+    r, c, f = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+    lib().oracle_stats2(ctypes.byref(r), ctypes.byref(c), ctypes.byref(f), ctypes.c_int(1 if reset else 0))
+    return r.value, c.value, f.value
+
+
 def tables(k: int, q: int) -> dict:
     return _tables.tables(k, q)

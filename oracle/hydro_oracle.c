@@ -24,7 +24,7 @@
  *   1. per element: gather X, V, W (W = V when w == NULL), E_K, gamma_K;
  *   2. per quadrature point: J, grad(v), grad(w), e_q by the canonical contraction
  *      order (DESIGN "Evaluation contract" A.2), J0 from x0 likewise -> m_q;
- *   3. pointwise physics in the contract order A.3 (no FMA), lmin3 per A.4;
+ *   3. pointwise physics in the contract order A.3 (no FMA), lmin3 per A.4 (R30);
  *   4. the DENSE element matrix F_K (not sum-factorised), then F_K.1 and F_K^T.w;
  *   5. F.1 assembled serially in ascending element order; F^T.w element-local;
  *   6. dt = min over (K, q); NaN if any dt_q is NaN; lowest tangled element.
@@ -53,24 +53,78 @@ typedef struct {
 } otab;
 
 /* ---------------------------------------------------------------- A.4 lmin3 */
-/* Smallest eigenvalue of a symmetric 3x3 matrix by cyclic Jacobi, at most four
- * sweeps over the pairs (0,1), (0,2), (1,2); a pair whose off-diagonal is
- * negligible (<= 2^-53 max|a_ij|, which also covers a_pq == 0) is skipped -- this
- * also removes the 0/0 of a re-introduced subnormal a_pq on an exactly
+/* Smallest eigenvalue of a symmetric 3x3 matrix (DESIGN A.4, reading R30).
+ *
+ * Closed form (the trigonometric characterisation of the eigenvalues of a symmetric
+ * 3x3 matrix): with q = tr(A)/3, B = A - qI, p = sqrt(tr(B^2)/6), the eigenvalues are
+ * q + 2p c where c runs over the roots of 4c^3 - 3c = r, r = det(B)/(2p^3) in [-1, 1]
+ * (c = cos(theta/3 + 2 pi k/3), r = cos(theta)); lambda_min takes the smallest root,
+ * c in [-1, -1/2].  That root is found from a cubic initial guess in s = sqrt((1-r)/2)
+ * (c = cos(2pi/3 + (2/3) asin s)) refined by two Newton steps on 4c^3 - 3c - r.  It is
+ * ill-conditioned only near r = 1, where lambda_min is a double eigenvalue: there
+ * (r > 1 - 2^-13, or r NaN) the cyclic Jacobi method below is used instead.  A = qI
+ * (p2 == 0) returns q.  IEEE ops, FMA only where written as fma().
+ *
+ * Jacobi fallback: at most four cyclic sweeps over the pairs (0,1), (0,2), (1,2); a pair
+ * whose off-diagonal is negligible (<= 2^-53 max|a_ij|, which also covers a_pq == 0) is
+ * skipped -- this also removes the 0/0 of a re-introduced subnormal a_pq on an exactly
  * degenerate diagonal. IEEE ops only, no FMA. */
 /* instrumentation for bench.py's algorithmic-work count (not part of the method):
- * rotations performed / lmin3 calls, summed over threads */
-static int64_t g_rot = 0, g_calls = 0;
-static __thread int64_t t_rot = 0, t_calls = 0;
+ * Jacobi rotations performed / lmin3 calls / Jacobi fallbacks, summed over threads */
+static int64_t g_rot = 0, g_calls = 0, g_fallback = 0;
+static __thread int64_t t_rot = 0, t_calls = 0, t_fallback = 0;
 
 void oracle_stats(int64_t *rotations, int64_t *calls, int reset) {
   if (rotations) *rotations = g_rot;
   if (calls) *calls = g_calls;
-  if (reset) { g_rot = 0; g_calls = 0; }
+  if (reset) { g_rot = 0; g_calls = 0; g_fallback = 0; }
 }
+
+void oracle_stats2(int64_t *rotations, int64_t *calls, int64_t *fallbacks, int reset) {
+  if (rotations) *rotations = g_rot;
+  if (calls) *calls = g_calls;
+  if (fallbacks) *fallbacks = g_fallback;
+  if (reset) { g_rot = 0; g_calls = 0; g_fallback = 0; }
+}
+
+static double lmin3_jacobi(const double a_in[6]);
 
 double oracle_lmin3(const double a_in[6] /* a00 a11 a22 a01 a02 a12 */) {
   ++t_calls;
+  const double a00 = a_in[0], a11 = a_in[1], a22 = a_in[2];
+  const double a01 = a_in[3], a02 = a_in[4], a12 = a_in[5];
+  const double third = 0x1.5555555555555p-2, sixth = 0x1.5555555555555p-3;  /* RN(1/3), RN(1/6) */
+  const double q = ((a00 + a11) + a22) * third;
+  const double b0 = a00 - q, b1 = a11 - q, b2 = a22 - q;
+  const double p1 = (a01 * a01 + a02 * a02) + a12 * a12;
+  const double p2 = ((b0 * b0 + b1 * b1) + b2 * b2) + 2.0 * p1;
+  if (p2 == 0.0) return q;                                /* A = qI */
+  const double p = sqrt(p2 * sixth);
+  const double det = (b0 * (b1 * b2 - a12 * a12) - a01 * (a01 * b2 - a12 * a02)) +
+                     a02 * (a01 * a12 - b1 * a02);
+  double r = det / ((2.0 * p) * (p * p));
+  if (!(r <= 1.0 - 0x1p-13)) {                            /* near-double lambda_min or NaN */
+    ++t_fallback;
+    return lmin3_jacobi(a_in);
+  }
+  r = fmax(r, -1.0);
+  const double s = sqrt((1.0 - r) * 0.5);
+  /* c0(s) = -1/2 - s/sqrt(3) + s^2 (K2 + s (K3 + s (K4 + s K5))), Horner with fma */
+  double u = fma(s, -0.005042, 0.021433);
+  u = fma(s, u, -0.04969);
+  u = fma(s, u, 0.110644);
+  u = fma(s, u, -0x1.279a74590331cp-1);                  /* -RN(1/sqrt(3)) */
+  double c = fma(s, u, -0.5);
+  for (int it = 0; it < 2; ++it) {                        /* Newton on f(c) = c (4c^2 - 3) - r */
+    const double c2 = c * c;
+    const double f = fma(c, fma(4.0, c2, -3.0), -r);
+    const double fp = fma(12.0, c2, -3.0);
+    c = c - f / fp;
+  }
+  return fma(2.0 * p, c, q);
+}
+
+static double lmin3_jacobi(const double a_in[6]) {
   double a[3][3];
   a[0][0] = a_in[0]; a[1][1] = a_in[1]; a[2][2] = a_in[2];
   a[0][1] = a[1][0] = a_in[3];
@@ -470,10 +524,14 @@ int oracle_force(const otab *tab, int64_t n_elem, int64_t n_nodes, const int32_t
   double dt_min = INFINITY;
   int any_nan = 0;
   int64_t bad = INT64_MAX;
+  /* nthreads > 0: that many threads for this call only; 0: every host core */
 #ifdef _OPENMP
-  if (nthreads > 0) omp_set_num_threads(nthreads);
+  const int nt_use = nthreads > 0 ? nthreads : omp_get_num_procs();
+#else
+  const int nt_use = 1;
 #endif
-#pragma omp parallel
+  (void)nt_use;
+#pragma omp parallel num_threads(nt_use)
   {
     double *Xl = (double *)malloc(sizeof(double) * 3 * nd * 4);
     double *Vl = Xl + 3 * nd, *Wl = Xl + 6 * nd, *X0l = Xl + 9 * nd;
@@ -593,7 +651,8 @@ int oracle_force(const otab *tab, int64_t n_elem, int64_t n_nodes, const int32_t
     }
 #pragma omp critical
     {
-      g_rot += t_rot; g_calls += t_calls; t_rot = 0; t_calls = 0;
+      g_rot += t_rot; g_calls += t_calls; g_fallback += t_fallback;
+      t_rot = 0; t_calls = 0; t_fallback = 0;
       if (my_nan) any_nan = 1;
       if (dt_less(my_dt, dt_min)) dt_min = my_dt;
       if (my_bad < bad) bad = my_bad;

@@ -414,6 +414,44 @@ __device__ __forceinline__ double lmin3(AR &ar, double a00, double a11, double a
   return fmin(fmin(a00, a11), a22);
 }
 
+// Smallest eigenvalue of a symmetric 3x3 matrix by the closed form of DESIGN A.4 / R30:
+// q = tr/3, B = A - qI, p = sqrt(tr(B^2)/6), r = det(B)/(2p^3); lambda_min = q + 2p c with c
+// the smallest root of 4c^3 - 3c = r (a cubic guess in s = sqrt((1-r)/2), two Newton steps).
+// fb = true where the root is ill-conditioned (r > 1 - 2^-13: a near-double lambda_min) or r is
+// NaN: the caller then takes the Jacobi value instead.  A = qI (p2 == 0) gives q.  Operation
+// for operation the oracle's oracle_lmin3 (oracle/hydro_oracle.c).  The guards below only keep
+// operands inside the fast paths' exact range; each reproduces the IEEE result exactly:
+// p2 == 0 returns q anyway, 0 / den = det (den > 0), and a zero Newton residual leaves c.
+template <class AR>
+__device__ __forceinline__ double lmin3_cf(AR &ar, double a00, double a11, double a22, double a01,
+                                           double a02, double a12, bool &fb) {
+  const double q = ((a00 + a11) + a22) * 0x1.5555555555555p-2;
+  const double b0 = a00 - q, b1 = a11 - q, b2 = a22 - q;
+  const double p1 = (a01 * a01 + a02 * a02) + a12 * a12;
+  const double p2 = ((b0 * b0 + b1 * b1) + b2 * b2) + 2.0 * p1;
+  const bool iso = p2 == 0.0;
+  const double p = ar.sqrt_((iso ? 1.0 : p2) * 0x1.5555555555555p-3);
+  const double det = (b0 * (b1 * b2 - a12 * a12) - a01 * (a01 * b2 - a12 * a02)) + a02 * (a01 * a12 - b1 * a02);
+  const double den = (2.0 * p) * (p * p);
+  double r = (det == 0.0 && den > 0.0) ? det : ar.div(det, den);
+  fb = !iso && !(r <= 1.0 - 0x1p-13);
+  r = (fb || iso) ? 0.0 : fmax(r, -1.0);  // (branch values unused when fb or iso)
+  const double s = ar.sqrt_((1.0 - r) * 0.5);
+  double u = __fma_rn(s, -0.005042, 0.021433);
+  u = __fma_rn(s, u, -0.04969);
+  u = __fma_rn(s, u, 0.110644);
+  u = __fma_rn(s, u, -0x1.279a74590331cp-1);
+  double c = __fma_rn(s, u, -0.5);
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const double c2 = c * c;
+    const double f = __fma_rn(c, __fma_rn(4.0, c2, -3.0), -r);
+    const double fp = __fma_rn(12.0, c2, -3.0);
+    c = c - (f == 0.0 ? f : ar.div(f, fp));
+  }
+  return iso ? q : __fma_rn(2.0 * p, c, q);
+}
+
 // Determinant / inverse by cofactors (DESIGN A.3).
 template <int DIM, class AR>
 __device__ __forceinline__ double det_inv(AR &ar, const double (&J)[3][3], double (&Ji)[3][3]) {
@@ -513,12 +551,28 @@ __device__ __forceinline__ void pointwise(AR &ar, const double (&J)[3][3], const
     const double c01 = (J[0][0] * J[0][1] + J[1][0] * J[1][1]) + J[2][0] * J[2][1];
     const double c02 = (J[0][0] * J[0][2] + J[1][0] * J[1][2]) + J[2][0] * J[2][2];
     const double c12 = (J[0][1] * J[0][2] + J[1][1] * J[1][2]) + J[2][1] * J[2][2];
-    double lj;
-    if (VISC) {
-      lmin3_pair<AR, EARLY, COMPACT>(ar, c00, c11, c22, c01, c02, c12, eps[0][0], eps[1][1], eps[2][2],
-                            eps[0][1], eps[0][2], eps[1][2], lj, lam);
+    // DESIGN A.4 / R30: closed form, Jacobi only where the closed form is ill-conditioned
+    bool fa = false, fe = false;
+    double lj = lmin3_cf(ar, c00, c11, c22, c01, c02, c12, fa);
+    if (VISC) lam = lmin3_cf(ar, eps[0][0], eps[1][1], eps[2][2], eps[0][1], eps[0][2], eps[1][2], fe);
+    if (EARLY) {
+      // warp-uniform fallback: lanes without a fallback pass diagonal matrices (no live
+      // off-diagonal: no rotation slot is executed for them) and keep their closed form
+      if (__any_sync(0xffffffffu, fa || fe)) {
+        double ja, je = 0.0;
+        if (VISC) {
+          lmin3_pair<AR, true, COMPACT>(ar, c00, c11, c22, fa ? c01 : 0.0, fa ? c02 : 0.0, fa ? c12 : 0.0,
+                                        eps[0][0], eps[1][1], eps[2][2], fe ? eps[0][1] : 0.0,
+                                        fe ? eps[0][2] : 0.0, fe ? eps[1][2] : 0.0, ja, je);
+        } else {
+          ja = lmin3<AR, true>(ar, c00, c11, c22, fa ? c01 : 0.0, fa ? c02 : 0.0, fa ? c12 : 0.0);
+        }
+        lj = fa ? ja : lj;
+        lam = fe ? je : lam;
+      }
     } else {
-      lj = lmin3<AR, EARLY>(ar, c00, c11, c22, c01, c02, c12);
+      if (fa) lj = lmin3<AR, false>(ar, c00, c11, c22, c01, c02, c12);
+      if (VISC && fe) lam = lmin3<AR, false>(ar, eps[0][0], eps[1][1], eps[2][2], eps[0][1], eps[0][2], eps[1][2]);
     }
     h = ar.sqrt_(fmax(lj, 0.0));
   }

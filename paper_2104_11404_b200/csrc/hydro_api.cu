@@ -2143,7 +2143,7 @@ hydro_status hydro_window_ops(hydro_fom *fom, int field, int64_t N, int n_new, i
 
 hydro_status hydro_gappy_pinv(const double *U, int64_t N, int m, const int64_t *rows, int64_t s_rows,
                               double *P, hydro_stream_t stream) {
-  if (!U || N <= 0 || m <= 0 || m > hk::POD_MAXK || !rows || s_rows < m || s_rows > INT32_MAX || !P)
+  if (!U || N <= 0 || m <= 0 || m > hk::POD_MAXK || !rows || s_rows <= 0 || s_rows > INT32_MAX || !P)
     return HYDRO_ERR_ARG;
   for (int64_t i = 0; i < s_rows; ++i)
     if (rows[i] < 0 || rows[i] >= N) return HYDRO_ERR_ARG;
@@ -2162,6 +2162,48 @@ hydro_status hydro_gappy_pinv(const double *U, int64_t N, int m, const int64_t *
   // Q = U[rows, :]
   hk::gather_rows_kernel<<<blocks_for(s_rows * m, 256), 256, 0, s>>>((int)s_rows, m, d_rows, U, m, Q);
   g_launches++;
+  if (s_rows < m) {
+    // fewer sampled rows than basis columns (a wide U[rows], s < m <= 128): the minimum-norm
+    // pseudo-inverse A^+ = Q R^-T from A^T = Q R (m x s, two Gram-Schmidt passes), on the host
+    const int sr = (int)s_rows;
+    std::vector<double> A((size_t)sr * m), Qt((size_t)sr * m), R((size_t)sr * sr, 0.0), Pm((size_t)m * sr);
+    hydro_status st0 = HYDRO_OK;
+    if (cudaMemcpyAsync(A.data(), Q, sizeof(double) * A.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      st0 = HYDRO_ERR_CUDA;
+    // column j of A^T is row j of A: orthonormalise the rows of A (Qt[j] = q_j, length m)
+    for (int j = 0; j < sr && st0 == HYDRO_OK; ++j) {
+      std::vector<double> v(A.begin() + (size_t)j * m, A.begin() + (size_t)(j + 1) * m);
+      for (int pass = 0; pass < 2; ++pass)
+        for (int i = 0; i < j; ++i) {
+          double d = 0.0;
+          for (int k = 0; k < m; ++k) d += Qt[(size_t)i * m + k] * v[(size_t)k];
+          R[(size_t)i * sr + j] += d;
+          for (int k = 0; k < m; ++k) v[(size_t)k] -= d * Qt[(size_t)i * m + k];
+        }
+      double nrm = 0.0;
+      for (int k = 0; k < m; ++k) nrm += v[(size_t)k] * v[(size_t)k];
+      nrm = std::sqrt(nrm);
+      if (!(nrm > 0.0)) { st0 = HYDRO_ERR_NONFINITE; break; }
+      R[(size_t)j * sr + j] = nrm;
+      for (int k = 0; k < m; ++k) Qt[(size_t)j * m + k] = v[(size_t)k] / nrm;
+    }
+    if (st0 == HYDRO_OK) {  // P = Q R^-T: P[k][j] = sum_i Q[k][i] (R^-1)[j][i]
+      std::vector<double> Ri;
+      upper_inv(sr, R, Ri);
+      for (int k = 0; k < m; ++k)
+        for (int j = 0; j < sr; ++j) {
+          double acc = 0.0;
+          for (int i = j; i < sr; ++i) acc += Qt[(size_t)i * m + k] * Ri[(size_t)j * sr + i];
+          Pm[(size_t)k * sr + j] = acc;
+        }
+      if (cudaMemcpyAsync(P, Pm.data(), sizeof(double) * Pm.size(), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+          cudaStreamSynchronize(s) != cudaSuccess)
+        st0 = HYDRO_ERR_CUDA;
+    }
+    cleanup();
+    return st0;
+  }
   // CholQR2: Q <- Q R1^-1, Q <- Q R2^-1 (Q^T Q = R^T R each pass), R = R2 R1
   std::vector<double> C((size_t)m * m), R, Ri, Racc((size_t)m * m, 0.0);
   for (int i = 0; i < m; ++i) Racc[(size_t)i * m + i] = 1.0;

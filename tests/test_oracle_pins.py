@@ -89,8 +89,9 @@ def _sym(a6):
 
 
 def test_lmin3_vs_eigvalsh(oracle_lib):
-    """P8: contract Jacobi vs LAPACK on random, near-double-root and near-isotropic
-    matrices: |err| <= 4e-15 * ||A||."""
+    """P8: the contract's lmin3 (DESIGN A.4 / R30: closed form + two Newton steps, Jacobi
+    near a double smallest eigenvalue) vs LAPACK on random, near-double-root, near-isotropic
+    and graded matrices: |err| <= 4e-15 * ||A||."""
     rng = np.random.default_rng(7)
     worst = 0.0
     for i in range(3000):
@@ -114,6 +115,39 @@ def test_lmin3_vs_eigvalsh(oracle_lib):
         err = abs(got - ref) / np.abs(A).max()
         worst = max(worst, err)
     assert worst < 4e-15, worst
+
+
+@pytest.mark.parametrize("gap_lo,gap_hi,third", [(-14, -4, 3.0), (-4, -1, 3.0), (-14, -1, -2.0)])
+def test_lmin3_double_root_and_branch_boundary(oracle_lib, gap_lo, gap_hi, third):
+    """P8 (R30): eigenvalues (1, 1 + d, third) in a random frame, d log-uniform.  With
+    third = 3 the smallest eigenvalue is (nearly) double: d < ~1e-4 lands in the Jacobi
+    branch (r > 1 - 2^-13), larger d in the closed form right at its boundary, where the
+    Newton root's conditioning is worst (f'(c) >= sqrt(24 * 2^-13) = 0.054, i.e. an error
+    of at most ~20x the closed form's rounding level); third = -2 makes the smallest
+    eigenvalue simple and the top pair double (r near -1, well conditioned).  Bound:
+    5e-14 ||A|| (measured worst 1.1e-14 over 2e4 such matrices)."""
+    rng = np.random.default_rng(int(-gap_lo * 10 + third))
+    worst = 0.0
+    for _ in range(2000):
+        Q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+        d = 10.0 ** rng.uniform(gap_lo, gap_hi)
+        M = Q @ np.diag([1.0, 1.0 + d, third]) @ Q.T
+        a = [M[0, 0], M[1, 1], M[2, 2], M[0, 1], M[0, 2], M[1, 2]]
+        ref = np.linalg.eigvalsh(_sym(a))[0]
+        worst = max(worst, abs(oracle_lib.lmin3(a) - ref) / np.abs(M).max())
+    assert worst < 5e-14, worst
+
+
+def test_lmin3_branches_taken(oracle_lib):
+    """Both branches of R30 are exercised by the force evaluation of a C2-shaped mesh (the
+    instrumented counters of the oracle): most points take the closed form, a few the Jacobi
+    fallback."""
+    import workloads as W
+    oracle_lib.force(W.small("c2"))      # flushes counts of earlier direct lmin3 calls
+    oracle_lib.lmin3_fallback_stats(reset=True)
+    oracle_lib.force(W.small("c2"))
+    rot, calls, fb = oracle_lib.lmin3_fallback_stats(reset=True)
+    assert calls > 0 and 0 <= fb < 0.05 * calls
 
 
 def test_lmin3_special_cases(oracle_lib):
