@@ -814,48 +814,126 @@ hydro_status hydro_sample_status_sync(hydro_sample *p, hydro_stream_t stream,
   return status_sync_impl(p->st, p->B, (cudaStream_t)stream, first_bad_elem);
 }
 
-hydro_status hydro_rom_lift(int64_t rows, int n, int B, const double *Phi, const double *os,
-                            int os_batched, const double *Y, double *out, hydro_stream_t stream) {
-  if (rows < 0 || n <= 0 || n > 256 || B <= 0 || !Phi || !os || !Y || !out) return HYDRO_ERR_ARG;
-  if (rows == 0) return HYDRO_OK;
-  const size_t smem = sizeof(double) * (size_t)(n * hk::LIFT_CB + hk::LIFT_RT * (n + 1));
-  static size_t smem_set = 0;
-  if (smem > 48 * 1024 && smem > smem_set) {
-    CUDA_OK(cudaFuncSetAttribute(hk::lift_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set = smem;
+}  // extern "C"
+
+namespace {
+
+template <int NKS>
+hydro_status launch_lift_mma(int64_t rows, int n, int B, const double *Phi, const double *os, int os_batched,
+                             const double *Y, double *out, cudaStream_t s) {
+  static std::atomic<int> sms{0};
+  if (sms.load() == 0) {
+    int dev = 0, v = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+    sms.store(v);
   }
-  dim3 grid((unsigned)((rows + hk::LIFT_RT - 1) / hk::LIFT_RT), (unsigned)((B + hk::LIFT_CB - 1) / hk::LIFT_CB));
-  hk::lift_kernel<<<grid, hk::LIFT_THREADS, smem, (cudaStream_t)stream>>>(rows, n, B, Phi, os, os_batched, Y, out);
+  const int64_t tiles = (rows + hk::LIFT_MMA_RT - 1) / hk::LIFT_MMA_RT;
+  const int64_t g = std::min<int64_t>(tiles, (int64_t)sms.load() * 2);   // persistent: 2 CTAs per SM
+  dim3 grid((unsigned)g, (unsigned)((B + 63) / 64));
+  hk::lift_mma_kernel<NKS><<<grid, hk::LIFT_MMA_THREADS, 0, s>>>(rows, n, B, Phi, os, os_batched, Y, out);
   g_launches++;
   CUDA_OK(cudaGetLastError());
   return HYDRO_OK;
 }
 
-static int project_groups(int64_t s_rows) {
-  int64_t g = (s_rows + 255) / 256;  // >= 256 rows per group
-  if (g > 148 * 8) g = 148 * 8;
+template <int MT>
+hydro_status launch_project_mma(int n, int64_t s_rows, int B, int G, int64_t chunk, const double *P,
+                                const double *f, double *part, double *r, cudaStream_t s) {
+  constexpr size_t smem = sizeof(double) * 4 * MT * 4 * 2 * 32;
+  static std::atomic<unsigned long long> attr_done{0};
+  int dev = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(attr_done.load() & bit)) {
+    CUDA_OK(cudaFuncSetAttribute(hk::project_mma_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_done.fetch_or(bit);
+  }
+  hk::project_mma_kernel<MT><<<G, hk::PROJ_MMA_THREADS, smem, s>>>(n, s_rows, B, chunk, P, f, part);
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  const int nB = n * B;
+  hk::project_mma_reduce_kernel<<<(nB + hk::PROJ_RED_OUT - 1) / hk::PROJ_RED_OUT, 256, 0, s>>>(nB, G, part, r);
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hydro_status hydro_rom_lift(int64_t rows, int n, int B, const double *Phi, const double *os,
+                            int os_batched, const double *Y, double *out, hydro_stream_t stream) {
+  if (rows < 0 || n <= 0 || n > 256 || B <= 0 || !Phi || !os || !Y || !out) return HYDRO_ERR_ARG;
+  if (rows == 0) return HYDRO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  // the FP64 tensor-pipe kernel (n <= 64); os/out rows of 16-byte aligned pairs
+  const bool aligned = ((uintptr_t)out % 16 == 0) && (!os_batched || (uintptr_t)os % 16 == 0) && B % 2 == 0;
+  if (aligned && n <= 64) {
+    const int nks = (n + 3) / 4;
+    if (nks <= 2) return launch_lift_mma<2>(rows, n, B, Phi, os, os_batched, Y, out, st);
+    if (nks <= 4) return launch_lift_mma<4>(rows, n, B, Phi, os, os_batched, Y, out, st);
+    if (nks <= 8) return launch_lift_mma<8>(rows, n, B, Phi, os, os_batched, Y, out, st);
+    if (nks <= 10) return launch_lift_mma<10>(rows, n, B, Phi, os, os_batched, Y, out, st);
+    return launch_lift_mma<16>(rows, n, B, Phi, os, os_batched, Y, out, st);
+  }
+  const size_t smem = sizeof(double) * (size_t)(n * hk::LIFT_CB + hk::LIFT_RT * (n + 1));
+  static std::atomic<unsigned long long> attr_done{0};
+  if (smem > 48 * 1024) {
+    int dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_done.load() & bit)) {
+      CUDA_OK(cudaFuncSetAttribute(hk::lift_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(double) * (256 * hk::LIFT_CB + hk::LIFT_RT * 257))));
+      attr_done.fetch_or(bit);
+    }
+  }
+  dim3 grid((unsigned)((rows + hk::LIFT_RT - 1) / hk::LIFT_RT), (unsigned)((B + hk::LIFT_CB - 1) / hk::LIFT_CB));
+  hk::lift_kernel<<<grid, hk::LIFT_THREADS, smem, st>>>(rows, n, B, Phi, os, os_batched, Y, out);
+  g_launches++;
+  CUDA_OK(cudaGetLastError());
+  return HYDRO_OK;
+}
+
+// split-K groups of the projection: the tensor-pipe kernel (n <= 40, B <= 64) uses up to
+// 2 CTAs per SM with >= 512 rows each; the fallback up to 8 per SM with >= 256 rows each
+static int project_groups(int n, int64_t s_rows, int B) {
+  const bool mma = n <= 40 && B <= 64;
+  int64_t g = mma ? (s_rows + 511) / 512 : (s_rows + 255) / 256;
+  const int64_t cap = mma ? 148 * 2 : 148 * 8;
+  if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;
 }
 
 size_t hydro_rom_project_workspace_bytes(int n, int64_t s_rows, int B) {
   if (n <= 0 || B <= 0 || s_rows < 0) return 0;
-  return sizeof(double) * (size_t)project_groups(s_rows) * n * B;
+  return sizeof(double) * (size_t)project_groups(n, s_rows, B) * n * B;
 }
 
 hydro_status hydro_rom_project(int n, int64_t s_rows, int B, const double *P, const double *f,
                                double *r, void *workspace, size_t ws_bytes, hydro_stream_t stream) {
   if (n <= 0 || n > hk::PROJ_MAXN || B <= 0 || B > hk::PROJ_MAXB || s_rows < 0 || !P || !f || !r)
     return HYDRO_ERR_ARG;
-  const int G = project_groups(s_rows);
+  const int G = project_groups(n, s_rows, B);
   if (!workspace || ws_bytes < sizeof(double) * (size_t)G * n * B) return HYDRO_ERR_WORKSPACE;
-  const int64_t chunk = (s_rows + G - 1) / G;
+  const int64_t chunk = std::max<int64_t>((s_rows + G - 1) / G, 1);
   cudaStream_t s = (cudaStream_t)stream;
-  hk::project_partial_kernel<<<G, hk::PROJ_THREADS, 0, s>>>(n, s_rows, B, chunk > 0 ? chunk : 1, P, f,
-                                                             (double *)workspace);
+  double *part = (double *)workspace;
+  if (n <= 40) {
+    const int mt = (n + 7) / 8;
+    if (mt == 1) return launch_project_mma<1>(n, s_rows, B, G, chunk, P, f, part, r, s);
+    if (mt == 2) return launch_project_mma<2>(n, s_rows, B, G, chunk, P, f, part, r, s);
+    if (mt == 3) return launch_project_mma<3>(n, s_rows, B, G, chunk, P, f, part, r, s);
+    if (mt == 4) return launch_project_mma<4>(n, s_rows, B, G, chunk, P, f, part, r, s);
+    return launch_project_mma<5>(n, s_rows, B, G, chunk, P, f, part, r, s);
+  }
+  hk::project_partial_kernel<<<G, hk::PROJ_THREADS, 0, s>>>(n, s_rows, B, chunk, P, f, part);
   g_launches++;
   CUDA_OK(cudaGetLastError());
-  hk::project_reduce_kernel<<<(n * B + 255) / 256, 256, 0, s>>>(n, B, G, (const double *)workspace, r);
+  hk::project_reduce_kernel<<<(n * B + 255) / 256, 256, 0, s>>>(n, B, G, part, r);
   g_launches++;
   CUDA_OK(cudaGetLastError());
   return HYDRO_OK;

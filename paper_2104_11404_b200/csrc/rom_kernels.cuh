@@ -72,6 +72,203 @@ lift_kernel(int64_t rows, int n, int B, const double *__restrict__ Phi,
   }
 }
 
+// ---------------------------------------------------------------------------- FP64 MMA
+// D (8x8) = A (8x4, row) B (4x8, col) + C on the FP64 tensor pipe (mma.sync m8n8k4 f64, the
+// DMMA path: 256 FMAs per warp instruction at the same 37 TF/s as DFMA, measured
+// profiles/r01_fp64_dmma_rate.txt).  Fragments (lane l): A[l>>2][l&3], B[l&3][l>>2],
+// C/D[l>>2][2(l&3) + {0,1}].  Not volatile: the scheduler may move loads across it.
+__device__ __forceinline__ void dmma_m8n8k4(double &d0, double &d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// lift on the tensor pipe: out[r][c] = os + sum_k Phi[r][k] Y[k][c] for n <= 4 NKS, B <= 64
+// per column block (grid.y).  Persistent CTAs of 8 warps over 128-row tiles (16 rows = two
+// m-tiles per warp); Y's column block is staged once per CTA in shared memory in fragment
+// order (conflict-free LDS.64); each warp preloads its 2 x NKS A fragments (Phi rows, 32 B
+// per row per k-step: full sectors) and issues 16 DMMAs per k-step from 32 accumulators.
+constexpr int LIFT_MMA_THREADS = 256, LIFT_MMA_RT = 128;
+template <int NKS>
+__global__ void __launch_bounds__(LIFT_MMA_THREADS, 2)
+lift_mma_kernel(int64_t rows, int n, int B, const double *__restrict__ Phi,
+                const double *__restrict__ os, int os_batched, const double *__restrict__ Y,
+                double *__restrict__ out) {
+  __shared__ double sY[NKS * 8 * 32];   // [kstep][ntile][lane]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c0 = blockIdx.y * 64;
+  for (int i = threadIdx.x; i < NKS * 8 * 32; i += LIFT_MMA_THREADS) {
+    const int l = i & 31, nt = (i >> 5) & 7, ks = i >> 8;
+    const int k = ks * 4 + (l & 3), c = c0 + nt * 8 + (l >> 2);
+    sY[i] = (k < n && c < B) ? Y[(int64_t)k * B + c] : 0.0;
+  }
+  __syncthreads();
+  const int64_t ntiles = (rows + LIFT_MMA_RT - 1) / LIFT_MMA_RT;
+  const int ar = lane >> 2, ak = lane & 3;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t rw = t * LIFT_MMA_RT + warp * 16;   // this warp's first row
+    double a[2][NKS];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int64_t r = rw + mt * 8 + ar;
+#pragma unroll
+      for (int ks = 0; ks < NKS; ++ks) {
+        const int k = ks * 4 + ak;
+        a[mt][ks] = (r < rows && k < n) ? __ldg(Phi + r * n + k) : 0.0;
+      }
+    }
+    double acc[2][8][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < NKS; ++ks) {
+      double b[8];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) b[nt] = sY[(ks * 8 + nt) * 32 + lane];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) dmma_m8n8k4(acc[mt][nt][0], acc[mt][nt][1], a[mt][ks], b[nt]);
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int64_t r = rw + mt * 8 + ar;
+      if (r >= rows) continue;
+      const double o1 = os_batched ? 0.0 : __ldg(os + r);
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const int c = c0 + nt * 8 + 2 * ak;
+        if (c + 1 < B) {
+          double2 o;
+          if (os_batched) {
+            o = __ldg(reinterpret_cast<const double2 *>(os + r * B + c));
+          } else {
+            o.x = o1;
+            o.y = o1;
+          }
+          double2 v;
+          v.x = o.x + acc[mt][nt][0];
+          v.y = o.y + acc[mt][nt][1];
+          *reinterpret_cast<double2 *>(out + r * B + c) = v;
+        } else if (c < B) {
+          out[r * B + c] = (os_batched ? __ldg(os + r * B + c) : o1) + acc[mt][nt][0];
+        }
+      }
+    }
+  }
+}
+
+// projection on the tensor pipe, split-K: CTA g reduces a fixed contiguous range of s into
+// a partial [n][B] (n <= 8 MT, B <= 64).  Within the CTA, warp w = 2 kg + nh takes every 4th
+// k-step of the range (k-group kg, fixed) for the column half nh (4 n-tiles) and all MT m-tiles
+// (40 accumulators for MT = 5); the four k-group partials of each half are summed in a fixed
+// tree through shared memory; project_mma_reduce sums the CTA partials in ascending g (fixed
+// order, parallel over 8 sub-ranges per output).  Deterministic.
+constexpr int PROJ_MMA_THREADS = 256;
+template <int MT>
+__global__ void __launch_bounds__(PROJ_MMA_THREADS, 2)
+project_mma_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *__restrict__ P,
+                   const double *__restrict__ f, double *__restrict__ part) {
+  extern __shared__ __align__(16) double sred[];   // [4 slots][MT*4 tiles][2][32]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nh = warp & 1, kg = warp >> 1;
+  const int64_t s_begin = (int64_t)blockIdx.x * chunk;
+  const int64_t s_end = s_begin + chunk < s_rows ? s_begin + chunk : s_rows;
+  const int ar = lane >> 2, ak = lane & 3;
+  double acc[MT][4][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  const bool fullB = B == 64;
+#pragma unroll 2
+  for (int64_t k0 = s_begin + kg * 4; k0 < s_end; k0 += 16) {
+    const int64_t k = k0 + ak;   // A: P[m][k] (m = 8 mt + (l >> 2)); B: f[k][c] (c = 8 nt + (l >> 2))
+    const bool kin = k < s_end;
+    double a[MT], b[4];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int m = mt * 8 + ar;
+      a[mt] = (kin && m < n) ? __ldg(P + (int64_t)m * s_rows + k) : 0.0;
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int c = (nh * 4 + nt) * 8 + ar;
+      b[nt] = (kin && (fullB || c < B)) ? __ldg(f + k * B + c) : 0.0;
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) dmma_m8n8k4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+  }
+  // fixed tree over the k-groups of each column half: (kg, kg + 2), then (0, 1)
+  constexpr int TS = MT * 4 * 2 * 32;
+#pragma unroll
+  for (int half = 2; half >= 1; half >>= 1) {
+    if (kg >= half && kg < 2 * half) {
+      double *dst = sred + ((kg - half) * 2 + nh) * TS;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          dst[((mt * 4 + nt) * 2 + 0) * 32 + lane] = acc[mt][nt][0];
+          dst[((mt * 4 + nt) * 2 + 1) * 32 + lane] = acc[mt][nt][1];
+        }
+    }
+    __syncthreads();
+    if (kg < half) {
+      const double *src = sred + (kg * 2 + nh) * TS;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          acc[mt][nt][0] += src[((mt * 4 + nt) * 2 + 0) * 32 + lane];
+          acc[mt][nt][1] += src[((mt * 4 + nt) * 2 + 1) * 32 + lane];
+        }
+    }
+    __syncthreads();
+  }
+  if (kg == 0) {
+    double *pg = part + (int64_t)blockIdx.x * n * B;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int m = mt * 8 + ar;
+      if (m >= n) continue;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int c = (nh * 4 + nt) * 8 + 2 * ak;
+        if (c < B) pg[m * B + c] = acc[mt][nt][0];
+        if (c + 1 < B) pg[m * B + c + 1] = acc[mt][nt][1];
+      }
+    }
+  }
+}
+
+// r[o] = sum_g part[g][o] in ascending g: 8 threads per output sum fixed contiguous g-ranges,
+// combined in ascending range order through shared memory.
+constexpr int PROJ_RED_OUT = 32;
+__global__ void __launch_bounds__(256) project_mma_reduce_kernel(int nB, int G, const double *__restrict__ part,
+                                                                 double *__restrict__ r) {
+  __shared__ double ssum[8][PROJ_RED_OUT];
+  const int o = blockIdx.x * PROJ_RED_OUT + (threadIdx.x & 31);
+  const int j = threadIdx.x >> 5;
+  const int per = (G + 7) / 8;
+  const int g0 = j * per, g1 = min(G, g0 + per);
+  double acc = 0.0;
+  if (o < nB)
+    for (int g = g0; g < g1; ++g) acc += __ldg(part + (int64_t)g * nB + o);
+  ssum[j][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (j == 0 && o < nB) {
+    double t = ssum[0][threadIdx.x];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) t += ssum[i][threadIdx.x];
+    r[o] = t;
+  }
+}
+
 constexpr int PROJ_THREADS = 256;
 constexpr int PROJ_TS = 32;      // s-rows per shared tile
 constexpr int PROJ_MAXN = 64;
