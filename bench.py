@@ -450,7 +450,22 @@ def bench_rom_step(plan, b, Phi_x, Phi_v, Phi_e, x_os, v_os, e_os, Pv, Pe, Cxv, 
         ms.append(e0.elapsed_time(e1))
     status = plan.status_sync()[0]
     step_ms = float(np.median(ms))
+    # NEXT-2: the previous-window offset transition (Eq. previous_os) at this size:
+    # three per-instance lifts of the final state over the closure rows + c_x = Phi_x^T v_os
+    tr = []
+    for i in range(4):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        hydro.rom_previous_window((Phi_x, Phi_v, Phi_e), (x_os, v_os, e_os), Y, (Phi_x, Phi_v, Phi_e), Phi_x)
+        e1.record()
+        torch.cuda.synchronize()
+        if i > 0:
+            tr.append(e0.elapsed_time(e1))
+    trans_ms = float(np.median(tr))
     return {"ms_per_step": step_ms, "instances": b.B, "sampled_force_passes": 2,
+            "previous_window_transition_ms": trans_ms,
+            "previous_window_transition_in_steps": round(trans_ms / step_ms, 4),
             "transpose_passes": 2, "qp_per_s": 2 * n_qp / (step_ms * 1e-3), "status": status,
             "what": "hyper-reduced RK2-average step, 64 instances, CUDA-graph replay"}
 

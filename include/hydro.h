@@ -266,7 +266,8 @@ hydro_status hydro_fom_advance(hydro_fom *fom, double *x, double *v, double *e,
  * Phi_{x,v,e}_S (closure rows, [rows][n] row-major) and the offsets (os_batched_flags bit 0/1/2:
  * x/v/e offset is [rows][B] instead of [rows]).  The offline operators are given:
  * R_v = Mhat_V^-1 Phi_v^T Phi_F1 (Z^T Phi_F1)^+ [nv][s_v], R_e likewise [ne][s_e] (Eq.
- * sol-ls-hyper), C_xv = Phi_x^T Phi_v [nx][nv], c_x = Phi_x^T v_os [nx].
+ * sol-ls-hyper), C_xv = Phi_x^T Phi_v [nx][nv], c_x = Phi_x^T v_os [nx] (
+ * os_batched_flags bit 3: c_x is [nx][B], for per-instance velocity offsets).
  * dt: device [B] per-instance step; dt_est (device [B] or NULL) = min over both stages'
  * estimates.  Two sampled force evaluations per step (storing the S0 elements'
  * point stresses) and two transposed F^T w passes.  All device pointers are kept by the
@@ -357,6 +358,22 @@ hydro_status hydro_window_ops(hydro_fom *fom, int field, int64_t N, int n_new, i
  * (offline routine); synchronises `stream`.                                                */
 hydro_status hydro_gappy_pinv(const double *U, int64_t N, int m, const int64_t *rows, int64_t s_rows,
                               double *P, hydro_stream_t stream);
+/* The previous-window offset of a time-window transition, PAPER Eq. previous_os:
+ *   os_w = os_{w-1} + Phi_{w-1} yhat_{w-1}(t_{w-1})      (os_new: device [rows][B], out)
+ * -- the lift of the previous window's final state over the basis rows (the FOM rows, or the
+ * sample-mesh closure rows of a hyper-reduced plan), per instance; os_prev is [rows] or
+ * [rows][B] (os_prev_batched).  With this offset the new window starts from
+ * yhat_w(t_{w-1}) = Phi_w^T (os_{w-1} + Phi_{w-1} yhat_{w-1} - os_w) = 0: Y_new (device
+ * [n_new][B], or NULL with n_new = 0) is zeroed.  The offset-dependent operator of the new
+ * window, c_x = Phi_x,w^T v_os,w, follows from hydro_basis_tproduct.  Asynchronous.         */
+hydro_status hydro_rom_window_offset(int64_t rows, int n_prev, int B, const double *Phi_prev,
+                                     const double *os_prev, int os_prev_batched, const double *Y_prev,
+                                     double *os_new, int n_new, double *Y_new, hydro_stream_t stream);
+/* out = Phi^T X  ([n][B], device): Phi device [N][n], X device [N][B], both row-major, by a
+ * fixed-order split-K reduction over the N rows (deterministic).  E.g. c_x = Phi_x^T v_os
+ * for per-instance offsets.  Allocates its own scratch; synchronises `stream`.   */
+hydro_status hydro_basis_tproduct(int64_t N, int n, int B, const double *Phi, const double *X, double *out,
+                                  hydro_stream_t stream);
 /* The integrands of the a-posteriori bound, Theorem 2 Eq. aposteriori-semi, at
  * one (lifted) state (x, v, e) of a ROM trajectory (DESIGN R29):
  *   eta[0] = | (I - M_V Phi_v Mhat_V^-1 Phi_v^T P_F1) F.1(x, v, e) |_2,

@@ -104,7 +104,8 @@ def rom_rk2avg_step(op, Yx, Yv, Ye, dt):
     vS_h = lift(op["Phi_v"], op["v_os"], Yv_h)
     _, FT, _ = forces(xS, vS, eS, vS_h)
     Ye_h = Ye + 0.5 * dt * (op["R_e"] @ FT)
-    Yx_h = Yx + 0.5 * dt * (op["c_x"][:, None] + op["C_xv"] @ Yv_h)
+    cx = op["c_x"][:, None] if op["c_x"].ndim == 1 else op["c_x"]   # [nx] or per instance [nx][B]
+    Yx_h = Yx + 0.5 * dt * (cx + op["C_xv"] @ Yv_h)
     xS_h = lift(op["Phi_x"], op["x_os"], Yx_h)
     eS_h = lift(op["Phi_e"], op["e_os"], Ye_h)
     F1h, _, dt2 = forces(xS_h, vS_h, eS_h, vS_h)
@@ -113,7 +114,7 @@ def rom_rk2avg_step(op, Yx, Yv, Ye, dt):
     vS_b = lift(op["Phi_v"], op["v_os"], Yvb)
     _, FTh, _ = forces(xS_h, vS_h, eS_h, vS_b)
     Ye1 = Ye + dt * (op["R_e"] @ FTh)
-    Yx1 = Yx + dt * (op["c_x"][:, None] + op["C_xv"] @ Yvb)
+    Yx1 = Yx + dt * (cx + op["C_xv"] @ Yvb)
     return Yx1, Yv1, Ye1, np.minimum(dt1, dt2)
 
 
@@ -172,9 +173,17 @@ def window_transition(Phi_new, Phi_old, os_new, os_old, Y):
     Phi_w^T (Phi_{w-1} yhat): the offsets are differenced first (lifting and then
     subtracting a large offset would cancel catastrophically for the e field's spike).
     Independent of the factored T, c form (window_transition_ops; hydro_window_ops on the GPU)."""
-    d = os_old - os_new
-    d = d[:, None] if d.ndim == 1 else d
+    o2 = lambda a: a[:, None] if a.ndim == 1 else a   # [rows] -> [rows][1]
+    d = o2(os_old) - o2(os_new)
     return Phi_new.T @ d + Phi_new.T @ (Phi_old @ Y)
+
+
+def previous_window_offset(Phi_prev, os_prev, Y_prev):
+    """The previous-window offset, PAPER Eq. previous_os, as written:
+        os_w = os_{w-1} + Phi_{w-1} yhat_{w-1}(t_{w-1})
+    (the lift of the previous window's final state; per instance, [rows][B])."""
+    os2 = os_prev[:, None] if os_prev.ndim == 1 else os_prev
+    return os2 + Phi_prev @ Y_prev
 
 
 def window_transition_oblique(Phi_new, Phi_old, os_new, os_old, Y, M):
@@ -191,25 +200,34 @@ def window_transition_oblique(Phi_new, Phi_old, os_new, os_old, Y, M):
 
 
 def windowed_advance(windows, Yx, Yv, Ye, t0, dt, beta1=0.85, beta2=1.02, gamma=0.8,
-                     max_iters=10**6):
+                     max_iters=10**6, offsets="fixed"):
     """The time-windowing online phase: for each window, `advance` with its
     own operators up to its end time, then map the reduced coordinates into the next
     window's bases (window_transition, from the two windows' bases and offsets in `op`).
     windows: list of dicts with keys op (the rom_rk2avg_step operators, incl. Phi_x/v/e and
-    x_os/v_os/e_os) and t_end.  Returns (Yx, Yv, Ye, t[B], next_dt[B], per-window
-    (accepted, rejected))."""
+    x_os/v_os/e_os) and t_end.  offsets = "previous": the offsets of window w > 1 are not
+    taken from its op but formed at the transition by Eq. previous_os per
+    instance, with c_x = Phi_x,w^T v_os,w per instance, and the new coordinates
+    by Eq. ic-tw with those offsets (zero up to rounding).  Returns (Yx, Yv, Ye, t[B],
+    next_dt[B], per-window (accepted, rejected))."""
     t = t0
     h = np.array(dt, dtype=np.float64)
     stats = []
     tB = None
+    ops = [dict(w["op"]) for w in windows]
     for wi, w in enumerate(windows):
-        Yx, Yv, Ye, tB, h, ns, nr, _ = advance(w["op"], Yx, Yv, Ye, t, w["t_end"], h, beta1, beta2,
+        Yx, Yv, Ye, tB, h, ns, nr, _ = advance(ops[wi], Yx, Yv, Ye, t, w["t_end"], h, beta1, beta2,
                                                gamma, max_iters)
         stats.append((ns, nr))
         t = w["t_end"]
         nxt = wi + 1
         if nxt < len(windows):
-            o, n = w["op"], windows[nxt]["op"]
+            o, n = ops[wi], ops[nxt]
+            if offsets == "previous":
+                n["x_os"] = previous_window_offset(o["Phi_x"], o["x_os"], Yx)
+                n["v_os"] = previous_window_offset(o["Phi_v"], o["v_os"], Yv)
+                n["e_os"] = previous_window_offset(o["Phi_e"], o["e_os"], Ye)
+                n["c_x"] = n["Phi_x"].T @ n["v_os"]
             Yx = window_transition(n["Phi_x"], o["Phi_x"], n["x_os"], o["x_os"], Yx)
             Yv = window_transition(n["Phi_v"], o["Phi_v"], n["v_os"], o["v_os"], Yv)
             Ye = window_transition(n["Phi_e"], o["Phi_e"], n["e_os"], o["e_os"], Ye)

@@ -1507,6 +1507,7 @@ hydro_status hydro_rom_rk2avg_step(hydro_rom *r, double *Yx, double *Yv, double 
     return cudaGetLastError() == cudaSuccess ? HYDRO_OK : HYDRO_ERR_CUDA;
   };
   const int fx = r->os_flags & 1, fv = (r->os_flags >> 1) & 1, fe = (r->os_flags >> 2) & 1;
+  const int fc = (r->os_flags >> 3) & 1;   // c_x per instance ([nx][B]: previous-window offsets)
 #define RS(call) do { if ((st = (call)) != HYDRO_OK) return st; } while (0)
   // ---- stage 1 at the lifted U~^n
   RS(lift(r->Phi_x, r->x_os, fx, r->rows_h1, r->nx, Yx, r->xS));
@@ -1519,7 +1520,7 @@ hydro_status hydro_rom_rk2avg_step(hydro_rom *r, double *Yx, double *Yv, double 
   RS(hydro_sample_force_transpose(r->p, r->S, r->wS, r->FTr, stream));
   RS(proj(r->R_e, r->ne, r->s_e, r->FTr, r->re, r->wse, r->wse_bytes));
   RS(axpy(r->ne, Ye, 0.5, r->re, r->Ye_h));                                    // ehat^{n+1/2}
-  RS(lift(r->C_xv, r->c_x, 0, r->nx, r->nv, r->Yv_h, r->rx));                  // c_x + C_xv vhat
+  RS(lift(r->C_xv, r->c_x, fc, r->nx, r->nv, r->Yv_h, r->rx));                 // c_x + C_xv vhat
   RS(axpy(r->nx, Yx, 0.5, r->rx, r->Yx_h));                                    // xhat^{n+1/2}
   // ---- stage 2 at U~^{n+1/2} (its velocity is wS)
   RS(lift(r->Phi_x, r->x_os, fx, r->rows_h1, r->nx, r->Yx_h, r->xS));
@@ -1534,7 +1535,7 @@ hydro_status hydro_rom_rk2avg_step(hydro_rom *r, double *Yx, double *Yv, double 
   RS(hydro_sample_force_transpose(r->p, r->S, r->vS, r->FTr, stream));
   RS(proj(r->R_e, r->ne, r->s_e, r->FTr, r->re, r->wse, r->wse_bytes));
   RS(axpy(r->ne, Ye, 1.0, r->re, Ye));                                         // ehat^{n+1}
-  RS(lift(r->C_xv, r->c_x, 0, r->nx, r->nv, r->Yvb, r->rx));
+  RS(lift(r->C_xv, r->c_x, fc, r->nx, r->nv, r->Yvb, r->rx));
   RS(axpy(r->nx, Yx, 1.0, r->rx, Yx));                                         // xhat^{n+1}
   CUDA_OK(cudaMemcpyAsync(Yv, r->Yv1, sizeof(double) * (size_t)r->nv * B, cudaMemcpyDeviceToDevice,
                           (cudaStream_t)stream));
@@ -2323,6 +2324,24 @@ hydro_status hydro_gappy_pinv(const double *U, int64_t N, int m, const int64_t *
   }
   cleanup();
   return st;
+}
+
+hydro_status hydro_rom_window_offset(int64_t rows, int n_prev, int B, const double *Phi_prev,
+                                     const double *os_prev, int os_prev_batched, const double *Y_prev,
+                                     double *os_new, int n_new, double *Y_new, hydro_stream_t stream) {
+  if (rows < 0 || n_prev <= 0 || B <= 0 || n_new < 0 || (n_new > 0 && !Y_new) || !os_new) return HYDRO_ERR_ARG;
+  // Eq. previous_os: os_w = os_{w-1} + Phi_{w-1} yhat_{w-1}(t_{w-1})  (the lift of the final state)
+  hydro_status st = hydro_rom_lift(rows, n_prev, B, Phi_prev, os_prev, os_prev_batched, Y_prev, os_new, stream);
+  if (st != HYDRO_OK) return st;
+  // yhat_w(t_{w-1}) = Phi_w^T (os_{w-1} + Phi_{w-1} yhat_{w-1} - os_w) = 0
+  if (n_new > 0) CUDA_OK(cudaMemsetAsync(Y_new, 0, sizeof(double) * (size_t)n_new * B, (cudaStream_t)stream));
+  return HYDRO_OK;
+}
+
+hydro_status hydro_basis_tproduct(int64_t N, int n, int B, const double *Phi, const double *X, double *out,
+                                  hydro_stream_t stream) {
+  if (N <= 0 || n <= 0 || B <= 0 || n > 1024 || B > 65536 || !Phi || !X || !out) return HYDRO_ERR_ARG;
+  return xprod(N, n, Phi, n, B, X, B, out, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -33,7 +33,7 @@ EXPORTED = ["hydro_ctx_workspace_bytes", "hydro_ctx_create", "hydro_ctx_destroy"
             "hydro_profile_release_captured", "hydro_selftest_ieee_fast",
             "hydro_fom_create", "hydro_fom_destroy", "hydro_mass_v_apply", "hydro_mass_v_solve",
             "hydro_mass_e_solve", "hydro_fom_energy", "hydro_rk2avg_step", "hydro_fom_advance", "hydro_rom_advance", "hydro_rom_create",
-            "hydro_fom_stage_state", "hydro_pod", "hydro_deim", "hydro_qdeim", "hydro_deim_oversampled", "hydro_mass_e_apply", "hydro_window_ops", "hydro_gappy_pinv", "hydro_rom_indicator", "hydro_index_copy_add",
+            "hydro_fom_stage_state", "hydro_pod", "hydro_deim", "hydro_qdeim", "hydro_deim_oversampled", "hydro_mass_e_apply", "hydro_window_ops", "hydro_gappy_pinv", "hydro_rom_window_offset", "hydro_basis_tproduct", "hydro_rom_indicator", "hydro_index_copy_add",
             "hydro_rom_destroy", "hydro_rom_rk2avg_step", "hydro_force_stress_bytes",
             "hydro_force_full_store", "hydro_force_transpose", "hydro_sample_stress_bytes",
             "hydro_force_sampled_store", "hydro_sample_force_transpose"]
@@ -101,6 +101,8 @@ def lib() -> ctypes.CDLL:
         L.hydro_mass_e_apply.argtypes = [vp, vp, vp, vp]
         L.hydro_window_ops.argtypes = [vp, i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
         L.hydro_gappy_pinv.argtypes = [vp, i64, i32, ctypes.POINTER(i64), i64, vp, vp]
+        L.hydro_rom_window_offset.argtypes = [i64, i32, i32, vp, vp, i32, vp, vp, i32, vp, vp]
+        L.hydro_basis_tproduct.argtypes = [i64, i32, i32, vp, vp, vp, vp]
         L.hydro_index_copy_add.argtypes = [i64, i32, vp, i64, vp, vp, i64, vp, i32, vp]
         L.hydro_rom_indicator.argtypes = [vp, vp, vp, vp, vp, _Visc, _Cfl, i32, vp, i32, vp, i32, vp, i32,
                                           ctypes.POINTER(i64), i32, vp, i32, ctypes.POINTER(i64),
@@ -482,6 +484,44 @@ def offline_projectors(Phi_x: torch.Tensor, Phi_v: torch.Tensor, Phi_e: torch.Te
     return P_v, P_e, C_xv, c_x.reshape(-1).contiguous()
 
 
+def rom_window_offset(Phi_prev: torch.Tensor, os_prev: torch.Tensor, Y_prev: torch.Tensor,
+                      n_new: int = 0, stream=None):
+    """Eq. previous_os: os_w = os_{w-1} + Phi_{w-1} Y_{w-1} ([rows][B]) and the new
+    window's zero initial coordinates ([n_new][B]) -- hydro_rom_window_offset."""
+    rows, n = Phi_prev.shape
+    B = Y_prev.shape[1]
+    os_new = torch.empty((rows, B), dtype=torch.float64, device=Phi_prev.device)
+    Y_new = torch.empty((n_new, B), dtype=torch.float64, device=Phi_prev.device) if n_new > 0 else None
+    _check(lib().hydro_rom_window_offset(rows, n, B, _ptr(Phi_prev), _ptr(os_prev), 1 if os_prev.dim() == 2 else 0,
+                                         _ptr(Y_prev.contiguous()), _ptr(os_new), n_new, _ptr(Y_new),
+                                         _stream(stream)), "hydro_rom_window_offset")
+    return os_new, Y_new
+
+
+def basis_tproduct(Phi: torch.Tensor, X: torch.Tensor, stream=None) -> torch.Tensor:
+    """Phi^T X ([n][B], device) -- hydro_basis_tproduct (deterministic split-K)."""
+    N, n = Phi.shape
+    X2 = X.reshape(N, -1).contiguous()
+    out = torch.empty((n, X2.shape[1]), dtype=torch.float64, device=Phi.device)
+    _check(lib().hydro_basis_tproduct(N, n, X2.shape[1], _ptr(Phi.contiguous()), _ptr(X2), _ptr(out),
+                                      _stream(stream)), "hydro_basis_tproduct")
+    return out
+
+
+def rom_previous_window(Phi_prev, os_prev, Y_prev, Phi_new, Phi_x_new, stream=None):
+    """The previous-window offsets of one transition for all three fields:
+    Phi_prev / os_prev / Y_prev / Phi_new: (x, v, e) tuples of the old window's bases, offsets and
+    final coordinates and the new window's bases.  Returns (x_os, v_os, e_os) [rows][B], the new
+    window's zero coordinates (Yx, Yv, Ye) and its per-instance c_x = Phi_x,w^T v_os,w [nx][B]."""
+    outs, Ys = [], []
+    for P0, o0, Y0, P1 in zip(Phi_prev, os_prev, Y_prev, Phi_new):
+        o1, Y1 = rom_window_offset(P0, o0, Y0, n_new=P1.shape[1], stream=stream)
+        outs.append(o1)
+        Ys.append(Y1)
+    c_x = basis_tproduct(Phi_x_new, outs[1], stream=stream)
+    return tuple(outs), tuple(Ys), c_x
+
+
 def rom_windowed_advance(windows, Yx, Yv, Ye, gamma, visc: Visc, cfl: Cfl, t0: float, dt,
                          ctrl: DtCtrl = DtCtrl(), max_iters=1000000, stream=None):
     """The time-windowing online phase: for each window advance with its own
@@ -502,6 +542,37 @@ def rom_windowed_advance(windows, Yx, Yv, Ye, gamma, visc: Visc, cfl: Cfl, t0: f
             Yv = rom_window_transition(Tv, cv, Yv, stream=stream)
             Ye = rom_window_transition(Te, ce, Ye, stream=stream)
     return Yx, Yv, Ye, tB, h, stats
+
+
+def rom_windowed_advance_previous(plan, windows, x_os, v_os, e_os, c_x, Yx, Yv, Ye, gamma,
+                                  visc: Visc, cfl: Cfl, t0: float, dt, ctrl: DtCtrl = DtCtrl(),
+                                  max_iters=1000000, stream=None):
+    """Time windows with previous-window offsets: window 1 runs with the given
+    offsets and c_x; at each transition the offsets of window w are the lifts of window w-1's
+    final state (rom_previous_window: hydro_rom_window_offset per field, c_x by
+    hydro_basis_tproduct), the coordinates restart at 0, and a new RomStepper is made with
+    the window's bases and operators.  windows: list of dicts with keys Phi_x, Phi_v, Phi_e,
+    R_v, R_e, C_xv (device) and t_end.  Returns (Yx, Yv, Ye, t[B], next_dt[B], per-window
+    (accepted, rejected), per-transition milliseconds (CUDA events))."""
+    t, h, stats, tB, trans_ms = t0, list(dt), [], None, []
+    os_ = (x_os, v_os, e_os)
+    cx = c_x
+    for wi, w in enumerate(windows):
+        st = RomStepper(plan, w["Phi_x"], w["Phi_v"], w["Phi_e"], *os_, w["R_v"], w["R_e"], w["C_xv"], cx)
+        tB, h, ns, nr, _ = st.advance(Yx, Yv, Ye, gamma, visc, cfl, t, w["t_end"], h, ctrl, max_iters, stream)
+        stats.append((ns, nr))
+        t = w["t_end"]
+        if wi + 1 < len(windows):
+            nw = windows[wi + 1]
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            os_, (Yx, Yv, Ye), cx = rom_previous_window(
+                (w["Phi_x"], w["Phi_v"], w["Phi_e"]), os_, (Yx, Yv, Ye),
+                (nw["Phi_x"], nw["Phi_v"], nw["Phi_e"]), nw["Phi_x"], stream=stream)
+            b.record()
+            torch.cuda.synchronize()
+            trans_ms.append(a.elapsed_time(b))
+    return Yx, Yv, Ye, tB, h, stats, trans_ms
 
 
 def pod(S: torch.Tensor, eps: float = 0.9999, max_k: Optional[int] = None, stream=None):
@@ -664,7 +735,8 @@ class RomStepper:
     def __init__(self, plan: SamplePlan, Phi_x, Phi_v, Phi_e, x_os, v_os, e_os, R_v, R_e, C_xv, c_x):
         self._keep = [t.contiguous() for t in (Phi_x, Phi_v, Phi_e, x_os, v_os, e_os, R_v, R_e, C_xv, c_x)]
         Phi_x, Phi_v, Phi_e, x_os, v_os, e_os, R_v, R_e, C_xv, c_x = self._keep
-        flags = (1 if x_os.dim() == 2 else 0) | (2 if v_os.dim() == 2 else 0) | (4 if e_os.dim() == 2 else 0)
+        flags = ((1 if x_os.dim() == 2 else 0) | (2 if v_os.dim() == 2 else 0) | (4 if e_os.dim() == 2 else 0)
+                 | (8 if c_x.dim() == 2 else 0))
         h = ctypes.c_void_p()
         _check(lib().hydro_rom_create(plan._h, Phi_x.shape[1], Phi_v.shape[1], Phi_e.shape[1], _ptr(Phi_x),
                                       _ptr(Phi_v), _ptr(Phi_e), _ptr(x_os), _ptr(v_os), _ptr(e_os), flags,

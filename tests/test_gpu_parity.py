@@ -132,3 +132,17 @@ def test_full_size_3d_sampled_outputs(oracle_lib, name):
                    f"{name} FTw sampled")
     dref = oracle_lib.force(prob, mode=1)
     assert H.dt_bitwise(got["dt"], dref["dt"]), (got["dt"], dref["dt"])
+
+
+@pytest.mark.slow
+def test_full_size_c2_every_output(oracle_lib):
+    """C2 at its BASELINE.json size in the bench's launch configuration: every assembled F.1
+    entry (all 2,146,689 nodes x 3) and every F^T.v entry against the oracle's full-mesh
+    evaluation, dt bit-exact."""
+    prob = W.config("c2")
+    got = H.run_full(prob)
+    ref = oracle_lib.force(prob)
+    assert got["status"] == 0 and ref["status"] == 0
+    H.assert_close(got["F1"], ref["F1"], ref["F1mag"], H.TOL_ASSEMBLED, "c2 F1 (all nodes)")
+    H.assert_close(got["FTw"], ref["FTw"], ref["FTwmag"], H.TOL_LOCAL, "c2 FTw (all elements)")
+    assert H.dt_bitwise(got["dt"], ref["dt"]), (got["dt"], ref["dt"])

@@ -109,7 +109,7 @@ def test_rom_batched_equals_single_and_full():
 
 
 @pytest.mark.slow
-def test_rom_full_size_c4_sampled_instances(oracle_lib):
+def test_rom_full_size_c4_sampled_instances(oracle_lib):  # rows of two instances; all dt below
     """C4 at its BASELINE size (64 instances, 2 % sample of the 64^3 mesh): two
     instances checked row by row against the oracle; all 64 dt values bit-exact for
     those instances."""
@@ -121,3 +121,44 @@ def test_rom_full_size_c4_sampled_instances(oracle_lib):
         H.assert_close(g["F1"][:, b], F1, F1m, H.TOL_LOCAL, f"F1_rows b={b}")
         H.assert_close(g["FT"][:, b], FT, FTm, H.TOL_LOCAL, f"FTw_rows b={b}")
         assert H.dt_bitwise(g["dt"][b], dt)
+
+
+@pytest.mark.slow
+def test_rom_full_size_c4_all_dt_projection_lift(oracle_lib):
+    """C4 at its BASELINE size: (a) dt of all 64 instances bit-exact against an oracle dt-only
+    pass per instance over the closure (the GPU's lifted state as input); (b) the projection of
+    the full sampled rows (s_v = 409 866, s_e = 41 944) against the oracle's naive loops with
+    the same offline operators (Eq. sol-ls-hyper); (c) the lift on 20 000 seeded
+    closure rows of each field against the oracle's naive lift; (d) the GPU-formed
+    offline operators against the oracle's (hydro_gappy_pinv vs numpy pinv)."""
+    from oracle import rom as orom
+    batch = W.c4()
+    g = gpu_step(batch)
+    assert g["status"][0] == 0
+    base, m = batch.base, batch.base.mesh
+    d, ncl, ne = m.dim, batch.closure_nodes.size, m.ne
+    for b in range(batch.B):
+        x = m.x0.copy()
+        x[:, batch.closure_nodes] = g["xS"][:, b].reshape(d, ncl)
+        v = np.zeros_like(m.x0)
+        v[:, batch.closure_nodes] = g["vS"][:, b].reshape(d, ncl)
+        e = base.e.copy()
+        e[batch.closure_elems] = g["eS"][:, b].reshape(-1, ne)
+        r = oracle_lib.force(base, elist=batch.closure_elems, x=x, v=v, e=e, mode=1)
+        assert r["status"] == 0
+        assert H.dt_bitwise(g["dt"][b], r["dt"]), (b, g["dt"][b], r["dt"])
+    P_v, P_e, C_xv, c_x = orom.offline_projectors(batch)
+    rv = hydro.rom_project(H.dev(P_v), g["F1_t"]).cpu().numpy()
+    re_ = hydro.rom_project(H.dev(P_e), g["FT_t"]).cpu().numpy()
+    H.assert_close(rv, oracle_lib.project(P_v, g["F1"]), np.abs(P_v) @ np.abs(g["F1"]), 1e-13, "r_v full")
+    H.assert_close(re_, oracle_lib.project(P_e, g["FT"]), np.abs(P_e) @ np.abs(g["FT"]), 1e-13, "r_e full")
+    rng = np.random.default_rng(2104)
+    for key, Phi, os_, Y in (("xS", batch.Phi_x, batch.x_os, batch.Yx), ("vS", batch.Phi_v, batch.v_os, batch.Yv),
+                             ("eS", batch.Phi_e, batch.e_os, batch.Ye)):
+        rows = np.sort(rng.choice(Phi.shape[0], 20_000, replace=False))
+        ref = oracle_lib.lift(np.ascontiguousarray(Phi[rows]), np.ascontiguousarray(os_[rows]), Y)
+        mag = np.abs(os_[rows] if os_.ndim == 2 else os_[rows][:, None]) + np.abs(Phi[rows]) @ np.abs(Y)
+        H.assert_close(g[key][rows], ref, mag, 1e-14, f"lift {key} (full size, sampled rows)")
+    got = [t.cpu().numpy() for t in H.gpu_offline_ops(batch)]
+    for gg, w, what in zip(got, (P_v, P_e, C_xv, c_x), ("P_v", "P_e", "C_xv", "c_x")):
+        assert np.abs(gg - w).max() <= 1e-11 * np.abs(w).max(), what

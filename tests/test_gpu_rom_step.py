@@ -169,3 +169,61 @@ def test_rom_windowed_advance_matches_oracle():
     for gt, want, what in zip(got[:3], ref[:3], ("xhat", "vhat", "ehat")):
         g_ = gt.cpu().numpy()
         assert np.abs(g_ - want).max() <= 1e-10 * np.abs(want).max(), what
+
+
+def test_rom_windowed_advance_previous_offsets_matches_oracle():
+    """Time windows with previous-window offsets (Eq. previous_os): window 2's
+    offsets are the per-instance lifts of window 1's final state (hydro_rom_window_offset), its
+    coordinates restart at 0 and c_x = Phi_x^T v_os per instance (hydro_basis_tproduct) --
+    against oracle/rom.windowed_advance(offsets="previous"): per-window step counts and times,
+    final coordinates within 1e-10 of their scale; the offsets themselves against the
+    oracle's lift of the GPU's window-1 state; the transition's cost recorded."""
+    b1 = W.c4(n_sample=6, B=3, small_mesh=True)
+    b2 = W.next_window(b1)
+    base = b1.base
+    ctx = H.context(base)
+    plan = hydro.SamplePlan(ctx, b1.sample_elems, b1.B)
+    g = H.dev(base.gamma)
+    visc, cfl = hydro.Visc(base.q1, base.q2, base.visc), hydro.Cfl(base.alpha, base.alpha_mu)
+
+    def op_of(b):
+        P_v, P_e, C_xv, c_x = orom.offline_projectors(b)
+        return dict(base=base, closure_elems=b.closure_elems, closure_nodes=b.closure_nodes,
+                    s0_nodes=b.s0_nodes, sample_elems=b.sample_elems, Phi_x=b.Phi_x, Phi_v=b.Phi_v,
+                    Phi_e=b.Phi_e, x_os=b.x_os, v_os=b.v_os, e_os=b.e_os, R_v=P_v, R_e=P_e,
+                    C_xv=C_xv, c_x=c_x)
+
+    def win_of(b, t_end):
+        P_v, P_e, C_xv, _ = H.gpu_offline_ops(b)
+        return dict(Phi_x=H.dev(b.Phi_x), Phi_v=H.dev(b.Phi_v), Phi_e=H.dev(b.Phi_e), R_v=P_v, R_e=P_e,
+                    C_xv=C_xv, t_end=t_end)
+    op1, op2 = op_of(b1), op_of(b2)
+    _, _, _, est0 = orom.rom_rk2avg_step(op1, b1.Yx, b1.Yv, b1.Ye, np.zeros(b1.B))
+    dt0 = 0.7 * est0
+    t1, t2 = 2.0 * float(est0.max()), 4.0 * float(est0.max())
+    ref = orom.windowed_advance([dict(op=op1, t_end=t1), dict(op=op2, t_end=t2)], b1.Yx.copy(),
+                                b1.Yv.copy(), b1.Ye.copy(), 0.0, dt0, max_iters=20, offsets="previous")
+    cx0 = H.gpu_offline_ops(b1)[3]
+    got = hydro.rom_windowed_advance_previous(
+        plan, [win_of(b1, t1), win_of(b2, t2)], H.dev(b1.x_os), H.dev(b1.v_os), H.dev(b1.e_os), cx0,
+        H.dev(b1.Yx), H.dev(b1.Yv), H.dev(b1.Ye), g, visc, cfl, 0.0, dt0, max_iters=20)
+    assert plan.status_sync()[0] == 0
+    for (nsg, nrg), (nsr, nrr) in zip(got[5], ref[5]):
+        assert list(nsg) == list(nsr) and list(nrg) == list(nrr)
+    np.testing.assert_allclose(got[3], ref[3], rtol=1e-12)
+    for gt, want, what in zip(got[:3], ref[:3], ("xhat", "vhat", "ehat")):
+        g_ = gt.cpu().numpy()
+        assert np.abs(g_ - want).max() <= 1e-10 * max(np.abs(want).max(), 1e-30), what
+    assert len(got[6]) == 1 and got[6][0] > 0
+    # the transition on its own: offsets = the lift of the final state, coordinates 0
+    Y = [H.dev(a) for a in (b1.Yx, b1.Yv, b1.Ye)]
+    os_new, Y0, cx = hydro.rom_previous_window(
+        (H.dev(b1.Phi_x), H.dev(b1.Phi_v), H.dev(b1.Phi_e)), (H.dev(b1.x_os), H.dev(b1.v_os), H.dev(b1.e_os)),
+        Y, (H.dev(b2.Phi_x), H.dev(b2.Phi_v), H.dev(b2.Phi_e)), H.dev(b2.Phi_x))
+    for o, P, os_, Yh in zip(os_new, (b1.Phi_x, b1.Phi_v, b1.Phi_e), (b1.x_os, b1.v_os, b1.e_os),
+                             (b1.Yx, b1.Yv, b1.Ye)):
+        want = orom.previous_window_offset(P, os_, Yh)
+        assert np.abs(o.cpu().numpy() - want).max() <= 1e-14 * np.abs(want).max()
+    assert all(float(y.abs().max()) == 0.0 for y in Y0)
+    cx_want = b2.Phi_x.T @ os_new[1].cpu().numpy()
+    assert np.abs(cx.cpu().numpy() - cx_want).max() <= 1e-12 * max(np.abs(cx_want).max(), 1e-30)

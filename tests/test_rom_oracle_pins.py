@@ -209,3 +209,62 @@ def test_P38_indicator_with_sns_basis_is_the_distance_to_its_span():
     # DEIM sampling (n rows) of an SNS basis still reproduces anything in its span exactly
     from oracle import offline
     assert rom.indicator_term(g, Phi, M, U, offline.deim(U)) <= 1e-11 * np.linalg.norm(g)
+
+
+def test_P42_previous_window_offset_starts_at_zero():
+    """Eq. previous_os (P:1372-1399): with os_w = os_{w-1} + Phi_{w-1} yhat_{w-1}, Eq. ic-tw
+    gives yhat_w = 0 (to rounding) for any next-window basis, and the new window's lifted
+    state os_w + Phi_w 0 is the previous window's final lift -- "the best approximation of the
+    final state in the previous window in the solution subspace of the current window"."""
+    from oracle import rom
+    rng = np.random.default_rng(42)
+    Q1 = _orth(rng, 60, 7)
+    Q2 = _orth(rng, 60, 9)                       # unrelated next-window basis
+    os1 = rng.standard_normal((60, 4))
+    Y1 = rng.standard_normal((7, 4))
+    os2 = rom.previous_window_offset(Q1, os1, Y1)
+    np.testing.assert_allclose(os2, os1 + Q1 @ Y1, rtol=0, atol=1e-14)
+    Y2 = rom.window_transition(Q2, Q1, os2, os1, Y1)
+    assert np.abs(Y2).max() <= 1e-14 * np.abs(os2).max()
+    np.testing.assert_allclose(rom.lift(Q2, os2, np.zeros((9, 4))), rom.lift(Q1, os1, Y1), atol=1e-14)
+    # a shared (1-D) offset becomes per instance
+    os2b = rom.previous_window_offset(Q1, os1[:, 0], Y1)
+    np.testing.assert_allclose(os2b, os1[:, :1] + Q1 @ Y1, atol=1e-14)
+
+
+def _small_rom_op(batch):
+    from oracle import rom
+    P_v, P_e, C_xv, c_x = rom.offline_projectors(batch)
+    return dict(base=batch.base, closure_elems=batch.closure_elems, closure_nodes=batch.closure_nodes,
+                s0_nodes=batch.s0_nodes, sample_elems=batch.sample_elems, Phi_x=batch.Phi_x,
+                Phi_v=batch.Phi_v, Phi_e=batch.Phi_e, x_os=batch.x_os, v_os=batch.v_os,
+                e_os=batch.e_os, R_v=P_v, R_e=P_e, C_xv=C_xv, c_x=c_x)
+
+
+def test_P43_previous_window_offsets_with_equal_bases_continue_the_trajectory(oracle_lib):
+    """Two windows with the same bases and previous-window offsets: window 2 restarts from
+    yhat = 0 about os_2 = os_1 + Phi yhat(t1), with c_x,2 = Phi_x^T v_os,2 = c_x + C_xv vhat(t1),
+    so its reduced dynamics are those of window 1 shifted by a constant and the lifted
+    trajectory continues unchanged: the final lifted state equals that of the same bases run
+    without a transition (stopped and restarted at t1, the same controller sequence), to
+    rounding; step counts agree."""
+    from oracle import rom
+    batch = W.c4(n_sample=6, B=2, small_mesh=True)
+    op = _small_rom_op(batch)
+    _, _, _, est0 = rom.rom_rk2avg_step(op, batch.Yx, batch.Yv, batch.Ye, np.zeros(batch.B))
+    dt0 = 0.5 * est0
+    t1, t2 = 1.5 * float(est0.max()), 3.0 * float(est0.max())
+    # reference: one window, stopped and restarted at t1
+    Yx, Yv, Ye, _, h, ns1, nr1, _ = rom.advance(op, batch.Yx, batch.Yv, batch.Ye, 0.0, t1, dt0)
+    Yx, Yv, Ye, tr, _, ns2, nr2, _ = rom.advance(op, Yx, Yv, Ye, t1, t2, h)
+    ref = [rom.lift(op[f"Phi_{f}"], op[f"{f}_os"], Y) for f, Y in zip("xve", (Yx, Yv, Ye))]
+    got = rom.windowed_advance([dict(op=op, t_end=t1), dict(op=op, t_end=t2)], batch.Yx, batch.Yv,
+                               batch.Ye, 0.0, dt0, offsets="previous")
+    # window 2's offsets, as windowed_advance formed them
+    Yx1, Yv1, Ye1, *_ = rom.advance(op, batch.Yx, batch.Yv, batch.Ye, 0.0, t1, dt0)
+    os2 = [rom.previous_window_offset(op[f"Phi_{f}"], op[f"{f}_os"], Y) for f, Y in zip("xve", (Yx1, Yv1, Ye1))]
+    lifted = [rom.lift(op[f"Phi_{f}"], o, Y) for f, o, Y in zip("xve", os2, got[:3])]
+    for a, b, what in zip(lifted, ref, ("x", "v", "e")):
+        assert np.abs(a - b).max() <= 1e-10 * np.abs(b).max(), what
+    np.testing.assert_allclose(got[3], tr, rtol=1e-14)
+    assert [list(x) for x in got[5][1]] == [list(ns2), list(nr2)]
