@@ -395,12 +395,65 @@ def bench_one(name, args, dev, flush, rank, world):
     else:
         out["e2e"] = e2e_rom(step_inputs=(Yx, Yv, Ye), step_outputs=(rv, re_, rx, dt), step=step,
                              n_qp=n_qp, args=args)
+        out["components"] = c4_components(b, plan, Phi_x, Phi_v, Phi_e, x_os, v_os, e_os, Yx, Yv, Ye,
+                                          xS, vS, eS, F1r, FTr, Pv, Pe, Cxv, cx, rv, re_, rx, wsv, wse,
+                                          flush, args)
         out["rom_rk2avg_step"] = bench_rom_step(plan, b, Phi_x, Phi_v, Phi_e, x_os, v_os, e_os,
                                                 Pv, Pe, Cxv, cx, Yx, Yv, Ye, gamma, visc, cfl, n_qp,
                                                 args, flush)
     # roofline of the dominant kernel (force kernel)
     out["roofline"] = roofline(name, base, m, n_units, kern_avg, prob, step_ms=ms)
     return out, prob
+
+
+def c4_components(b, plan, Phi_x, Phi_v, Phi_e, x_os, v_os, e_os, Yx, Yv, Ye, xS, vS, eS, F1r, FTr,
+                  Pv, Pe, Cxv, cx, rv, re_, rx, wsv, wse, flush, args):
+    """The C4 step's GEMM-shaped pieces timed on their own (CUDA events, L2 flushed before
+    each, median of K): the three lifts S7 and the two projections S9,
+    each against its own roofline max(algorithmic bytes / HBM, flops / FP64 peak)."""
+    import torch
+    from paper_2104_11404_b200 import hydro
+    hbm = measured_peaks().get("hbm_gbs", 6650.0) * 1e9
+    fp64 = FP64_PEAK_TFLOPS * 1e12
+    nred, B = Phi_x.shape[1], b.B
+
+    def timed(fn):
+        ts = []
+        for i in range(max(4, args.steps // 2)):
+            flush.zero_()
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            e.record()
+            torch.cuda.synchronize()
+            if i > 0:
+                ts.append(a.elapsed_time(e))
+        return float(np.median(ts))
+
+    def lift_model(rows, os_cols):
+        byts = 8.0 * (rows * nred + rows * os_cols + rows * B)      # Phi, offset, out
+        return byts, 2.0 * rows * nred * B
+
+    def proj_model(s_rows, n):
+        return 8.0 * (n * s_rows + s_rows * B + n * B), 2.0 * n * s_rows * B
+
+    out = {}
+    items = [("lift_x", lambda: hydro.rom_lift(Phi_x, x_os, Yx, out=xS), lift_model(Phi_x.shape[0], 1)),
+             ("lift_v", lambda: hydro.rom_lift(Phi_v, v_os, Yv, out=vS), lift_model(Phi_v.shape[0], 1)),
+             ("lift_e", lambda: hydro.rom_lift(Phi_e, e_os, Ye, out=eS), lift_model(Phi_e.shape[0], B)),
+             ("project_v", lambda: hydro.rom_project(Pv, F1r, out=rv, workspace=wsv), proj_model(plan.s_v, Pv.shape[0])),
+             ("project_e", lambda: hydro.rom_project(Pe, FTr, out=re_, workspace=wse), proj_model(plan.s_e, Pe.shape[0]))]
+    for name, fn, (byts, flops) in items:
+        ms = timed(fn)
+        floor = max(byts / hbm, flops / fp64) * 1e3
+        out[name] = {"ms": round(ms, 5), "alg_bytes": byts, "alg_flops": flops,
+                     "floor_ms": round(floor, 5), "frac": round(floor / ms, 4),
+                     "bound": "hbm" if byts / hbm >= flops / fp64 else "fp64"}
+    lifts = sum(out[k]["ms"] for k in ("lift_x", "lift_v", "lift_e"))
+    projs = sum(out[k]["ms"] for k in ("project_v", "project_e"))
+    out["lifts_ms"], out["projections_ms"] = round(lifts, 4), round(projs, 4)
+    out["kernels"] = "lift_mma_kernel (DMMA m8n8k4), project_mma_kernel + project_mma_reduce_kernel"
+    return out
 
 
 def max_over_ranks(value, dev, world):
@@ -1005,6 +1058,7 @@ def main():
             "e2e": head.get("e2e"), "gpu_launches": head["gpu_launches"],
             "roofline": head["roofline"], "clocks": head["clocks"],
             "force_kernel_ms": head["force_kernel_ms"], "force_kernel_share": head["force_kernel_share"],
+            **{k: head[k] for k in ("components", "rom_rk2avg_step") if k in head},
             "per_config": {k: {kk: vv for kk, vv in r.items() if kk not in ("clocks",)}
                            for k, r in res.items() if k != args.workload},
         }

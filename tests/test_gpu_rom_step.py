@@ -211,9 +211,15 @@ def test_rom_windowed_advance_previous_offsets_matches_oracle():
     for (nsg, nrg), (nsr, nrr) in zip(got[5], ref[5]):
         assert list(nsg) == list(nsr) and list(nrg) == list(nrr)
     np.testing.assert_allclose(got[3], ref[3], rtol=1e-12)
-    for gt, want, what in zip(got[:3], ref[:3], ("xhat", "vhat", "ehat")):
-        g_ = gt.cpu().numpy()
-        assert np.abs(g_ - want).max() <= 1e-10 * max(np.abs(want).max(), 1e-30), what
+    # window 2's coordinates restart at 0 (the oracle's Eq. ic-tw gives rounding noise there),
+    # so compare the lifted states of window 2, os_2 + Phi_2 yhat, relative to each field
+    Y1 = orom.windowed_advance([dict(op=op1, t_end=t1)], b1.Yx.copy(), b1.Yv.copy(), b1.Ye.copy(),
+                               0.0, dt0, max_iters=20)
+    for f, gt, want, Yf in zip("xve", got[:3], ref[:3], Y1[:3]):
+        os2 = orom.previous_window_offset(op1[f"Phi_{f}"], op1[f"{f}_os"], Yf)
+        a = orom.lift(op2[f"Phi_{f}"], os2, gt.cpu().numpy())
+        b_ = orom.lift(op2[f"Phi_{f}"], os2, want)
+        assert np.abs(a - b_).max() <= 1e-10 * np.abs(b_).max(), f
     assert len(got[6]) == 1 and got[6][0] > 0
     # the transition on its own: offsets = the lift of the final state, coordinates 0
     Y = [H.dev(a) for a in (b1.Yx, b1.Yv, b1.Ye)]
