@@ -719,6 +719,65 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
 #ifndef F3_COMPACT_Q3
 #define F3_COMPACT_Q3 0
 #endif
+// Task splits of the 3D contraction stages (r02): a stage's pencils are split into SPLIT parts
+// along one output index so that more of the CTA's threads work per round.  Each part reloads
+// its pencil's inputs; every output keeps its FMA chain (the forward ones: DESIGN A.2).  Parts
+// occupy contiguous task ranges (warp-uniform except at a range boundary) and each part's body
+// is compiled with its table indices as constants (constant-bank operands, no LDC).
+// forward stage 1 (q1 ranges), stage 2 (q2 ranges); backward b1 (per dl), b2 (per a2 range),
+// b3 (per a1 range).  Q2 (64-thread) / Q3 (224-thread) defaults; -D overrides for A/B builds.
+#ifndef SPLIT_F1_K2
+#define SPLIT_F1_K2 1
+#endif
+#ifndef SPLIT_F2_K2
+#define SPLIT_F2_K2 1
+#endif
+#ifndef SPLIT_B1_K2
+#define SPLIT_B1_K2 1
+#endif
+#ifndef SPLIT_B2_K2
+#define SPLIT_B2_K2 1
+#endif
+#ifndef SPLIT_B3_K2
+#define SPLIT_B3_K2 1
+#endif
+#ifndef SPLIT_F1_K3
+#define SPLIT_F1_K3 1
+#endif
+#ifndef SPLIT_F2_K3
+#define SPLIT_F2_K3 1
+#endif
+#ifndef SPLIT_B1_K3
+#define SPLIT_B1_K3 1
+#endif
+#ifndef SPLIT_B2_K3
+#define SPLIT_B2_K3 1
+#endif
+#ifndef SPLIT_B3_K3
+#define SPLIT_B3_K3 1
+#endif
+template <int K>
+struct Split {
+  static constexpr int F1 = K == 2 ? SPLIT_F1_K2 : SPLIT_F1_K3;   // divides Q
+  static constexpr int F2 = K == 2 ? SPLIT_F2_K2 : SPLIT_F2_K3;   // divides Q
+  static constexpr int B1 = K == 2 ? SPLIT_B1_K2 : SPLIT_B1_K3;   // 1 or 3
+  static constexpr int B2 = K == 2 ? SPLIT_B2_K2 : SPLIT_B2_K3;   // divides N
+  static constexpr int B3 = K == 2 ? SPLIT_B3_K2 : SPLIT_B3_K3;   // divides N
+};
+template <int V>
+struct IC {
+  static constexpr int value = V;
+};
+// body(IC<part>{}) for the runtime part in [0, S): one compiled copy per part
+template <int S, int P = 0, class F>
+__device__ __forceinline__ void part_dispatch(int part, F &&body) {
+  if constexpr (P + 1 >= S) {
+    body(IC<P>{});
+  } else {
+    if (part == P) body(IC<P>{});
+    else part_dispatch<S, P + 1>(part, body);
+  }
+}
 
 // ----------------------------------------------------------------------------- tables
 // The 1D tables in __constant__ memory (filled at context creation, packed order w, B, G, Bl):
@@ -900,8 +959,11 @@ force_kernel(const Params P) {
     if (u < EPB) {
       // stage 1: contract a1.  One task per (field comp, a2, a3) line: its N dofs are loaded
       // once and give all Q x {B, G} outputs (canonical FMA order per output, DESIGN A.2).
-      for (int t = lt; t < NF * DIM * N * N; t += NQ) {
-        const int a23 = t % (N * N), fc = t / (N * N);
+      constexpr int SP1 = Split<K>::F1, QP1 = Q / SP1, T1 = NF * DIM * N * N;
+      static_assert(Q % SP1 == 0, "SPLIT_F1 must divide Q");
+      for (int t = lt; t < T1 * SP1; t += NQ) {
+        const int t1 = t % T1;
+        const int a23 = t1 % (N * N), fc = t1 / (N * N);
         const int a2 = a23 % N, a3 = a23 / N;
         const double *src = Xs + fc * ND + (a3 * N + a2) * N;
         double x[N];
@@ -909,17 +971,21 @@ force_kernel(const Params P) {
         for (int a1 = 0; a1 < N; ++a1) x[a1] = src[a1];
         double *dB = S1b + ((fc * 2 + 0) * Q) * N * N + a2 * N + a3;
         double *dG = S1b + ((fc * 2 + 1) * Q) * N * N + a2 * N + a3;
+        part_dispatch<SP1>(t / T1, [&](auto pc) {
+          constexpr int part = decltype(pc)::value;
 #pragma unroll
-        for (int q1 = 0; q1 < Q; ++q1) {
-          double ab = CT::B(q1, 0) * x[0], ag = CT::G(q1, 0) * x[0];
+          for (int qq = 0; qq < QP1; ++qq) {
+            const int q1 = part * QP1 + qq;
+            double ab = CT::B(q1, 0) * x[0], ag = CT::G(q1, 0) * x[0];
 #pragma unroll
-          for (int a1 = 1; a1 < N; ++a1) {
-            ab = __fma_rn(CT::B(q1, a1), x[a1], ab);
-            ag = __fma_rn(CT::G(q1, a1), x[a1], ag);
+            for (int a1 = 1; a1 < N; ++a1) {
+              ab = __fma_rn(CT::B(q1, a1), x[a1], ab);
+              ag = __fma_rn(CT::G(q1, a1), x[a1], ag);
+            }
+            dB[q1 * N * N] = ab;
+            dG[q1 * N * N] = ag;
           }
-          dB[q1 * N * N] = ab;
-          dG[q1 * N * N] = ag;
-        }
+        });
       }
       if (WANT_E) {  // (j2, j3) lines, on the highest lanes
         for (int t = NQ - 1 - lt; t < M * M; t += NQ) {
@@ -942,8 +1008,11 @@ force_kernel(const Params P) {
     if (u < EPB) {
       // stage 2: contract a2 ; kind 0: B.UG (d/dxi1), 1: G.UB (d/dxi2), 2: B.UB (d/dxi3).
       // One task per (field comp, q1, a3): its 2N stage-1 values give all Q x 3 outputs.
-      for (int t = lt; t < NF * DIM * Q * N; t += NQ) {
-        const int a3 = t % N, r = t / N;
+      constexpr int SP2 = Split<K>::F2, QP2 = Q / SP2, T2 = NF * DIM * Q * N;
+      static_assert(Q % SP2 == 0, "SPLIT_F2 must divide Q");
+      for (int t = lt; t < T2 * SP2; t += NQ) {
+        const int t2 = t % T2;
+        const int a3 = t2 % N, r = t2 / N;
         const int q1 = r % Q, fc = r / Q;
         const double *pB = S1b + ((fc * 2 + 0) * Q + q1) * N * N + a3;
         const double *pG = S1b + ((fc * 2 + 1) * Q + q1) * N * N + a3;
@@ -951,19 +1020,23 @@ force_kernel(const Params P) {
 #pragma unroll
         for (int a2 = 0; a2 < N; ++a2) { uB[a2] = pB[a2 * N]; uG[a2] = pG[a2 * N]; }
         double *dst = S2b + ((fc * 3) * Q + q1) * Q * N + a3;
+        part_dispatch<SP2>(t / T2, [&](auto pc) {
+          constexpr int part = decltype(pc)::value;
 #pragma unroll
-        for (int q2 = 0; q2 < Q; ++q2) {
-          double d1 = CT::B(q2, 0) * uG[0], d2 = CT::G(q2, 0) * uB[0], d3 = CT::B(q2, 0) * uB[0];
+          for (int qq = 0; qq < QP2; ++qq) {
+            const int q2 = part * QP2 + qq;
+            double d1 = CT::B(q2, 0) * uG[0], d2 = CT::G(q2, 0) * uB[0], d3 = CT::B(q2, 0) * uB[0];
 #pragma unroll
-          for (int a2 = 1; a2 < N; ++a2) {
-            d1 = __fma_rn(CT::B(q2, a2), uG[a2], d1);
-            d2 = __fma_rn(CT::G(q2, a2), uB[a2], d2);
-            d3 = __fma_rn(CT::B(q2, a2), uB[a2], d3);
+            for (int a2 = 1; a2 < N; ++a2) {
+              d1 = __fma_rn(CT::B(q2, a2), uG[a2], d1);
+              d2 = __fma_rn(CT::G(q2, a2), uB[a2], d2);
+              d3 = __fma_rn(CT::B(q2, a2), uB[a2], d3);
+            }
+            dst[(0 * Q) * Q * N + q2 * N] = d1;
+            dst[(1 * Q) * Q * N + q2 * N] = d2;
+            dst[(2 * Q) * Q * N + q2 * N] = d3;
           }
-          dst[(0 * Q) * Q * N + q2 * N] = d1;
-          dst[(1 * Q) * Q * N + q2 * N] = d2;
-          dst[(2 * Q) * Q * N + q2 * N] = d3;
-        }
+        });
       }
       if (WANT_E) {  // (q1, j3) lines, on the highest lanes
         for (int t = NQ - 1 - lt; t < Q * M; t += NQ) {
@@ -1211,25 +1284,32 @@ force_kernel(const Params P) {
     if (u < EPB) {
       // b1: T[dl][c][q1][q2][a3] = sum_q3 (dl==2 ? G : B)[q3][a3] S[c][dl](q1,q2,q3); one task
       // per (c, q1, q2) pencil: its 3Q stresses give all 3 x N outputs
-      for (int t = lt; t < DIM * Q * Q; t += NQ) {
-        const int q12 = t % (Q * Q), c = t / (Q * Q);
+      constexpr int SB1 = Split<K>::B1, DLP = 3 / SB1, TB1 = DIM * Q * Q;
+      static_assert(3 % SB1 == 0, "SPLIT_B1 must divide 3");
+      for (int t = lt; t < TB1 * SB1; t += NQ) {
+        const int tb = t % TB1;
+        const int q12 = tb % (Q * Q), c = tb / (Q * Q);
         const int q1 = q12 % Q, q2 = q12 / Q;
+        part_dispatch<SB1>(t / TB1, [&](auto pc) {
+          constexpr int part = decltype(pc)::value;
 #pragma unroll
-        for (int dl = 0; dl < 3; ++dl) {
-          const double *src = Ss + (c * DIM + dl) * NQ + q12;
-          double sv[Q];
+          for (int dd = 0; dd < DLP; ++dd) {
+            const int dl = part * DLP + dd;
+            const double *src = Ss + (c * DIM + dl) * NQ + q12;
+            double sv[Q];
 #pragma unroll
-          for (int q3 = 0; q3 < Q; ++q3) sv[q3] = src[q3 * Q * Q];
-          double *dst = Tb + (((dl * DIM + c) * Q + q1) * Q + q2) * N;
+            for (int q3 = 0; q3 < Q; ++q3) sv[q3] = src[q3 * Q * Q];
+            double *dst = Tb + (((dl * DIM + c) * Q + q1) * Q + q2) * N;
 #pragma unroll
-          for (int a3 = 0; a3 < N; ++a3) {
-            double acc = 0.0;
+            for (int a3 = 0; a3 < N; ++a3) {
+              double acc = 0.0;
 #pragma unroll
-            for (int q3 = 0; q3 < Q; ++q3)
-              acc = __fma_rn(dl == 2 ? CT::G(q3, a3) : CT::B(q3, a3), sv[q3], acc);
-            dst[a3] = acc;
+              for (int q3 = 0; q3 < Q; ++q3)
+                acc = __fma_rn(dl == 2 ? CT::G(q3, a3) : CT::B(q3, a3), sv[q3], acc);
+              dst[a3] = acc;
+            }
           }
-        }
+        });
       }
       // f1[q1][q2][j3] = sum_q3 Bl[q3][j3] A(q1,q2,q3), (q1, q2) pencils on the highest lanes
       for (int t = NQ - 1 - lt; t < Q * Q; t += NQ) {
@@ -1250,8 +1330,11 @@ force_kernel(const Params P) {
     if (u < EPB) {
       // b2: W1[c][q1][a2][a3] = sum_q2 B[q2][a2] T0 ; W23 = sum_q2 G[q2][a2] T1 + B[q2][a2] T2;
       // one task per (c, q1, a3) pencil
-      for (int t = lt; t < DIM * Q * N; t += NQ) {
-        const int a3 = t % N, r = t / N;
+      constexpr int SB2 = Split<K>::B2, A2P = N / SB2, TB2 = DIM * Q * N;
+      static_assert(N % SB2 == 0, "SPLIT_B2 must divide N");
+      for (int t = lt; t < TB2 * SB2; t += NQ) {
+        const int tb = t % TB2;
+        const int a3 = tb % N, r = tb / N;
         const int q1 = r % Q, c = r / Q;
         const double *t0 = Tb + ((0 * DIM + c) * Q + q1) * Q * N + a3;
         const double *t1 = Tb + ((1 * DIM + c) * Q + q1) * Q * N + a3;
@@ -1261,18 +1344,22 @@ force_kernel(const Params P) {
         for (int q2 = 0; q2 < Q; ++q2) { v0[q2] = t0[q2 * N]; v1[q2] = t1[q2 * N]; v2[q2] = t2[q2 * N]; }
         double *w1 = Wb + ((0 * DIM + c) * Q + q1) * N * N + a3;
         double *w23 = Wb + ((1 * DIM + c) * Q + q1) * N * N + a3;
+        part_dispatch<SB2>(t / TB2, [&](auto pc) {
+          constexpr int part = decltype(pc)::value;
 #pragma unroll
-        for (int a2 = 0; a2 < N; ++a2) {
-          double acc1 = 0.0, acc23 = 0.0;
+          for (int aa = 0; aa < A2P; ++aa) {
+            const int a2 = part * A2P + aa;
+            double acc1 = 0.0, acc23 = 0.0;
 #pragma unroll
-          for (int q2 = 0; q2 < Q; ++q2) {
-            acc1 = __fma_rn(CT::B(q2, a2), v0[q2], acc1);
-            acc23 = __fma_rn(CT::G(q2, a2), v1[q2], acc23);
-            acc23 = __fma_rn(CT::B(q2, a2), v2[q2], acc23);
+            for (int q2 = 0; q2 < Q; ++q2) {
+              acc1 = __fma_rn(CT::B(q2, a2), v0[q2], acc1);
+              acc23 = __fma_rn(CT::G(q2, a2), v1[q2], acc23);
+              acc23 = __fma_rn(CT::B(q2, a2), v2[q2], acc23);
+            }
+            w1[a2 * N] = acc1;
+            w23[a2 * N] = acc23;
           }
-          w1[a2 * N] = acc1;
-          w23[a2 * N] = acc23;
-        }
+        });
       }
       // f2[q1][j2][j3] = sum_q2 Bl[q2][j2] f1[q1][q2][j3], (q1, j3) pencils on the highest lanes
       for (int t = NQ - 1 - lt; t < Q * M; t += NQ) {
@@ -1293,8 +1380,11 @@ force_kernel(const Params P) {
     if (u < EPB && unit0 + u < P.n_units) {
       // b3: F1[c][a] = sum_q1 G[q1][a1] W1[c][q1][a2][a3] + B[q1][a1] W23[c][q1][a2][a3];
       // one task per (c, a2, a3) pencil writes the N nodes a1 = 0..N-1 of component c
-      for (int t = lt; t < DIM * N * N; t += NQ) {
-        const int a23 = t % (N * N), c = t / (N * N);
+      constexpr int SB3 = Split<K>::B3, A1P = N / SB3, TB3 = DIM * N * N;
+      static_assert(N % SB3 == 0, "SPLIT_B3 must divide N");
+      for (int t = lt; t < TB3 * SB3; t += NQ) {
+        const int tb = t % TB3;
+        const int a23 = tb % (N * N), c = tb / (N * N);
         double w1v[Q], w23v[Q];
 #pragma unroll
         for (int q1 = 0; q1 < Q; ++q1) {
@@ -1303,17 +1393,21 @@ force_kernel(const Params P) {
         }
         const int a2 = a23 / N, a3 = a23 % N;  // Wb index a2 * N + a3
         const int a0 = (a3 * N + a2) * N;      // node a = a1 + N a2 + N^2 a3
+        part_dispatch<SB3>(t / TB3, [&](auto pc) {
+          constexpr int part = decltype(pc)::value;
 #pragma unroll
-        for (int a1 = 0; a1 < N; ++a1) {
-          double acc = 0.0;
+          for (int aa = 0; aa < A1P; ++aa) {
+            const int a1 = part * A1P + aa;
+            double acc = 0.0;
 #pragma unroll
-          for (int q1 = 0; q1 < Q; ++q1) {
-            acc = __fma_rn(CT::G(q1, a1), w1v[q1], acc);
-            acc = __fma_rn(CT::B(q1, a1), w23v[q1], acc);
+            for (int q1 = 0; q1 < Q; ++q1) {
+              acc = __fma_rn(CT::G(q1, a1), w1v[q1], acc);
+              acc = __fma_rn(CT::B(q1, a1), w23v[q1], acc);
+            }
+            const int s = GATHER1 && MODE == MODE_FORCE ? snode[a0 + a1] : P.slot[slot_base + a0 + a1];
+            if (s >= 0) P.evec[((int64_t)s * DIM + c) * B + b] = acc;
           }
-          const int s = GATHER1 && MODE == MODE_FORCE ? snode[a0 + a1] : P.slot[slot_base + a0 + a1];
-          if (s >= 0) P.evec[((int64_t)s * DIM + c) * B + b] = acc;
-        }
+        });
       }
       const int row = P.ftw_row ? P.ftw_row[l] : l;
       if (row >= 0) {  // (j2, j3) pencils on the highest lanes

@@ -837,19 +837,21 @@ hydro_status launch_lift_mma(int64_t rows, int n, int B, const double *Phi, cons
   return HYDRO_OK;
 }
 
-template <int MT>
+template <int MT, bool AT = false>
 hydro_status launch_project_mma(int n, int64_t s_rows, int B, int G, int64_t chunk, const double *P,
-                                const double *f, double *part, double *r, cudaStream_t s) {
+                                const double *f, double *part, double *r, cudaStream_t s,
+                                int64_t lda = -1, int64_t ldf = -1) {
   constexpr size_t smem = sizeof(double) * 4 * MT * 4 * 2 * 32;
   static std::atomic<unsigned long long> attr_done{0};
   int dev = 0;
   CUDA_OK(cudaGetDevice(&dev));
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(attr_done.load() & bit)) {
-    CUDA_OK(cudaFuncSetAttribute(hk::project_mma_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_OK(cudaFuncSetAttribute(hk::project_mma_kernel<MT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_done.fetch_or(bit);
   }
-  hk::project_mma_kernel<MT><<<G, hk::PROJ_MMA_THREADS, smem, s>>>(n, s_rows, B, chunk, P, f, part);
+  hk::project_mma_kernel<MT, AT><<<G, hk::PROJ_MMA_THREADS, smem, s>>>(
+      n, s_rows, B, chunk, P, lda >= 0 ? lda : s_rows, f, ldf >= 0 ? ldf : B, part);
   g_launches++;
   CUDA_OK(cudaGetLastError());
   const int nB = n * B;
@@ -898,10 +900,10 @@ hydro_status hydro_rom_lift(int64_t rows, int n, int B, const double *Phi, const
 }
 
 // split-K groups of the projection: the tensor-pipe kernel (n <= 40, B <= 64) uses up to
-// 2 CTAs per SM with >= 512 rows each; the fallback up to 8 per SM with >= 256 rows each
+// 2 CTAs per SM with >= 128 rows each; the fallback up to 8 per SM with >= 256 rows each
 static int project_groups(int n, int64_t s_rows, int B) {
   const bool mma = n <= 40 && B <= 64;
-  int64_t g = mma ? (s_rows + 511) / 512 : (s_rows + 255) / 256;
+  int64_t g = mma ? (s_rows + 127) / 128 : (s_rows + 255) / 256;
   const int64_t cap = mma ? 148 * 2 : 148 * 8;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
@@ -2094,6 +2096,25 @@ namespace {
 // G (device [na][nx]) = A^T X over N rows; A, X row-major with leading dimensions lda, ldx.
 hydro_status xprod(int64_t N, int na, const double *A, int64_t lda, int nx, const double *X, int64_t ldx,
                    double *G, cudaStream_t s) {
+  if (na <= 40 && nx <= 64) {
+    // the FP64 tensor-pipe split-K kernel with A read transposed (A^T X), fixed-order reduce
+    int64_t g = (N + 127) / 128;
+    if (g > 148 * 2) g = 148 * 2;
+    if (g < 1) g = 1;
+    const int64_t chunk = (N + g - 1) / g;
+    double *part = nullptr;
+    if (cudaMalloc(&part, sizeof(double) * (size_t)g * na * nx) != cudaSuccess) return HYDRO_ERR_CUDA;
+    const int mt = (na + 7) / 8;
+    hydro_status st;
+    if (mt == 1) st = launch_project_mma<1, true>(na, N, nx, (int)g, chunk, A, X, part, G, s, lda, ldx);
+    else if (mt == 2) st = launch_project_mma<2, true>(na, N, nx, (int)g, chunk, A, X, part, G, s, lda, ldx);
+    else if (mt == 3) st = launch_project_mma<3, true>(na, N, nx, (int)g, chunk, A, X, part, G, s, lda, ldx);
+    else if (mt == 4) st = launch_project_mma<4, true>(na, N, nx, (int)g, chunk, A, X, part, G, s, lda, ldx);
+    else st = launch_project_mma<5, true>(na, N, nx, (int)g, chunk, A, X, part, G, s, lda, ldx);
+    const bool ok = st == HYDRO_OK && cudaStreamSynchronize(s) == cudaSuccess;
+    cudaFree(part);
+    return ok ? HYDRO_OK : (st != HYDRO_OK ? st : HYDRO_ERR_CUDA);
+  }
   const int chunks = (int)std::min<int64_t>(hk::GRAM_CHUNKS, (N + hk::GRAM_KT - 1) / hk::GRAM_KT);
   const int64_t chunk = (N + chunks - 1) / chunks;
   double *part = nullptr;

@@ -167,10 +167,13 @@ lift_mma_kernel(int64_t rows, int n, int B, const double *__restrict__ Phi,
 // tree through shared memory; project_mma_reduce sums the CTA partials in ascending g (fixed
 // order, parallel over 8 sub-ranges per output).  Deterministic.
 constexpr int PROJ_MMA_THREADS = 256;
-template <int MT>
+// AT: A is stored transposed, A(m, k) = P[k * lda + m] (basis products Phi^T X with Phi
+// [s][lda] row-major); otherwise A(m, k) = P[m * lda + k] (the projector [n][s], lda = s).
+// B(k, c) = f[k * ldf + c].
+template <int MT, bool AT = false>
 __global__ void __launch_bounds__(PROJ_MMA_THREADS, 2)
 project_mma_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *__restrict__ P,
-                   const double *__restrict__ f, double *__restrict__ part) {
+                   int64_t lda, const double *__restrict__ f, int64_t ldf, double *__restrict__ part) {
   extern __shared__ __align__(16) double sred[];   // [4 slots][MT*4 tiles][2][32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nh = warp & 1, kg = warp >> 1;
@@ -185,18 +188,18 @@ project_mma_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *__
   const bool fullB = B == 64;
 #pragma unroll 2
   for (int64_t k0 = s_begin + kg * 4; k0 < s_end; k0 += 16) {
-    const int64_t k = k0 + ak;   // A: P[m][k] (m = 8 mt + (l >> 2)); B: f[k][c] (c = 8 nt + (l >> 2))
+    const int64_t k = k0 + ak;   // A: P(m, k) (m = 8 mt + (l >> 2)); B: f[k][c] (c = 8 nt + (l >> 2))
     const bool kin = k < s_end;
     double a[MT], b[4];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
       const int m = mt * 8 + ar;
-      a[mt] = (kin && m < n) ? __ldg(P + (int64_t)m * s_rows + k) : 0.0;
+      a[mt] = (kin && m < n) ? __ldg(P + (AT ? k * lda + m : (int64_t)m * lda + k)) : 0.0;
     }
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const int c = (nh * 4 + nt) * 8 + ar;
-      b[nt] = (kin && (fullB || c < B)) ? __ldg(f + k * B + c) : 0.0;
+      b[nt] = (kin && (fullB || c < B)) ? __ldg(f + k * ldf + c) : 0.0;
     }
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
