@@ -756,6 +756,15 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
 #ifndef SPLIT_B3_K3
 #define SPLIT_B3_K3 1
 #endif
+// Units per CTA of the batched 3D force kernel (r02): a CTA evaluates GEN_UPC consecutive units
+// (consecutive instances of one closure element) in turn, loading the 1D tables once.
+#ifndef GEN_UPC
+#define GEN_UPC 1
+#endif
+template <int DIM, int EPB, int MODE, bool BATCHED>
+__host__ __device__ constexpr int units_per_cta() {
+  return (DIM == 3 && EPB == 1 && BATCHED && MODE == MODE_FORCE) ? GEN_UPC : 1;
+}
 template <int K>
 struct Split {
   static constexpr int F1 = K == 2 ? SPLIT_F1_K2 : SPLIT_F1_K3;   // divides Q
@@ -846,13 +855,20 @@ force_kernel(const Params P) {
   const int tid = threadIdx.x;
   const int u = tid / NQ;               // unit within CTA (may be >= EPB for pad threads)
   const int lt = tid - u * NQ;          // Gauss point within unit
-  const int unit0 = blockIdx.x * EPB;
+  constexpr int UPC = units_per_cta<DIM, EPB, MODE, BATCHED>();
   const int B = BATCHED ? P.B : 1;
 
   // --- tables to shared memory
   for (int i = tid; i < Q; i += NT) sW[i] = P.tab_w[i];
   for (int i = tid; i < Q * N; i += NT) { sB[i] = P.tab_B[i]; sG[i] = P.tab_G[i]; }
   for (int i = tid; i < Q * M; i += NT) sBl[i] = P.tab_Bl[i];
+#pragma unroll 1
+  for (int iu = 0; iu < UPC; ++iu) {
+  const int unit0 = (blockIdx.x * UPC + iu) * EPB;
+  if (UPC > 1) {
+    if (unit0 >= P.n_units) break;      // (uniform over the CTA)
+    if (iu > 0) __syncthreads();        // the previous unit's last shared-memory reads
+  }
   for (int i = tid; i < EPB; i += NT) skey[i] = ~0ull;
 
   // --- S1 gather
@@ -1483,6 +1499,7 @@ force_kernel(const Params P) {
       }
     }
   }
+  }  // units of this CTA
   pdl_trigger();
 }
 

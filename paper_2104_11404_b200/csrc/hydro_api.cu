@@ -143,7 +143,8 @@ template <int DIM, int K, int Q, bool VISC, int MODE, bool BATCHED, bool HAS_W>
 hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
   constexpr int NF = hk::nfields<MODE, HAS_W>();
   using G = hk::Geo<DIM, K, Q, NF>;
-  const int64_t grid = ((int64_t)P.n_units + G::EPB - 1) / G::EPB;
+  constexpr int UPC = hk::units_per_cta<DIM, G::EPB, MODE, BATCHED>();
+  const int64_t grid = ((int64_t)P.n_units + G::EPB * UPC - 1) / (G::EPB * UPC);
   if (grid <= 0) return HYDRO_OK;
   constexpr bool SPEC2D = DIM == 2 && K == 2 && Q == 4 && MODE != hk::MODE_MQ && MODE != hk::MODE_FTW;
   using G2 = hk::G2<NF>;
