@@ -44,6 +44,10 @@ enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2, MODE_FTW = 3 };
 #define GEN_WARP_KEY 1
 #endif
 // one-unit 3D CTAs gather node ids and values in the same thread (no barrier in between)
+// Vectorised (LDS.128) reads of the stage-2 pencils in the last forward stage (3D, even N)
+#ifndef FP_VEC
+#define FP_VEC 1
+#endif
 #ifndef GEN_GATHER1
 #define GEN_GATHER1 1
 #endif
@@ -76,7 +80,10 @@ struct Geo {
   static constexpr bool SEPS = DIM == 3 && NQ >= 128 && GEN_SEPS;
   static constexpr int WORK = SEPS ? FWD + DIM * DIM * NQ + NQ : (FWD > BWD ? FWD : BWD);
   static_assert(!SEPS || TB + WB + F1B + F2B <= FWD, "SEPS layout");
-  static constexpr int UNIT = NF * DIM * ND + NE + WORK;
+  // the work region starts 16-byte aligned (NEP: NE rounded up to even) so that stage outputs
+  // can be read as double2 (LDS.128); every unit is an even number of doubles
+  static constexpr int NEP = (NE + 1) & ~1;
+  static constexpr int UNIT = (NF * DIM * ND + NEP + WORK + 1) & ~1;
   static constexpr int TABD = Q + Q * N * 2 + Q * M;             // w, B, G, Bl
   static constexpr size_t SMEM =
       sizeof(double) * (size_t)(TABD + EPB * UNIT) + sizeof(int) * ((EPB * ND + 1) / 2 * 2) +
@@ -648,12 +655,27 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
         const double *p1 = S2b + ((fc * 3 + 0) * Q + q1i) * Q * N + q2i * N;
         const double *p2 = S2b + ((fc * 3 + 1) * Q + q1i) * Q * N + q2i * N;
         const double *p3 = S2b + ((fc * 3 + 2) * Q + q1i) * Q * N + q2i * N;
-        double d0 = tB[0] * p1[0], d1 = tB[0] * p2[0], d2 = tG[0] * p3[0];
+        double v1[N], v2[N], v3[N];
+        if constexpr (N % 2 == 0 && FP_VEC) {   // 16-byte aligned pencils: LDS.128
+#pragma unroll
+          for (int a3 = 0; a3 < N; a3 += 2) {
+            const double2 x1 = *reinterpret_cast<const double2 *>(p1 + a3);
+            const double2 x2 = *reinterpret_cast<const double2 *>(p2 + a3);
+            const double2 x3 = *reinterpret_cast<const double2 *>(p3 + a3);
+            v1[a3] = x1.x; v1[a3 + 1] = x1.y;
+            v2[a3] = x2.x; v2[a3 + 1] = x2.y;
+            v3[a3] = x3.x; v3[a3 + 1] = x3.y;
+          }
+        } else {
+#pragma unroll
+          for (int a3 = 0; a3 < N; ++a3) { v1[a3] = p1[a3]; v2[a3] = p2[a3]; v3[a3] = p3[a3]; }
+        }
+        double d0 = tB[0] * v1[0], d1 = tB[0] * v2[0], d2 = tG[0] * v3[0];
 #pragma unroll
         for (int a3 = 1; a3 < N; ++a3) {
-          d0 = __fma_rn(tB[a3], p1[a3], d0);
-          d1 = __fma_rn(tB[a3], p2[a3], d1);
-          d2 = __fma_rn(tG[a3], p3[a3], d2);
+          d0 = __fma_rn(tB[a3], v1[a3], d0);
+          d1 = __fma_rn(tB[a3], v2[a3], d1);
+          d2 = __fma_rn(tG[a3], v3[a3], d2);
         }
         double *dst = f == 0 ? J[c] : (f == 1 ? Gv[c] : Gw[c]);
         dst[0] = d0; dst[1] = d1; dst[2] = d2;
@@ -951,7 +973,7 @@ force_kernel(const Params P) {
   double *U = units + uc * G::UNIT;
   double *Xs = U;                         // [NF][DIM][ND]
   double *Es = U + G::NF * DIM * ND;      // [NE]
-  double *Wk = Es + NE;                   // work region
+  double *Wk = Es + G::NEP;               // work region (16-byte aligned)
   const int gu = (unit0 + uc < P.n_units) ? unit0 + uc : 0;  // safe unit for reads
   const int lraw = BATCHED ? gu / B : gu;  // element (or, over compacted units, S0 row)
   const int l = P.unit_elem ? P.unit_elem[lraw] : lraw;
@@ -983,8 +1005,17 @@ force_kernel(const Params P) {
         const int a2 = a23 % N, a3 = a23 / N;
         const double *src = Xs + fc * ND + (a3 * N + a2) * N;
         double x[N];
+        if constexpr (N % 2 == 0 && FP_VEC) {   // 16-byte aligned line: LDS.128
 #pragma unroll
-        for (int a1 = 0; a1 < N; ++a1) x[a1] = src[a1];
+          for (int a1 = 0; a1 < N; a1 += 2) {
+            const double2 x2 = *reinterpret_cast<const double2 *>(src + a1);
+            x[a1] = x2.x;
+            x[a1 + 1] = x2.y;
+          }
+        } else {
+#pragma unroll
+          for (int a1 = 0; a1 < N; ++a1) x[a1] = src[a1];
+        }
         double *dB = S1b + ((fc * 2 + 0) * Q) * N * N + a2 * N + a3;
         double *dG = S1b + ((fc * 2 + 1) * Q) * N * N + a2 * N + a3;
         part_dispatch<SP1>(t / T1, [&](auto pc) {

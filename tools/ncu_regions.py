@@ -71,6 +71,14 @@ def main(rep):
         fp = c["DFMA"] + c["DMUL"] + c["DADD"]
         top = ", ".join(f"{k}:{v / s * 100:.0f}%" for k, v in c.most_common(5))
         print(f"{reg:26s} {s / tot * 100:5.1f}%  fp64 {fp / s * 100:4.0f}%   {top}")
+    # whole kernel: opcode totals (warp instructions), FP64-pipe opcodes first
+    allc = collections.Counter()
+    for c in agg.values():
+        allc.update(c)
+    d_ops = {k: v for k, v in allc.items() if k.startswith("D") and k not in ("DEPBAR",)}
+    print("FP64-pipe opcodes (warp instructions): " +
+          ", ".join(f"{k} {v:.4g}" for k, v in sorted(d_ops.items(), key=lambda kv: -kv[1])))
+    print("top opcodes: " + ", ".join(f"{k} {v / tot * 100:.1f}%" for k, v in allc.most_common(14)))
 
 
 if __name__ == "__main__":
