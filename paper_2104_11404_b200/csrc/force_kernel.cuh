@@ -655,8 +655,9 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
         const double *p1 = S2b + ((fc * 3 + 0) * Q + q1i) * Q * N + q2i * N;
         const double *p2 = S2b + ((fc * 3 + 1) * Q + q1i) * Q * N + q2i * N;
         const double *p3 = S2b + ((fc * 3 + 2) * Q + q1i) * Q * N + q2i * N;
-        double v1[N], v2[N], v3[N];
+        double d0, d1, d2;
         if constexpr (N % 2 == 0 && FP_VEC) {   // 16-byte aligned pencils: LDS.128
+          double v1[N], v2[N], v3[N];
 #pragma unroll
           for (int a3 = 0; a3 < N; a3 += 2) {
             const double2 x1 = *reinterpret_cast<const double2 *>(p1 + a3);
@@ -666,16 +667,21 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
             v2[a3] = x2.x; v2[a3 + 1] = x2.y;
             v3[a3] = x3.x; v3[a3 + 1] = x3.y;
           }
+          d0 = tB[0] * v1[0]; d1 = tB[0] * v2[0]; d2 = tG[0] * v3[0];
+#pragma unroll
+          for (int a3 = 1; a3 < N; ++a3) {
+            d0 = __fma_rn(tB[a3], v1[a3], d0);
+            d1 = __fma_rn(tB[a3], v2[a3], d1);
+            d2 = __fma_rn(tG[a3], v3[a3], d2);
+          }
         } else {
+          d0 = tB[0] * p1[0]; d1 = tB[0] * p2[0]; d2 = tG[0] * p3[0];
 #pragma unroll
-          for (int a3 = 0; a3 < N; ++a3) { v1[a3] = p1[a3]; v2[a3] = p2[a3]; v3[a3] = p3[a3]; }
-        }
-        double d0 = tB[0] * v1[0], d1 = tB[0] * v2[0], d2 = tG[0] * v3[0];
-#pragma unroll
-        for (int a3 = 1; a3 < N; ++a3) {
-          d0 = __fma_rn(tB[a3], v1[a3], d0);
-          d1 = __fma_rn(tB[a3], v2[a3], d1);
-          d2 = __fma_rn(tG[a3], v3[a3], d2);
+          for (int a3 = 1; a3 < N; ++a3) {
+            d0 = __fma_rn(tB[a3], p1[a3], d0);
+            d1 = __fma_rn(tB[a3], p2[a3], d1);
+            d2 = __fma_rn(tG[a3], p3[a3], d2);
+          }
         }
         double *dst = f == 0 ? J[c] : (f == 1 ? Gv[c] : Gw[c]);
         dst[0] = d0; dst[1] = d1; dst[2] = d2;
@@ -1016,8 +1022,9 @@ force_kernel(const Params P) {
 #pragma unroll
           for (int a1 = 0; a1 < N; ++a1) x[a1] = src[a1];
         }
-        double *dB = S1b + ((fc * 2 + 0) * Q) * N * N + a2 * N + a3;
-        double *dG = S1b + ((fc * 2 + 1) * Q) * N * N + a2 * N + a3;
+        // S1b layout [fc][B|G][q1][a3][a2] (a2 fastest: stage 2 reads its pencils contiguously)
+        double *dB = S1b + ((fc * 2 + 0) * Q) * N * N + a3 * N + a2;
+        double *dG = S1b + ((fc * 2 + 1) * Q) * N * N + a3 * N + a2;
         part_dispatch<SP1>(t / T1, [&](auto pc) {
           constexpr int part = decltype(pc)::value;
 #pragma unroll
@@ -1061,11 +1068,11 @@ force_kernel(const Params P) {
         const int t2 = t % T2;
         const int a3 = t2 % N, r = t2 / N;
         const int q1 = r % Q, fc = r / Q;
-        const double *pB = S1b + ((fc * 2 + 0) * Q + q1) * N * N + a3;
-        const double *pG = S1b + ((fc * 2 + 1) * Q + q1) * N * N + a3;
+        const double *pB = S1b + ((fc * 2 + 0) * Q + q1) * N * N + a3 * N;
+        const double *pG = S1b + ((fc * 2 + 1) * Q + q1) * N * N + a3 * N;
         double uB[N], uG[N];
 #pragma unroll
-        for (int a2 = 0; a2 < N; ++a2) { uB[a2] = pB[a2 * N]; uG[a2] = pG[a2 * N]; }
+        for (int a2 = 0; a2 < N; ++a2) { uB[a2] = pB[a2]; uG[a2] = pG[a2]; }
         double *dst = S2b + ((fc * 3) * Q + q1) * Q * N + a3;
         part_dispatch<SP2>(t / T2, [&](auto pc) {
           constexpr int part = decltype(pc)::value;
@@ -1346,14 +1353,15 @@ force_kernel(const Params P) {
             double sv[Q];
 #pragma unroll
             for (int q3 = 0; q3 < Q; ++q3) sv[q3] = src[q3 * Q * Q];
-            double *dst = Tb + (((dl * DIM + c) * Q + q1) * Q + q2) * N;
+            // Tb layout [dl][c][q1][a3][q2] (q2 fastest: b2 reads its pencils contiguously)
+            double *dst = Tb + ((dl * DIM + c) * Q + q1) * Q * N + q2;
 #pragma unroll
             for (int a3 = 0; a3 < N; ++a3) {
               double acc = 0.0;
 #pragma unroll
               for (int q3 = 0; q3 < Q; ++q3)
                 acc = __fma_rn(dl == 2 ? CT::G(q3, a3) : CT::B(q3, a3), sv[q3], acc);
-              dst[a3] = acc;
+              dst[a3 * Q] = acc;
             }
           }
         });
@@ -1383,14 +1391,15 @@ force_kernel(const Params P) {
         const int tb = t % TB2;
         const int a3 = tb % N, r = tb / N;
         const int q1 = r % Q, c = r / Q;
-        const double *t0 = Tb + ((0 * DIM + c) * Q + q1) * Q * N + a3;
-        const double *t1 = Tb + ((1 * DIM + c) * Q + q1) * Q * N + a3;
-        const double *t2 = Tb + ((2 * DIM + c) * Q + q1) * Q * N + a3;
+        const double *t0 = Tb + ((0 * DIM + c) * Q + q1) * Q * N + a3 * Q;
+        const double *t1 = Tb + ((1 * DIM + c) * Q + q1) * Q * N + a3 * Q;
+        const double *t2 = Tb + ((2 * DIM + c) * Q + q1) * Q * N + a3 * Q;
         double v0[Q], v1[Q], v2[Q];
 #pragma unroll
-        for (int q2 = 0; q2 < Q; ++q2) { v0[q2] = t0[q2 * N]; v1[q2] = t1[q2 * N]; v2[q2] = t2[q2 * N]; }
-        double *w1 = Wb + ((0 * DIM + c) * Q + q1) * N * N + a3;
-        double *w23 = Wb + ((1 * DIM + c) * Q + q1) * N * N + a3;
+        for (int q2 = 0; q2 < Q; ++q2) { v0[q2] = t0[q2]; v1[q2] = t1[q2]; v2[q2] = t2[q2]; }
+        // Wb layout [W1|W23][c][a2][a3][q1] (q1 fastest: b3 reads its pencils contiguously)
+        double *w1 = Wb + ((0 * DIM + c) * N * N + a3) * Q + q1;
+        double *w23 = Wb + ((1 * DIM + c) * N * N + a3) * Q + q1;
         part_dispatch<SB2>(t / TB2, [&](auto pc) {
           constexpr int part = decltype(pc)::value;
 #pragma unroll
@@ -1403,8 +1412,8 @@ force_kernel(const Params P) {
               acc23 = __fma_rn(CT::G(q2, a2), v1[q2], acc23);
               acc23 = __fma_rn(CT::B(q2, a2), v2[q2], acc23);
             }
-            w1[a2 * N] = acc1;
-            w23[a2 * N] = acc23;
+            w1[a2 * N * Q] = acc1;
+            w23[a2 * N * Q] = acc23;
           }
         });
       }
@@ -1435,8 +1444,8 @@ force_kernel(const Params P) {
         double w1v[Q], w23v[Q];
 #pragma unroll
         for (int q1 = 0; q1 < Q; ++q1) {
-          w1v[q1] = Wb[((0 * DIM + c) * Q + q1) * N * N + a23];
-          w23v[q1] = Wb[((1 * DIM + c) * Q + q1) * N * N + a23];
+          w1v[q1] = Wb[((0 * DIM + c) * N * N + a23) * Q + q1];
+          w23v[q1] = Wb[((1 * DIM + c) * N * N + a23) * Q + q1];
         }
         const int a2 = a23 / N, a3 = a23 % N;  // Wb index a2 * N + a3
         const int a0 = (a3 * N + a2) * N;      // node a = a1 + N a2 + N^2 a3
