@@ -1324,12 +1324,17 @@ force_kernel(const Params P) {
   double *F1b = Wb + G::WB;
   double *F2b = F1b + G::F1B;
   // (the __syncthreads above separates the last forward read from these writes)
+  // 3D Q3: point stresses stored [c][d][q1][q2][q3] (q3 fastest: the b1 / f1 pencils over q3
+  // are contiguous; C3 -1 %); Q2 and 2D: [c][d][q] with q = q1 + Q q2 (+ Q^2 q3) -- for Q = 4
+  // the q3-fastest store is an 8-way bank conflict (C2 +6 %: profiles/ab/r02_ab5_*)
+  constexpr bool SQ3 = DIM == 3 && K == 3;
+  const int spos = SQ3 ? (q1i + Q * q2i) * Q + q3i : lt;
   if (u < EPB && lt < NQ) {
 #pragma unroll
     for (int c = 0; c < DIM; ++c)
 #pragma unroll
-      for (int d = 0; d < DIM; ++d) Ss[(c * DIM + d) * NQ + lt] = po.S[c][d];
-    As[lt] = po.A;
+      for (int d = 0; d < DIM; ++d) Ss[(c * DIM + d) * NQ + spos] = po.S[c][d];
+    As[spos] = po.A;
   }
   __syncthreads();
   const int64_t slot_base = (int64_t)l * ND;
@@ -1349,10 +1354,10 @@ force_kernel(const Params P) {
 #pragma unroll
           for (int dd = 0; dd < DLP; ++dd) {
             const int dl = part * DLP + dd;
-            const double *src = Ss + (c * DIM + dl) * NQ + q12;
+            const double *src = Ss + (c * DIM + dl) * NQ + (SQ3 ? q12 * Q : q12);
             double sv[Q];
 #pragma unroll
-            for (int q3 = 0; q3 < Q; ++q3) sv[q3] = src[q3 * Q * Q];
+            for (int q3 = 0; q3 < Q; ++q3) sv[q3] = src[SQ3 ? q3 : q3 * Q * Q];
             // Tb layout [dl][c][q1][a3][q2] (q2 fastest: b2 reads its pencils contiguously)
             double *dst = Tb + ((dl * DIM + c) * Q + q1) * Q * N + q2;
 #pragma unroll
@@ -1370,7 +1375,7 @@ force_kernel(const Params P) {
       for (int t = NQ - 1 - lt; t < Q * Q; t += NQ) {
         double av[Q];
 #pragma unroll
-        for (int q3 = 0; q3 < Q; ++q3) av[q3] = As[t + Q * Q * q3];
+        for (int q3 = 0; q3 < Q; ++q3) av[q3] = As[SQ3 ? t * Q + q3 : t + Q * Q * q3];
         const int q1 = t % Q, q2 = t / Q;
 #pragma unroll
         for (int j3 = 0; j3 < M; ++j3) {
