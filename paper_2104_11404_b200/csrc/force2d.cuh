@@ -41,13 +41,23 @@ struct ColOut {
 // The q2 loop of one q1 column: forward last stage, pointwise, first backward stage.
 constexpr int F2D_NT = 64;
 
+// Threads per element (r02): TPE threads share an element's gathered dofs and take its q1
+// columns in turn (q1 = sub, sub + TPE, ...); their F.1 / F^T.w column sums are combined in
+// ascending sub at the end (fixed order).  TPE = 1 is the round-1 layout.
+#ifndef F2D_TPE
+#define F2D_TPE 1
+#endif
+constexpr int F2D_TPE_K = F2D_TPE;
+
 // U rows of the xi_1 contraction (canonical order): ub = sum_a1 B[q1][a1] X[fc][a1,a2],
 // ug = sum_a1 G[q1][a1] X[fc][a1,a2]; Xs is the thread's lane-interleaved dof column.
+// gathered dofs are interleaved over the CTA's elements: stride F2D_NT / TPE
 __device__ __forceinline__ void u_row(int q1, const double *Xs, int fc, int a2, double &ub,
                                       double &ug) {
-  const double x0 = Xs[(fc * 9 + a2 * 3 + 0) * F2D_NT];
-  const double x1 = Xs[(fc * 9 + a2 * 3 + 1) * F2D_NT];
-  const double x2 = Xs[(fc * 9 + a2 * 3 + 2) * F2D_NT];
+  constexpr int XS = F2D_NT / F2D_TPE;
+  const double x0 = Xs[(fc * 9 + a2 * 3 + 0) * XS];
+  const double x1 = Xs[(fc * 9 + a2 * 3 + 1) * XS];
+  const double x2 = Xs[(fc * 9 + a2 * 3 + 2) * XS];
   ub = c_t24.B[q1][0] * x0;
   ug = c_t24.G[q1][0] * x0;
   ub = __fma_rn(c_t24.B[q1][1], x1, ub);
@@ -94,7 +104,7 @@ __device__ __forceinline__ void column2d(AR &ar, int q1, const double (&UB)[6][3
 #pragma unroll (F2D_Q2_UNROLL_K)
   for (int q2 = 0; q2 < 4; ++q2) {
     const double mq = mq_cur;
-    mq_cur = __ldg(q2 < 3 ? mqp + 4 * (q2 + 1) : mqp + (q1 < 3 ? 1 : 0));
+    mq_cur = __ldg(q2 < 3 ? mqp + 4 * (q2 + 1) : mqp + (q1 + F2D_TPE_K < 4 ? F2D_TPE_K : 0));
     double J[3][3], Gv[3][3], Gw[3][3];
     constexpr int NF = HAS_W ? 3 : 2;
 #pragma unroll
@@ -160,7 +170,10 @@ __device__ __forceinline__ void column2d(AR &ar, int q1, const double (&UB)[6][3
 template <int NF>
 struct G2 {
   static constexpr int NT = F2D_NT;
-  static constexpr size_t SMEM = sizeof(double) * (size_t)(NF * 2 * 9 + 18 + 4) * NT;
+  static constexpr int TPE = F2D_TPE;
+  static constexpr int UPB = NT / TPE;   // elements (units) per CTA
+  // per element: gathered dofs NF*2*9 + e 4; per thread: F1 column sums 18
+  static constexpr size_t SMEM = sizeof(double) * (size_t)((NF * 2 * 9 + 4) * UPB + 18 * NT);
 };
 
 #ifndef F2D_MAXNREG
@@ -169,16 +182,20 @@ struct G2 {
 template <bool VISC, int MODE, bool BATCHED, bool HAS_W>
 __global__ void __maxnreg__(F2D_MAXNREG) force2d_kernel(const Params P) {
   constexpr int NF = HAS_W ? 3 : 2;
-  constexpr int ND = 9, NE = 4, NQ = 16, NT = F2D_NT;
+  constexpr int ND = 9, NE = 4, NQ = 16, NT = F2D_NT, TPE = F2D_TPE, UPB = NT / TPE;
   constexpr int NX = NF * 2 * ND;
+  static_assert(NT % TPE == 0 && (TPE == 1 || TPE == 2 || TPE == 4), "F2D_TPE");
   extern __shared__ __align__(16) double smem[];
-  double *Xs = smem + threadIdx.x;              // [NX][NT]   gathered x, v (, w)
-  double *Fs = smem + NX * NT + threadIdx.x;    // [18][NT]   F1 accumulators [c][a2][a1]
-  double *Es = Fs + 18 * NT;                    // [4][NT]    e dofs (off the register budget)
+  const int tid = threadIdx.x;
+  // element slot e of the CTA and this thread's place among its element's TPE threads (the
+  // TPE threads of an element are adjacent lanes)
+  const int e = tid / TPE, sub = tid % TPE;
+  double *Xs = smem + e;                        // [NX][UPB]  gathered x, v (, w) per element
+  double *Es = smem + NX * UPB + e;             // [4][UPB]   e dofs
+  double *Fs = smem + (NX + 4) * UPB + tid;     // [18][NT]   this thread's F1 column sums [c][a2][a1]
   __shared__ unsigned long long skey[NT / 32];
 
-  const int tid = threadIdx.x;
-  const int g0 = blockIdx.x * NT + tid;
+  const int g0 = blockIdx.x * UPB + e;
   const bool valid = g0 < P.n_units;
   const int g = valid ? g0 : P.n_units - 1;   // ragged tail: compute a copy, write nothing
   const int B = BATCHED ? P.B : 1;
@@ -187,23 +204,23 @@ __global__ void __maxnreg__(F2D_MAXNREG) force2d_kernel(const Params P) {
   const int gid = P.elem_gid ? __ldg(P.elem_gid + l) : l;
   const double gam = __ldg(P.gamma + gid);
 
-  // --- S1 gather
+  // --- S1 gather (the element's TPE threads split the nodes)
   {
-    int nd[ND];
 #pragma unroll
-    for (int a = 0; a < ND; ++a) nd[a] = __ldg(P.elem_nodes + (int64_t)l * ND + a);
+    for (int a = sub; a < ND; a += TPE) {
+      const int nd = __ldg(P.elem_nodes + (int64_t)l * ND + a);
 #pragma unroll
-    for (int f = 0; f < NF; ++f) {
-      const double *src = f == 0 ? P.x : (f == 1 ? P.v : P.w);
+      for (int f = 0; f < NF; ++f) {
+        const double *src = f == 0 ? P.x : (f == 1 ? P.v : P.w);
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int a = 0; a < ND; ++a)
-          Xs[((f * 2 + c) * ND + a) * NT] = __ldg(src + ((int64_t)c * P.ld_nodes + nd[a]) * B + b);
+        for (int c = 0; c < 2; ++c)
+          Xs[((f * 2 + c) * ND + a) * UPB] = __ldg(src + ((int64_t)c * P.ld_nodes + nd) * B + b);
+      }
     }
   }
 #pragma unroll
-  for (int j = 0; j < NE; ++j) Es[j * NT] = __ldg(P.e + ((int64_t)l * NE + j) * B + b);
+  for (int j = sub; j < NE; j += TPE) Es[j * UPB] = __ldg(P.e + ((int64_t)l * NE + j) * B + b);
+  if (TPE > 1) __syncwarp();
   double FT[2][2];  // FTw[j1][j2] accumulators
 #pragma unroll
   for (int j = 0; j < 2; ++j) FT[j][0] = FT[j][1] = 0.0;
@@ -219,10 +236,10 @@ __global__ void __maxnreg__(F2D_MAXNREG) force2d_kernel(const Params P) {
     const int64_t si = s_index(P, g, l, b);
     if (si >= 0) Sst = P.S_store + si * 4 * NQ;
   }
-  double mq0 = __ldg(P.mq + (int64_t)gid * NQ);  // m_q(0, 0); then prefetched point by point
+  double mq0 = __ldg(P.mq + (int64_t)gid * NQ + sub);  // m_q(sub, 0); then prefetched point by point
 
 #pragma unroll 1
-  for (int q1 = 0; q1 < 4; ++q1) {
+  for (int q1 = sub; q1 < 4; q1 += TPE) {
     // S2a: contract xi_1 for this q1 (canonical order)
     double UB[6][3], UG[6][3];
 #pragma unroll
@@ -235,8 +252,8 @@ __global__ void __maxnreg__(F2D_MAXNREG) force2d_kernel(const Params P) {
     double E1[2];
 #pragma unroll
     for (int j2 = 0; j2 < 2; ++j2) {
-      const double acc = c_t24.Bl[q1][0] * Es[(j2 * 2 + 0) * NT];
-      E1[j2] = __fma_rn(c_t24.Bl[q1][1], Es[(j2 * 2 + 1) * NT], acc);
+      const double acc = c_t24.Bl[q1][0] * Es[(j2 * 2 + 0) * UPB];
+      E1[j2] = __fma_rn(c_t24.Bl[q1][1], Es[(j2 * 2 + 1) * UPB], acc);
     }
     const double *mqp = P.mq + (int64_t)gid * NQ + q1;  // m_q at (q1, q2) = mqp[4 q2]
 
@@ -257,7 +274,8 @@ __global__ void __maxnreg__(F2D_MAXNREG) force2d_kernel(const Params P) {
     nan = nan || co.nan;
 
     if (MODE == MODE_FORCE) {
-      // S4, q1 stage (same FMA order as force_kernel's b2/b3: G.T0 then B.T1, ascending q1)
+      // S4, q1 stage (same FMA order as force_kernel's b2/b3: G.T0 then B.T1, ascending q1
+      // within this thread's columns)
 #pragma unroll
       for (int c = 0; c < 2; ++c)
 #pragma unroll
@@ -276,14 +294,51 @@ __global__ void __maxnreg__(F2D_MAXNREG) force2d_kernel(const Params P) {
     }
   }
 
+  // combine the element's TPE threads (sub 0 collects, ascending sub)
+  if (TPE > 1) {
+#pragma unroll
+    for (int o = 1; o < TPE; o <<= 1) {
+      const unsigned long long ko = __shfl_down_sync(0xffffffffu, kmin, o);
+      const int fl = __shfl_down_sync(0xffffffffu, (int)tangled | ((int)nan << 1), o);
+      kmin = ko < kmin ? ko : kmin;
+      tangled = tangled || (fl & 1);
+      nan = nan || (fl & 2);
+    }
+    if (MODE == MODE_FORCE) {
+      __syncwarp();
+      if (sub == 0) {
+#pragma unroll
+        for (int k = 0; k < 18; ++k) {
+          double acc = Fs[k * NT];
+#pragma unroll
+          for (int t = 1; t < TPE; ++t) acc = acc + Fs[k * NT + t];
+          Fs[k * NT] = acc;
+        }
+      }
+#pragma unroll
+      for (int j1 = 0; j1 < 2; ++j1)
+#pragma unroll
+        for (int j2 = 0; j2 < 2; ++j2) {
+          double acc = FT[j1][j2];
+          double part[TPE];
+#pragma unroll
+          for (int t = 1; t < TPE; ++t) part[t] = __shfl_down_sync(0xffffffffu, acc, t);
+#pragma unroll
+          for (int t = 1; t < TPE; ++t) acc = acc + part[t];
+          FT[j1][j2] = acc;
+        }
+    }
+  }
+
   // --- S6 dt: flags, warp min of keys, one atomic per CTA (per unit in batched mode)
-  if (valid) {
+  const bool lead = valid && sub == 0;
+  if (lead) {
     if (tangled) atomicMin(&P.st[b].first_bad, (unsigned long long)gid);
     if (nan) atomicOr(&P.st[b].nan_flag, 1u);
   }
-  if (!valid) kmin = ~0ull;
+  if (!lead) kmin = ~0ull;
   if (BATCHED) {
-    if (valid && kmin != ~0ull) atomicMin(&P.st[b].dt_key, kmin);
+    if (lead && kmin != ~0ull) atomicMin(&P.st[b].dt_key, kmin);
   } else {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -300,8 +355,8 @@ __global__ void __maxnreg__(F2D_MAXNREG) force2d_kernel(const Params P) {
     }
   }
 
-  // --- S5 outputs
-  if (MODE == MODE_FORCE && valid) {
+  // --- S5 outputs (the element's first thread)
+  if (MODE == MODE_FORCE && lead) {
 #pragma unroll
     for (int a = 0; a < ND; ++a) {
       const int s = __ldg(P.slot + (int64_t)l * ND + a);

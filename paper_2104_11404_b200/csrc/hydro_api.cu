@@ -152,7 +152,7 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
   // small meshes (C0: 64 elements) run the point-per-thread kernel (16x the threads);
   // hydro_set_2d_kernel overrides the choice (the tests run both paths)
   const int k2d = g_kernel_2d.load(std::memory_order_relaxed);
-  const bool use2d = SPEC2D && (k2d == 1 || (k2d == 0 && P.n_units >= 148 * G2::NT * 2));
+  const bool use2d = SPEC2D && (k2d == 1 || (k2d == 0 && P.n_units >= 148 * G2::UPB * 2));
   void (*kern)(const hk::Params) = hk::force_kernel<DIM, K, Q, VISC, MODE, BATCHED, HAS_W>;
   size_t smem = G::SMEM;
   int nt = G::NT;
@@ -162,7 +162,7 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
       kern = hk::force2d_kernel<VISC, MODE, BATCHED, HAS_W>;
       smem = G2::SMEM;
       nt = G2::NT;
-      grid2 = ((int64_t)P.n_units + G2::NT - 1) / G2::NT;  // one thread per unit
+      grid2 = ((int64_t)P.n_units + G2::UPB - 1) / G2::UPB;  // G2::TPE threads per unit
     }
   }
   // the dynamic shared-memory opt-in is a per-device function attribute: once per device
