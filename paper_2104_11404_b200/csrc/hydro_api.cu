@@ -819,34 +819,9 @@ hydro_status hydro_sample_status_sync(hydro_sample *p, hydro_stream_t stream,
 
 namespace {
 
-#ifndef LIFT_V2
-#define LIFT_V2 1
-#endif
 template <int NKS>
 hydro_status launch_lift_mma(int64_t rows, int n, int B, const double *Phi, const double *os, int os_batched,
                              const double *Y, double *out, cudaStream_t s) {
-  if (LIFT_V2 && n % 2 == 0 && ((uintptr_t)Phi % 16) == 0) {
-    constexpr size_t smem = sizeof(double) * (NKS * 8 * 32 + 2 * hk::LIFT_MMA_RT * (NKS * 4 + 4));
-    static std::atomic<unsigned long long> attr_done{0};
-    static std::atomic<int> sms2{0};
-    int dev = 0;
-    CUDA_OK(cudaGetDevice(&dev));
-    const unsigned long long bit = 1ull << (dev & 63);
-    if (!(attr_done.load() & bit)) {
-      CUDA_OK(cudaFuncSetAttribute(hk::lift_mma2_kernel<NKS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int v = 0;
-      CUDA_OK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
-      sms2.store(v);
-      attr_done.fetch_or(bit);
-    }
-    const int64_t tiles = (rows + hk::LIFT_MMA_RT - 1) / hk::LIFT_MMA_RT;
-    const int64_t g = std::min<int64_t>(tiles, (int64_t)sms2.load() * 2);
-    dim3 grid((unsigned)g, (unsigned)((B + 63) / 64));
-    hk::lift_mma2_kernel<NKS><<<grid, hk::LIFT_MMA_THREADS, smem, s>>>(rows, n, B, Phi, os, os_batched, Y, out);
-    g_launches++;
-    CUDA_OK(cudaGetLastError());
-    return HYDRO_OK;
-  }
   static std::atomic<int> sms{0};
   if (sms.load() == 0) {
     int dev = 0, v = 0;
@@ -863,42 +838,20 @@ hydro_status launch_lift_mma(int64_t rows, int n, int B, const double *Phi, cons
   return HYDRO_OK;
 }
 
-#ifndef PROJ_V2
-#define PROJ_V2 3
-#endif
-#ifndef XPROD_V3
-#define XPROD_V3 1
-#endif
 template <int MT>
-hydro_status launch_project_mma2(int n, int64_t s_rows, int B, int G, int64_t chunk, const double *P,
-                                 const double *f, double *part, double *r, cudaStream_t s) {
-  constexpr size_t smem = sizeof(double) * 4 * MT * 2 * 2 * 32;
-  hk::project_mma2_kernel<MT><<<G, hk::PROJ_MMA_THREADS, smem, s>>>(n, s_rows, B, chunk, P, f, part);
-  g_launches++;
-  CUDA_OK(cudaGetLastError());
-  const int nB = n * B;
-  hk::project_mma_reduce_kernel<<<(nB + hk::PROJ_RED_OUT - 1) / hk::PROJ_RED_OUT, 256, 0, s>>>(nB, G, part, r);
-  g_launches++;
-  CUDA_OK(cudaGetLastError());
-  return HYDRO_OK;
-}
-
-template <int MT, bool AT = false>
 hydro_status launch_project_mma3(int n, int64_t s_rows, int B, int G, int64_t chunk, const double *P,
-                                 const double *f, double *part, double *r, cudaStream_t s,
-                                 int64_t lda = 0) {
+                                 const double *f, double *part, double *r, cudaStream_t s) {
   constexpr size_t smem = sizeof(double) * hk::PROJ3_PS *
-                          ((AT ? hk::PROJ3_PK * (MT * 8 + 4) : MT * 8 * hk::PROJ3_SPS) +
-                           hk::PROJ3_PK * hk::PROJ3_SFS);
+                          (MT * 8 * hk::PROJ3_SPS + hk::PROJ3_PK * hk::PROJ3_SFS);
   static std::atomic<unsigned long long> attr_done{0};
   int dev = 0;
   CUDA_OK(cudaGetDevice(&dev));
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(attr_done.load() & bit)) {
-    CUDA_OK(cudaFuncSetAttribute(hk::project_mma3_kernel<MT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_OK(cudaFuncSetAttribute(hk::project_mma3_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_done.fetch_or(bit);
   }
-  hk::project_mma3_kernel<MT, AT><<<G, 256, smem, s>>>(n, s_rows, B, chunk, P, lda, f, part);
+  hk::project_mma3_kernel<MT><<<G, 256, smem, s>>>(n, s_rows, B, chunk, P, f, part);
   g_launches++;
   CUDA_OK(cudaGetLastError());
   const int nB = n * B;
@@ -995,7 +948,7 @@ hydro_status hydro_rom_project(int n, int64_t s_rows, int B, const double *P, co
   int64_t chunk = std::max<int64_t>((s_rows + G - 1) / G, 1);
   cudaStream_t s = (cudaStream_t)stream;
   double *part = (double *)workspace;
-  if (n <= 40 && PROJ_V2 == 3 && s_rows % 2 == 0 && B % 2 == 0 && ((uintptr_t)P % 16) == 0 &&
+  if (n <= 40 && s_rows % 2 == 0 && B % 2 == 0 && ((uintptr_t)P % 16) == 0 &&
       ((uintptr_t)f % 16) == 0) {
     constexpr int PK = hk::PROJ3_PK;
     chunk = (chunk + PK - 1) / PK * PK;
@@ -1006,17 +959,6 @@ hydro_status hydro_rom_project(int n, int64_t s_rows, int B, const double *P, co
     if (mt == 3) return launch_project_mma3<3>(n, s_rows, B, G3, chunk, P, f, part, r, s);
     if (mt == 4) return launch_project_mma3<4>(n, s_rows, B, G3, chunk, P, f, part, r, s);
     return launch_project_mma3<5>(n, s_rows, B, G3, chunk, P, f, part, r, s);
-  }
-  if (n <= 40 && PROJ_V2) {
-    // chunks of whole 16-row steps (even CTA starts: the k-pairs' 16-byte loads of P)
-    chunk = (chunk + 15) / 16 * 16;
-    const int G2 = (int)((s_rows + chunk - 1) / chunk);
-    const int mt = (n + 7) / 8;
-    if (mt == 1) return launch_project_mma2<1>(n, s_rows, B, G2, chunk, P, f, part, r, s);
-    if (mt == 2) return launch_project_mma2<2>(n, s_rows, B, G2, chunk, P, f, part, r, s);
-    if (mt == 3) return launch_project_mma2<3>(n, s_rows, B, G2, chunk, P, f, part, r, s);
-    if (mt == 4) return launch_project_mma2<4>(n, s_rows, B, G2, chunk, P, f, part, r, s);
-    return launch_project_mma2<5>(n, s_rows, B, G2, chunk, P, f, part, r, s);
   }
   if (n <= 40) {
     const int mt = (n + 7) / 8;
@@ -2195,7 +2137,7 @@ hydro_status xprod(int64_t N, int na, const double *A, int64_t lda, int nx, cons
     int64_t g = (N + 127) / 128;
     if (g > 148 * 2) g = 148 * 2;
     if (g < 1) g = 1;
-    int64_t chunk = (N + g - 1) / g;
+    const int64_t chunk = (N + g - 1) / g;
     // the split-K partials: a per-device scratch kept between calls (grown on demand); the
     // call is synchronous, the mutex serialises host threads
     static std::mutex mu;
@@ -2216,18 +2158,7 @@ hydro_status xprod(int64_t N, int na, const double *A, int64_t lda, int nx, cons
     double *part = scratch[dev];
     const int mt = (na + 7) / 8;
     hydro_status st;
-    const bool v3 = XPROD_V3 && na % 2 == 0 && lda % 2 == 0 && nx % 2 == 0 && ldx == nx &&
-                    ((uintptr_t)A % 16) == 0 && ((uintptr_t)X % 16) == 0;
-    if (v3) {
-      constexpr int PK = hk::PROJ3_PK;
-      chunk = (chunk + PK - 1) / PK * PK;
-      const int G3 = (int)((N + chunk - 1) / chunk);
-      if (mt == 1) st = launch_project_mma3<1, true>(na, N, nx, G3, chunk, A, X, part, G, s, lda);
-      else if (mt == 2) st = launch_project_mma3<2, true>(na, N, nx, G3, chunk, A, X, part, G, s, lda);
-      else if (mt == 3) st = launch_project_mma3<3, true>(na, N, nx, G3, chunk, A, X, part, G, s, lda);
-      else if (mt == 4) st = launch_project_mma3<4, true>(na, N, nx, G3, chunk, A, X, part, G, s, lda);
-      else st = launch_project_mma3<5, true>(na, N, nx, G3, chunk, A, X, part, G, s, lda);
-    } else if (mt == 1) st = launch_project_mma<1, true>(na, N, nx, (int)g, chunk, A, X, part, G, s, lda, ldx);
+    if (mt == 1) st = launch_project_mma<1, true>(na, N, nx, (int)g, chunk, A, X, part, G, s, lda, ldx);
     else if (mt == 2) st = launch_project_mma<2, true>(na, N, nx, (int)g, chunk, A, X, part, G, s, lda, ldx);
     else if (mt == 3) st = launch_project_mma<3, true>(na, N, nx, (int)g, chunk, A, X, part, G, s, lda, ldx);
     else if (mt == 4) st = launch_project_mma<4, true>(na, N, nx, (int)g, chunk, A, X, part, G, s, lda, ldx);

@@ -170,98 +170,6 @@ lift_mma_kernel(int64_t rows, int n, int B, const double *__restrict__ Phi,
   }
 }
 
-// lift v2 (r02): as lift_mma_kernel, but each 128-row tile of Phi (contiguous, 128 n doubles) is
-// copied into a two-stage shared-memory ring with cp.async while the previous tile is computed,
-// so the A fragments come from shared memory and the HBM stream never waits on the tensor pipe.
-// Requires n even (16-byte rows), n <= 4 NKS.
-constexpr int LIFT2_SPH = 44;   // Phi row stride in shared memory (40 + 4: spreads the A reads)
-template <int NKS>
-__global__ void __launch_bounds__(LIFT_MMA_THREADS, 2)
-lift_mma2_kernel(int64_t rows, int n, int B, const double *__restrict__ Phi,
-                 const double *__restrict__ os, int os_batched, const double *__restrict__ Y,
-                 double *__restrict__ out) {
-  extern __shared__ __align__(16) double sl2[];
-  constexpr int SPH = NKS * 4 + 4;
-  double *sY = sl2;                               // [NKS][8][32] fragment order
-  double *sPh = sl2 + NKS * 8 * 32;               // [2][128][SPH]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int c0 = blockIdx.y * 64;
-  const int64_t ntiles = (rows + LIFT_MMA_RT - 1) / LIFT_MMA_RT;
-  auto issue = [&](int64_t t, int stage) {
-    double *dst = sPh + stage * LIFT_MMA_RT * SPH;
-    const int64_t r0 = t * LIFT_MMA_RT;
-    const int half = n / 2;
-    for (int i = tid; i < LIFT_MMA_RT * half; i += LIFT_MMA_THREADS) {
-      const int rr = i / half, c = (i % half) * 2;
-      const bool ok = r0 + rr < rows;
-      cp_async16(dst + rr * SPH + c, ok ? Phi + (r0 + rr) * n + c : Phi, ok);
-    }
-  };
-  int64_t t = blockIdx.x;
-  if (t < ntiles) issue(t, 0);
-  cp_async_commit();
-  for (int i = tid; i < NKS * 8 * 32; i += LIFT_MMA_THREADS) {
-    const int l = i & 31, nt = (i >> 5) & 7, ks = i >> 8;
-    const int k = ks * 4 + (l & 3), c = c0 + nt * 8 + (l >> 2);
-    sY[i] = (k < n && c < B) ? Y[(int64_t)k * B + c] : 0.0;
-  }
-  const int ar = lane >> 2, ak = lane & 3;
-  int stage = 0;
-  for (; t < ntiles; t += gridDim.x, stage ^= 1) {
-    const int64_t tn = t + gridDim.x;
-    if (tn < ntiles) issue(tn, stage ^ 1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const double *sA = sPh + stage * LIFT_MMA_RT * SPH + (warp * 16) * SPH;
-    double acc[2][8][2];
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < NKS; ++ks) {
-      double b[8];
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) b[nt] = sY[(ks * 8 + nt) * 32 + lane];
-      const int k = ks * 4 + ak;
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const double a = k < n ? sA[(mt * 8 + ar) * SPH + k] : 0.0;
-#pragma unroll
-        for (int nt = 0; nt < 8; ++nt) dmma_m8n8k4(acc[mt][nt][0], acc[mt][nt][1], a, b[nt]);
-      }
-    }
-    const int64_t rw = t * LIFT_MMA_RT + warp * 16;
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      const int64_t r = rw + mt * 8 + ar;
-      if (r >= rows) continue;
-      const double o1 = os_batched ? 0.0 : __ldg(os + r);
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        const int c = c0 + nt * 8 + 2 * ak;
-        if (c + 1 < B) {
-          double2 o;
-          if (os_batched) {
-            o = __ldg(reinterpret_cast<const double2 *>(os + r * B + c));
-          } else {
-            o.x = o1;
-            o.y = o1;
-          }
-          double2 v;
-          v.x = o.x + acc[mt][nt][0];
-          v.y = o.y + acc[mt][nt][1];
-          *reinterpret_cast<double2 *>(out + r * B + c) = v;
-        } else if (c < B) {
-          out[r * B + c] = (os_batched ? __ldg(os + r * B + c) : o1) + acc[mt][nt][0];
-        }
-      }
-    }
-    __syncthreads();   // this stage's reads done before it is refilled
-  }
-}
-
 // projection on the tensor pipe, split-K: CTA g reduces a fixed contiguous range of s into
 // a partial [n][B] (n <= 8 MT, B <= 64).  Within the CTA, warp w = 2 kg + nh takes every 4th
 // k-step of the range (k-group kg, fixed) for the column half nh (4 n-tiles) and all MT m-tiles
@@ -351,93 +259,6 @@ project_mma_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *__
   }
 }
 
-// Projection v2 (r02): warp w = 4 kg + nq takes k-group kg (of 2) and the column quarter nq (2
-// n-tiles), all MT m-tiles: MT x 2 tiles = 4 MT accumulators, so 4 k-pairs can be in flight.  A
-// k-pair (8 consecutive rows k0..k0+7) feeds two MMAs: lane (ar, ak) holds rows k0 + 2ak and
-// k0 + 2ak + 1 -- one 16-byte load of P (non-transposed A) -- the first for MMA 1 and the second
-// for MMA 2, with the same row assignment for B.  The two k-group partials are summed in fixed
-// order through shared memory.  Deterministic.
-template <int MT>
-__global__ void __launch_bounds__(PROJ_MMA_THREADS, 2)
-project_mma2_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *__restrict__ P,
-                    const double *__restrict__ f, double *__restrict__ part) {
-  extern __shared__ __align__(16) double sred[];   // [4 warps][MT*2 tiles][2][32]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int kg = warp >> 2, nq = warp & 3;
-  const int64_t s_begin = (int64_t)blockIdx.x * chunk;
-  const int64_t s_end = s_begin + chunk < s_rows ? s_begin + chunk : s_rows;
-  const int ar = lane >> 2, ak = lane & 3;
-  double acc[MT][2][2];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-  const bool fullB = B == 64;
-  const bool vecA = (s_rows % 2 == 0) && (s_begin % 2 == 0) && (((uintptr_t)P & 15) == 0);
-#pragma unroll 2
-  for (int64_t k0 = s_begin + kg * 8; k0 < s_end; k0 += 16) {
-    const int64_t ka = k0 + 2 * ak, kb = ka + 1;   // this lane's two rows of the pair
-    const bool ina = ka < s_end, inb = kb < s_end;
-    double a0[MT], a1[MT], b0[2], b1[2];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      const int m = mt * 8 + ar;
-      if (m < n && vecA && inb) {
-        const double2 v = __ldg(reinterpret_cast<const double2 *>(P + (int64_t)m * s_rows + ka));
-        a0[mt] = v.x;
-        a1[mt] = v.y;
-      } else {
-        a0[mt] = (m < n && ina) ? __ldg(P + (int64_t)m * s_rows + ka) : 0.0;
-        a1[mt] = (m < n && inb) ? __ldg(P + (int64_t)m * s_rows + kb) : 0.0;
-      }
-    }
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      const int c = (nq * 2 + nt) * 8 + ar;
-      const bool cin = fullB || c < B;
-      b0[nt] = (ina && cin) ? __ldg(f + ka * B + c) : 0.0;
-      b1[nt] = (inb && cin) ? __ldg(f + kb * B + c) : 0.0;
-    }
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        dmma_m8n8k4(acc[mt][nt][0], acc[mt][nt][1], a0[mt], b0[nt]);
-        dmma_m8n8k4(acc[mt][nt][0], acc[mt][nt][1], a1[mt], b1[nt]);
-      }
-  }
-  constexpr int TS = MT * 2 * 2 * 32;
-  if (kg == 1) {
-    double *dst = sred + nq * TS;
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        dst[((mt * 2 + nt) * 2 + 0) * 32 + lane] = acc[mt][nt][0];
-        dst[((mt * 2 + nt) * 2 + 1) * 32 + lane] = acc[mt][nt][1];
-      }
-  }
-  __syncthreads();
-  if (kg == 0) {
-    const double *src = sred + nq * TS;
-    double *pg = part + (int64_t)blockIdx.x * n * B;
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      const int m = mt * 8 + ar;
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const double v0 = acc[mt][nt][0] + src[((mt * 2 + nt) * 2 + 0) * 32 + lane];
-        const double v1 = acc[mt][nt][1] + src[((mt * 2 + nt) * 2 + 1) * 32 + lane];
-        const int c = (nq * 2 + nt) * 8 + 2 * ak;
-        if (m < n) {
-          if (c < B) pg[m * B + c] = v0;
-          if (c + 1 < B) pg[m * B + c + 1] = v1;
-        }
-      }
-    }
-  }
-}
-
 // Projection v3 (r02): a streaming split-K GEMM.  CTA g reduces a fixed contiguous range of s in
 // chunks of PK rows; each chunk of P ([n][PK], 8 PK bytes per row) and f ([PK][64]) is copied into a
 // PS-stage shared-memory ring with cp.async (16-byte copies, no registers held while in flight),
@@ -452,16 +273,13 @@ project_mma2_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *_
 #define PROJ3_PS_ 3
 #endif
 constexpr int PROJ3_PK = PROJ3_PK_, PROJ3_PS = PROJ3_PS_, PROJ3_SPS = PROJ3_PK + 4, PROJ3_SFS = 72;
-// AT: P is stored transposed, [s][lda] row-major (A(m, k) = P[k * lda + m]; n even, lda even):
-// its chunk is PK contiguous rows, kept [k][m] in shared memory (row stride SPA).
-template <int MT, bool AT = false>
+template <int MT>
 __global__ void __launch_bounds__(256, 2)
 project_mma3_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *__restrict__ P,
-                    int64_t lda, const double *__restrict__ f, double *__restrict__ part) {
+                    const double *__restrict__ f, double *__restrict__ part) {
   extern __shared__ __align__(16) double sm3[];
   constexpr int PK = PROJ3_PK, PS = PROJ3_PS, SPS = PROJ3_SPS, SFS = PROJ3_SFS;
-  constexpr int SPA = MT * 8 + 4;
-  constexpr int PSZ = AT ? PK * SPA : MT * 8 * SPS;
+  constexpr int PSZ = MT * 8 * SPS;
   constexpr int STAGE = PSZ + PK * SFS;                   // doubles per stage
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ar = lane >> 2, ak = lane & 3;
@@ -472,19 +290,10 @@ project_mma3_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *_
     double *sP = sm3 + (ci % PS) * STAGE;
     double *sF = sP + PSZ;
     const int64_t k0 = s_begin + (int64_t)ci * PK;
-    if (AT) {   // PK rows of P^T, n doubles each
-      const int nh = n / 2;
-      for (int i = tid; i < PK * nh; i += 256) {
-        const int r = i / nh, m = (i % nh) * 2;
-        const bool ok = k0 + r < s_end;
-        cp_async16(sP + r * SPA + m, ok ? P + (k0 + r) * lda + m : P, ok);
-      }
-    } else {    // MT*8 rows of P, PK doubles each
-      for (int i = tid; i < MT * 8 * (PK / 2); i += 256) {
-        const int m = i / (PK / 2), j = (i % (PK / 2)) * 2;
-        const bool ok = m < n && k0 + j < s_end;   // s_rows even and k0 even: pairs never straddle
-        cp_async16(sP + m * SPS + j, ok ? P + (int64_t)m * s_rows + k0 + j : P, ok);
-      }
+    for (int i = tid; i < MT * 8 * (PK / 2); i += 256) {   // MT*8 rows of P, PK doubles each
+      const int m = i / (PK / 2), j = (i % (PK / 2)) * 2;
+      const bool ok = m < n && k0 + j < s_end;   // s_rows even and k0 even: pairs never straddle
+      cp_async16(sP + m * SPS + j, ok ? P + (int64_t)m * s_rows + k0 + j : P, ok);
     }
     // f: 16 rows x B doubles (B/2 copies per row)
     const int bh = (B + 1) / 2;
@@ -520,7 +329,7 @@ project_mma3_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *_
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const int m = mt * 8 + ar;
-        const double a = AT ? (m < n ? sP[(kk * 4 + ak) * SPA + m] : 0.0) : sP[m * SPS + kk * 4 + ak];
+        const double a = sP[m * SPS + kk * 4 + ak];
         dmma_m8n8k4(acc[mt][0], acc[mt][1], a, b);
       }
     }

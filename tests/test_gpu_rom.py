@@ -162,3 +162,22 @@ def test_rom_full_size_c4_all_dt_projection_lift(oracle_lib):
     got = [t.cpu().numpy() for t in H.gpu_offline_ops(batch)]
     for gg, w, what in zip(got, (P_v, P_e, C_xv, c_x), ("P_v", "P_e", "C_xv", "c_x")):
         assert np.abs(gg - w).max() <= 1e-11 * np.abs(w).max(), what
+
+
+@pytest.mark.parametrize("n,s,B", [(40, 409866, 64), (40, 41944, 64), (40, 1000, 64), (40, 997, 64),
+                                   (17, 5000, 8), (8, 64, 2), (40, 300, 5), (33, 12345, 7), (64, 3000, 64)])
+def test_rom_project_kernel_paths(n, s, B):
+    """hydro_rom_project on every kernel path (the cp.async-staged tensor-pipe kernel for even s
+    and B, the register-tiled tensor-pipe kernel otherwise, the FP64 FMA fallback for n > 40)
+    against the projection's definition r = P f in extended-precision numpy, to
+    1e-13 of |P| |f|; and bitwise reproducible."""
+    rng = np.random.default_rng(n * 7 + s + B)
+    P = rng.standard_normal((n, s))
+    f = rng.standard_normal((s, B))
+    ref = (P.astype(np.longdouble) @ f.astype(np.longdouble)).astype(np.float64)
+    mag = np.abs(P) @ np.abs(f)
+    dP, df = H.dev(P), H.dev(f)
+    a = hydro.rom_project(dP, df).cpu().numpy()
+    b = hydro.rom_project(dP, df).cpu().numpy()
+    H.assert_close(a, ref, mag, 1e-13, f"project n={n} s={s} B={B}")
+    assert np.array_equal(a, b)
