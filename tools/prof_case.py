@@ -22,7 +22,7 @@ import torch  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("workload", choices=["c0", "c1", "c2", "c3", "c4"])
+    ap.add_argument("workload", choices=["c0", "c1", "c2", "c3", "c4", "tg"])
     ap.add_argument("--iters", type=int, default=3)
     a = ap.parse_args()
     import workloads as W
