@@ -838,7 +838,7 @@ hydro_status launch_lift_mma(int64_t rows, int n, int B, const double *Phi, cons
   return HYDRO_OK;
 }
 
-template <int MT>
+template <int MT, bool P8>
 hydro_status launch_project_mma3(int n, int64_t s_rows, int B, int G, int64_t chunk, const double *P,
                                  const double *f, double *part, double *r, cudaStream_t s) {
   constexpr size_t smem = sizeof(double) * hk::PROJ3_PS *
@@ -848,10 +848,10 @@ hydro_status launch_project_mma3(int n, int64_t s_rows, int B, int G, int64_t ch
   CUDA_OK(cudaGetDevice(&dev));
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(attr_done.load() & bit)) {
-    CUDA_OK(cudaFuncSetAttribute(hk::project_mma3_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_OK(cudaFuncSetAttribute(hk::project_mma3_kernel<MT, P8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_done.fetch_or(bit);
   }
-  hk::project_mma3_kernel<MT><<<G, 256, smem, s>>>(n, s_rows, B, chunk, P, f, part);
+  hk::project_mma3_kernel<MT, P8><<<G, 256, smem, s>>>(n, s_rows, B, chunk, P, f, part);
   g_launches++;
   CUDA_OK(cudaGetLastError());
   const int nB = n * B;
@@ -948,17 +948,20 @@ hydro_status hydro_rom_project(int n, int64_t s_rows, int B, const double *P, co
   int64_t chunk = std::max<int64_t>((s_rows + G - 1) / G, 1);
   cudaStream_t s = (cudaStream_t)stream;
   double *part = (double *)workspace;
-  if (n <= 40 && s_rows % 2 == 0 && B % 2 == 0 && ((uintptr_t)P % 16) == 0 &&
-      ((uintptr_t)f % 16) == 0) {
+  if (n <= 40 && B % 2 == 0 && ((uintptr_t)P % 16) == 0 && ((uintptr_t)f % 16) == 0) {
     constexpr int PK = hk::PROJ3_PK;
     chunk = (chunk + PK - 1) / PK * PK;
     const int G3 = (int)((s_rows + chunk - 1) / chunk);
     const int mt = (n + 7) / 8;
-    if (mt == 1) return launch_project_mma3<1>(n, s_rows, B, G3, chunk, P, f, part, r, s);
-    if (mt == 2) return launch_project_mma3<2>(n, s_rows, B, G3, chunk, P, f, part, r, s);
-    if (mt == 3) return launch_project_mma3<3>(n, s_rows, B, G3, chunk, P, f, part, r, s);
-    if (mt == 4) return launch_project_mma3<4>(n, s_rows, B, G3, chunk, P, f, part, r, s);
-    return launch_project_mma3<5>(n, s_rows, B, G3, chunk, P, f, part, r, s);
+#define HK_P3(MT)                                                                      \
+  return s_rows % 2 ? launch_project_mma3<MT, true>(n, s_rows, B, G3, chunk, P, f, part, r, s) \
+                    : launch_project_mma3<MT, false>(n, s_rows, B, G3, chunk, P, f, part, r, s)
+    if (mt == 1) HK_P3(1);
+    if (mt == 2) HK_P3(2);
+    if (mt == 3) HK_P3(3);
+    if (mt == 4) HK_P3(4);
+    HK_P3(5);
+#undef HK_P3
   }
   if (n <= 40) {
     const int mt = (n + 7) / 8;

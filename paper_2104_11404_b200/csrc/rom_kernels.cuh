@@ -89,6 +89,11 @@ __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src,
   const int sz = pred ? 16 : 0;   // src-size 0: zero-fill
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem_src), "r"(sz));
 }
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gmem_src, bool pred) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(gmem_src), "r"(sz));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
@@ -265,7 +270,7 @@ project_mma_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *__
 // and warp w computes the column tile w (8 columns) for all MT m-tiles from shared memory (4 MMAs
 // of k 4 per m-tile and chunk; 2 MT accumulators).  The CTA partial is written per warp (no
 // cross-warp reduction); project_mma_reduce sums the CTA partials in ascending g.  Requires
-// n <= 8 MT, B <= 64, s_rows even and P 16-byte aligned.  Deterministic.
+// n <= 8 MT, B <= 64 and even, P and f 16-byte aligned.  Deterministic.
 #ifndef PROJ3_PK_
 #define PROJ3_PK_ 32
 #endif
@@ -273,7 +278,8 @@ project_mma_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *__
 #define PROJ3_PS_ 3
 #endif
 constexpr int PROJ3_PK = PROJ3_PK_, PROJ3_PS = PROJ3_PS_, PROJ3_SPS = PROJ3_PK + 4, PROJ3_SFS = 72;
-template <int MT>
+// P8: s_rows odd -- the rows of P are only 8-byte aligned, so P is copied in 8-byte pieces.
+template <int MT, bool P8 = false>
 __global__ void __launch_bounds__(256, 2)
 project_mma3_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *__restrict__ P,
                     const double *__restrict__ f, double *__restrict__ part) {
@@ -290,10 +296,18 @@ project_mma3_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *_
     double *sP = sm3 + (ci % PS) * STAGE;
     double *sF = sP + PSZ;
     const int64_t k0 = s_begin + (int64_t)ci * PK;
-    for (int i = tid; i < MT * 8 * (PK / 2); i += 256) {   // MT*8 rows of P, PK doubles each
-      const int m = i / (PK / 2), j = (i % (PK / 2)) * 2;
-      const bool ok = m < n && k0 + j < s_end;   // s_rows even and k0 even: pairs never straddle
-      cp_async16(sP + m * SPS + j, ok ? P + (int64_t)m * s_rows + k0 + j : P, ok);
+    if (P8) {
+      for (int i = tid; i < MT * 8 * PK; i += 256) {        // MT*8 rows of P, PK doubles each
+        const int m = i / PK, j = i % PK;
+        const bool ok = m < n && k0 + j < s_end;
+        cp_async8(sP + m * SPS + j, ok ? P + (int64_t)m * s_rows + k0 + j : P, ok);
+      }
+    } else {
+      for (int i = tid; i < MT * 8 * (PK / 2); i += 256) {
+        const int m = i / (PK / 2), j = (i % (PK / 2)) * 2;
+        const bool ok = m < n && k0 + j < s_end;   // s_rows even and k0 even: pairs never straddle
+        cp_async16(sP + m * SPS + j, ok ? P + (int64_t)m * s_rows + k0 + j : P, ok);
+      }
     }
     // f: 16 rows x B doubles (B/2 copies per row)
     const int bh = (B + 1) / 2;

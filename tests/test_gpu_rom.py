@@ -164,11 +164,12 @@ def test_rom_full_size_c4_all_dt_projection_lift(oracle_lib):
         assert np.abs(gg - w).max() <= 1e-11 * np.abs(w).max(), what
 
 
-@pytest.mark.parametrize("n,s,B", [(40, 409866, 64), (40, 41944, 64), (40, 1000, 64), (40, 997, 64),
+@pytest.mark.parametrize("n,s,B", [(40, 410031, 64), (40, 409866, 64), (40, 41944, 64), (40, 1000, 64), (40, 997, 64),
                                    (17, 5000, 8), (8, 64, 2), (40, 300, 5), (33, 12345, 7), (64, 3000, 64)])
 def test_rom_project_kernel_paths(n, s, B):
-    """hydro_rom_project on every kernel path (the cp.async-staged tensor-pipe kernel for even s
-    and B, the register-tiled tensor-pipe kernel otherwise, the FP64 FMA fallback for n > 40)
+    """hydro_rom_project on every kernel path (the cp.async-staged tensor-pipe kernel for even B,
+    with 16- or 8-byte copies of P for even / odd s -- C4's s_v = 410 031 is odd --, the
+    register-tiled tensor-pipe kernel for odd B, the FP64 FMA fallback for n > 40)
     against the projection's definition r = P f in extended-precision numpy, to
     1e-13 of |P| |f|; and bitwise reproducible."""
     rng = np.random.default_rng(n * 7 + s + B)

@@ -35,7 +35,7 @@ def main():
             ts.append(a.elapsed_time(b))
         return float(np.median(ts)) * 1e3
     out = []
-    for name, s in (("project_v", 409866), ("project_e", 41944)):
+    for name, s in (("project_v", 410031), ("project_e", 41944)):
         P, f = r(n, s), r(s, B)
         ws = hydro.rom_project_workspace(n, s, B, dev)
         o = torch.empty((n, B), dtype=torch.float64, device=dev)
@@ -43,7 +43,7 @@ def main():
         err = float((o - P @ f).abs().max() / (P.abs() @ f.abs()).max())
         out.append(f"{name}: {us:.1f} us (rel err {err:.1e})")
     # the same product with the operator stored transposed (Phi^T X, hydro_basis_tproduct; synchronous)
-    PT, f = r(409866, n), r(409866, B)
+    PT, f = r(410031, n), r(410031, B)
     us = timed(lambda: hydro.basis_tproduct(PT, f))
     out.append(f"tproduct_v: {us:.1f} us")
     for name, rows, batched in (("lift_x", 3544689, False), ("lift_e", 859904, True)):

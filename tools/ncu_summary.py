@@ -47,12 +47,13 @@ def _csv(args):
 def full(rep):
     rows = _csv(["-i", rep, "--page", "details", "--csv"])
     h = rows[0]
-    kname = None
+    kname, kid = None, None
     print(f"# ncu --set full summary of {rep}")
     for r in rows[1:]:
-        if kname is None:
-            kname = r[h.index("Kernel Name")]
-            print(f"kernel: {kname}")
+        rid = r[h.index("ID")] if "ID" in h else None
+        if kname is None or rid != kid:
+            kname, kid = r[h.index("Kernel Name")], rid
+            print(f"kernel [{rid}]: {kname}")
         if r[h.index("Metric Name")] in KEEP_DETAILS:
             print(f"  {r[h.index('Metric Name')]:<40} {r[h.index('Metric Value')]:>14} {r[h.index('Metric Unit')]}")
     raw = _csv(["-i", rep, "--page", "raw", "--csv"])
