@@ -380,7 +380,24 @@ def bench_one(name, args, dev, flush, rank, world):
     del gprof
     hydro.profile_release_captured()
     kern_avg = kern_ms / max(kern_n, 1)
-    out = dict(workload=name, ms_per_step=ms, qp_per_s=n_qp / (ms * 1e-3),
+    extra = {}
+    if name == "c0":
+        # C0 is latency-bound; report the per-call latency of back-to-back calls
+        # (1000 calls captured in one CUDA graph, no flush between them)
+        g1000 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1000):
+            for _ in range(1000):
+                step()
+        g1000.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g1000.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        extra["latency_us_back_to_back"] = e0.elapsed_time(e1) / 1000 * 1e3
+        del g1000
+    out = dict(workload=name, ms_per_step=ms, qp_per_s=n_qp / (ms * 1e-3), **extra,
                elements_per_s=n_units / (ms * 1e-3), n_qp=n_qp, force_kernel_ms=kern_avg,
                force_kernel_share=kern_avg / ms if ms > 0 else None,
                gpu_launches=launches, timing="CUDA-graph replay of the step, CUDA events; force kernel: external event-record nodes in a profiled capture of the same step",

@@ -152,7 +152,9 @@ hydro_status hydro_sample_lists(const hydro_sample *s, int32_t *closure_elems /*
  *   out[r][b] = os[r] (os_batched == 0) or os[r][b] (os_batched != 0)
  *               + sum_k Phi[r][k] Y[k][b],    r < rows, k < n, b < B.
  * Phi [rows][n] row-major, Y [n][B], out [rows][B].  Also serves the reduced position
- * RHS r_x = Phi_x^T v_os + (Phi_x^T Phi_v) Yhat_v with Phi = C_xv.            */
+ * RHS r_x = Phi_x^T v_os + (Phi_x^T Phi_v) Yhat_v with Phi = C_xv.  n <= 64,
+ * B even and 16-byte aligned out (and batched os): the FP64 tensor pipe (mma.sync m8n8k4
+ * f64); otherwise an FP64 FMA kernel (n <= 256).  Asynchronous; HYDRO_ERR_ARG on bad sizes. */
 hydro_status hydro_rom_lift(int64_t rows, int n, int B, const double *Phi, const double *os,
                             int os_batched, const double *Y, double *out, hydro_stream_t stream);
 
@@ -183,8 +185,11 @@ hydro_status hydro_sample_status_sync(hydro_sample *s, hydro_stream_t stream,
                                       int64_t *first_bad_elem);
 
 /* Projection (Eq. sol-ls-hyper, P:778-799 with the precomputed (Z^T Phi)^dagger):
- *   r[i][b] = sum_s P[i][s] f[s][b],  P [n][s_rows] row-major, f [s_rows][B], r [n][B].
- * Deterministic split-K; `workspace` (device) >= hydro_rom_project_workspace_bytes.     */
+ *   r[i][b] = sum_s P[i][s] f[s][b],  P [n][s_rows] row-major, f [s_rows][B], r [n][B],
+ * n <= 64, B <= 64.  Deterministic split-K: fixed contiguous row ranges per CTA, partials
+ * summed in a fixed order.  n <= 40: the FP64 tensor pipe (cp.async-staged operands for even
+ * B, register-tiled otherwise); n > 40: FP64 FMA.  `workspace` (device) >=
+ * hydro_rom_project_workspace_bytes, else HYDRO_ERR_WORKSPACE.  Asynchronous.              */
 size_t hydro_rom_project_workspace_bytes(int n, int64_t s_rows, int B);
 hydro_status hydro_rom_project(int n, int64_t s_rows, int B, const double *P, const double *f,
                                double *r, void *workspace, size_t ws_bytes,

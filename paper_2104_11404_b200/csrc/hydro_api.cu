@@ -830,7 +830,7 @@ hydro_status launch_lift_mma(int64_t rows, int n, int B, const double *Phi, cons
     sms.store(v);
   }
   const int64_t tiles = (rows + hk::LIFT_MMA_RT - 1) / hk::LIFT_MMA_RT;
-  const int64_t g = std::min<int64_t>(tiles, (int64_t)sms.load() * 2);   // persistent: 2 CTAs per SM
+  const int64_t g = std::min<int64_t>(tiles, (int64_t)sms.load() * LIFT_MINB);   // persistent CTAs
   dim3 grid((unsigned)g, (unsigned)((B + 63) / 64));
   hk::lift_mma_kernel<NKS><<<grid, hk::LIFT_MMA_THREADS, 0, s>>>(rows, n, B, Phi, os, os_batched, Y, out);
   g_launches++;

@@ -103,12 +103,19 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // m-tiles per warp); Y's column block is staged once per CTA in shared memory in fragment
 // order (conflict-free LDS.64); each warp preloads its 2 x NKS A fragments (Phi rows, 32 B
 // per row per k-step: full sectors) and issues 16 DMMAs per k-step from 32 accumulators.
-constexpr int LIFT_MMA_THREADS = 256, LIFT_MMA_RT = 128;
+#ifndef LIFT_WM
+#define LIFT_WM 2      // m-tiles (8 rows each) per warp
+#endif
+#ifndef LIFT_MINB
+#define LIFT_MINB 2    // CTAs per SM
+#endif
+constexpr int LIFT_MMA_THREADS = 256, LIFT_MMA_RT = 8 * 8 * LIFT_WM;
 template <int NKS>
-__global__ void __launch_bounds__(LIFT_MMA_THREADS, 2)
+__global__ void __launch_bounds__(LIFT_MMA_THREADS, LIFT_MINB)
 lift_mma_kernel(int64_t rows, int n, int B, const double *__restrict__ Phi,
                 const double *__restrict__ os, int os_batched, const double *__restrict__ Y,
                 double *__restrict__ out) {
+  constexpr int WM = LIFT_WM;
   __shared__ double sY[NKS * 8 * 32];   // [kstep][ntile][lane]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c0 = blockIdx.y * 64;
@@ -121,10 +128,10 @@ lift_mma_kernel(int64_t rows, int n, int B, const double *__restrict__ Phi,
   const int64_t ntiles = (rows + LIFT_MMA_RT - 1) / LIFT_MMA_RT;
   const int ar = lane >> 2, ak = lane & 3;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t rw = t * LIFT_MMA_RT + warp * 16;   // this warp's first row
-    double a[2][NKS];
+    const int64_t rw = t * LIFT_MMA_RT + warp * 8 * WM;   // this warp's first row
+    double a[WM][NKS];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
+    for (int mt = 0; mt < WM; ++mt) {
       const int64_t r = rw + mt * 8 + ar;
 #pragma unroll
       for (int ks = 0; ks < NKS; ++ks) {
@@ -132,9 +139,9 @@ lift_mma_kernel(int64_t rows, int n, int B, const double *__restrict__ Phi,
         a[mt][ks] = (r < rows && k < n) ? __ldg(Phi + r * n + k) : 0.0;
       }
     }
-    double acc[2][8][2];
+    double acc[WM][8][2];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < WM; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
 #pragma unroll
@@ -143,12 +150,12 @@ lift_mma_kernel(int64_t rows, int n, int B, const double *__restrict__ Phi,
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) b[nt] = sY[(ks * 8 + nt) * 32 + lane];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < WM; ++mt)
 #pragma unroll
         for (int nt = 0; nt < 8; ++nt) dmma_m8n8k4(acc[mt][nt][0], acc[mt][nt][1], a[mt][ks], b[nt]);
     }
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
+    for (int mt = 0; mt < WM; ++mt) {
       const int64_t r = rw + mt * 8 + ar;
       if (r >= rows) continue;
       const double o1 = os_batched ? 0.0 : __ldg(os + r);
