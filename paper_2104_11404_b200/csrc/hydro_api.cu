@@ -819,9 +819,9 @@ hydro_status hydro_sample_status_sync(hydro_sample *p, hydro_stream_t stream,
 
 namespace {
 
-template <int NKS>
-hydro_status launch_lift_mma(int64_t rows, int n, int B, const double *Phi, const double *os, int os_batched,
-                             const double *Y, double *out, cudaStream_t s) {
+template <int NKS, int WM, int MINB>
+hydro_status launch_lift_mma_t(int64_t rows, int n, int B, const double *Phi, const double *os, int os_batched,
+                               const double *Y, double *out, cudaStream_t s) {
   static std::atomic<int> sms{0};
   if (sms.load() == 0) {
     int dev = 0, v = 0;
@@ -829,13 +829,21 @@ hydro_status launch_lift_mma(int64_t rows, int n, int B, const double *Phi, cons
     CUDA_OK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
     sms.store(v);
   }
-  const int64_t tiles = (rows + hk::LIFT_MMA_RT - 1) / hk::LIFT_MMA_RT;
-  const int64_t g = std::min<int64_t>(tiles, (int64_t)sms.load() * LIFT_MINB);   // persistent CTAs
+  constexpr int RT = 8 * 8 * WM;
+  const int64_t tiles = (rows + RT - 1) / RT;
+  const int64_t g = std::min<int64_t>(tiles, (int64_t)sms.load() * MINB);   // persistent CTAs
   dim3 grid((unsigned)g, (unsigned)((B + 63) / 64));
-  hk::lift_mma_kernel<NKS><<<grid, hk::LIFT_MMA_THREADS, 0, s>>>(rows, n, B, Phi, os, os_batched, Y, out);
+  hk::lift_mma_kernel<NKS, WM, MINB><<<grid, hk::LIFT_MMA_THREADS, 0, s>>>(rows, n, B, Phi, os, os_batched, Y, out);
   g_launches++;
   CUDA_OK(cudaGetLastError());
   return HYDRO_OK;
+}
+
+template <int NKS>
+hydro_status launch_lift_mma(int64_t rows, int n, int B, const double *Phi, const double *os, int os_batched,
+                             const double *Y, double *out, cudaStream_t s) {
+  return os_batched ? launch_lift_mma_t<NKS, 1, 4>(rows, n, B, Phi, os, os_batched, Y, out, s)
+                    : launch_lift_mma_t<NKS, 2, 2>(rows, n, B, Phi, os, os_batched, Y, out, s);
 }
 
 template <int MT, bool P8>

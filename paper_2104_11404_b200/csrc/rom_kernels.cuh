@@ -103,19 +103,17 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // m-tiles per warp); Y's column block is staged once per CTA in shared memory in fragment
 // order (conflict-free LDS.64); each warp preloads its 2 x NKS A fragments (Phi rows, 32 B
 // per row per k-step: full sectors) and issues 16 DMMAs per k-step from 32 accumulators.
-#ifndef LIFT_WM
-#define LIFT_WM 2      // m-tiles (8 rows each) per warp
-#endif
-#ifndef LIFT_MINB
-#define LIFT_MINB 2    // CTAs per SM
-#endif
-constexpr int LIFT_MMA_THREADS = 256, LIFT_MMA_RT = 8 * 8 * LIFT_WM;
-template <int NKS>
-__global__ void __launch_bounds__(LIFT_MMA_THREADS, LIFT_MINB)
+// WM m-tiles (8 rows each) per warp, MINB CTAs per SM: (2, 2) for shared offsets (x, v: the
+// tensor pipe binds, 2 m-tiles reuse each B fragment), (1, 4) for per-instance offsets (e: the
+// offset read makes it HBM-bound; 4 CTAs per SM keep more bytes in flight) -- measured
+// (profiles/ab/r02_ab13_lift_warp_tile.txt).
+constexpr int LIFT_MMA_THREADS = 256;
+template <int NKS, int WM, int MINB>
+__global__ void __launch_bounds__(LIFT_MMA_THREADS, MINB)
 lift_mma_kernel(int64_t rows, int n, int B, const double *__restrict__ Phi,
                 const double *__restrict__ os, int os_batched, const double *__restrict__ Y,
                 double *__restrict__ out) {
-  constexpr int WM = LIFT_WM;
+  constexpr int LIFT_MMA_RT = 8 * 8 * WM;
   __shared__ double sY[NKS * 8 * 32];   // [kstep][ntile][lane]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c0 = blockIdx.y * 64;
