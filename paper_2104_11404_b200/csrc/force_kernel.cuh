@@ -130,6 +130,15 @@ __device__ __forceinline__ int64_t s_index(const Params &P, int unit, int l, int
 }
 
 // ----------------------------------------------------------------------------- helpers
+// min of a 64-bit key over the full warp with two 32-bit REDUX operations (high words, then the
+// low words of the lanes holding the minimal high word)
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long k) {
+  const unsigned hi = (unsigned)(k >> 32);
+  const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? (unsigned)k : 0xffffffffu);
+  return ((unsigned long long)mh << 32) | ml;
+}
+
 __device__ __forceinline__ unsigned long long dt_key(double d) {
   // order-preserving map of a double to uint64 (-0 < +0); NaN never reaches here
   unsigned long long b = (unsigned long long)__double_as_longlong(d);
@@ -443,7 +452,9 @@ __device__ __forceinline__ double lmin3_cf(AR &ar, double a00, double a11, doubl
   double r = (det == 0.0 && den > 0.0) ? det : ar.div(det, den);
   fb = !iso && !(r <= 1.0 - 0x1p-13);
   r = (fb || iso) ? 0.0 : fmax(r, -1.0);  // (branch values unused when fb or iso)
-  const double s = ar.sqrt_((1.0 - r) * 0.5);
+  // r, s, c, f, f' are scale-free: (1 - r)/2 lies in [2^-14, 1], f' = 12c^2 - 3 >= 0.05 and a
+  // nonzero f is far above 2^-967, so these fast paths need no range checks (*_unit)
+  const double s = ar.sqrt_unit((1.0 - r) * 0.5);
   double u = __fma_rn(s, -0.005042, 0.021433);
   u = __fma_rn(s, u, -0.04969);
   u = __fma_rn(s, u, 0.110644);
@@ -454,7 +465,7 @@ __device__ __forceinline__ double lmin3_cf(AR &ar, double a00, double a11, doubl
     const double c2 = c * c;
     const double f = __fma_rn(c, __fma_rn(4.0, c2, -3.0), -r);
     const double fp = __fma_rn(12.0, c2, -3.0);
-    c = c - (f == 0.0 ? f : ar.div(f, fp));
+    c = c - (f == 0.0 ? f : ar.div_unit(f, fp));
   }
   return iso ? q : __fma_rn(2.0 * p, c, q);
 }
@@ -1276,11 +1287,7 @@ force_kernel(const Params P) {
   if (GEN_WARP_KEY && DIM == 3 && EPB == 1) {
     // one unit per CTA: each warp's minimum goes straight to the unit's status word (no
     // shared-memory reduction, no CTA barrier before the backward pass)
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const unsigned long long o = __shfl_xor_sync(0xffffffffu, key, off);
-      key = o < key ? o : key;
-    }
+    key = warp_min_u64(key);
     if ((tid & 31) == 0 && key != ~0ull && unit0 < P.n_units) atomicMin(&P.st[b].dt_key, key);
   } else {
   {
