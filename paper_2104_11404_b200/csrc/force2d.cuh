@@ -70,6 +70,11 @@ __device__ __forceinline__ void u_row(int q1, const double *Xs, int fc, int a2, 
 #define F2D_Q2_UNROLL 2
 #endif
 constexpr int F2D_Q2_UNROLL_K = F2D_Q2_UNROLL;
+// unroll of the q1 column loop (1: rolled; the register budget caps it)
+#ifndef F2D_Q1_UNROLL
+#define F2D_Q1_UNROLL 1
+#endif
+constexpr int F2D_Q1_UNROLL_K = F2D_Q1_UNROLL;
 
 // F2D_KEEP: how many of the (field, component) rows of U stay in registers across the q2
 // loop (the position rows, 2); the velocity (and w) rows are re-contracted from the gathered
@@ -238,7 +243,7 @@ __global__ void __maxnreg__(F2D_MAXNREG) force2d_kernel(const Params P) {
   }
   double mq0 = __ldg(P.mq + (int64_t)gid * NQ + sub);  // m_q(sub, 0); then prefetched point by point
 
-#pragma unroll 1
+#pragma unroll (F2D_Q1_UNROLL_K)
   for (int q1 = sub; q1 < 4; q1 += TPE) {
     // S2a: contract xi_1 for this q1 (canonical order)
     double UB[6][3], UG[6][3];
