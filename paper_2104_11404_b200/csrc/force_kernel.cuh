@@ -795,6 +795,24 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
 #ifndef SPLIT_B3_K3
 #define SPLIT_B3_K3 1
 #endif
+// Unroll of the table-indexed loops of the 3D Q3 contraction stages (r02).  On sm_100a the
+// FP64 instructions take table entries as uniform-register operands (LDCU into URs); fully
+// unrolled, a Q3 stage keeps 48 table doubles live and the uniform file spills into regular
+// registers (R2UR / MOV.SPILL / IMAD.U32 moves: ~10 instructions per FP64 one in stage 1,
+// profiles/r02_v3_c3_*).  K3_ROLL_Q / K3_ROLL_N > 0 unroll the loops over Gauss points / over
+// nodes and dofs by that factor only (Q2 keeps full unrolling: its 24 entries fit).  Same FMA
+// chains, so the same bits.  C3 force call (profiles/ab/r02_ab19-20_*): full 6.56 ms; Q 3 with
+// N full 6.27 ms (kept); Q 2 / N full 6.27; Q 3 / N 2 6.41; Q 1 / N 1 6.56; Q full / N 2 6.56.
+#ifndef K3_ROLL_Q
+#define K3_ROLL_Q 3
+#endif
+#ifndef K3_ROLL_N
+#define K3_ROLL_N 0
+#endif
+// Fill the per-CTA shared table copy from the __constant__ tables (1) or from global memory (0)
+#ifndef TAB_CONST
+#define TAB_CONST 1
+#endif
 // Units per CTA of the batched 3D force kernel (r02): a CTA evaluates GEN_UPC consecutive units
 // (consecutive instances of one closure element) in turn, loading the 1D tables once.
 #ifndef GEN_UPC
@@ -879,6 +897,8 @@ __global__ void __launch_bounds__(KCfg<DIM, K, Q, nfields<MODE, HAS_W>(), EPB_>:
 force_kernel(const Params P) {
   constexpr int NF = nfields<MODE, HAS_W>();
   constexpr bool WANT_E = MODE != MODE_MQ && MODE != MODE_FTW;
+  constexpr int K3UQ = (K == 3 && K3_ROLL_Q > 0) ? K3_ROLL_Q : 64;  // loops over q
+  constexpr int K3UN = (K == 3 && K3_ROLL_N > 0) ? K3_ROLL_N : 64;  // loops over a / j
   using G = Geo<DIM, K, Q, NF, EPB_>;
   constexpr int N = G::N, M = G::M, ND = G::ND, NE = G::NE, NQ = G::NQ, EPB = G::EPB,
                 NT = G::NT;
@@ -897,10 +917,16 @@ force_kernel(const Params P) {
   constexpr int UPC = units_per_cta<DIM, EPB, MODE, BATCHED>();
   const int B = BATCHED ? P.B : 1;
 
-  // --- tables to shared memory
-  for (int i = tid; i < Q; i += NT) sW[i] = P.tab_w[i];
-  for (int i = tid; i < Q * N; i += NT) { sB[i] = P.tab_B[i]; sG[i] = P.tab_G[i]; }
-  for (int i = tid; i < Q * M; i += NT) sBl[i] = P.tab_Bl[i];
+  // --- tables to shared memory (from the __constant__ copy where there is one: a constant-
+  // cache hit instead of a global load at every CTA's start)
+  if constexpr (TAB_CONST && ((K == 2 && Q == 4) || (K == 3 && Q == 6))) {
+    const double *ct = K == 2 ? &c_t24.w[0] : &c_t36.w[0];  // packed w, B, G, Bl = sW.. layout
+    for (int i = tid; i < Q + 2 * Q * N + Q * M; i += NT) sW[i] = ct[i];
+  } else {
+    for (int i = tid; i < Q; i += NT) sW[i] = P.tab_w[i];
+    for (int i = tid; i < Q * N; i += NT) { sB[i] = P.tab_B[i]; sG[i] = P.tab_G[i]; }
+    for (int i = tid; i < Q * M; i += NT) sBl[i] = P.tab_Bl[i];
+  }
 #pragma unroll 1
   for (int iu = 0; iu < UPC; ++iu) {
   const int unit0 = (blockIdx.x * UPC + iu) * EPB;
@@ -1038,7 +1064,7 @@ force_kernel(const Params P) {
         double *dG = S1b + ((fc * 2 + 1) * Q) * N * N + a3 * N + a2;
         part_dispatch<SP1>(t / T1, [&](auto pc) {
           constexpr int part = decltype(pc)::value;
-#pragma unroll
+#pragma unroll (K3UQ)
           for (int qq = 0; qq < QP1; ++qq) {
             const int q1 = part * QP1 + qq;
             double ab = CT::B(q1, 0) * x[0], ag = CT::G(q1, 0) * x[0];
@@ -1059,7 +1085,7 @@ force_kernel(const Params P) {
           double ev[M];
 #pragma unroll
           for (int j1 = 0; j1 < M; ++j1) ev[j1] = src[j1];
-#pragma unroll
+#pragma unroll (K3UQ)
           for (int q1 = 0; q1 < Q; ++q1) {
             double acc = CT::Bl(q1, 0) * ev[0];
 #pragma unroll
@@ -1087,7 +1113,7 @@ force_kernel(const Params P) {
         double *dst = S2b + ((fc * 3) * Q + q1) * Q * N + a3;
         part_dispatch<SP2>(t / T2, [&](auto pc) {
           constexpr int part = decltype(pc)::value;
-#pragma unroll
+#pragma unroll (K3UQ)
           for (int qq = 0; qq < QP2; ++qq) {
             const int q2 = part * QP2 + qq;
             double d1 = CT::B(q2, 0) * uG[0], d2 = CT::G(q2, 0) * uB[0], d3 = CT::B(q2, 0) * uB[0];
@@ -1110,7 +1136,7 @@ force_kernel(const Params P) {
           double ev[M];
 #pragma unroll
           for (int j2 = 0; j2 < M; ++j2) ev[j2] = src[j2 * M];
-#pragma unroll
+#pragma unroll (K3UQ)
           for (int q2 = 0; q2 < Q; ++q2) {
             double acc = CT::Bl(q2, 0) * ev[0];
 #pragma unroll
@@ -1367,7 +1393,7 @@ force_kernel(const Params P) {
             for (int q3 = 0; q3 < Q; ++q3) sv[q3] = src[SQ3 ? q3 : q3 * Q * Q];
             // Tb layout [dl][c][q1][a3][q2] (q2 fastest: b2 reads its pencils contiguously)
             double *dst = Tb + ((dl * DIM + c) * Q + q1) * Q * N + q2;
-#pragma unroll
+#pragma unroll (K3UN)
             for (int a3 = 0; a3 < N; ++a3) {
               double acc = 0.0;
 #pragma unroll
@@ -1384,7 +1410,7 @@ force_kernel(const Params P) {
 #pragma unroll
         for (int q3 = 0; q3 < Q; ++q3) av[q3] = As[SQ3 ? t * Q + q3 : t + Q * Q * q3];
         const int q1 = t % Q, q2 = t / Q;
-#pragma unroll
+#pragma unroll (K3UN)
         for (int j3 = 0; j3 < M; ++j3) {
           double acc = 0.0;
 #pragma unroll
@@ -1414,7 +1440,7 @@ force_kernel(const Params P) {
         double *w23 = Wb + ((1 * DIM + c) * N * N + a3) * Q + q1;
         part_dispatch<SB2>(t / TB2, [&](auto pc) {
           constexpr int part = decltype(pc)::value;
-#pragma unroll
+#pragma unroll (K3UN)
           for (int aa = 0; aa < A2P; ++aa) {
             const int a2 = part * A2P + aa;
             double acc1 = 0.0, acc23 = 0.0;
@@ -1435,7 +1461,7 @@ force_kernel(const Params P) {
         double fv[Q];
 #pragma unroll
         for (int q2 = 0; q2 < Q; ++q2) fv[q2] = F1b[(q1 * Q + q2) * M + j3];
-#pragma unroll
+#pragma unroll (K3UN)
         for (int j2 = 0; j2 < M; ++j2) {
           double acc = 0.0;
 #pragma unroll
@@ -1463,7 +1489,7 @@ force_kernel(const Params P) {
         const int a0 = (a3 * N + a2) * N;      // node a = a1 + N a2 + N^2 a3
         part_dispatch<SB3>(t / TB3, [&](auto pc) {
           constexpr int part = decltype(pc)::value;
-#pragma unroll
+#pragma unroll (K3UN)
           for (int aa = 0; aa < A1P; ++aa) {
             const int a1 = part * A1P + aa;
             double acc = 0.0;
@@ -1484,7 +1510,7 @@ force_kernel(const Params P) {
           double fv[Q];
 #pragma unroll
           for (int q1 = 0; q1 < Q; ++q1) fv[q1] = F2b[(q1 * M + j2) * M + j3];
-#pragma unroll
+#pragma unroll (K3UN)
           for (int j1 = 0; j1 < M; ++j1) {
             double acc = 0.0;
 #pragma unroll
