@@ -51,6 +51,10 @@ enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2, MODE_FTW = 3 };
 #ifndef GEN_GATHER1
 #define GEN_GATHER1 1
 #endif
+// q1-stride padding (doubles) of the Q3 stage-2 blocks (see Geo::S2Q1)
+#ifndef S2PAD_K3
+#define S2PAD_K3 6
+#endif
 
 template <int DIM_, int K_, int Q_, int NF_, int EPB_ = 0>
 struct Geo {
@@ -64,7 +68,11 @@ struct Geo {
   static constexpr int NF = NF_;  // gathered H1 fields: x, v (, w)
   // per-unit shared-memory layout (doubles)
   static constexpr int S1 = DIM == 3 ? Q * N * N : Q * N;       // one stage-1 block
-  static constexpr int S2 = DIM == 3 ? Q * Q * N : 0;           // one stage-2 block
+  // stage-2 block [q1][q2][a3] with q1 stride S2Q1: for Q3 (Q = 6, N = 4) padded 24 -> 30 doubles
+  // so that the per-point LDS.128 pencil reads of forward_point spread over all 32 banks
+  // (unpadded: 3-way conflicts, 80 wavefronts per 7 warps instead of 38; ideal 28)
+  static constexpr int S2Q1 = (DIM == 3 && K == 3) ? Q * N + S2PAD_K3 : Q * N;
+  static constexpr int S2 = DIM == 3 ? Q * S2Q1 : 0;             // one stage-2 block
   static constexpr int E1 = DIM == 3 ? Q * M * M : Q * M;
   static constexpr int E2 = DIM == 3 ? Q * Q * M : 0;
   static constexpr int FWD = NF * DIM * 2 * S1 + NF * DIM * 3 * S2 + E1 + E2;
@@ -653,7 +661,7 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
   using G = Geo<DIM, K, Q, NF>;
   constexpr int N = G::N, M = G::M;
   if (DIM == 3) {
-    const double *S2b = Wk + G::NF * DIM * 2 * G::S1;    // [NF*DIM][3][Q][Q][N]
+    const double *S2b = Wk + G::NF * DIM * 2 * G::S1;    // [NF*DIM][3][Q][S2Q1: Q][N]
     const double *E2b = S2b + G::NF * DIM * 3 * G::S2 + G::E1;  // [Q][Q][M]
     double tB[N], tG[N];
 #pragma unroll
@@ -663,9 +671,9 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
 #pragma unroll
       for (int c = 0; c < DIM; ++c) {
         const int fc = f * DIM + c;
-        const double *p1 = S2b + ((fc * 3 + 0) * Q + q1i) * Q * N + q2i * N;
-        const double *p2 = S2b + ((fc * 3 + 1) * Q + q1i) * Q * N + q2i * N;
-        const double *p3 = S2b + ((fc * 3 + 2) * Q + q1i) * Q * N + q2i * N;
+        const double *p1 = S2b + (fc * 3 + 0) * G::S2 + q1i * G::S2Q1 + q2i * N;
+        const double *p2 = S2b + (fc * 3 + 1) * G::S2 + q1i * G::S2Q1 + q2i * N;
+        const double *p3 = S2b + (fc * 3 + 2) * G::S2 + q1i * G::S2Q1 + q2i * N;
         double d0, d1, d2;
         if constexpr (N % 2 == 0 && FP_VEC) {   // 16-byte aligned pencils: LDS.128
           double v1[N], v2[N], v3[N];
@@ -809,6 +817,12 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
 #ifndef K3_ROLL_N
 #define K3_ROLL_N 0
 #endif
+#ifndef K3_ROLL_B1
+#define K3_ROLL_B1 0
+#endif
+#ifndef K3_ROLL_DL
+#define K3_ROLL_DL 1
+#endif
 // Fill the per-CTA shared table copy from the __constant__ tables (1) or from global memory (0)
 #ifndef TAB_CONST
 #define TAB_CONST 1
@@ -899,6 +913,8 @@ force_kernel(const Params P) {
   constexpr bool WANT_E = MODE != MODE_MQ && MODE != MODE_FTW;
   constexpr int K3UQ = (K == 3 && K3_ROLL_Q > 0) ? K3_ROLL_Q : 64;  // loops over q
   constexpr int K3UN = (K == 3 && K3_ROLL_N > 0) ? K3_ROLL_N : 64;  // loops over a / j
+  constexpr int K3UB1 = (K == 3 && K3_ROLL_B1 > 0) ? K3_ROLL_B1 : 64;  // b1: loop over a3
+  constexpr int K3UD = (K == 3 && K3_ROLL_DL > 0) ? K3_ROLL_DL : 64;   // b1: loop over dl
   using G = Geo<DIM, K, Q, NF, EPB_>;
   constexpr int N = G::N, M = G::M, ND = G::ND, NE = G::NE, NQ = G::NQ, EPB = G::EPB,
                 NT = G::NT;
@@ -1033,7 +1049,7 @@ force_kernel(const Params P) {
 
   if (DIM == 3) {
     double *S1b = Wk;                              // [NF*DIM][2][Q][N][N]
-    double *S2b = Wk + G::NF * DIM * 2 * G::S1;    // [NF*DIM][3][Q][Q][N]
+    double *S2b = Wk + G::NF * DIM * 2 * G::S1;    // [NF*DIM][3][Q][S2Q1: Q][N]
     double *E1b = S2b + G::NF * DIM * 3 * G::S2;   // [Q][M][M]
     double *E2b = E1b + G::E1;                     // [Q][Q][M]
     using CT = CTab<K, Q>;
@@ -1110,7 +1126,7 @@ force_kernel(const Params P) {
         double uB[N], uG[N];
 #pragma unroll
         for (int a2 = 0; a2 < N; ++a2) { uB[a2] = pB[a2]; uG[a2] = pG[a2]; }
-        double *dst = S2b + ((fc * 3) * Q + q1) * Q * N + a3;
+        double *dst = S2b + (fc * 3) * G::S2 + q1 * G::S2Q1 + a3;
         part_dispatch<SP2>(t / T2, [&](auto pc) {
           constexpr int part = decltype(pc)::value;
 #pragma unroll (K3UQ)
@@ -1123,9 +1139,9 @@ force_kernel(const Params P) {
               d2 = __fma_rn(CT::G(q2, a2), uB[a2], d2);
               d3 = __fma_rn(CT::B(q2, a2), uB[a2], d3);
             }
-            dst[(0 * Q) * Q * N + q2 * N] = d1;
-            dst[(1 * Q) * Q * N + q2 * N] = d2;
-            dst[(2 * Q) * Q * N + q2 * N] = d3;
+            dst[0 * G::S2 + q2 * N] = d1;
+            dst[1 * G::S2 + q2 * N] = d2;
+            dst[2 * G::S2 + q2 * N] = d3;
           }
         });
       }
@@ -1384,7 +1400,7 @@ force_kernel(const Params P) {
         const int q1 = q12 % Q, q2 = q12 / Q;
         part_dispatch<SB1>(t / TB1, [&](auto pc) {
           constexpr int part = decltype(pc)::value;
-#pragma unroll
+#pragma unroll (K3UD)
           for (int dd = 0; dd < DLP; ++dd) {
             const int dl = part * DLP + dd;
             const double *src = Ss + (c * DIM + dl) * NQ + (SQ3 ? q12 * Q : q12);
@@ -1393,7 +1409,7 @@ force_kernel(const Params P) {
             for (int q3 = 0; q3 < Q; ++q3) sv[q3] = src[SQ3 ? q3 : q3 * Q * Q];
             // Tb layout [dl][c][q1][a3][q2] (q2 fastest: b2 reads its pencils contiguously)
             double *dst = Tb + ((dl * DIM + c) * Q + q1) * Q * N + q2;
-#pragma unroll (K3UN)
+#pragma unroll (K3UB1)
             for (int a3 = 0; a3 < N; ++a3) {
               double acc = 0.0;
 #pragma unroll
