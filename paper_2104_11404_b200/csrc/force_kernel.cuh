@@ -51,9 +51,12 @@ enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2, MODE_FTW = 3 };
 #ifndef GEN_GATHER1
 #define GEN_GATHER1 1
 #endif
-// q1-stride padding (doubles) of the Q3 stage-2 blocks (see Geo::S2Q1)
+// q1-stride padding (doubles) of the Q3 stage-2 blocks (see Geo::S2Q1) and stage-1 blocks (S1Q1)
 #ifndef S2PAD_K3
 #define S2PAD_K3 6
+#endif
+#ifndef S1PAD_K3
+#define S1PAD_K3 0
 #endif
 
 template <int DIM_, int K_, int Q_, int NF_, int EPB_ = 0>
@@ -67,7 +70,10 @@ struct Geo {
   static constexpr int NT = ((EPB * NQ + 31) / 32) * 32;
   static constexpr int NF = NF_;  // gathered H1 fields: x, v (, w)
   // per-unit shared-memory layout (doubles)
-  static constexpr int S1 = DIM == 3 ? Q * N * N : Q * N;       // one stage-1 block
+  // 3D stage-1 block [q1][a3][a2] with q1 stride S1Q1 = N^2 + S1PAD_K3 (Q3; padding 2 halves
+  // stage 2's modelled LDS.128 conflicts but measured +0.8 % on C3: profiles/ab/r02_ab24_*, so 0)
+  static constexpr int S1Q1 = (DIM == 3 && K == 3) ? N * N + S1PAD_K3 : N * N;
+  static constexpr int S1 = DIM == 3 ? Q * S1Q1 : Q * N;         // one stage-1 block
   // stage-2 block [q1][q2][a3] with q1 stride S2Q1: for Q3 (Q = 6, N = 4) padded 24 -> 30 doubles
   // so that the per-point LDS.128 pencil reads of forward_point spread over all 32 banks
   // (unpadded: 3-way conflicts, 80 wavefronts per 7 warps instead of 38; ideal 28)
@@ -1048,7 +1054,7 @@ force_kernel(const Params P) {
   else { q1i = lq % Q; q2i = (lq / Q) % Q; q3i = lq / (Q * Q); }
 
   if (DIM == 3) {
-    double *S1b = Wk;                              // [NF*DIM][2][Q][N][N]
+    double *S1b = Wk;                              // [NF*DIM][2][Q][S1Q1: N][N]
     double *S2b = Wk + G::NF * DIM * 2 * G::S1;    // [NF*DIM][3][Q][S2Q1: Q][N]
     double *E1b = S2b + G::NF * DIM * 3 * G::S2;   // [Q][M][M]
     double *E2b = E1b + G::E1;                     // [Q][Q][M]
@@ -1076,8 +1082,8 @@ force_kernel(const Params P) {
           for (int a1 = 0; a1 < N; ++a1) x[a1] = src[a1];
         }
         // S1b layout [fc][B|G][q1][a3][a2] (a2 fastest: stage 2 reads its pencils contiguously)
-        double *dB = S1b + ((fc * 2 + 0) * Q) * N * N + a3 * N + a2;
-        double *dG = S1b + ((fc * 2 + 1) * Q) * N * N + a3 * N + a2;
+        double *dB = S1b + (fc * 2 + 0) * G::S1 + a3 * N + a2;
+        double *dG = S1b + (fc * 2 + 1) * G::S1 + a3 * N + a2;
         part_dispatch<SP1>(t / T1, [&](auto pc) {
           constexpr int part = decltype(pc)::value;
 #pragma unroll (K3UQ)
@@ -1089,8 +1095,8 @@ force_kernel(const Params P) {
               ab = __fma_rn(CT::B(q1, a1), x[a1], ab);
               ag = __fma_rn(CT::G(q1, a1), x[a1], ag);
             }
-            dB[q1 * N * N] = ab;
-            dG[q1 * N * N] = ag;
+            dB[q1 * G::S1Q1] = ab;
+            dG[q1 * G::S1Q1] = ag;
           }
         });
       }
@@ -1121,8 +1127,8 @@ force_kernel(const Params P) {
         const int t2 = t % T2;
         const int a3 = t2 % N, r = t2 / N;
         const int q1 = r % Q, fc = r / Q;
-        const double *pB = S1b + ((fc * 2 + 0) * Q + q1) * N * N + a3 * N;
-        const double *pG = S1b + ((fc * 2 + 1) * Q + q1) * N * N + a3 * N;
+        const double *pB = S1b + (fc * 2 + 0) * G::S1 + q1 * G::S1Q1 + a3 * N;
+        const double *pG = S1b + (fc * 2 + 1) * G::S1 + q1 * G::S1Q1 + a3 * N;
         double uB[N], uG[N];
 #pragma unroll
         for (int a2 = 0; a2 < N; ++a2) { uB[a2] = pB[a2]; uG[a2] = pG[a2]; }
