@@ -425,10 +425,14 @@ hydro_status hydro_profile_release_captured(void);
 hydro_status hydro_basis_tables(int k, int q, double *xi, double *w, double *B, double *G,
                                 double *Bl);
 /* Kernel choice for 2D Q2/Q1 force evaluations (process-wide, all devices): 0 = by size
- * (default: one thread per element with >= 18 944 units, else one thread per point),
+ * (default: one thread per element with >= 18 944 units, else one lane per point -- the
+ * generic point-per-thread kernel when w != v),
  * 1 = always one thread per element (force2d_kernel), 2 = always one thread per point
- * (force_kernel).  Both evaluate the same contract with the same backward FMA order, so
- * results are bitwise identical; this is a test and A/B knob.  HYDRO_ERR_ARG otherwise.   */
+ * (force_kernel), 3 = one lane per point with the Gauss column q1 per warp (force2d_pl_kernel;
+ * w == v only, other calls keep the size-based choice).  Every kernel evaluates the same
+ * contract: dt is bitwise identical; 1 and 2 share the backward FMA order (bitwise identical
+ * F.1 / F^T.w), 3 sums the backward over q2 first (same values within the tolerances).
+ * A test and A/B knob.  HYDRO_ERR_ARG otherwise.                                           */
 hydro_status hydro_set_2d_kernel(int choice);
 /* Number of kernel launches issued by this library since load (host counter).            */
 int64_t hydro_launch_count(void);

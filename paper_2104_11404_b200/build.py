@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 SOURCES_CU = ["hydro_api.cu"]
 SOURCES_CPP = ["tables.cpp"]
-HEADERS = ["force_kernel.cuh", "force2d.cuh", "fom.cuh", "ieee_fast.cuh", "rom_kernels.cuh", "offline.cuh", "hydro_internal.h"]
+HEADERS = ["force_kernel.cuh", "force2d.cuh", "force2d_pl.cuh", "fom.cuh", "ieee_fast.cuh", "rom_kernels.cuh", "offline.cuh", "hydro_internal.h"]
 
 
 def _newer(target: str, deps) -> bool:

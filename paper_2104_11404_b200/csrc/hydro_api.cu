@@ -14,6 +14,7 @@
 
 #include "../../include/hydro.h"
 #include "force2d.cuh"
+#include "force2d_pl.cuh"
 #include "fom.cuh"
 #include "offline.cuh"
 #include "force_kernel.cuh"
@@ -123,7 +124,8 @@ struct ProfState {
 };
 ProfState g_prof;
 
-// 2D Q2 kernel choice (hydro_set_2d_kernel): 0 size-based, 1 element per thread, 2 point per thread
+// 2D Q2 kernel choice (hydro_set_2d_kernel): 0 size-based, 1 element per thread, 2 point per
+// thread (generic), 3 point per lane with q1 per warp (force2d_pl)
 std::atomic<int> g_kernel_2d{0};
 
 std::pair<cudaEvent_t, cudaEvent_t> prof_pair() {
@@ -149,10 +151,14 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
   constexpr bool SPEC2D = DIM == 2 && K == 2 && Q == 4 && MODE != hk::MODE_MQ && MODE != hk::MODE_FTW;
   using G2 = hk::G2<NF>;
   // one-thread-per-element 2D kernel only when there are enough elements to fill the GPU;
-  // small meshes (C0: 64 elements) run the point-per-thread kernel (16x the threads);
+  // small meshes (C0: 64 elements) run a point-per-thread kernel (16x the threads);
   // hydro_set_2d_kernel overrides the choice (the tests run both paths)
   const int k2d = g_kernel_2d.load(std::memory_order_relaxed);
   const bool use2d = SPEC2D && (k2d == 1 || (k2d == 0 && P.n_units >= 148 * G2::UPB * 2));
+  constexpr bool SPEC2L = SPEC2D && !HAS_W;
+  // small meshes (C0) and w == v: one lane per point, q1 per warp (C0 force call 14.1 -> 11.3 us;
+  // on C1 the element kernel stays ahead, 43.0 vs 45.5 us: profiles/ab/r02_ab21_2d_lane.txt)
+  const bool use2l = SPEC2L && (k2d == 3 || (k2d == 0 && !use2d));
   void (*kern)(const hk::Params) = hk::force_kernel<DIM, K, Q, VISC, MODE, BATCHED, HAS_W>;
   size_t smem = G::SMEM;
   int nt = G::NT;
@@ -165,16 +171,25 @@ hydro_status launch_force_k(const hk::Params &P, cudaStream_t s) {
       grid2 = ((int64_t)P.n_units + G2::UPB - 1) / G2::UPB;  // G2::TPE threads per unit
     }
   }
+  if constexpr (SPEC2L) {
+    if (use2l) {
+      kern = hk::force2d_pl_kernel<VISC, MODE, BATCHED>;
+      smem = hk::G2L::SMEM;
+      nt = hk::G2L::NT;
+      grid2 = ((int64_t)P.n_units + hk::G2L::UPB - 1) / hk::G2L::UPB;
+    }
+  }
+  const int kidx = use2l ? 2 : (use2d ? 1 : 0);
   // the dynamic shared-memory opt-in is a per-device function attribute: once per device
   // and kernel (bit d of the mask for device d)
-  static std::atomic<unsigned long long> attr_done[2];
+  static std::atomic<unsigned long long> attr_done[3];
   {
     int dev = 0;
     CUDA_OK(cudaGetDevice(&dev));
     const unsigned long long bit = 1ull << (dev & 63);
-    if (!(attr_done[use2d ? 1 : 0].load(std::memory_order_acquire) & bit)) {
+    if (!(attr_done[kidx].load(std::memory_order_acquire) & bit)) {
       CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_done[use2d ? 1 : 0].fetch_or(bit, std::memory_order_acq_rel);
+      attr_done[kidx].fetch_or(bit, std::memory_order_acq_rel);
     }
   }
   std::pair<cudaEvent_t, cudaEvent_t> ev;
@@ -358,7 +373,7 @@ hydro_status hydro_selftest_ieee_fast(uint64_t seed, int64_t n, int op, int dist
 }
 
 hydro_status hydro_set_2d_kernel(int choice) {
-  if (choice < 0 || choice > 2) return HYDRO_ERR_ARG;
+  if (choice < 0 || choice > 3) return HYDRO_ERR_ARG;
   g_kernel_2d.store(choice);
   return HYDRO_OK;
 }

@@ -220,11 +220,12 @@ def selftest_ieee_fast(seed: int, n: int, op: int, dist: int, stream=None):
     return tuple(int(x) for x in counts.cpu().tolist())
 
 
-_K2D = {"auto": 0, "element": 1, "point": 2}
+_K2D = {"auto": 0, "element": 1, "point": 2, "lane": 3}
 
 
 def set_kernel_2d(choice: str) -> None:
-    """hydro_set_2d_kernel: "auto" (by size), "element" (one thread per element) or "point"."""
+    """hydro_set_2d_kernel: "auto" (by size), "element" (one thread per element), "point" (one
+    thread per point, generic kernel) or "lane" (one lane per point, q1 per warp)."""
     _check(lib().hydro_set_2d_kernel(_K2D[choice]), "hydro_set_2d_kernel")
 
 

@@ -1,7 +1,8 @@
 """GPU parity of every kernel path against the oracle (DESIGN "Kernels"):
 
-* 2D Q2: the one-thread-per-element kernel (force2d) and the point-per-thread kernel
-  (force_kernel) -- forced with hydro_set_2d_kernel -- on C0/C1-shaped meshes, w != v,
+* 2D Q2: the one-thread-per-element kernel (force2d), the point-per-thread kernel
+  (force_kernel) and the point-per-lane kernel (force2d_pl, q1 per warp) -- forced with
+  hydro_set_2d_kernel -- on C0/C1-shaped meshes, w != v,
   dt_estimate, and a batched sample plan (hydro_force_sampled with B > 1);
 * degenerate and ragged meshes: one element (every dim/order), and element counts just
   below / at / above the CTA multiples;
@@ -27,7 +28,7 @@ from tests import gpu_helpers as H  # noqa: E402
 from paper_2104_11404_b200 import hydro  # noqa: E402
 
 
-@pytest.fixture(params=["element", "point"])
+@pytest.fixture(params=["element", "point", "lane"])
 def kernel2d(request, set_kernel_2d):
     set_kernel_2d(request.param)
     return request.param
@@ -104,10 +105,12 @@ def test_single_element(oracle_lib, set_kernel_2d, dim, k):
     check(prob, oracle_lib, what=f"one element d{dim}k{k}")
 
 
-@pytest.mark.parametrize("shape", [(63,), (64,), (65,), (127,), (129,)])
-def test_2d_ragged_counts(oracle_lib, set_kernel_2d, shape):
-    """Element counts around the 64-thread CTA of the element kernel."""
-    set_kernel_2d("element")
+@pytest.mark.parametrize("kind", ["element", "lane"])
+@pytest.mark.parametrize("shape", [(1,), (7,), (9,), (63,), (64,), (65,), (127,), (129,)])
+def test_2d_ragged_counts(oracle_lib, set_kernel_2d, shape, kind):
+    """Element counts around the 64-thread CTA of the element kernel and the 8-element CTA
+    of the point-per-lane kernel."""
+    set_kernel_2d(kind)
     prob = W.sedov_like(8, 2, (shape[0], 1), (0.0, 0.0), (shape[0] / 8.0, 0.125), delta=0.1,
                         e_floor=1e-4, vmode="uniform", vscale=0.1, name="ragged2d")
     check(prob, oracle_lib, what=f"2D {shape}")

@@ -98,9 +98,12 @@ def test_tangled_and_nan_status(oracle_lib):
     assert got["status"] == 0 and math.isfinite(got["dt"])
 
 
+@pytest.mark.parametrize("kind", ["auto", "element", "lane"])
 @pytest.mark.parametrize("name", ["c0", "c1"])
-def test_full_size_2d_configs(oracle_lib, name):
-    """C0 and C1 at their BASELINE.json sizes, every output compared."""
+def test_full_size_2d_configs(oracle_lib, set_kernel_2d, name, kind):
+    """C0 and C1 at their BASELINE.json sizes, every output compared; the size-based kernel
+    choice (what the bench times) and each 2D Q2 kernel forced."""
+    set_kernel_2d(kind)
     prob = W.config(name)
     ref = oracle_lib.force(prob)
     got = H.run_full(prob)

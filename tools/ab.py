@@ -1,8 +1,9 @@
 #!/usr/bin/env python
-"""A/B timing of kernel variants selected by env vars (HYDRO_2D_KERNEL, HYDRO_3D_KERNEL),
-one process, CUDA events, L2 flushed between calls.
+"""A/B timing of kernel variants, one process, CUDA events, L2 flushed between calls.
+A variant K2D=<auto|element|point|lane> selects the 2D Q2 kernel (hydro_set_2d_kernel); any
+other NAME=VALUE is set in the environment.
 
-    python tools/ab.py c3 HYDRO_3D_KERNEL=element HYDRO_3D_KERNEL=persistent
+    python tools/ab.py c1 K2D=element K2D=lane
 """
 import os
 import sys
@@ -46,7 +47,10 @@ def main():
     ref = None
     for var in variants:
         k, val = var.split("=")
-        os.environ[k] = val
+        if k == "K2D":
+            hydro.set_kernel_2d(val)
+        else:
+            os.environ[k] = val
         for _ in range(3):
             F1, FTw, dt = ctx.force_full(x, v, e, g, visc, cfl)
         torch.cuda.synchronize()

@@ -24,9 +24,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("workload", choices=["c0", "c1", "c2", "c3", "c4", "tg"])
     ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--k2d", default="auto", help="2D Q2 kernel (hydro_set_2d_kernel)")
     a = ap.parse_args()
     import workloads as W
     from paper_2104_11404_b200 import hydro
+    hydro.set_kernel_2d(a.k2d)
 
     dev = torch.device("cuda", 0)
     t = lambda arr, dt=torch.float64: torch.as_tensor(np.ascontiguousarray(arr)).to(dev, dt).contiguous()
