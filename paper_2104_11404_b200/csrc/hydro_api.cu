@@ -1696,42 +1696,100 @@ hydro_status hydro_rom_advance(hydro_rom *r, double *Yx, double *Yv, double *Ye,
 // ------------------------------------------------------------------------------ offline (NEXT-3)
 namespace {
 
-// Symmetric eigen-decomposition of a small dense matrix (host, cyclic Jacobi to full
-// convergence): A [n][n] row-major in, eigenvalues lam[n] descending, eigenvectors V [n][n]
-// (column c = eigenvector c), each with its largest-magnitude component positive.
+// Symmetric eigen-decomposition of a small dense matrix (host): Householder reduction to
+// tridiagonal form with the reflections accumulated, then the implicit-shift QL iteration on
+// the tridiagonal with the rotations applied to the accumulated basis (O(n^3); the cyclic
+// Jacobi used before took ~6 ms for the 64 x 64 snapshot Gram matrix).  A [n][n] row-major in,
+// eigenvalues lam[n] descending, eigenvectors V [n][n] (column c = eigenvector c), each with
+// its largest-magnitude component positive.  Backward stable: eigenvalue errors ~ n eps ||A||.
 void sym_eig_host(int n, std::vector<double> A, std::vector<double> &lam, std::vector<double> &V) {
+  auto a = [&](int i, int j) -> double & { return A[(size_t)i * n + j]; };
   V.assign((size_t)n * n, 0.0);
   for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0;
-  auto a = [&](int i, int j) -> double & { return A[(size_t)i * n + j]; };
-  for (int sweep = 0; sweep < 100; ++sweep) {
-    double off = 0.0, tot = 0.0;
-    for (int i = 0; i < n; ++i)
-      for (int j = 0; j < n; ++j) { tot += a(i, j) * a(i, j); if (i != j) off += a(i, j) * a(i, j); }
-    if (off <= 1e-30 * tot || off == 0.0) break;
-    for (int p = 0; p < n - 1; ++p)
-      for (int q = p + 1; q < n; ++q) {
-        const double apq = a(p, q);
-        if (apq == 0.0) continue;
-        const double theta = (a(q, q) - a(p, p)) / (2.0 * apq);
-        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
-        const double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
-        for (int k = 0; k < n; ++k) {  // A <- A J (columns p, q)
-          const double akp = a(k, p), akq = a(k, q);
-          a(k, p) = c * akp - sn * akq;
-          a(k, q) = sn * akp + c * akq;
+  auto z = [&](int i, int j) -> double & { return V[(size_t)i * n + j]; };
+  std::vector<double> d((size_t)n), e((size_t)n, 0.0), v((size_t)n), pv((size_t)n);
+  // Householder: for column k, reflect A[k+1:, k] onto a multiple of e_{k+1}; A <- H A H, Z <- Z H
+  for (int k = 0; k + 2 < n; ++k) {
+    double nx = 0.0;
+    for (int i = k + 1; i < n; ++i) nx += a(i, k) * a(i, k);
+    nx = std::sqrt(nx);
+    if (nx == 0.0) continue;
+    const double x0 = a(k + 1, k);
+    const double alpha = x0 >= 0.0 ? -nx : nx;
+    for (int i = 0; i <= k; ++i) v[(size_t)i] = 0.0;
+    for (int i = k + 1; i < n; ++i) v[(size_t)i] = a(i, k);
+    v[(size_t)k + 1] -= alpha;
+    double vv = 0.0;
+    for (int i = k + 1; i < n; ++i) vv += v[(size_t)i] * v[(size_t)i];
+    if (vv == 0.0) continue;
+    const double beta = 2.0 / vv;
+    // p = beta A v, q = p - (beta v^T p / 2) v, A <- A - v q^T - q v^T (rows/cols >= k)
+    double vp = 0.0;
+    for (int i = k; i < n; ++i) {
+      double acc = 0.0;
+      for (int j = k + 1; j < n; ++j) acc += a(i, j) * v[(size_t)j];
+      pv[(size_t)i] = beta * acc;
+      vp += v[(size_t)i] * pv[(size_t)i];
+    }
+    const double kk = 0.5 * beta * vp;
+    for (int i = k; i < n; ++i) pv[(size_t)i] -= kk * v[(size_t)i];
+    for (int i = k; i < n; ++i)
+      for (int j = k; j < n; ++j) a(i, j) -= v[(size_t)i] * pv[(size_t)j] + pv[(size_t)i] * v[(size_t)j];
+    for (int i = 0; i < n; ++i) {  // Z <- Z (I - beta v v^T)
+      double acc = 0.0;
+      for (int j = k + 1; j < n; ++j) acc += z(i, j) * v[(size_t)j];
+      acc *= beta;
+      for (int j = k + 1; j < n; ++j) z(i, j) -= acc * v[(size_t)j];
+    }
+  }
+  for (int i = 0; i < n; ++i) d[(size_t)i] = a(i, i);
+  for (int i = 0; i + 1 < n; ++i) e[(size_t)i] = a(i + 1, i);   // e[i]: between i and i+1
+  // implicit-shift QL on (d, e); e[n-1] = 0
+  const double eps = std::numeric_limits<double>::epsilon();
+  for (int l = 0; l < n; ++l) {
+    for (int iter = 0; iter < 60; ++iter) {
+      int m = l;
+      for (; m < n - 1; ++m) {
+        const double dd = std::fabs(d[(size_t)m]) + std::fabs(d[(size_t)m + 1]);
+        if (std::fabs(e[(size_t)m]) <= eps * dd) break;
+      }
+      if (m == l) break;
+      double g = (d[(size_t)l + 1] - d[(size_t)l]) / (2.0 * e[(size_t)l]);
+      double r = std::hypot(g, 1.0);
+      g = d[(size_t)m] - d[(size_t)l] + e[(size_t)l] / (g + (g >= 0.0 ? r : -r));
+      double sn = 1.0, c = 1.0, p = 0.0;
+      int i = m - 1;
+      bool deflated = false;
+      for (; i >= l; --i) {
+        const double f = sn * e[(size_t)i], b = c * e[(size_t)i];
+        r = std::hypot(f, g);
+        e[(size_t)i + 1] = r;
+        if (r == 0.0) {  // underflow: the subdiagonal split
+          d[(size_t)i + 1] -= p;
+          e[(size_t)m] = 0.0;
+          deflated = true;
+          break;
         }
-        for (int k = 0; k < n; ++k) {  // A <- J^T A (rows p, q)
-          const double apk = a(p, k), aqk = a(q, k);
-          a(p, k) = c * apk - sn * aqk;
-          a(q, k) = sn * apk + c * aqk;
-        }
+        sn = f / r;
+        c = g / r;
+        g = d[(size_t)i + 1] - p;
+        r = (d[(size_t)i] - g) * sn + 2.0 * c * b;
+        p = sn * r;
+        d[(size_t)i + 1] = g + p;
+        g = c * r - b;
         for (int k = 0; k < n; ++k) {
-          const double vkp = V[(size_t)k * n + p], vkq = V[(size_t)k * n + q];
-          V[(size_t)k * n + p] = c * vkp - sn * vkq;
-          V[(size_t)k * n + q] = sn * vkp + c * vkq;
+          const double zf = z(k, i + 1);
+          z(k, i + 1) = sn * z(k, i) + c * zf;
+          z(k, i) = c * z(k, i) - sn * zf;
         }
       }
+      if (deflated) continue;
+      d[(size_t)l] -= p;
+      e[(size_t)l] = g;
+      e[(size_t)m] = 0.0;
+    }
   }
+  for (int i = 0; i < n; ++i) a(i, i) = d[(size_t)i];
   std::vector<int> order((size_t)n);
   for (int i = 0; i < n; ++i) order[(size_t)i] = i;
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return a(x, x) > a(y, y); });
@@ -1810,6 +1868,80 @@ bool lstsq_host(int rows, int n, std::vector<double> A, std::vector<double> &b) 
   return true;
 }
 
+// A per-device scratch buffer of the offline routines (split-K partials), kept between calls
+// and grown on demand; the routines using it synchronise their stream before returning, and
+// the lock serialises host threads for the duration of a call.
+struct Scratch {
+  std::mutex mu;
+  double *p[64] = {};
+  size_t n[64] = {};
+  double *get(size_t need) {  // call with mu held
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    dev &= 63;
+    if (n[dev] < need) {
+      cudaFree(p[dev]);
+      p[dev] = nullptr;
+      n[dev] = 0;
+      if (cudaMalloc(&p[dev], sizeof(double) * need) != cudaSuccess) return nullptr;
+      n[dev] = need;
+    }
+    return p[dev];
+  }
+};
+Scratch g_gram_scratch;
+
+int sm_count() {
+  static std::atomic<int> sms{0};
+  if (sms.load() == 0) {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return 148;
+    sms.store(v);
+  }
+  return sms.load();
+}
+
+// G (device [n][n], full) = the Gram matrix of A's n vectors of length N on the FP64 tensor pipe
+// (gram_mma_kernel, split-K over ~2 CTAs per SM, fixed-order reduce); synchronous.
+// kfast: A(i, k) = A[i * ld + k] (snapshot rows), else A[k * ld + i] (basis columns).
+hydro_status gram_mma(int n, int64_t N, int64_t ld, bool kfast, const double *A, double *G, cudaStream_t s) {
+  const int tiles = (n + hk::GMMA_T - 1) / hk::GMMA_T;
+  const int64_t kblocks = (N + hk::GMMA_KB - 1) / hk::GMMA_KB;
+  int64_t chunks = std::max<int64_t>(1, (int64_t)sm_count() * 2 / ((int64_t)tiles * tiles));
+  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, kblocks / 4));
+  const int64_t chunk = (kblocks + chunks - 1) / chunks * hk::GMMA_KB;
+  chunks = (N + chunk - 1) / chunk;
+  std::lock_guard<std::mutex> lk(g_gram_scratch.mu);
+  double *part = g_gram_scratch.get((size_t)chunks * n * n);
+  if (!part) return HYDRO_ERR_CUDA;
+  const dim3 grid((unsigned)chunks, (unsigned)tiles, (unsigned)tiles);
+  if (kfast) hk::gram_mma_kernel<true><<<grid, 256, 0, s>>>(n, N, chunk, ld, A, part);
+  else hk::gram_mma_kernel<false><<<grid, 256, 0, s>>>(n, N, chunk, ld, A, part);
+  const int nn = n * n;
+  hk::project_mma_reduce_kernel<<<(nn + hk::PROJ_RED_OUT - 1) / hk::PROJ_RED_OUT, 256, 0, s>>>(nn, (int)chunks, part, G);
+  g_launches += 2;
+  const bool ok = cudaGetLastError() == cudaSuccess && cudaStreamSynchronize(s) == cudaSuccess;
+  return ok ? HYDRO_OK : HYDRO_ERR_CUDA;
+}
+
+// out[r][c] (row stride ldo) = sum_k A(r, k) Y[k][c], r < rows, c < B <= 64, K <= 64, on the FP64
+// tensor pipe (tall_mma_kernel); A(r, k) = at ? A[k * lda + r] : A[r * lda + k].  Asynchronous.
+// In place (out == A, !at, ldo == lda) is allowed.
+template <bool AT>
+hydro_status tall_mma(int64_t rows, int K, int B, const double *A, int64_t lda, const double *Y, double *out,
+                      int64_t ldo, cudaStream_t s) {
+  if (K <= 0 || K > 64 || B <= 0 || B > 64) return HYDRO_ERR_ARG;
+  const int64_t tiles = (rows + 127) / 128;
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count() * 2));
+  if (K <= 8) hk::tall_mma_kernel<AT, 2><<<g, 256, 0, s>>>(rows, K, B, A, lda, Y, out, ldo);
+  else if (K <= 16) hk::tall_mma_kernel<AT, 4><<<g, 256, 0, s>>>(rows, K, B, A, lda, Y, out, ldo);
+  else if (K <= 32) hk::tall_mma_kernel<AT, 8><<<g, 256, 0, s>>>(rows, K, B, A, lda, Y, out, ldo);
+  else hk::tall_mma_kernel<AT, 16><<<g, 256, 0, s>>>(rows, K, B, A, lda, Y, out, ldo);
+  g_launches++;
+  return cudaGetLastError() == cudaSuccess ? HYDRO_OK : HYDRO_ERR_CUDA;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1826,16 +1958,23 @@ hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k
   double *part = nullptr, *G = nullptr, *W = nullptr;
   hydro_status st = HYDRO_OK;
   auto cleanup = [&]() { cudaFree(part); cudaFree(G); cudaFree(W); };
-  if (cudaMalloc(&part, sizeof(double) * (size_t)chunks * ns * ns) != cudaSuccess ||
+  if ((!(ns <= 64 && max_k <= 64) && cudaMalloc(&part, sizeof(double) * (size_t)chunks * ns * ns) != cudaSuccess) ||
       cudaMalloc(&G, sizeof(double) * (size_t)ns * ns) != cudaSuccess) {
     cleanup();
     return HYDRO_ERR_CUDA;
   }
-  // G = S S^T (the snapshot Gram matrix; S holds one snapshot per row)
-  hk::gram_partial_kernel<<<dim3((unsigned)chunks, (unsigned)tiles, (unsigned)tiles), hk::GRAM_T * hk::GRAM_T, 0, s>>>(
-      ns, N, chunk, N, 1, S, part);
-  hk::gram_reduce_kernel<<<(ns * ns + 255) / 256, 256, 0, s>>>(ns, chunks, part, G);
-  g_launches += 2;
+  // G = S S^T (the snapshot Gram matrix; S holds one snapshot per row), on the FP64 tensor pipe
+  // when the snapshot count allows the tall basis formation below (ns <= 64), else the tiled
+  // FMA kernel
+  const bool mma = ns <= 64 && max_k <= 64;
+  if (mma) {
+    if (gram_mma(ns, N, N, true, S, G, s) != HYDRO_OK) { cleanup(); return HYDRO_ERR_CUDA; }
+  } else {
+    hk::gram_partial_kernel<<<dim3((unsigned)chunks, (unsigned)tiles, (unsigned)tiles), hk::GRAM_T * hk::GRAM_T, 0, s>>>(
+        ns, N, chunk, N, 1, S, part);
+    hk::gram_reduce_kernel<<<(ns * ns + 255) / 256, 256, 0, s>>>(ns, chunks, part, G);
+    g_launches += 2;
+  }
   std::vector<double> hG((size_t)ns * ns), lam, V;
   if (cudaGetLastError() != cudaSuccess ||
       cudaMemcpyAsync(hG.data(), G, sizeof(double) * hG.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -1873,8 +2012,12 @@ hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k
     cleanup();
     return HYDRO_ERR_CUDA;
   }
-  hk::snapshot_combine_kernel<<<blocks_for(N, 128), 128, 0, s>>>(ns, N, k, max_k, S, W, Phi);
-  g_launches++;
+  if (mma) {  // Phi = S^T W on the tensor pipe (A read transposed from the snapshot rows)
+    if (tall_mma<true>(N, ns, k, S, N, W, Phi, max_k, s) != HYDRO_OK) { cleanup(); return HYDRO_ERR_CUDA; }
+  } else {
+    hk::snapshot_combine_kernel<<<blocks_for(N, 128), 128, 0, s>>>(ns, N, k, max_k, S, W, Phi);
+    g_launches++;
+  }
   if (cudaGetLastError() != cudaSuccess) { cleanup(); return HYDRO_ERR_CUDA; }
   // One CholQR pass: the Gram route leaves Phi orthonormal only to ~eps (sigma_1/sigma_k)^2;
   // Phi <- Phi R^-1 with R^T R = Phi^T Phi restores it to rounding (same span).
@@ -1884,11 +2027,15 @@ hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k
     const int ch = (int)std::min<int64_t>(hk::GRAM_CHUNKS, (N + hk::GRAM_KT - 1) / hk::GRAM_KT);
     const int64_t chs = (N + ch - 1) / ch;
     const int kt = (k + hk::GRAM_T - 1) / hk::GRAM_T;
-    bool ok = cudaMalloc(&P2, sizeof(double) * (size_t)ch * k * k) == cudaSuccess &&
+    bool ok = (mma || cudaMalloc(&P2, sizeof(double) * (size_t)ch * k * k) == cudaSuccess) &&
               cudaMalloc(&G2, sizeof(double) * (size_t)k * k) == cudaSuccess &&
               cudaMalloc(&Rinv, sizeof(double) * (size_t)k * k) == cudaSuccess;
     std::vector<double> C((size_t)k * k, 0.0), Ri((size_t)k * k, 0.0);
-    if (ok) {  // Phi^T Phi: the same tiled Gram kernel on the columns of the row-major basis
+    if (ok && mma) {  // Phi^T Phi on the tensor pipe (the basis columns)
+      ok = gram_mma(k, N, max_k, false, Phi, G2, s) == HYDRO_OK &&
+           cudaMemcpyAsync(C.data(), G2, sizeof(double) * C.size(), cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+           cudaStreamSynchronize(s) == cudaSuccess;
+    } else if (ok) {  // Phi^T Phi: the same tiled Gram kernel on the columns of the row-major basis
       hk::gram_partial_kernel<<<dim3((unsigned)ch, (unsigned)kt, (unsigned)kt), hk::GRAM_T * hk::GRAM_T, 0, s>>>(
           k, N, chs, 1, max_k, Phi, P2);
       hk::gram_reduce_kernel<<<(k * k + 255) / 256, 256, 0, s>>>(k, ch, P2, G2);
@@ -1921,8 +2068,12 @@ hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k
     }
     if (ok) {
       ok = cudaMemcpyAsync(Rinv, Ri.data(), sizeof(double) * Ri.size(), cudaMemcpyHostToDevice, s) == cudaSuccess;
-      hk::right_mult_kernel<<<blocks_for(N, 128), 128, 0, s>>>(N, k, max_k, Rinv, Phi);
-      g_launches++;
+      if (mma) {  // Phi <- Phi R^-1 in place on the tensor pipe
+        ok = ok && tall_mma<false>(N, k, k, Phi, max_k, Rinv, Phi, max_k, s) == HYDRO_OK;
+      } else {
+        hk::right_mult_kernel<<<blocks_for(N, 128), 128, 0, s>>>(N, k, max_k, Rinv, Phi);
+        g_launches++;
+      }
       ok = ok && cudaGetLastError() == cudaSuccess && cudaStreamSynchronize(s) == cudaSuccess;
     }
     cudaFree(P2); cudaFree(Rinv); cudaFree(G2);

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "rom_kernels.cuh"  // dmma_m8n8k4, project_mma_reduce_kernel
+
 namespace hk {
 
 constexpr int GRAM_T = 16;        // output tile (GRAM_T x GRAM_T per block)
@@ -303,6 +305,150 @@ __global__ void index_copy_add_kernel(int64_t n, int dim, const double *__restri
   const double v = src[c * ld_src + si];
   double *d = dst + c * ld_dst + di;
   *d = add ? *d + v : v;
+}
+
+// ------------------------------------------------------------------ FP64 tensor-pipe GEMMs
+// Gram matrices of the offline phase on the tensor pipe (DMMA m8n8k4): partial[c][i][j] =
+// sum over k in chunk c of A(i, k) A(j, k), A(i, k) = KFAST ? A[i * ld + k] (snapshots S [ns][N])
+// : A[k * ld + i] (the columns of a row-major basis Phi [N][ld]).  CTA (c, ti, tj) computes the
+// 64 x 64 output tile (ti, tj) over row chunk c in k-blocks of 32: every warp stages the eight
+// 8 x 4 fragments of one k-step into shared memory in fragment order (lane = row * 4 + k: each
+// lane's global load is one double of a fully used 32-byte sector; the fragment reads are
+// conflict-free LDS.64), the next k-block is loaded into registers while the current one is
+// multiplied; warp w owns m-tiles 2 (w & 3) .. + 1 and n-tiles 4 (w >> 2) .. + 3 (8 DMMAs per
+// k-step).  A B fragment (k x n8) of the Gram is the A fragment of n-tile nt, so a diagonal
+// tile stages one operand.  Partials are summed by project_mma_reduce_kernel in ascending
+// chunk order: deterministic.
+constexpr int GMMA_T = 64;     // output tile
+constexpr int GMMA_KB = 32;    // k-block (8 k-steps of 4)
+template <bool KFAST>
+__global__ void __launch_bounds__(256, 2)
+gram_mma_kernel(int n, int64_t N, int64_t chunk, int64_t ld, const double *__restrict__ A,
+                double *__restrict__ partial) {
+  __shared__ double sF[2][8 * 8 * 32];   // [operand][k-step][8-row tile][lane]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ti = blockIdx.y, tj = blockIdx.z;
+  const bool same = ti == tj;
+  const int64_t k0 = (int64_t)blockIdx.x * chunk;
+  const int64_t k1 = k0 + chunk < N ? k0 + chunk : N;
+  const int fr = lane >> 2, fk = lane & 3;
+  double ra[8], rb[8];
+  // warp w stages k-step w of a k-block: fragment (ks = w, tile q) = rows q*8 + fr, k = 4w + fk
+  auto load = [&](int64_t kb) {
+    const int64_t k = kb + warp * 4 + fk;
+    const bool kin = k < k1;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int i = ti * GMMA_T + q * 8 + fr, j = tj * GMMA_T + q * 8 + fr;
+      ra[q] = (kin && i < n) ? __ldg(KFAST ? A + (int64_t)i * ld + k : A + k * ld + i) : 0.0;
+      if (!same) rb[q] = (kin && j < n) ? __ldg(KFAST ? A + (int64_t)j * ld + k : A + k * ld + j) : 0.0;
+    }
+  };
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int mt0 = (warp & 3) * 2, nt0 = (warp >> 2) * 4;
+  if (k0 < k1) load(k0);
+  for (int64_t kb = k0; kb < k1; kb += GMMA_KB) {
+    __syncthreads();   // the previous k-block's fragment reads are done
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      sF[0][(warp * 8 + q) * 32 + lane] = ra[q];
+      if (!same) sF[1][(warp * 8 + q) * 32 + lane] = rb[q];
+    }
+    __syncthreads();
+    if (kb + GMMA_KB < k1) load(kb + GMMA_KB);
+    const double *fa = sF[0], *fb = same ? sF[0] : sF[1];
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const double a0 = fa[(ks * 8 + mt0) * 32 + lane], a1 = fa[(ks * 8 + mt0 + 1) * 32 + lane];
+      double b[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) b[t] = fb[(ks * 8 + nt0 + t) * 32 + lane];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        dmma_m8n8k4(acc[0][t][0], acc[0][t][1], a0, b[t]);
+        dmma_m8n8k4(acc[1][t][0], acc[1][t][1], a1, b[t]);
+      }
+    }
+  }
+  double *out = partial + (int64_t)blockIdx.x * n * n;
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const int i = ti * GMMA_T + (mt0 + a) * 8 + fr;
+    if (i >= n) continue;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int j = tj * GMMA_T + (nt0 + t) * 8 + 2 * fk;
+      if (j < n) out[(int64_t)i * n + j] = acc[a][t][0];
+      if (j + 1 < n) out[(int64_t)i * n + j + 1] = acc[a][t][1];
+    }
+  }
+}
+
+// out[r][c] = sum_k A(r, k) Y[k][c] for c < B <= 64, k < K <= 4 NKS, A(r, k) = AT ? A[k * lda + r]
+// (Phi = S^T W from the snapshots S [ns][N]) : A[r * lda + k] (Phi <- Phi R^-1); out row stride
+// ldo.  The lift kernel's scheme (lift_mma_kernel): persistent CTAs of 8 warps over 128-row
+// tiles, Y staged once per CTA in fragment order, each warp 2 m-tiles x 8 n-tiles.  A warp
+// reads all of its rows' A fragments before it writes any of its outputs and no other warp
+// touches those rows, so with !AT the call may be in place (out == A, ldo == lda): A and out
+// are deliberately not __restrict__.
+template <bool AT, int NKS>
+__global__ void __launch_bounds__(256, 2)
+tall_mma_kernel(int64_t rows, int K, int B, const double *A, int64_t lda,
+                const double *__restrict__ Y, double *out, int64_t ldo) {
+  __shared__ double sY[NKS * 8 * 32];   // [kstep][ntile][lane]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < NKS * 8 * 32; i += 256) {
+    const int l = i & 31, nt = (i >> 5) & 7, ks = i >> 8;
+    const int k = ks * 4 + (l & 3), c = nt * 8 + (l >> 2);
+    sY[i] = (k < K && c < B) ? Y[(int64_t)k * B + c] : 0.0;
+  }
+  __syncthreads();
+  const int64_t ntiles = (rows + 127) / 128;
+  const int ar = lane >> 2, ak = lane & 3;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t rw = t * 128 + warp * 16;
+    double a[2][NKS];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int64_t r = rw + mt * 8 + ar;
+#pragma unroll
+      for (int ks = 0; ks < NKS; ++ks) {
+        const int k = ks * 4 + ak;
+        a[mt][ks] = (r < rows && k < K) ? __ldg(AT ? A + (int64_t)k * lda + r : A + r * lda + k) : 0.0;
+      }
+    }
+    double acc[2][8][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < NKS; ++ks) {
+      double b[8];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) b[nt] = sY[(ks * 8 + nt) * 32 + lane];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) dmma_m8n8k4(acc[mt][nt][0], acc[mt][nt][1], a[mt][ks], b[nt]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int64_t r = rw + mt * 8 + ar;
+      if (r >= rows) continue;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const int c = nt * 8 + 2 * ak;
+        if (c < B) out[r * ldo + c] = acc[mt][nt][0];
+        if (c + 1 < B) out[r * ldo + c + 1] = acc[mt][nt][1];
+      }
+    }
+  }
 }
 
 }  // namespace hk
