@@ -1890,6 +1890,8 @@ struct Scratch {
   }
 };
 Scratch g_gram_scratch;
+Scratch g_deim_scratch;   // Q-DEIM / DEIM: transposed basis, norms, pivots
+void transpose(int64_t N, int64_t m, const double *A, double *At, cudaStream_t s);
 
 int sm_count() {
   static std::atomic<int> sms{0};
@@ -2179,9 +2181,59 @@ hydro_status mass_columns(hydro_fom *F, int field, int64_t N, int n, const doubl
 
 extern "C" {
 
+// Q-DEIM for m <= 64 by column-norm downdating (qdeim_dd_kernel): one read of U^T per pivot;
+// the transposed copy and the norms live in a per-device scratch kept between calls.
+static hydro_status qdeim_downdate(const double *U, int64_t N, int m, int64_t *idx, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_deim_scratch.mu);
+  double *buf = g_deim_scratch.get((size_t)N * m + 2 * (size_t)N + (size_t)m * m + 2 * hk::DEIM_BLOCKS);
+  if (!buf) return HYDRO_ERR_CUDA;
+  double *Ut = buf, *nu = Ut + (size_t)N * m, *nu0 = nu + N, *Q = nu0 + N, *bval = Q + (size_t)m * m;
+  int64_t *bidx = (int64_t *)(bval + hk::DEIM_BLOCKS);
+  transpose(N, m, U, Ut, s);
+  std::vector<double> hv(hk::DEIM_BLOCKS), row((size_t)m), hq((size_t)m * m);
+  std::vector<int64_t> hi(hk::DEIM_BLOCKS);
+  for (int k = 0; k < m; ++k) {
+    hk::qdeim_dd_kernel<64><<<hk::DEIM_BLOCKS, hk::DEIM_THREADS, 0, s>>>(N, m, k, Q, Ut, nu, nu0, bval, bidx);
+    g_launches++;
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(hv.data(), bval, sizeof(double) * hk::DEIM_BLOCKS, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(hi.data(), bidx, sizeof(int64_t) * hk::DEIM_BLOCKS, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return HYDRO_ERR_CUDA;
+    double best = -1.0;
+    int64_t p = -1;
+    for (int b = 0; b < hk::DEIM_BLOCKS; ++b)  // blocks cover ascending row ranges
+      if (hi[(size_t)b] >= 0 && hv[(size_t)b] > best) { best = hv[(size_t)b]; p = hi[(size_t)b]; }
+    if (p < 0 || !(best > 0.0)) return HYDRO_ERR_NONFINITE;
+    idx[k] = p;
+    if (k + 1 == m) break;
+    // q_k = the pivot row's residual (MGS against q_0 .. q_{k-1}), normalised
+    if (cudaMemcpyAsync(row.data(), U + p * m, sizeof(double) * m, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return HYDRO_ERR_CUDA;
+    for (int l = 0; l < k; ++l) {
+      const double *ql = hq.data() + (size_t)l * m;
+      double d = 0.0;
+      for (int j = 0; j < m; ++j) d = std::fma(row[(size_t)j], ql[j], d);
+      for (int j = 0; j < m; ++j) row[(size_t)j] = std::fma(-d, ql[j], row[(size_t)j]);
+    }
+    double n2 = 0.0;
+    for (int j = 0; j < m; ++j) n2 += row[(size_t)j] * row[(size_t)j];
+    if (!(n2 > 0.0)) return HYDRO_ERR_NONFINITE;
+    const double inv = 1.0 / std::sqrt(n2);
+    for (int j = 0; j < m; ++j) hq[(size_t)k * m + j] = row[(size_t)j] * inv;
+    if (cudaMemcpyAsync(Q + (size_t)k * m, hq.data() + (size_t)k * m, sizeof(double) * m, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return HYDRO_ERR_CUDA;
+    hk::mark_chosen_kernel<<<1, 1, 0, s>>>(nu, p);
+    g_launches++;
+  }
+  return cudaStreamSynchronize(s) == cudaSuccess ? HYDRO_OK : HYDRO_ERR_CUDA;
+}
+
 hydro_status hydro_qdeim(const double *U, int64_t N, int m, int64_t *idx, hydro_stream_t stream) {
   if (!U || N <= 0 || m <= 0 || m > N || m > 4096 || !idx) return HYDRO_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
+  if (m <= 64) return qdeim_downdate(U, N, m, idx, s);
   double *Rt = nullptr, *q = nullptr, *bval = nullptr;
   int64_t *bidx = nullptr;
   auto cleanup = [&]() { cudaFree(Rt); cudaFree(q); cudaFree(bval); cudaFree(bidx); };
@@ -2253,6 +2305,9 @@ hydro_status hydro_deim_oversampled(const double *U, int64_t N, int m, int n_s, 
     cleanup();
     return HYDRO_ERR_CUDA;
   }
+  // |residual| of the current column, kept for its further picks (scratch kept between calls)
+  std::unique_lock<std::mutex> lk(g_deim_scratch.mu);
+  double *absr = g_deim_scratch.get((size_t)N);
   std::vector<double> rows((size_t)n_s * m), hv(hk::DEIM_BLOCKS);
   std::vector<int64_t> hi(hk::DEIM_BLOCKS);
   const unsigned char one = 1;
@@ -2273,7 +2328,10 @@ hydro_status hydro_deim_oversampled(const double *U, int64_t N, int m, int n_s, 
     }
     const int n_add = n_s / m + (j < n_s % m ? 1 : 0);
     for (int t = 0; t < n_add; ++t) {  // the n_add largest |residual| rows outside I, in order
-      hk::deim_residual_kernel<<<hk::DEIM_BLOCKS, hk::DEIM_THREADS, 0, s>>>(N, m, j, U, c, bval, bidx, mask);
+      if (absr && t > 0)   // further picks of column j: arg-max of the kept |residual|
+        hk::argmax_masked_kernel<<<hk::DEIM_BLOCKS, hk::DEIM_THREADS, 0, s>>>(N, absr, mask, bval, bidx);
+      else
+        hk::deim_residual_kernel<<<hk::DEIM_BLOCKS, hk::DEIM_THREADS, 0, s>>>(N, m, j, U, c, bval, bidx, mask, absr);
       g_launches++;
       if (cudaGetLastError() != cudaSuccess ||
           cudaMemcpyAsync(hv.data(), bval, sizeof(double) * hk::DEIM_BLOCKS, cudaMemcpyDeviceToHost, s) != cudaSuccess ||

@@ -126,7 +126,7 @@ constexpr int DEIM_BLOCKS = 148 * 4, DEIM_THREADS = 256;
 __global__ void __launch_bounds__(DEIM_THREADS) deim_residual_kernel(
     int64_t N, int m, int j, const double *__restrict__ U, const double *__restrict__ c,
     double *__restrict__ bval, int64_t *__restrict__ bidx,
-    const unsigned char *__restrict__ mask = nullptr) {
+    const unsigned char *__restrict__ mask = nullptr, double *__restrict__ absr = nullptr) {
   __shared__ double sv[DEIM_THREADS];
   __shared__ int64_t si[DEIM_THREADS];
   const int64_t chunk = (N + DEIM_BLOCKS - 1) / DEIM_BLOCKS;
@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(DEIM_THREADS) deim_residual_kernel(
     double acc = 0.0;
     for (int i = 0; i < j; ++i) acc = __fma_rn(row[i], c[i], acc);
     const double v = fabs(row[j] - acc);
+    if (absr) absr[r] = v;   // kept for the oversampled greedy's further picks of column j
     if (v > best) { best = v; bi = r; }   // ascending r per thread: first maximum kept
   }
   sv[threadIdx.x] = best;
@@ -449,6 +450,117 @@ tall_mma_kernel(int64_t rows, int K, int B, const double *A, int64_t lda,
       }
     }
   }
+}
+
+// Q-DEIM by column-norm downdating (the pivoted QR of U^T the way LAPACK's geqp3 tracks its
+// column norms): nu[r] = |u_r|^2 - sum_{l<k} (q_l . u_r)^2 is the squared norm of row r's
+// residual after k pivots (q_l: the orthonormalised pivot residuals), so a step reads each row
+// once (Ut column-major [m][N], coalesced) and updates nu in place -- no residual matrix is
+// rewritten.  Where the downdate cancels (nu <= sqrt(eps) nu0, nu0 the original norm) the
+// row's residual norm is recomputed from u_r against all k+1 directions Q [k+1][m] (MGS order,
+// as geqp3 recomputes).  Chosen rows carry nu = -1 and are never picked again.  step == 0:
+// nu = nu0 = |u_r|^2.  Block-wise arg-max of nu (ties: the lowest row) into (bval, bidx).
+// |u_r - sum_{l<k} q_l (q_l . res)|^2 by modified Gram-Schmidt against Q [k][m] (m <= 64);
+// out of line so that its 64-entry row does not raise the register count of the main loop
+__device__ __noinline__ double qdeim_recompute(const double *__restrict__ Ut, int64_t N, int m, int64_t r,
+                                               const double *__restrict__ Q, int k) {
+  double u[64];
+  for (int j = 0; j < m; ++j) u[j] = Ut[(int64_t)j * N + r];
+  for (int l = 0; l < k; ++l) {
+    const double *ql = Q + (int64_t)l * m;
+    double d = 0.0;
+    for (int j = 0; j < m; ++j) d = __fma_rn(u[j], ql[j], d);
+    for (int j = 0; j < m; ++j) u[j] = __fma_rn(-d, ql[j], u[j]);
+  }
+  double n2 = 0.0;
+  for (int j = 0; j < m; ++j) n2 = __fma_rn(u[j], u[j], n2);
+  return n2;
+}
+
+template <int M>
+__global__ void __launch_bounds__(DEIM_THREADS) qdeim_dd_kernel(
+    int64_t N, int m, int step, const double *__restrict__ Q, const double *__restrict__ Ut,
+    double *__restrict__ nu, double *__restrict__ nu0, double *__restrict__ bval,
+    int64_t *__restrict__ bidx) {
+  __shared__ double sv[DEIM_THREADS];
+  __shared__ int64_t si[DEIM_THREADS];
+  __shared__ double sq[M];
+  const double *qk = Q + (int64_t)(step > 0 ? step - 1 : 0) * m;   // the newest direction
+  for (int j = threadIdx.x; j < M; j += DEIM_THREADS) sq[j] = (step > 0 && j < m) ? qk[j] : 0.0;
+  __syncthreads();
+  const int64_t chunk = (N + DEIM_BLOCKS - 1) / DEIM_BLOCKS;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < N ? lo + chunk : N;
+  const double tol = 1.4901161193847656e-08;   // sqrt(DBL_EPSILON)
+  double best = -1.0;
+  int64_t bi = -1;
+  for (int64_t r = lo + threadIdx.x; r < hi; r += DEIM_THREADS) {
+    double n2;
+    if (step == 0) {
+      n2 = 0.0;
+#pragma unroll 8
+      for (int j = 0; j < m; ++j) {
+        const double v = Ut[(int64_t)j * N + r];
+        n2 = __fma_rn(v, v, n2);
+      }
+      nu0[r] = n2;
+    } else {
+      n2 = nu[r];
+      if (n2 < 0.0) continue;   // chosen
+      double c = 0.0;
+#pragma unroll 8
+      for (int j = 0; j < m; ++j) c = __fma_rn(Ut[(int64_t)j * N + r], sq[j], c);
+      n2 = n2 - c * c;
+      const double n0 = nu0[r];
+      if (!(n2 > tol * n0)) n2 = n0 > 0.0 ? qdeim_recompute(Ut, N, m, r, Q, step) : 0.0;   // cancellation
+    }
+    nu[r] = n2;
+    if (n2 > best) { best = n2; bi = r; }   // ascending r per thread: first maximum kept
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int w = DEIM_THREADS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const double a = sv[threadIdx.x], b = sv[threadIdx.x + w];
+      const int64_t ia = si[threadIdx.x], ib = si[threadIdx.x + w];
+      if (b > a || (b == a && ib >= 0 && (ia < 0 || ib < ia))) { sv[threadIdx.x] = b; si[threadIdx.x] = ib; }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { bval[blockIdx.x] = sv[0]; bidx[blockIdx.x] = si[0]; }
+}
+
+__global__ void mark_chosen_kernel(double *nu, int64_t p) { nu[p] = -1.0; }
+
+// block-wise arg-max of stored |res| over the rows outside the mask (ties: the lowest row)
+__global__ void __launch_bounds__(DEIM_THREADS) argmax_masked_kernel(
+    int64_t N, const double *__restrict__ absr, const unsigned char *__restrict__ mask,
+    double *__restrict__ bval, int64_t *__restrict__ bidx) {
+  __shared__ double sv[DEIM_THREADS];
+  __shared__ int64_t si[DEIM_THREADS];
+  const int64_t chunk = (N + DEIM_BLOCKS - 1) / DEIM_BLOCKS;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < N ? lo + chunk : N;
+  double best = -1.0;
+  int64_t bi = -1;
+  for (int64_t r = lo + threadIdx.x; r < hi; r += DEIM_THREADS) {
+    if (mask[r]) continue;
+    const double v = absr[r];
+    if (v > best) { best = v; bi = r; }
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int w = DEIM_THREADS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const double a = sv[threadIdx.x], b = sv[threadIdx.x + w];
+      const int64_t ia = si[threadIdx.x], ib = si[threadIdx.x + w];
+      if (b > a || (b == a && ib >= 0 && (ia < 0 || ib < ia))) { sv[threadIdx.x] = b; si[threadIdx.x] = ib; }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { bval[blockIdx.x] = sv[0]; bidx[blockIdx.x] = si[0]; }
 }
 
 }  // namespace hk
