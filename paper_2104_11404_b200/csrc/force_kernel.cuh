@@ -58,6 +58,12 @@ enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2, MODE_FTW = 3 };
 #ifndef S1PAD_K3
 #define S1PAD_K3 0
 #endif
+// 3D Q2 (K = 2) bank-conflict layouts of the contraction stage buffers (r02; tools/bank_sim.py):
+// 1 = padded strides and a q1-fastest stage-2 task order (modelled shared wavefronts per unit
+// 756 -> 666), Wb / f2 placed over the dead point stresses; 0 = the round-1 layout.
+#ifndef LAYOUT_K2
+#define LAYOUT_K2 1
+#endif
 
 template <int DIM_, int K_, int Q_, int NF_, int EPB_ = 0>
 struct Geo {
@@ -79,14 +85,29 @@ struct Geo {
   // (unpadded: 3-way conflicts, 80 wavefronts per 7 warps instead of 38; ideal 28)
   static constexpr int S2Q1 = (DIM == 3 && K == 3) ? Q * N + S2PAD_K3 : Q * N;
   static constexpr int S2 = DIM == 3 ? Q * S2Q1 : 0;             // one stage-2 block
+  static constexpr bool LK2 = DIM == 3 && K == 2 && LAYOUT_K2;
+  // K = 2 layout (modelled wavefronts per unit 756 -> 666 within +24 doubles, which keeps the
+  // 196 KB shared carve-out at 14 CTAs/SM -- a wider padding (-17 %, +386 doubles) pushed the
+  // carve-out to 228 KB and cost C4 9 % through the smaller L1): stage-1 fc stride 73 (was 72),
+  // stage-2 fc stride 147 (was 144), Tb c stride 50 (was 48), Wb [w: 162][c: 54][a2 a3: 6][q1]
+  static constexpr int S1Q1X = S1Q1;                              // stage-1 q1 stride
+  static constexpr int S1X = DIM == 3 ? Q * S1Q1X : S1;           // stage-1 B|G stride
+  static constexpr int S1FC = LK2 ? 2 * S1X + 1 : 2 * S1X;        // stage-1 fc stride
+  static constexpr int S2FC = LK2 ? 3 * S2 + 3 : 3 * S2;          // stage-2 fc stride
+  static constexpr int S1TOT = DIM == 3 ? NF * DIM * S1FC : NF * DIM * 2 * S1;
+  static constexpr int S2TOT = DIM == 3 ? NF * DIM * S2FC : 0;
+  static constexpr int TA3 = Q, TQ1 = Q * N, TC = LK2 ? Q * Q * N + 2 : Q * Q * N, TDL = DIM * TC;
+  static constexpr int WA = LK2 ? 6 : Q, WC = LK2 ? 54 : N * N * Q, WW = LK2 ? 162 : DIM * N * N * Q;
   static constexpr int E1 = DIM == 3 ? Q * M * M : Q * M;
   static constexpr int E2 = DIM == 3 ? Q * Q * M : 0;
-  static constexpr int FWD = NF * DIM * 2 * S1 + NF * DIM * 3 * S2 + E1 + E2;
-  static constexpr int TB = DIM == 3 ? DIM * DIM * Q * Q * N : DIM * DIM * Q * N;
-  static constexpr int WB = DIM == 3 ? 2 * DIM * Q * N * N : 0;
+  static constexpr int FWD = S1TOT + S2TOT + E1 + E2;
+  static constexpr int TB = DIM == 3 ? DIM * TDL : DIM * DIM * Q * N;
+  static constexpr int WB = DIM == 3 ? 2 * WW : 0;
   static constexpr int F1B = DIM == 3 ? Q * Q * M : Q * M;
   static constexpr int F2B = DIM == 3 ? Q * M * M : 0;
-  static constexpr int BWD = DIM * DIM * NQ + NQ + TB + WB + F1B + F2B;
+  // LK2: Wb and f2 live over the point stresses S_q (dead once b1 has read them)
+  static_assert(!LK2 || WB + F2B <= DIM * DIM * NQ, "LK2 Wb placement");
+  static constexpr int BWD = DIM * DIM * NQ + NQ + TB + F1B + (LK2 ? 0 : WB + F2B);
   // SEPS (3D Q3 and larger): the point stresses S_q, A_q get their own region after the
   // forward buffers, so they can be written without waiting for every warp to finish its
   // forward reads (one barrier fewer per element); the backward work arrays still overlap
@@ -667,8 +688,8 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
   using G = Geo<DIM, K, Q, NF>;
   constexpr int N = G::N, M = G::M;
   if (DIM == 3) {
-    const double *S2b = Wk + G::NF * DIM * 2 * G::S1;    // [NF*DIM][3][Q][S2Q1: Q][N]
-    const double *E2b = S2b + G::NF * DIM * 3 * G::S2 + G::E1;  // [Q][Q][M]
+    const double *S2b = Wk + G::S1TOT;                   // [NF*DIM: S2FC][3][Q][S2Q1: Q][N]
+    const double *E2b = S2b + G::S2TOT + G::E1;          // [Q][Q][M]
     double tB[N], tG[N];
 #pragma unroll
     for (int a3 = 0; a3 < N; ++a3) { tB[a3] = sB[q3i * N + a3]; tG[a3] = sG[q3i * N + a3]; }
@@ -677,9 +698,9 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
 #pragma unroll
       for (int c = 0; c < DIM; ++c) {
         const int fc = f * DIM + c;
-        const double *p1 = S2b + (fc * 3 + 0) * G::S2 + q1i * G::S2Q1 + q2i * N;
-        const double *p2 = S2b + (fc * 3 + 1) * G::S2 + q1i * G::S2Q1 + q2i * N;
-        const double *p3 = S2b + (fc * 3 + 2) * G::S2 + q1i * G::S2Q1 + q2i * N;
+        const double *p1 = S2b + fc * G::S2FC + 0 * G::S2 + q1i * G::S2Q1 + q2i * N;
+        const double *p2 = S2b + fc * G::S2FC + 1 * G::S2 + q1i * G::S2Q1 + q2i * N;
+        const double *p3 = S2b + fc * G::S2FC + 2 * G::S2 + q1i * G::S2Q1 + q2i * N;
         double d0, d1, d2;
         if constexpr (N % 2 == 0 && FP_VEC) {   // 16-byte aligned pencils: LDS.128
           double v1[N], v2[N], v3[N];
@@ -1054,9 +1075,9 @@ force_kernel(const Params P) {
   else { q1i = lq % Q; q2i = (lq / Q) % Q; q3i = lq / (Q * Q); }
 
   if (DIM == 3) {
-    double *S1b = Wk;                              // [NF*DIM][2][Q][S1Q1: N][N]
-    double *S2b = Wk + G::NF * DIM * 2 * G::S1;    // [NF*DIM][3][Q][S2Q1: Q][N]
-    double *E1b = S2b + G::NF * DIM * 3 * G::S2;   // [Q][M][M]
+    double *S1b = Wk;                              // [NF*DIM: S1FC][2: S1X][Q: S1Q1X][N][N]
+    double *S2b = Wk + G::S1TOT;                   // [NF*DIM: S2FC][3][Q][S2Q1: Q][N]
+    double *E1b = S2b + G::S2TOT;                  // [Q][M][M]
     double *E2b = E1b + G::E1;                     // [Q][Q][M]
     using CT = CTab<K, Q>;
     if (u < EPB) {
@@ -1082,8 +1103,8 @@ force_kernel(const Params P) {
           for (int a1 = 0; a1 < N; ++a1) x[a1] = src[a1];
         }
         // S1b layout [fc][B|G][q1][a3][a2] (a2 fastest: stage 2 reads its pencils contiguously)
-        double *dB = S1b + (fc * 2 + 0) * G::S1 + a3 * N + a2;
-        double *dG = S1b + (fc * 2 + 1) * G::S1 + a3 * N + a2;
+        double *dB = S1b + fc * G::S1FC + a3 * N + a2;
+        double *dG = S1b + fc * G::S1FC + G::S1X + a3 * N + a2;
         part_dispatch<SP1>(t / T1, [&](auto pc) {
           constexpr int part = decltype(pc)::value;
 #pragma unroll (K3UQ)
@@ -1095,8 +1116,8 @@ force_kernel(const Params P) {
               ab = __fma_rn(CT::B(q1, a1), x[a1], ab);
               ag = __fma_rn(CT::G(q1, a1), x[a1], ag);
             }
-            dB[q1 * G::S1Q1] = ab;
-            dG[q1 * G::S1Q1] = ag;
+            dB[q1 * G::S1Q1X] = ab;
+            dG[q1 * G::S1Q1X] = ag;
           }
         });
       }
@@ -1125,14 +1146,16 @@ force_kernel(const Params P) {
       static_assert(Q % SP2 == 0, "SPLIT_F2 must divide Q");
       for (int t = lt; t < T2 * SP2; t += NQ) {
         const int t2 = t % T2;
-        const int a3 = t2 % N, r = t2 / N;
-        const int q1 = r % Q, fc = r / Q;
-        const double *pB = S1b + (fc * 2 + 0) * G::S1 + q1 * G::S1Q1 + a3 * N;
-        const double *pG = S1b + (fc * 2 + 1) * G::S1 + q1 * G::S1Q1 + a3 * N;
+        // LK2: q1 fastest over the lanes (conflict-free stage-2 stores with the padded strides)
+        const int a3 = G::LK2 ? (t2 / Q) % N : t2 % N;
+        const int q1 = G::LK2 ? t2 % Q : (t2 / N) % Q;
+        const int fc = t2 / (Q * N);
+        const double *pB = S1b + fc * G::S1FC + q1 * G::S1Q1X + a3 * N;
+        const double *pG = pB + G::S1X;
         double uB[N], uG[N];
 #pragma unroll
         for (int a2 = 0; a2 < N; ++a2) { uB[a2] = pB[a2]; uG[a2] = pG[a2]; }
-        double *dst = S2b + (fc * 3) * G::S2 + q1 * G::S2Q1 + a3;
+        double *dst = S2b + fc * G::S2FC + q1 * G::S2Q1 + a3;
         part_dispatch<SP2>(t / T2, [&](auto pc) {
           constexpr int part = decltype(pc)::value;
 #pragma unroll (K3UQ)
@@ -1375,9 +1398,9 @@ force_kernel(const Params P) {
   double *Ss = G::SEPS ? Wk + G::FWD : Wk;  // [DIM*DIM][NQ]
   double *As = Ss + DIM * DIM * NQ;         // [NQ]
   double *Tb = G::SEPS ? Wk : As + NQ;
-  double *Wb = Tb + G::TB;
-  double *F1b = Wb + G::WB;
-  double *F2b = F1b + G::F1B;
+  double *F1b = G::LK2 ? Tb + G::TB : Tb + G::TB + G::WB;
+  double *Wb = G::LK2 ? Ss : Tb + G::TB;          // LK2: over the dead point stresses
+  double *F2b = G::LK2 ? Ss + G::WB : F1b + G::F1B;
   // (the __syncthreads above separates the last forward read from these writes)
   // 3D Q3: point stresses stored [c][d][q1][q2][q3] (q3 fastest: the b1 / f1 pencils over q3
   // are contiguous; C3 -1 %); Q2 and 2D: [c][d][q] with q = q1 + Q q2 (+ Q^2 q3) -- for Q = 4
@@ -1414,14 +1437,14 @@ force_kernel(const Params P) {
 #pragma unroll
             for (int q3 = 0; q3 < Q; ++q3) sv[q3] = src[SQ3 ? q3 : q3 * Q * Q];
             // Tb layout [dl][c][q1][a3][q2] (q2 fastest: b2 reads its pencils contiguously)
-            double *dst = Tb + ((dl * DIM + c) * Q + q1) * Q * N + q2;
+            double *dst = Tb + dl * G::TDL + c * G::TC + q1 * G::TQ1 + q2;
 #pragma unroll (K3UB1)
             for (int a3 = 0; a3 < N; ++a3) {
               double acc = 0.0;
 #pragma unroll
               for (int q3 = 0; q3 < Q; ++q3)
                 acc = __fma_rn(dl == 2 ? CT::G(q3, a3) : CT::B(q3, a3), sv[q3], acc);
-              dst[a3 * Q] = acc;
+              dst[a3 * G::TA3] = acc;
             }
           }
         });
@@ -1451,15 +1474,15 @@ force_kernel(const Params P) {
         const int tb = t % TB2;
         const int a3 = tb % N, r = tb / N;
         const int q1 = r % Q, c = r / Q;
-        const double *t0 = Tb + ((0 * DIM + c) * Q + q1) * Q * N + a3 * Q;
-        const double *t1 = Tb + ((1 * DIM + c) * Q + q1) * Q * N + a3 * Q;
-        const double *t2 = Tb + ((2 * DIM + c) * Q + q1) * Q * N + a3 * Q;
+        const double *t0 = Tb + 0 * G::TDL + c * G::TC + q1 * G::TQ1 + a3 * G::TA3;
+        const double *t1 = Tb + 1 * G::TDL + c * G::TC + q1 * G::TQ1 + a3 * G::TA3;
+        const double *t2 = Tb + 2 * G::TDL + c * G::TC + q1 * G::TQ1 + a3 * G::TA3;
         double v0[Q], v1[Q], v2[Q];
 #pragma unroll
         for (int q2 = 0; q2 < Q; ++q2) { v0[q2] = t0[q2]; v1[q2] = t1[q2]; v2[q2] = t2[q2]; }
         // Wb layout [W1|W23][c][a2][a3][q1] (q1 fastest: b3 reads its pencils contiguously)
-        double *w1 = Wb + ((0 * DIM + c) * N * N + a3) * Q + q1;
-        double *w23 = Wb + ((1 * DIM + c) * N * N + a3) * Q + q1;
+        double *w1 = Wb + 0 * G::WW + c * G::WC + a3 * G::WA + q1;
+        double *w23 = Wb + 1 * G::WW + c * G::WC + a3 * G::WA + q1;
         part_dispatch<SB2>(t / TB2, [&](auto pc) {
           constexpr int part = decltype(pc)::value;
 #pragma unroll (K3UN)
@@ -1472,8 +1495,8 @@ force_kernel(const Params P) {
               acc23 = __fma_rn(CT::G(q2, a2), v1[q2], acc23);
               acc23 = __fma_rn(CT::B(q2, a2), v2[q2], acc23);
             }
-            w1[a2 * N * Q] = acc1;
-            w23[a2 * N * Q] = acc23;
+            w1[a2 * N * G::WA] = acc1;
+            w23[a2 * N * G::WA] = acc23;
           }
         });
       }
@@ -1504,8 +1527,8 @@ force_kernel(const Params P) {
         double w1v[Q], w23v[Q];
 #pragma unroll
         for (int q1 = 0; q1 < Q; ++q1) {
-          w1v[q1] = Wb[((0 * DIM + c) * N * N + a23) * Q + q1];
-          w23v[q1] = Wb[((1 * DIM + c) * N * N + a23) * Q + q1];
+          w1v[q1] = Wb[0 * G::WW + c * G::WC + a23 * G::WA + q1];
+          w23v[q1] = Wb[1 * G::WW + c * G::WC + a23 * G::WA + q1];
         }
         const int a2 = a23 / N, a3 = a23 % N;  // Wb index a2 * N + a3
         const int a0 = (a3 * N + a2) * N;      // node a = a1 + N a2 + N^2 a3
