@@ -128,6 +128,7 @@ struct Geo {
 struct Params {
   int32_t n_units;          // full: n_elem; batched: n_cl_elem * B
   int B;                    // instances (1 in full mode)
+  int b_shift;              // log2(B) when B is a power of two, else -1 (set by launch_force)
   int64_t ld_nodes;         // H1 component stride in nodes (n_nodes or n_cl_nodes)
   const int32_t *elem_nodes;  // [n_l][ND] node ids (closure-local in batched mode)
   const int32_t *elem_gid;    // batched: closure-local -> global element id; NULL = identity
@@ -157,6 +158,13 @@ struct Params {
   // MODE_FTW over compacted units: unit_elem[row] = the closure element of S0 row `row`.
   const int32_t *unit_elem;
 };
+
+// unit -> (element row, instance) of the batched layout unit = l * B + b: a shift for the usual
+// power-of-two instance counts (the signed division by a runtime B was ~2 % of all warp
+// instructions of the C4 kernel, computed twice per CTA)
+__device__ __forceinline__ int unit_row(const Params &P, int g) {
+  return P.b_shift >= 0 ? (int)((unsigned)g >> P.b_shift) : (int)((unsigned)g / (unsigned)P.B);
+}
 
 __device__ __forceinline__ int64_t s_index(const Params &P, int unit, int l, int b) {
   if (!P.ftw_row) return unit;
@@ -986,7 +994,7 @@ force_kernel(const Params P) {
     // barrier between the two), threads ND .. ND+NE-1 load the e dofs
     const int gu = unit0;
     if (gu < P.n_units) {
-      const int lr = BATCHED ? gu / B : gu;
+      const int lr = BATCHED ? unit_row(P, gu) : gu;
       const int l0 = P.unit_elem ? P.unit_elem[lr] : lr;
       const int b0 = BATCHED ? gu - lr * B : 0;
       if (tid < ND) {
@@ -1014,7 +1022,7 @@ force_kernel(const Params P) {
     const int gu = unit0 + uu;
     int nd = 0;
     if (gu < P.n_units) {
-      const int lr = BATCHED ? gu / B : gu;
+      const int lr = BATCHED ? unit_row(P, gu) : gu;
       nd = P.elem_nodes[(P.unit_elem ? P.unit_elem[lr] : lr) * ND + a];
     }
     snode[uu * ND + a] = nd;
@@ -1031,7 +1039,7 @@ force_kernel(const Params P) {
       const int gu = unit0 + uu;
       double val = 0.0;
       if (gu < P.n_units) {
-        const int b = BATCHED ? gu % B : 0;
+        const int b = BATCHED ? gu - unit_row(P, gu) * B : 0;
         const int64_t idx = ((int64_t)c * P.ld_nodes + snode[uu * ND + a]) * B + b;
         const double *src = NF == 1 ? P.x : (f == 0 ? P.x : (f == 1 ? P.v : P.w));
         val = __ldg(src + idx);
@@ -1044,7 +1052,7 @@ force_kernel(const Params P) {
         const int gu = unit0 + uu;
         double val = 0.0;
         if (gu < P.n_units) {
-          const int l = BATCHED ? gu / B : gu, b = BATCHED ? gu % B : 0;
+          const int l = BATCHED ? unit_row(P, gu) : gu, b = BATCHED ? gu - l * B : 0;
           val = __ldg(P.e + ((int64_t)l * NE + j) * B + b);
         }
         units[uu * G::UNIT + G::NF * DIM * ND + j] = val;
@@ -1061,9 +1069,9 @@ force_kernel(const Params P) {
   double *Es = U + G::NF * DIM * ND;      // [NE]
   double *Wk = Es + G::NEP;               // work region (16-byte aligned)
   const int gu = (unit0 + uc < P.n_units) ? unit0 + uc : 0;  // safe unit for reads
-  const int lraw = BATCHED ? gu / B : gu;  // element (or, over compacted units, S0 row)
+  const int lraw = BATCHED ? unit_row(P, gu) : gu;  // element (or, over compacted units, S0 row)
   const int l = P.unit_elem ? P.unit_elem[lraw] : lraw;
-  const int b = BATCHED ? gu % B : 0;
+  const int b = BATCHED ? gu - lraw * B : 0;
   const int gid = P.elem_gid ? P.elem_gid[l] : l;
 
   // --- S2 forward contractions (canonical order, DESIGN A.2)
@@ -1385,7 +1393,7 @@ force_kernel(const Params P) {
     }
   } else if (tid < EPB) {
     const int g2 = unit0 + tid;
-    if (g2 < P.n_units && skey[tid] != ~0ull) atomicMin(&P.st[g2 % B].dt_key, skey[tid]);
+    if (g2 < P.n_units && skey[tid] != ~0ull) atomicMin(&P.st[g2 - unit_row(P, g2) * B].dt_key, skey[tid]);
   }
   }
   if (MODE == MODE_DT) {

@@ -246,7 +246,11 @@ hydro_status launch_force_t(int mode, bool visc, bool batched, bool has_w, const
 }
 
 hydro_status launch_force(int dim, int k, int mode, bool visc, bool batched, bool has_w,
-                          const hk::Params &P, cudaStream_t s) {
+                          const hk::Params &P0, cudaStream_t s) {
+  hk::Params P = P0;
+  P.b_shift = -1;
+  for (int sh = 0; sh < 31; ++sh)
+    if (P.B == (1 << sh)) { P.b_shift = sh; break; }
   if (dim == 2 && k == 2) return launch_force_t<2, 2, 4>(mode, visc, batched, has_w, P, s);
   if (dim == 3 && k == 2) return launch_force_t<3, 2, 4>(mode, visc, batched, has_w, P, s);
   if (dim == 2 && k == 3) return launch_force_t<2, 3, 6>(mode, visc, batched, has_w, P, s);
