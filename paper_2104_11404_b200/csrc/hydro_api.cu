@@ -2092,15 +2092,13 @@ hydro_status hydro_pod(const double *S, int ns, int64_t N, double eps, int max_k
 hydro_status hydro_deim(const double *U, int64_t N, int m, int64_t *idx, hydro_stream_t stream) {
   if (!U || N <= 0 || m <= 0 || m > N || m > 4096 || !idx) return HYDRO_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  double *c = nullptr, *bval = nullptr;
-  int64_t *bidx = nullptr;
-  auto cleanup = [&]() { cudaFree(c); cudaFree(bval); cudaFree(bidx); };
-  if (cudaMalloc(&c, sizeof(double) * (size_t)m) != cudaSuccess ||
-      cudaMalloc(&bval, sizeof(double) * hk::DEIM_BLOCKS) != cudaSuccess ||
-      cudaMalloc(&bidx, sizeof(int64_t) * hk::DEIM_BLOCKS) != cudaSuccess) {
-    cleanup();
-    return HYDRO_ERR_CUDA;
-  }
+  // device scratch (kept between calls): c [m], block maxima [DEIM_BLOCKS], their rows
+  std::unique_lock<std::mutex> lk(g_deim_scratch.mu);
+  double *c = g_deim_scratch.get((size_t)m + 2 * hk::DEIM_BLOCKS);
+  if (!c) return HYDRO_ERR_CUDA;
+  double *bval = c + m;
+  int64_t *bidx = (int64_t *)(bval + hk::DEIM_BLOCKS);
+  auto cleanup = [&]() {};
   std::vector<double> rows((size_t)m * m), hv(hk::DEIM_BLOCKS), hc((size_t)m);
   std::vector<int64_t> hi(hk::DEIM_BLOCKS);
   hydro_status st = HYDRO_OK;
@@ -2298,20 +2296,16 @@ hydro_status hydro_deim_oversampled(const double *U, int64_t N, int m, int n_s, 
                                     hydro_stream_t stream) {
   if (!U || N <= 0 || m <= 0 || m > 4096 || n_s < m || n_s > N || n_s > 65536 || !idx) return HYDRO_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  double *c = nullptr, *bval = nullptr;
-  int64_t *bidx = nullptr;
-  unsigned char *mask = nullptr;
-  auto cleanup = [&]() { cudaFree(c); cudaFree(bval); cudaFree(bidx); cudaFree(mask); };
-  if (cudaMalloc(&c, sizeof(double) * (size_t)m) != cudaSuccess ||
-      cudaMalloc(&bval, sizeof(double) * hk::DEIM_BLOCKS) != cudaSuccess ||
-      cudaMalloc(&bidx, sizeof(int64_t) * hk::DEIM_BLOCKS) != cudaSuccess ||
-      cudaMalloc(&mask, (size_t)N) != cudaSuccess || cudaMemsetAsync(mask, 0, (size_t)N, s) != cudaSuccess) {
-    cleanup();
-    return HYDRO_ERR_CUDA;
-  }
-  // |residual| of the current column, kept for its further picks (scratch kept between calls)
+  // device scratch (kept between calls): |residual| of the current column (kept for its further
+  // picks) [N], c [m], block maxima and their rows [DEIM_BLOCKS], the chosen-row mask [N bytes]
   std::unique_lock<std::mutex> lk(g_deim_scratch.mu);
-  double *absr = g_deim_scratch.get((size_t)N);
+  double *absr = g_deim_scratch.get((size_t)N + m + 2 * hk::DEIM_BLOCKS + ((size_t)N + 7) / 8);
+  if (!absr) return HYDRO_ERR_CUDA;
+  double *c = absr + N, *bval = c + m;
+  int64_t *bidx = (int64_t *)(bval + hk::DEIM_BLOCKS);
+  unsigned char *mask = (unsigned char *)(bidx + hk::DEIM_BLOCKS);
+  if (cudaMemsetAsync(mask, 0, (size_t)N, s) != cudaSuccess) return HYDRO_ERR_CUDA;
+  auto cleanup = [&]() {};
   std::vector<double> rows((size_t)n_s * m), hv(hk::DEIM_BLOCKS);
   std::vector<int64_t> hi(hk::DEIM_BLOCKS);
   const unsigned char one = 1;
