@@ -154,7 +154,9 @@ hydro_status hydro_sample_lists(const hydro_sample *s, int32_t *closure_elems /*
  * Phi [rows][n] row-major, Y [n][B], out [rows][B].  Also serves the reduced position
  * RHS r_x = Phi_x^T v_os + (Phi_x^T Phi_v) Yhat_v with Phi = C_xv.  n <= 64,
  * B even and 16-byte aligned out (and batched os): the FP64 tensor pipe (mma.sync m8n8k4
- * f64); otherwise an FP64 FMA kernel (n <= 256).  Asynchronous; HYDRO_ERR_ARG on bad sizes. */
+ * f64); otherwise an FP64 FMA kernel (n <= 224: its shared-memory staging; larger n gives
+ * HYDRO_ERR_ARG).  rows = 0 is a no-op (the row pointers may
+ * be NULL).  Asynchronous; HYDRO_ERR_ARG on bad sizes.                                      */
 hydro_status hydro_rom_lift(int64_t rows, int n, int B, const double *Phi, const double *os,
                             int os_batched, const double *Y, double *out, hydro_stream_t stream);
 
@@ -189,7 +191,8 @@ hydro_status hydro_sample_status_sync(hydro_sample *s, hydro_stream_t stream,
  * n <= 64, B <= 64.  Deterministic split-K: fixed contiguous row ranges per CTA, partials
  * summed in a fixed order.  n <= 40: the FP64 tensor pipe (cp.async-staged operands for even
  * B, register-tiled otherwise); n > 40: FP64 FMA.  `workspace` (device) >=
- * hydro_rom_project_workspace_bytes, else HYDRO_ERR_WORKSPACE.  Asynchronous.              */
+ * hydro_rom_project_workspace_bytes, else HYDRO_ERR_WORKSPACE.  s_rows = 0 (an empty
+ * sample) sets r = 0 (P, f and the workspace may be NULL).  Asynchronous.                   */
 size_t hydro_rom_project_workspace_bytes(int n, int64_t s_rows, int B);
 hydro_status hydro_rom_project(int n, int64_t s_rows, int B, const double *P, const double *f,
                                double *r, void *workspace, size_t ws_bytes,

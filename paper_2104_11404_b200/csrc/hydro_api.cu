@@ -918,8 +918,9 @@ extern "C" {
 
 hydro_status hydro_rom_lift(int64_t rows, int n, int B, const double *Phi, const double *os,
                             int os_batched, const double *Y, double *out, hydro_stream_t stream) {
-  if (rows < 0 || n <= 0 || n > 256 || B <= 0 || !Phi || !os || !Y || !out) return HYDRO_ERR_ARG;
-  if (rows == 0) return HYDRO_OK;
+  if (rows < 0 || n <= 0 || n > 256 || B <= 0) return HYDRO_ERR_ARG;
+  if (rows == 0) return HYDRO_OK;   // nothing to lift (the row pointers may be NULL)
+  if (!Phi || !os || !Y || !out) return HYDRO_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   // the FP64 tensor-pipe kernel (n <= 64); os/out rows of 16-byte aligned pairs
   const bool aligned = ((uintptr_t)out % 16 == 0) && (!os_batched || (uintptr_t)os % 16 == 0) && B % 2 == 0;
@@ -931,15 +932,18 @@ hydro_status hydro_rom_lift(int64_t rows, int n, int B, const double *Phi, const
     if (nks <= 10) return launch_lift_mma<10>(rows, n, B, Phi, os, os_batched, Y, out, st);
     return launch_lift_mma<16>(rows, n, B, Phi, os, os_batched, Y, out, st);
   }
+  // the FMA kernel stages Y's column block and the Phi rows: (n LIFT_CB + LIFT_RT (n + 1))
+  // doubles, up to the device's opt-in maximum (n <= 224 on B200)
   const size_t smem = sizeof(double) * (size_t)(n * hk::LIFT_CB + hk::LIFT_RT * (n + 1));
   static std::atomic<unsigned long long> attr_done{0};
   if (smem > 48 * 1024) {
-    int dev = 0;
+    int dev = 0, optin = 0;
     CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (smem > (size_t)optin) return HYDRO_ERR_ARG;
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(attr_done.load() & bit)) {
-      CUDA_OK(cudaFuncSetAttribute(hk::lift_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(sizeof(double) * (256 * hk::LIFT_CB + hk::LIFT_RT * 257))));
+      CUDA_OK(cudaFuncSetAttribute(hk::lift_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
       attr_done.fetch_or(bit);
     }
   }
@@ -968,8 +972,12 @@ size_t hydro_rom_project_workspace_bytes(int n, int64_t s_rows, int B) {
 
 hydro_status hydro_rom_project(int n, int64_t s_rows, int B, const double *P, const double *f,
                                double *r, void *workspace, size_t ws_bytes, hydro_stream_t stream) {
-  if (n <= 0 || n > hk::PROJ_MAXN || B <= 0 || B > hk::PROJ_MAXB || s_rows < 0 || !P || !f || !r)
+  if (n <= 0 || n > hk::PROJ_MAXN || B <= 0 || B > hk::PROJ_MAXB || s_rows < 0 || !r)
     return HYDRO_ERR_ARG;
+  if (s_rows == 0)   // an empty sample: the empty sum (P and f may be NULL)
+    return cudaMemsetAsync(r, 0, sizeof(double) * (size_t)n * B, (cudaStream_t)stream) == cudaSuccess
+               ? HYDRO_OK : HYDRO_ERR_CUDA;
+  if (!P || !f) return HYDRO_ERR_ARG;
   const int G = project_groups(n, s_rows, B);
   if (!workspace || ws_bytes < sizeof(double) * (size_t)G * n * B) return HYDRO_ERR_WORKSPACE;
   int64_t chunk = std::max<int64_t>((s_rows + G - 1) / G, 1);

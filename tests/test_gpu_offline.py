@@ -42,7 +42,7 @@ def test_pod_known_svd_matches_oracle():
         _sig_close(sg, so)
         Pg = Phi_g.cpu().numpy()
         k = Pg.shape[1]
-        np.testing.assert_allclose(Pg.T @ Pg, np.eye(k), atol=1e-9)
+        np.testing.assert_allclose(Pg.T @ Pg, np.eye(k), atol=1e-12)
         good = so[:k] >= 1e-3 * so[0]
         np.testing.assert_allclose(Pg[:, good], Phi_o[:, good], atol=1e-8)
 
