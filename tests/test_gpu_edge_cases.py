@@ -89,3 +89,34 @@ def test_qdeim_cancellation_rows_match_lapack():
     ref = ooff.qdeim(U)
     np.testing.assert_array_equal(got, ref)
     assert len(set(got.tolist())) == m
+
+
+def test_qdeim_wide_basis_fallback_matches_lapack():
+    """m > 64 columns: the residual-rewriting Q-DEIM path (the downdating kernel keeps m <= 64)."""
+    rng = np.random.default_rng(70)
+    U, _ = np.linalg.qr(rng.standard_normal((3000, 70)))
+    U = np.ascontiguousarray(U)
+    np.testing.assert_array_equal(hydro.qdeim(H.dev(U)), ooff.qdeim(U))
+
+
+def test_pod_many_snapshots_fallback_matches_oracle():
+    """ns > 64 snapshots: the tiled FMA Gram / basis kernels (the tensor-pipe path takes
+    ns <= 64); singular values and the well-separated basis columns against the oracle's SVD,
+    orthonormal to 1e-12 after CholQR."""
+    rng = np.random.default_rng(80)
+    N, ns = 30_001, 80
+    Q1, _ = np.linalg.qr(rng.standard_normal((N, ns)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((ns, ns)))
+    sv = np.array([2.0 / 1.25 ** i for i in range(ns)])
+    S = np.ascontiguousarray(((Q1 * sv) @ Q2.T).T)
+    Phi_g, sg = hydro.pod(H.dev(S), eps=0.999)
+    Phi_o, so = ooff.pod(S, eps=0.999)
+    assert Phi_g.shape == Phi_o.shape
+    tol = 1e-13 * so[0] ** 2 / np.maximum(so, 1e-300) + 1e-12 * so
+    assert np.all(np.abs(sg - so) <= tol)
+    P = Phi_g.cpu().numpy()
+    k = P.shape[1]
+    assert np.abs(P.T @ P - np.eye(k)).max() <= 1e-12
+    good = so[:k] >= 1e-3 * so[0]
+    Pg, Po = P[:, good], Phi_o[:, good]
+    assert np.abs(Pg - Po).max() <= 1e-8
