@@ -64,6 +64,10 @@ enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2, MODE_FTW = 3 };
 #ifndef LAYOUT_K2
 #define LAYOUT_K2 1
 #endif
+// 3D Q3: bank-conflict-avoiding order of the stage-2 tasks (see the stage-2 loop); 0 = plain order
+#ifndef PERM_K3
+#define PERM_K3 1
+#endif
 
 template <int DIM_, int K_, int Q_, int NF_, int EPB_ = 0>
 struct Geo {
@@ -1155,9 +1159,25 @@ force_kernel(const Params P) {
       for (int t = lt; t < T2 * SP2; t += NQ) {
         const int t2 = t % T2;
         // LK2: q1 fastest over the lanes (conflict-free stage-2 stores with the padded strides)
-        const int a3 = G::LK2 ? (t2 / Q) % N : t2 % N;
-        const int q1 = G::LK2 ? t2 % Q : (t2 / N) % Q;
-        const int fc = t2 / (Q * N);
+        int a3 = G::LK2 ? (t2 / Q) % N : t2 % N;
+        int q1 = G::LK2 ? t2 % Q : (t2 / N) % Q;
+        int fc = t2 / (Q * N);
+        if constexpr (PERM_K3 && K == 3 && G::NF * DIM == 6 && N == 4 && Q == 6) {
+          // Q3: each half-warp takes four (fc, q1) pencils whose stage-2 store offsets are
+          // {0, 4, 8, 12} mod 16 doubles (fc stride 540, q1 stride 30): four consecutive fc of
+          // one q1, then {4, 5} x {q1, q1 + 4} for q1 = 0, 1, then {4, 5} x {2, 3}
+          // (modelled stage-2 store wavefronts per element 324 -> 180, tools/bank_sim.py)
+          const int pc = t2 >> 2;
+          a3 = t2 & 3;
+          if (pc < 24) {
+            q1 = pc >> 2;
+            fc = pc & 3;
+          } else {
+            const int r = pc - 24, g = r >> 2, wi = r & 3;
+            fc = 4 + (wi & 1);
+            q1 = g + (wi >> 1) * (g < 2 ? 4 : 1);
+          }
+        }
         const double *pB = S1b + fc * G::S1FC + q1 * G::S1Q1X + a3 * N;
         const double *pG = pB + G::S1X;
         double uB[N], uG[N];
