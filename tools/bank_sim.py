@@ -7,7 +7,8 @@ Wavefronts of one warp-wide shared access: 64-bit accesses run as two half-warp 
 "L1 Wavefronts Shared" of profiles/r02_q2_c4_force_full (stage-1 stores 56, stage-2 loads 54,
 stage-2 stores 108, b2 loads 54, b3 loads 28 per unit: all reproduced).
 
-    python tools/bank_sim.py        # the round-1 layout vs LAYOUT_K2 = 1
+    python tools/bank_sim.py        # Q2: the round-1 layout vs LAYOUT_K2 = 1;
+                                    # Q3: the stage-2 task order without / with PERM_K3
 """
 from collections import defaultdict
 
@@ -78,7 +79,33 @@ def backward(TDL, TC, TQ1, TA3, WW, WC, WA):
     return dict(b1_st=cost(48, b1s), b2_ld=cost(36, b2l, 16), b2_st=cost(36, b2s), b3_ld=cost(27, b3l, 16))
 
 
+def q3_stage2(perm):
+    """3D Q3 (N = 4, Q = 6, 224-thread CTAs) stage-2 loads (LDS.128) and stores, per element;
+    strides S1Q1 16, S1 96, fc 192 (stage 1), S2Q1 30, S2 180, fc 540 (stage 2)."""
+    global NT
+    nt, NT = NT, 224
+    try:
+        def dec(t):
+            if not perm:
+                return t // 24, (t // 4) % 6, t % 4
+            pc, a3 = t >> 2, t & 3
+            if pc < 24:
+                return pc & 3, pc >> 2, a3
+            r = pc - 24
+            g, wi = r >> 2, r & 3
+            return 4 + (wi & 1), g + (wi >> 1) * (4 if g < 2 else 1), a3
+        ld = [lambda t, bg=bg, k=k: (lambda fc, q1, a3: fc * 192 + bg * 96 + q1 * 16 + a3 * 4 + 2 * k)(*dec(t))
+              for bg in range(2) for k in range(2)]
+        st = [lambda t, k=k, q2=q2: (lambda fc, q1, a3: fc * 540 + k * 180 + q1 * 30 + q2 * 4 + a3)(*dec(t))
+              for k in range(3) for q2 in range(6)]
+        return dict(stage2_ld=cost(144, ld, 16), stage2_st=cost(144, st))
+    finally:
+        NT = nt
+
+
 def main():
+    for perm in (False, True):
+        print(f"Q3 stage 2, PERM_K3 = {int(perm)}: {q3_stage2(perm)}")
     for name, f, b in (("round-1 layout", (72, 36, 9, 144, 48, 12, "a3"), (144, 48, 12, 4, 108, 36, 4)),
                        ("LAYOUT_K2 = 1", (73, 36, 9, 147, 48, 12, "q1"), (150, 50, 12, 4, 162, 54, 6))):
         fw, bw = forward(*f), backward(*b)
