@@ -138,6 +138,21 @@ def test_full_size_3d_sampled_outputs(oracle_lib, name):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("name", ["c3", "tg"])
+def test_full_size_every_output(oracle_lib, name):
+    """C3 (3D Q3/Q2, 258 048 elements, the bench's launch configuration with the Q3 layouts and
+    task orders) and the Taylor-Green 64^3 workload: every assembled F.1 entry and every F^T.v
+    entry against the oracle's full-mesh evaluation, dt bit-exact."""
+    prob = W.config(name)
+    got = H.run_full(prob)
+    ref = oracle_lib.force(prob)
+    assert got["status"] == 0 and ref["status"] == 0
+    H.assert_close(got["F1"], ref["F1"], ref["F1mag"], H.TOL_ASSEMBLED, f"{name} F1 (all nodes)")
+    H.assert_close(got["FTw"], ref["FTw"], ref["FTwmag"], H.TOL_LOCAL, f"{name} FTw (all elements)")
+    assert H.dt_bitwise(got["dt"], ref["dt"]), (got["dt"], ref["dt"])
+
+
+@pytest.mark.slow
 def test_full_size_c2_every_output(oracle_lib):
     """C2 at its BASELINE.json size in the bench's launch configuration: every assembled F.1
     entry (all 2,146,689 nodes x 3) and every F^T.v entry against the oracle's full-mesh
