@@ -64,6 +64,9 @@ enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2, MODE_FTW = 3 };
 #ifndef LAYOUT_K2
 #define LAYOUT_K2 1
 #endif
+#ifndef XS_UNDER_K2
+#define XS_UNDER_K2 1
+#endif
 // 3D Q3: bank-conflict-avoiding order of the stage-2 tasks (see the stage-2 loop); 0 = plain order
 #ifndef PERM_K3
 #define PERM_K3 1
@@ -94,9 +97,13 @@ struct Geo {
   // 196 KB shared carve-out at 14 CTAs/SM -- a wider padding (-17 %, +386 doubles) pushed the
   // carve-out to 228 KB and cost C4 9 % through the smaller L1): stage-1 fc stride 73 (was 72),
   // stage-2 fc stride 147 (was 144), Tb c stride 50 (was 48), Wb [w: 162][c: 54][a2 a3: 6][q1]
-  static constexpr int S1Q1X = S1Q1;                              // stage-1 q1 stride
+  // XK2 (XS_UNDER_K2): the gathered dofs live inside the stage-2 span (dead once stage 1 has
+  // read them), which pays for a stage-1 q1 stride of 12 (conflict-free stage-2 pencil reads:
+  // modelled 54 -> 30 wavefronts per unit) at +22 doubles per unit
+  static constexpr bool XK2 = LK2 && XS_UNDER_K2;
+  static constexpr int S1Q1X = XK2 ? 12 : S1Q1;                   // stage-1 q1 stride
   static constexpr int S1X = DIM == 3 ? Q * S1Q1X : S1;           // stage-1 B|G stride
-  static constexpr int S1FC = LK2 ? 2 * S1X + 1 : 2 * S1X;        // stage-1 fc stride
+  static constexpr int S1FC = XK2 ? 2 * S1X + 9 : (LK2 ? 2 * S1X + 1 : 2 * S1X);  // stage-1 fc stride
   static constexpr int S2FC = LK2 ? 3 * S2 + 3 : 3 * S2;          // stage-2 fc stride
   static constexpr int S1TOT = DIM == 3 ? NF * DIM * S1FC : NF * DIM * 2 * S1;
   static constexpr int S2TOT = DIM == 3 ? NF * DIM * S2FC : 0;
@@ -122,7 +129,12 @@ struct Geo {
   // the work region starts 16-byte aligned (NEP: NE rounded up to even) so that stage outputs
   // can be read as double2 (LDS.128); every unit is an even number of doubles
   static constexpr int NEP = (NE + 1) & ~1;
-  static constexpr int UNIT = (NF * DIM * ND + NEP + WORK + 1) & ~1;
+  // unit layout: [gathered dofs Xs | e dofs | work] or, XK2, [work] with Xs, Es at XOFF (inside
+  // the stage-2 span: written by the gather, read by stage 1, overwritten by stage 2)
+  static constexpr int XOFF = XK2 ? S1TOT : 0;
+  static constexpr int WKOFF = XK2 ? 0 : NF * DIM * ND + NEP;
+  static_assert(!XK2 || NF * DIM * ND + NEP <= S2TOT, "XK2 placement");
+  static constexpr int UNIT = (WKOFF + WORK + 1) & ~1;
   static constexpr int TABD = Q + Q * N * 2 + Q * M;             // w, B, G, Bl
   static constexpr size_t SMEM =
       sizeof(double) * (size_t)(TABD + EPB * UNIT) + sizeof(int) * ((EPB * ND + 1) / 2 * 2) +
@@ -1010,14 +1022,14 @@ force_kernel(const Params P) {
           const double *src = NF == 1 ? P.x : (f == 0 ? P.x : (f == 1 ? P.v : P.w));
 #pragma unroll
           for (int c = 0; c < DIM; ++c)
-            units[(f * DIM + c) * ND + tid] = __ldg(src + ((int64_t)c * P.ld_nodes + nd) * B + b0);
+            units[G::XOFF + (f * DIM + c) * ND + tid] = __ldg(src + ((int64_t)c * P.ld_nodes + nd) * B + b0);
         }
       } else if (WANT_E && tid < ND + NE) {
         const int j = tid - ND;
-        units[G::NF * DIM * ND + j] = __ldg(P.e + ((int64_t)l0 * NE + j) * B + b0);
+        units[G::XOFF + G::NF * DIM * ND + j] = __ldg(P.e + ((int64_t)l0 * NE + j) * B + b0);
       }
     } else {
-      for (int i = tid; i < G::NF * DIM * ND + NE; i += NT) units[i] = 0.0;
+      for (int i = tid; i < G::NF * DIM * ND + NE; i += NT) units[G::XOFF + i] = 0.0;
     }
   } else {
   // node ids, then fields (unit fastest for coalescing across instances)
@@ -1048,7 +1060,7 @@ force_kernel(const Params P) {
         const double *src = NF == 1 ? P.x : (f == 0 ? P.x : (f == 1 ? P.v : P.w));
         val = __ldg(src + idx);
       }
-      units[uu * G::UNIT + (f * DIM + c) * ND + a] = val;
+      units[uu * G::UNIT + G::XOFF + (f * DIM + c) * ND + a] = val;
     }
     if (WANT_E) {
       for (int i = tid; i < EPB * NE; i += NT) {
@@ -1059,7 +1071,7 @@ force_kernel(const Params P) {
           const int l = BATCHED ? unit_row(P, gu) : gu, b = BATCHED ? gu - l * B : 0;
           val = __ldg(P.e + ((int64_t)l * NE + j) * B + b);
         }
-        units[uu * G::UNIT + G::NF * DIM * ND + j] = val;
+        units[uu * G::UNIT + G::XOFF + G::NF * DIM * ND + j] = val;
       }
     }
   }
@@ -1069,9 +1081,9 @@ force_kernel(const Params P) {
   const bool active = (u < EPB) && (unit0 + u < P.n_units) && (lt < NQ);
   const int uc = u < EPB ? u : EPB - 1;  // clamp pad threads onto a real unit buffer (reads only)
   double *U = units + uc * G::UNIT;
-  double *Xs = U;                         // [NF][DIM][ND]
-  double *Es = U + G::NF * DIM * ND;      // [NE]
-  double *Wk = Es + G::NEP;               // work region (16-byte aligned)
+  double *Xs = U + G::XOFF;               // [NF][DIM][ND]
+  double *Es = Xs + G::NF * DIM * ND;     // [NE]
+  double *Wk = U + G::WKOFF;              // work region (16-byte aligned)
   const int gu = (unit0 + uc < P.n_units) ? unit0 + uc : 0;  // safe unit for reads
   const int lraw = BATCHED ? unit_row(P, gu) : gu;  // element (or, over compacted units, S0 row)
   const int l = P.unit_elem ? P.unit_elem[lraw] : lraw;

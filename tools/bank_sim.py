@@ -107,7 +107,8 @@ def main():
     for perm in (False, True):
         print(f"Q3 stage 2, PERM_K3 = {int(perm)}: {q3_stage2(perm)}")
     for name, f, b in (("round-1 layout", (72, 36, 9, 144, 48, 12, "a3"), (144, 48, 12, 4, 108, 36, 4)),
-                       ("LAYOUT_K2 = 1", (73, 36, 9, 147, 48, 12, "q1"), (150, 50, 12, 4, 162, 54, 6))):
+                       ("LAYOUT_K2 = 1", (73, 36, 9, 147, 48, 12, "q1"), (150, 50, 12, 4, 162, 54, 6)),
+                       ("+ XS_UNDER_K2", (105, 48, 12, 147, 48, 12, "q1"), (150, 50, 12, 4, 162, 54, 6))):
         fw, bw = forward(*f), backward(*b)
         print(f"{name:16s} forward {fw} backward {bw} total {sum(fw.values()) + sum(bw.values())}")
 
