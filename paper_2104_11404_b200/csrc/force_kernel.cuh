@@ -67,6 +67,9 @@ enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2, MODE_FTW = 3 };
 #ifndef XS_UNDER_K2
 #define XS_UNDER_K2 1
 #endif
+#ifndef EJ_K2
+#define EJ_K2 1
+#endif
 // 3D Q3: bank-conflict-avoiding order of the stage-2 tasks (see the stage-2 loop); 0 = plain order
 #ifndef PERM_K3
 #define PERM_K3 1
@@ -758,11 +761,15 @@ __device__ __forceinline__ void forward_point(const double *sB, const double *sG
       }
     }
     if (WANT_E) {
+      // E2b: [q1][q2][j3], or [j3][q1][q2] for K = 2 (EJ_K2: a half-warp's 16 points read 16
+      // consecutive doubles, one wavefront instead of two)
+      constexpr bool EJ = G::LK2 && EJ_K2;
       const double *tb = sBl + q3i * M;
-      const double *src = E2b + (q1i * Q + q2i) * M;
+      const double *src = EJ ? E2b + q1i * Q + q2i : E2b + (q1i * Q + q2i) * M;
+      constexpr int ES = EJ ? Q * Q : 1;
       double acc = tb[0] * src[0];
 #pragma unroll
-      for (int j3 = 1; j3 < M; ++j3) acc = __fma_rn(tb[j3], src[j3], acc);
+      for (int j3 = 1; j3 < M; ++j3) acc = __fma_rn(tb[j3], src[j3 * ES], acc);
       eq = acc;
     }
   } else {
@@ -1226,7 +1233,8 @@ force_kernel(const Params P) {
             double acc = CT::Bl(q2, 0) * ev[0];
 #pragma unroll
             for (int j2 = 1; j2 < M; ++j2) acc = __fma_rn(CT::Bl(q2, j2), ev[j2], acc);
-            E2b[(q1 * Q + q2) * M + j3] = acc;
+            if constexpr (G::LK2 && EJ_K2) E2b[(j3 * Q + q1) * Q + q2] = acc;
+            else E2b[(q1 * Q + q2) * M + j3] = acc;
           }
         }
       }
