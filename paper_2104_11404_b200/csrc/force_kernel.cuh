@@ -70,6 +70,9 @@ enum Mode { MODE_FORCE = 0, MODE_DT = 1, MODE_MQ = 2, MODE_FTW = 3 };
 #ifndef EJ_K2
 #define EJ_K2 1
 #endif
+#ifndef S1FCPAD_K3
+#define S1FCPAD_K3 2
+#endif
 // 3D Q3: bank-conflict-avoiding order of the stage-2 tasks (see the stage-2 loop); 0 = plain order
 #ifndef PERM_K3
 #define PERM_K3 1
@@ -106,7 +109,11 @@ struct Geo {
   static constexpr bool XK2 = LK2 && XS_UNDER_K2;
   static constexpr int S1Q1X = XK2 ? 12 : S1Q1;                   // stage-1 q1 stride
   static constexpr int S1X = DIM == 3 ? Q * S1Q1X : S1;           // stage-1 B|G stride
-  static constexpr int S1FC = XK2 ? 2 * S1X + 9 : (LK2 ? 2 * S1X + 1 : 2 * S1X);  // stage-1 fc stride
+  // stage-1 fc stride: K = 2 as above; Q3 with the PERM_K3 stage-2 order: +2 doubles, so that the
+  // four consecutive fc of a half-warp read their stage-1 pencils from distinct banks (modelled
+  // stage-2 loads 144 -> 72 wavefronts per element)
+  static constexpr int S1FC = XK2 ? 2 * S1X + 9
+                                  : (LK2 ? 2 * S1X + 1 : (DIM == 3 && K == 3 && PERM_K3 ? 2 * S1X + S1FCPAD_K3 : 2 * S1X));
   static constexpr int S2FC = LK2 ? 3 * S2 + 3 : 3 * S2;          // stage-2 fc stride
   static constexpr int S1TOT = DIM == 3 ? NF * DIM * S1FC : NF * DIM * 2 * S1;
   static constexpr int S2TOT = DIM == 3 ? NF * DIM * S2FC : 0;
