@@ -117,7 +117,11 @@ struct Geo {
   static constexpr int S2FC = LK2 ? 3 * S2 + 3 : 3 * S2;          // stage-2 fc stride
   static constexpr int S1TOT = DIM == 3 ? NF * DIM * S1FC : NF * DIM * 2 * S1;
   static constexpr int S2TOT = DIM == 3 ? NF * DIM * S2FC : 0;
-  static constexpr int TA3 = Q, TQ1 = Q * N, TC = LK2 ? Q * Q * N + 2 : Q * Q * N, TDL = DIM * TC;
+  // Tb: XK2 leaves the backward region room under the forward one, so Tb takes the strides that
+  // make both the b1 stores and the b2 pencil reads conflict-free (with q1-fastest b2 tasks):
+  // [dl: 246][c: 82][q1: 20][a3: 6][q2]
+  static constexpr int TA3 = XK2 ? 6 : Q, TQ1 = XK2 ? 20 : Q * N,
+                       TC = XK2 ? 82 : (LK2 ? Q * Q * N + 2 : Q * Q * N), TDL = DIM * TC;
   static constexpr int WA = LK2 ? 6 : Q, WC = LK2 ? 54 : N * N * Q, WW = LK2 ? 162 : DIM * N * N * Q;
   static constexpr int E1 = DIM == 3 ? Q * M * M : Q * M;
   static constexpr int E2 = DIM == 3 ? Q * Q * M : 0;
@@ -144,6 +148,7 @@ struct Geo {
   static constexpr int XOFF = XK2 ? S1TOT : 0;
   static constexpr int WKOFF = XK2 ? 0 : NF * DIM * ND + NEP;
   static_assert(!XK2 || NF * DIM * ND + NEP <= S2TOT, "XK2 placement");
+  static_assert(!XK2 || NF != 2 || BWD <= FWD, "XK2: the backward region stays under the forward one");
   static constexpr int UNIT = (WKOFF + WORK + 1) & ~1;
   static constexpr int TABD = Q + Q * N * 2 + Q * M;             // w, B, G, Bl
   static constexpr size_t SMEM =
@@ -1527,8 +1532,9 @@ force_kernel(const Params P) {
       static_assert(N % SB2 == 0, "SPLIT_B2 must divide N");
       for (int t = lt; t < TB2 * SB2; t += NQ) {
         const int tb = t % TB2;
-        const int a3 = tb % N, r = tb / N;
-        const int q1 = r % Q, c = r / Q;
+        const int a3 = G::XK2 ? (tb / Q) % N : tb % N;   // XK2: q1 fastest over the lanes
+        const int q1 = G::XK2 ? tb % Q : (tb / N) % Q;
+        const int c = tb / (Q * N);
         const double *t0 = Tb + 0 * G::TDL + c * G::TC + q1 * G::TQ1 + a3 * G::TA3;
         const double *t1 = Tb + 1 * G::TDL + c * G::TC + q1 * G::TQ1 + a3 * G::TA3;
         const double *t2 = Tb + 2 * G::TDL + c * G::TC + q1 * G::TQ1 + a3 * G::TA3;

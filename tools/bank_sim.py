@@ -66,11 +66,14 @@ def forward(SFC, SBG, S1Q1, S2FC, S2K, S2Q1, order2):
     return dict(stage1_st=cost(T1, st1), stage2_ld=cost(T2, ld2), stage2_st=cost(T2, st2), fwd_point_ld=cost(64, fp))
 
 
-def backward(TDL, TC, TQ1, TA3, WW, WC, WA):
+def backward(TDL, TC, TQ1, TA3, WW, WC, WA, b2_q1fast=False):
     d1 = lambda t: (t // 16, (t % 16) % 4, (t % 16) // 4)                     # c, q1, q2
     b1s = [lambda t, dl=dl, a3=a3: (lambda c, q1, q2: dl * TDL + c * TC + q1 * TQ1 + a3 * TA3 + q2)(*d1(t))
            for dl in range(3) for a3 in range(N)]
-    d2 = lambda t: (t // 12, (t // 3) % 4, t % 3)                             # c, q1, a3
+    if b2_q1fast:
+        d2 = lambda t: (t // 12, t % 4, (t // 4) % 3)                         # c, q1, a3
+    else:
+        d2 = lambda t: (t // 12, (t // 3) % 4, t % 3)
     b2l = [lambda t, dl=dl, q2=q2: (lambda c, q1, a3: dl * TDL + c * TC + q1 * TQ1 + a3 * TA3 + q2)(*d2(t))
            for dl in range(3) for q2 in (0, 2)]
     b2s = [lambda t, w=w, a2=a2: (lambda c, q1, a3: w * WW + c * WC + (a2 * 3 + a3) * WA + q1)(*d2(t))
@@ -108,7 +111,7 @@ def main():
         print(f"Q3 stage 2, PERM_K3 = {int(perm)}: {q3_stage2(perm)}")
     for name, f, b in (("round-1 layout", (72, 36, 9, 144, 48, 12, "a3"), (144, 48, 12, 4, 108, 36, 4)),
                        ("LAYOUT_K2 = 1", (73, 36, 9, 147, 48, 12, "q1"), (150, 50, 12, 4, 162, 54, 6)),
-                       ("+ XS_UNDER_K2", (105, 48, 12, 147, 48, 12, "q1"), (150, 50, 12, 4, 162, 54, 6))):
+                       ("+ XS_UNDER_K2", (105, 48, 12, 147, 48, 12, "q1"), (246, 82, 20, 6, 162, 54, 6, True))):
         fw, bw = forward(*f), backward(*b)
         print(f"{name:16s} forward {fw} backward {bw} total {sum(fw.values()) + sum(bw.values())}")
 
