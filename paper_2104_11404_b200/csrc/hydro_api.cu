@@ -959,7 +959,7 @@ hydro_status hydro_rom_lift(int64_t rows, int n, int B, const double *Phi, const
 static int project_groups(int n, int64_t s_rows, int B) {
   const bool mma = n <= 40 && B <= 64;
   int64_t g = mma ? (s_rows + 127) / 128 : (s_rows + 255) / 256;
-  const int64_t cap = mma ? 148 * 2 : 148 * 8;
+  const int64_t cap = mma ? 148 * std::max(2, hk::PROJ3_MINB) : 148 * 8;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;

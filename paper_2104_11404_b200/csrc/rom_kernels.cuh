@@ -282,10 +282,25 @@ project_mma_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *__
 #ifndef PROJ3_PS_
 #define PROJ3_PS_ 3
 #endif
-constexpr int PROJ3_PK = PROJ3_PK_, PROJ3_PS = PROJ3_PS_, PROJ3_SPS = PROJ3_PK + 4, PROJ3_SFS = 72;
+// column tiles (8 columns each) per warp: 1 -- warp w takes column tile w over every k-step;
+// 2 -- warp w takes the column pair w % 4 over the k-steps of parity w / 4, so each A fragment
+// loaded from shared memory feeds two MMAs (0.7 instead of 1.2 shared loads per MMA); the two
+// k-parity partials are summed in a fixed order (even + odd) before the CTA partial is written.
+#ifndef PROJ3_NTW_
+#define PROJ3_NTW_ 2
+#endif
+// resident CTAs per SM (the split-K group count is 148 x this): the ring holds PS stages of
+// (8 MT (PK + 4) + 72 PK) doubles per CTA
+#ifndef PROJ3_MINB_
+#define PROJ3_MINB_ 2
+#endif
+constexpr int PROJ3_MINB = PROJ3_MINB_;
+constexpr int PROJ3_PK = PROJ3_PK_, PROJ3_PS = PROJ3_PS_, PROJ3_SPS = PROJ3_PK + 4, PROJ3_SFS = 72,
+              PROJ3_NTW = PROJ3_NTW_;
+static_assert(PROJ3_NTW == 1 || PROJ3_NTW == 2, "PROJ3_NTW");
 // P8: s_rows odd -- the rows of P are only 8-byte aligned, so P is copied in 8-byte pieces.
 template <int MT, bool P8 = false>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, PROJ3_MINB)
 project_mma3_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *__restrict__ P,
                     const double *__restrict__ f, double *__restrict__ part) {
   extern __shared__ __align__(16) double sm3[];
@@ -327,9 +342,15 @@ project_mma3_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *_
       }
     }
   };
-  double acc[MT][2];
+  constexpr int NTW = PROJ3_NTW;
+  double acc[MT][NTW][2];
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int t = 0; t < NTW; ++t) acc[mt][t][0] = acc[mt][t][1] = 0.0;
+  // column base and first k-step of this warp
+  const int cb = NTW == 1 ? warp * 8 : (warp & 3) * 16;
+  const int kg = NTW == 1 ? 0 : warp >> 2;
 #pragma unroll
   for (int ci = 0; ci < PS - 1; ++ci) {
     if (ci < nchunks) issue(ci);
@@ -343,26 +364,53 @@ project_mma3_kernel(int n, int64_t s_rows, int B, int64_t chunk, const double *_
     const double *sP = sm3 + (ci % PS) * STAGE;
     const double *sF = sP + PSZ;
 #pragma unroll
-    for (int kk = 0; kk < PK / 4; ++kk) {
-      const double b = sF[(kk * 4 + ak) * SFS + warp * 8 + ar];
+    for (int k2 = 0; k2 < PK / 4 / NTW; ++k2) {
+      const int kk = k2 * NTW + kg;
+      double b[NTW];
+#pragma unroll
+      for (int t = 0; t < NTW; ++t) b[t] = sF[(kk * 4 + ak) * SFS + cb + t * 8 + ar];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const int m = mt * 8 + ar;
         const double a = sP[m * SPS + kk * 4 + ak];
-        dmma_m8n8k4(acc[mt][0], acc[mt][1], a, b);
+#pragma unroll
+        for (int t = 0; t < NTW; ++t) dmma_m8n8k4(acc[mt][t][0], acc[mt][t][1], a, b[t]);
       }
     }
     __syncthreads();
   }
+  if (NTW == 2) {  // odd-parity warps hand their partial to the even ones (the ring is free)
+    double *xs = sm3 + ((warp & 3) * 32 + lane) * (MT * 4);
+    if (kg == 1) {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          xs[(mt * 2 + t) * 2 + 0] = acc[mt][t][0];
+          xs[(mt * 2 + t) * 2 + 1] = acc[mt][t][1];
+        }
+    }
+    __syncthreads();
+    if (kg == 1) return;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        acc[mt][t][0] = acc[mt][t][0] + xs[(mt * 2 + t) * 2 + 0];
+        acc[mt][t][1] = acc[mt][t][1] + xs[(mt * 2 + t) * 2 + 1];
+      }
+  }
   double *pg = part + (int64_t)blockIdx.x * n * B;
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-    const int m = mt * 8 + ar, c = warp * 8 + 2 * ak;
-    if (m < n) {
-      if (c < B) pg[m * B + c] = acc[mt][0];
-      if (c + 1 < B) pg[m * B + c + 1] = acc[mt][1];
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int t = 0; t < NTW; ++t) {
+      const int m = mt * 8 + ar, c = cb + t * 8 + 2 * ak;
+      if (m < n) {
+        if (c < B) pg[m * B + c] = acc[mt][t][0];
+        if (c + 1 < B) pg[m * B + c + 1] = acc[mt][t][1];
+      }
     }
-  }
 }
 
 // r[o] = sum_g part[g][o] in ascending g: 8 threads per output sum fixed contiguous g-ranges,
