@@ -1,0 +1,175 @@
+"""Seeded random sweep of the boundary calls against the oracle: mesh dimension, order,
+shape (ragged element counts), node perturbation, velocity pattern, viscosity on/off, w = v
+or a separate w, the 2D kernel choice, and -- for the sampled call -- batch size B, sample
+size and basis width.  Every case is a pure function of its integer seed (the choices are
+drawn from numpy's PCG64 on the test side; the problem data come from workloads/ as
+everywhere else), so a failure reproduces with
+
+    python tests/test_gpu_random_sweep.py full SEED      (or: rom SEED)
+
+and `python tests/test_gpu_random_sweep.py sweep START COUNT` runs a longer sweep of both
+kinds on the GPU box (seeds START .. START+COUNT-1), printing one line per case.
+
+Bars as everywhere (BASELINE north_star; DESIGN "Tolerances"): F.1 within 1e-11 (assembled)
+or 1e-12 (sampled rows), F^T.w within 1e-12 of max(|ref|, M), dt bit-exact."""
+from __future__ import annotations
+
+import sys
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    if __name__ != "__main__":
+        pytest.skip("no CUDA device", allow_module_level=True)
+
+from tests import gpu_helpers as H  # noqa: E402
+from paper_2104_11404_b200 import hydro  # noqa: E402
+
+
+def random_problem(seed: int, rom: bool = False):
+    """(problem, description, 2D kernel choice, w or None) of one seed."""
+    rng = np.random.default_rng(seed)
+    dim = int(rng.integers(2, 4))
+    k = int(rng.integers(2, 4))
+    nq = 4 if k == 2 else 6
+    hi_n = (13 if dim == 2 else 6) if k == 2 else (7 if dim == 2 else 4)
+    shape = tuple(int(rng.integers(1, hi_n + 1)) for _ in range(dim))
+    kind = "sedov" if rom else ["sedov", "sedov", "gresho", "tg", "triple"][int(rng.integers(0, 5))]
+    cfg = 9000 + seed
+    if kind == "gresho" and dim == 2:
+        prob = W.gresho(cfg, shape, k=k, nq=nq)
+    elif kind == "tg" and dim == 3:
+        prob = W.taylor_green(cfg, shape, k=k, nq=nq)
+    elif kind == "triple" and dim == 3:
+        prob = W.triple_point(cfg, shape, hi=tuple(0.25 * s for s in shape), k=k, nq=nq)
+    else:
+        kind = "sedov"
+        h = float(rng.choice([0.01875, 0.125, 1.0]))
+        delta = float(rng.choice([0.0, 0.03, 0.1]))
+        vmode = str(rng.choice(["uniform", "radial", "zero"]))
+        prob = W.sedov_like(cfg, dim, shape, (0.0,) * dim, tuple(h * s for s in shape), delta=delta,
+                            e_floor=float(rng.choice([1e-6, 1e-3, 0.5])), vmode=vmode,
+                            vscale=float(rng.choice([0.05, 0.5])), k=k, nq=nq, name=f"sweep{seed}")
+        kind += f"(h={h},delta={delta},{vmode})"
+    if rng.integers(0, 3) == 0:
+        prob.visc = not prob.visc
+    k2d = str(rng.choice(["auto", "element", "point", "lane"])) if (dim == 2 and k == 2) else "auto"
+    w = None
+    if not rom and rng.integers(0, 2) == 0:
+        w = W.uniform_pm(W.stream_seed(cfg, 77), prob.v.size, 0.3).reshape(prob.v.shape)
+    what = f"seed {seed}: {kind} d{dim} Q{k} {shape} visc={prob.visc} k2d={k2d} w={'v' if w is None else 'own'}"
+    return prob, what, k2d, w
+
+
+def run_full_case(oracle_lib, seed: int) -> str:
+    prob, what, k2d, w = random_problem(seed)
+    hydro.set_kernel_2d(k2d)
+    try:
+        if w is not None:
+            prob.w = w
+        ref = oracle_lib.force(prob)
+        got = H.run_full(prob, w=w)
+    finally:
+        hydro.set_kernel_2d("auto")
+    assert got["status"] == ref["status"], (what, got["status"], ref["status"])
+    if ref["status"] != 0:
+        return what + f" -> status {ref['status']} on both sides"
+    e1 = H.assert_close(got["F1"], ref["F1"], ref["F1mag"], H.TOL_ASSEMBLED, f"{what} F1")
+    e2 = H.assert_close(got["FTw"], ref["FTw"], ref["FTwmag"], H.TOL_LOCAL, f"{what} FTw")
+    assert H.dt_bitwise(got["dt"], ref["dt"]), (what, got["dt"], ref["dt"])
+    return what + f" -> F1 {e1:.1e} FTw {e2:.1e} dt {got['dt']!r}"
+
+
+def oracle_instance(oracle_lib, batch, xS, vS, eS, b):
+    """Instance b of the batch through the oracle: its element-list force evaluation over the
+    closure with the lifted state scattered into the full mesh; sampled rows, dt and status."""
+    base, m = batch.base, batch.base.mesh
+    d, ncl, ne = m.dim, batch.closure_nodes.size, m.ne
+    x = m.x0.copy()
+    x[:, batch.closure_nodes] = xS[:, b].reshape(d, ncl)
+    v = np.zeros_like(m.x0)
+    v[:, batch.closure_nodes] = vS[:, b].reshape(d, ncl)
+    e = base.e.copy()
+    e[batch.closure_elems] = eS[:, b].reshape(-1, ne)
+    r = oracle_lib.force(base, elist=batch.closure_elems, x=x, v=v, e=e)
+    return dict(F1=r["F1"][:, batch.s0_nodes].reshape(-1), F1m=r["F1mag"][:, batch.s0_nodes].reshape(-1),
+                FT=r["FTw"][batch.sample_elems].reshape(-1), FTm=r["FTwmag"][batch.sample_elems].reshape(-1),
+                dt=r["dt"], status=r["status"])
+
+
+def run_rom_case(oracle_lib, seed: int) -> str:
+    from tests.test_gpu_rom import gpu_step
+    base, what, k2d, _ = random_problem(seed, rom=True)
+    rng = np.random.default_rng(100003 + seed)
+    m = base.mesh
+    E = m.n_elem
+    B = int(rng.choice([1, 2, 3, 4, 5, 7, 8, 16, 31, 64]))
+    ns = int(rng.integers(1, min(E, 8) + 1))
+    # basis width within the smallest possible row counts (ns elements' L2 dofs; one element's nodes)
+    n_red = min(int(rng.choice([1, 3, 8, 17, 40])), ns * m.ne, m.dim * (m.k + 1) ** m.dim)
+    batch = W.rom_batch(base, cfg=9500 + seed, B=B, n_sample=ns, n_red=n_red)
+    what += f" B={B} sample={ns} of {E} n_red={n_red}"
+    hydro.set_kernel_2d(k2d)
+    try:
+        g = gpu_step(batch)
+    finally:
+        hydro.set_kernel_2d("auto")
+    # every instance: dt bit-exact (NaN on both sides when the lifted energy goes negative at a
+    # point, DESIGN R12; tangled instances still evaluate, R16); the rows of all finite instances
+    worst1 = worst2 = 0.0
+    statuses = set()
+    for b in range(B):
+        o = oracle_instance(oracle_lib, batch, g["xS"], g["vS"], g["eS"], b)
+        statuses.add(int(o["status"]))
+        if np.isnan(o["dt"]):
+            assert np.isnan(g["dt"][b]), (what, b, g["dt"][b])
+            continue
+        assert H.dt_bitwise(g["dt"][b], o["dt"]), (what, b, g["dt"][b], o["dt"])
+        worst1 = max(worst1, H.assert_close(g["F1"][:, b], o["F1"], o["F1m"], H.TOL_LOCAL, f"{what} F1_rows b={b}"))
+        worst2 = max(worst2, H.assert_close(g["FT"][:, b], o["FT"], o["FTm"], H.TOL_LOCAL, f"{what} FTw_rows b={b}"))
+    # the batch-wide status: 0 iff every instance is clean, else one of the instances' codes
+    st = int(g["status"][0])
+    assert (st == 0) == (statuses == {0}) and st in statuses, (what, st, statuses)
+    # projection of the sampled rows against the plain definition (fp64 numpy product)
+    F = np.nan_to_num(g["F1"])
+    P = W.uniform_pm(W.stream_seed(9500 + seed, 78), n_red * F.shape[0], 1.0).reshape(n_red, -1)
+    r = hydro.rom_project(H.dev(P), H.dev(F)).cpu().numpy()
+    H.assert_close(r, P @ F, np.abs(P) @ np.abs(F), 1e-13, f"{what} projection")
+    return what + f" -> F1 {worst1:.1e} FTw {worst2:.1e} statuses {sorted(statuses)}"
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_full_force(oracle_lib, seed):
+    run_full_case(oracle_lib, seed)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_random_sampled_force(oracle_lib, seed):
+    run_rom_case(oracle_lib, seed)
+
+
+if __name__ == "__main__":
+    import oracle
+    oracle.build()
+    mode = sys.argv[1]
+    if mode == "full":
+        print(run_full_case(oracle, int(sys.argv[2])))
+    elif mode == "rom":
+        print(run_rom_case(oracle, int(sys.argv[2])))
+    else:
+        start, count = int(sys.argv[2]), int(sys.argv[3])
+        bad = 0
+        for s in range(start, start + count):
+            for name, fn in (("full", run_full_case), ("rom", run_rom_case)):
+                try:
+                    print(name, fn(oracle, s), flush=True)
+                except Exception as ex:  # noqa: BLE001
+                    bad += 1
+                    print(name, f"seed {s} FAILED: {type(ex).__name__}: {str(ex)[:400]}", flush=True)
+        print(f"sweep done: {bad} failures")
+        sys.exit(1 if bad else 0)
