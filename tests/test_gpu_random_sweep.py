@@ -5,10 +5,10 @@ size and basis width.  Every case is a pure function of its integer seed (the ch
 drawn from numpy's PCG64 on the test side; the problem data come from workloads/ as
 everywhere else), so a failure reproduces with
 
-    python tests/test_gpu_random_sweep.py full SEED      (or: rom SEED)
+    python tests/test_gpu_random_sweep.py full SEED      (or: rom SEED, fom SEED)
 
 and `python tests/test_gpu_random_sweep.py sweep START COUNT` runs a longer sweep of both
-kinds on the GPU box (seeds START .. START+COUNT-1), printing one line per case.
+kinds (and of two RK2-average FOM steps per seed, run_fom_case) on the GPU box (seeds START .. START+COUNT-1), printing one line per case.
 
 Bars as everywhere (BASELINE north_star; DESIGN "Tolerances"): F.1 within 1e-11 (assembled)
 or 1e-12 (sampled rows), F^T.w within 1e-12 of max(|ref|, M), dt bit-exact."""
@@ -143,6 +143,58 @@ def run_rom_case(oracle_lib, seed: int) -> str:
     return what + f" -> F1 {worst1:.1e} FTw {worst2:.1e} statuses {sorted(statuses)}"
 
 
+def run_fom_case(seed: int) -> str:
+    """Two RK2-average steps (PAPER Eq. RK2-avg) of a random box problem with a smooth
+    positive energy field against oracle/fom.py: states within 1e-11 of their largest entry,
+    the step's dt estimate to 1e-10 (tests/test_gpu_fom.py's bars), v.n = 0 rows exactly 0."""
+    import oracle
+    from oracle import fom as ofom
+    rng = np.random.default_rng(200003 + seed)
+    dim = int(rng.integers(2, 4))
+    k = int(rng.integers(2, 4))
+    nq = 4 if k == 2 else 6
+    hi_n = (9 if dim == 2 else 4) if k == 2 else (4 if dim == 2 else 2)
+    shape = tuple(int(rng.integers(1, hi_n + 1)) for _ in range(dim))
+    h = float(rng.choice([0.02, 0.1, 1.0]))
+    delta = float(rng.choice([0.0, 0.04, 0.08] if k == 2 else [0.0, 0.02, 0.04]))
+    prob = W.sedov_like(9700 + seed, dim, shape, (0.0,) * dim, tuple(h * s for s in shape), delta=delta,
+                        e_floor=1e-2, vmode=str(rng.choice(["uniform", "radial"])),
+                        vscale=float(rng.choice([0.02, 0.2])) * min(1.0, 10.0 * h), k=k, nq=nq,
+                        name=f"fomsweep{seed}")
+    prob.e[:] = 1.0 + 0.5 * rng.random(prob.e.shape)
+    prob.visc = bool(rng.integers(0, 4) != 0)
+    what = f"seed {seed}: fom d{dim} Q{k} {shape} h={h} delta={delta} visc={prob.visc}"
+    m = prob.mesh
+    bc = ofom.bc_dofs_box(m)
+    prob.v.reshape(-1)[bc] = 0.0
+    ref = ofom.Fom(m, bc)
+    ctx = H.context(prob)
+    f = hydro.Fom(ctx, bc)
+    x, v, e, g = H.dev(prob.x), H.dev(prob.v), H.dev(prob.e), H.dev(prob.gamma)
+    visc, cfl = hydro.Visc(prob.q1, prob.q2, prob.visc), hydro.Cfl(prob.alpha, prob.alpha_mu)
+    xr, vr, er = prob.x.copy(), prob.v.copy(), prob.e.copy()
+    r0 = oracle.force(prob)
+    if r0["status"] != 0:
+        return what + f" -> skipped (initial status {r0['status']})"
+    dt = float(rng.choice([0.1, 0.25])) * r0["dt"]
+    its = 0
+    for _ in range(2):
+        xr, vr, er, dt_r = ofom.rk2avg_step(ref, prob, xr, vr, er, dt)
+        if not np.isfinite(dt_r):
+            return what + " -> skipped (the oracle's step leaves the valid states)"
+        dt_g, iters = f.step(x, v, e, g, visc, cfl, dt, cg_tol=1e-14, cg_max_iter=4000)
+        its += int(np.sum(iters))
+        assert ctx.status_sync()[0] == 0, what
+        assert abs(dt_g - dt_r) <= 1e-10 * abs(dt_r), (what, dt_g, dt_r)
+    worst = 0.0
+    for got, want, name in ((x, xr, "x"), (v, vr, "v"), (e, er, "e")):
+        err = np.abs(got.cpu().numpy() - want).max() / max(np.abs(want).max(), 1e-300)
+        assert err <= 1e-11, (what, name, err)
+        worst = max(worst, err)
+    assert np.array_equal(v.cpu().numpy().reshape(-1)[bc], np.zeros(bc.size)), what
+    return what + f" -> worst {worst:.1e}, {its} CG iterations"
+
+
 @pytest.mark.parametrize("seed", range(40))
 def test_random_full_force(oracle_lib, seed):
     run_full_case(oracle_lib, seed)
@@ -153,6 +205,11 @@ def test_random_sampled_force(oracle_lib, seed):
     run_rom_case(oracle_lib, seed)
 
 
+@pytest.mark.parametrize("seed", range(12))
+def test_random_fom_steps(oracle_lib, seed):
+    run_fom_case(seed)
+
+
 if __name__ == "__main__":
     import oracle
     oracle.build()
@@ -161,11 +218,14 @@ if __name__ == "__main__":
         print(run_full_case(oracle, int(sys.argv[2])))
     elif mode == "rom":
         print(run_rom_case(oracle, int(sys.argv[2])))
+    elif mode == "fom":
+        print(run_fom_case(int(sys.argv[2])))
     else:
         start, count = int(sys.argv[2]), int(sys.argv[3])
         bad = 0
         for s in range(start, start + count):
-            for name, fn in (("full", run_full_case), ("rom", run_rom_case)):
+            for name, fn in (("full", run_full_case), ("rom", run_rom_case),
+                             ("fom", lambda o, sd: run_fom_case(sd))):
                 try:
                     print(name, fn(oracle, s), flush=True)
                 except Exception as ex:  # noqa: BLE001
