@@ -408,27 +408,6 @@ __global__ void __launch_bounds__(DOT_THREADS) assemble_dot_kernel(
   block_partial(acc, part);
 }
 
-// x += alpha p; r -= alpha Ap; z = Dinv r;  part = block partials of r . z  (fused)
-__global__ void __launch_bounds__(DOT_THREADS) cg_xr_dot_kernel(
-    int64_t n, const double *__restrict__ sc, const double *__restrict__ p,
-    const double *__restrict__ Ap, const double *__restrict__ dinv, double *__restrict__ x,
-    double *__restrict__ r, double *__restrict__ z, double *__restrict__ part) {
-  const int64_t chunk = (n + DOT_BLOCKS - 1) / DOT_BLOCKS;
-  const int64_t lo = (int64_t)blockIdx.x * chunk;
-  const int64_t hi = lo + chunk < n ? lo + chunk : n;
-  const double al = sc[2];
-  double acc = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) {
-    x[i] = __fma_rn(al, p[i], x[i]);
-    const double ri = __fma_rn(-al, Ap[i], r[i]);
-    r[i] = ri;
-    const double zi = dinv[i] * ri;
-    z[i] = zi;
-    acc = __fma_rn(ri, zi, acc);
-  }
-  block_partial(acc, part);
-}
-
 // Fixed-order sum of the DOT_BLOCKS partials by one 256-thread block: thread t adds
 // partials t, t+256, ... in order, then a fixed tree (deterministic, ~2 us instead of a
 // serial loop's ~40 us).
@@ -451,32 +430,52 @@ __global__ void __launch_bounds__(256) dot_final_kernel(const double *__restrict
   if (threadIdx.x == 0) *out = s_;
 }
 
-// sc[1] = p.Ap ; alpha = rz / pAp      and      sc[3] = r.z ; beta = rz_new / rz ; rz = rz_new
-__global__ void __launch_bounds__(256) dot_final_alpha_kernel(const double *__restrict__ part, double *sc) {
-  const double s_ = sum_partials(part);
-  if (threadIdx.x == 0) {
-    sc[1] = s_;
-    // a zero residual (rz = 0) or a vanishing p.Ap would give 0/0: the iterate is final
-    sc[2] = (sc[0] == 0.0 || s_ == 0.0) ? 0.0 : sc[0] / s_;
+// The two per-iteration vector passes of PCG with the dot finalisations folded in (4 launches
+// per iteration instead of 6): every CTA sums the DOT_BLOCKS partials of the preceding kernel
+// itself, in sum_partials' fixed order, so all CTAs hold the same bits as the former one-block
+// finalisation kernels.  The partials a kernel reads (pin) and writes (pout) are different
+// arrays, and r.z lives in two slots of sc used alternately (rz_in is read by every CTA,
+// rz_out written by CTA 0), so no CTA reads what another writes.
+// x += alpha p; r -= alpha Ap; z = Dinv r; pout = block partials of r.z;  alpha = rz / p.Ap
+__global__ void __launch_bounds__(DOT_THREADS) cg_xr_dot_fused_kernel(
+    int64_t n, double *__restrict__ sc, int rz_in, const double *__restrict__ pin,
+    const double *__restrict__ p, const double *__restrict__ Ap, const double *__restrict__ dinv,
+    double *__restrict__ x, double *__restrict__ r, double *__restrict__ z, double *__restrict__ pout) {
+  const double pAp = sum_partials(pin);
+  const double rz = sc[rz_in];
+  // a zero residual (rz = 0) or a vanishing p.Ap would give 0/0: the iterate is final
+  const double al = (rz == 0.0 || pAp == 0.0) ? 0.0 : rz / pAp;
+  if (blockIdx.x == 0 && threadIdx.x == 0) { sc[1] = pAp; sc[2] = al; }
+  const int64_t chunk = (n + DOT_BLOCKS - 1) / DOT_BLOCKS;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < n ? lo + chunk : n;
+  double acc = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) {
+    x[i] = __fma_rn(al, p[i], x[i]);
+    const double ri = __fma_rn(-al, Ap[i], r[i]);
+    r[i] = ri;
+    const double zi = dinv[i] * ri;
+    z[i] = zi;
+    acc = __fma_rn(ri, zi, acc);
   }
+  block_partial(acc, pout);
 }
-__global__ void __launch_bounds__(256) dot_final_beta_kernel(const double *__restrict__ part, double *sc) {
-  const double s_ = sum_partials(part);
-  if (threadIdx.x == 0) {
-    sc[3] = s_;
-    sc[4] = sc[0] == 0.0 ? 0.0 : s_ / sc[0];
-    sc[0] = s_;
-  }
+// p = z + beta p;  beta = rz_new / rz with rz_new the sum of pin; sc[rz_out] = rz_new
+__global__ void __launch_bounds__(DOT_THREADS) cg_p_fused_kernel(
+    int64_t n, double *__restrict__ sc, int rz_in, int rz_out, const double *__restrict__ pin,
+    const double *__restrict__ z, double *__restrict__ p) {
+  const double rzn = sum_partials(pin);
+  const double rz = sc[rz_in];
+  const double be = rz == 0.0 ? 0.0 : rzn / rz;
+  if (blockIdx.x == 0 && threadIdx.x == 0) { sc[3] = rzn; sc[4] = be; sc[rz_out] = rzn; }
+  const int64_t chunk = (n + DOT_BLOCKS - 1) / DOT_BLOCKS;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < n ? lo + chunk : n;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_THREADS) p[i] = __fma_rn(be, p[i], z[i]);
 }
 
-// ---- PCG (Jacobi) pieces.  sc: [0] rz, [1] pAp, [2] alpha, [3] rz_new, [4] beta, [5] rz0
-__global__ void cg_alpha_kernel(double *sc) {
-  sc[2] = (sc[0] == 0.0 || sc[1] == 0.0) ? 0.0 : sc[0] / sc[1];
-}
-__global__ void cg_beta_kernel(double *sc) {
-  sc[4] = sc[0] == 0.0 ? 0.0 : sc[3] / sc[0];
-  sc[0] = sc[3];
-}
+// ---- PCG (Jacobi) pieces.  sc: [0] / [8] rz (alternating), [1] pAp, [2] alpha, [3] rz_new,
+// [4] beta, [5] rz0
 __global__ void cg_init_kernel(int64_t n, const double *__restrict__ b, const double *__restrict__ mask,
                                const double *__restrict__ dinv, double *__restrict__ x,
                                double *__restrict__ r, double *__restrict__ z, double *__restrict__ p) {
@@ -501,24 +500,6 @@ __global__ void cg_residual_kernel(int64_t n, const double *__restrict__ Ap,
   z[i] = zi;
   p[i] = zi;
 }
-__global__ void cg_xr_kernel(int64_t n, const double *__restrict__ sc, const double *__restrict__ p,
-                             const double *__restrict__ Ap, const double *__restrict__ dinv,
-                             double *__restrict__ x, double *__restrict__ r, double *__restrict__ z) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double al = sc[2];
-  x[i] = __fma_rn(al, p[i], x[i]);
-  const double ri = __fma_rn(-al, Ap[i], r[i]);
-  r[i] = ri;
-  z[i] = dinv[i] * ri;
-}
-__global__ void cg_p_kernel(int64_t n, const double *__restrict__ sc, const double *__restrict__ z,
-                            double *__restrict__ p) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  p[i] = __fma_rn(sc[4], p[i], z[i]);
-}
-
 // out = mask * (a + s * b)   (masked: the v.n = 0 components stay exactly 0 when a has 0 there)
 __global__ void axpy_kernel(int64_t n, const double *__restrict__ a, double s,
                             const double *__restrict__ b, const double *__restrict__ mask,

@@ -1195,17 +1195,18 @@ hydro_status pcg(hydro_fom *f, const double *b, double *x, double tol, int max_i
       else
         hk::assemble_dot_kernel<2><<<hk::DOT_BLOCKS, hk::DOT_THREADS, 0, s>>>(
             d.n_nodes, f->c->off, f->c->evec, f->mask, f->p, f->Ap, f->part);
-      hk::dot_final_alpha_kernel<<<1, 256, 0, s>>>(f->part, f->sc);
-      hk::cg_xr_dot_kernel<<<hk::DOT_BLOCKS, hk::DOT_THREADS, 0, s>>>(n, f->sc, f->p, f->Ap, f->dinv,
-                                                                     x, f->r, f->z, f->part);
-      hk::dot_final_beta_kernel<<<1, 256, 0, s>>>(f->part, f->sc);
-      hk::cg_p_kernel<<<g, 256, 0, s>>>(n, f->sc, f->z, f->p);
-      g_launches += 5;
+      // r.z alternates between sc[0] and sc[8] (read by all CTAs / written by one: fom.cuh)
+      const int rz_in = (it & 1) ? 8 : 0, rz_out = (it & 1) ? 0 : 8;
+      hk::cg_xr_dot_fused_kernel<<<hk::DOT_BLOCKS, hk::DOT_THREADS, 0, s>>>(
+          n, f->sc, rz_in, f->part, f->p, f->Ap, f->dinv, x, f->r, f->z, f->part + hk::DOT_BLOCKS);
+      hk::cg_p_fused_kernel<<<hk::DOT_BLOCKS, hk::DOT_THREADS, 0, s>>>(n, f->sc, rz_in, rz_out,
+                                                                      f->part + hk::DOT_BLOCKS, f->z, f->p);
+      g_launches += 3;
       CUDA_OK(cudaGetLastError());
       ++it;
       if (it % 4 == 0 || it == max_iter) {
         double rz = 0.0;
-        CUDA_OK(cudaMemcpyAsync(&rz, f->sc + 0, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaMemcpyAsync(&rz, f->sc + rz_out, sizeof(double), cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaStreamSynchronize(s));
         rel = sqrt(rz / bz);
         if (!(rel > tol)) break;
@@ -1247,7 +1248,7 @@ hydro_status hydro_fom_create(hydro_ctx *c, const int64_t *bc_dofs, int64_t n_bc
   const size_t n = (size_t)f->n, nE = (size_t)(E * ne);
   if (!alloc(&f->mask, n) || !alloc(&f->dinv, n) || !alloc(&f->Minv, nE * ne) ||
       !alloc(&f->csum, nE) || !alloc(&f->r, n) || !alloc(&f->z, n) || !alloc(&f->p, n) ||
-      !alloc(&f->Ap, n) || !alloc(&f->part, hk::DOT_BLOCKS) || !alloc(&f->sc, 8) ||
+      !alloc(&f->Ap, n) || !alloc(&f->part, 2 * hk::DOT_BLOCKS) || !alloc(&f->sc, 16) ||
       !alloc(&f->F1, n) || !alloc(&f->F1x, n) || !alloc(&f->FTw, nE) || !alloc(&f->FTx, nE) ||
       !alloc(&f->dv, n) || !alloc(&f->vh, n) || !alloc(&f->eh, nE) || !alloc(&f->xh, n) ||
       !alloc(&f->v1, n) || !alloc(&f->vbar, n) || !alloc(&f->dts, 2) ||
