@@ -5,10 +5,10 @@ size and basis width.  Every case is a pure function of its integer seed (the ch
 drawn from numpy's PCG64 on the test side; the problem data come from workloads/ as
 everywhere else), so a failure reproduces with
 
-    python tests/test_gpu_random_sweep.py full SEED      (or: rom SEED, fom SEED)
+    python tests/test_gpu_random_sweep.py full SEED      (or: rom SEED, fom SEED, romstep SEED)
 
-and `python tests/test_gpu_random_sweep.py sweep START COUNT` runs a longer sweep of both
-kinds (and of two RK2-average FOM steps per seed, run_fom_case) on the GPU box (seeds START .. START+COUNT-1), printing one line per case.
+and `python tests/test_gpu_random_sweep.py sweep START COUNT [KINDS]` runs a longer sweep of both
+kinds (and of two RK2-average FOM steps and two hyper-reduced ROM steps per seed) on the GPU box (seeds START .. START+COUNT-1), printing one line per case.
 
 Bars as everywhere (BASELINE north_star; DESIGN "Tolerances"): F.1 within 1e-11 (assembled)
 or 1e-12 (sampled rows), F^T.w within 1e-12 of max(|ref|, M), dt bit-exact."""
@@ -195,6 +195,58 @@ def run_fom_case(seed: int) -> str:
     return what + f" -> worst {worst:.1e}, {its} CG iterations"
 
 
+def run_romstep_case(seed: int) -> str:
+    """Two hyper-reduced RK2-average ROM steps (PAPER Eq. RK2-avg-rom-hr) of a random
+    batch with per-instance dt against oracle/rom.py (tests/test_gpu_rom_step.py's bars: reduced
+    coordinates within 1e-10 of their scale, stage dt estimates to 1e-10)."""
+    from oracle import rom as orom
+    base, what, k2d, _ = random_problem(seed, rom=True)
+    rng = np.random.default_rng(300007 + seed)
+    m = base.mesh
+    E = m.n_elem
+    B = int(rng.choice([1, 2, 3, 5, 8]))
+    ns = int(rng.integers(1, min(E, 6) + 1))
+    # basis width at most half the sampled L2 rows, so the gappy pseudo-inverses stay well conditioned
+    n_red = max(1, min(int(rng.choice([1, 2, 4, 8, 12])), (ns * m.ne) // 2))
+    batch = W.rom_batch(base, cfg=9800 + seed, B=B, n_sample=ns, n_red=n_red)
+    what += f" B={B} sample={ns} of {E} n_red={n_red}"
+    P_v, P_e, C_xv, c_x = orom.offline_projectors(batch)
+    op = dict(base=base, closure_elems=batch.closure_elems, closure_nodes=batch.closure_nodes,
+              s0_nodes=batch.s0_nodes, sample_elems=batch.sample_elems, Phi_x=batch.Phi_x,
+              Phi_v=batch.Phi_v, Phi_e=batch.Phi_e, x_os=batch.x_os, v_os=batch.v_os,
+              e_os=batch.e_os, R_v=P_v, R_e=P_e, C_xv=C_xv, c_x=c_x)
+    rx, rv, re = batch.Yx.copy(), batch.Yv.copy(), batch.Ye.copy()
+    _, _, _, dt0 = orom.rom_rk2avg_step(op, rx, rv, re, np.zeros(B))
+    if not np.isfinite(dt0).all() or (dt0 <= 0).any():
+        return what + " -> skipped (an instance starts tangled or with a negative energy)"
+    dt = float(rng.choice([0.1, 0.2])) * dt0 * (1.0 + 0.1 * np.arange(B))
+    ctx = H.context(base)
+    hydro.set_kernel_2d(k2d)
+    try:
+        plan = hydro.SamplePlan(ctx, batch.sample_elems, B)
+        st = hydro.RomStepper(plan, H.dev(batch.Phi_x), H.dev(batch.Phi_v), H.dev(batch.Phi_e),
+                              H.dev(batch.x_os), H.dev(batch.v_os), H.dev(batch.e_os),
+                              *H.gpu_offline_ops(batch))
+        Yx, Yv, Ye = H.dev(batch.Yx), H.dev(batch.Yv), H.dev(batch.Ye)
+        visc, cfl = hydro.Visc(base.q1, base.q2, base.visc), hydro.Cfl(base.alpha, base.alpha_mu)
+        g = H.dev(base.gamma)
+        for _ in range(2):
+            rx, rv, re, dte_ref = orom.rom_rk2avg_step(op, rx, rv, re, dt)
+            if not np.isfinite(dte_ref).all():
+                return what + " -> skipped (the oracle's step leaves the valid states)"
+            dte = st.step(Yx, Yv, Ye, g, visc, cfl, H.dev(dt))
+            assert plan.status_sync()[0] == 0, what
+            np.testing.assert_allclose(dte.cpu().numpy(), dte_ref, rtol=1e-10, err_msg=what)
+    finally:
+        hydro.set_kernel_2d("auto")
+    worst = 0.0
+    for got, want, name in ((Yx, rx, "xhat"), (Yv, rv, "vhat"), (Ye, re, "ehat")):
+        err = np.abs(got.cpu().numpy() - want).max() / max(np.abs(want).max(), 1e-300)
+        assert err <= 1e-10, (what, name, err)
+        worst = max(worst, err)
+    return what + f" -> worst {worst:.1e}"
+
+
 @pytest.mark.parametrize("seed", range(40))
 def test_random_full_force(oracle_lib, seed):
     run_full_case(oracle_lib, seed)
@@ -210,6 +262,11 @@ def test_random_fom_steps(oracle_lib, seed):
     run_fom_case(seed)
 
 
+@pytest.mark.parametrize("seed", range(12))
+def test_random_rom_steps(oracle_lib, seed):
+    run_romstep_case(seed)
+
+
 if __name__ == "__main__":
     import oracle
     oracle.build()
@@ -220,12 +277,18 @@ if __name__ == "__main__":
         print(run_rom_case(oracle, int(sys.argv[2])))
     elif mode == "fom":
         print(run_fom_case(int(sys.argv[2])))
+    elif mode == "romstep":
+        print(run_romstep_case(int(sys.argv[2])))
     else:
         start, count = int(sys.argv[2]), int(sys.argv[3])
+        kinds = sys.argv[4].split(",") if len(sys.argv) > 4 else ["full", "rom", "fom", "romstep"]
         bad = 0
         for s in range(start, start + count):
             for name, fn in (("full", run_full_case), ("rom", run_rom_case),
-                             ("fom", lambda o, sd: run_fom_case(sd))):
+                             ("fom", lambda o, sd: run_fom_case(sd)),
+                             ("romstep", lambda o, sd: run_romstep_case(sd))):
+                if name not in kinds:
+                    continue
                 try:
                     print(name, fn(oracle, s), flush=True)
                 except Exception as ex:  # noqa: BLE001
