@@ -14,6 +14,7 @@ Bars as everywhere (BASELINE north_star; DESIGN "Tolerances"): F.1 within 1e-11 
 or 1e-12 (sampled rows), F^T.w within 1e-12 of max(|ref|, M), dt bit-exact."""
 from __future__ import annotations
 
+import os
 import sys
 
 import numpy as np
@@ -38,6 +39,7 @@ def random_problem(seed: int, rom: bool = False):
     k = int(rng.integers(2, 4))
     nq = 4 if k == 2 else 6
     hi_n = (13 if dim == 2 else 6) if k == 2 else (7 if dim == 2 else 4)
+    hi_n *= int(os.environ.get("SWEEP_SCALE", "1"))   # larger meshes for the recorded sweeps
     shape = tuple(int(rng.integers(1, hi_n + 1)) for _ in range(dim))
     kind = "sedov" if rom else ["sedov", "sedov", "gresho", "tg", "triple"][int(rng.integers(0, 5))]
     cfg = 9000 + seed
