@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(G2L::NT, F2L_MINB) force2d_pl_kernel(const Par
   double *F1s = smem + G2L::O_F;     // [j2][q1*8 + e]
   __shared__ unsigned long long skey[4];
   __shared__ int sflag[UPB];
+  __shared__ int sslot[ND * UPB];   // assembly slot of (a, e), loaded with the node ids
 
   const int tid = threadIdx.x;
   const int w = tid >> 5, lane = tid & 31;
@@ -77,6 +78,9 @@ __global__ void __launch_bounds__(G2L::NT, F2L_MINB) force2d_pl_kernel(const Par
     if (tid < 72) {
       const int a = tid >> 3;
       const int nd = __ldg(P.elem_nodes + l * ND + a);
+      // the slot of this node's F.1 partial: its latency hides behind the whole element here
+      // instead of sitting in front of the final stores
+      if (MODE == MODE_FORCE) sslot[tid] = __ldg(P.slot + l * ND + a);
 #pragma unroll
       for (int f = 0; f < 2; ++f) {
         const double *src = f == 0 ? P.x : P.v;
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(G2L::NT, F2L_MINB) force2d_pl_kernel(const Par
           acc = __fma_rn(sTB[12 + qq * 3 + a1], t0[qq * 8], acc);
           acc = __fma_rn(sTB[qq * 3 + a1], t1[qq * 8], acc);
         }
-        const int sl = __ldg(P.slot + l * ND + a);
+        const int sl = sslot[a * UPB + ee];
         if (sl >= 0) P.evec[((int64_t)sl * 2 + c) * B + b] = acc;
       } else {
         const int j = (t - 144) >> 3, j1 = j & 1, j2 = j >> 1;
