@@ -165,7 +165,12 @@ mass_apply_kernel(const MassParams P) {
 // wm: precomputed w_q m_q [E][64].  evec: [slot][3].
 __constant__ double c_mB24[4][3];  // Q2 GLL basis at the 4 GL points (filled at FOM setup)
 
-__global__ void __launch_bounds__(256) mass_apply3_q2_kernel(int32_t n_elem, int64_t n_nodes,
+#ifdef MASS3_MINB
+#define MASS3_BOUNDS __launch_bounds__(256, MASS3_MINB)
+#else
+#define MASS3_BOUNDS __launch_bounds__(256)
+#endif
+__global__ void MASS3_BOUNDS mass_apply3_q2_kernel(int32_t n_elem, int64_t n_nodes,
                                                             const int32_t *__restrict__ elem_nodes,
                                                             const int32_t *__restrict__ slot,
                                                             const double *__restrict__ wm,
@@ -384,8 +389,12 @@ __device__ __forceinline__ void block_partial(double v, double *part) {
 }
 
 // Ap = mask * assemble(evec) and part = block partials of p . Ap  (fused)
+// 8 CTAs per SM (32 registers, a few spilled words): all DOT_BLOCKS CTAs resident in one wave
+#ifndef ASM_DOT_MINB
+#define ASM_DOT_MINB 8
+#endif
 template <int DIM>
-__global__ void __launch_bounds__(DOT_THREADS) assemble_dot_kernel(
+__global__ void __launch_bounds__(DOT_THREADS, ASM_DOT_MINB) assemble_dot_kernel(
     int64_t n_nodes, const int32_t *__restrict__ off, const double *__restrict__ evec,
     const double *__restrict__ mask, const double *__restrict__ p, double *__restrict__ Ap,
     double *__restrict__ part) {
@@ -437,7 +446,12 @@ __global__ void __launch_bounds__(256) dot_final_kernel(const double *__restrict
 // arrays, and r.z lives in two slots of sc used alternately (rz_in is read by every CTA,
 // rz_out written by CTA 0), so no CTA reads what another writes.
 // x += alpha p; r -= alpha Ap; z = Dinv r; pout = block partials of r.z;  alpha = rz / p.Ap
-__global__ void __launch_bounds__(DOT_THREADS) cg_xr_dot_fused_kernel(
+// (8 CTAs per SM: all DOT_BLOCKS = 148 x 8 CTAs resident in one wave -- at 40 registers only 6 fit and the
+// last 296 CTAs ran as a third-full second wave)
+#ifndef CG_XR_MINB
+#define CG_XR_MINB 8
+#endif
+__global__ void __launch_bounds__(DOT_THREADS, CG_XR_MINB) cg_xr_dot_fused_kernel(
     int64_t n, double *__restrict__ sc, int rz_in, const double *__restrict__ pin,
     const double *__restrict__ p, const double *__restrict__ Ap, const double *__restrict__ dinv,
     double *__restrict__ x, double *__restrict__ r, double *__restrict__ z, double *__restrict__ pout) {
