@@ -5,7 +5,7 @@ size and basis width.  Every case is a pure function of its integer seed (the ch
 drawn from numpy's PCG64 on the test side; the problem data come from workloads/ as
 everywhere else), so a failure reproduces with
 
-    python tests/test_gpu_random_sweep.py full SEED      (or: rom SEED, fom SEED, romstep SEED)
+    python tests/test_gpu_random_sweep.py full SEED      (or: rom SEED, fom SEED, romstep SEED, offline SEED)
 
 and `python tests/test_gpu_random_sweep.py sweep START COUNT [KINDS]` runs a longer sweep of both
 kinds (and of two RK2-average FOM steps and two hyper-reduced ROM steps per seed) on the GPU box (seeds START .. START+COUNT-1), printing one line per case.
@@ -249,6 +249,42 @@ def run_romstep_case(seed: int) -> str:
     return what + f" -> worst {worst:.1e}"
 
 
+def run_offline_case(seed: int) -> str:
+    """The offline selections on a random orthonormal basis: greedy DEIM, Q-DEIM and
+    the oversampled greedy must return the oracle's indices exactly; POD of random snapshots with
+    a geometric spectrum must return the oracle's basis size, singular values and an orthonormal
+    basis (tests/test_gpu_offline.py's bars)."""
+    from oracle import offline as ooff
+    rng = np.random.default_rng(400009 + seed)
+    m = int(rng.choice([1, 2, 3, 7, 16, 33, 40, 64]))
+    N = int(rng.integers(m, m + int(rng.choice([4, 300, 30_000]))) + 1)
+    n_s = int(rng.integers(m, min(N, 2 * m + 5) + 1))
+    U, _ = np.linalg.qr(rng.standard_normal((N, m)))
+    U = np.ascontiguousarray(U)
+    what = f"seed {seed}: offline N={N} m={m} n_s={n_s}"
+    Ud = H.dev(U)
+    np.testing.assert_array_equal(hydro.deim(Ud), ooff.deim(U), err_msg=what + " deim")
+    np.testing.assert_array_equal(hydro.qdeim(Ud), ooff.qdeim(U), err_msg=what + " qdeim")
+    np.testing.assert_array_equal(hydro.deim_oversampled(Ud, n_s), ooff.deim_oversampled(U, n_s),
+                                  err_msg=what + " oversampled")
+    ns = int(rng.integers(2, 41))
+    Np = int(rng.integers(ns, 20_000))
+    Q1, _ = np.linalg.qr(rng.standard_normal((Np, ns)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((ns, ns)))
+    sv = 3.0 / float(rng.choice([1.3, 1.6, 2.5])) ** np.arange(ns)
+    S = np.ascontiguousarray(((Q1 * sv) @ Q2.T).T)
+    eps = float(rng.choice([0.9, 0.99, 0.9999]))
+    Phi_g, sg = hydro.pod(H.dev(S), eps=eps)
+    Phi_o, so = ooff.pod(S, eps=eps)
+    assert Phi_g.shape == Phi_o.shape, (what, Phi_g.shape, Phi_o.shape)
+    tol = 1e-13 * so[0] ** 2 / np.maximum(so, 1e-300) + 1e-12 * so
+    assert np.all(np.abs(sg - so) <= tol), (what, float(np.max(np.abs(sg - so) / tol)))
+    Pg = Phi_g.cpu().numpy()
+    k = Pg.shape[1]
+    np.testing.assert_allclose(Pg.T @ Pg, np.eye(k), atol=1e-12, err_msg=what + " pod orthonormality")
+    return what + f" pod N={Np} ns={ns} eps={eps} k={k} -> ok"
+
+
 @pytest.mark.parametrize("seed", range(40))
 def test_random_full_force(oracle_lib, seed):
     run_full_case(oracle_lib, seed)
@@ -269,6 +305,11 @@ def test_random_rom_steps(oracle_lib, seed):
     run_romstep_case(seed)
 
 
+@pytest.mark.parametrize("seed", range(10))
+def test_random_offline_selections(seed):
+    run_offline_case(seed)
+
+
 if __name__ == "__main__":
     import oracle
     oracle.build()
@@ -281,14 +322,17 @@ if __name__ == "__main__":
         print(run_fom_case(int(sys.argv[2])))
     elif mode == "romstep":
         print(run_romstep_case(int(sys.argv[2])))
+    elif mode == "offline":
+        print(run_offline_case(int(sys.argv[2])))
     else:
         start, count = int(sys.argv[2]), int(sys.argv[3])
-        kinds = sys.argv[4].split(",") if len(sys.argv) > 4 else ["full", "rom", "fom", "romstep"]
+        kinds = sys.argv[4].split(",") if len(sys.argv) > 4 else ["full", "rom", "fom", "romstep", "offline"]
         bad = 0
         for s in range(start, start + count):
             for name, fn in (("full", run_full_case), ("rom", run_rom_case),
                              ("fom", lambda o, sd: run_fom_case(sd)),
-                             ("romstep", lambda o, sd: run_romstep_case(sd))):
+                             ("romstep", lambda o, sd: run_romstep_case(sd)),
+                             ("offline", lambda o, sd: run_offline_case(sd))):
                 if name not in kinds:
                     continue
                 try:
